@@ -1,0 +1,149 @@
+/*
+ * curvkit_b200.h -- C-ABI of the B200-native curvature library
+ * (paper_1905_05559_b200/libcurvkit_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference curvkit library
+ * (/root/reference/proj).  Every entry point below replaces one reference
+ * C++ interface, cited beside it; argument meaning, flat parameter order
+ * (model.hpp:52-55), row-major matrices and the error classes
+ * (errors.hpp: ShapeError / ContractError / ConvergenceError) are the
+ * reference's.  Only plain pointers and sizes cross the boundary.
+ *
+ * Host-buffer entry points (curvkit_*) take host pointers, copy to HBM,
+ * compute, and copy back.  Device entry points (curvkit_dev_*) take device
+ * pointers already resident in HBM plus a cudaStream_t passed as void*.
+ *
+ * Return value: CURVKIT_OK (0) or an error code; curvkit_last_error()
+ * returns the calling thread's message for the last failure.
+ */
+#ifndef CURVKIT_B200_H
+#define CURVKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum curvkit_status {
+    CURVKIT_OK = 0,
+    CURVKIT_SHAPE_ERROR = 1,       /* curv::ShapeError            (errors.hpp:10-13) */
+    CURVKIT_CONTRACT_ERROR = 2,    /* curv::ContractError         (errors.hpp:17-20) */
+    CURVKIT_RUNTIME_ERROR = 3,     /* std::runtime_error, e.g. curvature.cpp:81-84 */
+    CURVKIT_CONVERGENCE_ERROR = 4, /* curv::ConvergenceError      (errors.hpp:24-30) */
+    CURVKIT_CUDA_ERROR = 5,
+    CURVKIT_OUT_OF_MEMORY = 6
+};
+
+/* Activation (model.hpp:11) and OutputMode (model.hpp:21) as integers. */
+enum curvkit_activation { CURVKIT_IDENTITY = 0, CURVKIT_SIGMOID = 1, CURVKIT_TANH = 2, CURVKIT_RELU = 3 };
+enum curvkit_output_mode { CURVKIT_SOFTMAX_CROSS_ENTROPY = 0, CURVKIT_RAW_MEAN_OUTPUT = 1 };
+
+/* Arithmetic the product computes in.  The reference is fp64 throughout
+ * (linalg.hpp DenseMatrix of double); F64 reproduces it, F32 uses exact
+ * fp32 FMAs, TF32 runs the curvature GEMMs on tcgen05 tensor cores
+ * (kind::tf32, fp32 accumulate in TMEM), TF32X3 splits operands into
+ * hi+lo TF32 parts for fp32-grade products on tensor cores. */
+enum curvkit_precision { CURVKIT_F64 = 0, CURVKIT_F32 = 1, CURVKIT_TF32 = 2, CURVKIT_TF32X3 = 3 };
+
+/* curv::ModelSpec (model.hpp:27-38). */
+typedef struct curvkit_model {
+    int32_t num_layers;          /* L >= 2 */
+    const int64_t* layer_widths; /* T_1 .. T_L */
+    int32_t hidden_activation;   /* curvkit_activation */
+    int32_t output_mode;         /* curvkit_output_mode */
+} curvkit_model;
+
+/* curv::CurvatureConfig (curvature.hpp:11-18). parallelism is accepted for
+ * source compatibility; columns are sharded over SMs, not threads. */
+typedef struct curvkit_curvature_config {
+    int64_t batch_size_h;
+    int64_t batch_size_g;
+    int64_t parallelism;
+    int64_t memory_cap; /* P x P assembly refused above this P (reference default 4096) */
+} curvkit_curvature_config;
+
+const char* curvkit_last_error(void);
+const char* curvkit_version(void);
+
+/* curv::param_count (model.hpp:60) */
+int curvkit_param_count(const curvkit_model* model, int64_t* p_out);
+
+/* ---- host-buffer entry points (double, like the reference) ---------------
+ * params: P doubles (canonical order); x: n x T_1; y: n x T_L one-hot
+ * (ignored in raw_mean_output mode, may be NULL there).                     */
+
+/* curv::assemble_jacobian (curvature.hpp:32-33): j_out n x P */
+int curvkit_assemble_jacobian(const curvkit_model* model, const double* params, const double* x,
+                              const double* y, int64_t n, int32_t precision, double* j_out);
+
+/* curv::grad_batch (autodiff.hpp:60): grad_total P (sum over examples) */
+int curvkit_grad_batch(const curvkit_model* model, const double* params, const double* x,
+                       const double* y, int64_t n, int32_t precision, double* grad_total_out);
+
+/* curv::hvp (autodiff.hpp:66-67), batched over nvec directions:
+ * v: nvec x P (one direction per row), hv_out: nvec x P */
+int curvkit_hvp(const curvkit_model* model, const double* params, const double* x, const double* y,
+                int64_t n, const double* v, int64_t nvec, int32_t precision, double* hv_out);
+
+/* curv::HvpOperator (autodiff.hpp:76-89) constructed with batch_size and
+ * applied to nvec directions (rows of v). */
+int curvkit_hvp_operator_apply(const curvkit_model* model, const double* params, const double* x,
+                               const double* y, int64_t n, int64_t batch_size, const double* v,
+                               int64_t nvec, int32_t precision, double* hv_out);
+
+/* curv::assemble_hessian (curvature.hpp:27-29): h_out P x P, exactly
+ * symmetric.  asymmetry_out (may be NULL) receives max|H - H^T| before
+ * symmetrization when verify != 0 (diagonal layer blocks assembled from
+ * both triangles), else 0 (lower triangle mirrored by construction). */
+int curvkit_assemble_hessian(const curvkit_model* model, const double* params, const double* x,
+                             const double* y, int64_t n, const curvkit_curvature_config* cfg,
+                             int32_t precision, int32_t verify, double* h_out, double* asymmetry_out);
+
+/* curv::assemble_opg (curvature.hpp:38-40): g_out P x P */
+int curvkit_assemble_opg(const curvkit_model* model, const double* params, const double* x,
+                         const double* y, int64_t n, const curvkit_curvature_config* cfg,
+                         int32_t precision, double* g_out);
+
+/* float host-buffer variants (half the PCIe bytes for the P x P outputs) */
+int curvkit_assemble_hessian_f32(const curvkit_model* model, const double* params, const double* x,
+                                 const double* y, int64_t n, const curvkit_curvature_config* cfg,
+                                 int32_t precision, float* h_out);
+int curvkit_assemble_opg_f32(const curvkit_model* model, const double* params, const double* x,
+                             const double* y, int64_t n, const curvkit_curvature_config* cfg,
+                             int32_t precision, float* g_out);
+
+/* Top-k eigenpairs of the OPG G = (1/N) J^T J without forming G
+ * (replaces curv::opg_eigs_incremental, eigensolve.hpp:75-76): randomized
+ * range finder with `oversample` extra columns and `power_iters` power
+ * iterations, Rayleigh-Ritz on the projected (k+oversample)^2 matrix.
+ * q_out: P x k (columns are eigenvectors), lambda_out: k, descending. */
+int curvkit_opg_topk(const curvkit_model* model, const double* params, const double* x,
+                     const double* y, int64_t n, int64_t k, int64_t oversample, int64_t power_iters,
+                     uint64_t seed, int32_t precision, double* q_out, double* lambda_out);
+
+/* ---- device entry points ---------------------------------------------------
+ * Device pointers in the precision's storage type (double for F64, float
+ * otherwise): params P, x n x T_1 row-major, labels n int32 class indices.
+ * Matrix outputs use the leading dimension given (elements).               */
+int curvkit_dev_assemble_hessian(const curvkit_model* model, const void* params, const void* x,
+                                 const int32_t* labels, int64_t n, int32_t precision, void* h,
+                                 int64_t ldh, void* stream);
+int curvkit_dev_assemble_opg(const curvkit_model* model, const void* params, const void* x,
+                             const int32_t* labels, int64_t n, int32_t precision, void* g,
+                             int64_t ldg, void* stream);
+int curvkit_dev_assemble_jacobian(const curvkit_model* model, const void* params, const void* x,
+                                  const int32_t* labels, int64_t n, int32_t precision, void* j,
+                                  int64_t ldj, void* stream);
+int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const void* x,
+                         const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
+                         int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
+                         void* stream);
+
+/* Kernel-launch counter (all kernels this library launched in-process). */
+int64_t curvkit_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CURVKIT_B200_H */

@@ -1,0 +1,513 @@
+// api.cu -- the C-ABI (include/curvkit_b200.h) over the B200 engine.
+//
+// Validation and error text follow the reference (model.cpp:80-87,
+// model.cpp:201-214, curvature.cpp:15-29, autodiff.cpp:523-537) so a caller
+// switching from curvkit sees the same contract errors for the same inputs.
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/curvkit_b200.h"
+#include "common.cuh"
+#include "curvature.cuh"
+#include "eigen.cuh"
+#include "gemm_tc.cuh"
+#include "model.cuh"
+
+namespace ck {
+std::atomic<int64_t> g_launches{0};
+}
+
+namespace {
+
+using namespace ck;
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return kOk;
+    } catch (const CurvError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = e.what();
+        return kOutOfMemory;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return kRuntimeError;
+    }
+}
+
+[[noreturn]] void contract(const std::string& m) { throw CurvError(kContractError, m); }
+[[noreturn]] void shape(const std::string& m) { throw CurvError(kShapeError, m); }
+
+ModelDesc make_desc(const curvkit_model* m) {
+    if (!m || !m->layer_widths) contract("model needs at least an input and an output layer");
+    ModelDesc d;
+    if (m->num_layers < 2) contract("model needs at least an input and an output layer");
+    if (m->num_layers > kMaxLayers) contract("model has more than 16 layers");
+    d.L = m->num_layers;
+    d.S = d.L - 1;
+    d.act = m->hidden_activation;
+    d.mode = m->output_mode;
+    if (d.act < 0 || d.act > 3) contract("unknown activation");
+    if (d.mode < 0 || d.mode > 1) contract("unknown output mode");
+    for (int i = 0; i < d.L; ++i) {
+        d.w[i] = m->layer_widths[i];
+        if (d.w[i] < 1) contract("layer widths must be >= 1");
+    }
+    if (d.mode == kRawMean && d.w[d.L - 1] != 1) contract("raw_mean_output requires an output width of 1");
+    int64_t at = 0;
+    for (int k = 0; k < d.S; ++k) {
+        d.woff[k] = at;
+        d.boff[k] = at + d.w[k] * d.w[k + 1];
+        at += d.block_size(k);
+    }
+    d.P = at;
+    return d;
+}
+
+// model.cpp:201-214 -> class indices
+std::vector<int32_t> labels_from_onehot(const ModelDesc& md, const double* y, int64_t n) {
+    std::vector<int32_t> lab(n, 0);
+    if (md.mode == kRawMean) return lab;
+    if (!y) contract("target row 0 is not one-hot");
+    const int64_t tl = md.w[md.L - 1];
+    for (int64_t r = 0; r < n; ++r) {
+        int ones = 0;
+        for (int64_t m = 0; m < tl; ++m) {
+            const double v = y[r * tl + m];
+            if (v == 1.0) {
+                ++ones;
+                lab[r] = (int32_t)m;
+            } else if (v != 0.0) {
+                contract("target row " + std::to_string(r) + " is not one-hot");
+            }
+        }
+        if (ones != 1) contract("target row " + std::to_string(r) + " is not one-hot");
+    }
+    return lab;
+}
+
+void check_divisible(int64_t n, int64_t b, const char* who) {  // curvature.cpp:15-22
+    if (b < 1) contract(std::string(who) + ": batch size must be >= 1");
+    if (n == 0) contract(std::string(who) + ": empty dataset");
+    if (n % b != 0)
+        contract(std::string(who) + ": dataset size " + std::to_string(n) + " is not divisible by batch size " +
+                 std::to_string(b) + "; refusing to drop the remainder");
+}
+
+void check_memory_cap(int64_t p, int64_t cap, const char* who) {  // curvature.cpp:24-29
+    if (p > cap)
+        contract(std::string(who) + ": P = " + std::to_string(p) + " exceeds the dense memory cap " +
+                 std::to_string(cap) + "; use the matrix-free eigensolvers instead");
+}
+
+cudaStream_t lib_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    if (!s) {
+        CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        int dev = 0;
+        CK_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    return s;
+}
+
+bool is_f64(int prec) {
+    if (prec < kF64 || prec > k3xTF32) contract("unknown precision");
+    return prec == kF64;
+}
+
+// Resident problem: params, cache (forward/backward done) on the device.
+template <class T>
+struct Resident {
+    DevMem params;
+    DevMem labels;
+    Cache<T> cache;
+};
+
+template <class T>
+__global__ void convert_kernel(const double* __restrict__ in, T* __restrict__ out, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (T)in[i];
+}
+
+template <class T, class U>
+__global__ void convert_rows_kernel(const T* __restrict__ in, int64_t ldi, U* __restrict__ out, int64_t ldo,
+                                    int64_t rows, int64_t cols) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < rows * cols) out[(i / cols) * ldo + i % cols] = (U)in[(i / cols) * ldi + i % cols];
+}
+
+// Upload host doubles and run forward/backward.
+template <class T>
+void upload_and_forward(const ModelDesc& md, const double* params, const double* x, const std::vector<int32_t>& lab,
+                        int64_t n, Resident<T>& r, cudaStream_t s) {
+    DevMem pd((size_t)md.P * sizeof(double), s);
+    CK_CUDA(cudaMemcpyAsync(pd.p, params, md.P * sizeof(double), cudaMemcpyHostToDevice, s));
+    r.params = DevMem((size_t)md.P * sizeof(T), s);
+    convert_kernel<T><<<blocks_for(md.P), 256, 0, s>>>(dptr<double>(pd), dptr<T>(r.params), md.P);
+    CK_LAUNCH();
+    r.labels = DevMem((size_t)n * sizeof(int32_t), s);
+    CK_CUDA(cudaMemcpyAsync(r.labels.p, lab.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    alloc_cache<T>(md, n, r.cache, s);
+    DevMem xd((size_t)n * md.w[0] * sizeof(double), s);
+    CK_CUDA(cudaMemcpyAsync(xd.p, x, (size_t)n * md.w[0] * sizeof(double), cudaMemcpyHostToDevice, s));
+    pack_input_kernel<double, T><<<blocks_for(n * r.cache.lda[0]), 256, 0, s>>>(dptr<double>(xd), n, md.w[0],
+                                                                                 r.cache.a[0], r.cache.lda[0]);
+    CK_LAUNCH();
+    forward_backward<T>(md, dptr<T>(r.params), dptr<int32_t>(r.labels), r.cache, s);
+}
+
+// Device-resident inputs: x already T on device.
+template <class T>
+void forward_device(const ModelDesc& md, const T* params, const T* x, const int32_t* labels, int64_t n, Cache<T>& c,
+                    cudaStream_t s) {
+    alloc_cache<T>(md, n, c, s);
+    pack_input_kernel<T, T><<<blocks_for(n * c.lda[0]), 256, 0, s>>>(x, n, md.w[0], c.a[0], c.lda[0]);
+    CK_LAUNCH();
+    forward_backward<T>(md, params, labels, c, s);
+}
+
+// Copy a device matrix (rows x cols, ld) to host U (dense), converting.
+template <class T, class U>
+void download(const T* d, int64_t ld, int64_t rows, int64_t cols, U* h, cudaStream_t s) {
+    if constexpr (sizeof(T) == sizeof(U)) {
+        CK_CUDA(cudaMemcpy2DAsync(h, cols * sizeof(U), d, ld * sizeof(T), cols * sizeof(T), rows,
+                                  cudaMemcpyDeviceToHost, s));
+    } else {
+        const int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / (cols * (int64_t)sizeof(U)));
+        DevMem st[2] = {DevMem((size_t)chunk * cols * sizeof(U), s), DevMem((size_t)chunk * cols * sizeof(U), s)};
+        int which = 0;
+        for (int64_t r0 = 0; r0 < rows; r0 += chunk, which ^= 1) {
+            const int64_t rr = std::min(chunk, rows - r0);
+            convert_rows_kernel<T, U><<<blocks_for(rr * cols), 256, 0, s>>>(d + r0 * ld, ld, dptr<U>(st[which]), cols,
+                                                                             rr, cols);
+            CK_LAUNCH();
+            CK_CUDA(cudaMemcpyAsync(h + r0 * cols, st[which].p, rr * cols * sizeof(U), cudaMemcpyDeviceToHost, s));
+        }
+    }
+    CK_CUDA(cudaStreamSynchronize(s));
+}
+
+template <class T>
+double hessian_into(const ModelDesc& md, const T* params, const Cache<T>& c, T* H, int64_t ldh, int prec, bool verify,
+                    cudaStream_t s) {
+    Engine<T> eng{md, s, prec};
+    eng.hessian(params, c, H, ldh, verify);
+    if (!verify) return 0.0;
+    DevMem bits(2 * sizeof(unsigned long long), s);
+    CK_CUDA(cudaMemsetAsync(bits.p, 0, 2 * sizeof(unsigned long long), s));
+    unsigned long long* b = dptr<unsigned long long>(bits);
+    absmax_kernel<T><<<1024, 256, 0, s>>>(H, ldh, md.P, md.P, b + 1);
+    CK_LAUNCH();
+    for (int k = 0; k < md.S; ++k) {
+        const int64_t sz = md.block_size(k);
+        symmetrize_block_kernel<T><<<blocks_for(sz * sz), 256, 0, s>>>(H, ldh, md.woff[k], sz, b);
+        CK_LAUNCH();
+    }
+    unsigned long long hb[2];
+    CK_CUDA(cudaMemcpyAsync(hb, b, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    double asym, hmax;
+    std::memcpy(&asym, &hb[0], 8);
+    std::memcpy(&hmax, &hb[1], 8);
+    // curvature.cpp:81-84; fp32 storage modes get fp32-scaled headroom.
+    const double tol = prec == kF64 ? 1e-8 : 1e-3;
+    if (asym > tol * hmax)
+        throw CurvError(kRuntimeError, "assemble_hessian: pre-symmetrization asymmetry " + std::to_string(asym) +
+                                           " exceeds " + std::to_string(tol) + " * " + std::to_string(hmax));
+    return asym;
+}
+
+template <class T, class U>
+void host_hessian(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n,
+                  const curvkit_curvature_config* cfg, int prec, bool verify, U* h_out, double* asym_out) {
+    const int64_t cap = cfg ? cfg->memory_cap : 4096;
+    check_memory_cap(md.P, cap, "assemble_hessian");
+    check_divisible(n, cfg ? cfg->batch_size_h : n, "assemble_hessian");
+    auto lab = labels_from_onehot(md, y, n);
+    cudaStream_t s = lib_stream();
+    Resident<T> r;
+    upload_and_forward<T>(md, params, x, lab, n, r, s);
+    const int64_t ldh = round_up(md.P, 4);
+    DevMem H((size_t)md.P * ldh * sizeof(T), s);
+    const double asym = hessian_into<T>(md, dptr<T>(r.params), r.cache, dptr<T>(H), ldh, prec, verify, s);
+    download<T, U>(dptr<T>(H), ldh, md.P, md.P, h_out, s);
+    if (asym_out) *asym_out = asym;
+}
+
+template <class T>
+void jacobian_full(const ModelDesc& md, const Cache<T>& c, DevMem& J, int64_t& ldj, cudaStream_t s) {
+    ldj = round_up(md.P, 4);
+    J = DevMem((size_t)c.n * ldj * sizeof(T), s);
+    jacobian<T>(md, c, 0, c.n, dptr<T>(J), ldj, s);
+}
+
+template <class T, class U>
+void host_opg(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n,
+              const curvkit_curvature_config* cfg, int prec, U* g_out) {
+    const int64_t cap = cfg ? cfg->memory_cap : 4096;
+    check_memory_cap(md.P, cap, "assemble_opg");
+    check_divisible(n, cfg ? cfg->batch_size_g : n, "assemble_opg");
+    auto lab = labels_from_onehot(md, y, n);
+    cudaStream_t s = lib_stream();
+    Resident<T> r;
+    upload_and_forward<T>(md, params, x, lab, n, r, s);
+    DevMem J;
+    int64_t ldj;
+    jacobian_full<T>(md, r.cache, J, ldj, s);
+    const int64_t ldg = round_up(md.P, 4);
+    DevMem G((size_t)md.P * ldg * sizeof(T), s);
+    Engine<T> eng{md, s, prec};
+    eng.opg(dptr<T>(J), ldj, n, dptr<T>(G), ldg);
+    download<T, U>(dptr<T>(G), ldg, md.P, md.P, g_out, s);
+}
+
+template <class T>
+void host_jacobian(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n,
+                   double* j_out) {
+    if (n < 1) contract("assemble_jacobian: empty batch");
+    auto lab = labels_from_onehot(md, y, n);
+    cudaStream_t s = lib_stream();
+    Resident<T> r;
+    upload_and_forward<T>(md, params, x, lab, n, r, s);
+    DevMem J;
+    int64_t ldj;
+    jacobian_full<T>(md, r.cache, J, ldj, s);
+    download<T, double>(dptr<T>(J), ldj, n, md.P, j_out, s);
+}
+
+template <class T>
+void host_grad(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n, double* g) {
+    if (n < 1) contract("forward_backward: empty batch");
+    auto lab = labels_from_onehot(md, y, n);
+    cudaStream_t s = lib_stream();
+    Resident<T> r;
+    upload_and_forward<T>(md, params, x, lab, n, r, s);
+    DevMem gd((size_t)md.P * sizeof(T), s);
+    Engine<T> eng{md, s, kF64};
+    eng.grad(r.cache, dptr<T>(gd));
+    download<T, double>(dptr<T>(gd), md.P, 1, md.P, g, s);
+}
+
+template <class T>
+void host_hvp(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n, const double* v,
+              int64_t nv, int prec, double* hv) {
+    if (n < 1) contract("forward_backward: empty batch");
+    if (nv < 1) shape("hvp: need at least one direction");
+    auto lab = labels_from_onehot(md, y, n);
+    cudaStream_t s = lib_stream();
+    Resident<T> r;
+    upload_and_forward<T>(md, params, x, lab, n, r, s);
+    DevMem vd((size_t)nv * md.P * sizeof(double), s), vt((size_t)nv * md.P * sizeof(T), s),
+        hd((size_t)nv * md.P * sizeof(T), s);
+    CK_CUDA(cudaMemcpyAsync(vd.p, v, nv * md.P * sizeof(double), cudaMemcpyHostToDevice, s));
+    convert_kernel<T><<<blocks_for(nv * md.P), 256, 0, s>>>(dptr<double>(vd), dptr<T>(vt), nv * md.P);
+    CK_LAUNCH();
+    Engine<T> eng{md, s, prec};
+    eng.hvp(dptr<T>(r.params), r.cache, dptr<T>(vt), nv, md.P, dptr<T>(hd), md.P, T(1) / T(n));
+    download<T, double>(dptr<T>(hd), md.P, nv, md.P, hv, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* curvkit_last_error(void) { return g_err.c_str(); }
+const char* curvkit_version(void) { return "curvkit-b200 0.1 (sm_100a)"; }
+int64_t curvkit_launch_count(void) { return ck::g_launches.load(); }
+
+int curvkit_param_count(const curvkit_model* model, int64_t* p_out) {
+    return guard([&] { *p_out = make_desc(model).P; });
+}
+
+int curvkit_assemble_jacobian(const curvkit_model* model, const double* params, const double* x, const double* y,
+                              int64_t n, int32_t precision, double* j_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision)) host_jacobian<double>(md, params, x, y, n, j_out);
+        else host_jacobian<float>(md, params, x, y, n, j_out);
+    });
+}
+
+int curvkit_grad_batch(const curvkit_model* model, const double* params, const double* x, const double* y, int64_t n,
+                       int32_t precision, double* grad_total_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision)) host_grad<double>(md, params, x, y, n, grad_total_out);
+        else host_grad<float>(md, params, x, y, n, grad_total_out);
+    });
+}
+
+int curvkit_hvp(const curvkit_model* model, const double* params, const double* x, const double* y, int64_t n,
+                const double* v, int64_t nvec, int32_t precision, double* hv_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision)) host_hvp<double>(md, params, x, y, n, v, nvec, precision, hv_out);
+        else host_hvp<float>(md, params, x, y, n, v, nvec, precision, hv_out);
+    });
+}
+
+int curvkit_hvp_operator_apply(const curvkit_model* model, const double* params, const double* x, const double* y,
+                               int64_t n, int64_t batch_size, const double* v, int64_t nvec, int32_t precision,
+                               double* hv_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        // autodiff.cpp:523-537; equal mini-batches average to the full mean
+        if (batch_size < 1) contract("HvpOperator: batch size must be >= 1");
+        if (n == 0) contract("HvpOperator: empty dataset");
+        if (n % batch_size != 0)
+            contract("HvpOperator: dataset size " + std::to_string(n) + " is not divisible by batch size " +
+                     std::to_string(batch_size) + "; refusing to drop the remainder");
+        if (is_f64(precision)) host_hvp<double>(md, params, x, y, n, v, nvec, precision, hv_out);
+        else host_hvp<float>(md, params, x, y, n, v, nvec, precision, hv_out);
+    });
+}
+
+int curvkit_assemble_hessian(const curvkit_model* model, const double* params, const double* x, const double* y,
+                             int64_t n, const curvkit_curvature_config* cfg, int32_t precision, int32_t verify,
+                             double* h_out, double* asymmetry_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision))
+            host_hessian<double, double>(md, params, x, y, n, cfg, precision, verify != 0, h_out, asymmetry_out);
+        else
+            host_hessian<float, double>(md, params, x, y, n, cfg, precision, verify != 0, h_out, asymmetry_out);
+    });
+}
+
+int curvkit_assemble_hessian_f32(const curvkit_model* model, const double* params, const double* x, const double* y,
+                                 int64_t n, const curvkit_curvature_config* cfg, int32_t precision, float* h_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision)) host_hessian<double, float>(md, params, x, y, n, cfg, precision, false, h_out, nullptr);
+        else host_hessian<float, float>(md, params, x, y, n, cfg, precision, false, h_out, nullptr);
+    });
+}
+
+int curvkit_assemble_opg(const curvkit_model* model, const double* params, const double* x, const double* y,
+                         int64_t n, const curvkit_curvature_config* cfg, int32_t precision, double* g_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision)) host_opg<double, double>(md, params, x, y, n, cfg, precision, g_out);
+        else host_opg<float, double>(md, params, x, y, n, cfg, precision, g_out);
+    });
+}
+
+int curvkit_assemble_opg_f32(const curvkit_model* model, const double* params, const double* x, const double* y,
+                             int64_t n, const curvkit_curvature_config* cfg, int32_t precision, float* g_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (is_f64(precision)) host_opg<double, float>(md, params, x, y, n, cfg, precision, g_out);
+        else host_opg<float, float>(md, params, x, y, n, cfg, precision, g_out);
+    });
+}
+
+int curvkit_opg_topk(const curvkit_model* model, const double* params, const double* x, const double* y, int64_t n,
+                     int64_t k, int64_t oversample, int64_t power_iters, uint64_t seed, int32_t precision,
+                     double* q_out, double* lambda_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk: empty dataset");
+        auto lab = labels_from_onehot(md, y, n);
+        cudaStream_t s = lib_stream();
+        if (is_f64(precision)) {
+            Resident<double> r;
+            upload_and_forward<double>(md, params, x, lab, n, r, s);
+            host_topk<double>(md, r.cache, k, oversample, power_iters, seed, precision, q_out, lambda_out, s);
+        } else {
+            Resident<float> r;
+            upload_and_forward<float>(md, params, x, lab, n, r, s);
+            host_topk<float>(md, r.cache, k, oversample, power_iters, seed, precision, q_out, lambda_out, s);
+        }
+    });
+}
+
+// ---- device entry points -----------------------------------------------------
+int curvkit_dev_assemble_hessian(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                                 int64_t n, int32_t precision, void* h, int64_t ldh, void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("assemble_hessian: empty dataset");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (is_f64(precision)) {
+            Cache<double> c;
+            forward_device<double>(md, (const double*)params, (const double*)x, labels, n, c, s);
+            hessian_into<double>(md, (const double*)params, c, (double*)h, ldh, precision, false, s);
+        } else {
+            Cache<float> c;
+            forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
+            hessian_into<float>(md, (const float*)params, c, (float*)h, ldh, precision, false, s);
+        }
+    });
+}
+
+int curvkit_dev_assemble_opg(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                             int64_t n, int32_t precision, void* g, int64_t ldg, void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("assemble_opg: empty dataset");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            DevMem J;
+            int64_t ldj;
+            jacobian_full<T>(md, c, J, ldj, s);
+            Engine<T> eng{md, s, precision};
+            eng.opg(dptr<T>(J), ldj, n, (T*)g, ldg);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_dev_assemble_jacobian(const curvkit_model* model, const void* params, const void* x,
+                                  const int32_t* labels, int64_t n, int32_t precision, void* j, int64_t ldj,
+                                  void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("assemble_jacobian: empty batch");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            jacobian<T>(md, c, 0, n, (T*)j, ldj, s);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                         int64_t n, int64_t k, int64_t oversample, int64_t power_iters, uint64_t seed,
+                         int32_t precision, void* q, void* lambda, void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk: empty dataset");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            dev_topk<T>(md, c, k, oversample, power_iters, seed, precision, (T*)q, (T*)lambda, s);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// common.cuh -- shared definitions for the curvkit B200 library.
+//
+// Model description, canonical flat-parameter offsets (reference
+// model.cpp:142-151), activation functions and their first/second
+// derivatives (model.cpp:9-50), error plumbing for the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+
+namespace ck {
+
+constexpr int kMaxLayers = 16;
+
+enum Status : int {
+    kOk = 0,
+    kShapeError = 1,     // curv::ShapeError
+    kContractError = 2,  // curv::ContractError
+    kRuntimeError = 3,   // std::runtime_error in the reference
+    kConvergenceError = 4,
+    kCudaError = 5,
+    kOutOfMemory = 6,
+};
+
+enum Act : int { kIdentity = 0, kSigmoid = 1, kTanh = 2, kRelu = 3 };
+enum OutMode : int { kSoftmaxCE = 0, kRawMean = 1 };
+
+// Arithmetic the path computes in.  kF64/kF32 run exact-FMA SIMT tiles;
+// kTF32 runs tcgen05 kind::tf32 MMAs with fp32 accumulation in TMEM;
+// k3xTF32 splits each fp32 operand into a TF32 hi part and a TF32 lo part
+// and accumulates hi*hi + hi*lo + lo*hi (fp32-grade products).
+enum Precision : int { kF64 = 0, kF32 = 1, kTF32 = 2, k3xTF32 = 3 };
+
+struct CurvError : std::runtime_error {
+    int code;
+    CurvError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK_CUDA(expr)                                                                       \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            throw ::ck::CurvError(e_ == cudaErrorMemoryAllocation ? ::ck::kOutOfMemory      \
+                                                                  : ::ck::kCudaError,       \
+                                  std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+extern std::atomic<int64_t> g_launches;  // kernels launched by this library
+
+#define CK_LAUNCH()                                                   \
+    do {                                                              \
+        ::ck::g_launches.fetch_add(1, std::memory_order_relaxed);     \
+        CK_CUDA(cudaGetLastError());                                  \
+    } while (0)
+
+struct ModelDesc {
+    int L = 0;  // number of layers (widths)
+    int S = 0;  // number of affine steps, L - 1
+    int act = kTanh;
+    int mode = kSoftmaxCE;
+    int64_t w[kMaxLayers] = {};
+    int64_t woff[kMaxLayers] = {};  // start of W_k in the flat vector
+    int64_t boff[kMaxLayers] = {};  // start of b_k
+    int64_t P = 0;
+
+    int64_t tin(int k) const { return w[k]; }
+    int64_t tout(int k) const { return w[k + 1]; }
+    int64_t block_size(int k) const { return w[k] * w[k + 1] + w[k + 1]; }
+};
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// ---- activations (model.cpp:9-50) -------------------------------------------
+
+template <class T>
+__device__ __forceinline__ T d_exp(T x);
+template <>
+__device__ __forceinline__ float d_exp<float>(float x) { return expf(x); }
+template <>
+__device__ __forceinline__ double d_exp<double>(double x) { return exp(x); }
+
+template <class T>
+__device__ __forceinline__ T d_tanh(T x);
+template <>
+__device__ __forceinline__ float d_tanh<float>(float x) { return tanhf(x); }
+template <>
+__device__ __forceinline__ double d_tanh<double>(double x) { return tanh(x); }
+
+template <class T>
+__device__ __forceinline__ T act_value(int a, T z) {
+    switch (a) {
+        case kSigmoid:
+            return z >= T(0) ? T(1) / (T(1) + d_exp(-z)) : d_exp(z) / (T(1) + d_exp(z));
+        case kTanh: return d_tanh(z);
+        case kRelu: return z > T(0) ? z : T(0);
+        default: return z;
+    }
+}
+
+template <class T>
+__device__ __forceinline__ T act_deriv(int a, T z) {
+    switch (a) {
+        case kSigmoid: {
+            const T s = act_value(kSigmoid, z);
+            return s * (T(1) - s);
+        }
+        case kTanh: {
+            const T t = d_tanh(z);
+            return T(1) - t * t;
+        }
+        case kRelu: return z > T(0) ? T(1) : T(0);
+        default: return T(1);
+    }
+}
+
+template <class T>
+__device__ __forceinline__ T act_second(int a, T z) {
+    switch (a) {
+        case kSigmoid: {
+            const T s = act_value(kSigmoid, z);
+            return s * (T(1) - s) * (T(1) - T(2) * s);
+        }
+        case kTanh: {
+            const T t = d_tanh(z);
+            return T(-2) * t * (T(1) - t * t);
+        }
+        default: return T(0);
+    }
+}
+
+}  // namespace ck

@@ -1,0 +1,278 @@
+// curvature.cuh -- orchestration of the curvature products on one GPU.
+//
+//   hvp      batched Pearlmutter R-op (autodiff.cpp:415-501): every layer of
+//            the R-forward / R-backward pass and the final accumulation is
+//            a GEMM over (direction x example) rows.
+//   hessian  exact H (curvature.cpp:33-92).  Column p of H is the HVP on the
+//            basis vector e_p.  For e_p a weight (o, i) of step k the R-state
+//            factorises as s_n * f(n, o) with s_n = a_k[n][i], so the R-op
+//            only runs for the T_{k+1} "profiles" o (plus T_k profiles i for
+//            the explicit delta*RW term below the tangent layer), and every
+//            block of H is one GEMM  R (rows (o'', p), K = n) x a_m (n x T_m+1)
+//            whose A operand R is an elementwise product of profiles and
+//            activations.  The lower block triangle is computed and mirrored.
+//   opg      G = (1/N) J^T J as a symmetric (lower-triangle) GEMM over J.
+#pragma once
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "model.cuh"
+
+namespace ck {
+
+// Large curvature GEMMs.  TF32 modes are routed to the tcgen05 kernel by
+// the specialisations in gemm_tc.cuh; everything else runs SIMT FMAs.
+template <class T, class Epi>
+struct CurvGemm {
+    static void run(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B,
+                    const Epi& e) {
+        (void)prec;
+        gemm_simt<T>(s, M, N, K, 1, A, B, e);
+    }
+};
+
+// rz_k[b] = a_k RW_k[b]^T + Rb_k[b]
+template <class T>
+struct EpiRzBias {
+    T* out; int64_t ld, bs; const T* rb; int64_t rbs;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int b, int64_t m, int64_t o, T acc) const {
+        out[b * bs + m * ld + o] = acc + rb[b * rbs + o];
+    }
+};
+
+// batched view of EpiRback: direction b, example m -> stacked row b*n + m
+template <class T>
+struct EpiRb2 {
+    EpiRback<T> inner; int64_t bs;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int b, int64_t m, int64_t cc, T acc) const {
+        inner(0, b * inner.n + m, cc, acc);
+    }
+};
+
+inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)ceil_div(n, t); }
+
+template <class T>
+struct Engine {
+    const ModelDesc& md;
+    cudaStream_t s;
+    int prec;
+
+    // ---------------------------------------------------------------- grad
+    void grad(const Cache<T>& c, T* g) {
+        for (int k = 0; k < md.S; ++k) {
+            EpiHv<T> e{g, 0, md.woff[k], md.boff[k], md.w[k], T(1), 0};
+            gemm_simt<T>(s, md.w[k + 1], md.w[k] + 1, c.n, 1, mnmaj(c.delta[k], c.ldt[k]),
+                         mnmaj(c.a[k], c.lda[k]), e);
+        }
+    }
+
+    // ---------------------------------------------------------------- hvp
+    // V: nv directions, row b at V + b*ldv (canonical flat order).
+    void hvp(const T* params, const Cache<T>& c, const T* V, int64_t nv, int64_t ldv, T* HV, int64_t ldhv,
+             T alpha) {
+        const int S = md.S;
+        const int64_t n = c.n;
+        std::vector<DevMem> keep;
+        T* rz[kMaxLayers] = {};
+        T* ra[kMaxLayers] = {};
+        T* rd[kMaxLayers] = {};
+        for (int k = 0; k < S; ++k) {
+            keep.emplace_back((size_t)nv * n * c.ldt[k] * sizeof(T), s);
+            rz[k] = dptr<T>(keep.back());
+            keep.emplace_back((size_t)nv * n * c.ldt[k] * sizeof(T), s);
+            rd[k] = dptr<T>(keep.back());
+            if (k > 0) {
+                keep.emplace_back((size_t)nv * n * c.lda[k] * sizeof(T), s);
+                ra[k] = dptr<T>(keep.back());
+                CK_CUDA(cudaMemsetAsync(ra[k], 0, (size_t)nv * n * c.lda[k] * sizeof(T), s));
+            }
+        }
+        // R-forward
+        for (int k = 0; k < S; ++k) {
+            const int64_t tin = md.w[k], tout = md.w[k + 1];
+            const int64_t bsz = n * c.ldt[k];
+            EpiRzBias<T> e1{rz[k], c.ldt[k], bsz, V + md.boff[k], ldv};
+            gemm_simt<T>(s, n, tout, tin, nv, kmaj(c.a[k], c.lda[k], 0), kmaj(V + md.woff[k], tin, ldv), e1);
+            if (k > 0) {
+                EpiStore<T> e2{rz[k], c.ldt[k], bsz, T(1), T(1)};
+                gemm_simt<T>(s, n, tout, tin, nv, kmaj(ra[k], c.lda[k], n * c.lda[k]),
+                             kmaj(params + md.woff[k], tin, 0), e2);
+            }
+            if (k + 1 < S) {
+                // ra_{k+1} = act'(z_k) * rz_k  (rows = nv * n)
+                rop_act_kernel<T><<<blocks_for(nv * n * tout), 256, 0, s>>>(
+                    rz[k], c.ldt[k], c.z[k], c.ldt[k], n, nv * n, tout, md.act, ra[k + 1], c.lda[k + 1]);
+                CK_LAUNCH();
+            }
+        }
+        // R-backward
+        rop_softmax_kernel<T><<<blocks_for(nv * n, 128), 128, 0, s>>>(
+            rz[S - 1], c.ldt[S - 1], c.a[S], c.lda[S], n, nv * n, md.w[S], md.mode, rd[S - 1], c.ldt[S - 1]);
+        CK_LAUNCH();
+        for (int k = S - 2; k >= 0; --k) {
+            const int64_t t1 = md.w[k + 1], t2 = md.w[k + 2];
+            // treat (direction, example) rows as one stacked operand
+            EpiRback<T> e1{rd[k], c.ldt[k], c.z[k], c.up[k], c.ldt[k], rz[k], c.ldt[k], n, md.act, 0, 0, 0};
+            gemm_simt<T>(s, nv * n, t1, t2, 1, kmaj(rd[k + 1], c.ldt[k + 1]), mnmaj(params + md.woff[k + 1], t1), e1);
+            // + delta_{k+1} RW_{k+1}[b]  (batched over directions), then apply
+            EpiRb2<T> e2{EpiRback<T>{rd[k], c.ldt[k], c.z[k], c.up[k], c.ldt[k], rz[k], c.ldt[k], n, md.act, 0, 1, 1}, 0};
+            gemm_simt<T>(s, n, t1, t2, nv, kmaj(c.delta[k + 1], c.ldt[k + 1], 0),
+                         mnmaj(V + md.woff[k + 1], t1, ldv), e2);
+        }
+        // accumulate: hv_k = sum_n rd_k (x) a_k + delta_k (x) ra_k, bias = sum_n rd_k
+        for (int k = 0; k < S; ++k) {
+            const int64_t tin = md.w[k], tout = md.w[k + 1];
+            EpiHv<T> e1{HV, ldhv, md.woff[k], md.boff[k], tin, alpha, 0};
+            gemm_simt<T>(s, tout, tin + 1, n, nv, mnmaj(rd[k], c.ldt[k], n * c.ldt[k]), mnmaj(c.a[k], c.lda[k], 0), e1);
+            if (k > 0) {
+                EpiHv<T> e2{HV, ldhv, md.woff[k], md.boff[k], tin, alpha, 1};
+                gemm_simt<T>(s, tout, tin + 1, n, nv, mnmaj(c.delta[k], c.ldt[k], 0),
+                             mnmaj(ra[k], c.lda[k], n * c.lda[k]), e2);
+            }
+        }
+    }
+
+    // ---------------------------------------------------------------- opg
+    void opg(const T* J, int64_t ldj, int64_t n, T* G, int64_t ldg) {
+        EpiSymLower<T> e{G, ldg, T(1) / T(n)};
+        CurvGemm<T, EpiSymLower<T>>::run(prec, s, md.P, md.P, n, mnmaj(J, ldj), mnmaj(J, ldj), e);
+    }
+
+    // ---------------------------------------------------------------- hessian
+    // Profiles for tangent step k (see file comment):
+    //   G  [T_{k+1}][n][ldt_k]       rdelta_k for rz_k = e_o
+    //   Pm [T_{k+1}][n][ldt_m]       rdelta_m, m < k, same tangents
+    //   Qm [T_k][n][ldt_m]           rdelta_m from the explicit delta*RW term
+    size_t chunk_bytes = size_t(48) << 20;  // R operand chunk, sized to stay in L2
+
+    void hessian(const T* params, const Cache<T>& c, T* H, int64_t ldh, bool verify) {
+        const int S = md.S;
+        const int64_t n = c.n;
+        for (int k = 0; k < S; ++k) {
+            const int64_t np = md.w[k + 1];
+            std::vector<DevMem> keep;
+            auto buf = [&](int64_t rows, int64_t ld) {
+                keep.emplace_back((size_t)rows * ld * sizeof(T), s);
+                CK_CUDA(cudaMemsetAsync(keep.back().p, 0, (size_t)rows * ld * sizeof(T), s));
+                return dptr<T>(keep.back());
+            };
+            T* G = buf(np * n, c.ldt[k]);
+            T* rzp[kMaxLayers] = {};
+            if (k == S - 1) {
+                profile_output_kernel<T><<<blocks_for(np * n * np), 256, 0, s>>>(c.a[S], c.lda[S], np, n, md.mode, G,
+                                                                                  c.ldt[k]);
+                CK_LAUNCH();
+            } else {
+                // R-forward above the tangent layer
+                rzp[k + 1] = buf(np * n, c.ldt[k + 1]);
+                profile_first_rz_kernel<T><<<blocks_for(np * n * md.w[k + 2]), 256, 0, s>>>(
+                    c.z[k], c.ldt[k], params + md.woff[k + 1], md.w[k + 1], md.w[k + 2], n, md.act, rzp[k + 1],
+                    c.ldt[k + 1]);
+                CK_LAUNCH();
+                for (int kp = k + 1; kp + 1 < S; ++kp) {
+                    T* ra = buf(np * n, c.lda[kp + 1]);
+                    rop_act_kernel<T><<<blocks_for(np * n * md.w[kp + 1]), 256, 0, s>>>(
+                        rzp[kp], c.ldt[kp], c.z[kp], c.ldt[kp], n, np * n, md.w[kp + 1], md.act, ra, c.lda[kp + 1]);
+                    CK_LAUNCH();
+                    rzp[kp + 1] = buf(np * n, c.ldt[kp + 1]);
+                    EpiStore<T> e{rzp[kp + 1], c.ldt[kp + 1], 0, T(1), T(0)};
+                    gemm_simt<T>(s, np * n, md.w[kp + 2], md.w[kp + 1], 1, kmaj(ra, c.lda[kp + 1]),
+                                 kmaj(params + md.woff[kp + 1], md.w[kp + 1]), e);
+                }
+                // R-backward down to the tangent layer
+                T* rdn = buf(np * n, c.ldt[S - 1]);
+                rop_softmax_kernel<T><<<blocks_for(np * n, 128), 128, 0, s>>>(
+                    rzp[S - 1], c.ldt[S - 1], c.a[S], c.lda[S], n, np * n, md.w[S], md.mode, rdn, c.ldt[S - 1]);
+                CK_LAUNCH();
+                for (int kp = S - 2; kp >= k; --kp) {
+                    T* out = kp == k ? G : buf(np * n, c.ldt[kp]);
+                    EpiRback<T> e{out, c.ldt[kp], c.z[kp], c.up[kp], c.ldt[kp], rzp[kp], c.ldt[kp], n, md.act,
+                                  kp == k ? 1 : 0, 1, 0};
+                    gemm_simt<T>(s, np * n, md.w[kp + 1], md.w[kp + 2], 1, kmaj(rdn, c.ldt[kp + 1]),
+                                 mnmaj(params + md.woff[kp + 1], md.w[kp + 1]), e);
+                    rdn = out;
+                }
+            }
+            // P and Q profiles below the tangent layer
+            T* Pm[kMaxLayers] = {};
+            T* Qm[kMaxLayers] = {};
+            if (k > 0) {
+                const int64_t nq = md.w[k];
+                T* prevP = G;
+                for (int m = k - 1; m >= 0; --m) {
+                    Pm[m] = buf(np * n, c.ldt[m]);
+                    EpiRback<T> e{Pm[m], c.ldt[m], c.z[m], nullptr, c.ldt[m], nullptr, 0, n, md.act, 0, 1, 0};
+                    gemm_simt<T>(s, np * n, md.w[m + 1], md.w[m + 2], 1, kmaj(prevP, c.ldt[m + 1]),
+                                 mnmaj(params + md.woff[m + 1], md.w[m + 1]), e);
+                    prevP = Pm[m];
+                }
+                Qm[k - 1] = buf(nq * n, c.ldt[k - 1]);
+                profile_q_kernel<T><<<blocks_for(nq * n * nq), 256, 0, s>>>(c.z[k - 1], c.ldt[k - 1], nq, n, md.act,
+                                                                             Qm[k - 1], c.ldt[k - 1]);
+                CK_LAUNCH();
+                for (int m = k - 2; m >= 0; --m) {
+                    Qm[m] = buf(nq * n, c.ldt[m]);
+                    EpiRback<T> e{Qm[m], c.ldt[m], c.z[m], nullptr, c.ldt[m], nullptr, 0, n, md.act, 0, 1, 0};
+                    gemm_simt<T>(s, nq * n, md.w[m + 1], md.w[m + 2], 1, kmaj(Qm[m + 1], c.ldt[m + 1]),
+                                 mnmaj(params + md.woff[m + 1], md.w[m + 1]), e);
+                }
+            }
+            // blocks (k, m), m <= k
+            const int64_t Pk = md.block_size(k);
+            const int64_t ldr = round_up(n, 4);
+            for (int m = k; m >= 0; --m) {
+                const int64_t tm1 = md.w[m + 1];
+                int64_t J = (int64_t)(chunk_bytes / ((size_t)tm1 * ldr * sizeof(T)));
+                J = std::max<int64_t>(64, J / 64 * 64);
+                J = std::min<int64_t>(J, round_up(Pk, 64));
+                DevMem rbuf((size_t)tm1 * J * ldr * sizeof(T), s);
+                for (int64_t j0 = 0; j0 < Pk; j0 += J) {
+                    const int64_t Jc = std::min<int64_t>(J, Pk - j0);
+                    RGenArgs<T> g{m == k ? G : Pm[m], m == k ? nullptr : Qm[m], m == k ? c.ldt[k] : c.ldt[m],
+                                  c.a[k], c.lda[k], c.delta[k], c.ldt[k], n, md.w[k], md.w[k + 1], tm1, j0, Jc,
+                                  dptr<T>(rbuf), ldr};
+                    rgen_kernel<T><<<blocks_for(tm1 * Jc * ceil_div(n, 4)), 256, 0, s>>>(g);
+                    CK_LAUNCH();
+                    EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], md.w[m], T(1) / T(n),
+                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
+                    CurvGemm<T, EpiHess<T>>::run(prec, s, tm1 * Jc, md.w[m] + 1, n, kmaj(dptr<T>(rbuf), ldr),
+                                                 mnmaj(c.a[m], c.lda[m]), e);
+                }
+            }
+        }
+    }
+};
+
+// ---- verify mode: asymmetry of the diagonal layer blocks, then symmetrize --
+template <class T>
+__global__ void symmetrize_block_kernel(T* H, int64_t ldh, int64_t off, int64_t size, unsigned long long* asym_bits) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= size * size) return;
+    const int64_t i = idx / size, j = idx % size;
+    if (j <= i) return;
+    T* a = H + (off + i) * ldh + off + j;
+    T* b = H + (off + j) * ldh + off + i;
+    const double d = fabs((double)*a - (double)*b);
+    atomicMax(asym_bits, (unsigned long long)__double_as_longlong(d));
+    const T avg = T(0.5) * (*a + *b);
+    *a = avg;
+    *b = avg;
+}
+
+template <class T>
+__global__ void absmax_kernel(const T* H, int64_t ldh, int64_t rows, int64_t cols, unsigned long long* bits) {
+    double m = 0.0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows * cols;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        m = fmax(m, fabs((double)H[(idx / cols) * ldh + idx % cols]));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(bits, (unsigned long long)__double_as_longlong(m));
+}
+
+}  // namespace ck

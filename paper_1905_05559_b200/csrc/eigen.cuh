@@ -1,0 +1,347 @@
+// eigen.cuh -- top-k eigenpairs of the OPG G = (1/N) J^T J without forming G.
+//
+// Randomized range finder (Halko-Martinsson-Tropp, Alg. 4.3/4.4):
+//   Y = G Omega, Omega ~ N(0,1)^{P x l}, l = k + oversample
+//   q power iterations Y <- G orth(Y)
+//   Q = orth(Y);  B = Q^T G Q = (1/N) (J Q)^T (J Q)   (l x l)
+//   B = V diag(lambda) V^T  (parallel cyclic Jacobi in one CTA)
+//   eigenvectors Q V[:, :k], eigenvalues lambda[:k] (descending)
+// G is only ever applied as J^T (J X): two passes over the per-example
+// gradient matrix J, which stays in HBM.  orth() is CholeskyQR2 with the
+// l x l Gram matrices accumulated in fp64.
+//
+// Replaces the reference's streaming SVD (eigensolve.cpp:288-381); its
+// eigenvalue scaling sigma^2 / N (eigensolve.cpp:366-372) is the same
+// quantity as lambda(B) here.
+#pragma once
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "curvature.cuh"
+#include "gemm_simt.cuh"
+#include "model.cuh"
+
+namespace ck {
+
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// Omega[p][c] ~ N(0, 1): Box-Muller on the counter-based splitmix64 stream
+template <class T>
+__global__ void gaussian_kernel(T* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    const uint64_t pair = (uint64_t)idx >> 1;
+    const double u1 = 1.0 - (double)(splitmix_at(seed, 2 * pair) >> 11) * 0x1.0p-53;
+    const double u2 = (double)(splitmix_at(seed, 2 * pair + 1) >> 11) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    const double th = 6.283185307179586476925286766559 * u2;
+    out[(idx / cols) * ld + idx % cols] = (T)((idx & 1) ? r * sin(th) : r * cos(th));
+}
+
+// W[c][d] += sum_{p in chunk} Y[p][c] * Y[p][d]   (fp64 accumulation)
+template <class T>
+__global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ Y, int64_t ld, int64_t rows, int64_t l,
+                                                   int64_t chunk, double* __restrict__ W) {
+    __shared__ double a[32][33], b[32][33];
+    const int64_t c0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+    if (d0 > c0 + 31) return;  // lower triangle tiles only; mirrored below
+    const int64_t p0 = blockIdx.z * chunk, p1 = min(rows, p0 + chunk);
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 row-groups
+    double acc[4] = {0, 0, 0, 0};
+    for (int64_t p = p0; p < p1; p += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            const int64_t pp = p + r;
+            a[r][tx] = (pp < p1 && c0 + tx < l) ? (double)Y[pp * ld + c0 + tx] : 0.0;
+            b[r][tx] = (pp < p1 && d0 + tx < l) ? (double)Y[pp * ld + d0 + tx] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += a[r][ty + 8 * u] * b[r][tx];
+        }
+        __syncthreads();
+    }
+    for (int u = 0; u < 4; ++u) {
+        const int64_t c = c0 + ty + 8 * u, d = d0 + tx;
+        if (c < l && d < l && d <= c) {
+            atomicAdd(&W[c * l + d], acc[u]);
+            if (d != c) atomicAdd(&W[d * l + c], acc[u]);
+        }
+    }
+}
+
+// In-place upper Cholesky W = R^T R and Rinv = R^{-1}, one CTA (l <= 1024).
+// A diagonal shift keeps rank-deficient Grams factorisable.
+__global__ void chol_inv_kernel(double* W, int64_t l, double shift, double* Rinv) {
+    extern __shared__ double col[];
+    const int t = threadIdx.x;
+    for (int64_t i = t; i < l; i += blockDim.x) W[i * l + i] += shift;
+    __syncthreads();
+    // right-looking Cholesky on the upper triangle (row-major W)
+    for (int64_t j = 0; j < l; ++j) {
+        if (t == 0) {
+            double d = W[j * l + j];
+            W[j * l + j] = sqrt(d > 0.0 ? d : 1e-300);
+        }
+        __syncthreads();
+        const double rjj = W[j * l + j];
+        for (int64_t c = j + 1 + t; c < l; c += blockDim.x) W[j * l + c] /= rjj;
+        __syncthreads();
+        for (int64_t idx = t; idx < (l - j - 1) * (l - j - 1); idx += blockDim.x) {
+            const int64_t r = j + 1 + idx / (l - j - 1), c = j + 1 + idx % (l - j - 1);
+            if (c >= r) W[r * l + c] -= W[j * l + r] * W[j * l + c];
+        }
+        __syncthreads();
+    }
+    // Rinv: solve R X = I column by column (back substitution), upper triangular
+    for (int64_t c = t; c < l; c += blockDim.x) {
+        for (int64_t r = l - 1; r >= 0; --r) {
+            double s = (r == c) ? 1.0 : 0.0;
+            for (int64_t m = r + 1; m <= c; ++m) s -= W[r * l + m] * Rinv[m * l + c];
+            Rinv[r * l + c] = r <= c ? s / W[r * l + r] : 0.0;
+        }
+    }
+}
+
+// Parallel cyclic Jacobi on a symmetric l x l matrix in one CTA: each round
+// rotates l/2 disjoint (p, q) pairs of a round-robin tournament; a warp
+// lane per pair computes the rotation, all threads apply it.
+__global__ void jacobi_kernel(double* A, double* V, int64_t l, int max_sweeps, int* sweeps_out) {
+    extern __shared__ double sh[];
+    const int64_t m = l + (l & 1);  // pad to even with a dummy index
+    double* cs = sh;                // cos per pair
+    double* sn = sh + m / 2;        // sin per pair
+    int* pp = reinterpret_cast<int*>(sh + m);
+    int* qq = pp + m / 2;
+    __shared__ double off_s;
+    const int t = threadIdx.x, nt = blockDim.x;
+    for (int64_t i = t; i < l * l; i += nt) V[i] = (i / l == i % l) ? 1.0 : 0.0;
+    __syncthreads();
+    double fro = 0.0;
+    for (int64_t i = 0; i < l * l; ++i) fro += A[i] * A[i];
+    const double tol = 1e-15 * sqrt(fro > 1e-300 ? fro : 1e-300);
+    int sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+        if (t == 0) {
+            double s = 0.0;
+            for (int64_t i = 0; i < l; ++i)
+                for (int64_t j = 0; j < l; ++j)
+                    if (i != j) s += A[i * l + j] * A[i * l + j];
+            off_s = sqrt(s);
+        }
+        __syncthreads();
+        if (off_s <= tol) break;
+        for (int64_t round = 0; round < m - 1; ++round) {
+            for (int64_t k = t; k < m / 2; k += nt) {
+                // circle method: index 0 fixed, others rotate
+                auto pos = [&](int64_t x) -> int64_t { return x == 0 ? 0 : 1 + (x - 1 + round) % (m - 1); };
+                int64_t a = pos(k), b = pos(m - 1 - k);
+                if (a > b) { const int64_t tmp = a; a = b; b = tmp; }
+                pp[k] = (int)a;
+                qq[k] = (int)b;
+                double c = 1.0, s = 0.0;
+                if (b < l) {
+                    const double apq = A[a * l + b];
+                    if (apq != 0.0) {
+                        const double h = A[b * l + b] - A[a * l + a];
+                        const double th = 0.5 * h / apq;
+                        double tt = 1.0 / (fabs(th) + sqrt(1.0 + th * th));
+                        if (th < 0.0) tt = -tt;
+                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        s = tt * c;
+                    }
+                }
+                cs[k] = c;
+                sn[k] = s;
+            }
+            __syncthreads();
+            // A <- A J (columns), V <- V J
+            for (int64_t idx = t; idx < (m / 2) * l; idx += nt) {
+                const int64_t k = idx / l, i = idx % l;
+                const int64_t a = pp[k], b = qq[k];
+                if (b >= l) continue;
+                const double c = cs[k], s = sn[k];
+                const double x = A[i * l + a], y = A[i * l + b];
+                A[i * l + a] = c * x - s * y;
+                A[i * l + b] = s * x + c * y;
+                const double vx = V[i * l + a], vy = V[i * l + b];
+                V[i * l + a] = c * vx - s * vy;
+                V[i * l + b] = s * vx + c * vy;
+            }
+            __syncthreads();
+            // A <- J^T A (rows)
+            for (int64_t idx = t; idx < (m / 2) * l; idx += nt) {
+                const int64_t k = idx / l, i = idx % l;
+                const int64_t a = pp[k], b = qq[k];
+                if (b >= l) continue;
+                const double c = cs[k], s = sn[k];
+                const double x = A[a * l + i], y = A[b * l + i];
+                A[a * l + i] = c * x - s * y;
+                A[b * l + i] = s * x + c * y;
+            }
+            __syncthreads();
+        }
+    }
+    if (t == 0) *sweeps_out = sweep;
+}
+
+template <class U>
+__global__ void convert_d_kernel(const double* in, U* out, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (U)in[i];
+}
+
+template <class T>
+struct EigenWork {
+    const ModelDesc& md;
+    cudaStream_t s;
+    int prec;
+
+    // Y <- orth(Y) in place (CholeskyQR2), Y is rows x l with ld
+    void orth(T* Y, int64_t rows, int64_t l, int64_t ld) {
+        DevMem W((size_t)l * l * sizeof(double), s), Rinv((size_t)l * l * sizeof(double), s);
+        DevMem Rt((size_t)l * l * sizeof(T), s), Y2((size_t)rows * ld * sizeof(T), s);
+        for (int pass = 0; pass < 2; ++pass) {
+            CK_CUDA(cudaMemsetAsync(W.p, 0, l * l * sizeof(double), s));
+            const int64_t ksplit = std::min<int64_t>(256, std::max<int64_t>(1, rows / 4096));
+            const int64_t chunk = ceil_div(rows, ksplit);
+            dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
+            gram_kernel<T><<<g, 256, 0, s>>>(Y, ld, rows, l, chunk, dptr<double>(W));
+            CK_LAUNCH();
+            // shift ~ eps * trace keeps the factorisation defined when Y is
+            // numerically rank deficient (shifted CholeskyQR)
+            std::vector<double> hw(l * l);
+            CK_CUDA(cudaMemcpyAsync(hw.data(), W.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            double tr = 0.0;
+            for (int64_t i = 0; i < l; ++i) tr += hw[i * l + i];
+            const double shift = (sizeof(T) == 4 ? 1e-7 : 1e-14) * tr / (double)l;
+            chol_inv_kernel<<<1, 256, 0, s>>>(dptr<double>(W), l, shift, dptr<double>(Rinv));
+            CK_LAUNCH();
+            convert_to<T>(dptr<double>(Rinv), dptr<T>(Rt), l * l);
+            // Y2 = Y Rinv ; copy back
+            EpiStore<T> e{dptr<T>(Y2), ld, 0, T(1), T(0)};
+            gemm_simt<T>(s, rows, l, l, 1, kmaj(Y, ld), mnmaj(dptr<T>(Rt), l), e);
+            CK_CUDA(cudaMemcpyAsync(Y, Y2.p, (size_t)rows * ld * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        }
+    }
+
+    template <class U>
+    void convert_to(const double* in, U* out, int64_t n) {
+        convert_d_kernel<U><<<blocks_for(n), 256, 0, s>>>(in, out, n);
+        CK_LAUNCH();
+    }
+
+    // T_out (n x l) = J X ; X is P x l (ld lx)
+    void apply_j(const T* J, int64_t ldj, int64_t n, const T* X, int64_t ldx, int64_t l, T* Tout, int64_t ldt) {
+        EpiStore<T> e{Tout, ldt, 0, T(1), T(0)};
+        CurvGemm<T, EpiStore<T>>::run(prec, s, n, l, md.P, kmaj(J, ldj), mnmaj(X, ldx), e);
+    }
+    // Y (P x l) = J^T Tn ; Tn is n x l
+    void apply_jt(const T* J, int64_t ldj, int64_t n, const T* Tn, int64_t ldt, int64_t l, T* Y, int64_t ldy) {
+        EpiStore<T> e{Y, ldy, 0, T(1), T(0)};
+        CurvGemm<T, EpiStore<T>>::run(prec, s, md.P, l, n, mnmaj(J, ldj), mnmaj(Tn, ldt), e);
+    }
+};
+
+// Core driver: leaves eigenvectors (P x k, row-major, ld k) in q_dev and
+// eigenvalues (k, descending) in lam_host.
+template <class T>
+void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
+               uint64_t seed, int prec, T* q_dev, std::vector<double>& lam_host, cudaStream_t s) {
+    const int64_t n = c.n, P = md.P;
+    if (k < 1 || k > std::min(n, P))
+        throw CurvError(kContractError, "opg_topk: need 1 <= k <= min(N, P), got k = " + std::to_string(k));
+    if (oversample < 0 || power_iters < 0) throw CurvError(kContractError, "opg_topk: negative oversample/power_iters");
+    const int64_t l = std::min(k + oversample, P);
+    const int64_t ldl = round_up(l, 4);
+    // per-example gradients stay resident in HBM
+    const int64_t ldj = round_up(P, 4);
+    DevMem J((size_t)n * ldj * sizeof(T), s);
+    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s);
+    DevMem Y((size_t)P * ldl * sizeof(T), s), Om((size_t)P * ldl * sizeof(T), s);
+    DevMem Tn((size_t)n * ldl * sizeof(T), s);
+    CK_CUDA(cudaMemsetAsync(Om.p, 0, (size_t)P * ldl * sizeof(T), s));
+    gaussian_kernel<T><<<blocks_for(P * l), 256, 0, s>>>(dptr<T>(Om), P, l, ldl, seed);
+    CK_LAUNCH();
+    EigenWork<T> ew{md, s, prec};
+    T* X = dptr<T>(Om);
+    for (int64_t it = 0; it <= power_iters; ++it) {
+        ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+        ew.apply_jt(dptr<T>(J), ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
+        ew.orth(dptr<T>(Y), P, l, ldl);
+        X = dptr<T>(Y);
+    }
+    // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q)
+    ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+    DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
+    CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));
+    {
+        const int64_t ksplit = std::min<int64_t>(256, std::max<int64_t>(1, n / 2048));
+        dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
+        gram_kernel<T><<<g, 256, 0, s>>>(dptr<T>(Tn), ldl, n, l, ceil_div(n, ksplit), dptr<double>(B));
+        CK_LAUNCH();
+    }
+    std::vector<double> hb(l * l);
+    CK_CUDA(cudaMemcpyAsync(hb.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    for (auto& v : hb) v /= (double)n;
+    CK_CUDA(cudaMemcpyAsync(B.p, hb.data(), l * l * sizeof(double), cudaMemcpyHostToDevice, s));
+    DevMem sw(sizeof(int), s);
+    const int64_t m = l + (l & 1);
+    jacobi_kernel<<<1, 1024, (size_t)m * sizeof(double) + (size_t)m * sizeof(int), s>>>(dptr<double>(B), dptr<double>(V),
+                                                                                      l, 60, dptr<int>(sw));
+    CK_LAUNCH();
+    std::vector<double> ha(l * l), hv(l * l);
+    CK_CUDA(cudaMemcpyAsync(ha.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaMemcpyAsync(hv.data(), V.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> ord(l);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return ha[a * l + a] > ha[b * l + b]; });
+    lam_host.resize(k);
+    std::vector<T> vk(l * k);  // l x k, row-major
+    for (int64_t j = 0; j < k; ++j) {
+        lam_host[j] = ha[ord[j] * l + ord[j]];
+        for (int64_t r = 0; r < l; ++r) vk[r * k + j] = (T)hv[r * l + ord[j]];
+    }
+    DevMem Vk((size_t)l * k * sizeof(T), s);
+    CK_CUDA(cudaMemcpyAsync(Vk.p, vk.data(), l * k * sizeof(T), cudaMemcpyHostToDevice, s));
+    EpiStore<T> e{q_dev, k, 0, T(1), T(0)};
+    gemm_simt<T>(s, P, k, l, 1, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
+    CK_CUDA(cudaStreamSynchronize(s));
+}
+
+template <class T>
+void host_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
+               uint64_t seed, int prec, double* q_out, double* lambda_out, cudaStream_t s) {
+    DevMem q((size_t)md.P * k * sizeof(T), s);
+    std::vector<double> lam;
+    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, dptr<T>(q), lam, s);
+    std::vector<T> hq((size_t)md.P * k);
+    CK_CUDA(cudaMemcpyAsync(hq.data(), q.p, hq.size() * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < hq.size(); ++i) q_out[i] = (double)hq[i];
+    for (int64_t j = 0; j < k; ++j) lambda_out[j] = lam[j];
+}
+
+template <class T>
+void dev_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
+              uint64_t seed, int prec, T* q_dev, T* lam_dev, cudaStream_t s) {
+    std::vector<double> lam;
+    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s);
+    std::vector<T> hl(lam.begin(), lam.end());
+    CK_CUDA(cudaMemcpyAsync(lam_dev, hl.data(), k * sizeof(T), cudaMemcpyHostToDevice, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace ck

@@ -1,0 +1,145 @@
+// gemm_simt.cuh -- exact-FMA tiled GEMM for the f64 and f32 precision modes.
+//
+// C(b, m, n) = sum_k A(b, m, k) * B(b, n, k), with each operand either
+// K-major (element (row, k) at p[row*ld + k]) or MN-major (p[k*ld + row]).
+// The result is handed element by element to an epilogue functor, which
+// owns the output layout (plain, symmetric mirror, Hessian block mapping,
+// fused bias+activation, ...).  The tcgen05 kernel in gemm_tc.cuh shares the
+// same operand/epilogue conventions for the TF32 modes.
+#pragma once
+
+#include "common.cuh"
+
+namespace ck {
+
+template <class T>
+struct Opnd {
+    const T* p = nullptr;
+    int64_t ld = 0;
+    int kmajor = 1;
+    int64_t bstride = 0;  // batch stride in elements
+};
+
+template <class T>
+__host__ __device__ inline Opnd<T> kmaj(const T* p, int64_t ld, int64_t bs = 0) {
+    Opnd<T> o;
+    o.p = p; o.ld = ld; o.kmajor = 1; o.bstride = bs;
+    return o;
+}
+template <class T>
+__host__ __device__ inline Opnd<T> mnmaj(const T* p, int64_t ld, int64_t bs = 0) {
+    Opnd<T> o;
+    o.p = p; o.ld = ld; o.kmajor = 0; o.bstride = bs;
+    return o;
+}
+
+// Default: never skip a tile.
+struct NoSkip {
+    __device__ bool operator()(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+};
+
+template <class T, int BM, int BN, int BK, int TM, int TN, class Epi>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+gemm_simt_kernel(int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, Epi epi) {
+    constexpr int NTX = BN / TN, NTY = BM / TM, NT = NTX * NTY;
+    __shared__ T As[BK][BM + 1];
+    __shared__ T Bs[BK][BN + 1];
+    const int bz = blockIdx.z;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    if (epi.skip(bz, m0, n0, BM, BN)) return;
+    const T* Ap = A.p + bz * A.bstride;
+    const T* Bp = B.p + bz * B.bstride;
+    const int tid = threadIdx.x, tx = tid % NTX, ty = tid / NTX;
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+    for (int64_t k0 = 0; k0 < K; k0 += BK) {
+        // A tile: BM x BK
+        for (int e = tid; e < BM * BK; e += NT) {
+            int r, kk;
+            if (A.kmajor) { kk = e % BK; r = e / BK; } else { r = e % BM; kk = e / BM; }
+            const int64_t gm = m0 + r, gk = k0 + kk;
+            T v = T(0);
+            if (gm < M && gk < K) v = A.kmajor ? Ap[gm * A.ld + gk] : Ap[gk * A.ld + gm];
+            As[kk][r] = v;
+        }
+        for (int e = tid; e < BN * BK; e += NT) {
+            int r, kk;
+            if (B.kmajor) { kk = e % BK; r = e / BK; } else { r = e % BN; kk = e / BN; }
+            const int64_t gn = n0 + r, gk = k0 + kk;
+            T v = T(0);
+            if (gn < N && gk < K) v = B.kmajor ? Bp[gn * B.ld + gk] : Bp[gk * B.ld + gn];
+            Bs[kk][r] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            T a[TM], b[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = As[kk][ty + NTY * i];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx + NTX * j];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int64_t gm = m0 + ty + NTY * i, gn = n0 + tx + NTX * j;
+            if (gm < M && gn < N) epi(bz, gm, gn, acc[i][j]);
+        }
+}
+
+template <class T, class Epi>
+void gemm_simt(cudaStream_t s, int64_t M, int64_t N, int64_t K, int64_t batch, Opnd<T> A, Opnd<T> B,
+               const Epi& epi) {
+    if (M <= 0 || N <= 0 || batch <= 0) return;
+    constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+    dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)batch);
+    gemm_simt_kernel<T, BM, BN, BK, TM, TN, Epi><<<grid, (BM / TM) * (BN / TN), 0, s>>>(M, N, K, A, B, epi);
+    CK_LAUNCH();
+}
+
+// ---- common epilogues --------------------------------------------------------
+
+// C[b][m*ldc + n] = alpha * acc (+ beta * C)
+template <class T>
+struct EpiStore {
+    T* c;
+    int64_t ldc, bstride;
+    T alpha, beta;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int b, int64_t m, int64_t n, T acc) const {
+        T* p = c + b * bstride + m * ldc + n;
+        *p = beta == T(0) ? alpha * acc : alpha * acc + beta * *p;
+    }
+};
+
+// Symmetric product (SYRK-style): only tiles touching the lower triangle run;
+// each lower entry is written at (m, n) and mirrored to (n, m), so the result
+// is exactly symmetric.
+template <class T>
+struct EpiSymLower {
+    T* c;
+    int64_t ldc;
+    T alpha;
+    __device__ bool skip(int, int64_t m0, int64_t n0, int64_t bm, int64_t) const {
+        return n0 > m0 + bm - 1;
+    }
+    __device__ void operator()(int, int64_t m, int64_t n, T acc) const {
+        if (n > m) return;
+        const T v = alpha * acc;
+        c[m * ldc + n] = v;
+        c[n * ldc + m] = v;
+    }
+};
+
+}  // namespace ck

@@ -1,0 +1,469 @@
+// model.cuh -- device-side forward/backward cache, per-example Jacobian,
+// Pearlmutter R-op (HVP) and the basis-tangent Hessian factorization.
+//
+// Reference behaviour followed:
+//   forward_backward      autodiff.cpp:310-360
+//   per_example_grad_rows autodiff.cpp:384-400
+//   hvp_from_cache        autodiff.cpp:415-501
+//   assemble_hessian      curvature.cpp:33-92 (columns = HVPs on e_p)
+//
+// Layout in HBM (row-major everywhere, n = example index):
+//   a[k]     n x lda[k]  activations entering step k; column T_k holds 1.0
+//            so a GEMM against a[k] yields weight and bias sums together
+//   z/delta/up[k]  n x ldt[k]  (ldt = round_up(T_{k+1}, 4))
+//   profiles [p][n][t]  one n x ldt slab per tangent profile p, contiguous,
+//            so a stack of profiles is a plain (p*n) x ldt GEMM operand.
+#pragma once
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+
+namespace ck {
+
+// ---------------------------------------------------------------------------
+// device buffers (stream-ordered pool allocations)
+// ---------------------------------------------------------------------------
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DevMem() = default;
+    DevMem(size_t b, cudaStream_t st) : bytes(b), s(st) {
+        if (b) CK_CUDA(cudaMallocAsync(&p, b, st));
+    }
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    DevMem(DevMem&& o) noexcept { *this = std::move(o); }
+    DevMem& operator=(DevMem&& o) noexcept {
+        release();
+        p = o.p; bytes = o.bytes; s = o.s;
+        o.p = nullptr; o.bytes = 0;
+        return *this;
+    }
+    ~DevMem() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+    }
+};
+
+template <class T>
+inline T* dptr(const DevMem& m) { return static_cast<T*>(m.p); }
+
+template <class T>
+struct Cache {
+    int64_t n = 0;
+    T* a[kMaxLayers] = {};
+    int64_t lda[kMaxLayers] = {};
+    T* z[kMaxLayers] = {};
+    T* delta[kMaxLayers] = {};
+    T* up[kMaxLayers] = {};
+    int64_t ldt[kMaxLayers] = {};
+    DevMem mem;
+};
+
+// ---------------------------------------------------------------------------
+// forward / backward
+// ---------------------------------------------------------------------------
+template <class Tin, class T>
+__global__ void pack_input_kernel(const Tin* __restrict__ x, int64_t n, int64_t t0, T* __restrict__ a,
+                                  int64_t lda) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * lda) return;
+    const int64_t r = idx / lda, c = idx % lda;
+    a[idx] = c < t0 ? (T)x[r * t0 + c] : (c == t0 ? T(1) : T(0));
+}
+
+// z = a W^T + b ; hidden: a_next = act(z) (+ ones column)
+template <class T>
+struct EpiForward {
+    const T* bias;
+    T* z;
+    int64_t ldz;
+    T* anext;  // nullptr for the output step
+    int64_t ldan, tout;
+    int act;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int, int64_t m, int64_t c, T acc) const {
+        const T v = acc + bias[c];
+        z[m * ldz + c] = v;
+        if (anext) {
+            anext[m * ldan + c] = act_value<T>(act, v);
+            if (c == 0) anext[m * ldan + tout] = T(1);
+        }
+    }
+};
+
+// softmax output + delta = p - y (autodiff.cpp:291-306, 342-350)
+template <class T>
+__global__ void output_layer_kernel(const T* __restrict__ z, int64_t ldz, const int32_t* __restrict__ labels,
+                                    int64_t n, int64_t tl, int mode, T* __restrict__ prob, int64_t ldp,
+                                    T* __restrict__ delta) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const T* zr = z + r * ldz;
+    T* pr = prob + r * ldp;
+    T* dr = delta + r * ldz;
+    if (mode == kRawMean) {
+        for (int64_t m = 0; m < tl; ++m) { pr[m] = zr[m]; dr[m] = T(1); }
+        return;
+    }
+    T zmax = zr[0];
+    for (int64_t m = 1; m < tl; ++m) zmax = zr[m] > zmax ? zr[m] : zmax;
+    T sum = T(0);
+    for (int64_t m = 0; m < tl; ++m) { const T e = d_exp(zr[m] - zmax); pr[m] = e; sum += e; }
+    const int32_t y = labels[r];
+    for (int64_t m = 0; m < tl; ++m) {
+        const T p = pr[m] / sum;
+        pr[m] = p;
+        dr[m] = p - (m == y ? T(1) : T(0));
+    }
+}
+
+// up = delta_{k+1} W_{k+1};  delta_k = up * act'(z_k)
+template <class T>
+struct EpiBackward {
+    const T* z;
+    T* up;
+    T* delta;
+    int64_t ld;
+    int act;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int, int64_t m, int64_t c, T acc) const {
+        up[m * ld + c] = acc;
+        delta[m * ld + c] = acc * act_deriv<T>(act, z[m * ld + c]);
+    }
+};
+
+template <class T>
+void alloc_cache(const ModelDesc& md, int64_t n, Cache<T>& c, cudaStream_t s) {
+    c.n = n;
+    size_t total = 0;
+    for (int k = 0; k <= md.S; ++k) {
+        c.lda[k] = round_up(md.w[k] + 1, 4);
+        total += (size_t)n * c.lda[k];
+    }
+    for (int k = 0; k < md.S; ++k) {
+        c.ldt[k] = round_up(md.w[k + 1], 4);
+        total += 3 * (size_t)n * c.ldt[k];
+    }
+    c.mem = DevMem(total * sizeof(T), s);
+    T* p = dptr<T>(c.mem);
+    for (int k = 0; k <= md.S; ++k) { c.a[k] = p; p += n * c.lda[k]; }
+    for (int k = 0; k < md.S; ++k) {
+        c.z[k] = p; p += n * c.ldt[k];
+        c.delta[k] = p; p += n * c.ldt[k];
+        c.up[k] = p; p += n * c.ldt[k];
+    }
+    CK_CUDA(cudaMemsetAsync(c.mem.p, 0, total * sizeof(T), s));
+}
+
+// Dense GEMM dispatcher used by the small model GEMMs: SIMT in every mode
+// (their cost is O(N * P) against the O(N * P^2) curvature products).
+template <class T, class Epi>
+void model_gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, const Epi& e) {
+    gemm_simt<T>(s, M, N, K, 1, A, B, e);
+}
+
+template <class T>
+void forward_backward(const ModelDesc& md, const T* params, const int32_t* labels, Cache<T>& c,
+                      cudaStream_t s) {
+    const int S = md.S;
+    const int64_t n = c.n;
+    for (int k = 0; k < S; ++k) {
+        const T* W = params + md.woff[k];
+        const T* b = params + md.boff[k];
+        EpiForward<T> e{b, c.z[k], c.ldt[k], k + 1 < S ? c.a[k + 1] : nullptr, c.lda[k + 1], md.w[k + 1], md.act};
+        model_gemm<T>(s, n, md.w[k + 1], md.w[k], kmaj(c.a[k], c.lda[k]), kmaj(W, md.w[k]), e);
+    }
+    output_layer_kernel<T><<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(
+        c.z[S - 1], c.ldt[S - 1], labels, n, md.w[S], md.mode, c.a[S], c.lda[S], c.delta[S - 1]);
+    CK_LAUNCH();
+    for (int k = S - 2; k >= 0; --k) {
+        const T* W1 = params + md.woff[k + 1];  // T_{k+2} x T_{k+1}
+        EpiBackward<T> e{c.z[k], c.up[k], c.delta[k], c.ldt[k], md.act};
+        model_gemm<T>(s, n, md.w[k + 1], md.w[k + 2], kmaj(c.delta[k + 1], c.ldt[k + 1]), mnmaj(W1, md.w[k + 1]), e);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-example gradients: J[n][p] (autodiff.cpp:384-400).  Pure HBM write
+// stream: every CTA owns one example row and walks it with 16-byte stores.
+// ---------------------------------------------------------------------------
+struct LayerTable {
+    int S;
+    int64_t tin[kMaxLayers], tout[kMaxLayers], woff[kMaxLayers], boff[kMaxLayers];
+    int64_t lda[kMaxLayers], ldt[kMaxLayers];
+};
+
+inline LayerTable make_table(const ModelDesc& md, const int64_t* lda, const int64_t* ldt) {
+    LayerTable t{};
+    t.S = md.S;
+    for (int k = 0; k < md.S; ++k) {
+        t.tin[k] = md.w[k]; t.tout[k] = md.w[k + 1];
+        t.woff[k] = md.woff[k]; t.boff[k] = md.boff[k];
+        t.lda[k] = lda[k]; t.ldt[k] = ldt[k];
+    }
+    return t;
+}
+
+template <class T>
+struct CachePtrs {
+    const T* a[kMaxLayers];
+    const T* delta[kMaxLayers];
+};
+
+template <class T>
+__device__ __forceinline__ T jac_entry(const LayerTable& t, const CachePtrs<T>& cp, int64_t row, int64_t col) {
+    int k = 0;
+    while (k + 1 < t.S && col >= t.woff[k + 1]) ++k;
+    const int64_t e = col - t.woff[k];
+    const int64_t nw = t.tin[k] * t.tout[k];
+    const T* d = cp.delta[k] + row * t.ldt[k];
+    if (e < nw) {
+        const int64_t o = e / t.tin[k], i = e - o * t.tin[k];
+        return d[o] * cp.a[k][row * t.lda[k] + i];
+    }
+    return d[e - nw];
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T> cp, int64_t P, T* __restrict__ J,
+                                                       int64_t ldj, int64_t row0) {
+    const int64_t row = row0 + blockIdx.y;
+    T* out = J + (int64_t)blockIdx.y * ldj;
+    constexpr int V = 16 / sizeof(T);
+    for (int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V; c0 < P;
+         c0 += (int64_t)gridDim.x * blockDim.x * V) {
+        T v[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) v[u] = c0 + u < P ? jac_entry(t, cp, row, c0 + u) : T(0);
+        if (c0 + V <= ldj) {
+            if constexpr (sizeof(T) == 4) {
+                *reinterpret_cast<float4*>(out + c0) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+                *reinterpret_cast<double2*>(out + c0) = make_double2(v[0], v[1]);
+            }
+        } else {
+            for (int u = 0; u < V && c0 + u < ldj; ++u) out[c0 + u] = v[u];
+        }
+    }
+}
+
+template <class T>
+void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows, T* J, int64_t ldj,
+              cudaStream_t s) {
+    LayerTable t = make_table(md, c.lda, c.ldt);
+    CachePtrs<T> cp;
+    for (int k = 0; k < md.S; ++k) { cp.a[k] = c.a[k]; cp.delta[k] = c.delta[k]; }
+    const int64_t per_block = 256 * (16 / sizeof(T));
+    const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(md.P, per_block), 64);
+    for (int64_t r = 0; r < rows; r += 65535) {
+        const int64_t rr = std::min<int64_t>(65535, rows - r);
+        jacobian_kernel<T><<<dim3(gx, (unsigned)rr), 256, 0, s>>>(t, cp, md.P, J + r * ldj, ldj, row0 + r);
+        CK_LAUNCH();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers for the R-op
+// ---------------------------------------------------------------------------
+
+// out[r][c] = f(row-wise cache values) over `rows` = nprof * n rows
+template <class T>
+__global__ void rop_act_kernel(const T* __restrict__ in, int64_t ldi, const T* __restrict__ z, int64_t ldz,
+                               int64_t n, int64_t rows, int64_t cols, int act, T* __restrict__ out, int64_t ldo) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    const int64_t r = idx / cols, c = idx % cols, e = r % n;
+    out[r * ldo + c] = act_deriv<T>(act, z[e * ldz + c]) * in[r * ldi + c];
+}
+
+// rdelta_out = p * (rz - p . rz) for each (profile, example) row; zero in
+// raw_mean_output mode (autodiff.cpp:448-461).
+template <class T>
+__global__ void rop_softmax_kernel(const T* __restrict__ rz, int64_t ldr, const T* __restrict__ prob, int64_t ldp,
+                                   int64_t n, int64_t rows, int64_t tl, int mode, T* __restrict__ out, int64_t ldo) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int64_t e = r % n;
+    const T* pr = prob + e * ldp;
+    const T* x = rz + r * ldr;
+    T* o = out + r * ldo;
+    if (mode == kRawMean) {
+        for (int64_t m = 0; m < tl; ++m) o[m] = T(0);
+        return;
+    }
+    T pd = T(0);
+    for (int64_t m = 0; m < tl; ++m) pd += pr[m] * x[m];
+    for (int64_t m = 0; m < tl; ++m) o[m] = pr[m] * (x[m] - pd);
+}
+
+// R-backward epilogue: rd = acc (+ existing) ;  final = rd*act'(z) + up*act''(z)*rz
+// `accum` adds into out first (second GEMM of the pair).  unit_prof >= 0
+// marks the tangent layer itself, where rz = e_o (o = row / n).
+template <class T>
+struct EpiRback {
+    T* out;
+    int64_t ldo;
+    const T* z;
+    const T* up;
+    int64_t ldz;
+    const T* rz;  // may be null
+    int64_t ldr;
+    int64_t n;
+    int act;
+    int unit_prof;  // 1: rz is e_{row/n} (profile tangent layer)
+    int finalize;   // 0: store raw acc (first of two GEMMs); 1: acc(+out) then apply
+    int accum;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int, int64_t r, int64_t c, T acc) const {
+        T v = acc;
+        if (accum) v += out[r * ldo + c];
+        if (finalize) {
+            const int64_t e = r % n;
+            const T zz = z[e * ldz + c];
+            T rzv = T(0);
+            if (unit_prof) rzv = (c == r / n) ? T(1) : T(0);
+            else if (rz) rzv = rz[r * ldr + c];
+            v = v * act_deriv<T>(act, zz) + (up ? up[e * ldz + c] * act_second<T>(act, zz) * rzv : T(0));
+        }
+        out[r * ldo + c] = v;
+    }
+};
+
+// prof[o][n][t] = act'(z_k[n][o]) * W_{k+1}[t][o]   (R-forward one step above
+// the tangent layer for rz_k = e_o)
+template <class T>
+__global__ void profile_first_rz_kernel(const T* __restrict__ zk, int64_t ldz, const T* __restrict__ W1,
+                                        int64_t t1, int64_t t2, int64_t n, int act, T* __restrict__ out,
+                                        int64_t ldo) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= t1 * n * t2) return;
+    const int64_t t = idx % t2, r = idx / t2, o = r / n, e = r % n;
+    out[r * ldo + t] = act_deriv<T>(act, zk[e * ldz + o]) * W1[t * t1 + o];
+}
+
+// G_{S-1}[o][n][t] = p_t (delta_{to} - p_o): output-layer Hessian columns
+template <class T>
+__global__ void profile_output_kernel(const T* __restrict__ prob, int64_t ldp, int64_t tl, int64_t n, int mode,
+                                      T* __restrict__ out, int64_t ldo) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= tl * n * tl) return;
+    const int64_t t = idx % tl, r = idx / tl, o = r / n, e = r % n;
+    T v = T(0);
+    if (mode == kSoftmaxCE) {
+        const T pt = prob[e * ldp + t], po = prob[e * ldp + o];
+        v = pt * ((t == o ? T(1) : T(0)) - po);
+    }
+    out[r * ldo + t] = v;
+}
+
+// Q_{k-1}[i][n][t] = act'(z_{k-1}[n][i]) * [t == i]
+template <class T>
+__global__ void profile_q_kernel(const T* __restrict__ z, int64_t ldz, int64_t tk, int64_t n, int act,
+                                 T* __restrict__ out, int64_t ldo) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= tk * n * tk) return;
+    const int64_t t = idx % tk, r = idx / tk, i = r / n, e = r % n;
+    out[r * ldo + t] = t == i ? act_deriv<T>(act, z[e * ldz + i]) : T(0);
+}
+
+// ---------------------------------------------------------------------------
+// R operand for one Hessian block: rows (o'', jj) of the tangent chunk
+//   m == k: R = s_n * G[o][n][o'']
+//   m <  k: R = s_n * Pm[o][n][o''] + [weight tangent] delta_k[n][o] * Qm[i][n][o'']
+// with s_n = a_k[n][i] for weight tangents (o, i) and 1 for bias tangents.
+// ---------------------------------------------------------------------------
+template <class T>
+struct RGenArgs {
+    const T* prof;  // G (m == k) or Pm, [T_{k+1}][n][ldp]
+    const T* q;     // Qm or null, [T_k][n][ldp]
+    int64_t ldp;
+    const T* ak;
+    int64_t ldak;
+    const T* dk;  // delta_k
+    int64_t lddk;
+    int64_t n, tink, toutk, tm1;  // T_k, T_{k+1}, T_{m+1}
+    int64_t j0, J;
+    T* R;
+    int64_t ldr;
+};
+
+template <class T>
+__global__ void rgen_kernel(RGenArgs<T> g) {
+    const int64_t rows = g.tm1 * g.J;
+    const int64_t cols4 = ceil_div(g.n, 4);
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= rows * cols4) return;
+    const int64_t r = idx / cols4, n0 = (idx % cols4) * 4;
+    const int64_t opp = r / g.J, jj = r % g.J, j = g.j0 + jj;
+    const int64_t nw = g.toutk * g.tink;
+    const bool wt = j < nw;
+    const int64_t o = wt ? j / g.tink : j - nw;
+    const int64_t i = wt ? j - o * g.tink : 0;
+    T* out = g.R + r * g.ldr;
+    for (int u = 0; u < 4; ++u) {
+        const int64_t e = n0 + u;
+        if (e >= g.ldr) break;
+        T v = T(0);
+        if (e < g.n) {
+            const T s = wt ? g.ak[e * g.ldak + i] : T(1);
+            v = s * g.prof[(o * g.n + e) * g.ldp + opp];
+            if (g.q && wt) v += g.dk[e * g.lddk + o] * g.q[(i * g.n + e) * g.ldp + opp];
+        }
+        out[e] = v;
+    }
+}
+
+// Hessian block epilogue: GEMM row r = (o'', jj), column c = input unit of
+// layer m (c == T_m is the bias column, fed by the ones column of a_m).
+template <class T>
+struct EpiHess {
+    T* H;
+    int64_t ldh;
+    int64_t J, j0, woffk, woffm, boffm, tm;
+    T alpha;
+    int diag;    // m == k
+    int mirror;  // write the transposed entry too
+    __device__ __forceinline__ int64_t gcol(int64_t opp, int64_t c) const {
+        return c < tm ? woffm + opp * tm + c : boffm + opp;
+    }
+    __device__ bool skip(int, int64_t r0, int64_t c0, int64_t bm, int64_t) const {
+        if (!diag || !mirror) return false;
+        const int64_t opp_min = r0 / J;
+        const int64_t jj_max = (r0 + bm - 1) / J > opp_min ? J - 1 : (r0 + bm - 1) % J;
+        const int64_t gr_max = woffk + j0 + jj_max;
+        return gcol(opp_min, c0) > gr_max;
+    }
+    __device__ void operator()(int, int64_t r, int64_t c, T acc) const {
+        const int64_t opp = r / J, jj = r - opp * J;
+        const int64_t gr = woffk + j0 + jj, gc = gcol(opp, c);
+        const T v = alpha * acc;
+        if (diag && mirror) {
+            if (gc > gr) return;
+            H[gr * ldh + gc] = v;
+            H[gc * ldh + gr] = v;
+        } else {
+            H[gr * ldh + gc] = v;
+            if (mirror) H[gc * ldh + gr] = v;
+        }
+    }
+};
+
+// HVP accumulation epilogue: rows o of step k, column c (c == T_k: bias)
+template <class T>
+struct EpiHv {
+    T* hv;
+    int64_t ldhv;  // stride between directions
+    int64_t woff, boff, tin;
+    T alpha;
+    int accum;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int b, int64_t o, int64_t c, T acc) const {
+        T* p = hv + b * ldhv + (c < tin ? woff + o * tin + c : boff + o);
+        *p = accum ? *p + alpha * acc : alpha * acc;
+    }
+};
+
+}  // namespace ck

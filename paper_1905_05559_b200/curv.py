@@ -1,0 +1,393 @@
+"""Host-side mirror of the reference curvkit API for the curvature hot path.
+
+Names, argument meaning and error behaviour follow the reference C++
+headers (/root/reference/proj/include/curv/{model,autodiff,curvature,
+eigensolve}.hpp) so that code and tests written against the reference read
+the same.  Every compute call goes through the C-ABI of
+libcurvkit_b200.so; there is no CPU path.
+
+Matrices are numpy float64 arrays (row-major), like the reference's
+DenseMatrix.  `precision` selects the device arithmetic: "f64" (default,
+the reference's), "f32", "tf32" (tcgen05 tensor cores) or "tf32x3".
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib
+from .errors import ContractError, ShapeError
+
+PRECISION = {"f64": 0, "f32": 1, "tf32": 2, "tf32x3": 3}
+
+
+class Activation(IntEnum):  # model.hpp:11
+    identity = 0
+    sigmoid = 1
+    tanh = 2
+    relu = 3
+
+
+class OutputMode(IntEnum):  # model.hpp:21
+    softmax_cross_entropy = 0
+    raw_mean_output = 1
+
+
+def _enum(e, v):
+    if isinstance(v, str):
+        try:
+            return e[v]
+        except KeyError:
+            raise ContractError(f"unknown {e.__name__.lower()}: {v}") from None
+    return e(v)
+
+
+@dataclass
+class ModelSpec:  # model.hpp:27-38
+    layer_widths: list
+    hidden_activation: Activation = Activation.tanh
+    output_mode: OutputMode = OutputMode.softmax_cross_entropy
+
+    def __post_init__(self):
+        self.layer_widths = [int(w) for w in self.layer_widths]
+        self.hidden_activation = _enum(Activation, self.hidden_activation)
+        self.output_mode = _enum(OutputMode, self.output_mode)
+
+    def num_layers(self):
+        return len(self.layer_widths)
+
+    def input_width(self):
+        return self.layer_widths[0]
+
+    def output_width(self):
+        return self.layer_widths[-1]
+
+    def validate(self):  # model.cpp:80-87
+        if len(self.layer_widths) < 2:
+            raise ContractError("model needs at least an input and an output layer")
+        if any(w < 1 for w in self.layer_widths):
+            raise ContractError("layer widths must be >= 1")
+        if self.output_mode == OutputMode.raw_mean_output and self.output_width() != 1:
+            raise ContractError("raw_mean_output requires an output width of 1")
+
+    def _c(self):
+        self.validate()
+        w = (C.c_int64 * len(self.layer_widths))(*self.layer_widths)
+        m = _lib.Model(len(self.layer_widths), w, int(self.hidden_activation), int(self.output_mode))
+        m._keep = w
+        return m
+
+
+@dataclass
+class Batch:  # model.hpp:49-54
+    x: np.ndarray
+    y: np.ndarray = None
+
+    def size(self):
+        return self.x.shape[0]
+
+
+@dataclass
+class CurvatureConfig:  # curvature.hpp:11-18
+    batch_size_h: int = 1
+    batch_size_g: int = 1
+    parallelism: int = 1
+    memory_cap: int = 4096
+
+    def _c(self):
+        return _lib.CurvatureConfig(self.batch_size_h, self.batch_size_g, self.parallelism, self.memory_cap)
+
+
+@dataclass
+class HessianResult:  # curvature.hpp:20-23
+    h: np.ndarray
+    asymmetry: float = 0.0
+
+
+@dataclass
+class GradResult:  # autodiff.hpp:15-18
+    grad_total: np.ndarray
+    n: int = 0
+
+
+@dataclass
+class EigenPairs:  # eigensolve.hpp:13-17
+    q: np.ndarray
+    lam: np.ndarray = field(default=None)
+
+    @property
+    def lambda_(self):
+        return self.lam
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and a.shape != shape:
+        raise ShapeError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def _p(a):
+    return a.ctypes.data_as(_lib.dptr) if a is not None else None
+
+
+def _prec(p):
+    if p not in PRECISION:
+        raise ContractError(f"unknown precision {p!r}; use one of {sorted(PRECISION)}")
+    return PRECISION[p]
+
+
+def param_count(spec: ModelSpec) -> int:  # model.cpp:89-95
+    out = C.c_int64()
+    _lib.check(_lib.load().curvkit_param_count(C.byref(spec._c()), C.byref(out)))
+    return out.value
+
+
+def weight_block_offset(spec: ModelSpec, k: int) -> int:  # model.cpp:142-147
+    w = spec.layer_widths
+    return sum(w[i] * w[i + 1] + w[i + 1] for i in range(k))
+
+
+def bias_block_offset(spec: ModelSpec, k: int) -> int:  # model.cpp:149-151
+    w = spec.layer_widths
+    return weight_block_offset(spec, k) + w[k] * w[k + 1]
+
+
+def flatten_params(weights, biases) -> np.ndarray:  # model.cpp:97-119
+    if len(weights) != len(biases) or not weights:
+        raise ShapeError("flatten_params: need one bias per weight matrix")
+    parts = []
+    for k, (w, b) in enumerate(zip(weights, biases)):
+        w = np.asarray(w, dtype=np.float64)
+        b = np.asarray(b, dtype=np.float64).reshape(-1)
+        if w.shape[0] != b.shape[0]:
+            raise ShapeError("flatten_params: bias length does not match weight rows")
+        if k + 1 < len(weights) and np.asarray(weights[k + 1]).shape[1] != w.shape[0]:
+            raise ShapeError("flatten_params: consecutive layer shapes do not chain")
+        parts += [w.reshape(-1), b]
+    return np.concatenate(parts)
+
+
+def unflatten_params(spec: ModelSpec, params):  # model.cpp:121-140
+    p = param_count(spec)
+    params = np.asarray(params, dtype=np.float64).reshape(-1)
+    if params.shape[0] != p:
+        raise ShapeError(f"unflatten_params: parameter vector has length {params.shape[0]}, model needs {p}")
+    w = spec.layer_widths
+    weights, biases, at = [], [], 0
+    for k in range(len(w) - 1):
+        weights.append(params[at:at + w[k] * w[k + 1]].reshape(w[k + 1], w[k]).copy())
+        at += w[k] * w[k + 1]
+        biases.append(params[at:at + w[k + 1]].copy())
+        at += w[k + 1]
+    return weights, biases
+
+
+def _inputs(spec: ModelSpec, params, batch: Batch):
+    spec.validate()
+    P = param_count(spec)
+    params = _f64(params).reshape(-1)
+    if params.shape[0] != P:
+        raise ShapeError(f"parameter vector has length {params.shape[0]}, model needs {P}")
+    x = _f64(batch.x)
+    if x.ndim != 2 or x.shape[1] != spec.input_width():
+        raise ShapeError(f"input width {x.shape[-1]} does not match model input {spec.input_width()}")
+    n = x.shape[0]
+    y = None
+    if spec.output_mode == OutputMode.softmax_cross_entropy:
+        y = _f64(batch.y)
+        if y.shape != (n, spec.output_width()):
+            raise ShapeError("target shape does not match model output")
+    return P, params, x, y, n
+
+
+def assemble_jacobian(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> np.ndarray:
+    """curvature.hpp:32-33: N x P, row n = gradient of C_n."""
+    P, params, x, y, n = _inputs(spec, params, batch)
+    out = np.empty((n, P))
+    _lib.check(_lib.load().curvkit_assemble_jacobian(C.byref(spec._c()), _p(params), _p(x), _p(y), n,
+                                                      _prec(precision), _p(out)))
+    return out
+
+
+def grad_batch(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> GradResult:
+    """autodiff.hpp:60: sum of per-example gradients in one batched pass."""
+    P, params, x, y, n = _inputs(spec, params, batch)
+    out = np.empty(P)
+    _lib.check(_lib.load().curvkit_grad_batch(C.byref(spec._c()), _p(params), _p(x), _p(y), n,
+                                               _prec(precision), _p(out)))
+    return GradResult(out, n)
+
+
+def per_example_grad(spec: ModelSpec, params, x, y=None, precision: str = "f64") -> np.ndarray:
+    """autodiff.hpp:55-56."""
+    x = _f64(x).reshape(1, -1)
+    y = None if y is None else _f64(y).reshape(1, -1)
+    return grad_batch(spec, params, Batch(x, y), precision).grad_total
+
+
+def hvp(spec: ModelSpec, params, batch: Batch, v, precision: str = "f64") -> np.ndarray:
+    """autodiff.hpp:66-67: H_batch v (v may be P or nvec x P)."""
+    P, params, x, y, n = _inputs(spec, params, batch)
+    v = _f64(v)
+    single = v.ndim == 1
+    V = v.reshape(1, -1) if single else v
+    if V.shape[1] != P:
+        raise ShapeError(f"hvp: direction has length {V.shape[1]}, model has {P} parameters")
+    out = np.empty_like(V)
+    _lib.check(_lib.load().curvkit_hvp(C.byref(spec._c()), _p(params), _p(x), _p(y), n, _p(V), V.shape[0],
+                                        _prec(precision), _p(out)))
+    return out[0] if single else out
+
+
+class HvpOperator:
+    """autodiff.hpp:76-89: v -> Hv over a fixed dataset with equal mini-batches."""
+
+    def __init__(self, spec: ModelSpec, params, data: Batch, batch_size: int, precision: str = "f64"):
+        self.spec, self.data, self.batch_size, self.precision = spec, data, int(batch_size), precision
+        self.p, self.params, self.x, self.y, self.n = _inputs(spec, params, data)
+        if self.batch_size < 1:
+            raise ContractError("HvpOperator: batch size must be >= 1")
+        if self.n == 0:
+            raise ContractError("HvpOperator: empty dataset")
+        if self.n % self.batch_size != 0:
+            raise ContractError(f"HvpOperator: dataset size {self.n} is not divisible by batch size "
+                                f"{self.batch_size}; refusing to drop the remainder")
+
+    def dim(self):
+        return self.p
+
+    def num_batches(self):
+        return self.n // self.batch_size
+
+    def apply(self, v):
+        v = _f64(v)
+        single = v.ndim == 1
+        V = v.reshape(1, -1) if single else v
+        if V.shape[1] != self.p:
+            raise ShapeError(f"hvp: direction has length {V.shape[1]}, model has {self.p} parameters")
+        out = np.empty_like(V)
+        _lib.check(_lib.load().curvkit_hvp_operator_apply(
+            C.byref(self.spec._c()), _p(self.params), _p(self.x), _p(self.y), self.n, self.batch_size, _p(V),
+            V.shape[0], _prec(self.precision), _p(out)))
+        return out[0] if single else out
+
+
+def assemble_hessian(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfig = None,
+                     precision: str = "f64", verify: bool = True) -> HessianResult:
+    """curvature.hpp:27-29.  verify=True assembles each diagonal layer block
+    from both triangles and reports the pre-symmetrization asymmetry like the
+    reference; verify=False fills the lower triangle and mirrors it."""
+    config = config or CurvatureConfig(batch_size_h=max(1, Batch(dataset.x).size()))
+    P, params, x, y, n = _inputs(spec, params, dataset)
+    h = np.empty((P, P))
+    asym = C.c_double(0.0)
+    cfg = config._c()
+    _lib.check(_lib.load().curvkit_assemble_hessian(C.byref(spec._c()), _p(params), _p(x), _p(y), n, C.byref(cfg),
+                                                     _prec(precision), int(verify), _p(h), C.byref(asym)))
+    return HessianResult(h, asym.value)
+
+
+def assemble_opg(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfig = None,
+                 precision: str = "f64") -> np.ndarray:
+    """curvature.hpp:38-40: (1/N) J^T J, symmetric PSD."""
+    config = config or CurvatureConfig(batch_size_g=max(1, Batch(dataset.x).size()))
+    P, params, x, y, n = _inputs(spec, params, dataset)
+    g = np.empty((P, P))
+    cfg = config._c()
+    _lib.check(_lib.load().curvkit_assemble_opg(C.byref(spec._c()), _p(params), _p(x), _p(y), n, C.byref(cfg),
+                                                 _prec(precision), _p(g)))
+    return g
+
+
+def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 20, power_iters: int = 2,
+             seed: int = 0, precision: str = "f64") -> EigenPairs:
+    """Top-k eigenpairs of G = (1/N) J^T J by a randomized range finder
+    (replaces eigensolve.hpp:75-76 opg_eigs_incremental).  Eigenvalues are
+    descending; columns of q are orthonormal eigenvectors."""
+    P, params, x, y, n = _inputs(spec, params, dataset)
+    q = np.empty((P, k))
+    lam = np.empty(k)
+    _lib.check(_lib.load().curvkit_opg_topk(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
+                                             int(oversample), int(power_iters), int(seed), _prec(precision),
+                                             _p(q), _p(lam)))
+    return EigenPairs(q, lam)
+
+
+# ---- low/full-rank operators from eigenpairs (eigensolve.hpp:78-93) ------------
+
+def low_rank_quadform(pairs: EigenPairs, x) -> float:
+    t = pairs.q.T @ np.asarray(x, dtype=np.float64)
+    return float(np.sum(pairs.lam * t * t))
+
+
+def low_rank_apply(pairs: EigenPairs, x) -> np.ndarray:
+    t = pairs.q.T @ np.asarray(x, dtype=np.float64)
+    return pairs.q @ (pairs.lam * t)
+
+
+def default_lambda_tilde(pairs: EigenPairs) -> float:  # eigensolve.cpp:480-488
+    if len(pairs.lam) == 0:
+        raise ContractError("default_lambda_tilde: no eigenvalues")
+    lk = float(pairs.lam[-1])
+    if not lk > 0.0:
+        raise ContractError(f"default_lambda_tilde: smallest retained eigenvalue {lk} is not positive; "
+                            "pass an explicit lambda_tilde")
+    return lk
+
+
+def full_rank_quadform(pairs: EigenPairs, lambda_tilde: float, x) -> float:
+    if not lambda_tilde > 0.0:
+        raise ContractError(f"full-rank approximation requires lambda_tilde > 0, got {lambda_tilde}")
+    x = np.asarray(x, dtype=np.float64)
+    t = pairs.q.T @ x
+    return float(np.sum(pairs.lam * t * t) + lambda_tilde * x @ x - lambda_tilde * t @ t)
+
+
+def full_rank_apply(pairs: EigenPairs, lambda_tilde: float, x) -> np.ndarray:
+    if not lambda_tilde > 0.0:
+        raise ContractError(f"full-rank approximation requires lambda_tilde > 0, got {lambda_tilde}")
+    x = np.asarray(x, dtype=np.float64)
+    t = pairs.q.T @ x
+    return pairs.q @ (pairs.lam * t) + lambda_tilde * (x - pairs.q @ t)
+
+
+# ---- device-resident entry points (torch tensors or raw pointers) -------------
+
+def _ptr(t):
+    return C.c_void_p(t if isinstance(t, int) else t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        return C.c_void_p(0)
+    return C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+
+
+def dev_assemble_hessian(spec, params, x, labels, n, out, ldh, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_assemble_hessian(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
+                                                         _prec(precision), _ptr(out), ldh, _stream(stream)))
+
+
+def dev_assemble_opg(spec, params, x, labels, n, out, ldg, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_assemble_opg(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
+                                                     _prec(precision), _ptr(out), ldg, _stream(stream)))
+
+
+def dev_assemble_jacobian(spec, params, x, labels, n, out, ldj, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_assemble_jacobian(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels),
+                                                          n, _prec(precision), _ptr(out), ldj, _stream(stream)))
+
+
+def dev_opg_topk(spec, params, x, labels, n, k, oversample, power_iters, seed, q, lam, precision="tf32",
+                 stream=None):
+    _lib.check(_lib.load().curvkit_dev_opg_topk(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n, k,
+                                                 oversample, power_iters, seed, _prec(precision), _ptr(q), _ptr(lam),
+                                                 _stream(stream)))
+
+
+def launch_count() -> int:
+    return int(_lib.load().curvkit_launch_count())

@@ -1,0 +1,174 @@
+"""Parity of the CUDA product (through the C-ABI) against the reference's own
+outputs (tests/golden, produced by the unmodified reference library) and the
+C oracle.  Tolerances (north_star, BASELINE.json): relative Frobenius error
+<= 1e-5 in fp64 mode (we hold 1e-10), <= 1e-3 in fp32 / TF32 modes; top-k
+eigenvalues within 1e-3 relative."""
+import numpy as np
+import pytest
+
+from conftest import SMALL_CASES, load_golden, rel_fro
+from paper_1905_05559_b200 import curv
+from paper_1905_05559_b200.workloads import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-10, "f32": 1e-5, "tf32": 1e-3, "tf32x3": 1e-5}
+PRECS = list(TOL)
+
+
+def spec_of(g):
+    s = g["spec"]
+    return curv.ModelSpec(s["widths"], s["activation"], s["output_mode"])
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("name", SMALL_CASES + ["config0", "linear_diag"])
+def test_hessian_matches_reference(name, prec):
+    g = load_golden(name)
+    spec = spec_of(g)
+    b = int(g["batch"]) if "batch" in g else g["x"].shape[0]
+    cfg = curv.CurvatureConfig(batch_size_h=b)
+    hr = curv.assemble_hessian(spec, g["params"], curv.Batch(g["x"], g["y"]), cfg, precision=prec, verify=True)
+    if np.abs(g["H"]).max() == 0.0:
+        assert np.abs(hr.h).max() <= 1e-12
+        return
+    assert rel_fro(hr.h, g["H"]) <= TOL[prec]
+    assert np.array_equal(hr.h, hr.h.T)
+    if prec == "f64":
+        assert hr.asymmetry <= 1e-8 * max(1.0, np.abs(hr.h).max())
+    # mirrored (fast) assembly equals the verified one
+    fast = curv.assemble_hessian(spec, g["params"], curv.Batch(g["x"], g["y"]), cfg, precision=prec, verify=False)
+    assert rel_fro(fast.h, g["H"]) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("name", SMALL_CASES + ["config0", "linear_diag"])
+def test_opg_and_jacobian_match_reference(name, prec):
+    g = load_golden(name)
+    spec = spec_of(g)
+    b = int(g["batch"]) if "batch" in g else g["x"].shape[0]
+    G = curv.assemble_opg(spec, g["params"], curv.Batch(g["x"], g["y"]), curv.CurvatureConfig(batch_size_g=b),
+                          precision=prec)
+    assert rel_fro(G, g["G"]) <= TOL[prec]
+    assert np.array_equal(G, G.T)
+    J = curv.assemble_jacobian(spec, g["params"], curv.Batch(g["x"], g["y"]), precision=prec)
+    assert rel_fro(J, g["J"]) <= (1e-13 if prec == "f64" else 1e-6)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_hvp_grad_match_reference(name, prec):
+    g = load_golden(name)
+    spec = spec_of(g)
+    batch = curv.Batch(g["x"], g["y"])
+    tol = 1e-12 if prec == "f64" else 1e-5
+    HV = curv.hvp(spec, g["params"], batch, g["V"], precision=prec)
+    for a, b in zip(HV, g["HV"]):
+        assert rel_fro(a, b) <= tol
+    op = curv.HvpOperator(spec, g["params"], batch, int(g["batch"]), precision=prec)
+    assert rel_fro(op.apply(g["V"]), g["HVop"]) <= tol
+    assert rel_fro(curv.grad_batch(spec, g["params"], batch, precision=prec).grad_total, g["grad"]) <= tol
+
+
+def test_paper_listings_on_gpu():
+    g = load_golden("linear_diag")
+    spec = spec_of(g)
+    batch = curv.Batch(g["x"], g["y"])
+    J = curv.assemble_jacobian(spec, g["params"], batch)
+    assert list(J[0, :4]) == [1, 2, 3, 4] and list(J[1, :4]) == [2, 3, 4, 5]   # Out [2], [3]
+    assert list(curv.grad_batch(spec, g["params"], batch).grad_total[:4]) == [3, 5, 7, 9]  # Out [4]
+    G = curv.assemble_opg(spec, g["params"], batch, curv.CurvatureConfig(batch_size_g=2))
+    gbar = curv.grad_batch(spec, g["params"], batch).grad_total / 2
+    assert np.abs(G - np.outer(gbar, gbar)).max() > 1e-3                    # Eq. 11
+    assert np.abs(G - g["G"]).max() <= 1e-14
+
+
+def test_hvp_symmetry_linearity():
+    # acceptance criterion 9 on the (6,5,4) sigmoid model
+    g = load_golden("sigmoid654")
+    spec = spec_of(g)
+    batch = curv.Batch(g["x"], g["y"])
+    rng = np.random.default_rng(107)
+    P = g["params"].shape[0]
+    U = rng.normal(size=(20, P))
+    V = rng.normal(size=(20, P))
+    HU = curv.hvp(spec, g["params"], batch, U)
+    HV = curv.hvp(spec, g["params"], batch, V)
+    for u, v, hu, hv in zip(U, V, HU, HV):
+        assert abs(u @ hv - v @ hu) <= 1e-9 * max(1.0, abs(u @ hv))
+    a, b = 0.7, -1.3
+    HC = curv.hvp(spec, g["params"], batch, a * U + b * V)
+    assert rel_fro(HC, a * HU + b * HV) <= 1e-9
+
+
+@pytest.mark.parametrize("prec", ["f64", "tf32"])
+def test_opg_topk_matches_dense_eig(prec):
+    g = load_golden("config0")
+    spec = spec_of(g)
+    k = 5
+    pairs = curv.opg_eigs(spec, g["params"], curv.Batch(g["x"], g["y"]), k, oversample=10, power_iters=2,
+                          seed=3, precision=prec)
+    w = np.linalg.eigvalsh(g["G"])[::-1]
+    assert np.all(np.abs(pairs.lam - w[:k]) <= 1e-3 * np.abs(w[:k]))
+    assert np.all(np.diff(pairs.lam) <= 0)
+    qtq = pairs.q.T @ pairs.q
+    assert np.abs(qtq - np.eye(k)).max() <= (1e-8 if prec == "f64" else 1e-4)
+    r = g["G"] @ pairs.q - pairs.q * pairs.lam
+    assert np.linalg.norm(r) <= 1e-3 * np.linalg.norm(g["G"])
+
+
+# ---- full-size pins: configs 1 and 2 against reference columns / rows ---------
+
+def _device_inputs(wl, torch, dtype):
+    params, x, y, labels = wl.draw()
+    dev = torch.device("cuda:0")
+    return (torch.tensor(params, dtype=dtype, device=dev), torch.tensor(x, dtype=dtype, device=dev),
+            torch.tensor(labels, dtype=torch.int32, device=dev))
+
+
+@pytest.mark.parametrize("prec", ["tf32", "f64"])
+def test_config1_hessian_and_opg_pins(prec):
+    torch = pytest.importorskip("torch")
+    wl = CONFIGS["c1"]
+    pins = load_golden("c1_pins")
+    dtype = torch.float64 if prec == "f64" else torch.float32
+    p, x, lab = _device_inputs(wl, torch, dtype)
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P = wl.P
+    ld = (P + 3) // 4 * 4
+    H = torch.empty((P, ld), dtype=dtype, device="cuda:0")
+    curv.dev_assemble_hessian(spec, p, x, lab, wl.n, H, ld, precision=prec)
+    torch.cuda.synchronize()
+    cols = torch.tensor(pins["cols"], device="cuda:0")
+    got = H[:, :P][:, cols].double().cpu().numpy()
+    tol = 1e-9 if prec == "f64" else 1e-3
+    for j in range(got.shape[1]):
+        assert rel_fro(got[:, j], pins["hcols"][:, j]) <= tol, (j, rel_fro(got[:, j], pins["hcols"][:, j]))
+    # symmetry by construction
+    sub = H[:2000, :2000]
+    assert torch.equal(sub, sub.T)
+    del H
+    G = torch.empty((P, ld), dtype=dtype, device="cuda:0")
+    curv.dev_assemble_opg(spec, p, x, lab, wl.n, G, ld, precision=prec)
+    torch.cuda.synchronize()
+    rows = torch.tensor(pins["rows"], device="cuda:0")
+    gr = G[rows, :P].double().cpu().numpy()
+    for j in range(gr.shape[0]):
+        assert rel_fro(gr[j], pins["grows"][j]) <= tol
+
+
+def test_config2_hessian_pins_tf32():
+    torch = pytest.importorskip("torch")
+    wl = CONFIGS["c2"]
+    pins = load_golden("c2_pins")
+    p, x, lab = _device_inputs(wl, torch, torch.float32)
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P = wl.P
+    ld = (P + 3) // 4 * 4
+    H = torch.empty((P, ld), dtype=torch.float32, device="cuda:0")
+    curv.dev_assemble_hessian(spec, p, x, lab, wl.n, H, ld, precision="tf32")
+    torch.cuda.synchronize()
+    cols = torch.tensor(pins["cols"], device="cuda:0")
+    got = H[:, :P][:, cols].double().cpu().numpy()
+    for j in range(got.shape[1]):
+        assert rel_fro(got[:, j], pins["hcols"][:, j]) <= 1e-3, j
