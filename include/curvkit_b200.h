@@ -140,6 +140,19 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
                          int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
                          void* stream);
 
+/* The curvature GEMM engine on its own (fp32 storage): C[m][n] = alpha *
+ * sum_k A(m,k) B(n,k) with A(m,k) = a[m*lda+k] if a_kmajor else a[k*lda+m]
+ * (likewise B).  TF32/TF32X3 run the tcgen05 kernel, F32 the SIMT one. */
+int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, int32_t a_kmajor,
+                     const float* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha,
+                     int32_t precision, void* stream);
+
+/* CUDA-event timing of the hot kernels (GEMMs, Jacobian writer, R-operand
+ * generator, forward/backward).  begin() clears and enables; end() writes a
+ * JSON object {region: {ms, launches, flops, bytes}} into json_out. */
+int curvkit_profile_begin(void);
+int curvkit_profile_end(char* json_out, int64_t capacity);
+
 /* Kernel-launch counter (all kernels this library launched in-process). */
 int64_t curvkit_launch_count(void);
 

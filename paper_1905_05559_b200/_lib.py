@@ -33,6 +33,8 @@ SIGNATURES = {
     "curvkit_last_error": [],
     "curvkit_version": [],
     "curvkit_launch_count": [],
+    "curvkit_profile_begin": [],
+    "curvkit_profile_end": [C.c_char_p, i64],
     "curvkit_param_count": [_MP, C.POINTER(i64)],
     "curvkit_assemble_jacobian": [_MP, dptr, dptr, dptr, i64, i32, dptr],
     "curvkit_grad_batch": [_MP, dptr, dptr, dptr, i64, i32, dptr],
@@ -46,6 +48,7 @@ SIGNATURES = {
     "curvkit_dev_assemble_hessian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_opg": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_jacobian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
+    "curvkit_dev_gemm": [i64, i64, i64, vptr, i64, i32, vptr, i64, i32, vptr, i64, C.c_float, i32, vptr],
     "curvkit_dev_opg_topk": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
 }
 _RESTYPES = {"curvkit_last_error": C.c_char_p, "curvkit_version": C.c_char_p, "curvkit_launch_count": i64}

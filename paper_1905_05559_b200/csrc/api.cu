@@ -15,6 +15,7 @@
 #include "eigen.cuh"
 #include "gemm_tc.cuh"
 #include "model.cuh"
+#include "prof.cuh"
 
 namespace ck {
 std::atomic<int64_t> g_launches{0};
@@ -328,6 +329,46 @@ const char* curvkit_last_error(void) { return g_err.c_str(); }
 const char* curvkit_version(void) { return "curvkit-b200 0.1 (sm_100a)"; }
 int64_t curvkit_launch_count(void) { return ck::g_launches.load(); }
 
+int curvkit_profile_begin(void) {
+    return guard([&] {
+        Profiler& p = Profiler::get();
+        std::lock_guard<std::mutex> g(p.mu);
+        for (auto& kv : p.recs)
+            for (auto& r : kv.second) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+        p.recs.clear();
+        p.on = true;
+    });
+}
+
+int curvkit_profile_end(char* json_out, int64_t capacity) {
+    return guard([&] {
+        Profiler& p = Profiler::get();
+        std::lock_guard<std::mutex> g(p.mu);
+        p.on = false;
+        CK_CUDA(cudaDeviceSynchronize());
+        std::string js = "{";
+        bool first = true;
+        for (auto& kv : p.recs) {
+            double ms = 0.0, fl = 0.0, by = 0.0;
+            for (auto& r : kv.second) {
+                float t = 0.f;
+                CK_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+                ms += t; fl += r.flops; by += r.bytes;
+                cudaEventDestroy(r.a); cudaEventDestroy(r.b);
+            }
+            char buf[256];
+            snprintf(buf, sizeof(buf), "%s\"%s\": {\"ms\": %.6f, \"launches\": %zu, \"flops\": %.6e, \"bytes\": %.6e}",
+                     first ? "" : ", ", kv.first.c_str(), ms, kv.second.size(), fl, by);
+            js += buf;
+            first = false;
+        }
+        js += "}";
+        p.recs.clear();
+        if ((int64_t)js.size() + 1 > capacity) throw CurvError(kShapeError, "profile buffer too small");
+        std::memcpy(json_out, js.c_str(), js.size() + 1);
+    });
+}
+
 int curvkit_param_count(const curvkit_model* model, int64_t* p_out) {
     return guard([&] { *p_out = make_desc(model).P; });
 }
@@ -489,6 +530,20 @@ int curvkit_dev_assemble_jacobian(const curvkit_model* model, const void* params
         };
         if (is_f64(precision)) run(double{});
         else run(float{});
+    });
+}
+
+int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, int32_t a_kmajor,
+                     const float* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha,
+                     int32_t precision, void* stream) {
+    return guard([&] {
+        if (m < 0 || n < 0 || k < 1) shape("dev_gemm: bad shape");
+        if (precision == kF64) contract("dev_gemm: fp32 storage only");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        EpiStore<float> e{c, ldc, 0, alpha, 0.f};
+        Opnd<float> A = a_kmajor ? kmaj(a, lda) : mnmaj(a, lda);
+        Opnd<float> B = b_kmajor ? kmaj(b, ldb) : mnmaj(b, ldb);
+        CurvGemm<float, EpiStore<float>>::run(precision, s, m, n, k, A, B, e);
     });
 }
 

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "model.cuh"
+#include "prof.cuh"
 
 namespace ck {
 
@@ -140,6 +141,8 @@ struct Engine {
     // ---------------------------------------------------------------- opg
     void opg(const T* J, int64_t ldj, int64_t n, T* G, int64_t ldg) {
         EpiSymLower<T> e{G, ldg, T(1) / T(n)};
+        ProfScope ps("opg_gemm", s, 2.0 * (double)md.P * (double)(md.P + 1) / 2.0 * (double)n,
+                     (double)sizeof(T) * ((double)n * md.P + (double)md.P * md.P));
         CurvGemm<T, EpiSymLower<T>>::run(prec, s, md.P, md.P, n, mnmaj(J, ldj), mnmaj(J, ldj), e);
     }
 
@@ -149,6 +152,22 @@ struct Engine {
     //   Pm [T_{k+1}][n][ldt_m]       rdelta_m, m < k, same tangents
     //   Qm [T_k][n][ldt_m]           rdelta_m from the explicit delta*RW term
     size_t chunk_bytes = size_t(48) << 20;  // R operand chunk, sized to stay in L2
+
+    // Output entries of one (k, m, chunk) block that the assembly needs: all
+    // of an off-diagonal block, the lower triangle (gc <= gr) of a diagonal one.
+    double hess_required_entries(int k, int m, int64_t j0, int64_t Jc) const {
+        const int64_t tm = md.w[m], tm1 = md.w[m + 1];
+        if (m != k) return (double)Jc * tm1 * (tm + 1);
+        double cnt = 0.0;
+        for (int64_t jj = 0; jj < Jc; ++jj) {
+            const int64_t j = j0 + jj;  // row offset inside the block
+            for (int64_t o = 0; o < tm1; ++o) {
+                cnt += (double)std::max<int64_t>(0, std::min<int64_t>(tm, j - o * tm + 1));
+                if (j >= md.boff[m] - md.woff[m] + o) cnt += 1.0;
+            }
+        }
+        return cnt;
+    }
 
     void hessian(const T* params, const Cache<T>& c, T* H, int64_t ldh, bool verify) {
         const int S = md.S;
@@ -236,10 +255,15 @@ struct Engine {
                     RGenArgs<T> g{m == k ? G : Pm[m], m == k ? nullptr : Qm[m], m == k ? c.ldt[k] : c.ldt[m],
                                   c.a[k], c.lda[k], c.delta[k], c.ldt[k], n, md.w[k], md.w[k + 1], tm1, j0, Jc,
                                   dptr<T>(rbuf), ldr};
-                    rgen_kernel<T><<<blocks_for(tm1 * Jc * ceil_div(n, 4)), 256, 0, s>>>(g);
-                    CK_LAUNCH();
+                    {
+                        ProfScope ps("hess_rgen", s, 0.0, (double)sizeof(T) * tm1 * Jc * ldr);
+                        rgen_kernel<T><<<blocks_for(tm1 * Jc * ceil_div(n, 4)), 256, 0, s>>>(g);
+                        CK_LAUNCH();
+                    }
                     EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], md.w[m], T(1) / T(n),
                                  m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
+                    ProfScope ps("hess_gemm", s, 2.0 * (double)n * hess_required_entries(k, m, j0, Jc),
+                                 (double)sizeof(T) * ((double)tm1 * Jc * ldr + hess_required_entries(k, m, j0, Jc)));
                     CurvGemm<T, EpiHess<T>>::run(prec, s, tm1 * Jc, md.w[m] + 1, n, kmaj(dptr<T>(rbuf), ldr),
                                                  mnmaj(c.a[m], c.lda[m]), e);
                 }

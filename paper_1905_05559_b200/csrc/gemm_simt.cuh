@@ -121,6 +121,15 @@ struct EpiStore {
         T* p = c + b * bstride + m * ldc + n;
         *p = beta == T(0) ? alpha * acc : alpha * acc + beta * *p;
     }
+    // tensor-core epilogue: v[rr][cc] = acc(row0 + rr, col0 + cc), coalesced rows
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
+        const int64_t col = col0 + lane;
+        if (col >= N) return;
+        for (int rr = 0; rr < 32 && row0 + rr < M; ++rr) {
+            T* p = c + (row0 + rr) * ldc + col;
+            *p = beta == T(0) ? alpha * (T)v[rr][lane] : alpha * (T)v[rr][lane] + beta * *p;
+        }
+    }
 };
 
 // Symmetric product (SYRK-style): only tiles touching the lower triangle run;
@@ -139,6 +148,18 @@ struct EpiSymLower {
         const T v = alpha * acc;
         c[m * ldc + n] = v;
         c[n * ldc + m] = v;
+    }
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
+        {  // lower entries, row by row (lanes along columns)
+            const int64_t col = col0 + lane;
+            for (int rr = 0; rr < 32 && row0 + rr < M; ++rr)
+                if (col < N && col <= row0 + rr) c[(row0 + rr) * ldc + col] = alpha * (T)v[rr][lane];
+        }
+        {  // mirrored entries, column by column (lanes along rows)
+            const int64_t row = row0 + lane;
+            for (int cc = 0; cc < 32 && col0 + cc < N; ++cc)
+                if (row < M && col0 + cc < row) c[(col0 + cc) * ldc + row] = alpha * (T)v[lane][cc];
+        }
     }
 };
 

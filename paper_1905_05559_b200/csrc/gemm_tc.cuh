@@ -1,3 +1,458 @@
-// gemm_tc.cuh -- tcgen05 (TF32) GEMM for the curvature products.
+// gemm_tc.cuh -- tcgen05 TF32 GEMM for the curvature products (sm_100a).
+//
+// C(m, n) = sum_k A(m, k) B(n, k), A/B fp32 in HBM (K-major or MN-major),
+// multiplied by kind::tf32 tensor-core MMAs with fp32 accumulation in TMEM.
+//
+//   warp 0      TMA producer: cp.async.bulk.tensor 2D tiles, SWIZZLE_128B,
+//               4-stage smem ring (full/empty mbarriers)
+//   warp 1      MMA issuer: one lane issues tcgen05.mma (M=128, N=BN, K=8)
+//               and commits completion to the empty / tmem_full barriers
+//   warp 2      TMEM allocator (2 x BN accumulator columns, double buffer)
+//   warps 4-7   epilogue: tcgen05.ld 32x32 blocks -> smem transpose ->
+//               coalesced stores through the epilogue functor (plain store,
+//               symmetric mirror, Hessian block mapping)
+// Persistent: one CTA per SM walks the tile list; tiles the functor marks
+// as skippable (upper triangle of a symmetric product) cost nothing.
+//
+// k3xTF32 runs three MMAs per k-step on hi/lo TF32 splits of both operands
+// (hi*hi + hi*lo + lo*hi); the lo parts are separate operands prepared by
+// split_tf32_kernel.
 #pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "curvature.cuh"
+
+namespace ck {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int STAGES = 4;
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SWIZZLE_128B shared-memory matrix descriptor (sm_100 layout: version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // version
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, M=128, N=n.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
+    return (1u << 4)                       // D format f32
+           | (2u << 7)                     // A tf32
+           | (2u << 10)                    // B tf32
+           | ((a_mn ? 1u : 0u) << 15)      // A major (0 K, 1 MN)
+           | ((b_mn ? 1u : 0u) << 16)      // B major
+           | ((uint32_t)(n >> 3) << 17)    // N / 8
+           | ((uint32_t)(BM >> 4) << 24);  // M / 16
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- kernel
+struct TcShape {
+    int64_t M, N, K;
+    int a_mn, b_mn;  // operand is MN-major
+    int nsplit;      // 1: tf32, 3: 3xTF32 (hi*hi + hi*lo + lo*hi)
+};
+
+template <int BN>
+struct TcSmem {
+    static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+    static constexpr int B_BYTES = BN * BK * 4;
+    static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;
+    static constexpr int MAX_SMEM = 227 * 1024;
+    __host__ __device__ static constexpr int stage_bytes(int nsplit) { return (A_BYTES + B_BYTES) * (nsplit == 1 ? 1 : 2); }
+    __host__ __device__ static constexpr int stages(int nsplit) {
+        const int st = (MAX_SMEM - 1024 - EPI_BYTES - 256) / stage_bytes(nsplit);
+        return st > STAGES ? STAGES : st;
+    }
+    __host__ __device__ static constexpr int bytes(int nsplit) {
+        return 1024 + stages(nsplit) * stage_bytes(nsplit) + EPI_BYTES + 256;
+    }
+};
+
+// Load one operand tile (rows x BK) of a K-major or MN-major operand.
+template <int ROWS>
+__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int mn, int64_t r0,
+                                          int64_t k0) {
+    if (!mn) {
+        tma_load_2d(dst, map, bar, (int32_t)k0, (int32_t)r0);
+    } else {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) tma_load_2d(dst + i * 4096, map, bar, (int32_t)(r0 + 32 * i), (int32_t)k0);
+    }
+}
+
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+               const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcShape sh,
+               Epi epi) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_BYTES = TcSmem<BN>::A_BYTES, B_BYTES = TcSmem<BN>::B_BYTES;
+    const int split = sh.nsplit == 1 ? 1 : 2;  // operand copies per stage (hi[, lo])
+    const int STAGE_BYTES = (A_BYTES + B_BYTES) * split;
+    const int NST = TcSmem<BN>::stages(sh.nsplit);
+    uint8_t* stage_base = smem;
+    float* epi_buf = reinterpret_cast<float*>(smem + NST * STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES + TcSmem<BN>::EPI_BYTES);
+    uint64_t* full = bars;                // [STAGES]
+    uint64_t* empty = bars + STAGES;      // [STAGES]
+    uint64_t* tfull = bars + 2 * STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;         // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t mt = ceil_div(sh.M, BM), nt = ceil_div(sh.N, BN);
+    const int64_t ntiles = mt * nt;
+    const int64_t nk = ceil_div(sh.K, BK);
+
+    if (warp == 0 && lane == 0) {
+        prefetch_map(&mapA);
+        prefetch_map(&mapB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "n"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes = (uint32_t)STAGE_BYTES;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t m0 = (t / nt) * BM, n0 = (t % nt) * BN;
+                if (epi.skip(0, m0, n0, BM, BN)) continue;
+                for (int64_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], bytes);
+                    uint8_t* sa = stage_base + stage * STAGE_BYTES;
+                    uint8_t* sb = sa + A_BYTES * split;
+                    const int64_t k0 = kb * BK;
+                    load_tile<BM>(sa, &mapA, &full[stage], sh.a_mn, m0, k0);
+                    load_tile<BN>(sb, &mapB, &full[stage], sh.b_mn, n0, k0);
+                    if (split == 2) {
+                        load_tile<BM>(sa + A_BYTES, &mapAlo, &full[stage], sh.a_mn, m0, k0);
+                        load_tile<BN>(sb + B_BYTES, &mapBlo, &full[stage], sh.b_mn, n0, k0);
+                    }
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            const uint32_t idesc = idesc_tf32(BN, sh.a_mn, sh.b_mn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t m0 = (t / nt) * BM, n0 = (t % nt) * BN;
+                if (epi.skip(0, m0, n0, BM, BN)) continue;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                for (int64_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
+                    const uint32_t sb = sa + A_BYTES * split;
+#pragma unroll
+                    for (int ks = 0; ks < BK / 8; ++ks) {
+                        // K-major: +32 B inside the 128 B swizzle row; MN-major: next 8-row group
+                        const uint32_t aoff = sh.a_mn ? ks * 1024 : ks * 32;
+                        const uint32_t boff = sh.b_mn ? ks * 1024 : ks * 32;
+                        const uint32_t albo = sh.a_mn ? 4096 : 16, blbo = sh.b_mn ? 4096 : 16;
+                        const uint64_t ahi = smem_desc(sa + aoff, albo, 1024);
+                        const uint64_t bhi = smem_desc(sb + boff, blbo, 1024);
+                        const uint32_t accf = (kb > 0 || ks > 0) ? 1u : 0u;
+                        mma_tf32(d, ahi, bhi, idesc, accf);
+                        if (split == 2) {
+                            const uint64_t alo = smem_desc(sa + A_BYTES + aoff, albo, 1024);
+                            const uint64_t blo = smem_desc(sb + B_BYTES + boff, blbo, 1024);
+                            mma_tf32(d, ahi, blo, idesc, 1u);
+                            mma_tf32(d, alo, bhi, idesc, 1u);
+                        }
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue
+        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+        float(*buf)[33] = reinterpret_cast<float(*)[33]>(epi_buf + ew * 32 * 33);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t m0 = (t / nt) * BM, n0 = (t % nt) * BN;
+            if (epi.skip(0, m0, n0, BM, BN)) continue;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row0 = m0 + ew * 32;
+            for (int cb = 0; cb < BN / 32; ++cb) {
+                const int64_t col0 = n0 + cb * 32;
+                if (col0 >= sh.N) break;
+                float v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                if (row0 < sh.M) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) buf[lane][i] = v[i];
+                    __syncwarp();
+                    epi.block(row0, col0, sh.M, sh.N, buf, lane);
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN));
+    }
+}
+
+// ---------------------------------------------------------------- host side
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw CurvError(kCudaError, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D fp32 tensor map over an operand of `rows` x K (K-major: p[r*ld + k];
+// MN-major: p[k*ld + r]), box = one BK x box_rows tile (or 32 x 32 pieces).
+inline CUtensorMap make_map(const float* p, int64_t rows, int64_t K, int64_t ld, int mn, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2], strides[1];
+    cuuint32_t box[2], es[2] = {1, 1};
+    if (!mn) {
+        dims[0] = (cuuint64_t)K; dims[1] = (cuuint64_t)rows;
+        box[0] = BK; box[1] = (cuuint32_t)box_rows;
+    } else {
+        dims[0] = (cuuint64_t)rows; dims[1] = (cuuint64_t)K;
+        box[0] = 32; box[1] = BK;
+    }
+    strides[0] = (cuuint64_t)ld * 4;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || (strides[0] & 15))
+        throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+inline int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+// hi = tf32(x) (round to nearest), lo = tf32(x - hi); padding columns copied as 0
+__global__ void split_tf32_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                  float* __restrict__ hi, float* __restrict__ lo) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * cols) return;
+    const int64_t off = (i / cols) * ld + i % cols;
+    const float v = x[off];
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    const float hf = __uint_as_float(h);
+    uint32_t l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - hf));
+    hi[off] = hf;
+    lo[off] = __uint_as_float(l);
+}
+
+template <int BN, class Epi>
+void launch(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& alo,
+            const CUtensorMap& blo, const Epi& e) {
+    const int smem = TcSmem<BN>::bytes(sh.nsplit);
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     std::max(TcSmem<BN>::bytes(1), TcSmem<BN>::bytes(3))));
+        attr_set = true;
+    }
+    const int64_t tiles = ceil_div(sh.M, BM) * ceil_div(sh.N, BN);
+    const int grid = (int)std::min<int64_t>(tiles, num_sms());
+    tc_gemm_kernel<BN, Epi><<<grid, kThreads, smem, s>>>(a, b, alo, blo, sh, e);
+    CK_LAUNCH();
+}
+
+}  // namespace tc
+
+// TF32 tensor-core GEMM with the generic epilogue contract (Epi::block).
+template <class Epi>
+void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<float> A, Opnd<float> B,
+               const Epi& e) {
+    if (M <= 0 || N <= 0) return;
+    tc::TcShape sh{M, N, K, A.kmajor ? 0 : 1, B.kmajor ? 0 : 1, prec == k3xTF32 ? 3 : 1};
+    const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
+    DevMem alo, blo, ahi, bhi;
+    const float* pa = A.p;
+    const float* pb = B.p;
+    const float* pal = A.p;
+    const float* pbl = B.p;
+    if (sh.nsplit == 3) {
+        // split both operands into hi/lo TF32 parts (same layout and pitch)
+        auto split = [&](const Opnd<float>& o, int64_t rows, DevMem& hi, DevMem& lo) {
+            const int64_t r = o.kmajor ? rows : K, c = o.kmajor ? K : rows;
+            hi = DevMem((size_t)r * o.ld * 4, s);
+            lo = DevMem((size_t)r * o.ld * 4, s);
+            tc::split_tf32_kernel<<<(unsigned)ceil_div(r * c, 256), 256, 0, s>>>(o.p, r, c, o.ld, dptr<float>(hi),
+                                                                                 dptr<float>(lo));
+            CK_LAUNCH();
+        };
+        split(A, M, ahi, alo);
+        pa = dptr<float>(ahi);
+        pal = dptr<float>(alo);
+        if (B.p == A.p && B.ld == A.ld && B.kmajor == A.kmajor) {
+            pb = pa;
+            pbl = pal;
+        } else {
+            split(B, N, bhi, blo);
+            pb = dptr<float>(bhi);
+            pbl = dptr<float>(blo);
+        }
+    }
+    const int box_b = bn;
+    CUtensorMap ma = tc::make_map(pa, M, K, A.ld, sh.a_mn, tc::BM);
+    CUtensorMap mb = tc::make_map(pb, N, K, B.ld, sh.b_mn, box_b);
+    CUtensorMap mal = tc::make_map(pal, M, K, A.ld, sh.a_mn, tc::BM);
+    CUtensorMap mbl = tc::make_map(pbl, N, K, B.ld, sh.b_mn, box_b);
+    if (bn == 256) tc::launch<256>(s, sh, ma, mb, mal, mbl, e);
+    else if (bn == 128) tc::launch<128>(s, sh, ma, mb, mal, mbl, e);
+    else tc::launch<64>(s, sh, ma, mb, mal, mbl, e);
+}
+
+// Route TF32 precisions of the large curvature GEMMs to the tensor cores.
+template <class Epi>
+struct CurvGemm<float, Epi> {
+    static void run(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<float> A, Opnd<float> B,
+                    const Epi& e) {
+        if (prec == kTF32 || prec == k3xTF32) gemm_tf32(prec, s, M, N, K, A, B, e);
+        else gemm_simt<float>(s, M, N, K, 1, A, B, e);
+    }
+};
+
+}  // namespace ck

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "prof.cuh"
 
 namespace ck {
 
@@ -170,6 +171,9 @@ void forward_backward(const ModelDesc& md, const T* params, const int32_t* label
                       cudaStream_t s) {
     const int S = md.S;
     const int64_t n = c.n;
+    double fl = 0.0;
+    for (int k = 0; k < S; ++k) fl += 4.0 * n * md.w[k] * md.w[k + 1];
+    ProfScope ps("fwd_bwd", s, fl, 0.0);
     for (int k = 0; k < S; ++k) {
         const T* W = params + md.woff[k];
         const T* b = params + md.boff[k];
@@ -253,6 +257,7 @@ __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T
 template <class T>
 void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows, T* J, int64_t ldj,
               cudaStream_t s) {
+    ProfScope ps("jacobian", s, 0.0, (double)sizeof(T) * rows * md.P);
     LayerTable t = make_table(md, c.lda, c.ldt);
     CachePtrs<T> cp;
     for (int k = 0; k < md.S; ++k) { cp.a[k] = c.a[k]; cp.delta[k] = c.delta[k]; }
@@ -447,6 +452,26 @@ struct EpiHess {
         } else {
             H[gr * ldh + gc] = v;
             if (mirror) H[gc * ldh + gr] = v;
+        }
+    }
+    // tensor-core epilogue (32 x 32 block, coalesced in both store directions)
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
+        const bool tri = diag && mirror;
+        {  // direct: H[gr][gc], lanes along columns
+            const int64_t c = col0 + lane;
+            for (int rr = 0; rr < 32 && row0 + rr < M; ++rr) {
+                const int64_t r = row0 + rr, opp = r / J, gr = woffk + j0 + (r - opp * J);
+                const int64_t gc = gcol(opp, c);
+                if (c < N && (!tri || gc <= gr)) H[gr * ldh + gc] = alpha * (T)v[rr][lane];
+            }
+        }
+        if (mirror) {  // transposed: H[gc][gr], lanes along rows
+            const int64_t r = row0 + lane;
+            const int64_t opp = r / J, gr = woffk + j0 + (r - opp * J);
+            for (int cc = 0; cc < 32 && col0 + cc < N; ++cc) {
+                const int64_t gc = gcol(opp, col0 + cc);
+                if (r < M && (!tri || gc < gr)) H[gc * ldh + gr] = alpha * (T)v[lane][cc];
+            }
         }
     }
 };

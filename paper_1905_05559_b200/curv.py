@@ -391,3 +391,22 @@ def dev_opg_topk(spec, params, x, labels, n, k, oversample, power_iters, seed, q
 
 def launch_count() -> int:
     return int(_lib.load().curvkit_launch_count())
+
+
+def profile_begin():
+    """Start CUDA-event timing of the library's hot kernels."""
+    _lib.check(_lib.load().curvkit_profile_begin())
+
+
+def profile_end() -> dict:
+    """Stop timing; {region: {ms, launches, flops, bytes}} summed over the window."""
+    import json
+    buf = C.create_string_buffer(1 << 16)
+    _lib.check(_lib.load().curvkit_profile_end(buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def dev_gemm(m, n, k, a, lda, a_kmajor, b, ldb, b_kmajor, c, ldc, alpha=1.0, precision="tf32", stream=None):
+    """The curvature GEMM engine on device fp32 buffers (C = alpha A B^T)."""
+    _lib.check(_lib.load().curvkit_dev_gemm(m, n, k, _ptr(a), lda, int(a_kmajor), _ptr(b), ldb, int(b_kmajor),
+                                             _ptr(c), ldc, float(alpha), _prec(precision), _stream(stream)))
