@@ -82,13 +82,13 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // SWIZZLE_128B shared-memory matrix descriptor (sm_100 layout: version 1).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // version
-    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    d |= (uint64_t)1 << 46;       // version
+    d |= (uint64_t)layout << 61;  // 2: SWIZZLE_128B, 1: SWIZZLE_128B_BASE32B
     return d;
 }
 
@@ -138,6 +138,8 @@ struct TcShape {
     int64_t M, N, K;
     int a_mn, b_mn;  // operand is MN-major
     int nsplit;      // 1: tf32, 3: 3xTF32 (hi*hi + hi*lo + lo*hi)
+    uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides (bytes)
+    uint32_t mn_layout;                 // MN-major descriptor layout type
 };
 
 template <int BN>
@@ -261,16 +263,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 #pragma unroll
                     for (int ks = 0; ks < BK / 8; ++ks) {
                         // K-major: +32 B inside the 128 B swizzle row; MN-major: next 8-row group
-                        const uint32_t aoff = sh.a_mn ? ks * 1024 : ks * 32;
-                        const uint32_t boff = sh.b_mn ? ks * 1024 : ks * 32;
-                        const uint32_t albo = sh.a_mn ? 4096 : 16, blbo = sh.b_mn ? 4096 : 16;
-                        const uint64_t ahi = smem_desc(sa + aoff, albo, 1024);
-                        const uint64_t bhi = smem_desc(sb + boff, blbo, 1024);
+                        const uint32_t aoff = sh.a_mn ? ks * sh.mn_kstep : ks * 32;
+                        const uint32_t boff = sh.b_mn ? ks * sh.mn_kstep : ks * 32;
+                        const uint32_t albo = sh.a_mn ? sh.mn_lbo : 16, blbo = sh.b_mn ? sh.mn_lbo : 16;
+                        const uint32_t asbo = sh.a_mn ? sh.mn_sbo : 1024, bsbo = sh.b_mn ? sh.mn_sbo : 1024;
+                        const uint32_t alay = sh.a_mn ? sh.mn_layout : 2, blay = sh.b_mn ? sh.mn_layout : 2;
+                        const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
+                        const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
                         const uint32_t accf = (kb > 0 || ks > 0) ? 1u : 0u;
                         mma_tf32(d, ahi, bhi, idesc, accf);
                         if (split == 2) {
-                            const uint64_t alo = smem_desc(sa + A_BYTES + aoff, albo, 1024);
-                            const uint64_t blo = smem_desc(sb + B_BYTES + boff, blbo, 1024);
+                            const uint64_t alo = smem_desc(sa + A_BYTES + aoff, albo, asbo, alay);
+                            const uint64_t blo = smem_desc(sb + B_BYTES + boff, blbo, bsbo, blay);
                             mma_tf32(d, ahi, blo, idesc, 1u);
                             mma_tf32(d, alo, bhi, idesc, 1u);
                         }
@@ -350,8 +354,9 @@ inline CUtensorMap make_map(const float* p, int64_t rows, int64_t K, int64_t ld,
     strides[0] = (cuuint64_t)ld * 4;
     if ((reinterpret_cast<uintptr_t>(p) & 15) || (strides[0] & 15))
         throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
+    const CUtensorMapSwizzle swz = mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return m;
@@ -406,7 +411,12 @@ template <class Epi>
 void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<float> A, Opnd<float> B,
                const Epi& e) {
     if (M <= 0 || N <= 0) return;
-    tc::TcShape sh{M, N, K, A.kmajor ? 0 : 1, B.kmajor ? 0 : 1, prec == k3xTF32 ? 3 : 1};
+    // MN-major 32-bit operands use the 128B swizzle with 32B atoms
+    // (SWIZZLE_128B_BASE32B, TMA SWIZZLE_128B_ATOM_32B): LBO = stride between
+    // 32-element MN slices (BK rows x 128 B), SBO = stride between 4-row K
+    // groups, one K=8 MMA step = 8 rows.  Plain SWIZZLE_128B reads zeros here.
+    tc::TcShape sh{M, N, K, A.kmajor ? 0 : 1, B.kmajor ? 0 : 1, prec == k3xTF32 ? 3 : 1,
+                   (uint32_t)tc::BK * 128u, 512u, 1024u, 1u};
     const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
     DevMem alo, blo, ahi, bhi;
     const float* pa = A.p;
