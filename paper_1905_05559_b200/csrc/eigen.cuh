@@ -281,7 +281,9 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         ew.orth(dptr<T>(Y), P, l, ldl);
         X = dptr<T>(Y);
     }
-    // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q)
+    // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q).  The subspace only needs TF32,
+    // the Ritz values do not: this one pass runs as 3xTF32 in TF32 mode.
+    ew.prec = prec == kTF32 ? k3xTF32 : prec;
     ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
     DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
     CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));
