@@ -109,19 +109,32 @@ void check_memory_cap(int64_t p, int64_t cap, const char* who) {  // curvature.c
                  std::to_string(cap) + "; use the matrix-free eigensolvers instead");
 }
 
+// Keep the stream-ordered pool's memory mapped between calls: the curvature
+// workspaces (R chunks, profiles, J) are ~1 GB and would otherwise be
+// returned to the driver at every synchronisation and re-mapped next call.
+void keep_pool_memory() {
+    static bool done[64] = {};
+    int dev = 0;
+    CK_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (dev < 64) done[dev] = true;
+}
+
 cudaStream_t lib_stream() {
     static thread_local cudaStream_t s = nullptr;
-    if (!s) {
-        CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        int dev = 0;
-        CK_CUDA(cudaGetDevice(&dev));
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
+    keep_pool_memory();
+    if (!s) CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     return s;
+}
+
+cudaStream_t dev_stream(void* stream) {
+    keep_pool_memory();
+    return static_cast<cudaStream_t>(stream);
 }
 
 bool is_f64(int prec) {
@@ -250,7 +263,7 @@ void host_hessian(const ModelDesc& md, const double* params, const double* x, co
 
 template <class T>
 void jacobian_full(const ModelDesc& md, const Cache<T>& c, DevMem& J, int64_t& ldj, cudaStream_t s) {
-    ldj = round_up(md.P, 4);
+    ldj = round_up(md.P, 32);
     J = DevMem((size_t)c.n * ldj * sizeof(T), s);
     jacobian<T>(md, c, 0, c.n, dptr<T>(J), ldj, s);
 }
@@ -481,7 +494,7 @@ int curvkit_dev_assemble_hessian(const curvkit_model* model, const void* params,
     return guard([&] {
         ModelDesc md = make_desc(model);
         if (n < 1) contract("assemble_hessian: empty dataset");
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cudaStream_t s = dev_stream(stream);
         if (is_f64(precision)) {
             Cache<double> c;
             forward_device<double>(md, (const double*)params, (const double*)x, labels, n, c, s);
@@ -499,7 +512,7 @@ int curvkit_dev_assemble_opg(const curvkit_model* model, const void* params, con
     return guard([&] {
         ModelDesc md = make_desc(model);
         if (n < 1) contract("assemble_opg: empty dataset");
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cudaStream_t s = dev_stream(stream);
         auto run = [&](auto tag) {
             using T = decltype(tag);
             Cache<T> c;
@@ -521,7 +534,7 @@ int curvkit_dev_assemble_jacobian(const curvkit_model* model, const void* params
     return guard([&] {
         ModelDesc md = make_desc(model);
         if (n < 1) contract("assemble_jacobian: empty batch");
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cudaStream_t s = dev_stream(stream);
         auto run = [&](auto tag) {
             using T = decltype(tag);
             Cache<T> c;
@@ -539,7 +552,7 @@ int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t ld
     return guard([&] {
         if (m < 0 || n < 0 || k < 1) shape("dev_gemm: bad shape");
         if (precision == kF64) contract("dev_gemm: fp32 storage only");
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cudaStream_t s = dev_stream(stream);
         EpiStore<float> e{c, ldc, 0, alpha, 0.f};
         Opnd<float> A = a_kmajor ? kmaj(a, lda) : mnmaj(a, lda);
         Opnd<float> B = b_kmajor ? kmaj(b, ldb) : mnmaj(b, ldb);
@@ -553,7 +566,7 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
     return guard([&] {
         ModelDesc md = make_desc(model);
         if (n < 1) contract("opg_topk: empty dataset");
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cudaStream_t s = dev_stream(stream);
         auto run = [&](auto tag) {
             using T = decltype(tag);
             Cache<T> c;

@@ -151,7 +151,7 @@ struct Engine {
     //   G  [T_{k+1}][n][ldt_k]       rdelta_k for rz_k = e_o
     //   Pm [T_{k+1}][n][ldt_m]       rdelta_m, m < k, same tangents
     //   Qm [T_k][n][ldt_m]           rdelta_m from the explicit delta*RW term
-    size_t chunk_bytes = size_t(48) << 20;  // R operand chunk, sized to stay in L2
+    size_t chunk_bytes = size_t(256) << 20;  // R operand chunk (streamed once from HBM)
 
     // Output entries of one (k, m, chunk) block that the assembly needs: all
     // of an off-diagonal block, the lower triangle (gc <= gr) of a diagonal one.
@@ -180,6 +180,7 @@ struct Engine {
                 CK_CUDA(cudaMemsetAsync(keep.back().p, 0, (size_t)rows * ld * sizeof(T), s));
                 return dptr<T>(keep.back());
             };
+            ProfScope prof_stage("hess_profiles", s, 0.0, 0.0);
             T* G = buf(np * n, c.ldt[k]);
             T* rzp[kMaxLayers] = {};
             if (k == S - 1) {
@@ -241,30 +242,57 @@ struct Engine {
                                  mnmaj(params + md.woff[m + 1], md.w[m + 1]), e);
                 }
             }
+            prof_stage.end();
+            ProfScope prep_stage("hess_prep", s, 0.0, 0.0);
+            // n-contiguous copies for the R generator (all reads 16-byte vectors)
+            const int64_t ldn = round_up(n, 4);
+            const int64_t tk = md.w[k];
+            T* akT = buf(tk + 1, ldn);
+            transpose<T>(s, c.a[k], c.lda[k], 0, akT, ldn, 0, n, tk + 1, 1);
+            T* dkT = buf(np, ldn);
+            transpose<T>(s, c.delta[k], c.ldt[k], 0, dkT, ldn, 0, n, np, 1);
+            T* GT = buf(np * np, ldn);
+            transpose<T>(s, G, c.ldt[k], n * c.ldt[k], GT, ldn, np * ldn, n, np, np);
+            T* PT[kMaxLayers] = {};
+            T* QT[kMaxLayers] = {};
+            for (int m = k - 1; m >= 0; --m) {
+                const int64_t tm1 = md.w[m + 1];
+                PT[m] = buf(np * tm1, ldn);
+                transpose<T>(s, Pm[m], c.ldt[m], n * c.ldt[m], PT[m], ldn, tm1 * ldn, n, tm1, np);
+                QT[m] = buf(tk * tm1, ldn);
+                transpose<T>(s, Qm[m], c.ldt[m], n * c.ldt[m], QT[m], ldn, tm1 * ldn, n, tm1, tk);
+            }
+            prep_stage.end();
             // blocks (k, m), m <= k
             const int64_t Pk = md.block_size(k);
-            const int64_t ldr = round_up(n, 4);
+            const int64_t ldr = ldn;
             for (int m = k; m >= 0; --m) {
-                const int64_t tm1 = md.w[m + 1];
+                const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                 int64_t J = (int64_t)(chunk_bytes / ((size_t)tm1 * ldr * sizeof(T)));
-                J = std::max<int64_t>(64, J / 64 * 64);
-                J = std::min<int64_t>(J, round_up(Pk, 64));
+                J = std::max<int64_t>(128, J / 128 * 128);
+                J = std::min<int64_t>(J, round_up(Pk, 128));
                 DevMem rbuf((size_t)tm1 * J * ldr * sizeof(T), s);
                 for (int64_t j0 = 0; j0 < Pk; j0 += J) {
                     const int64_t Jc = std::min<int64_t>(J, Pk - j0);
-                    RGenArgs<T> g{m == k ? G : Pm[m], m == k ? nullptr : Qm[m], m == k ? c.ldt[k] : c.ldt[m],
-                                  c.a[k], c.lda[k], c.delta[k], c.ldt[k], n, md.w[k], md.w[k + 1], tm1, j0, Jc,
-                                  dptr<T>(rbuf), ldr};
+                    // R rows (o'', jj) whose block entries are all above the
+                    // diagonal are neither generated nor multiplied
+                    int64_t opp_hi = tm1;
+                    if (m == k && !verify && j0 + Jc - 1 < tm * tm1) opp_hi = std::min(tm1, (j0 + Jc - 1) / tm + 1);
+                    const int64_t rows = opp_hi * Jc;
+                    RGenArgs<T> g{m == k ? GT : PT[m], m == k ? nullptr : QT[m], akT, dkT, ldn, n, tk, np, tm1,
+                                  j0, Jc, rows, dptr<T>(rbuf), ldr};
                     {
-                        ProfScope ps("hess_rgen", s, 0.0, (double)sizeof(T) * tm1 * Jc * ldr);
-                        rgen_kernel<T><<<blocks_for(tm1 * Jc * ceil_div(n, 4)), 256, 0, s>>>(g);
+                        ProfScope ps("hess_rgen", s, 0.0, (double)sizeof(T) * rows * ldr);
+                        const int64_t work = rows * (ldr / 4);
+                        rgen_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 16), 256, 0, s>>>(g);
                         CK_LAUNCH();
                     }
-                    EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], md.w[m], T(1) / T(n),
+                    EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
                                  m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
-                    ProfScope ps("hess_gemm", s, 2.0 * (double)n * hess_required_entries(k, m, j0, Jc),
-                                 (double)sizeof(T) * ((double)tm1 * Jc * ldr + hess_required_entries(k, m, j0, Jc)));
-                    CurvGemm<T, EpiHess<T>>::run(prec, s, tm1 * Jc, md.w[m] + 1, n, kmaj(dptr<T>(rbuf), ldr),
+                    // algorithmic work is counted only while profiling (host loop)
+                    const double req = Profiler::get().on ? hess_required_entries(k, m, j0, Jc) : 0.0;
+                    ProfScope ps("hess_gemm", s, 2.0 * (double)n * req, (double)sizeof(T) * ((double)rows * ldr + req));
+                    CurvGemm<T, EpiHess<T>>::run(prec, s, rows, tm + 1, n, kmaj(dptr<T>(rbuf), ldr),
                                                  mnmaj(c.a[m], c.lda[m]), e);
                 }
             }

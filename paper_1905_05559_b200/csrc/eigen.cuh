@@ -263,9 +263,9 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         throw CurvError(kContractError, "opg_topk: need 1 <= k <= min(N, P), got k = " + std::to_string(k));
     if (oversample < 0 || power_iters < 0) throw CurvError(kContractError, "opg_topk: negative oversample/power_iters");
     const int64_t l = std::min(k + oversample, P);
-    const int64_t ldl = round_up(l, 4);
+    const int64_t ldl = round_up(l, 32);
     // per-example gradients stay resident in HBM
-    const int64_t ldj = round_up(P, 4);
+    const int64_t ldj = round_up(P, 32);
     DevMem J((size_t)n * ldj * sizeof(T), s);
     jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s);
     DevMem Y((size_t)P * ldl * sizeof(T), s), Om((size_t)P * ldl * sizeof(T), s);

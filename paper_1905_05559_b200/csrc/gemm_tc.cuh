@@ -74,6 +74,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1, int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -140,6 +149,7 @@ struct TcShape {
     int nsplit;      // 1: tf32, 3: 3xTF32 (hi*hi + hi*lo + lo*hi)
     uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides (bytes)
     uint32_t mn_layout;                 // MN-major descriptor layout type
+    int a_3d, b_3d;                     // MN-major operand loaded by one 3D TMA box
 };
 
 template <int BN>
@@ -159,14 +169,17 @@ struct TcSmem {
 };
 
 // Load one operand tile (rows x BK) of a K-major or MN-major operand.
+// MN-major tiles are [32-row atom][BK k-rows][32 elements]; a 3D map
+// (elem-in-atom, k, atom) fetches all atoms of the tile in one box.
 template <int ROWS>
-__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int mn, int64_t r0,
-                                          int64_t k0) {
+__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int mn, int mn3d,
+                                          int64_t r0, int64_t k0, int atoms) {
     if (!mn) {
         tma_load_2d(dst, map, bar, (int32_t)k0, (int32_t)r0);
+    } else if (mn3d) {
+        tma_load_3d(dst, map, bar, 0, (int32_t)k0, (int32_t)(r0 / 32));
     } else {
-#pragma unroll
-        for (int i = 0; i < ROWS / 32; ++i) tma_load_2d(dst + i * 4096, map, bar, (int32_t)(r0 + 32 * i), (int32_t)k0);
+        for (int i = 0; i < atoms; ++i) tma_load_2d(dst + i * 4096, map, bar, (int32_t)(r0 + 32 * i), (int32_t)k0);
     }
 }
 
@@ -222,21 +235,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         if (lane == 0) {  // ---------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t bytes = (uint32_t)STAGE_BYTES;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const int64_t m0 = (t / nt) * BM, n0 = (t % nt) * BN;
                 if (epi.skip(0, m0, n0, BM, BN)) continue;
+                // MN-major B of a ragged last tile: only the atoms that hold columns
+                const int batoms = (sh.b_mn && !sh.b_3d) ? (int)::min((int64_t)(BN / 32), ceil_div(sh.N - n0, 32))
+                                                         : BN / 32;
+                const uint32_t bytes = (uint32_t)((A_BYTES + batoms * 4096 * (sh.b_mn && !sh.b_3d ? 1 : 0) +
+                                                   (sh.b_mn && !sh.b_3d ? 0 : B_BYTES)) * split);
                 for (int64_t kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], bytes);
                     uint8_t* sa = stage_base + stage * STAGE_BYTES;
                     uint8_t* sb = sa + A_BYTES * split;
                     const int64_t k0 = kb * BK;
-                    load_tile<BM>(sa, &mapA, &full[stage], sh.a_mn, m0, k0);
-                    load_tile<BN>(sb, &mapB, &full[stage], sh.b_mn, n0, k0);
+                    load_tile<BM>(sa, &mapA, &full[stage], sh.a_mn, sh.a_3d, m0, k0, BM / 32);
+                    load_tile<BN>(sb, &mapB, &full[stage], sh.b_mn, sh.b_3d, n0, k0, batoms);
                     if (split == 2) {
-                        load_tile<BM>(sa + A_BYTES, &mapAlo, &full[stage], sh.a_mn, m0, k0);
-                        load_tile<BN>(sb + B_BYTES, &mapBlo, &full[stage], sh.b_mn, n0, k0);
+                        load_tile<BM>(sa + A_BYTES, &mapAlo, &full[stage], sh.a_mn, sh.a_3d, m0, k0, BM / 32);
+                        load_tile<BN>(sb + B_BYTES, &mapBlo, &full[stage], sh.b_mn, sh.b_3d, n0, k0, batoms);
                     }
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
@@ -244,7 +261,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t idesc = idesc_tf32(BN, sh.a_mn, sh.b_mn);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -254,6 +270,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 if (epi.skip(0, m0, n0, BM, BN)) continue;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
+                // ragged last N tile: the MMA only spans the live columns
+                const int ntile = (int)::min((int64_t)BN, (sh.N - n0 + 15) / 16 * 16);
+                const uint32_t idesc = idesc_tf32(ntile, sh.a_mn, sh.b_mn);
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
                 for (int64_t kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
@@ -323,6 +342,283 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     }
 }
 
+// ---------------------------------------------------------------- CTA pair
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x BN tile.
+// Each CTA stages its own 128 rows of A and BN/2 rows of B; the leader
+// (rank 0) issues M=256 MMAs that read both CTAs' shared memory, so every
+// SM moves 2/3 of the operand bytes of the single-CTA 128 x BN tile for the
+// same MMA work.  Completion is multicast to both CTAs' barriers.
+namespace pair {
+
+constexpr int EPI_WARPS = 8;
+constexpr int kThreads2 = 128 + 32 * EPI_WARPS;  // warps 0-3 control, 4-11 epilogue
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t map_to_leader(uint32_t local_smem) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local_smem));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Remote arrive on a barrier in the pair (default .release.cta semantics, as
+// CUTLASS's ClusterBarrier).  Waits stay CTA-scoped: a cluster-scope acquire
+// in a polling loop makes ptxas emit an L1 invalidate (CCTL.IVALL) per poll.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_cluster(uint64_t* bar, uint32_t bytes) { mbar_expect_tx(bar, bytes); }
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
+
+// TMA into this CTA's smem, completion counted on the leader's barrier
+__device__ __forceinline__ void tma2_2d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
+                                        int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma2_3d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
+                                        int32_t c1, int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+        "%5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+template <int ROWS>
+__device__ __forceinline__ void load_tile2(uint8_t* dst, const CUtensorMap* map, uint32_t bar, int mn, int mn3d,
+                                           int64_t r0, int64_t k0) {
+    if (!mn) {
+        tma2_2d(dst, map, bar, (int32_t)k0, (int32_t)r0);
+    } else if (mn3d) {
+        tma2_3d(dst, map, bar, 0, (int32_t)k0, (int32_t)(r0 / 32));
+    } else {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) tma2_2d(dst + i * 4096, map, bar, (int32_t)(r0 + 32 * i), (int32_t)k0);
+    }
+}
+
+__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    const uint32_t z = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(z)
+        : "memory");
+}
+
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+
+__host__ __device__ constexpr uint32_t idesc2_tf32(int n, bool a_mn, bool b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <int BN>
+struct PairSmem {
+    static constexpr int A_BYTES = 128 * BK * 4;       // own 128 rows
+    static constexpr int B_BYTES = (BN / 2) * BK * 4;  // own half of B
+    static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;
+    static constexpr int MAX_SMEM = 227 * 1024;
+    __host__ __device__ static constexpr int stage_bytes(int nsplit) { return (A_BYTES + B_BYTES) * (nsplit == 1 ? 1 : 2); }
+    __host__ __device__ static constexpr int stages(int nsplit) {
+        const int st = (MAX_SMEM - 1024 - EPI_BYTES - 512) / stage_bytes(nsplit);
+        return st > 8 ? 8 : st;
+    }
+    __host__ __device__ static constexpr int bytes(int nsplit) {
+        return 1024 + stages(nsplit) * stage_bytes(nsplit) + EPI_BYTES + 512;
+    }
+};
+
+template <int BN, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcShape sh,
+                    Epi epi) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using S = PairSmem<BN>;
+    const int split = sh.nsplit == 1 ? 1 : 2;
+    const int STAGE_BYTES = S::stage_bytes(sh.nsplit);
+    const int NST = S::stages(sh.nsplit);
+    uint8_t* stage_base = smem;
+    float* epi_buf = reinterpret_cast<float*>(smem + NST * STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES + S::EPI_BYTES);
+    uint64_t* full = bars;            // [8]  (leader's copy is the live one)
+    uint64_t* empty = bars + 8;       // [8]  (both CTAs, multicast commit)
+    uint64_t* tfull = bars + 16;      // [2]  (both CTAs, multicast commit)
+    uint64_t* tempty = bars + 18;     // [2]  (leader's copy; remote arrivals)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 20);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cta_rank();
+    const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
+    const int64_t mt = ceil_div(sh.M, 256), nt = ceil_div(sh.N, BN);
+    const int64_t ntiles = mt * nt;
+    const int64_t nk = ceil_div(sh.K, BK);
+
+    if (warp == 0 && lane == 0) {
+        prefetch_map(&mapA);
+        prefetch_map(&mapB);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 2);  // leader arrive.expect_tx + peer arrive
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "n"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    auto tile_ntile = [&](int64_t n0) -> int {
+        // live columns of this tile, in steps of 64 so each CTA's half is a
+        // whole number of 32-row MN atoms
+        return (int)::min((int64_t)BN, (sh.N - n0 + 63) / 64 * 64);
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes_leader = (uint32_t)(2 * STAGE_BYTES);
+            for (int64_t t = pair_id; t < ntiles; t += npairs) {
+                const int64_t m0 = (t / nt) * 256, n0 = (t % nt) * BN;
+                if (epi.skip(0, m0, n0, 256, BN)) continue;
+                const int64_t half = tile_ntile(n0) / 2;
+                const int64_t am0 = m0 + 128 * rank, bn0 = n0 + half * rank;
+                for (int64_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
+                    if (rank == 0) mbar_expect_tx_cluster(&full[stage], bytes_leader);
+                    else mbar_arrive_cluster(fb);
+                    uint8_t* sa = stage_base + stage * STAGE_BYTES;
+                    uint8_t* sb = sa + S::A_BYTES * split;
+                    const int64_t k0 = kb * BK;
+                    load_tile2<128>(sa, &mapA, fb, sh.a_mn, sh.a_3d, am0, k0);
+                    load_tile2<BN / 2>(sb, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0);
+                    if (split == 2) {
+                        load_tile2<128>(sa + S::A_BYTES, &mapAlo, fb, sh.a_mn, sh.a_3d, am0, k0);
+                        load_tile2<BN / 2>(sb + S::B_BYTES, &mapBlo, fb, sh.b_mn, sh.b_3d, bn0, k0);
+                    }
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = pair_id; t < ntiles; t += npairs) {
+                const int64_t m0 = (t / nt) * 256, n0 = (t % nt) * BN;
+                if (epi.skip(0, m0, n0, 256, BN)) continue;
+                mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t idesc = idesc2_tf32(tile_ntile(n0), sh.a_mn, sh.b_mn);
+                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                for (int64_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait_cluster(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
+                    const uint32_t sb = sa + S::A_BYTES * split;
+#pragma unroll
+                    for (int ks = 0; ks < BK / 8; ++ks) {
+                        const uint32_t aoff = sh.a_mn ? ks * sh.mn_kstep : ks * 32;
+                        const uint32_t boff = sh.b_mn ? ks * sh.mn_kstep : ks * 32;
+                        const uint32_t albo = sh.a_mn ? sh.mn_lbo : 16, blbo = sh.b_mn ? sh.mn_lbo : 16;
+                        const uint32_t asbo = sh.a_mn ? sh.mn_sbo : 1024, bsbo = sh.b_mn ? sh.mn_sbo : 1024;
+                        const uint32_t alay = sh.a_mn ? sh.mn_layout : 2, blay = sh.b_mn ? sh.mn_layout : 2;
+                        const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
+                        const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
+                        mma2_tf32(d, ahi, bhi, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        if (split == 2) {
+                            mma2_tf32(d, ahi, smem_desc(sb + S::B_BYTES + boff, blbo, bsbo, blay), idesc, 1u);
+                            mma2_tf32(d, smem_desc(sa + S::A_BYTES + aoff, albo, asbo, alay), bhi, idesc, 1u);
+                        }
+                    }
+                    commit2(&empty[stage]);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+                commit2(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, 8 warps)
+        const int ew = warp - 4;
+        const int quad = warp % 4;   // TMEM lanes 32*quad .. +31
+        const int chalf = ew / 4;    // column half of the tile
+        float(*buf)[33] = reinterpret_cast<float(*)[33]>(epi_buf + ew * 32 * 33);
+        const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = pair_id; t < ntiles; t += npairs) {
+            const int64_t m0 = (t / nt) * 256, n0 = (t % nt) * BN;
+            if (epi.skip(0, m0, n0, 256, BN)) continue;
+            mbar_wait_cluster(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row0 = m0 + 128 * rank + quad * 32;
+            for (int cb = chalf * (BN / 64); cb < (chalf + 1) * (BN / 64); ++cb) {
+                const int64_t col0 = n0 + cb * 32;
+                if (col0 >= sh.N) break;
+                float v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                if (row0 < sh.M) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) buf[lane][i] = v[i];
+                    __syncwarp();
+                    epi.block(row0, col0, sh.M, sh.N, buf, lane);
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN));
+    }
+}
+
+}  // namespace pair
+
 // ---------------------------------------------------------------- host side
 inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -340,8 +636,22 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D fp32 tensor map over an operand of `rows` x K (K-major: p[r*ld + k];
 // MN-major: p[k*ld + r]), box = one BK x box_rows tile (or 32 x 32 pieces).
-inline CUtensorMap make_map(const float* p, int64_t rows, int64_t K, int64_t ld, int mn, int box_rows) {
+inline CUtensorMap make_map(const float* p, int64_t rows, int64_t K, int64_t ld, int mn, int box_rows,
+                           bool mn3d = false) {
     CUtensorMap m;
+    if (mn && mn3d) {
+        // (element in 32-wide atom, k, atom): atom stride 128 B
+        cuuint64_t dims3[3] = {32, (cuuint64_t)K, (cuuint64_t)ceil_div(rows, 32)};
+        cuuint64_t str3[2] = {(cuuint64_t)ld * 4, 128};
+        cuuint32_t box3[3] = {32, BK, (cuuint32_t)(box_rows / 32)}, es3[3] = {1, 1, 1};
+        if ((reinterpret_cast<uintptr_t>(p) & 15) || (str3[0] & 15))
+            throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
+        CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims3, str3, box3, es3,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (3D) failed: " + std::to_string((int)r));
+        return m;
+    }
     cuuint64_t dims[2], strides[1];
     cuuint32_t box[2], es[2] = {1, 1};
     if (!mn) {
@@ -404,6 +714,23 @@ void launch(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const CUten
     CK_LAUNCH();
 }
 
+template <int BN, class Epi>
+void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const CUtensorMap& b,
+                 const CUtensorMap& alo, const CUtensorMap& blo, const Epi& e) {
+    using S = pair::PairSmem<BN>;
+    const int smem = S::bytes(sh.nsplit);
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK_CUDA(cudaFuncSetAttribute(pair::tc_gemm_pair_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     std::max(S::bytes(1), S::bytes(3))));
+        attr_set = true;
+    }
+    const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN);
+    const int grid = 2 * (int)std::min<int64_t>(tiles, num_sms() / 2);
+    pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, sh, e);
+    CK_LAUNCH();
+}
+
 }  // namespace tc
 
 // TF32 tensor-core GEMM with the generic epilogue contract (Epi::block).
@@ -415,8 +742,12 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     // (SWIZZLE_128B_BASE32B, TMA SWIZZLE_128B_ATOM_32B): LBO = stride between
     // 32-element MN slices (BK rows x 128 B), SBO = stride between 4-row K
     // groups, one K=8 MMA step = 8 rows.  Plain SWIZZLE_128B reads zeros here.
+    // a 3D box may read up to the next multiple of 32 rows: only when the
+    // pitch covers it (reads past `rows` land in masked output rows/columns)
+    const int a3 = (!A.kmajor && A.ld >= round_up(M, 32)) ? 1 : 0;
+    const int b3 = (!B.kmajor && B.ld >= round_up(N, 32)) ? 1 : 0;
     tc::TcShape sh{M, N, K, A.kmajor ? 0 : 1, B.kmajor ? 0 : 1, prec == k3xTF32 ? 3 : 1,
-                   (uint32_t)tc::BK * 128u, 512u, 1024u, 1u};
+                   (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, a3, b3};
     const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
     DevMem alo, blo, ahi, bhi;
     const float* pa = A.p;
@@ -445,11 +776,20 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
             pbl = dptr<float>(blo);
         }
     }
-    const int box_b = bn;
-    CUtensorMap ma = tc::make_map(pa, M, K, A.ld, sh.a_mn, tc::BM);
-    CUtensorMap mb = tc::make_map(pb, N, K, B.ld, sh.b_mn, box_b);
-    CUtensorMap mal = tc::make_map(pal, M, K, A.ld, sh.a_mn, tc::BM);
-    CUtensorMap mbl = tc::make_map(pbl, N, K, B.ld, sh.b_mn, box_b);
+    // CTA-pair (cta_group::2) tiles of 256 x bn when M gives every pair work;
+    // each CTA then stages only bn/2 rows of B.
+    static const bool no_pair = getenv("CURVKIT_NO_PAIR") != nullptr;
+    const bool use_pair = !no_pair && bn >= 128 && M >= 512;
+    const int box_b = use_pair ? bn / 2 : bn;
+    CUtensorMap ma = tc::make_map(pa, M, K, A.ld, sh.a_mn, tc::BM, a3);
+    CUtensorMap mb = tc::make_map(pb, N, K, B.ld, sh.b_mn, box_b, b3);
+    CUtensorMap mal = tc::make_map(pal, M, K, A.ld, sh.a_mn, tc::BM, a3);
+    CUtensorMap mbl = tc::make_map(pbl, N, K, B.ld, sh.b_mn, box_b, b3);
+    if (use_pair) {
+        if (bn == 256) tc::launch_pair<256>(s, sh, ma, mb, mal, mbl, e);
+        else tc::launch_pair<128>(s, sh, ma, mb, mal, mbl, e);
+        return;
+    }
     if (bn == 256) tc::launch<256>(s, sh, ma, mb, mal, mbl, e);
     else if (bn == 128) tc::launch<128>(s, sh, ma, mb, mal, mbl, e);
     else tc::launch<64>(s, sh, ma, mb, mal, mbl, e);

@@ -141,7 +141,7 @@ void alloc_cache(const ModelDesc& md, int64_t n, Cache<T>& c, cudaStream_t s) {
     c.n = n;
     size_t total = 0;
     for (int k = 0; k <= md.S; ++k) {
-        c.lda[k] = round_up(md.w[k] + 1, 4);
+        c.lda[k] = round_up(md.w[k] + 1, 32);
         total += (size_t)n * c.lda[k];
     }
     for (int k = 0; k < md.S; ++k) {
@@ -382,43 +382,72 @@ __global__ void profile_q_kernel(const T* __restrict__ z, int64_t ldz, int64_t t
 // ---------------------------------------------------------------------------
 template <class T>
 struct RGenArgs {
-    const T* prof;  // G (m == k) or Pm, [T_{k+1}][n][ldp]
-    const T* q;     // Qm or null, [T_k][n][ldp]
-    int64_t ldp;
-    const T* ak;
-    int64_t ldak;
-    const T* dk;  // delta_k
-    int64_t lddk;
+    const T* prof;  // G (m == k) or Pm, transposed: [T_{k+1}][T_{m+1}][ldn]
+    const T* q;     // Qm transposed [T_k][T_{m+1}][ldn], or null
+    const T* akT;   // a_k transposed [T_k + 1][ldn]
+    const T* dkT;   // delta_k transposed [T_{k+1}][ldn]
+    int64_t ldn;
     int64_t n, tink, toutk, tm1;  // T_k, T_{k+1}, T_{m+1}
-    int64_t j0, J;
+    int64_t j0, J, rows;          // rows = (o'' rows generated) * J
     T* R;
     int64_t ldr;
 };
 
+// One thread per 4 consecutive examples of one R row: every read and the
+// write are 16-byte vectors along n (all operands are n-contiguous).
 template <class T>
-__global__ void rgen_kernel(RGenArgs<T> g) {
-    const int64_t rows = g.tm1 * g.J;
-    const int64_t cols4 = ceil_div(g.n, 4);
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= rows * cols4) return;
-    const int64_t r = idx / cols4, n0 = (idx % cols4) * 4;
-    const int64_t opp = r / g.J, jj = r % g.J, j = g.j0 + jj;
-    const int64_t nw = g.toutk * g.tink;
-    const bool wt = j < nw;
-    const int64_t o = wt ? j / g.tink : j - nw;
-    const int64_t i = wt ? j - o * g.tink : 0;
-    T* out = g.R + r * g.ldr;
-    for (int u = 0; u < 4; ++u) {
-        const int64_t e = n0 + u;
-        if (e >= g.ldr) break;
-        T v = T(0);
-        if (e < g.n) {
-            const T s = wt ? g.ak[e * g.ldak + i] : T(1);
-            v = s * g.prof[(o * g.n + e) * g.ldp + opp];
-            if (g.q && wt) v += g.dk[e * g.lddk + o] * g.q[(i * g.n + e) * g.ldp + opp];
+__global__ void __launch_bounds__(256) rgen_kernel(RGenArgs<T> g) {
+    const int64_t n4 = g.ldr / 4;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < g.rows * n4;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / n4, e = (idx - r * n4) * 4;
+        const int64_t opp = r / g.J, jj = r - opp * g.J, j = g.j0 + jj;
+        const int64_t nw = g.toutk * g.tink;
+        const bool wt = j < nw;
+        const int64_t o = wt ? j / g.tink : j - nw;
+        const int64_t i = wt ? j - o * g.tink : 0;
+        using V = typename std::conditional<sizeof(T) == 4, float4, double4>::type;
+        V p = *reinterpret_cast<const V*>(g.prof + (o * g.tm1 + opp) * g.ldn + e);
+        if (wt) {
+            const V s = *reinterpret_cast<const V*>(g.akT + i * g.ldn + e);
+            p.x *= s.x; p.y *= s.y; p.z *= s.z; p.w *= s.w;
+            if (g.q) {
+                const V d = *reinterpret_cast<const V*>(g.dkT + o * g.ldn + e);
+                const V qv = *reinterpret_cast<const V*>(g.q + (i * g.tm1 + opp) * g.ldn + e);
+                p.x += d.x * qv.x; p.y += d.y * qv.y; p.z += d.z * qv.z; p.w += d.w * qv.w;
+            }
         }
-        out[e] = v;
+        *reinterpret_cast<V*>(g.R + r * g.ldr + e) = p;
     }
+}
+
+// out[b][c][r] = in[b][r][c]  (rows x cols per batch; 32x32 smem tiles)
+template <class T>
+__global__ void transpose_kernel(const T* __restrict__ in, int64_t ldi, int64_t bsi, T* __restrict__ out,
+                                 int64_t ldo, int64_t bso, int64_t rows, int64_t cols) {
+    __shared__ T tile[32][33];
+    const int64_t b = blockIdx.z;
+    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    const T* ip = in + b * bsi;
+    T* op = out + b * bso;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t r = r0 + y, c = c0 + threadIdx.x;
+        tile[y][threadIdx.x] = (r < rows && c < cols) ? ip[r * ldi + c] : T(0);
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t c = c0 + y, r = r0 + threadIdx.x;
+        if (c < cols && r < ldo) op[c * ldo + r] = r < rows ? tile[threadIdx.x][y] : T(0);
+    }
+}
+
+template <class T>
+void transpose(cudaStream_t s, const T* in, int64_t ldi, int64_t bsi, T* out, int64_t ldo, int64_t bso, int64_t rows,
+               int64_t cols, int64_t batch) {
+    // covers padding columns r in [rows, ldo) with zeros
+    dim3 grid((unsigned)ceil_div(ldo, 32), (unsigned)ceil_div(cols, 32), (unsigned)batch);
+    transpose_kernel<T><<<grid, dim3(32, 8), 0, s>>>(in, ldi, bsi, out, ldo, bso, rows, cols);
+    CK_LAUNCH();
 }
 
 // Hessian block epilogue: GEMM row r = (o'', jj), column c = input unit of
@@ -457,20 +486,31 @@ struct EpiHess {
     // tensor-core epilogue (32 x 32 block, coalesced in both store directions)
     __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
         const bool tri = diag && mirror;
+        // one division per block; rows advance (o'', jj) incrementally
+        const int64_t opp0 = row0 / J, jj0 = row0 - opp0 * J;
+        const int nrows = (int)::min((int64_t)32, M - row0);
         {  // direct: H[gr][gc], lanes along columns
             const int64_t c = col0 + lane;
-            for (int rr = 0; rr < 32 && row0 + rr < M; ++rr) {
-                const int64_t r = row0 + rr, opp = r / J, gr = woffk + j0 + (r - opp * J);
-                const int64_t gc = gcol(opp, c);
-                if (c < N && (!tri || gc <= gr)) H[gr * ldh + gc] = alpha * (T)v[rr][lane];
+            const bool live = c < N;
+            const bool wcol = c < tm;
+            int64_t opp = opp0, jj = jj0;
+            for (int rr = 0; rr < nrows; ++rr) {
+                const int64_t gr = woffk + j0 + jj;
+                const int64_t gc = wcol ? woffm + opp * tm + c : boffm + opp;
+                if (live && (!tri || gc <= gr)) H[gr * ldh + gc] = alpha * (T)v[rr][lane];
+                if (++jj == J) { jj = 0; ++opp; }
             }
         }
-        if (mirror) {  // transposed: H[gc][gr], lanes along rows
-            const int64_t r = row0 + lane;
-            const int64_t opp = r / J, gr = woffk + j0 + (r - opp * J);
-            for (int cc = 0; cc < 32 && col0 + cc < N; ++cc) {
-                const int64_t gc = gcol(opp, col0 + cc);
-                if (r < M && (!tri || gc < gr)) H[gc * ldh + gr] = alpha * (T)v[lane][cc];
+        if (mirror && lane < nrows) {  // transposed: H[gc][gr], lanes along rows
+            int64_t opp = opp0, jj = jj0 + lane;
+            while (jj >= J) { jj -= J; ++opp; }
+            const int64_t gr = woffk + j0 + jj;
+            const int ncols = (int)::min((int64_t)32, N - col0);
+            const int64_t wbase = woffm + opp * tm;
+            for (int cc = 0; cc < ncols; ++cc) {
+                const int64_t c = col0 + cc;
+                const int64_t gc = c < tm ? wbase + c : boffm + opp;
+                if (!tri || gc < gr) H[gc * ldh + gr] = alpha * (T)v[lane][cc];
             }
         }
     }

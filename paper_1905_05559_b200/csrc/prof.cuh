@@ -42,7 +42,8 @@ struct ProfScope {
         cudaEventCreate(&a);
         cudaEventRecord(a, s);
     }
-    ~ProfScope() {
+    ~ProfScope() { end(); }
+    void end() {
         if (!a) return;
         cudaEvent_t b;
         cudaEventCreate(&b);
@@ -50,6 +51,7 @@ struct ProfScope {
         Profiler& p = Profiler::get();
         std::lock_guard<std::mutex> g(p.mu);
         p.recs[name].push_back({a, b, flops, bytes});
+        a = nullptr;
     }
 };
 
