@@ -134,7 +134,7 @@ def reference_sample(wl, threads, budget_s=12.0):
     if kind == "port":
         raise RuntimeError("oracle/_ref missing; build it with `make -C oracle`")
     # Hessian columns spread over the parameter blocks, `threads` lanes
-    ncol = max(threads, 2 * threads)
+    ncol = threads
     c0 = 0
     t = time.perf_counter()
     lib.hessian_columns_sample(spec, params, x, y, c0, c0 + ncol, threads)
@@ -142,7 +142,7 @@ def reference_sample(wl, threads, budget_s=12.0):
     t = time.perf_counter()
     lib.jacobian(spec, params, x, y)
     tj = time.perf_counter() - t
-    nrow = 16 * threads
+    nrow = 4 * threads
     t = time.perf_counter()
     lib.opg_rows_sample(spec, params, x, y, 0, nrow, threads)
     tr = max(1e-9, time.perf_counter() - t - tj)
