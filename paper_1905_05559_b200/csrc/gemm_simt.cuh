@@ -121,13 +121,27 @@ struct EpiStore {
         T* p = c + b * bstride + m * ldc + n;
         *p = beta == T(0) ? alpha * acc : alpha * acc + beta * *p;
     }
-    // tensor-core epilogue: v[rr][cc] = acc(row0 + rr, col0 + cc), coalesced rows
-    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
-        const int64_t col = col0 + lane;
-        if (col >= N) return;
-        for (int rr = 0; rr < 32 && row0 + rr < M; ++rr) {
-            T* p = c + (row0 + rr) * ldc + col;
-            *p = beta == T(0) ? alpha * (T)v[rr][lane] : alpha * (T)v[rr][lane] + beta * *p;
+    // tensor-core epilogue (see EpiBlock contract below)
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float*,
+                          int lane) const {
+        const int q = lane & 7, rsub = lane >> 3;
+        const int64_t col = col0 + 4 * q;
+        const bool vec = sizeof(T) == 4 && beta == T(0) && (ldc & 3) == 0;
+        for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + rsub;
+            const int64_t row = row0 + r;
+            if (row >= M) break;
+            T* p = c + row * ldc + col;
+            const float4 x = *reinterpret_cast<const float4*>(&buf[r][4 * q]);
+            if constexpr (sizeof(T) == 4) {
+                if (vec && col + 3 < N) {
+                    __stcs(reinterpret_cast<float4*>(p), make_float4(alpha * x.x, alpha * x.y, alpha * x.z, alpha * x.w));
+                    continue;
+                }
+            }
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+            for (int u = 0; u < 4 && col + u < N; ++u)
+                p[u] = beta == T(0) ? alpha * (T)xs[u] : alpha * (T)xs[u] + beta * p[u];
         }
     }
 };
@@ -149,16 +163,36 @@ struct EpiSymLower {
         c[m * ldc + n] = v;
         c[n * ldc + m] = v;
     }
-    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
-        {  // lower entries, row by row (lanes along columns)
-            const int64_t col = col0 + lane;
-            for (int rr = 0; rr < 32 && row0 + rr < M; ++rr)
-                if (col < N && col <= row0 + rr) c[(row0 + rr) * ldc + col] = alpha * (T)v[rr][lane];
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float* v,
+                          int lane) const {
+        {  // lower entries (col <= row): 16-byte vectors along rows
+            const int q = lane & 7, rsub = lane >> 3;
+            const int64_t col = col0 + 4 * q;
+            for (int it = 0; it < 8; ++it) {
+                const int r = it * 4 + rsub;
+                const int64_t row = row0 + r;
+                if (row >= M) break;
+                const float4 x = *reinterpret_cast<const float4*>(&buf[r][4 * q]);
+                T* p = c + row * ldc + col;
+                if constexpr (sizeof(T) == 4) {
+                    if ((ldc & 3) == 0 && col + 3 <= row && col + 3 < N) {
+                        __stcs(reinterpret_cast<float4*>(p),
+                               make_float4(alpha * x.x, alpha * x.y, alpha * x.z, alpha * x.w));
+                        continue;
+                    }
+                }
+                const float xs[4] = {x.x, x.y, x.z, x.w};
+                for (int u = 0; u < 4; ++u)
+                    if (col + u < N && col + u <= row) __stcs(&p[u], alpha * (T)xs[u]);
+            }
         }
-        {  // mirrored entries, column by column (lanes along rows)
+        {  // mirrored strictly-lower entries: this lane's row, straight from registers
             const int64_t row = row0 + lane;
-            for (int cc = 0; cc < 32 && col0 + cc < N; ++cc)
-                if (row < M && col0 + cc < row) c[(col0 + cc) * ldc + row] = alpha * (T)v[lane][cc];
+            if (row < M) {
+#pragma unroll
+                for (int cc = 0; cc < 32; ++cc)  // constant trip count keeps v[] in registers
+                    if (col0 + cc < N && col0 + cc < row) __stcs(&c[(col0 + cc) * ldc + row], alpha * (T)v[cc]);
+            }
         }
     }
 };

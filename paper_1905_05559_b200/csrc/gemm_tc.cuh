@@ -142,6 +142,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Epilogue block contract: after stage_block, buf[r][c] (16-byte aligned rows
+// of 36 floats) holds acc(row0 + r, col0 + c) for the warp's 32 x 32 block and
+// v[] still holds this lane's own row (row0 + lane) -- so stores along rows
+// use buf (lanes across columns, 16-byte vectors) and transposed stores use v
+// (lanes across rows, one register per column).
+__device__ __forceinline__ void stage_block(float (*buf)[36], const float* v, int lane) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(&buf[lane][4 * q]) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+}
+
 // ---------------------------------------------------------------- kernel
 struct TcShape {
     int64_t M, N, K;
@@ -156,7 +168,7 @@ template <int BN>
 struct TcSmem {
     static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
     static constexpr int B_BYTES = BN * BK * 4;
-    static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;
+    static constexpr int EPI_BYTES = 4 * 32 * 36 * 4;
     static constexpr int MAX_SMEM = 227 * 1024;
     __host__ __device__ static constexpr int stage_bytes(int nsplit) { return (A_BYTES + B_BYTES) * (nsplit == 1 ? 1 : 2); }
     __host__ __device__ static constexpr int stages(int nsplit) {
@@ -307,7 +319,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         }
     } else if (warp >= 4) {  // ---------------- epilogue
         const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
-        float(*buf)[33] = reinterpret_cast<float(*)[33]>(epi_buf + ew * 32 * 33);
+        float(*buf)[36] = reinterpret_cast<float(*)[36]>(epi_buf + ew * 32 * 36);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -322,10 +334,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
                 if (row0 < sh.M) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) buf[lane][i] = v[i];
-                    __syncwarp();
-                    epi.block(row0, col0, sh.M, sh.N, buf, lane);
+                    stage_block(buf, v, lane);
+                    epi.block(row0, col0, sh.M, sh.N, buf, v, lane);
                     __syncwarp();
                 }
             }
@@ -381,33 +391,54 @@ __device__ __forceinline__ void mbar_expect_tx_cluster(uint64_t* bar, uint32_t b
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 
 // TMA into this CTA's smem, completion counted on the leader's barrier
+// Operand tiles are re-read by neighbouring tiles: keep them in L2 against the
+// P x P output stream (evict_last policy on every TMA load).
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void tma2_2d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
-                                        int32_t c1) {
+                                        int32_t c1, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-        "%4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void tma2_3d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
-                                        int32_t c1, int32_t c2) {
+                                        int32_t c1, int32_t c2, uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-        "%5}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1), "r"(c2)
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
         : "memory");
+}
+
+// Grouped rasterisation: consecutive tile indices walk GROUP_M m-tiles down a
+// column before moving right, so the ~74 tiles in flight share a few A and B
+// panels in L2.
+constexpr int64_t GROUP_M = 16;
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t mt, int64_t nt, int64_t& mi, int64_t& ni) {
+    const int64_t per = GROUP_M * nt;
+    const int64_t g = t / per, local = t - g * per;
+    const int64_t gm = ::min(GROUP_M, mt - g * GROUP_M);
+    mi = g * GROUP_M + local % gm;
+    ni = local / gm;
 }
 
 template <int ROWS>
 __device__ __forceinline__ void load_tile2(uint8_t* dst, const CUtensorMap* map, uint32_t bar, int mn, int mn3d,
-                                           int64_t r0, int64_t k0) {
+                                           int64_t r0, int64_t k0, uint64_t pol) {
     if (!mn) {
-        tma2_2d(dst, map, bar, (int32_t)k0, (int32_t)r0);
+        tma2_2d(dst, map, bar, (int32_t)k0, (int32_t)r0, pol);
     } else if (mn3d) {
-        tma2_3d(dst, map, bar, 0, (int32_t)k0, (int32_t)(r0 / 32));
+        tma2_3d(dst, map, bar, 0, (int32_t)k0, (int32_t)(r0 / 32), pol);
     } else {
 #pragma unroll
-        for (int i = 0; i < ROWS / 32; ++i) tma2_2d(dst + i * 4096, map, bar, (int32_t)(r0 + 32 * i), (int32_t)k0);
+        for (int i = 0; i < ROWS / 32; ++i)
+            tma2_2d(dst + i * 4096, map, bar, (int32_t)(r0 + 32 * i), (int32_t)k0, pol);
     }
 }
 
@@ -438,7 +469,7 @@ template <int BN>
 struct PairSmem {
     static constexpr int A_BYTES = 128 * BK * 4;       // own 128 rows
     static constexpr int B_BYTES = (BN / 2) * BK * 4;  // own half of B
-    static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;
+    static constexpr int EPI_BYTES = EPI_WARPS * 32 * 36 * 4;
     static constexpr int MAX_SMEM = 227 * 1024;
     __host__ __device__ static constexpr int stage_bytes(int nsplit) { return (A_BYTES + B_BYTES) * (nsplit == 1 ? 1 : 2); }
     __host__ __device__ static constexpr int stages(int nsplit) {
@@ -512,8 +543,11 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t bytes_leader = (uint32_t)(2 * STAGE_BYTES);
+            const uint64_t pol = evict_last_policy();
             for (int64_t t = pair_id; t < ntiles; t += npairs) {
-                const int64_t m0 = (t / nt) * 256, n0 = (t % nt) * BN;
+                int64_t mi, ni;
+                tile_coords(t, mt, nt, mi, ni);
+                const int64_t m0 = mi * 256, n0 = ni * BN;
                 if (epi.skip(0, m0, n0, 256, BN)) continue;
                 const int64_t half = tile_ntile(n0) / 2;
                 const int64_t am0 = m0 + 128 * rank, bn0 = n0 + half * rank;
@@ -525,11 +559,11 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     uint8_t* sa = stage_base + stage * STAGE_BYTES;
                     uint8_t* sb = sa + S::A_BYTES * split;
                     const int64_t k0 = kb * BK;
-                    load_tile2<128>(sa, &mapA, fb, sh.a_mn, sh.a_3d, am0, k0);
-                    load_tile2<BN / 2>(sb, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0);
+                    load_tile2<128>(sa, &mapA, fb, sh.a_mn, sh.a_3d, am0, k0, pol);
+                    load_tile2<BN / 2>(sb, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0, pol);
                     if (split == 2) {
-                        load_tile2<128>(sa + S::A_BYTES, &mapAlo, fb, sh.a_mn, sh.a_3d, am0, k0);
-                        load_tile2<BN / 2>(sb + S::B_BYTES, &mapBlo, fb, sh.b_mn, sh.b_3d, bn0, k0);
+                        load_tile2<128>(sa + S::A_BYTES, &mapAlo, fb, sh.a_mn, sh.a_3d, am0, k0, pol);
+                        load_tile2<BN / 2>(sb + S::B_BYTES, &mapBlo, fb, sh.b_mn, sh.b_3d, bn0, k0, pol);
                     }
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
@@ -542,7 +576,9 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t t = pair_id; t < ntiles; t += npairs) {
-                const int64_t m0 = (t / nt) * 256, n0 = (t % nt) * BN;
+                int64_t mi, ni;
+                tile_coords(t, mt, nt, mi, ni);
+                const int64_t m0 = mi * 256, n0 = ni * BN;
                 if (epi.skip(0, m0, n0, 256, BN)) continue;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -579,12 +615,14 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const int ew = warp - 4;
         const int quad = warp % 4;   // TMEM lanes 32*quad .. +31
         const int chalf = ew / 4;    // column half of the tile
-        float(*buf)[33] = reinterpret_cast<float(*)[33]>(epi_buf + ew * 32 * 33);
+        float(*buf)[36] = reinterpret_cast<float(*)[36]>(epi_buf + ew * 32 * 36);
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = pair_id; t < ntiles; t += npairs) {
-            const int64_t m0 = (t / nt) * 256, n0 = (t % nt) * BN;
+            int64_t mi, ni;
+            tile_coords(t, mt, nt, mi, ni);
+            const int64_t m0 = mi * 256, n0 = ni * BN;
             if (epi.skip(0, m0, n0, 256, BN)) continue;
             mbar_wait_cluster(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -595,10 +633,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
                 if (row0 < sh.M) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) buf[lane][i] = v[i];
-                    __syncwarp();
-                    epi.block(row0, col0, sh.M, sh.N, buf, lane);
+                    stage_block(buf, v, lane);
+                    epi.block(row0, col0, sh.M, sh.N, buf, v, lane);
                     __syncwarp();
                 }
             }

@@ -484,33 +484,51 @@ struct EpiHess {
         }
     }
     // tensor-core epilogue (32 x 32 block, coalesced in both store directions)
-    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*v)[33], int lane) const {
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float* v,
+                          int lane) const {
         const bool tri = diag && mirror;
-        // one division per block; rows advance (o'', jj) incrementally
+        // one division per block; each row's (o'', jj) follows by carrying
         const int64_t opp0 = row0 / J, jj0 = row0 - opp0 * J;
         const int nrows = (int)::min((int64_t)32, M - row0);
-        {  // direct: H[gr][gc], lanes along columns
-            const int64_t c = col0 + lane;
-            const bool live = c < N;
-            const bool wcol = c < tm;
-            int64_t opp = opp0, jj = jj0;
-            for (int rr = 0; rr < nrows; ++rr) {
-                const int64_t gr = woffk + j0 + jj;
-                const int64_t gc = wcol ? woffm + opp * tm + c : boffm + opp;
-                if (live && (!tri || gc <= gr)) H[gr * ldh + gc] = alpha * (T)v[rr][lane];
-                if (++jj == J) { jj = 0; ++opp; }
+        {  // direct: H[gr][gc], 16-byte vectors along gc
+            const int q = lane & 7, rsub = lane >> 3;
+            const int64_t c = col0 + 4 * q;
+            for (int it = 0; it < 8; ++it) {
+                const int r = it * 4 + rsub;
+                if (r >= nrows) break;
+                int64_t opp = opp0, jj = jj0 + r;
+                while (jj >= J) { jj -= J; ++opp; }
+                const int64_t gr = woffk + j0 + jj, wb = woffm + opp * tm;
+                const float4 x = *reinterpret_cast<const float4*>(&buf[r][4 * q]);
+                T* row = H + gr * ldh;
+                if constexpr (sizeof(T) == 4) {
+                    const int64_t gc = wb + c;
+                    if (c + 3 < tm && c + 3 < N && ((gc | ldh) & 3) == 0 && (!tri || gc + 3 <= gr)) {
+                        __stcs(reinterpret_cast<float4*>(row + gc),
+                               make_float4(alpha * x.x, alpha * x.y, alpha * x.z, alpha * x.w));
+                        continue;
+                    }
+                }
+                const float xs[4] = {x.x, x.y, x.z, x.w};
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t cc = c + u;
+                    if (cc >= N) break;
+                    const int64_t gc = cc < tm ? wb + cc : boffm + opp;
+                    if (!tri || gc <= gr) __stcs(&row[gc], alpha * (T)xs[u]);
+                }
             }
         }
-        if (mirror && lane < nrows) {  // transposed: H[gc][gr], lanes along rows
+        if (mirror && lane < nrows) {  // transposed: H[gc][gr], this lane's row from registers
             int64_t opp = opp0, jj = jj0 + lane;
             while (jj >= J) { jj -= J; ++opp; }
             const int64_t gr = woffk + j0 + jj;
             const int ncols = (int)::min((int64_t)32, N - col0);
             const int64_t wbase = woffm + opp * tm;
-            for (int cc = 0; cc < ncols; ++cc) {
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) {  // constant trip count keeps v[] in registers
                 const int64_t c = col0 + cc;
                 const int64_t gc = c < tm ? wbase + c : boffm + opp;
-                if (!tri || gc < gr) H[gc * ldh + gr] = alpha * (T)v[lane][cc];
+                if (cc < ncols && (!tri || gc < gr)) __stcs(&H[gc * ldh + gr], alpha * (T)v[cc]);
             }
         }
     }
