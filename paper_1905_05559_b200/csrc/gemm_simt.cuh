@@ -40,7 +40,7 @@ struct NoSkip {
 
 template <class T, int BM, int BN, int BK, int TM, int TN, class Epi>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
-gemm_simt_kernel(int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, Epi epi) {
+gemm_simt_kernel(int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, Epi epi, int64_t kchunk) {
     constexpr int NTX = BN / TN, NTY = BM / TM, NT = NTX * NTY;
     __shared__ T As[BK][BM + 1];
     __shared__ T Bs[BK][BN + 1];
@@ -49,6 +49,13 @@ gemm_simt_kernel(int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, Epi epi)
     if (epi.skip(bz, m0, n0, BM, BN)) return;
     const T* Ap = A.p + bz * A.bstride;
     const T* Bp = B.p + bz * B.bstride;
+    int64_t kbeg = 0;
+    if (kchunk > 0) {  // split-K: grid.z indexes K ranges, operands are not batched
+        kbeg = bz * kchunk;
+        K = ::min(K, kbeg + kchunk);
+        Ap = A.p;
+        Bp = B.p;
+    }
     const int tid = threadIdx.x, tx = tid % NTX, ty = tid / NTX;
     T acc[TM][TN];
 #pragma unroll
@@ -56,7 +63,7 @@ gemm_simt_kernel(int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, Epi epi)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
 
-    for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    for (int64_t k0 = kbeg; k0 < K; k0 += BK) {
         // A tile: BM x BK
         for (int e = tid; e < BM * BK; e += NT) {
             int r, kk;
@@ -98,13 +105,16 @@ gemm_simt_kernel(int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, Epi epi)
         }
 }
 
+// batch > 0: batched GEMM over grid.z.  kchunk > 0: split-K instead, grid.z =
+// ceil(K / kchunk) ranges, the epilogue sees the range index as its batch.
 template <class T, class Epi>
 void gemm_simt(cudaStream_t s, int64_t M, int64_t N, int64_t K, int64_t batch, Opnd<T> A, Opnd<T> B,
-               const Epi& epi) {
+               const Epi& epi, int64_t kchunk = 0) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
     constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
-    dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)batch);
-    gemm_simt_kernel<T, BM, BN, BK, TM, TN, Epi><<<grid, (BM / TM) * (BN / TN), 0, s>>>(M, N, K, A, B, epi);
+    const int64_t gz = kchunk > 0 ? ceil_div(K, kchunk) : batch;
+    dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)gz);
+    gemm_simt_kernel<T, BM, BN, BK, TM, TN, Epi><<<grid, (BM / TM) * (BN / TN), 0, s>>>(M, N, K, A, B, epi, kchunk);
     CK_LAUNCH();
 }
 

@@ -161,9 +161,43 @@ void alloc_cache(const ModelDesc& md, int64_t n, Cache<T>& c, cudaStream_t s) {
 
 // Dense GEMM dispatcher used by the small model GEMMs: SIMT in every mode
 // (their cost is O(N * P) against the O(N * P^2) curvature products).
+// Split-K partial sums: split z writes its own M x N slab (deterministic;
+// the slabs are summed in a fixed order by finalize_kernel).
+template <class T>
+struct EpiPartial {
+    T* ws;
+    int64_t ld, slab;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int z, int64_t m, int64_t n, T acc) const { ws[z * slab + m * ld + n] = acc; }
+};
+
+template <class T, class Epi>
+__global__ void finalize_kernel(const T* __restrict__ ws, int64_t splits, int64_t M, int64_t N, Epi epi) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M * N) return;
+    T acc = T(0);
+    for (int64_t z = 0; z < splits; ++z) acc += ws[z * M * N + i];
+    epi(0, i / N, i % N, acc);
+}
+
+// Tall-K, narrow-output layer GEMMs (e.g. 1000 x 32 x 784) give the 64 x 64
+// tile grid only a few CTAs: split K across grid.z so all SMs stream the
+// operands, then apply the layer epilogue in one elementwise pass.
 template <class T, class Epi>
 void model_gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, const Epi& e) {
-    gemm_simt<T>(s, M, N, K, 1, A, B, e);
+    const int64_t tiles = ceil_div(M, 64) * ceil_div(N, 64);
+    int64_t splits = std::min<int64_t>(ceil_div(2 * 148, tiles), K / 64);
+    if (splits < 2) {
+        gemm_simt<T>(s, M, N, K, 1, A, B, e);
+        return;
+    }
+    const int64_t kc = round_up(ceil_div(K, splits), 16);
+    splits = ceil_div(K, kc);
+    DevMem ws((size_t)splits * M * N * sizeof(T), s);
+    EpiPartial<T> ep{dptr<T>(ws), N, M * N};
+    gemm_simt<T>(s, M, N, K, 1, A, B, ep, kc);
+    finalize_kernel<T, Epi><<<(unsigned)ceil_div(M * N, 256), 256, 0, s>>>(dptr<T>(ws), splits, M, N, e);
+    CK_LAUNCH();
 }
 
 template <class T>
