@@ -35,6 +35,48 @@ struct CurvGemm {
     }
 };
 
+// Fused weight-tangent Hessian block: the R operand is formed on chip from
+// the extended activation tile and the profiles.  Specialised for TF32 in
+// gemm_tc.cuh; returns false where no fused kernel exists (then the R
+// operand is materialised by rgen_kernel).
+template <class T>
+struct HessFusedArgs {
+    const T* akT;       // a_k^T extended: row r holds a_k[., r mod T_k]
+    int64_t ak_rows;
+    const T* qT;        // Q_m^T extended [T_{m+1}][qrows][ldn] or null (m == k)
+    int64_t qrows, q_rows_total;
+    const T* pv;        // G or P_m transposed [T_{k+1}][T_{m+1}][ldn]
+    const T* dT;        // delta_k^T [T_{k+1}][ldn]
+    const T* am;        // a_m [n][lda_m] (B operand, MN-major)
+    int64_t lda_m, ldn, n, tk, tm, tm1, nw;
+    int diag;
+};
+
+template <class T>
+struct HessFused {
+    static bool run(int, cudaStream_t, const HessFusedArgs<T>&, const EpiHess<T>&) { return false; }
+};
+
+// out[r][.] = in[r mod period][.]  (row replication for the extended tiles)
+template <class T>
+__global__ void replicate_rows_kernel(const T* __restrict__ in, int64_t period, int64_t ld, T* __restrict__ out,
+                                      int64_t rows, int64_t in_bstride, int64_t out_bstride) {
+    const int64_t b = blockIdx.y;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ld; i += (int64_t)gridDim.x * blockDim.x)
+        out[b * out_bstride + i] = in[b * in_bstride + ((i / ld) % period) * ld + i % ld];
+}
+
+// QX[o''][r][n] = QT[(r mod T_k)][o''][n]
+template <class T>
+__global__ void qext_kernel(const T* __restrict__ qt, int64_t tk, int64_t tm1, int64_t ldn, T* __restrict__ qx,
+                            int64_t rows) {
+    const int64_t opp = blockIdx.y;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ldn; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / ldn, e = i - r * ldn;
+        qx[(opp * rows + r) * ldn + e] = qt[((r % tk) * tm1 + opp) * ldn + e];
+    }
+}
+
 // rz_k[b] = a_k RW_k[b]^T + Rb_k[b]
 template <class T>
 struct EpiRzBias {
@@ -158,13 +200,18 @@ struct Engine {
     double hess_required_entries(int k, int m, int64_t j0, int64_t Jc) const {
         const int64_t tm = md.w[m], tm1 = md.w[m + 1];
         if (m != k) return (double)Jc * tm1 * (tm + 1);
+        // row j of the block needs clamp(j - o*tm + 1, 0, tm) weight columns of
+        // band o and the bias column when j >= tm*tm1 + o: closed-form sums
+        auto S = [tm](int64_t x, int64_t a) -> double {  // sum_{j<x} clamp(j - a + 1, 0, tm)
+            if (x <= a) return 0.0;
+            const double r = (double)std::min(x - a, tm);
+            return r * (r + 1.0) / 2.0 + (double)std::max<int64_t>(0, x - a - tm) * (double)tm;
+        };
+        const int64_t j1 = j0 + Jc, bias0 = md.boff[m] - md.woff[m];
         double cnt = 0.0;
-        for (int64_t jj = 0; jj < Jc; ++jj) {
-            const int64_t j = j0 + jj;  // row offset inside the block
-            for (int64_t o = 0; o < tm1; ++o) {
-                cnt += (double)std::max<int64_t>(0, std::min<int64_t>(tm, j - o * tm + 1));
-                if (j >= md.boff[m] - md.woff[m] + o) cnt += 1.0;
-            }
+        for (int64_t o = 0; o < tm1; ++o) {
+            cnt += S(j1, o * tm) - S(j0, o * tm);
+            cnt += (double)std::max<int64_t>(0, j1 - std::max(j0, bias0 + o));
         }
         return cnt;
     }
@@ -244,8 +291,9 @@ struct Engine {
             }
             prof_stage.end();
             ProfScope prep_stage("hess_prep", s, 0.0, 0.0);
-            // n-contiguous copies for the R generator (all reads 16-byte vectors)
-            const int64_t ldn = round_up(n, 4);
+            // n-contiguous copies for the R generator (all reads 16-byte vectors);
+            // a 32-multiple pitch keeps every K-block of 32 examples inside a row
+            const int64_t ldn = round_up(n, 32);
             const int64_t tk = md.w[k];
             T* akT = buf(tk + 1, ldn);
             transpose<T>(s, c.a[k], c.lda[k], 0, akT, ldn, 0, n, tk + 1, 1);
@@ -262,17 +310,51 @@ struct Engine {
                 QT[m] = buf(tk * tm1, ldn);
                 transpose<T>(s, Qm[m], c.ldt[m], n * c.ldt[m], QT[m], ldn, tm1 * ldn, n, tm1, tk);
             }
+            // Extended copies for the fused TF32 kernel: a 128-row activation
+            // tile starting anywhere in [0, T_k) reads rows r -> r mod T_k.
+            const bool fused = prec == kTF32 && sizeof(T) == 4;
+            const int64_t ak_rows = tk + 256;
+            T* akX = nullptr;
+            T* QX[kMaxLayers] = {};
+            if (fused) {
+                akX = buf(ak_rows, ldn);
+                replicate_rows_kernel<T><<<dim3(blocks_for(ak_rows * ldn), 1), 256, 0, s>>>(akT, tk, ldn, akX, ak_rows, 0, 0);
+                CK_LAUNCH();
+                for (int m = k - 1; m >= 0; --m) {
+                    const int64_t tm1 = md.w[m + 1];
+                    QX[m] = buf(tm1 * ak_rows, ldn);
+                    // QT[m] is [i][o''][n]; QX[m] is [o''][r][n] with r -> i = r mod T_k
+                    qext_kernel<T><<<dim3(blocks_for(ak_rows * ldn), (unsigned)tm1), 256, 0, s>>>(
+                        QT[m], tk, tm1, ldn, QX[m], ak_rows);
+                    CK_LAUNCH();
+                }
+            }
             prep_stage.end();
             // blocks (k, m), m <= k
             const int64_t Pk = md.block_size(k);
+            const int64_t nw = md.w[k + 1] * tk;
             const int64_t ldr = ldn;
             for (int m = k; m >= 0; --m) {
+                // weight tangents through the fused kernel where it exists; the
+                // chunked R path below then only covers the bias tangents
+                int64_t jbeg = 0;
+                if (fused) {
+                    const int64_t tm = md.w[m], tm1 = md.w[m + 1];
+                    HessFusedArgs<T> fa{akX, ak_rows, m == k ? nullptr : QX[m], ak_rows, tm1 * ak_rows,
+                                        m == k ? GT : PT[m], dkT, c.a[m], c.lda[m], ldn, n, tk, tm, tm1, nw,
+                                        (m == k && !verify) ? 1 : 0};
+                    EpiHess<T> e{H, ldh, nw, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
+                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
+                    const double req = Profiler::get().on ? hess_required_entries(k, m, 0, nw) : 0.0;
+                    ProfScope ps("hess_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * req);
+                    if (HessFused<T>::run(prec, s, fa, e)) jbeg = nw;
+                }
                 const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                 int64_t J = (int64_t)(chunk_bytes / ((size_t)tm1 * ldr * sizeof(T)));
                 J = std::max<int64_t>(128, J / 128 * 128);
-                J = std::min<int64_t>(J, round_up(Pk, 128));
+                J = std::min<int64_t>(J, round_up(Pk - jbeg, 128));
                 DevMem rbuf((size_t)tm1 * J * ldr * sizeof(T), s);
-                for (int64_t j0 = 0; j0 < Pk; j0 += J) {
+                for (int64_t j0 = jbeg; j0 < Pk; j0 += J) {
                     const int64_t Jc = std::min<int64_t>(J, Pk - j0);
                     // R rows (o'', jj) whose block entries are all above the
                     // diagonal are neither generated nor multiplied

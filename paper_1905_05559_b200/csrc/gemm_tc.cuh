@@ -653,6 +653,266 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     }
 }
 
+// ---------------------------------------------------------------- fused Hessian block
+// Weight-tangent rows of one Hessian block (k, m) without materialising R:
+//   A[(o'', j), n] = a_k[n, i] * PV[o][o''][n]  (+ delta_k[n, o] * Q[o''][i][n]   if m < k)
+// with j = o * T_k + i.  Per K-block the producer TMA-loads the activation
+// tile a_k^T[i0 .. i0+127][n0 .. n0+31] (and the Q tile), four transform
+// warps scale it in place (one thread per row, swizzle-aware 16-byte smem
+// accesses), fence it into the async proxy and arrive on the leader's full
+// barrier; the MMA then runs exactly as in tc_gemm_pair_kernel.  Rows are
+// enumerated per o'' band (j >= jstart(o'')), so only tiles holding lower-
+// triangle entries are visited.
+struct FusedHess {
+    const float* pv;   // [T_{k+1}][T_{m+1}][ldn]  (G or P_m, n-contiguous)
+    const float* dT;   // delta_k^T [T_{k+1}][ldn]   (m < k only)
+    int64_t ldn, tk, tm, tm1, nw;  // T_k, T_m, T_{m+1}, weight tangents T_{k+1} T_k
+    int64_t qrows;     // rows per o'' slab of the extended Q^T (m < k)
+    int diag, hasq;
+    const int4* tiles;  // (o'', j0, n0, -) of every pair tile holding required entries
+    int64_t ntiles;
+    // first tangent row of band o'' (aligned to the 256-row pair tile)
+    __host__ __device__ int64_t jstart(int64_t opp) const {
+        if (!diag) return 0;
+        const int64_t s = (opp * tm) / 256 * 256;
+        return s < nw ? s : nw;
+    }
+    __host__ __device__ int64_t band_tiles(int64_t opp) const { return ceil_div(nw - jstart(opp), 256); }
+};
+
+constexpr int kFusedThreads = 128 + 32 * EPI_WARPS + 128;  // control, epilogue, transform
+
+template <int BN>
+struct FusedSmem {
+    static constexpr int A_BYTES = 128 * BK * 4;
+    static constexpr int B_BYTES = (BN / 2) * BK * 4;
+    static constexpr int EPI_BYTES = EPI_WARPS * 32 * 36 * 4;
+    static constexpr int MAX_SMEM = 227 * 1024;
+    __host__ __device__ static constexpr int stage_bytes(int hasq) { return A_BYTES * (hasq ? 2 : 1) + B_BYTES; }
+    __host__ __device__ static constexpr int stages(int hasq) {
+        const int st = (MAX_SMEM - 1024 - EPI_BYTES - 1024) / stage_bytes(hasq);
+        return st > 8 ? 8 : st;
+    }
+    __host__ __device__ static constexpr int bytes(int hasq) {
+        return 1024 + stages(hasq) * stage_bytes(hasq) + EPI_BYTES + 1024;
+    }
+};
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int BN, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
+tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_constant__ CUtensorMap mapQ,
+                     const __grid_constant__ CUtensorMap mapB, FusedHess fh, TcShape sh, Epi epi) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using S = FusedSmem<BN>;
+    const int STAGE_BYTES = S::stage_bytes(fh.hasq);
+    const int NST = S::stages(fh.hasq);
+    const int A_OFF_Q = S::A_BYTES, B_OFF = S::A_BYTES * (fh.hasq ? 2 : 1);
+    uint8_t* stage_base = smem;
+    float* epi_buf = reinterpret_cast<float*>(smem + NST * STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES + S::EPI_BYTES);
+    uint64_t* full = bars;         // [8] leader: 1 producer + 8 transform-warp arrivals, B tx
+    uint64_t* empty = bars + 8;    // [8] both CTAs (multicast commit)
+    uint64_t* afull = bars + 16;   // [8] local: A (and Q) tiles landed
+    uint64_t* tfull = bars + 24;   // [2]
+    uint64_t* tempty = bars + 26;  // [2] leader
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cta_rank();
+    const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
+    const int64_t ntiles = fh.ntiles;
+    const int64_t nk = ceil_div(sh.K, BK);
+    constexpr int TW0 = 4 + EPI_WARPS;  // first transform warp
+
+    // tile t -> (o'', first tangent row j0, n0) from the host-built list of
+    // tiles that hold required entries; rows of the pair tile are j0 .. j0+255
+    // and the virtual GEMM row is o'' * nw + j
+    auto tile_of = [&](int64_t t, int64_t& opp, int64_t& j0, int64_t& n0) {
+        const int4 tl = __ldg(&fh.tiles[t]);
+        opp = tl.x;
+        j0 = tl.y;
+        n0 = tl.z;
+    };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_map(&mapAk);
+        prefetch_map(&mapB);
+        if (fh.hasq) prefetch_map(&mapQ);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1 + 2 * 4);
+            mbar_init(&empty[s], 1);
+            mbar_init(&afull[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "n"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    auto tile_ntile = [&](int64_t n0) -> int { return (int)::min((int64_t)BN, (sh.N - n0 + 63) / 64 * 64); };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- producer
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint64_t pol = evict_last_policy();
+            for (int64_t t = pair_id; t < ntiles; t += npairs) {
+                int64_t opp, j0, n0;
+                tile_of(t, opp, j0, n0);
+                const int64_t jr = j0 + 128 * rank;           // this CTA's first tangent row
+                const int64_t i0 = jr % fh.tk;                // row in the extended a_k^T
+                const int64_t half = tile_ntile(n0) / 2;
+                const int64_t bn0 = n0 + half * rank;
+                for (int64_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = stage_base + stage * STAGE_BYTES;
+                    const int64_t k0 = kb * BK;
+                    mbar_expect_tx(&afull[stage], (uint32_t)(S::A_BYTES * (fh.hasq ? 2 : 1)));
+                    tma_load_2d(sa, &mapAk, &afull[stage], (int32_t)k0, (int32_t)i0);
+                    if (fh.hasq) tma_load_2d(sa + A_OFF_Q, &mapQ, &afull[stage], (int32_t)k0, (int32_t)(opp * fh.qrows + i0));
+                    const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
+                    if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * S::B_BYTES));
+                    load_tile2<BN / 2>(sa + B_OFF, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0, pol);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = pair_id; t < ntiles; t += npairs) {
+                int64_t opp, j0, n0;
+                tile_of(t, opp, j0, n0);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t idesc = idesc2_tf32(tile_ntile(n0), false, sh.b_mn);
+                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                for (int64_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
+                    const uint32_t sb = sa + B_OFF;
+#pragma unroll
+                    for (int ks = 0; ks < BK / 8; ++ks) {
+                        const uint32_t boff = sh.b_mn ? ks * sh.mn_kstep : ks * 32;
+                        const uint32_t blbo = sh.b_mn ? sh.mn_lbo : 16, bsbo = sh.b_mn ? sh.mn_sbo : 1024;
+                        const uint32_t blay = sh.b_mn ? sh.mn_layout : 2;
+                        mma2_tf32(d, smem_desc(sa + ks * 32, 16, 1024, 2), smem_desc(sb + boff, blbo, bsbo, blay),
+                                  idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                    }
+                    commit2(&empty[stage]);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+                commit2(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= TW0) {  // ---------------- A transform (both CTAs)
+        const int row = (warp - TW0) * 32 + lane;  // tile row owned by this thread
+        const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = pair_id; t < ntiles; t += npairs) {
+            int64_t opp, j0, n0;
+            tile_of(t, opp, j0, n0);
+            const int64_t j = j0 + 128 * rank + row;
+            const int64_t o = ::min(j, fh.nw - 1) / fh.tk;  // rows past the band are masked later
+            const float* pvrow = fh.pv + (o * fh.tm1 + opp) * fh.ldn;
+            const float* drow = fh.hasq ? fh.dT + o * fh.ldn : nullptr;
+            const int sw = row & 7;
+            for (int64_t kb = 0; kb < nk; ++kb) {
+                mbar_wait(&afull[stage], phase);
+                uint8_t* sa = stage_base + stage * STAGE_BYTES + row * 128;
+                const int64_t n0k = kb * BK;
+                // all loads first (8 smem + 8 profile vectors in flight), then
+                // the products, then the stores: logical 16-byte chunk L holds
+                // examples n0k + 4L .. +3 and sits at physical chunk L ^ (row & 7)
+                float4 x[8], p[8];
+#pragma unroll
+                for (int L = 0; L < 8; ++L) x[L] = *reinterpret_cast<const float4*>(sa + ((L ^ sw) << 4));
+#pragma unroll
+                for (int L = 0; L < 8; ++L) p[L] = __ldg(reinterpret_cast<const float4*>(pvrow + n0k + 4 * L));
+#pragma unroll
+                for (int L = 0; L < 8; ++L) {
+                    x[L].x *= p[L].x; x[L].y *= p[L].y; x[L].z *= p[L].z; x[L].w *= p[L].w;
+                }
+                if (fh.hasq) {
+#pragma unroll
+                    for (int L = 0; L < 8; ++L) {
+                        const float4 q = *reinterpret_cast<const float4*>(sa + A_OFF_Q + ((L ^ sw) << 4));
+                        const float4 dd = __ldg(reinterpret_cast<const float4*>(drow + n0k + 4 * L));
+                        x[L].x += dd.x * q.x; x[L].y += dd.y * q.y; x[L].z += dd.z * q.z; x[L].w += dd.w * q.w;
+                    }
+                }
+#pragma unroll
+                for (int L = 0; L < 8; ++L) *reinterpret_cast<float4*>(sa + ((L ^ sw) << 4)) = x[L];
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(fb0 + stage * 8);
+                if (++stage == NST) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs)
+        const int ew = warp - 4;
+        const int quad = warp % 4;
+        const int chalf = ew / 4;
+        float(*buf)[36] = reinterpret_cast<float(*)[36]>(epi_buf + ew * 32 * 36);
+        const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = pair_id; t < ntiles; t += npairs) {
+            int64_t opp, j0, n0;
+            tile_of(t, opp, j0, n0);
+            const int64_t m0 = opp * fh.nw + j0;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row0 = m0 + 128 * rank + quad * 32;
+            const int64_t band_end = (opp + 1) * fh.nw;  // rows beyond the band are not stored
+            for (int cb = chalf * (BN / 64); cb < (chalf + 1) * (BN / 64); ++cb) {
+                const int64_t col0 = n0 + cb * 32;
+                if (col0 >= sh.N) break;
+                float v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                if (row0 < band_end) {
+                    stage_block(buf, v, lane);
+                    epi.block(row0, col0, band_end, sh.N, buf, v, lane);
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN));
+    }
+}
+
 }  // namespace pair
 
 // ---------------------------------------------------------------- host side
@@ -830,6 +1090,47 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     else if (bn == 128) tc::launch<128>(s, sh, ma, mb, mal, mbl, e);
     else tc::launch<64>(s, sh, ma, mb, mal, mbl, e);
 }
+
+// Fused Hessian block (TF32 only): weight-tangent rows of block (k, m) with
+// the A operand generated in shared memory (see tc_hess_fused_kernel).
+template <>
+struct HessFused<float> {
+    static bool run(int prec, cudaStream_t s, const HessFusedArgs<float>& a, const EpiHess<float>& e) {
+        if (prec != kTF32) return false;
+        constexpr int BN = 256;
+        namespace pair = tc::pair;
+        pair::FusedHess fh{a.pv, a.dT, a.ldn, a.tk, a.tm, a.tm1, a.nw, a.qrows, a.diag, a.qT ? 1 : 0, nullptr, 0};
+        const int64_t N = a.tm + 1;  // weight columns + bias column of block m
+        // tile list: every (o'' band, 256-row j tile, n tile) holding a required entry
+        std::vector<int4> list;
+        for (int64_t o = 0; o < a.tm1; ++o)
+            for (int64_t j0 = fh.jstart(o); j0 < a.nw; j0 += 256)
+                for (int64_t n0 = 0; n0 < N; n0 += BN)
+                    if (!e.skip(0, o * a.nw + j0, n0, 256, BN)) list.push_back(make_int4((int)o, (int)j0, (int)n0, 0));
+        if (list.empty()) return true;
+        DevMem tl(list.size() * sizeof(int4), s);
+        CK_CUDA(cudaMemcpyAsync(tl.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+        fh.tiles = dptr<int4>(tl);
+        fh.ntiles = (int64_t)list.size();
+        const int b3 = a.lda_m >= round_up(N, 32) ? 1 : 0;
+        tc::TcShape sh{0, N, a.n, 0, 1, 1, (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, 0, b3};
+        CUtensorMap mak = tc::make_map(a.akT, a.ak_rows, a.n, a.ldn, 0, 128);
+        CUtensorMap mq = a.qT ? tc::make_map(a.qT, a.q_rows_total, a.n, a.ldn, 0, 128) : mak;
+        CUtensorMap mb = tc::make_map(a.am, N, a.n, a.lda_m, 1, BN / 2, b3);
+        using S = pair::FusedSmem<BN>;
+        static bool attr = false;
+        if (!attr) {
+            CK_CUDA(cudaFuncSetAttribute(pair::tc_hess_fused_kernel<BN, EpiHess<float>>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(S::bytes(0), S::bytes(1))));
+            attr = true;
+        }
+        const int grid = 2 * (int)std::min<int64_t>(fh.ntiles, tc::num_sms() / 2);
+        pair::tc_hess_fused_kernel<BN, EpiHess<float>><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
+            mak, mq, mb, fh, sh, e);
+        CK_LAUNCH();
+        return true;
+    }
+};
 
 // Route TF32 precisions of the large curvature GEMMs to the tensor cores.
 template <class Epi>

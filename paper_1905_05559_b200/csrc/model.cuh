@@ -494,10 +494,10 @@ struct EpiHess {
     T alpha;
     int diag;    // m == k
     int mirror;  // write the transposed entry too
-    __device__ __forceinline__ int64_t gcol(int64_t opp, int64_t c) const {
+    __host__ __device__ __forceinline__ int64_t gcol(int64_t opp, int64_t c) const {
         return c < tm ? woffm + opp * tm + c : boffm + opp;
     }
-    __device__ bool skip(int, int64_t r0, int64_t c0, int64_t bm, int64_t) const {
+    __host__ __device__ bool skip(int, int64_t r0, int64_t c0, int64_t bm, int64_t) const {
         if (!diag || !mirror) return false;
         const int64_t opp_min = r0 / J;
         const int64_t jj_max = (r0 + bm - 1) / J > opp_min ? J - 1 : (r0 + bm - 1) % J;
