@@ -50,6 +50,7 @@ struct HessFusedArgs {
     const T* am;        // a_m [n][lda_m] (B operand, MN-major)
     int64_t lda_m, ldn, n, tk, tm, tm1, nw;
     int diag;
+    int64_t rows;  // all tangent rows of step k (weights then biases)
 };
 
 template <class T>
@@ -342,12 +343,12 @@ struct Engine {
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                     HessFusedArgs<T> fa{akX, ak_rows, m == k ? nullptr : QX[m], ak_rows, tm1 * ak_rows,
                                         m == k ? GT : PT[m], dkT, c.a[m], c.lda[m], ldn, n, tk, tm, tm1, nw,
-                                        (m == k && !verify) ? 1 : 0};
-                    EpiHess<T> e{H, ldh, nw, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
+                                        (m == k && !verify) ? 1 : 0, Pk};
+                    EpiHess<T> e{H, ldh, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
                                  m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
-                    const double req = Profiler::get().on ? hess_required_entries(k, m, 0, nw) : 0.0;
+                    const double req = Profiler::get().on ? hess_required_entries(k, m, 0, Pk) : 0.0;
                     ProfScope ps("hess_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * req);
-                    if (HessFused<T>::run(prec, s, fa, e)) jbeg = nw;
+                    if (HessFused<T>::run(prec, s, fa, e)) jbeg = Pk;
                 }
                 const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                 int64_t J = (int64_t)(chunk_bytes / ((size_t)tm1 * ldr * sizeof(T)));

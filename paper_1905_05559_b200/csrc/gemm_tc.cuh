@@ -201,7 +201,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcShape sh,
                Epi epi) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by offset from the __shared__ array, so the compiler
+    // keeps the shared state space (LDS/STS, not generic LD/ST) for derived pointers
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int A_BYTES = TcSmem<BN>::A_BYTES, B_BYTES = TcSmem<BN>::B_BYTES;
     const int split = sh.nsplit == 1 ? 1 : 2;  // operand copies per stage (hi[, lo])
     const int STAGE_BYTES = (A_BYTES + B_BYTES) * split;
@@ -487,7 +489,9 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcShape sh,
                     Epi epi) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by offset from the __shared__ array, so the compiler
+    // keeps the shared state space (LDS/STS, not generic LD/ST) for derived pointers
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     using S = PairSmem<BN>;
     const int split = sh.nsplit == 1 ? 1 : 2;
     const int STAGE_BYTES = S::stage_bytes(sh.nsplit);
@@ -671,13 +675,13 @@ struct FusedHess {
     int diag, hasq;
     const int4* tiles;  // (o'', j0, n0, -) of every pair tile holding required entries
     int64_t ntiles;
+    int64_t rows;       // tangent rows of the block: nw weights, then T_{k+1} biases (s = 1)
     // first tangent row of band o'' (aligned to the 256-row pair tile)
     __host__ __device__ int64_t jstart(int64_t opp) const {
         if (!diag) return 0;
         const int64_t s = (opp * tm) / 256 * 256;
-        return s < nw ? s : nw;
+        return s < rows ? s : rows;
     }
-    __host__ __device__ int64_t band_tiles(int64_t opp) const { return ceil_div(nw - jstart(opp), 256); }
 };
 
 constexpr int kFusedThreads = 128 + 32 * EPI_WARPS + 128;  // control, epilogue, transform
@@ -707,7 +711,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_constant__ CUtensorMap mapQ,
                      const __grid_constant__ CUtensorMap mapB, FusedHess fh, TcShape sh, Epi epi) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by offset from the __shared__ array, so the compiler
+    // keeps the shared state space (LDS/STS, not generic LD/ST) for derived pointers
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     using S = FusedSmem<BN>;
     const int STAGE_BYTES = S::stage_bytes(fh.hasq);
     const int NST = S::stages(fh.hasq);
@@ -834,8 +840,9 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         for (int64_t t = pair_id; t < ntiles; t += npairs) {
             int64_t opp, j0, n0;
             tile_of(t, opp, j0, n0);
-            const int64_t j = j0 + 128 * rank + row;
-            const int64_t o = ::min(j, fh.nw - 1) / fh.tk;  // rows past the band are masked later
+            const int64_t j = ::min(j0 + 128 * rank + row, fh.rows - 1);  // rows past the band are masked later
+            const bool bias = j >= fh.nw;  // bias tangent: s_n = 1, no delta*Q term
+            const int64_t o = bias ? j - fh.nw : j / fh.tk;
             const float* pvrow = fh.pv + (o * fh.tm1 + opp) * fh.ldn;
             const float* drow = fh.hasq ? fh.dT + o * fh.ldn : nullptr;
             const int sw = row & 7;
@@ -853,9 +860,13 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 for (int L = 0; L < 8; ++L) p[L] = __ldg(reinterpret_cast<const float4*>(pvrow + n0k + 4 * L));
 #pragma unroll
                 for (int L = 0; L < 8; ++L) {
-                    x[L].x *= p[L].x; x[L].y *= p[L].y; x[L].z *= p[L].z; x[L].w *= p[L].w;
+                    if (bias) {
+                        x[L] = p[L];
+                    } else {
+                        x[L].x *= p[L].x; x[L].y *= p[L].y; x[L].z *= p[L].z; x[L].w *= p[L].w;
+                    }
                 }
-                if (fh.hasq) {
+                if (fh.hasq && !bias) {
 #pragma unroll
                     for (int L = 0; L < 8; ++L) {
                         const float4 q = *reinterpret_cast<const float4*>(sa + A_OFF_Q + ((L ^ sw) << 4));
@@ -882,11 +893,11 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         for (int64_t t = pair_id; t < ntiles; t += npairs) {
             int64_t opp, j0, n0;
             tile_of(t, opp, j0, n0);
-            const int64_t m0 = opp * fh.nw + j0;
+            const int64_t m0 = opp * fh.rows + j0;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t row0 = m0 + 128 * rank + quad * 32;
-            const int64_t band_end = (opp + 1) * fh.nw;  // rows beyond the band are not stored
+            const int64_t band_end = (opp + 1) * fh.rows;  // rows beyond the band are not stored
             for (int cb = chalf * (BN / 64); cb < (chalf + 1) * (BN / 64); ++cb) {
                 const int64_t col0 = n0 + cb * 32;
                 if (col0 >= sh.N) break;
@@ -1099,14 +1110,16 @@ struct HessFused<float> {
         if (prec != kTF32) return false;
         constexpr int BN = 256;
         namespace pair = tc::pair;
-        pair::FusedHess fh{a.pv, a.dT, a.ldn, a.tk, a.tm, a.tm1, a.nw, a.qrows, a.diag, a.qT ? 1 : 0, nullptr, 0};
+        pair::FusedHess fh{a.pv, a.dT, a.ldn, a.tk, a.tm, a.tm1, a.nw, a.qrows, a.diag, a.qT ? 1 : 0, nullptr, 0,
+                           a.rows};
         const int64_t N = a.tm + 1;  // weight columns + bias column of block m
         // tile list: every (o'' band, 256-row j tile, n tile) holding a required entry
         std::vector<int4> list;
         for (int64_t o = 0; o < a.tm1; ++o)
-            for (int64_t j0 = fh.jstart(o); j0 < a.nw; j0 += 256)
+            for (int64_t j0 = fh.jstart(o); j0 < a.rows; j0 += 256)
                 for (int64_t n0 = 0; n0 < N; n0 += BN)
-                    if (!e.skip(0, o * a.nw + j0, n0, 256, BN)) list.push_back(make_int4((int)o, (int)j0, (int)n0, 0));
+                    if (!e.skip(0, o * a.rows + j0, n0, 256, BN))
+                        list.push_back(make_int4((int)o, (int)j0, (int)n0, 0));
         if (list.empty()) return true;
         DevMem tl(list.size() * sizeof(int4), s);
         CK_CUDA(cudaMemcpyAsync(tl.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
