@@ -140,6 +140,20 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
                          int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
                          void* stream);
 
+/* Row shards for multi-GPU runs (no collective on the data path).  A shard
+ * assembles the lower-triangle entries of rows [row_begin, row_end) and their
+ * mirrored copies into a full-size output buffer; the shards of
+ * curvkit_shard_rows(P, nshards, s, ...) for s = 0..nshards-1 write disjoint
+ * entries whose union is the full matrix (rows balanced by triangle area).
+ * opg_shard needs row_begin % 4 == 0 (the boundaries of shard_rows are). */
+int curvkit_shard_rows(int64_t p, int64_t nshards, int64_t shard, int64_t* row_begin, int64_t* row_end);
+int curvkit_dev_hessian_shard(const curvkit_model* model, const void* params, const void* x,
+                              const int32_t* labels, int64_t n, int32_t precision, int64_t row_begin,
+                              int64_t row_end, void* h, int64_t ldh, void* stream);
+int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const void* x,
+                          const int32_t* labels, int64_t n, int32_t precision, int64_t row_begin,
+                          int64_t row_end, void* g, int64_t ldg, void* stream);
+
 /* The curvature GEMM engine on its own (fp32 storage): C[m][n] = alpha *
  * sum_k A(m,k) B(n,k) with A(m,k) = a[m*lda+k] if a_kmajor else a[k*lda+m]
  * (likewise B).  TF32/TF32X3 run the tcgen05 kernel, F32 the SIMT one. */

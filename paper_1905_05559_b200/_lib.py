@@ -48,6 +48,9 @@ SIGNATURES = {
     "curvkit_dev_assemble_hessian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_opg": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_jacobian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
+    "curvkit_shard_rows": [i64, i64, i64, C.POINTER(i64), C.POINTER(i64)],
+    "curvkit_dev_hessian_shard": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
+    "curvkit_dev_opg_shard": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
     "curvkit_dev_gemm": [i64, i64, i64, vptr, i64, i32, vptr, i64, i32, vptr, i64, C.c_float, i32, vptr],
     "curvkit_dev_opg_topk": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
 }

@@ -546,6 +546,67 @@ int curvkit_dev_assemble_jacobian(const curvkit_model* model, const void* params
     });
 }
 
+// ---- row shards (multi-GPU without a data-path collective) --------------------
+// Row r of the lower triangle holds r + 1 entries, so shard s of `nshards`
+// takes rows [P sqrt(s/n), P sqrt((s+1)/n)), rounded to 32 rows (one MN atom;
+// tiles straddling a boundary are computed by both shards and masked).
+int curvkit_shard_rows(int64_t p, int64_t nshards, int64_t shard, int64_t* row_begin, int64_t* row_end) {
+    return guard([&] {
+        if (p < 1 || nshards < 1 || shard < 0 || shard >= nshards) contract("shard_rows: bad arguments");
+        auto bound = [&](int64_t s) -> int64_t {
+            if (s <= 0) return 0;
+            if (s >= nshards) return p;
+            const double b = (double)p * std::sqrt((double)s / (double)nshards);
+            return std::min<int64_t>(p, (int64_t)std::llround(b / 32.0) * 32);
+        };
+        *row_begin = bound(shard);
+        *row_end = std::max(*row_begin, bound(shard + 1));
+    });
+}
+
+int curvkit_dev_hessian_shard(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                              int64_t n, int32_t precision, int64_t row_begin, int64_t row_end, void* h, int64_t ldh,
+                              void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("assemble_hessian: empty dataset");
+        if (row_begin < 0 || row_end < row_begin) contract("hessian_shard: bad row range");
+        cudaStream_t s = dev_stream(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            Engine<T> eng{md, s, precision};
+            eng.hessian((const T*)params, c, (T*)h, ldh, false, row_begin, row_end);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                          int64_t n, int32_t precision, int64_t row_begin, int64_t row_end, void* g, int64_t ldg,
+                          void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("assemble_opg: empty dataset");
+        if (row_begin < 0 || row_end < row_begin || (row_begin & 3)) contract("opg_shard: bad row range");
+        cudaStream_t s = dev_stream(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            DevMem J;
+            int64_t ldj;
+            jacobian_full<T>(md, c, J, ldj, s);
+            Engine<T> eng{md, s, precision};
+            eng.opg(dptr<T>(J), ldj, n, (T*)g, ldg, row_begin, row_end);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
 int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, int32_t a_kmajor,
                      const float* b, int64_t ldb, int32_t b_kmajor, float* c, int64_t ldc, float alpha,
                      int32_t precision, void* stream) {

@@ -182,11 +182,16 @@ struct Engine {
     }
 
     // ---------------------------------------------------------------- opg
-    void opg(const T* J, int64_t ldj, int64_t n, T* G, int64_t ldg) {
-        EpiSymLower<T> e{G, ldg, T(1) / T(n)};
-        ProfScope ps("opg_gemm", s, 2.0 * (double)md.P * (double)(md.P + 1) / 2.0 * (double)n,
-                     (double)sizeof(T) * ((double)n * md.P + (double)md.P * md.P));
-        CurvGemm<T, EpiSymLower<T>>::run(prec, s, md.P, md.P, n, mnmaj(J, ldj), mnmaj(J, ldj), e);
+    // Rows [rb, re) of the lower triangle and their mirrors (a row shard; the
+    // full product is rb = 0, re = P).  rb must be a multiple of 4 (TMA base).
+    void opg(const T* J, int64_t ldj, int64_t n, T* G, int64_t ldg, int64_t rb = 0, int64_t re = -1) {
+        if (re < 0 || re > md.P) re = md.P;
+        if (rb >= re) return;
+        EpiSymLower<T> e{G, ldg, T(1) / T(n), rb};
+        const double entries = (double)re * (re + 1) / 2.0 - (double)rb * (rb + 1) / 2.0;
+        ProfScope ps("opg_gemm", s, 2.0 * entries * (double)n,
+                     (double)sizeof(T) * ((double)n * re + 2.0 * entries));
+        CurvGemm<T, EpiSymLower<T>>::run(prec, s, re - rb, re, n, mnmaj(J + rb, ldj), mnmaj(J, ldj), e);
     }
 
     // ---------------------------------------------------------------- hessian
@@ -217,11 +222,15 @@ struct Engine {
         return cnt;
     }
 
-    void hessian(const T* params, const Cache<T>& c, T* H, int64_t ldh, bool verify) {
+    // Tangent rows [rlo, rhi) of H (their lower entries and mirrors); the full
+    // assembly is rlo = 0, rhi = P.  Layers with no owned row are skipped.
+    void hessian(const T* params, const Cache<T>& c, T* H, int64_t ldh, bool verify, int64_t rlo = 0,
+                 int64_t rhi = INT64_MAX) {
         const int S = md.S;
         const int64_t n = c.n;
         for (int k = 0; k < S; ++k) {
             const int64_t np = md.w[k + 1];
+            if (md.woff[k] + md.block_size(k) <= rlo || md.woff[k] >= rhi) continue;
             std::vector<DevMem> keep;
             auto buf = [&](int64_t rows, int64_t ld) {
                 keep.emplace_back((size_t)rows * ld * sizeof(T), s);
@@ -345,8 +354,10 @@ struct Engine {
                                         m == k ? GT : PT[m], dkT, c.a[m], c.lda[m], ldn, n, tk, tm, tm1, nw,
                                         (m == k && !verify) ? 1 : 0, Pk};
                     EpiHess<T> e{H, ldh, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
-                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
-                    const double req = Profiler::get().on ? hess_required_entries(k, m, 0, Pk) : 0.0;
+                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1, rlo, rhi};
+                    const int64_t js = std::clamp<int64_t>(rlo - md.woff[k], 0, Pk);
+                    const int64_t je = std::clamp<int64_t>(rhi - md.woff[k], 0, Pk);
+                    const double req = Profiler::get().on ? hess_required_entries(k, m, js, je - js) : 0.0;
                     ProfScope ps("hess_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * req);
                     if (HessFused<T>::run(prec, s, fa, e)) jbeg = Pk;
                 }
@@ -357,6 +368,7 @@ struct Engine {
                 DevMem rbuf((size_t)tm1 * J * ldr * sizeof(T), s);
                 for (int64_t j0 = jbeg; j0 < Pk; j0 += J) {
                     const int64_t Jc = std::min<int64_t>(J, Pk - j0);
+                    if (md.woff[k] + j0 + Jc <= rlo || md.woff[k] + j0 >= rhi) continue;  // no owned row
                     // R rows (o'', jj) whose block entries are all above the
                     // diagonal are neither generated nor multiplied
                     int64_t opp_hi = tm1;
@@ -371,7 +383,7 @@ struct Engine {
                         CK_LAUNCH();
                     }
                     EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
-                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1};
+                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1, rlo, rhi};
                     // algorithmic work is counted only while profiling (host loop)
                     const double req = Profiler::get().on ? hess_required_entries(k, m, j0, Jc) : 0.0;
                     ProfScope ps("hess_gemm", s, 2.0 * (double)n * req, (double)sizeof(T) * ((double)rows * ldr + req));

@@ -164,10 +164,14 @@ struct EpiSymLower {
     T* c;
     int64_t ldc;
     T alpha;
+    // row shard: the GEMM's A operand starts at matrix row roff, so GEMM row m
+    // is matrix row m + roff (columns are always absolute)
+    int64_t roff = 0;
     __device__ bool skip(int, int64_t m0, int64_t n0, int64_t bm, int64_t) const {
-        return n0 > m0 + bm - 1;
+        return n0 > m0 + roff + bm - 1;
     }
     __device__ void operator()(int, int64_t m, int64_t n, T acc) const {
+        m += roff;
         if (n > m) return;
         const T v = alpha * acc;
         c[m * ldc + n] = v;
@@ -180,8 +184,8 @@ struct EpiSymLower {
             const int64_t col = col0 + 4 * q;
             for (int it = 0; it < 8; ++it) {
                 const int r = it * 4 + rsub;
-                const int64_t row = row0 + r;
-                if (row >= M) break;
+                if (row0 + r >= M) break;
+                const int64_t row = row0 + r + roff;
                 const float4 x = *reinterpret_cast<const float4*>(&buf[r][4 * q]);
                 T* p = c + row * ldc + col;
                 if constexpr (sizeof(T) == 4) {
@@ -197,8 +201,8 @@ struct EpiSymLower {
             }
         }
         {  // mirrored strictly-lower entries: this lane's row, straight from registers
-            const int64_t row = row0 + lane;
-            if (row < M) {
+            if (row0 + lane < M) {
+                const int64_t row = row0 + lane + roff;
 #pragma unroll
                 for (int cc = 0; cc < 32; ++cc)  // constant trip count keeps v[] in registers
                     if (col0 + cc < N && col0 + cc < row) __stcs(&c[(col0 + cc) * ldc + row], alpha * (T)v[cc]);

@@ -1116,10 +1116,13 @@ struct HessFused<float> {
         // tile list: every (o'' band, 256-row j tile, n tile) holding a required entry
         std::vector<int4> list;
         for (int64_t o = 0; o < a.tm1; ++o)
-            for (int64_t j0 = fh.jstart(o); j0 < a.rows; j0 += 256)
+            for (int64_t j0 = fh.jstart(o); j0 < a.rows; j0 += 256) {
+                // tangent rows of this pair tile must intersect the owned shard
+                if (e.woffk + j0 + 256 <= e.rlo || e.woffk + j0 >= e.rhi) continue;
                 for (int64_t n0 = 0; n0 < N; n0 += BN)
                     if (!e.skip(0, o * a.rows + j0, n0, 256, BN))
                         list.push_back(make_int4((int)o, (int)j0, (int)n0, 0));
+            }
         if (list.empty()) return true;
         DevMem tl(list.size() * sizeof(int4), s);
         CK_CUDA(cudaMemcpyAsync(tl.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice, s));

@@ -494,6 +494,10 @@ struct EpiHess {
     T alpha;
     int diag;    // m == k
     int mirror;  // write the transposed entry too
+    // shard of tangent rows owned by this call (global H row of the lower
+    // entry); entries of other rows and their mirrors are left untouched
+    int64_t rlo = 0, rhi = INT64_MAX;
+    __host__ __device__ __forceinline__ bool owns(int64_t gr) const { return gr >= rlo && gr < rhi; }
     __host__ __device__ __forceinline__ int64_t gcol(int64_t opp, int64_t c) const {
         return c < tm ? woffm + opp * tm + c : boffm + opp;
     }
@@ -508,6 +512,7 @@ struct EpiHess {
         const int64_t opp = r / J, jj = r - opp * J;
         const int64_t gr = woffk + j0 + jj, gc = gcol(opp, c);
         const T v = alpha * acc;
+        if (!owns(gr)) return;
         if (diag && mirror) {
             if (gc > gr) return;
             H[gr * ldh + gc] = v;
@@ -533,6 +538,7 @@ struct EpiHess {
                 int64_t opp = opp0, jj = jj0 + r;
                 while (jj >= J) { jj -= J; ++opp; }
                 const int64_t gr = woffk + j0 + jj, wb = woffm + opp * tm;
+                if (!owns(gr)) continue;
                 const float4 x = *reinterpret_cast<const float4*>(&buf[r][4 * q]);
                 T* row = H + gr * ldh;
                 if constexpr (sizeof(T) == 4) {
@@ -556,7 +562,7 @@ struct EpiHess {
             int64_t opp = opp0, jj = jj0 + lane;
             while (jj >= J) { jj -= J; ++opp; }
             const int64_t gr = woffk + j0 + jj;
-            const int ncols = (int)::min((int64_t)32, N - col0);
+            const int ncols = owns(gr) ? (int)::min((int64_t)32, N - col0) : 0;
             const int64_t wbase = woffm + opp * tm;
 #pragma unroll
             for (int cc = 0; cc < 32; ++cc) {  // constant trip count keeps v[] in registers

@@ -410,3 +410,22 @@ def dev_gemm(m, n, k, a, lda, a_kmajor, b, ldb, b_kmajor, c, ldc, alpha=1.0, pre
     """The curvature GEMM engine on device fp32 buffers (C = alpha A B^T)."""
     _lib.check(_lib.load().curvkit_dev_gemm(m, n, k, _ptr(a), lda, int(a_kmajor), _ptr(b), ldb, int(b_kmajor),
                                              _ptr(c), ldc, float(alpha), _prec(precision), _stream(stream)))
+
+
+def shard_rows(p: int, nshards: int, shard: int):
+    """Row range [begin, end) of shard `shard` (triangle-area balanced, 32-aligned)."""
+    b, e = C.c_int64(), C.c_int64()
+    _lib.check(_lib.load().curvkit_shard_rows(p, nshards, shard, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def dev_hessian_shard(spec, params, x, labels, n, row_begin, row_end, out, ldh, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_hessian_shard(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
+                                                      _prec(precision), row_begin, row_end, _ptr(out), ldh,
+                                                      _stream(stream)))
+
+
+def dev_opg_shard(spec, params, x, labels, n, row_begin, row_end, out, ldg, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_opg_shard(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
+                                                  _prec(precision), row_begin, row_end, _ptr(out), ldg,
+                                                  _stream(stream)))
