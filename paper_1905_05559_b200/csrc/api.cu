@@ -109,9 +109,10 @@ void check_memory_cap(int64_t p, int64_t cap, const char* who) {  // curvature.c
                  std::to_string(cap) + "; use the matrix-free eigensolvers instead");
 }
 
-// Keep the stream-ordered pool's memory mapped between calls: the curvature
-// workspaces (R chunks, profiles, J) are ~1 GB and would otherwise be
-// returned to the driver at every synchronisation and re-mapped next call.
+// Keep up to 16 GB of the stream-ordered pool mapped between calls: the
+// curvature workspaces (profiles, extended tiles, J for moderate P) would
+// otherwise be returned to the driver at every synchronisation and re-mapped
+// on the next call; giant one-off buffers (an 84 GB J) are still released.
 void keep_pool_memory() {
     static bool done[64] = {};
     int dev = 0;
@@ -119,7 +120,7 @@ void keep_pool_memory() {
     if (dev < 64 && done[dev]) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
+        uint64_t thr = uint64_t(16) << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     if (dev < 64) done[dev] = true;
@@ -262,10 +263,10 @@ void host_hessian(const ModelDesc& md, const double* params, const double* x, co
 }
 
 template <class T>
-void jacobian_full(const ModelDesc& md, const Cache<T>& c, DevMem& J, int64_t& ldj, cudaStream_t s) {
+void jacobian_full(const ModelDesc& md, const Cache<T>& c, DevMem& J, int64_t& ldj, cudaStream_t s, bool rn = false) {
     ldj = round_up(md.P, 32);
     J = DevMem((size_t)c.n * ldj * sizeof(T), s);
-    jacobian<T>(md, c, 0, c.n, dptr<T>(J), ldj, s);
+    jacobian<T>(md, c, 0, c.n, dptr<T>(J), ldj, s, rn);
 }
 
 template <class T, class U>
@@ -280,7 +281,7 @@ void host_opg(const ModelDesc& md, const double* params, const double* x, const 
     upload_and_forward<T>(md, params, x, lab, n, r, s);
     DevMem J;
     int64_t ldj;
-    jacobian_full<T>(md, r.cache, J, ldj, s);
+    jacobian_full<T>(md, r.cache, J, ldj, s, prec == kTF32);
     const int64_t ldg = round_up(md.P, 4);
     DevMem G((size_t)md.P * ldg * sizeof(T), s);
     Engine<T> eng{md, s, prec};
@@ -519,7 +520,7 @@ int curvkit_dev_assemble_opg(const curvkit_model* model, const void* params, con
             forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
             DevMem J;
             int64_t ldj;
-            jacobian_full<T>(md, c, J, ldj, s);
+            jacobian_full<T>(md, c, J, ldj, s, precision == kTF32);
             Engine<T> eng{md, s, precision};
             eng.opg(dptr<T>(J), ldj, n, (T*)g, ldg);
         };
@@ -598,7 +599,7 @@ int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const 
             forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
             DevMem J;
             int64_t ldj;
-            jacobian_full<T>(md, c, J, ldj, s);
+            jacobian_full<T>(md, c, J, ldj, s, precision == kTF32);
             Engine<T> eng{md, s, precision};
             eng.opg(dptr<T>(J), ldj, n, (T*)g, ldg, row_begin, row_end);
         };

@@ -75,6 +75,13 @@ struct ModelDesc {
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
+// fp32 -> nearest TF32 (10-bit mantissa), kept in fp32 storage
+__device__ __forceinline__ float round_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 // ---- activations (model.cpp:9-50) -------------------------------------------
 
 template <class T>

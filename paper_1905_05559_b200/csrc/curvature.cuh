@@ -184,6 +184,7 @@ struct Engine {
     // ---------------------------------------------------------------- opg
     // Rows [rb, re) of the lower triangle and their mirrors (a row shard; the
     // full product is rb = 0, re = P).  rb must be a multiple of 4 (TMA base).
+    // In TF32 mode J must have been stored rounded (jacobian(..., rn = true)).
     void opg(const T* J, int64_t ldj, int64_t n, T* G, int64_t ldg, int64_t rb = 0, int64_t re = -1) {
         if (re < 0 || re > md.P) re = md.P;
         if (rb >= re) return;
@@ -191,7 +192,7 @@ struct Engine {
         const double entries = (double)re * (re + 1) / 2.0 - (double)rb * (rb + 1) / 2.0;
         ProfScope ps("opg_gemm", s, 2.0 * entries * (double)n,
                      (double)sizeof(T) * ((double)n * re + 2.0 * entries));
-        CurvGemm<T, EpiSymLower<T>>::run(prec, s, re - rb, re, n, mnmaj(J + rb, ldj), mnmaj(J, ldj), e);
+        CurvGemm<T, EpiSymLower<T>>::run(prec, s, re - rb, re, n, pre_rounded(mnmaj(J + rb, ldj)), pre_rounded(mnmaj(J, ldj)), e);
     }
 
     // ---------------------------------------------------------------- hessian

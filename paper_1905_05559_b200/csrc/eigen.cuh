@@ -244,12 +244,12 @@ struct EigenWork {
     // T_out (n x l) = J X ; X is P x l (ld lx)
     void apply_j(const T* J, int64_t ldj, int64_t n, const T* X, int64_t ldx, int64_t l, T* Tout, int64_t ldt) {
         EpiStore<T> e{Tout, ldt, 0, T(1), T(0)};
-        CurvGemm<T, EpiStore<T>>::run(prec, s, n, l, md.P, kmaj(J, ldj), mnmaj(X, ldx), e);
+        CurvGemm<T, EpiStore<T>>::run(prec, s, n, l, md.P, pre_rounded(kmaj(J, ldj)), mnmaj(X, ldx), e);
     }
     // Y (P x l) = J^T Tn ; Tn is n x l
     void apply_jt(const T* J, int64_t ldj, int64_t n, const T* Tn, int64_t ldt, int64_t l, T* Y, int64_t ldy) {
         EpiStore<T> e{Y, ldy, 0, T(1), T(0)};
-        CurvGemm<T, EpiStore<T>>::run(prec, s, md.P, l, n, mnmaj(J, ldj), mnmaj(Tn, ldt), e);
+        CurvGemm<T, EpiStore<T>>::run(prec, s, md.P, l, n, pre_rounded(mnmaj(J, ldj)), mnmaj(Tn, ldt), e);
     }
 };
 
@@ -267,7 +267,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     // per-example gradients stay resident in HBM
     const int64_t ldj = round_up(P, 32);
     DevMem J((size_t)n * ldj * sizeof(T), s);
-    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s);
+    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
     DevMem Y((size_t)P * ldl * sizeof(T), s), Om((size_t)P * ldl * sizeof(T), s);
     DevMem Tn((size_t)n * ldl * sizeof(T), s);
     CK_CUDA(cudaMemsetAsync(Om.p, 0, (size_t)P * ldl * sizeof(T), s));
@@ -281,9 +281,8 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         ew.orth(dptr<T>(Y), P, l, ldl);
         X = dptr<T>(Y);
     }
-    // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q).  The subspace only needs TF32,
-    // the Ritz values do not: this one pass runs as 3xTF32 in TF32 mode.
-    ew.prec = prec == kTF32 ? k3xTF32 : prec;
+    // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q) with round-to-nearest TF32
+    // operands (J stored rounded, Q rounded per GEMM): unbiased products.
     ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
     DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
     CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));

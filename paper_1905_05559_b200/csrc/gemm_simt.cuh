@@ -18,7 +18,14 @@ struct Opnd {
     int64_t ld = 0;
     int kmajor = 1;
     int64_t bstride = 0;  // batch stride in elements
+    int rounded = 0;      // values already rounded to TF32 by their producer
 };
+
+template <class T>
+inline Opnd<T> pre_rounded(Opnd<T> o) {
+    o.rounded = 1;
+    return o;
+}
 
 template <class T>
 __host__ __device__ inline Opnd<T> kmaj(const T* p, int64_t ld, int64_t bs = 0) {

@@ -875,7 +875,11 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                     }
                 }
 #pragma unroll
-                for (int L = 0; L < 8; ++L) *reinterpret_cast<float4*>(sa + ((L ^ sw) << 4)) = x[L];
+                for (int L = 0; L < 8; ++L) {  // round to nearest TF32 (the MMA would truncate)
+                    x[L].x = round_tf32(x[L].x); x[L].y = round_tf32(x[L].y);
+                    x[L].z = round_tf32(x[L].z); x[L].w = round_tf32(x[L].w);
+                    *reinterpret_cast<float4*>(sa + ((L ^ sw) << 4)) = x[L];
+                }
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(fb0 + stage * 8);
@@ -989,6 +993,19 @@ inline int num_sms() {
     return n;
 }
 
+// out = nearest TF32 of in, over a flat range (whole pitched buffers)
+__global__ void round_tf32_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t count) {
+    const int64_t n4 = count / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 v = reinterpret_cast<const float4*>(in)[i];
+        v.x = round_tf32(v.x); v.y = round_tf32(v.y); v.z = round_tf32(v.z); v.w = round_tf32(v.w);
+        reinterpret_cast<float4*>(out)[i] = v;
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = round_tf32(in[i]);
+}
+
 // hi = tf32(x) (round to nearest), lo = tf32(x - hi); padding columns copied as 0
 __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
                                   float* __restrict__ hi, float* __restrict__ lo) {
@@ -1061,6 +1078,28 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     const float* pb = B.p;
     const float* pal = A.p;
     const float* pbl = B.p;
+    if (sh.nsplit == 1) {
+        // the MMA truncates fp32 to TF32 (a bias towards zero in every
+        // product): operands not pre-rounded by their producer get a
+        // round-to-nearest copy (same layout and pitch, padding included)
+        auto round_copy = [&](const Opnd<float>& o, int64_t rows, DevMem& out) -> const float* {
+            const int64_t r = o.kmajor ? rows : K, c = o.kmajor ? K : rows;
+            // last row only up to what a TMA box can touch (never past the source)
+            const int64_t count = (r - 1) * o.ld + std::min(o.ld, round_up(c, 32)) / 4 * 4;
+            out = DevMem((size_t)count * 4, s);
+            tc::round_tf32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(count, 1024), 148 * 32), 256, 0, s>>>(
+                o.p, dptr<float>(out), count);
+            CK_LAUNCH();
+            return dptr<float>(out);
+        };
+        if (!A.rounded) pa = round_copy(A, M, ahi);
+        if (!B.rounded) {
+            if (B.p == A.p && B.ld == A.ld && B.kmajor == A.kmajor) pb = pa;
+            else pb = round_copy(B, N, bhi);
+        }
+        pal = pa;
+        pbl = pb;
+    }
     if (sh.nsplit == 3) {
         // split both operands into hi/lo TF32 parts (same layout and pitch)
         auto split = [&](const Opnd<float>& o, int64_t rows, DevMem& hi, DevMem& lo) {
@@ -1132,7 +1171,12 @@ struct HessFused<float> {
         tc::TcShape sh{0, N, a.n, 0, 1, 1, (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, 0, b3};
         CUtensorMap mak = tc::make_map(a.akT, a.ak_rows, a.n, a.ldn, 0, 128);
         CUtensorMap mq = a.qT ? tc::make_map(a.qT, a.q_rows_total, a.n, a.ldn, 0, 128) : mak;
-        CUtensorMap mb = tc::make_map(a.am, N, a.n, a.lda_m, 1, BN / 2, b3);
+        // B = a_m, rounded to nearest TF32 (n rows x lda_m, padding included)
+        DevMem amr((size_t)a.n * a.lda_m * 4, s);
+        tc::round_tf32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(a.n * a.lda_m, 1024), 148 * 32), 256, 0, s>>>(
+            a.am, dptr<float>(amr), a.n * a.lda_m);
+        CK_LAUNCH();
+        CUtensorMap mb = tc::make_map(dptr<float>(amr), N, a.n, a.lda_m, 1, BN / 2, b3);
         using S = pair::FusedSmem<BN>;
         static bool attr = false;
         if (!attr) {

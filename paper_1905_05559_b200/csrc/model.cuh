@@ -267,7 +267,7 @@ __device__ __forceinline__ T jac_entry(const LayerTable& t, const CachePtrs<T>& 
 
 template <class T>
 __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T> cp, int64_t P, T* __restrict__ J,
-                                                       int64_t ldj, int64_t row0) {
+                                                       int64_t ldj, int64_t row0, int rn_tf32) {
     const int64_t row = row0 + blockIdx.y;
     T* out = J + (int64_t)blockIdx.y * ldj;
     constexpr int V = 16 / sizeof(T);
@@ -276,6 +276,12 @@ __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T
         T v[V];
 #pragma unroll
         for (int u = 0; u < V; ++u) v[u] = c0 + u < P ? jac_entry(t, cp, row, c0 + u) : T(0);
+        if constexpr (sizeof(T) == 4) {
+            if (rn_tf32) {
+#pragma unroll
+                for (int u = 0; u < V; ++u) v[u] = round_tf32(v[u]);
+            }
+        }
         if (c0 + V <= ldj) {
             if constexpr (sizeof(T) == 4) {
                 *reinterpret_cast<float4*>(out + c0) = make_float4(v[0], v[1], v[2], v[3]);
@@ -288,9 +294,12 @@ __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T
     }
 }
 
+// rn_tf32: store J pre-rounded to TF32 (round to nearest) when it only feeds
+// TF32 tensor-core products; the MMA itself truncates the low mantissa bits,
+// which biases every product towards zero.
 template <class T>
 void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows, T* J, int64_t ldj,
-              cudaStream_t s) {
+              cudaStream_t s, bool rn_tf32 = false) {
     ProfScope ps("jacobian", s, 0.0, (double)sizeof(T) * rows * md.P);
     LayerTable t = make_table(md, c.lda, c.ldt);
     CachePtrs<T> cp;
@@ -299,7 +308,8 @@ void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows
     const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(md.P, per_block), 64);
     for (int64_t r = 0; r < rows; r += 65535) {
         const int64_t rr = std::min<int64_t>(65535, rows - r);
-        jacobian_kernel<T><<<dim3(gx, (unsigned)rr), 256, 0, s>>>(t, cp, md.P, J + r * ldj, ldj, row0 + r);
+        jacobian_kernel<T><<<dim3(gx, (unsigned)rr), 256, 0, s>>>(t, cp, md.P, J + r * ldj, ldj, row0 + r,
+                                                                   rn_tf32 ? 1 : 0);
         CK_LAUNCH();
     }
 }
