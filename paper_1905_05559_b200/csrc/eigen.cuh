@@ -208,6 +208,7 @@ struct EigenWork {
 
     // Y <- orth(Y) in place (CholeskyQR2), Y is rows x l with ld
     void orth(T* Y, int64_t rows, int64_t l, int64_t ld) {
+        ProfScope ps("eig_orth", s, 2.0 * 2.0 * 2.0 * (double)rows * l * l, 0.0);
         DevMem W((size_t)l * l * sizeof(double), s), Rinv((size_t)l * l * sizeof(double), s);
         DevMem Rt((size_t)l * l * sizeof(T), s), Y2((size_t)rows * ld * sizeof(T), s);
         for (int pass = 0; pass < 2; ++pass) {
@@ -243,11 +244,13 @@ struct EigenWork {
 
     // T_out (n x l) = J X ; X is P x l (ld lx)
     void apply_j(const T* J, int64_t ldj, int64_t n, const T* X, int64_t ldx, int64_t l, T* Tout, int64_t ldt) {
+        ProfScope ps("eig_apply_j", s, 2.0 * (double)n * md.P * l, (double)sizeof(T) * n * md.P);
         EpiStore<T> e{Tout, ldt, 0, T(1), T(0)};
         CurvGemm<T, EpiStore<T>>::run(prec, s, n, l, md.P, pre_rounded(kmaj(J, ldj)), mnmaj(X, ldx), e);
     }
     // Y (P x l) = J^T Tn ; Tn is n x l
     void apply_jt(const T* J, int64_t ldj, int64_t n, const T* Tn, int64_t ldt, int64_t l, T* Y, int64_t ldy) {
+        ProfScope ps("eig_apply_jt", s, 2.0 * (double)n * md.P * l, (double)sizeof(T) * n * md.P);
         EpiStore<T> e{Y, ldy, 0, T(1), T(0)};
         CurvGemm<T, EpiStore<T>>::run(prec, s, md.P, l, n, pre_rounded(mnmaj(J, ldj)), mnmaj(Tn, ldt), e);
     }

@@ -294,6 +294,40 @@ __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T
     }
 }
 
+// Structured writer: one CTA per (example row, layer k) keeps its activation
+// chunk a_k[n, 4t .. 4t+3] in registers and streams the T_{k+1} rows
+// delta_k[n, o] * a_k[n, :] of the weight block, then the bias entries.
+// Needs T_k % 4 == 0 and 16-byte aligned block starts (checked by the host).
+template <class T>
+__global__ void __launch_bounds__(256) jacobian_rows_kernel(LayerTable t, CachePtrs<T> cp, T* __restrict__ J,
+                                                            int64_t ldj, int64_t row0, int rn_tf32) {
+    const int k = blockIdx.y;
+    const int64_t row = row0 + blockIdx.x;
+    const int64_t tin = t.tin[k], tout = t.tout[k];
+    T* out = J + (int64_t)blockIdx.x * ldj;
+    const T* a = cp.a[k] + row * t.lda[k];
+    const T* d = cp.delta[k] + row * t.ldt[k];
+    auto rnd = [&](T v) -> T {
+        if constexpr (sizeof(T) == 4) return rn_tf32 ? round_tf32(v) : v;
+        return v;
+    };
+    for (int64_t i4 = threadIdx.x; i4 * 4 < tin; i4 += blockDim.x) {
+        const T a0 = a[4 * i4], a1 = a[4 * i4 + 1], a2 = a[4 * i4 + 2], a3 = a[4 * i4 + 3];
+        T* dst = out + t.woff[k] + 4 * i4;
+        for (int64_t o = 0; o < tout; ++o) {
+            const T dv = __ldg(&d[o]);
+            if constexpr (sizeof(T) == 4) {
+                __stcs(reinterpret_cast<float4*>(dst + o * tin),
+                       make_float4(rnd(dv * a0), rnd(dv * a1), rnd(dv * a2), rnd(dv * a3)));
+            } else {
+                dst[o * tin] = dv * a0; dst[o * tin + 1] = dv * a1;
+                dst[o * tin + 2] = dv * a2; dst[o * tin + 3] = dv * a3;
+            }
+        }
+    }
+    for (int64_t o = threadIdx.x; o < tout; o += blockDim.x) out[t.boff[k] + o] = rnd(d[o]);
+}
+
 // rn_tf32: store J pre-rounded to TF32 (round to nearest) when it only feeds
 // TF32 tensor-core products; the MMA itself truncates the low mantissa bits,
 // which biases every product towards zero.
@@ -304,6 +338,17 @@ void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows
     LayerTable t = make_table(md, c.lda, c.ldt);
     CachePtrs<T> cp;
     for (int k = 0; k < md.S; ++k) { cp.a[k] = c.a[k]; cp.delta[k] = c.delta[k]; }
+    bool structured = (ldj % 4 == 0);
+    for (int k = 0; k < md.S; ++k) structured = structured && md.w[k] % 4 == 0 && md.woff[k] % 4 == 0;
+    if (structured) {
+        for (int64_t r = 0; r < rows; r += (int64_t)1 << 30) {
+            const int64_t rr = std::min<int64_t>((int64_t)1 << 30, rows - r);
+            jacobian_rows_kernel<T><<<dim3((unsigned)rr, (unsigned)md.S), 256, 0, s>>>(t, cp, J + r * ldj, ldj,
+                                                                                      row0 + r, rn_tf32 ? 1 : 0);
+            CK_LAUNCH();
+        }
+        return;
+    }
     const int64_t per_block = 256 * (16 / sizeof(T));
     const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(md.P, per_block), 64);
     for (int64_t r = 0; r < rows; r += 65535) {

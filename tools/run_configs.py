@@ -36,7 +36,7 @@ for name in which:
             curv.dev_opg_topk(spec, p, xx, ll, wl.n, k, wl.oversample, wl.power_iters, 7, q, lam, precision="tf32")
             torch.cuda.synchronize()
             print(name, "topk", it, "%.1f ms" % ((time.time() - t) * 1e3), flush=True)
-        print("  ", {k2: (round(v["ms"], 2), v["launches"]) for k2, v in curv.profile_end().items()})
+        print("  ", {k2: (round(v["ms"], 2), v["launches"], round(v["flops"] / v["ms"] / 1e9, 1) if v["flops"] else None, round(v["bytes"] / v["ms"] / 1e6, 1) if v["bytes"] else None) for k2, v in curv.profile_end().items()})
         lamc = lam.cpu()
         print("   lambda[:5]", lamc[:5].tolist(), "lambda[-3:]", lamc[-3:].tolist())
         qtq = q.T @ q
