@@ -27,10 +27,13 @@ using namespace ck;
 
 thread_local std::string g_err;
 
+void trim_pool();
+
 template <class F>
 int guard(F&& f) {
     try {
         f();
+        trim_pool();
         return kOk;
     } catch (const CurvError& e) {
         g_err = e.what();
@@ -42,6 +45,24 @@ int guard(F&& f) {
         g_err = e.what();
         return kRuntimeError;
     }
+}
+
+// bytes of pool memory kept mapped between calls (CURVKIT_POOL_KEEP_GB,
+// default 16): a host that re-runs config-4 sized calls keeps its J mapped
+size_t pool_keep_bytes() {
+    static const size_t keep = [] {
+        const char* e = getenv("CURVKIT_POOL_KEEP_GB");
+        const double gb = e ? atof(e) : 16.0;
+        return (size_t)((gb > 0 ? gb : 0.0) * double(1ull << 30));
+    }();
+    return keep;
+}
+
+void trim_pool() {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, pool_keep_bytes());
 }
 
 [[noreturn]] void contract(const std::string& m) { throw CurvError(kContractError, m); }
@@ -109,10 +130,11 @@ void check_memory_cap(int64_t p, int64_t cap, const char* who) {  // curvature.c
                  std::to_string(cap) + "; use the matrix-free eigensolvers instead");
 }
 
-// Keep up to 16 GB of the stream-ordered pool mapped between calls: the
-// curvature workspaces (profiles, extended tiles, J for moderate P) would
-// otherwise be returned to the driver at every synchronisation and re-mapped
-// on the next call; giant one-off buffers (an 84 GB J) are still released.
+// Never release the stream-ordered pool at synchronisation points inside a
+// call: a sync while an 84 GB J is live would otherwise unmap every freed
+// workspace and re-map it on the next allocation.  Keep up to 16 GB mapped
+// between calls (curvature workspaces are reused); trim_pool returns the
+// rest once the call's frees have completed.
 void keep_pool_memory() {
     static bool done[64] = {};
     int dev = 0;
@@ -120,7 +142,7 @@ void keep_pool_memory() {
     if (dev < 64 && done[dev]) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = uint64_t(16) << 30;
+        uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     if (dev < 64) done[dev] = true;
@@ -618,7 +640,8 @@ int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t ld
         EpiStore<float> e{c, ldc, 0, alpha, 0.f};
         Opnd<float> A = a_kmajor ? kmaj(a, lda) : mnmaj(a, lda);
         Opnd<float> B = b_kmajor ? kmaj(b, ldb) : mnmaj(b, ldb);
-        CurvGemm<float, EpiStore<float>>::run(precision, s, m, n, k, A, B, e);
+        if (precision == kTF32 || precision == k3xTF32) gemm_tf32_store(precision, s, m, n, k, A, B, c, ldc, alpha);
+        else CurvGemm<float, EpiStore<float>>::run(precision, s, m, n, k, A, B, e);
     });
 }
 

@@ -16,11 +16,14 @@
 #pragma once
 
 #include <algorithm>
+#include <memory>
 #include <numeric>
 #include <vector>
 
 #include "common.cuh"
 #include "curvature.cuh"
+#include "gemm_tc.cuh"
+#include "kr.cuh"
 #include "gemm_simt.cuh"
 #include "model.cuh"
 
@@ -80,10 +83,18 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ Y, int6
 }
 
 // In-place upper Cholesky W = R^T R and Rinv = R^{-1}, one CTA (l <= 1024).
-// A diagonal shift keeps rank-deficient Grams factorisable.
-__global__ void chol_inv_kernel(double* W, int64_t l, double shift, double* Rinv) {
-    extern __shared__ double col[];
+// A diagonal shift rel * trace(W) / l keeps rank-deficient Grams
+// factorisable (shifted CholeskyQR); it is formed here, not on the host.
+__global__ void chol_inv_kernel(double* W, int64_t l, double rel, double* Rinv) {
+    __shared__ double shift_s;
     const int t = threadIdx.x;
+    if (t == 0) {
+        double tr = 0.0;
+        for (int64_t i = 0; i < l; ++i) tr += W[i * l + i];
+        shift_s = rel * tr / (double)l;
+    }
+    __syncthreads();
+    const double shift = shift_s;
     for (int64_t i = t; i < l; i += blockDim.x) W[i * l + i] += shift;
     __syncthreads();
     // right-looking Cholesky on the upper triangle (row-major W)
@@ -112,86 +123,140 @@ __global__ void chol_inv_kernel(double* W, int64_t l, double shift, double* Rinv
     }
 }
 
-// Parallel cyclic Jacobi on a symmetric l x l matrix in one CTA: each round
-// rotates l/2 disjoint (p, q) pairs of a round-robin tournament; a warp
-// lane per pair computes the rotation, all threads apply it.
-__global__ void jacobi_kernel(double* A, double* V, int64_t l, int max_sweeps, int* sweeps_out) {
+// Parallel cyclic Jacobi on a symmetric l x l matrix in one CTA (blockDim
+// 128 x 8): each round rotates the l/2 disjoint (p, q) pairs of a round-robin
+// tournament; a thread per pair computes the rotation, all threads apply it
+// (threadIdx.x walks the matrix index, threadIdx.y the pairs).  A lives in
+// shared memory at an odd pitch when it fits (conflict-free column access);
+// the eigenvectors are kept transposed (Vt row p = eigenvector p) so every
+// rotation update is a pair of contiguous rows.  A rotation is skipped once
+// |a_pq| is at fp64 roundoff of its diagonal pair (|a_pq| <= 1e-15
+// sqrt|a_pp a_qq|, or below 1e-18 ||A||_F); a sweep without rotations ends
+// the iteration (the threshold Jacobi method).  Out: A's diagonal holds the
+// eigenvalues, V (l x l, row-major) the eigenvectors by columns.
+__global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int l, int max_sweeps,
+                                                      int* sweeps_out, int a_in_smem) {
     extern __shared__ double sh[];
-    const int64_t m = l + (l & 1);  // pad to even with a dummy index
-    double* cs = sh;                // cos per pair
-    double* sn = sh + m / 2;        // sin per pair
+    const int m = l + (l & 1);  // pad to even with a dummy index
+    const int np = m / 2;
+    double* cs = sh;            // cos per pair
+    double* sn = sh + np;       // sin per pair
     int* pp = reinterpret_cast<int*>(sh + m);
-    int* qq = pp + m / 2;
-    __shared__ double off_s;
-    const int t = threadIdx.x, nt = blockDim.x;
-    for (int64_t i = t; i < l * l; i += nt) V[i] = (i / l == i % l) ? 1.0 : 0.0;
+    int* qq = pp + np;
+    const int lda = a_in_smem ? l + ((l + 1) & 1) : l;  // odd pitch in shared memory
+    double* A = a_in_smem ? sh + m + np + 1 : Ag;
+    double* Vt = V;  // transposed during the iteration
+    __shared__ int nrot;
+    __shared__ double red[32];
+    const int tx = threadIdx.x, ty = threadIdx.y, t = ty * blockDim.x + tx, nt = blockDim.x * blockDim.y;
+    double part = 0.0;
+    for (int r = ty; r < l; r += blockDim.y)
+        for (int c = tx; c < l; c += blockDim.x) {
+            const double v = Ag[r * l + c];
+            part += v * v;
+            if (a_in_smem) A[r * lda + c] = v;
+            Vt[r * l + c] = r == c ? 1.0 : 0.0;
+        }
+    for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    if ((t & 31) == 0) red[t >> 5] = part;
     __syncthreads();
-    double fro = 0.0;
-    for (int64_t i = 0; i < l * l; ++i) fro += A[i] * A[i];
-    const double tol = 1e-15 * sqrt(fro > 1e-300 ? fro : 1e-300);
+    if (t == 0) {
+        double f = 0.0;
+        for (int w = 0; w < nt / 32; ++w) f += red[w];
+        red[0] = sqrt(f);
+    }
+    __syncthreads();
+    const double tiny = 1e-18 * red[0];
     int sweep = 0;
     for (; sweep < max_sweeps; ++sweep) {
-        if (t == 0) {
-            double s = 0.0;
-            for (int64_t i = 0; i < l; ++i)
-                for (int64_t j = 0; j < l; ++j)
-                    if (i != j) s += A[i * l + j] * A[i * l + j];
-            off_s = sqrt(s);
-        }
+        if (t == 0) nrot = 0;
         __syncthreads();
-        if (off_s <= tol) break;
-        for (int64_t round = 0; round < m - 1; ++round) {
-            for (int64_t k = t; k < m / 2; k += nt) {
+        for (int round = 0; round < m - 1; ++round) {
+            for (int k = t; k < np; k += nt) {
                 // circle method: index 0 fixed, others rotate
-                auto pos = [&](int64_t x) -> int64_t { return x == 0 ? 0 : 1 + (x - 1 + round) % (m - 1); };
-                int64_t a = pos(k), b = pos(m - 1 - k);
-                if (a > b) { const int64_t tmp = a; a = b; b = tmp; }
-                pp[k] = (int)a;
-                qq[k] = (int)b;
+                const int x0 = k, x1 = m - 1 - k;
+                int a = x0 == 0 ? 0 : 1 + (x0 - 1 + round) % (m - 1);
+                int b = x1 == 0 ? 0 : 1 + (x1 - 1 + round) % (m - 1);
+                if (a > b) { const int tmp = a; a = b; b = tmp; }
+                pp[k] = a;
+                qq[k] = b;
                 double c = 1.0, s = 0.0;
                 if (b < l) {
-                    const double apq = A[a * l + b];
-                    if (apq != 0.0) {
-                        const double h = A[b * l + b] - A[a * l + a];
-                        const double th = 0.5 * h / apq;
+                    const double apq = A[a * lda + b], app = A[a * lda + a], aqq = A[b * lda + b];
+                    if (fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), tiny)) {
+                        const double th = 0.5 * (aqq - app) / apq;
                         double tt = 1.0 / (fabs(th) + sqrt(1.0 + th * th));
                         if (th < 0.0) tt = -tt;
                         c = 1.0 / sqrt(1.0 + tt * tt);
                         s = tt * c;
+                        atomicAdd(&nrot, 1);
                     }
                 }
                 cs[k] = c;
                 sn[k] = s;
             }
             __syncthreads();
-            // A <- A J (columns), V <- V J
-            for (int64_t idx = t; idx < (m / 2) * l; idx += nt) {
-                const int64_t k = idx / l, i = idx % l;
-                const int64_t a = pp[k], b = qq[k];
-                if (b >= l) continue;
-                const double c = cs[k], s = sn[k];
-                const double x = A[i * l + a], y = A[i * l + b];
-                A[i * l + a] = c * x - s * y;
-                A[i * l + b] = s * x + c * y;
-                const double vx = V[i * l + a], vy = V[i * l + b];
-                V[i * l + a] = c * vx - s * vy;
-                V[i * l + b] = s * vx + c * vy;
+            // A <- A J (columns a, b), Vt <- J^T Vt (rows a, b)
+            for (int k = ty; k < np; k += blockDim.y) {
+                const double s = sn[k];
+                if (s == 0.0) continue;
+                const int a = pp[k], b = qq[k];
+                const double c = cs[k];
+                for (int i = tx; i < l; i += blockDim.x) {
+                    const double x = A[i * lda + a], y = A[i * lda + b];
+                    A[i * lda + a] = c * x - s * y;
+                    A[i * lda + b] = s * x + c * y;
+                    const double vx = Vt[a * l + i], vy = Vt[b * l + i];
+                    Vt[a * l + i] = c * vx - s * vy;
+                    Vt[b * l + i] = s * vx + c * vy;
+                }
             }
             __syncthreads();
-            // A <- J^T A (rows)
-            for (int64_t idx = t; idx < (m / 2) * l; idx += nt) {
-                const int64_t k = idx / l, i = idx % l;
-                const int64_t a = pp[k], b = qq[k];
-                if (b >= l) continue;
-                const double c = cs[k], s = sn[k];
-                const double x = A[a * l + i], y = A[b * l + i];
-                A[a * l + i] = c * x - s * y;
-                A[b * l + i] = s * x + c * y;
+            // A <- J^T A (rows a, b)
+            for (int k = ty; k < np; k += blockDim.y) {
+                const double s = sn[k];
+                if (s == 0.0) continue;
+                const int a = pp[k], b = qq[k];
+                const double c = cs[k];
+                for (int i = tx; i < l; i += blockDim.x) {
+                    const double x = A[a * lda + i], y = A[b * lda + i];
+                    A[a * lda + i] = c * x - s * y;
+                    A[b * lda + i] = s * x + c * y;
+                }
             }
             __syncthreads();
         }
+        if (nrot == 0) break;
+        __syncthreads();
     }
+    if (a_in_smem)
+        for (int r = ty; r < l; r += blockDim.y)
+            for (int c = tx; c < l; c += blockDim.x) Ag[r * l + c] = A[r * lda + c];
+    __syncthreads();
+    // Vt -> V in place (swap across the diagonal)
+    for (int r = ty; r < l; r += blockDim.y)
+        for (int c = tx; c < r; c += blockDim.x) {
+            const double x = Vt[r * l + c];
+            Vt[r * l + c] = Vt[c * l + r];
+            Vt[c * l + r] = x;
+        }
     if (t == 0) *sweeps_out = sweep;
+}
+
+// one-CTA symmetric eigensolve of the l x l matrix A (in place: diagonal =
+// eigenvalues, V = eigenvectors by columns)
+inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_t s) {
+    const int64_t m = l + (l & 1);
+    const size_t base = (size_t)(m + m / 2 + 1) * sizeof(double);
+    const size_t with_a = base + (size_t)l * (l + 1) * sizeof(double);
+    const bool smem_a = with_a <= 200 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    jacobi_kernel<<<1, dim3(128, 8), smem_a ? with_a : base, s>>>(A, V, (int)l, 60, sweeps, smem_a ? 1 : 0);
+    CK_LAUNCH();
 }
 
 template <class U>
@@ -205,34 +270,30 @@ struct EigenWork {
     const ModelDesc& md;
     cudaStream_t s;
     int prec;
+    const Cache<T>* c = nullptr;
+    const KrOperands* kr = nullptr;  // set: J X / J^T T from the activations (J never formed)
 
-    // Y <- orth(Y) in place (CholeskyQR2), Y is rows x l with ld
-    void orth(T* Y, int64_t rows, int64_t l, int64_t ld) {
-        ProfScope ps("eig_orth", s, 2.0 * 2.0 * 2.0 * (double)rows * l * l, 0.0);
+    // Y <- orth(Y) (CholeskyQR2, fp64 Gram): pass 1 writes Y Rinv into the
+    // scratch Y2, pass 2 writes back into Y; no host round trip
+    void orth(T* Y, T* Y2, int64_t rows, int64_t l, int64_t ld) {
+        ProfScope ps("eig_orth", s, 2.0 * 2.0 * 2.0 * (double)rows * l * l, 2.0 * 2.0 * 2.0 * sizeof(T) * rows * ld);
         DevMem W((size_t)l * l * sizeof(double), s), Rinv((size_t)l * l * sizeof(double), s);
-        DevMem Rt((size_t)l * l * sizeof(T), s), Y2((size_t)rows * ld * sizeof(T), s);
+        DevMem Rt((size_t)l * l * sizeof(T), s);
+        T* src = Y;
+        T* dst = Y2;
         for (int pass = 0; pass < 2; ++pass) {
             CK_CUDA(cudaMemsetAsync(W.p, 0, l * l * sizeof(double), s));
             const int64_t ksplit = std::min<int64_t>(256, std::max<int64_t>(1, rows / 4096));
             const int64_t chunk = ceil_div(rows, ksplit);
             dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
-            gram_kernel<T><<<g, 256, 0, s>>>(Y, ld, rows, l, chunk, dptr<double>(W));
+            gram_kernel<T><<<g, 256, 0, s>>>(src, ld, rows, l, chunk, dptr<double>(W));
             CK_LAUNCH();
-            // shift ~ eps * trace keeps the factorisation defined when Y is
-            // numerically rank deficient (shifted CholeskyQR)
-            std::vector<double> hw(l * l);
-            CK_CUDA(cudaMemcpyAsync(hw.data(), W.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
-            CK_CUDA(cudaStreamSynchronize(s));
-            double tr = 0.0;
-            for (int64_t i = 0; i < l; ++i) tr += hw[i * l + i];
-            const double shift = (sizeof(T) == 4 ? 1e-7 : 1e-14) * tr / (double)l;
-            chol_inv_kernel<<<1, 256, 0, s>>>(dptr<double>(W), l, shift, dptr<double>(Rinv));
+            chol_inv_kernel<<<1, 256, 0, s>>>(dptr<double>(W), l, sizeof(T) == 4 ? 1e-7 : 1e-14, dptr<double>(Rinv));
             CK_LAUNCH();
             convert_to<T>(dptr<double>(Rinv), dptr<T>(Rt), l * l);
-            // Y2 = Y Rinv ; copy back
-            EpiStore<T> e{dptr<T>(Y2), ld, 0, T(1), T(0)};
-            gemm_simt<T>(s, rows, l, l, 1, kmaj(Y, ld), mnmaj(dptr<T>(Rt), l), e);
-            CK_CUDA(cudaMemcpyAsync(Y, Y2.p, (size_t)rows * ld * sizeof(T), cudaMemcpyDeviceToDevice, s));
+            EpiStore<T> e{dst, ld, 0, T(1), T(0)};
+            gemm_simt<T>(s, rows, l, l, 1, kmaj(src, ld), mnmaj(dptr<T>(Rt), l), e);
+            std::swap(src, dst);
         }
     }
 
@@ -244,15 +305,32 @@ struct EigenWork {
 
     // T_out (n x l) = J X ; X is P x l (ld lx)
     void apply_j(const T* J, int64_t ldj, int64_t n, const T* X, int64_t ldx, int64_t l, T* Tout, int64_t ldt) {
-        ProfScope ps("eig_apply_j", s, 2.0 * (double)n * md.P * l, (double)sizeof(T) * n * md.P);
+        ProfScope ps("eig_apply_j", s, 2.0 * (double)n * md.P * l, kr ? 0.0 : (double)sizeof(T) * n * md.P);
+        if constexpr (std::is_same_v<T, float>) {
+            if (kr) {
+                kr_apply_j(md, *c, *kr, X, ldx, l, Tout, ldt, s);
+                return;
+            }
+            if (prec == kTF32 || prec == k3xTF32) {  // split-K: only ceil(N/256) row tiles
+                gemm_tf32_store(prec, s, n, l, md.P, read_once(pre_rounded(kmaj(J, ldj))), mnmaj(X, ldx), Tout,
+                                ldt);
+                return;
+            }
+        }
         EpiStore<T> e{Tout, ldt, 0, T(1), T(0)};
         CurvGemm<T, EpiStore<T>>::run(prec, s, n, l, md.P, pre_rounded(kmaj(J, ldj)), mnmaj(X, ldx), e);
     }
     // Y (P x l) = J^T Tn ; Tn is n x l
     void apply_jt(const T* J, int64_t ldj, int64_t n, const T* Tn, int64_t ldt, int64_t l, T* Y, int64_t ldy) {
-        ProfScope ps("eig_apply_jt", s, 2.0 * (double)n * md.P * l, (double)sizeof(T) * n * md.P);
+        ProfScope ps("eig_apply_jt", s, 2.0 * (double)n * md.P * l, kr ? 0.0 : (double)sizeof(T) * n * md.P);
+        if constexpr (std::is_same_v<T, float>) {
+            if (kr) {
+                kr_apply_jt(md, *c, *kr, Tn, ldt, l, Y, ldy, s);
+                return;
+            }
+        }
         EpiStore<T> e{Y, ldy, 0, T(1), T(0)};
-        CurvGemm<T, EpiStore<T>>::run(prec, s, md.P, l, n, pre_rounded(mnmaj(J, ldj)), mnmaj(Tn, ldt), e);
+        CurvGemm<T, EpiStore<T>>::run(prec, s, md.P, l, n, read_once(pre_rounded(mnmaj(J, ldj))), mnmaj(Tn, ldt), e);
     }
 };
 
@@ -267,26 +345,34 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     if (oversample < 0 || power_iters < 0) throw CurvError(kContractError, "opg_topk: negative oversample/power_iters");
     const int64_t l = std::min(k + oversample, P);
     const int64_t ldl = round_up(l, 32);
-    // per-example gradients stay resident in HBM
-    const int64_t ldj = round_up(P, 32);
+    // TF32: J X and J^T T straight from the activations and deltas (kr.cuh);
+    // otherwise the per-example gradients are formed once and stay in HBM
+    std::unique_ptr<KrOperands> krop;
+    if constexpr (std::is_same_v<T, float>)
+        if (prec == kTF32 && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
+    const int64_t ldj = krop ? 0 : round_up(P, 32);
     DevMem J((size_t)n * ldj * sizeof(T), s);
-    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
-    DevMem Y((size_t)P * ldl * sizeof(T), s), Om((size_t)P * ldl * sizeof(T), s);
+    if (!krop) jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
+    DevMem Y((size_t)P * ldl * sizeof(T), s), Om((size_t)P * ldl * sizeof(T), s), Y2((size_t)P * ldl * sizeof(T), s);
     DevMem Tn((size_t)n * ldl * sizeof(T), s);
-    CK_CUDA(cudaMemsetAsync(Om.p, 0, (size_t)P * ldl * sizeof(T), s));
-    gaussian_kernel<T><<<blocks_for(P * l), 256, 0, s>>>(dptr<T>(Om), P, l, ldl, seed);
-    CK_LAUNCH();
-    EigenWork<T> ew{md, s, prec};
+    {
+        ProfScope ps("eig_sketch", s, 0.0, (double)sizeof(T) * P * ldl);
+        CK_CUDA(cudaMemsetAsync(Om.p, 0, (size_t)P * ldl * sizeof(T), s));
+        gaussian_kernel<T><<<blocks_for(P * l), 256, 0, s>>>(dptr<T>(Om), P, l, ldl, seed);
+        CK_LAUNCH();
+    }
+    EigenWork<T> ew{md, s, prec, &c, krop.get()};
     T* X = dptr<T>(Om);
     for (int64_t it = 0; it <= power_iters; ++it) {
         ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
         ew.apply_jt(dptr<T>(J), ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
-        ew.orth(dptr<T>(Y), P, l, ldl);
+        ew.orth(dptr<T>(Y), dptr<T>(Y2), P, l, ldl);
         X = dptr<T>(Y);
     }
     // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q) with round-to-nearest TF32
     // operands (J stored rounded, Q rounded per GEMM): unbiased products.
     ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+    ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l + 2.0 * (double)P * l * k, 0.0);
     DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
     CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));
     {
@@ -295,16 +381,14 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         gram_kernel<T><<<g, 256, 0, s>>>(dptr<T>(Tn), ldl, n, l, ceil_div(n, ksplit), dptr<double>(B));
         CK_LAUNCH();
     }
+    ProfScope pj("eig_ritz_eig", s, 0.0, 0.0);
     std::vector<double> hb(l * l);
     CK_CUDA(cudaMemcpyAsync(hb.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
     for (auto& v : hb) v /= (double)n;
     CK_CUDA(cudaMemcpyAsync(B.p, hb.data(), l * l * sizeof(double), cudaMemcpyHostToDevice, s));
     DevMem sw(sizeof(int), s);
-    const int64_t m = l + (l & 1);
-    jacobi_kernel<<<1, 1024, (size_t)m * sizeof(double) + (size_t)m * sizeof(int), s>>>(dptr<double>(B), dptr<double>(V),
-                                                                                      l, 60, dptr<int>(sw));
-    CK_LAUNCH();
+    jacobi_eig(dptr<double>(B), dptr<double>(V), l, dptr<int>(sw), s);
     std::vector<double> ha(l * l), hv(l * l);
     CK_CUDA(cudaMemcpyAsync(ha.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaMemcpyAsync(hv.data(), V.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -318,6 +402,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         lam_host[j] = ha[ord[j] * l + ord[j]];
         for (int64_t r = 0; r < l; ++r) vk[r * k + j] = (T)hv[r * l + ord[j]];
     }
+    pj.end();
     DevMem Vk((size_t)l * k * sizeof(T), s);
     CK_CUDA(cudaMemcpyAsync(Vk.p, vk.data(), l * k * sizeof(T), cudaMemcpyHostToDevice, s));
     EpiStore<T> e{q_dev, k, 0, T(1), T(0)};

@@ -19,11 +19,18 @@ struct Opnd {
     int kmajor = 1;
     int64_t bstride = 0;  // batch stride in elements
     int rounded = 0;      // values already rounded to TF32 by their producer
+    int once = 0;         // every element read by one tile only (L2 evict_first)
 };
 
 template <class T>
 inline Opnd<T> pre_rounded(Opnd<T> o) {
     o.rounded = 1;
+    return o;
+}
+
+template <class T>
+inline Opnd<T> read_once(Opnd<T> o) {
+    o.once = 1;
     return o;
 }
 

@@ -162,7 +162,15 @@ struct TcShape {
     uint32_t mn_lbo, mn_sbo, mn_kstep;  // MN-major descriptor strides (bytes)
     uint32_t mn_layout;                 // MN-major descriptor layout type
     int a_3d, b_3d;                     // MN-major operand loaded by one 3D TMA box
+    int ksplit = 1;                     // pair kernel: K slabs per tile (Epi::block_split)
+    int a_once = 0, b_once = 0;         // streamed operand: L2 evict_first
 };
+
+// Epilogues that take a K-slab index (split-K partial products)
+template <class E, class = void>
+struct EpiSplitK : std::false_type {};
+template <class E>
+struct EpiSplitK<E, std::void_t<decltype(E::kSplitK)>> : std::true_type {};
 
 template <int BN>
 struct TcSmem {
@@ -401,6 +409,12 @@ __device__ __forceinline__ uint64_t evict_last_policy() {
     return p;
 }
 
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void tma2_2d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
                                         int32_t c1, uint64_t pol) {
     asm volatile(
@@ -511,6 +525,16 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const int64_t mt = ceil_div(sh.M, 256), nt = ceil_div(sh.N, BN);
     const int64_t ntiles = mt * nt;
     const int64_t nk = ceil_div(sh.K, BK);
+    // work unit t = (K slab t / ntiles, tile t % ntiles): concurrent units
+    // share a K slab, so the B rows they stream stay in L2
+    const int64_t ksl = sh.ksplit > 1 ? sh.ksplit : 1;
+    const int64_t nunits = ntiles * ksl;
+    const int64_t kcb = ceil_div(nk, ksl);
+    auto unit_of = [&](int64_t t, int64_t& mi, int64_t& ni, int64_t& kb0, int64_t& kb1) {
+        tile_coords(t % ntiles, mt, nt, mi, ni);
+        kb0 = (t / ntiles) * kcb;
+        kb1 = ::min(nk, kb0 + kcb);
+    };
 
     if (warp == 0 && lane == 0) {
         prefetch_map(&mapA);
@@ -547,15 +571,16 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t bytes_leader = (uint32_t)(2 * STAGE_BYTES);
-            const uint64_t pol = evict_last_policy();
-            for (int64_t t = pair_id; t < ntiles; t += npairs) {
-                int64_t mi, ni;
-                tile_coords(t, mt, nt, mi, ni);
+            const uint64_t keep = evict_last_policy(), stream = evict_first_policy();
+            const uint64_t pa = sh.a_once ? stream : keep, pb = sh.b_once ? stream : keep;
+            for (int64_t t = pair_id; t < nunits; t += npairs) {
+                int64_t mi, ni, kb0, kb1;
+                unit_of(t, mi, ni, kb0, kb1);
                 const int64_t m0 = mi * 256, n0 = ni * BN;
                 if (epi.skip(0, m0, n0, 256, BN)) continue;
                 const int64_t half = tile_ntile(n0) / 2;
                 const int64_t am0 = m0 + 128 * rank, bn0 = n0 + half * rank;
-                for (int64_t kb = 0; kb < nk; ++kb) {
+                for (int64_t kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
                     if (rank == 0) mbar_expect_tx_cluster(&full[stage], bytes_leader);
@@ -563,11 +588,11 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     uint8_t* sa = stage_base + stage * STAGE_BYTES;
                     uint8_t* sb = sa + S::A_BYTES * split;
                     const int64_t k0 = kb * BK;
-                    load_tile2<128>(sa, &mapA, fb, sh.a_mn, sh.a_3d, am0, k0, pol);
-                    load_tile2<BN / 2>(sb, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0, pol);
+                    load_tile2<128>(sa, &mapA, fb, sh.a_mn, sh.a_3d, am0, k0, pa);
+                    load_tile2<BN / 2>(sb, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0, pb);
                     if (split == 2) {
-                        load_tile2<128>(sa + S::A_BYTES, &mapAlo, fb, sh.a_mn, sh.a_3d, am0, k0, pol);
-                        load_tile2<BN / 2>(sb + S::B_BYTES, &mapBlo, fb, sh.b_mn, sh.b_3d, bn0, k0, pol);
+                        load_tile2<128>(sa + S::A_BYTES, &mapAlo, fb, sh.a_mn, sh.a_3d, am0, k0, pa);
+                        load_tile2<BN / 2>(sb + S::B_BYTES, &mapBlo, fb, sh.b_mn, sh.b_3d, bn0, k0, pb);
                     }
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
@@ -579,16 +604,16 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t t = pair_id; t < ntiles; t += npairs) {
-                int64_t mi, ni;
-                tile_coords(t, mt, nt, mi, ni);
+            for (int64_t t = pair_id; t < nunits; t += npairs) {
+                int64_t mi, ni, kb0, kb1;
+                unit_of(t, mi, ni, kb0, kb1);
                 const int64_t m0 = mi * 256, n0 = ni * BN;
                 if (epi.skip(0, m0, n0, 256, BN)) continue;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t idesc = idesc2_tf32(tile_ntile(n0), sh.a_mn, sh.b_mn);
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
-                for (int64_t kb = 0; kb < nk; ++kb) {
+                for (int64_t kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
@@ -602,7 +627,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         const uint32_t alay = sh.a_mn ? sh.mn_layout : 2, blay = sh.b_mn ? sh.mn_layout : 2;
                         const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
                         const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
-                        mma2_tf32(d, ahi, bhi, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        mma2_tf32(d, ahi, bhi, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                         if (split == 2) {
                             mma2_tf32(d, ahi, smem_desc(sb + S::B_BYTES + boff, blbo, bsbo, blay), idesc, 1u);
                             mma2_tf32(d, smem_desc(sa + S::A_BYTES + aoff, albo, asbo, alay), bhi, idesc, 1u);
@@ -623,9 +648,9 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t t = pair_id; t < ntiles; t += npairs) {
-            int64_t mi, ni;
-            tile_coords(t, mt, nt, mi, ni);
+        for (int64_t t = pair_id; t < nunits; t += npairs) {
+            int64_t mi, ni, kb0, kb1;
+            unit_of(t, mi, ni, kb0, kb1);
             const int64_t m0 = mi * 256, n0 = ni * BN;
             if (epi.skip(0, m0, n0, 256, BN)) continue;
             mbar_wait_cluster(&tfull[acc], acc_phase);
@@ -638,7 +663,10 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
                 if (row0 < sh.M) {
                     stage_block(buf, v, lane);
-                    epi.block(row0, col0, sh.M, sh.N, buf, v, lane);
+                    if constexpr (EpiSplitK<Epi>::value)
+                        epi.block_split((int)(t / ntiles), row0, col0, sh.M, sh.N, buf, v, lane);
+                    else
+                        epi.block(row0, col0, sh.M, sh.N, buf, v, lane);
                     __syncwarp();
                 }
             }
@@ -1049,7 +1077,7 @@ void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const 
                                      std::max(S::bytes(1), S::bytes(3))));
         attr_set = true;
     }
-    const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN);
+    const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN) * std::max(1, sh.ksplit);
     const int grid = 2 * (int)std::min<int64_t>(tiles, num_sms() / 2);
     pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, sh, e);
     CK_LAUNCH();
@@ -1060,7 +1088,7 @@ void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const 
 // TF32 tensor-core GEMM with the generic epilogue contract (Epi::block).
 template <class Epi>
 void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<float> A, Opnd<float> B,
-               const Epi& e) {
+               const Epi& e, int ksplit = 1) {
     if (M <= 0 || N <= 0) return;
     // MN-major 32-bit operands use the 128B swizzle with 32B atoms
     // (SWIZZLE_128B_BASE32B, TMA SWIZZLE_128B_ATOM_32B): LBO = stride between
@@ -1071,7 +1099,7 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     const int a3 = (!A.kmajor && A.ld >= round_up(M, 32)) ? 1 : 0;
     const int b3 = (!B.kmajor && B.ld >= round_up(N, 32)) ? 1 : 0;
     tc::TcShape sh{M, N, K, A.kmajor ? 0 : 1, B.kmajor ? 0 : 1, prec == k3xTF32 ? 3 : 1,
-                   (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, a3, b3};
+                   (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, a3, b3, ksplit, A.once, B.once};
     const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
     DevMem alo, blo, ahi, bhi;
     const float* pa = A.p;
@@ -1125,7 +1153,8 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     // CTA-pair (cta_group::2) tiles of 256 x bn when M gives every pair work;
     // each CTA then stages only bn/2 rows of B.
     static const bool no_pair = getenv("CURVKIT_NO_PAIR") != nullptr;
-    const bool use_pair = !no_pair && bn >= 128 && M >= 512;
+    const bool use_pair = (!no_pair && bn >= 128 && M >= 512) || ksplit > 1;
+    if (ksplit > 1 && (bn < 128 || M < 512)) throw CurvError(kRuntimeError, "split-K needs the CTA-pair kernel");
     const int box_b = use_pair ? bn / 2 : bn;
     CUtensorMap ma = tc::make_map(pa, M, K, A.ld, sh.a_mn, tc::BM, a3);
     CUtensorMap mb = tc::make_map(pb, N, K, B.ld, sh.b_mn, box_b, b3);
@@ -1139,6 +1168,70 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     if (bn == 256) tc::launch<256>(s, sh, ma, mb, mal, mbl, e);
     else if (bn == 128) tc::launch<128>(s, sh, ma, mb, mal, mbl, e);
     else tc::launch<64>(s, sh, ma, mb, mal, mbl, e);
+}
+
+namespace tc {
+// K-slab partial products: slab k of the workspace holds the tile products
+// over its K range (plain stores, no atomics)
+struct EpiSlab {
+    static constexpr bool kSplitK = true;
+    float* ws;
+    int64_t ldw, slab;
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ void operator()(int, int64_t, int64_t, float) const {}
+    __device__ void block_split(int k, int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36],
+                                const float* v, int lane) const {
+        EpiStore<float>{ws + k * slab, ldw, 0, 1.f, 0.f}.block(row0, col0, M, N, buf, v, lane);
+    }
+    __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float* v,
+                          int lane) const {
+        block_split(0, row0, col0, M, N, buf, v, lane);
+    }
+};
+
+// C = sum over slabs in fixed order (deterministic), 4 columns per thread
+__global__ void slab_sum_kernel(const float* __restrict__ ws, int64_t ldw, int64_t slab, int nslab, int64_t M,
+                                int64_t N, float alpha, float* __restrict__ C, int64_t ldc) {
+    const int64_t nq = ldw / 4;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M * nq) return;
+    const int64_t r = i / nq, c = (i % nq) * 4;
+    if (c >= N) return;
+    float4 acc = __ldcs(reinterpret_cast<const float4*>(ws + r * ldw + c));
+    for (int k = 1; k < nslab; ++k) {
+        const float4 x = __ldcs(reinterpret_cast<const float4*>(ws + k * slab + r * ldw + c));
+        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    for (int u = 0; u < 4 && c + u < N; ++u) C[r * ldc + c + u] = alpha * a[u];
+}
+}  // namespace tc
+
+// C (M x N, ldc) = A B on the tensor cores.  When the tile grid alone leaves
+// most SM pairs idle (short M, long K: J X with M = N examples) K is cut into
+// slabs whose partial tiles are summed afterwards in fixed order.
+inline void gemm_tf32_store(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<float> A,
+                            Opnd<float> B, float* C, int64_t ldc, float alpha = 1.f) {
+    const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
+    const int64_t pairs = tc::num_sms() / 2;
+    const int64_t tiles = ceil_div(M, 256) * ceil_div(N, bn);
+    const int64_t nk = ceil_div(K, tc::BK);
+    int64_t ks = 1;
+    if (bn >= 128 && M >= 512 && tiles < pairs && nk >= 64) {
+        const int64_t target = std::min<int64_t>(ceil_div(8 * pairs, tiles), nk / 16);
+        const int64_t kcb = ceil_div(nk, target);
+        ks = ceil_div(nk, kcb);  // every slab non-empty
+    }
+    if (ks <= 1) {
+        gemm_tf32(prec, s, M, N, K, A, B, EpiStore<float>{C, ldc, 0, alpha, 0.f});
+        return;
+    }
+    const int64_t ldw = round_up(N, 4), slab = M * ldw;
+    DevMem ws((size_t)(ks * slab) * sizeof(float), s);
+    gemm_tf32(prec, s, M, N, K, A, B, tc::EpiSlab{dptr<float>(ws), ldw, slab}, (int)ks);
+    tc::slab_sum_kernel<<<(unsigned)ceil_div(M * (ldw / 4), 256), 256, 0, s>>>(dptr<float>(ws), ldw, slab, (int)ks,
+                                                                              M, N, alpha, C, ldc);
+    CK_LAUNCH();
 }
 
 // Fused Hessian block (TF32 only): weight-tangent rows of block (k, m) with

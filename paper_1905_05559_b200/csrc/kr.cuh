@@ -1,0 +1,510 @@
+// kr.cuh -- J X and J^T T for the randomized top-k OPG eigensolver without
+// ever forming J (the N x P matrix of per-example gradients).
+//
+// Row n of J restricted to layer k's weights is the Khatri-Rao (row-wise
+// Kronecker) product delta_k[n, :] (x) a_k[n, :] -- reference autodiff.cpp
+// accumulates exactly these outer products per example -- and its bias part
+// is delta_k[n, :].  Hence, with X_{k,o} = rows woff_k + o*T_k .. + T_k - 1
+// of X (the tangents of output unit o's incoming weights):
+//
+//   (J X)[n, c]           = sum_k sum_o delta_k[n, o] (A_k X_{k,o})[n, c]
+//                           + sum_k (delta_k Xb_k)[n, c]
+//   (J^T T)[(k,o,i), c]   = sum_n a_k[n, i] delta_k[n, o] T[n, c]
+//   (J^T T)[(k,o), c]     = (delta_k^T T)[o, c]                    (biases)
+//
+// The same flops as the dense products (2 N P l each) but the operands are
+// the activations (N x T_k) and the l-column blocks, all L2-resident, instead
+// of an N x P matrix streamed from HBM (84 GB for config 4): the products are
+// tensor-core bound instead of HBM bound, and J's allocation and generation
+// disappear.
+//
+// Both kernels are CTA-pair (cta_group::2) tcgen05 kind::tf32 GEMMs with
+// 256 x 256 tiles whose N = 256 columns are two output units o (128 columns
+// of c each, one per CTA of the pair):
+//   kr_kernel<false>  (J X): D = A_k[n-tile, :] [X_{k,o} | X_{k,o+1}]; the
+//       epilogue scales each TMEM row by delta_k[n, o] and accumulates over a
+//       chunk of o in registers, then stores one K-slab of partial sums
+//       (summed in fixed order afterwards: deterministic).
+//   kr_kernel<true>   (J^T T): D = A_k^T[i-tile, :] [delta_o . T | delta_o+1 . T];
+//       transform warps scale the TMA-loaded T tile's k-rows (examples) by
+//       delta_k[n, o] in shared memory (a 128-byte swizzle row is one k, so
+//       the scaling is swizzle-agnostic), round to nearest TF32, and hand the
+//       stage to the MMA.
+#pragma once
+
+#include "gemm_tc.cuh"
+#include "model.cuh"
+
+namespace ck {
+namespace tc {
+namespace pair {
+
+struct KrArgs {
+    int64_t mt;           // row tiles (JX: n-tiles of 256 examples; JT: i-tiles of 256 inputs)
+    int64_t nop;          // o pairs: ceil(T_{k+1} / 2)
+    int64_t chunk;        // JX: o pairs per work unit
+    int64_t nk;           // k-blocks per o pair (JX: ceil(T_k / 32); JT: ceil(n / 32))
+    int64_t tk, to, woff;  // T_k, T_{k+1}, first weight row of layer k in X / Y
+    const float* delta;    // JX: delta_k (n x ldd); JT: delta_k^T (T_{k+1} x ldd, ldd >= 32 nk)
+    int64_t ldd;
+    int64_t n;             // examples
+    float* out;            // JX: slab workspace (+ slab0 * slab); JT: Y (+ c0)
+    int64_t ldo, slab;     // JX: floats per slab
+    int64_t rows;          // JX: n ; JT: T_k
+    int64_t l;             // live columns of this 128-wide column tile
+    int64_t ksplit;        // JT: example slabs (partial Y in slab ks of out)
+};
+
+constexpr int KR_BN = 256;
+
+template <bool JT>
+struct KrCfg {
+    static constexpr int THREADS = 128 + 32 * EPI_WARPS + (JT ? 128 : 0);
+    static constexpr int A_BYTES = 128 * BK * 4;
+    static constexpr int B_BYTES = (KR_BN / 2) * BK * 4;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int EPI_BYTES = 0;  // epilogues store from registers
+    static constexpr int STAGES_ = (227 * 1024 - 1024 - EPI_BYTES - 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_ > 8 ? 8 : STAGES_;
+    static constexpr int BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 1024;
+};
+
+template <bool JT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KrCfg<JT>::THREADS, 1)
+kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, KrArgs ka,
+          uint32_t mn_lbo, uint32_t mn_sbo, uint32_t mn_kstep, int a3d, int b3d) {
+    using C = KrCfg<JT>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    constexpr int NST = C::STAGES;
+    uint8_t* stage_base = smem;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE_BYTES + C::EPI_BYTES);
+    uint64_t* full = bars;         // [8] leader: operand bytes (+ transform arrivals)
+    uint64_t* empty = bars + 8;    // [8] both CTAs (multicast commit)
+    uint64_t* bfull = bars + 16;   // [8] local: raw T tile landed (JT)
+    uint64_t* tfull = bars + 24;   // [2]
+    uint64_t* tempty = bars + 26;  // [2] leader
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cta_rank();
+    const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
+    const int64_t nchunk = JT ? ka.nop * ka.ksplit : ceil_div(ka.nop, ka.chunk);
+    const int64_t nunits = ka.mt * nchunk;
+    const int64_t kcb = JT ? ceil_div(ka.nk, ka.ksplit) : ka.nk;
+    constexpr int TW0 = 4 + EPI_WARPS;
+    // unit u -> (row tile, o-pair range, k-block range, slab); units sharing
+    // an o range run side by side, so the B operand they stream stays in L2
+    auto unit_of = [&](int64_t u, int64_t& mi, int64_t& op0, int64_t& op1, int64_t& kb0, int64_t& kb1,
+                       int64_t& slab) {
+        mi = u % ka.mt;
+        const int64_t ch = u / ka.mt;
+        if (JT) {
+            op0 = ch % ka.nop;
+            op1 = op0 + 1;
+            slab = ch / ka.nop;
+            kb0 = slab * kcb;
+            kb1 = ::min(ka.nk, kb0 + kcb);
+        } else {
+            op0 = ch * ka.chunk;
+            op1 = ::min(ka.nop, op0 + ka.chunk);
+            slab = ch;
+            kb0 = 0;
+            kb1 = ka.nk;
+        }
+    };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_map(&mapA);
+        prefetch_map(&mapB);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], JT ? 1 + 2 * 4 : 2);
+            mbar_init(&empty[s], 1);
+            mbar_init(&bfull[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "n"(2 * KR_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint64_t pol = evict_last_policy();
+            for (int64_t u = pair_id; u < nunits; u += npairs) {
+                int64_t mi, op0, op1, kb0, kb1, sl;
+                unit_of(u, mi, op0, op1, kb0, kb1, sl);
+                const int64_t r0 = mi * 256 + 128 * rank;  // this CTA's A rows
+                for (int64_t op = op0; op < op1; ++op) {
+                    const int64_t o = 2 * op + rank;         // this CTA's output unit
+                    for (int64_t kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = stage_base + stage * C::STAGE_BYTES;
+                        uint8_t* sb = sa + C::A_BYTES;
+                        const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
+                        const int64_t k0 = kb * BK;
+                        if constexpr (JT) {
+                            if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * C::A_BYTES));
+                            load_tile2<128>(sa, &mapA, fb, 1, a3d, r0, k0, pol);
+                            mbar_expect_tx(&bfull[stage], (uint32_t)C::B_BYTES);
+                            load_tile<128>(sb, &mapB, &bfull[stage], 1, b3d, 0, k0, 4);
+                        } else {
+                            if (rank == 0) mbar_expect_tx_cluster(&full[stage], (uint32_t)(2 * C::STAGE_BYTES));
+                            else mbar_arrive_cluster(fb);
+                            load_tile2<128>(sa, &mapA, fb, 0, 0, r0, k0, pol);
+                            // rows of X past this unit's T_k meet zero-filled A columns
+                            load_tile2<128>(sb, &mapB, fb, 1, b3d, 0, ka.woff + o * ka.tk + k0, pol);
+                        }
+                        if (++stage == NST) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            const uint32_t idesc = idesc2_tf32(KR_BN, JT, true);
+            for (int64_t u = pair_id; u < nunits; u += npairs) {
+                int64_t mi, op0, op1, kb0, kb1, sl;
+                unit_of(u, mi, op0, op1, kb0, kb1, sl);
+                for (int64_t op = op0; op < op1; ++op) {
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem_base + (uint32_t)(acc * KR_BN);
+                    for (int64_t kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t sa = smem_u32(stage_base + stage * C::STAGE_BYTES);
+                        const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                        for (int ks = 0; ks < BK / 8; ++ks) {
+                            const uint64_t ad = JT ? smem_desc(sa + ks * mn_kstep, mn_lbo, mn_sbo, 1)
+                                                   : smem_desc(sa + ks * 32, 16, 1024, 2);
+                            const uint64_t bd = smem_desc(sb + ks * mn_kstep, mn_lbo, mn_sbo, 1);
+                            mma2_tf32(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                        }
+                        commit2(&empty[stage]);
+                        if (++stage == NST) { stage = 0; phase ^= 1; }
+                    }
+                    commit2(&tfull[acc]);
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
+            }
+        }
+    } else if (JT && warp >= TW0) {  // ---------------- T-tile scaling (both CTAs)
+        // thread t scales the 16-byte chunks t + 128 r (r < 8) of this CTA's
+        // 16 KB T tile, so one warp instruction covers 512 contiguous bytes
+        // (no bank conflicts).  Chunk g sits in 128-byte row g / 8 = one k
+        // (example) of a 32-column atom: k = t / 8 for even r, t / 8 + 16 for odd.
+        const int t = threadIdx.x - TW0 * 32;
+        const int klo = t / 8;
+        const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t u = pair_id; u < nunits; u += npairs) {
+            int64_t mi, op0, op1, kb0, kb1, sl;
+            unit_of(u, mi, op0, op1, kb0, kb1, sl);
+            const int64_t o = 2 * op0 + rank;
+            // delta_k^T row o, eight k-blocks ahead of the stages that need them
+            const float* drow = ka.delta + (o < ka.to ? o : 0) * ka.ldd + klo;
+            const float live = o < ka.to ? 1.f : 0.f;
+            for (int64_t kbg = kb0; kbg < kb1; kbg += 8) {
+                float d0[8], d1[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const bool in = kbg + j < kb1;
+                    d0[j] = in ? live * __ldg(drow + (kbg + j) * BK) : 0.f;
+                    d1[j] = in ? live * __ldg(drow + (kbg + j) * BK + 16) : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (kbg + j >= kb1) break;
+                    mbar_wait(&bfull[stage], phase);
+                    float4* p = reinterpret_cast<float4*>(stage_base + stage * C::STAGE_BYTES + C::A_BYTES) + t;
+                    float4 x[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) x[r] = p[128 * r];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const float dv = (r & 1) ? d1[j] : d0[j];
+                        x[r].x = round_tf32(x[r].x * dv); x[r].y = round_tf32(x[r].y * dv);
+                        x[r].z = round_tf32(x[r].z * dv); x[r].w = round_tf32(x[r].w * dv);
+                        p[128 * r] = x[r];
+                    }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(fb0 + stage * 8);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < TW0) {  // ---------------- epilogue (both CTAs)
+        const int ew = warp - 4;
+        const int quad = warp % 4;   // TMEM lanes 32*quad .. +31
+        const int chalf = ew / 4;
+        const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
+        const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t u = pair_id; u < nunits; u += npairs) {
+            int64_t mi, op0, op1, kb0, kb1, sl;
+            unit_of(u, mi, op0, op1, kb0, kb1, sl);
+            const int64_t row0 = mi * 256 + 128 * rank + quad * 32;
+            if constexpr (!JT) {
+                // row n = row0 + lane; columns 64*chalf .. +63 of both o of each pair
+                const int64_t nrow = row0 + lane;
+                const bool live = nrow < ka.rows;
+                float sum[64];
+#pragma unroll
+                for (int j = 0; j < 64; ++j) sum[j] = 0.f;
+                for (int64_t op = op0; op < op1; ++op) {
+                    mbar_wait(&tfull[acc], acc_phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int x = 0; x < 2; ++x) {
+                        const int64_t o = 2 * op + x;
+                        const float dv = (live && o < ka.to) ? __ldg(ka.delta + nrow * ka.ldd + o) : 0.f;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float v[32];
+                            tmem_ld32(lane_base + (uint32_t)(acc * KR_BN + x * 128 + chalf * 64 + h * 32), v);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) sum[h * 32 + j] = fmaf(dv, v[j], sum[h * 32 + j]);
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
+                if (live) {
+                    float4* dst = reinterpret_cast<float4*>(ka.out + sl * ka.slab + nrow * ka.ldo + chalf * 64);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        __stcs(dst + j, make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]));
+                }
+            } else {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                // TMEM columns 128*chalf.. hold output unit o; lane = input i,
+                // whose 32-column run of Y row (woff + o T_k + i) is contiguous
+                const int64_t o = 2 * op0 + chalf;
+                const int64_t i = row0 + lane;
+                float* yrow = ka.out + sl * ka.slab + (ka.woff + o * ka.tk + i) * ka.ldo;
+                const bool vec = (ka.ldo & 3) == 0;
+                for (int cb = 0; cb < 4; ++cb) {
+                    const int64_t c0 = cb * 32;
+                    if (c0 >= ka.l || o >= ka.to) break;
+                    float v[32];
+                    tmem_ld32(lane_base + (uint32_t)(acc * KR_BN + chalf * 128 + cb * 32), v);
+                    if (i < ka.rows) {
+                        if (vec && c0 + 32 <= ka.l) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                __stcs(reinterpret_cast<float4*>(yrow + c0) + q,
+                                       make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (c0 + j < ka.l) yrow[c0 + j] = v[j];
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * KR_BN));
+    }
+}
+
+}  // namespace pair
+
+// out[r, c] = tf32(in[r, c]) for c < cols, 0 in the padding columns
+__global__ void round_pad_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t rows, int64_t cols,
+                                 int64_t ld) {
+    const int64_t nq = ld / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * nq;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / nq, c = (i % nq) * 4;
+        const float4 v = *reinterpret_cast<const float4*>(in + r * ld + c);
+        float4 w;
+        w.x = c + 0 < cols ? round_tf32(v.x) : 0.f;
+        w.y = c + 1 < cols ? round_tf32(v.y) : 0.f;
+        w.z = c + 2 < cols ? round_tf32(v.z) : 0.f;
+        w.w = c + 3 < cols ? round_tf32(v.w) : 0.f;
+        *reinterpret_cast<float4*>(out + r * ld + c) = w;
+    }
+}
+
+}  // namespace tc
+
+// Rounded (to nearest TF32) copies of the activations and deltas of every
+// layer, shared by all J X / J^T T products of one eigensolve.
+struct KrOperands {
+    DevMem mem;
+    const float* a[kMaxLayers] = {};
+    const float* d[kMaxLayers] = {};
+    const float* dT[kMaxLayers] = {};  // delta_k^T (T_{k+1} x ldn, not rounded), zero padded
+    int64_t ldn = 0;
+
+    KrOperands(const ModelDesc& md, const Cache<float>& c, cudaStream_t s) {
+        ldn = round_up(c.n, 32);
+        size_t total = 0;
+        for (int k = 0; k < md.S; ++k) total += (size_t)c.n * (c.lda[k] + c.ldt[k]) + (size_t)md.w[k + 1] * ldn;
+        mem = DevMem(total * sizeof(float), s);
+        float* p = dptr<float>(mem);
+        auto round = [&](const float* src, int64_t count) -> const float* {
+            tc::round_tf32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(count, 1024), 148 * 32), 256, 0, s>>>(src, p,
+                                                                                                            count);
+            CK_LAUNCH();
+            const float* out = p;
+            p += count;
+            return out;
+        };
+        for (int k = 0; k < md.S; ++k) {
+            a[k] = round(c.a[k], c.n * c.lda[k]);
+            d[k] = round(c.delta[k], c.n * c.ldt[k]);
+        }
+        for (int k = 0; k < md.S; ++k) {
+            transpose<float>(s, c.delta[k], c.ldt[k], 0, p, ldn, 0, c.n, md.w[k + 1], 1);
+            dT[k] = p;
+            p += (size_t)md.w[k + 1] * ldn;
+        }
+    }
+};
+
+// Khatri-Rao products need 16-byte aligned pitches for TMA
+inline bool kr_supported(const ModelDesc& md, const Cache<float>& c) {
+    for (int k = 0; k < md.S; ++k)
+        if (c.lda[k] % 4 || c.ldt[k] % 4) return false;
+    return true;
+}
+
+template <bool JT>
+void kr_launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const tc::pair::KrArgs& ka, int a3d,
+               int b3d) {
+    using C = tc::pair::KrCfg<JT>;
+    static bool attr = false;
+    if (!attr) {
+        CK_CUDA(cudaFuncSetAttribute(tc::pair::kr_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES));
+        attr = true;
+    }
+    const int64_t units = ka.mt * (JT ? ka.nop * ka.ksplit : ceil_div(ka.nop, ka.chunk));
+    const int grid = 2 * (int)std::min<int64_t>(units, tc::num_sms() / 2);
+    tc::pair::kr_kernel<JT><<<grid, C::THREADS, C::BYTES, s>>>(ma, mb, ka, (uint32_t)tc::BK * 128u, 512u, 1024u, a3d,
+                                                               b3d);
+    CK_LAUNCH();
+}
+
+// T (n x l, ldt) = J X for X (P x l, ldx; ldx a multiple of 32)
+inline void kr_apply_j(const ModelDesc& md, const Cache<float>& c, const KrOperands& op, const float* X, int64_t ldx,
+                       int64_t l, float* T, int64_t ldt, cudaStream_t s) {
+    const int64_t n = c.n, P = md.P;
+    const int64_t pairs = tc::num_sms() / 2;
+    const int64_t mt = ceil_div(n, 256);
+    // X rounded to nearest TF32 with zero padding columns
+    DevMem xr((size_t)P * ldx * sizeof(float), s);
+    tc::round_pad_kernel<<<(unsigned)std::min<int64_t>(ceil_div(P * ldx / 4, 256), 148 * 16), 256, 0, s>>>(
+        X, dptr<float>(xr), P, l, ldx);
+    CK_LAUNCH();
+    // work split: each layer's o pairs cut into chunks so ~8 units per SM pair
+    int64_t chunk[kMaxLayers], nslab = 0, base[kMaxLayers];
+    for (int k = 0; k < md.S; ++k) {
+        const int64_t nop = ceil_div(md.w[k + 1], 2);
+        const int64_t want = std::max<int64_t>(1, ceil_div(8 * pairs, mt));
+        chunk[k] = ceil_div(nop, std::min(nop, want));
+        base[k] = nslab;
+        nslab += ceil_div(nop, chunk[k]);
+    }
+    const int64_t bias_base = nslab;
+    nslab += md.S;
+    const int64_t ldw = 128, slab = n * ldw;
+    DevMem ws((size_t)(nslab * slab) * sizeof(float), s);
+    for (int64_t c0 = 0; c0 < l; c0 += 128) {
+        const int64_t lc = std::min<int64_t>(128, l - c0);
+        const float* xc = dptr<float>(xr) + c0;
+        const int b3 = ldx >= round_up(lc, 32) ? 1 : 0;
+        for (int k = 0; k < md.S; ++k) {
+            const int64_t tk = md.w[k], to = md.w[k + 1];
+            CUtensorMap ma = tc::make_map(op.a[k], n, tk, c.lda[k], 0, 128);
+            CUtensorMap mb = tc::make_map(xc, lc, P, ldx, 1, 128, b3);
+            tc::pair::KrArgs ka{mt, ceil_div(to, 2), chunk[k], ceil_div(tk, tc::BK), tk, to, md.woff[k],
+                                c.delta[k], c.ldt[k], n, dptr<float>(ws) + base[k] * slab, ldw, slab, n, lc, 1};
+            kr_launch<false>(s, ma, mb, ka, 0, b3);
+            // bias tangents: delta_k Xb_k
+            gemm_tf32(kTF32, s, n, lc, to, pre_rounded(kmaj(op.d[k], c.ldt[k])),
+                      pre_rounded(mnmaj(xc + md.boff[k] * ldx, ldx)),
+                      EpiStore<float>{dptr<float>(ws) + (bias_base + k) * slab, ldw, 0, 1.f, 0.f});
+        }
+        tc::slab_sum_kernel<<<(unsigned)ceil_div(n * (ldw / 4), 256), 256, 0, s>>>(dptr<float>(ws), ldw, slab,
+                                                                                  (int)nslab, n, lc, 1.f, T + c0, ldt);
+        CK_LAUNCH();
+    }
+}
+
+// Y (P x l, ldy) = J^T T for T (n x l, ldtn; ldtn a multiple of 32)
+inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOperands& op, const float* Tn,
+                        int64_t ldtn, int64_t l, float* Y, int64_t ldy, cudaStream_t s) {
+    const int64_t n = c.n;
+    const int64_t pairs = tc::num_sms() / 2;
+    for (int64_t c0 = 0; c0 < l; c0 += 128) {
+        const int64_t lc = std::min<int64_t>(128, l - c0);
+        const float* tc0 = Tn + c0;
+        const int b3 = ldtn >= round_up(lc, 32) ? 1 : 0;
+        CUtensorMap mb = tc::make_map(tc0, lc, n, ldtn, 1, 128, b3);
+        for (int k = 0; k < md.S; ++k) {
+            const int64_t tk = md.w[k], to = md.w[k + 1];
+            const int a3 = c.lda[k] >= round_up(tk, 32) ? 1 : 0;
+            CUtensorMap ma = tc::make_map(op.a[k], tk, n, c.lda[k], 1, 128, a3);
+            const int64_t mt = ceil_div(tk, 256), nop = ceil_div(to, 2), nk = ceil_div(n, tc::BK);
+            // few (i-tile, o-pair) units (a narrow layer): split the examples
+            // into slabs of partial products, summed in fixed order after
+            int64_t ks = 1;
+            if (mt * nop < 2 * pairs) ks = std::max<int64_t>(1, std::min(ceil_div(4 * pairs, mt * nop), nk / 8));
+            if (ks > 1) ks = ceil_div(nk, ceil_div(nk, ks));  // every slab non-empty
+            if (ks == 1) {
+                tc::pair::KrArgs ka{mt, nop, 1, nk, tk, to, md.woff[k], op.dT[k], op.ldn, n, Y + c0, ldy, 0, tk, lc, 1};
+                kr_launch<true>(s, ma, mb, ka, a3, b3);
+            } else {
+                const int64_t rows = to * tk, slab = rows * 128;
+                DevMem ws((size_t)(ks * slab) * sizeof(float), s);
+                tc::pair::KrArgs ka{mt, nop, 1, nk, tk, to, 0, op.dT[k], op.ldn, n, dptr<float>(ws), 128, slab, tk,
+                                    lc, ks};
+                kr_launch<true>(s, ma, mb, ka, a3, b3);
+                tc::slab_sum_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, s>>>(
+                    dptr<float>(ws), 128, slab, (int)ks, rows, lc, 1.f, Y + md.woff[k] * ldy + c0, ldy);
+                CK_LAUNCH();
+            }
+            // bias rows: delta_k^T T (short M, long K: split over K)
+            gemm_tf32_store(kTF32, s, to, lc, n, pre_rounded(mnmaj(op.d[k], c.ldt[k])), mnmaj(tc0, ldtn),
+                            Y + md.boff[k] * ldy + c0, ldy);
+        }
+    }
+}
+
+}  // namespace ck

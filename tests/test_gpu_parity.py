@@ -172,3 +172,34 @@ def test_config2_hessian_pins_tf32():
     got = H[:, :P][:, cols].double().cpu().numpy()
     for j in range(got.shape[1]):
         assert rel_fro(got[:, j], pins["hcols"][:, j]) <= 1e-3, j
+
+
+@pytest.mark.parametrize("prec", ["tf32", "f32"])
+def test_config1_topk_against_dual_gram(prec):
+    """Top-k of G at config-1 size (P = 23860, N = 4096): the K-split J X
+    product and the device CholeskyQR2 path.  The nonzero spectrum of
+    G = (1/N) J^T J equals that of the dual Gram (1/N) J J^T (N x N), formed
+    here in fp64 from the fp64 Jacobian."""
+    torch = pytest.importorskip("torch")
+    wl = CONFIGS["c1"]
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P, n = wl.P, wl.n
+    p64, x64, lab = _device_inputs(wl, torch, torch.float64)
+    J = torch.empty((n, P), dtype=torch.float64, device="cuda:0")
+    curv.dev_assemble_jacobian(spec, p64, x64, lab, n, J, P, precision="f64")
+    w = torch.linalg.eigvalsh(J @ J.T / n).flip(0)[:10].cpu().numpy()
+    del J
+    k = 20
+    q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
+    lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
+    curv.dev_opg_topk(spec, p64.float(), x64.float(), lab, n, k, 20, 2, 7, q, lam, precision=prec)
+    torch.cuda.synchronize()
+    lam = lam.double().cpu().numpy()
+    assert np.all(np.diff(lam) <= 0)
+    # the C - 1 = 9 separated eigenvalues (softmax: one direction per free
+    # logit) within 1e-3; the first bulk eigenvalue is a range-finder
+    # accuracy question (20 + 20 columns, 2 power iterations), not precision
+    assert np.all(np.abs(lam[:9] - w[:9]) <= 1e-3 * np.abs(w[:9])), (lam[:10], w)
+    assert lam[9] <= w[9] * (1 + 1e-3) and lam[9] >= 0.9 * w[9]
+    qtq = (q.T.double() @ q.double()).cpu().numpy()
+    assert np.abs(qtq - np.eye(k)).max() <= 1e-4
