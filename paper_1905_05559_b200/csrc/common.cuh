@@ -76,10 +76,11 @@ __host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + 
 __host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 // fp32 -> nearest TF32 (10-bit mantissa), kept in fp32 storage
+// Round-half-away on the magnitude bits: the result of cvt.rna.tf32.f32 for
+// every finite value, +-Inf and quiet NaNs, in two integer ops (ptxas expands
+// cvt.rna.tf32 into an Inf test plus predicated adds and moves).
 __device__ __forceinline__ float round_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // ---- activations (model.cpp:9-50) -------------------------------------------

@@ -704,6 +704,14 @@ struct FusedHess {
     const int4* tiles;  // (o'', j0, n0, -) of every pair tile holding required entries
     int64_t ntiles;
     int64_t rows;       // tangent rows of the block: nw weights, then T_{k+1} biases (s = 1)
+    int pv_tma;         // profile / delta rows of a CTA's weight rows staged by TMA (else __ldg)
+    // first output unit o whose profile row the producer stages for a CTA
+    // whose first tangent row is jr (rows jr .. jr + 127 use units o_first ..)
+    __host__ __device__ int64_t o_first(int64_t jr) const {
+        const int64_t to = rows - nw;
+        const int64_t o = jr < nw ? jr / tk : 0;
+        return o < to ? o : to - 1;
+    }
     // first tangent row of band o'' (aligned to the 256-row pair tile)
     __host__ __device__ int64_t jstart(int64_t opp) const {
         if (!diag) return 0;
@@ -712,15 +720,25 @@ struct FusedHess {
     }
 };
 
-constexpr int kFusedThreads = 128 + 32 * EPI_WARPS + 128;  // control, epilogue, transform
+// control (4 warps), epilogue (8: two per TMEM lane quadrant, each half the
+// tile width), transform (FUSED_TW: FUSED_TW / 4 threads per tile row, each
+// a contiguous share of the row's eight 16-byte chunks)
+constexpr int FUSED_EPI = 8, FUSED_TW = 4;
+constexpr int TW_CH = 8 / (FUSED_TW / 4);  // chunks per transform thread
+constexpr int kFusedThreads = 128 + 32 * FUSED_EPI + 32 * FUSED_TW;
+constexpr int PV_ROWS = 8;  // profile rows (output units o) staged per CTA and stage
 
 template <int BN>
 struct FusedSmem {
     static constexpr int A_BYTES = 128 * BK * 4;
     static constexpr int B_BYTES = (BN / 2) * BK * 4;
-    static constexpr int EPI_BYTES = EPI_WARPS * 32 * 36 * 4;
+    static constexpr int PV_BYTES = PV_ROWS * BK * 4;  // one 128-byte row of examples per unit
+    static constexpr int EPI_BYTES = FUSED_EPI * 32 * 36 * 4;
     static constexpr int MAX_SMEM = 227 * 1024;
-    __host__ __device__ static constexpr int stage_bytes(int hasq) { return A_BYTES * (hasq ? 2 : 1) + B_BYTES; }
+    // stage: A | Q (m < k) | B | PV rows | delta^T rows (m < k)
+    __host__ __device__ static constexpr int stage_bytes(int hasq) {
+        return (A_BYTES + PV_BYTES) * (hasq ? 2 : 1) + B_BYTES;
+    }
     __host__ __device__ static constexpr int stages(int hasq) {
         const int st = (MAX_SMEM - 1024 - EPI_BYTES - 1024) / stage_bytes(hasq);
         return st > 8 ? 8 : st;
@@ -730,6 +748,10 @@ struct FusedSmem {
     }
 };
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -737,7 +759,8 @@ __device__ __forceinline__ void fence_proxy_async() {
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_constant__ CUtensorMap mapQ,
-                     const __grid_constant__ CUtensorMap mapB, FusedHess fh, TcShape sh, Epi epi) {
+                     const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapPV,
+                     const __grid_constant__ CUtensorMap mapDT, FusedHess fh, TcShape sh, Epi epi) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by offset from the __shared__ array, so the compiler
     // keeps the shared state space (LDS/STS, not generic LD/ST) for derived pointers
@@ -746,6 +769,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
     const int STAGE_BYTES = S::stage_bytes(fh.hasq);
     const int NST = S::stages(fh.hasq);
     const int A_OFF_Q = S::A_BYTES, B_OFF = S::A_BYTES * (fh.hasq ? 2 : 1);
+    const int PV_OFF = B_OFF + S::B_BYTES, DT_OFF = PV_OFF + S::PV_BYTES;
     uint8_t* stage_base = smem;
     float* epi_buf = reinterpret_cast<float*>(smem + NST * STAGE_BYTES);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES + S::EPI_BYTES);
@@ -761,7 +785,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
     const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int64_t ntiles = fh.ntiles;
     const int64_t nk = ceil_div(sh.K, BK);
-    constexpr int TW0 = 4 + EPI_WARPS;  // first transform warp
+    constexpr int TW0 = 4 + FUSED_EPI;  // first transform warp
 
     // tile t -> (o'', first tangent row j0, n0) from the host-built list of
     // tiles that hold required entries; rows of the pair tile are j0 .. j0+255
@@ -778,13 +802,13 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         prefetch_map(&mapB);
         if (fh.hasq) prefetch_map(&mapQ);
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 1 + 2 * 4);
+            mbar_init(&full[s], 1 + 2 * FUSED_TW);
             mbar_init(&empty[s], 1);
             mbar_init(&afull[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * EPI_WARPS);
+            mbar_init(&tempty[a], 2 * FUSED_EPI);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -817,9 +841,15 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = stage_base + stage * STAGE_BYTES;
                     const int64_t k0 = kb * BK;
-                    mbar_expect_tx(&afull[stage], (uint32_t)(S::A_BYTES * (fh.hasq ? 2 : 1)));
+                    mbar_expect_tx(&afull[stage], (uint32_t)((S::A_BYTES + (fh.pv_tma ? S::PV_BYTES : 0)) *
+                                                             (fh.hasq ? 2 : 1)));
                     tma_load_2d(sa, &mapAk, &afull[stage], (int32_t)k0, (int32_t)i0);
                     if (fh.hasq) tma_load_2d(sa + A_OFF_Q, &mapQ, &afull[stage], (int32_t)k0, (int32_t)(opp * fh.qrows + i0));
+                    if (fh.pv_tma) {  // profile rows (o_first .. + 7, o''), examples k0 .. k0 + 31
+                        const int32_t of = (int32_t)fh.o_first(jr);
+                        tma_load_3d(sa + PV_OFF, &mapPV, &afull[stage], (int32_t)k0, (int32_t)opp, of);
+                        if (fh.hasq) tma_load_3d(sa + DT_OFF, &mapDT, &afull[stage], (int32_t)k0, 0, of);
+                    }
                     const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
                     if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * S::B_BYTES));
                     load_tile2<BN / 2>(sa + B_OFF, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0, pol);
@@ -861,7 +891,8 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             }
         }
     } else if (warp >= TW0) {  // ---------------- A transform (both CTAs)
-        const int row = (warp - TW0) * 32 + lane;  // tile row owned by this thread
+        const int row = ((warp - TW0) & 3) * 32 + lane;  // tile row of this thread
+        const int L0 = FUSED_TW == 4 ? 0 : ((warp - TW0) >> 2) * TW_CH;  // its chunks L0 .. L0 + TW_CH - 1
         const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
         int stage = 0;
         uint32_t phase = 0;
@@ -874,39 +905,63 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             const float* pvrow = fh.pv + (o * fh.tm1 + opp) * fh.ldn;
             const float* drow = fh.hasq ? fh.dT + o * fh.ldn : nullptr;
             const int sw = row & 7;
+            // weight rows read their profile (and delta) row from the stage
+            const int64_t slot = o - fh.o_first(j0 + 128 * rank);
+            const bool staged = fh.pv_tma && !bias && slot >= 0 && slot < PV_ROWS;
+            // pull the profile (and delta) lines of the next k-blocks into L1
+            // ahead of use: the loads below then miss L2 latency, not the MMA
+            constexpr int PF = 3;
+            for (int64_t kb = 0; kb < PF && kb < nk && !staged; ++kb) {
+                prefetch_l1(pvrow + kb * BK);
+                if (drow) prefetch_l1(drow + kb * BK);
+            }
             for (int64_t kb = 0; kb < nk; ++kb) {
+                if (kb + PF < nk && !staged) {
+                    prefetch_l1(pvrow + (kb + PF) * BK);
+                    if (drow) prefetch_l1(drow + (kb + PF) * BK);
+                }
                 mbar_wait(&afull[stage], phase);
-                uint8_t* sa = stage_base + stage * STAGE_BYTES + row * 128;
+                uint8_t* st = stage_base + stage * STAGE_BYTES;
+                uint8_t* sa = st + row * 128;
                 const int64_t n0k = kb * BK;
+                const float4* pst = reinterpret_cast<const float4*>(st + PV_OFF + slot * 128);
+                const float4* dst_ = reinterpret_cast<const float4*>(st + DT_OFF + slot * 128);
                 // all loads first (8 smem + 8 profile vectors in flight), then
                 // the products, then the stores: logical 16-byte chunk L holds
                 // examples n0k + 4L .. +3 and sits at physical chunk L ^ (row & 7)
-                float4 x[8], p[8];
+                float4 x[TW_CH], p[TW_CH];
 #pragma unroll
-                for (int L = 0; L < 8; ++L) x[L] = *reinterpret_cast<const float4*>(sa + ((L ^ sw) << 4));
+                for (int u = 0; u < TW_CH; ++u) x[u] = *reinterpret_cast<const float4*>(sa + (((L0 + u) ^ sw) << 4));
+                if (staged) {
 #pragma unroll
-                for (int L = 0; L < 8; ++L) p[L] = __ldg(reinterpret_cast<const float4*>(pvrow + n0k + 4 * L));
+                    for (int u = 0; u < TW_CH; ++u) p[u] = pst[L0 + u];
+                } else {
 #pragma unroll
-                for (int L = 0; L < 8; ++L) {
+                    for (int u = 0; u < TW_CH; ++u)
+                        p[u] = __ldg(reinterpret_cast<const float4*>(pvrow + n0k + 4 * (L0 + u)));
+                }
+#pragma unroll
+                for (int u = 0; u < TW_CH; ++u) {
                     if (bias) {
-                        x[L] = p[L];
+                        x[u] = p[u];
                     } else {
-                        x[L].x *= p[L].x; x[L].y *= p[L].y; x[L].z *= p[L].z; x[L].w *= p[L].w;
+                        x[u].x *= p[u].x; x[u].y *= p[u].y; x[u].z *= p[u].z; x[u].w *= p[u].w;
                     }
                 }
                 if (fh.hasq && !bias) {
 #pragma unroll
-                    for (int L = 0; L < 8; ++L) {
-                        const float4 q = *reinterpret_cast<const float4*>(sa + A_OFF_Q + ((L ^ sw) << 4));
-                        const float4 dd = __ldg(reinterpret_cast<const float4*>(drow + n0k + 4 * L));
-                        x[L].x += dd.x * q.x; x[L].y += dd.y * q.y; x[L].z += dd.z * q.z; x[L].w += dd.w * q.w;
+                    for (int u = 0; u < TW_CH; ++u) {
+                        const float4 q = *reinterpret_cast<const float4*>(sa + A_OFF_Q + (((L0 + u) ^ sw) << 4));
+                        const float4 dd = staged ? dst_[L0 + u]
+                                                 : __ldg(reinterpret_cast<const float4*>(drow + n0k + 4 * (L0 + u)));
+                        x[u].x += dd.x * q.x; x[u].y += dd.y * q.y; x[u].z += dd.z * q.z; x[u].w += dd.w * q.w;
                     }
                 }
 #pragma unroll
-                for (int L = 0; L < 8; ++L) {  // round to nearest TF32 (the MMA would truncate)
-                    x[L].x = round_tf32(x[L].x); x[L].y = round_tf32(x[L].y);
-                    x[L].z = round_tf32(x[L].z); x[L].w = round_tf32(x[L].w);
-                    *reinterpret_cast<float4*>(sa + ((L ^ sw) << 4)) = x[L];
+                for (int u = 0; u < TW_CH; ++u) {  // round to nearest TF32 (the MMA would truncate)
+                    x[u].x = round_tf32(x[u].x); x[u].y = round_tf32(x[u].y);
+                    x[u].z = round_tf32(x[u].z); x[u].w = round_tf32(x[u].w);
+                    *reinterpret_cast<float4*>(sa + (((L0 + u) ^ sw) << 4)) = x[u];
                 }
                 fence_proxy_async();
                 __syncwarp();
@@ -1008,6 +1063,23 @@ inline CUtensorMap make_map(const float* p, int64_t rows, int64_t K, int64_t ld,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+// 3D fp32 map without swizzle over p[(c * d1 + b) * ld0 + a] -- dims
+// (d0, d1, d2), dim-2 stride s2 elements -- box (b0, b1, b2)
+inline CUtensorMap make_map_plain3(const float* p, int64_t d0, int64_t d1, int64_t d2, int64_t s2, int b0, int b1,
+                                   int b2) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+    cuuint64_t str[2] = {(cuuint64_t)d0 * 4, (cuuint64_t)s2 * 4};
+    cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2}, es[3] = {1, 1, 1};
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || (str[0] & 15) || (str[1] & 15))
+        throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with 16-byte pitches");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims, str, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (plain 3D) failed: " + std::to_string((int)r));
     return m;
 }
 
@@ -1243,7 +1315,12 @@ struct HessFused<float> {
         constexpr int BN = 256;
         namespace pair = tc::pair;
         pair::FusedHess fh{a.pv, a.dT, a.ldn, a.tk, a.tm, a.tm1, a.nw, a.qrows, a.diag, a.qT ? 1 : 0, nullptr, 0,
-                           a.rows};
+                           a.rows, 0};
+        // a CTA's 128 weight rows span at most 127 / T_k + 2 output units
+        const int64_t to = a.rows - a.nw;
+        fh.pv_tma = (127 / a.tk + 2 <= pair::PV_ROWS) ? 1 : 0;
+        CUtensorMap mpv = tc::make_map_plain3(a.pv, a.ldn, a.tm1, to, a.tm1 * a.ldn, 32, 1, pair::PV_ROWS);
+        CUtensorMap mdt = a.qT ? tc::make_map_plain3(a.dT, a.ldn, 1, to, a.ldn, 32, 1, pair::PV_ROWS) : mpv;
         const int64_t N = a.tm + 1;  // weight columns + bias column of block m
         // tile list: every (o'' band, 256-row j tile, n tile) holding a required entry
         std::vector<int4> list;
@@ -1279,7 +1356,7 @@ struct HessFused<float> {
         }
         const int grid = 2 * (int)std::min<int64_t>(fh.ntiles, tc::num_sms() / 2);
         pair::tc_hess_fused_kernel<BN, EpiHess<float>><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
-            mak, mq, mb, fh, sh, e);
+            mak, mq, mb, mpv, mdt, fh, sh, e);
         CK_LAUNCH();
         return true;
     }

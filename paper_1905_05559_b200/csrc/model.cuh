@@ -577,6 +577,46 @@ struct EpiHess {
             if (mirror) H[gc * ldh + gr] = v;
         }
     }
+    // register-only epilogue (fused kernel): lane = row row0 + lane holds the
+    // 32 accumulators of columns col0 .. col0 + 31 in v[]; the row's entries
+    // are 128 contiguous bytes of H (16-byte stores), the mirrored column
+    // entries are one coalesced 128-byte store per column
+    __device__ void block_regs(int64_t row0, int64_t col0, int64_t M, int64_t N, const float* v, int lane) const {
+        const bool tri = diag && mirror;
+        const int64_t r = row0 + lane;
+        if (r >= M) return;
+        const int64_t opp = r / J, jj = r - opp * J;
+        const int64_t gr = woffk + j0 + jj;
+        if (!owns(gr)) return;
+        const int ncols = (int)::min((int64_t)32, N - col0);
+        const int64_t wbase = woffm + opp * tm;
+        T* row = H + gr * ldh;
+        if constexpr (sizeof(T) == 4) {
+            // whole 32-column run inside the weight columns and the triangle
+            const int64_t gc0 = wbase + col0;
+            if (ncols == 32 && col0 + 32 <= tm && ((gc0 | ldh) & 3) == 0 && (!tri || gc0 + 31 <= gr)) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    __stcs(reinterpret_cast<float4*>(row + gc0) + q,
+                           make_float4(alpha * v[4 * q], alpha * v[4 * q + 1], alpha * v[4 * q + 2], alpha * v[4 * q + 3]));
+                if (mirror) {
+#pragma unroll
+                    for (int cc = 0; cc < 32; ++cc)
+                        if (!tri || gc0 + cc < gr) __stcs(&H[(gc0 + cc) * ldh + gr], alpha * (T)v[cc]);
+                }
+                return;
+            }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 32; ++cc) {  // constant trip count keeps v[] in registers
+            const int64_t c = col0 + cc;
+            const int64_t gc = c < tm ? wbase + c : boffm + opp;
+            if (cc < ncols && (!tri || gc <= gr)) {
+                __stcs(&row[gc], alpha * (T)v[cc]);
+                if (mirror && (!tri || gc < gr)) __stcs(&H[gc * ldh + gr], alpha * (T)v[cc]);
+            }
+        }
+    }
     // tensor-core epilogue (32 x 32 block, coalesced in both store directions)
     __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float* v,
                           int lane) const {
