@@ -705,6 +705,8 @@ struct FusedHess {
     int64_t ntiles;
     int64_t rows;       // tangent rows of the block: nw weights, then T_{k+1} biases (s = 1)
     int pv_tma;         // profile / delta rows of a CTA's weight rows staged by TMA (else __ldg)
+    long long* trace = nullptr;  // dev: pipeline event stamps (8 x 1024) of CTA 0
+    int tma_h = 0;               // interior 32 x 32 blocks stored by TMA (mapH)
     // first output unit o whose profile row the producer stages for a CTA
     // whose first tangent row is jr (rows jr .. jr + 127 use units o_first ..)
     __host__ __device__ int64_t o_first(int64_t jr) const {
@@ -725,16 +727,20 @@ struct FusedHess {
 // a contiguous share of the row's eight 16-byte chunks)
 constexpr int FUSED_EPI = 8, FUSED_TW = 4;
 constexpr int TW_CH = 8 / (FUSED_TW / 4);  // chunks per transform thread
-constexpr int kFusedThreads = 128 + 32 * FUSED_EPI + 32 * FUSED_TW;
 constexpr int PV_ROWS = 8;  // profile rows (output units o) staged per CTA and stage
+constexpr bool STAGE_PV = true;  // profile rows ride the stage (TMA), no L2 round trip in the transform
+constexpr int kFusedThreads = 128 + 32 * FUSED_EPI + 32 * FUSED_TW;
 
 template <int BN>
 struct FusedSmem {
     static constexpr int A_BYTES = 128 * BK * 4;
     static constexpr int B_BYTES = (BN / 2) * BK * 4;
-    static constexpr int PV_BYTES = PV_ROWS * BK * 4;  // one 128-byte row of examples per unit
-    static constexpr int EPI_BYTES = FUSED_EPI * 32 * 36 * 4;
+    // per epilogue warp: a 1024-aligned 4 KB slot holding one swizzled 32 x 32
+    // block (the TMA store box, or the staging block of the scalar path)
+    static constexpr int EPI_SLOT = 4 * 1024;
+    static constexpr int EPI_BYTES = FUSED_EPI * EPI_SLOT;
     static constexpr int MAX_SMEM = 227 * 1024;
+    static constexpr int PV_BYTES = STAGE_PV ? PV_ROWS * BK * 4 : 0;  // one 128-byte row of examples per unit
     // stage: A | Q (m < k) | B | PV rows | delta^T rows (m < k)
     __host__ __device__ static constexpr int stage_bytes(int hasq) {
         return (A_BYTES + PV_BYTES) * (hasq ? 2 : 1) + B_BYTES;
@@ -748,6 +754,16 @@ struct FusedSmem {
     }
 };
 
+// TMA store of one smem box; bulk-group bookkeeping
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -760,7 +776,8 @@ template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_constant__ CUtensorMap mapQ,
                      const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapPV,
-                     const __grid_constant__ CUtensorMap mapDT, FusedHess fh, TcShape sh, Epi epi) {
+                     const __grid_constant__ CUtensorMap mapDT, const __grid_constant__ CUtensorMap mapH, FusedHess fh,
+                     TcShape sh, Epi epi) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by offset from the __shared__ array, so the compiler
     // keeps the shared state space (LDS/STS, not generic LD/ST) for derived pointers
@@ -773,15 +790,18 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
     uint8_t* stage_base = smem;
     float* epi_buf = reinterpret_cast<float*>(smem + NST * STAGE_BYTES);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES + S::EPI_BYTES);
-    uint64_t* full = bars;         // [8] leader: 1 producer + 8 transform-warp arrivals, B tx
+    uint64_t* full = bars;         // [8] leader: 1 producer + transform-warp arrivals, B tx
     uint64_t* empty = bars + 8;    // [8] both CTAs (multicast commit)
-    uint64_t* afull = bars + 16;   // [8] local: A (and Q) tiles landed
+    uint64_t* afull = bars + 16;   // [8] local: A (Q, profile rows) landed
     uint64_t* tfull = bars + 24;   // [2]
     uint64_t* tempty = bars + 26;  // [2] leader
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cta_rank();
+    // dev trace (fh.trace set): clock64 stamps of pipeline events in CTA 0
+    constexpr int64_t TRN = 1024;
+    long long* trace = (fh.trace && blockIdx.x == 0) ? fh.trace : nullptr;
     const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int64_t ntiles = fh.ntiles;
     const int64_t nk = ceil_div(sh.K, BK);
@@ -829,6 +849,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         if (lane == 0) {  // ---------------- producer
             int stage = 0;
             uint32_t phase = 0;
+            int64_t tg = 0;
             const uint64_t pol = evict_last_policy();
             for (int64_t t = pair_id; t < ntiles; t += npairs) {
                 int64_t opp, j0, n0;
@@ -839,6 +860,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 const int64_t bn0 = n0 + half * rank;
                 for (int64_t kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if (trace) { if (tg < TRN) trace[0 * TRN + tg] = clock64(); ++tg; }
                     uint8_t* sa = stage_base + stage * STAGE_BYTES;
                     const int64_t k0 = kb * BK;
                     mbar_expect_tx(&afull[stage], (uint32_t)((S::A_BYTES + (fh.pv_tma ? S::PV_BYTES : 0)) *
@@ -863,15 +885,18 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            int64_t tg = 0, tt = 0;
             for (int64_t t = pair_id; t < ntiles; t += npairs) {
                 int64_t opp, j0, n0;
                 tile_of(t, opp, j0, n0);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ++tt;
                 tc_fence_after();
                 const uint32_t idesc = idesc2_tf32(tile_ntile(n0), false, sh.b_mn);
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
                 for (int64_t kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    if (trace) { if (tg < TRN) trace[3 * TRN + tg] = clock64(); ++tg; }
                     tc_fence_after();
                     const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
                     const uint32_t sb = sa + B_OFF;
@@ -896,6 +921,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
         int stage = 0;
         uint32_t phase = 0;
+        int64_t tg = 0;
         for (int64_t t = pair_id; t < ntiles; t += npairs) {
             int64_t opp, j0, n0;
             tile_of(t, opp, j0, n0);
@@ -905,30 +931,21 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             const float* pvrow = fh.pv + (o * fh.tm1 + opp) * fh.ldn;
             const float* drow = fh.hasq ? fh.dT + o * fh.ldn : nullptr;
             const int sw = row & 7;
+            const bool trw = trace && threadIdx.x == TW0 * 32;
             // weight rows read their profile (and delta) row from the stage
             const int64_t slot = o - fh.o_first(j0 + 128 * rank);
             const bool staged = fh.pv_tma && !bias && slot >= 0 && slot < PV_ROWS;
-            // pull the profile (and delta) lines of the next k-blocks into L1
-            // ahead of use: the loads below then miss L2 latency, not the MMA
-            constexpr int PF = 3;
-            for (int64_t kb = 0; kb < PF && kb < nk && !staged; ++kb) {
-                prefetch_l1(pvrow + kb * BK);
-                if (drow) prefetch_l1(drow + kb * BK);
-            }
-            for (int64_t kb = 0; kb < nk; ++kb) {
-                if (kb + PF < nk && !staged) {
-                    prefetch_l1(pvrow + (kb + PF) * BK);
-                    if (drow) prefetch_l1(drow + (kb + PF) * BK);
-                }
+            for (int64_t kb = 0; kb < nk; ++kb, ++tg) {
                 mbar_wait(&afull[stage], phase);
+                if (trw && tg < TRN) trace[1 * TRN + tg] = clock64();
                 uint8_t* st = stage_base + stage * STAGE_BYTES;
                 uint8_t* sa = st + row * 128;
                 const int64_t n0k = kb * BK;
                 const float4* pst = reinterpret_cast<const float4*>(st + PV_OFF + slot * 128);
                 const float4* dst_ = reinterpret_cast<const float4*>(st + DT_OFF + slot * 128);
-                // all loads first (8 smem + 8 profile vectors in flight), then
-                // the products, then the stores: logical 16-byte chunk L holds
-                // examples n0k + 4L .. +3 and sits at physical chunk L ^ (row & 7)
+                // all loads first, then the products, then the stores: logical
+                // 16-byte chunk L holds examples n0k + 4L .. +3 and sits at
+                // physical chunk L ^ (row & 7)
                 float4 x[TW_CH], p[TW_CH];
 #pragma unroll
                 for (int u = 0; u < TW_CH; ++u) x[u] = *reinterpret_cast<const float4*>(sa + (((L0 + u) ^ sw) << 4));
@@ -963,9 +980,12 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                     x[u].z = round_tf32(x[u].z); x[u].w = round_tf32(x[u].w);
                     *reinterpret_cast<float4*>(sa + (((L0 + u) ^ sw) << 4)) = x[u];
                 }
+                if (trw && tg < TRN) trace[4 * TRN + tg] = clock64();
                 fence_proxy_async();
+                if (trw && tg < TRN) trace[5 * TRN + tg] = clock64();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(fb0 + stage * 8);
+                if (trw && tg < TRN) trace[2 * TRN + tg] = clock64();
                 if (++stage == NST) { stage = 0; phase ^= 1; }
             }
         }
@@ -973,15 +993,19 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         const int ew = warp - 4;
         const int quad = warp % 4;
         const int chalf = ew / 4;
-        float(*buf)[36] = reinterpret_cast<float(*)[36]>(epi_buf + ew * 32 * 36);
+        uint8_t* slot = reinterpret_cast<uint8_t*>(epi_buf) + ew * S::EPI_SLOT;
+        float* box = reinterpret_cast<float*>(slot);  // 32 rows x 128 B, 128-byte swizzle
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t t = pair_id; t < ntiles; t += npairs) {
+        const bool tre = trace && threadIdx.x == 4 * 32;
+        int64_t tt = 0;
+        for (int64_t t = pair_id; t < ntiles; t += npairs, ++tt) {
             int64_t opp, j0, n0;
             tile_of(t, opp, j0, n0);
             const int64_t m0 = opp * fh.rows + j0;
             mbar_wait(&tfull[acc], acc_phase);
+            if (tre && tt < TRN) trace[6 * TRN + tt] = clock64();
             tc_fence_after();
             const int64_t row0 = m0 + 128 * rank + quad * 32;
             const int64_t band_end = (opp + 1) * fh.rows;  // rows beyond the band are not stored
@@ -991,16 +1015,58 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
                 if (row0 < band_end) {
-                    stage_block(buf, v, lane);
-                    epi.block(row0, col0, band_end, sh.N, buf, v, lane);
+                    int64_t gr0, gc0;
+                    // the slot is free once the previous box's TMA store has read it
+                    if (lane == 0) bulk_wait_read();
                     __syncwarp();
+                    const bool via_tma = fh.tma_h && epi.tma_block(row0, col0, band_end, sh.N, gr0, gc0);
+                    const float sc = via_tma ? epi.alpha : 1.f;  // the scalar path applies alpha itself
+                    // direct block: row = lane, 16-byte chunk q at q ^ (lane & 7)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<float4*>(box + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                            make_float4(sc * v[4 * q], sc * v[4 * q + 1], sc * v[4 * q + 2], sc * v[4 * q + 3]);
+                    if (via_tma) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) v[c] *= epi.alpha;
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&mapH, box, (int32_t)gc0, (int32_t)gr0);
+                            bulk_commit();
+                        }
+                        if (epi.mirror) {
+                            if (lane == 0) bulk_wait_read();
+                            __syncwarp();
+                            // transposed box: row c holds this block's column c, element lane
+#pragma unroll
+                            for (int c = 0; c < 32; ++c)
+                                box[c * 32 + ((((lane >> 2) ^ (c & 7)) << 2) | (lane & 3))] = v[c];
+                            fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0) {
+                                tma_store_2d(&mapH, box, (int32_t)gr0, (int32_t)gc0);
+                                bulk_commit();
+                            }
+                        }
+                    } else {
+                        __syncwarp();
+                        epi.block_any(row0, col0, band_end, sh.N,
+                                      [&](int r, int q) {
+                                          return *reinterpret_cast<const float4*>(box + r * 32 + ((q ^ (r & 7)) << 2));
+                                      },
+                                      v, lane);
+                        __syncwarp();
+                    }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+            if (tre && tt < TRN) trace[7 * TRN + tt] = clock64();
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (lane == 0) bulk_wait_all();  // epilogue stores complete before exit
     }
     tc_fence_before();
     __syncthreads();
@@ -1080,6 +1146,21 @@ inline CUtensorMap make_map_plain3(const float* p, int64_t d0, int64_t d1, int64
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (plain 3D) failed: " + std::to_string((int)r));
+    return m;
+}
+
+// H (rows x ldh fp32, rows <= ldh) as 32 x 32 boxes with the 128-byte swizzle
+inline CUtensorMap make_map_h(float* H, int64_t ldh) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)ldh, (cuuint64_t)ldh};
+    cuuint64_t str[1] = {(cuuint64_t)ldh * 4};
+    cuuint32_t box[2] = {32, 32}, es[2] = {1, 1};
+    if ((reinterpret_cast<uintptr_t>(H) & 15) || (str[0] & 15))
+        throw CurvError(kCudaError, "TMA store target must be 16-byte aligned with a 16-byte row pitch");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, H, dims, str, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (H) failed: " + std::to_string((int)r));
     return m;
 }
 
@@ -1318,7 +1399,7 @@ struct HessFused<float> {
                            a.rows, 0};
         // a CTA's 128 weight rows span at most 127 / T_k + 2 output units
         const int64_t to = a.rows - a.nw;
-        fh.pv_tma = (127 / a.tk + 2 <= pair::PV_ROWS) ? 1 : 0;
+        fh.pv_tma = (pair::STAGE_PV && 127 / a.tk + 2 <= pair::PV_ROWS) ? 1 : 0;
         CUtensorMap mpv = tc::make_map_plain3(a.pv, a.ldn, a.tm1, to, a.tm1 * a.ldn, 32, 1, pair::PV_ROWS);
         CUtensorMap mdt = a.qT ? tc::make_map_plain3(a.dT, a.ldn, 1, to, a.ldn, 32, 1, pair::PV_ROWS) : mpv;
         const int64_t N = a.tm + 1;  // weight columns + bias column of block m
@@ -1355,9 +1436,31 @@ struct HessFused<float> {
             attr = true;
         }
         const int grid = 2 * (int)std::min<int64_t>(fh.ntiles, tc::num_sms() / 2);
+        static const bool tracing = getenv("CURVKIT_TRACE") != nullptr;
+        DevMem trbuf;
+        if (tracing) {
+            trbuf = DevMem(8 * 1024 * sizeof(long long), s);
+            CK_CUDA(cudaMemsetAsync(trbuf.p, 0, 8 * 1024 * sizeof(long long), s));
+            fh.trace = dptr<long long>(trbuf);
+        }
+        // H as a 2D map of 32 x 32 boxes (128-byte swizzle) for the epilogue
+        fh.tma_h = (e.ldh % 4 == 0) ? 1 : 0;
+        CUtensorMap mh = fh.tma_h ? tc::make_map_h(e.H, e.ldh) : mb;
         pair::tc_hess_fused_kernel<BN, EpiHess<float>><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
-            mak, mq, mb, mpv, mdt, fh, sh, e);
+            mak, mq, mb, mpv, mdt, mh, fh, sh, e);
         CK_LAUNCH();
+        if (tracing) {
+            std::vector<long long> h(8 * 1024);
+            CK_CUDA(cudaMemcpyAsync(h.data(), trbuf.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            static int call = 0;
+            char fn[64];
+            snprintf(fn, sizeof fn, "gpurun_out/trace_%d.bin", call++);
+            if (FILE* f = fopen(fn, "wb")) {
+                fwrite(h.data(), sizeof(long long), h.size(), f);
+                fclose(f);
+            }
+        }
         return true;
     }
 };

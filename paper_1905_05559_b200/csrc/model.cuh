@@ -577,6 +577,18 @@ struct EpiHess {
             if (mirror) H[gc * ldh + gr] = v;
         }
     }
+    // 32 x 32 block stored by two TMA boxes (direct at (gr0, gc0), mirror at
+    // (gc0, gr0)): rows in one band and owned, columns inside the weight
+    // columns, and on diagonal blocks strictly below the diagonal
+    __device__ bool tma_block(int64_t row0, int64_t col0, int64_t M, int64_t N, int64_t& gr0, int64_t& gc0) const {
+        if (row0 + 32 > M || col0 + 32 > N || col0 + 32 > tm) return false;
+        const int64_t opp = row0 / J, jj = row0 - opp * J;
+        if (jj + 32 > J) return false;
+        gr0 = woffk + j0 + jj;
+        if (gr0 < rlo || gr0 + 32 > rhi) return false;
+        gc0 = woffm + opp * tm + col0;
+        return !(diag && mirror && gc0 + 31 >= gr0);
+    }
     // register-only epilogue (fused kernel): lane = row row0 + lane holds the
     // 32 accumulators of columns col0 .. col0 + 31 in v[]; the row's entries
     // are 128 contiguous bytes of H (16-byte stores), the mirrored column
@@ -620,6 +632,13 @@ struct EpiHess {
     // tensor-core epilogue (32 x 32 block, coalesced in both store directions)
     __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float* v,
                           int lane) const {
+        block_any(row0, col0, M, N, [&](int r, int q) { return *reinterpret_cast<const float4*>(&buf[r][4 * q]); },
+                  v, lane);
+    }
+    // same, the staged block read through get(r, q) = columns 4q .. 4q+3 of row r
+    template <class Get>
+    __device__ void block_any(int64_t row0, int64_t col0, int64_t M, int64_t N, Get get, const float* v,
+                              int lane) const {
         const bool tri = diag && mirror;
         // one division per block; each row's (o'', jj) follows by carrying
         const int64_t opp0 = row0 / J, jj0 = row0 - opp0 * J;
@@ -634,7 +653,7 @@ struct EpiHess {
                 while (jj >= J) { jj -= J; ++opp; }
                 const int64_t gr = woffk + j0 + jj, wb = woffm + opp * tm;
                 if (!owns(gr)) continue;
-                const float4 x = *reinterpret_cast<const float4*>(&buf[r][4 * q]);
+                const float4 x = get(r, q);
                 T* row = H + gr * ldh;
                 if constexpr (sizeof(T) == 4) {
                     const int64_t gc = wb + c;
