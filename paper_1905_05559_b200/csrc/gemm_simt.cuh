@@ -181,6 +181,15 @@ struct EpiSymLower {
     // row shard: the GEMM's A operand starts at matrix row roff, so GEMM row m
     // is matrix row m + roff (columns are always absolute)
     int64_t roff = 0;
+    // tensor-core epilogue: 32 x 32 blocks strictly below the diagonal go out
+    // as two TMA boxes (entry block at (row, col), mirror at (col, row))
+    static constexpr bool kTmaStore = true;
+    __device__ bool tma_block(int64_t row0, int64_t col0, int64_t M, int64_t N, int64_t& gr0, int64_t& gc0) const {
+        if (row0 + 32 > M || col0 + 32 > N) return false;
+        gr0 = row0 + roff;
+        gc0 = col0;
+        return gc0 + 31 < gr0;
+    }
     __device__ bool skip(int, int64_t m0, int64_t n0, int64_t bm, int64_t) const {
         return n0 > m0 + roff + bm - 1;
     }

@@ -166,6 +166,12 @@ struct TcShape {
     int a_once = 0, b_once = 0;         // streamed operand: L2 evict_first
 };
 
+// Epilogues whose interior blocks are stored by TMA boxes (Epi::tma_block)
+template <class E, class = void>
+struct EpiTma : std::false_type {};
+template <class E>
+struct EpiTma<E, std::void_t<decltype(E::kTmaStore)>> : std::true_type {};
+
 // Epilogues that take a K-slab index (split-K partial products)
 template <class E, class = void>
 struct EpiSplitK : std::false_type {};
@@ -481,11 +487,28 @@ __host__ __device__ constexpr uint32_t idesc2_tf32(int n, bool a_mn, bool b_mn) 
            ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// TMA store of one smem box; bulk-group bookkeeping
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 template <int BN>
 struct PairSmem {
     static constexpr int A_BYTES = 128 * BK * 4;       // own 128 rows
     static constexpr int B_BYTES = (BN / 2) * BK * 4;  // own half of B
-    static constexpr int EPI_BYTES = EPI_WARPS * 32 * 36 * 4;
+    // per epilogue warp a 1024-aligned 5 KB slot: the 32 x 36 staging block,
+    // or the swizzled 32 x 32 TMA store box
+    static constexpr int EPI_SLOT = 5 * 1024;
+    static constexpr int EPI_BYTES = EPI_WARPS * EPI_SLOT;
     static constexpr int MAX_SMEM = 227 * 1024;
     __host__ __device__ static constexpr int stage_bytes(int nsplit) { return (A_BYTES + B_BYTES) * (nsplit == 1 ? 1 : 2); }
     __host__ __device__ static constexpr int stages(int nsplit) {
@@ -500,8 +523,8 @@ struct PairSmem {
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                    const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo, TcShape sh,
-                    Epi epi) {
+                    const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo,
+                    const __grid_constant__ CUtensorMap mapC, TcShape sh, Epi epi) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by offset from the __shared__ array, so the compiler
     // keeps the shared state space (LDS/STS, not generic LD/ST) for derived pointers
@@ -644,7 +667,9 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const int ew = warp - 4;
         const int quad = warp % 4;   // TMEM lanes 32*quad .. +31
         const int chalf = ew / 4;    // column half of the tile
-        float(*buf)[36] = reinterpret_cast<float(*)[36]>(epi_buf + ew * 32 * 36);
+        uint8_t* slot = reinterpret_cast<uint8_t*>(epi_buf) + ew * S::EPI_SLOT;
+        float(*buf)[36] = reinterpret_cast<float(*)[36]>(slot);
+        float* box = reinterpret_cast<float*>(slot);  // 32 rows x 128 B, 128-byte swizzle
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -662,6 +687,38 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
                 if (row0 < sh.M) {
+                    if constexpr (EpiTma<Epi>::value) {
+                        // the slot is free once the previous box's TMA store has read it
+                        if (lane == 0) bulk_wait_read();
+                        __syncwarp();
+                        int64_t gr0, gc0;
+                        if (epi.tma_block(row0, col0, sh.M, sh.N, gr0, gc0)) {
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) v[c] *= epi.alpha;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                *reinterpret_cast<float4*>(box + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                                    make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                            fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0) {
+                                tma_store_2d(&mapC, box, (int32_t)gc0, (int32_t)gr0);
+                                bulk_commit();
+                                bulk_wait_read();
+                            }
+                            __syncwarp();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c)
+                                box[c * 32 + ((((lane >> 2) ^ (c & 7)) << 2) | (lane & 3))] = v[c];
+                            fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0) {
+                                tma_store_2d(&mapC, box, (int32_t)gr0, (int32_t)gc0);
+                                bulk_commit();
+                            }
+                            continue;
+                        }
+                    }
                     stage_block(buf, v, lane);
                     if constexpr (EpiSplitK<Epi>::value)
                         epi.block_split((int)(t / ntiles), row0, col0, sh.M, sh.N, buf, v, lane);
@@ -675,6 +732,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if constexpr (EpiTma<Epi>::value)
+            if (lane == 0) bulk_wait_all();  // epilogue stores complete before exit
     }
     tc_fence_before();
     __syncthreads();
@@ -754,23 +813,10 @@ struct FusedSmem {
     }
 };
 
-// TMA store of one smem box; bulk-group bookkeeping
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
-                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
@@ -1232,7 +1278,12 @@ void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const 
     }
     const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN) * std::max(1, sh.ksplit);
     const int grid = 2 * (int)std::min<int64_t>(tiles, num_sms() / 2);
-    pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, sh, e);
+    CUtensorMap mc = a;  // unused unless the epilogue stores by TMA
+    if constexpr (EpiTma<Epi>::value) {
+        if (e.ldc % 4) throw CurvError(kContractError, "tensor-core symmetric store needs ldc % 4 == 0");
+        mc = make_map_h(e.c, e.ldc);
+    }
+    pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, mc, sh, e);
     CK_LAUNCH();
 }
 
