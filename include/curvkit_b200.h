@@ -154,6 +154,37 @@ int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const 
                           const int32_t* labels, int64_t n, int32_t precision, int64_t row_begin,
                           int64_t row_end, void* g, int64_t ldg, void* stream);
 
+/* Parameter-row-sharded top-k across GPUs (one process per GPU).  Rank r
+ * owns the contiguous parameter rows [p_begin, p_end) of
+ * curvkit_topk_shard_rows(model, nranks, r, ...): whole output-unit weight
+ * blocks and 4-aligned bias blocks, balanced by parameter count.  The
+ * solver all-reduces (NCCL, over NVLink) only the N x l product J X and the
+ * l x l Gram matrices; q receives this rank's rows of the eigenvectors
+ * ((p_end - p_begin) x k, row-major), lambda all k eigenvalues (identical on
+ * every rank).  NCCL is loaded at run time (the copy already in the process,
+ * else libnccl.so.2; CURVKIT_NCCL_LIB overrides).  TF32 only. */
+#define CURVKIT_COMM_ID_BYTES 128
+typedef struct curvkit_comm_s* curvkit_comm;
+int curvkit_comm_unique_id(uint8_t* id_out);
+int curvkit_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, curvkit_comm* out);
+int curvkit_comm_destroy(curvkit_comm comm);
+int curvkit_topk_shard_rows(const curvkit_model* model, int64_t nshards, int64_t shard, int64_t* p_begin,
+                            int64_t* p_end);
+int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params, const void* x,
+                                 const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
+                                 int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
+                                 void* stream, curvkit_comm comm);
+
+/* Matrix-free Jacobian operator on a parameter-row range (TF32, J never
+ * formed): transpose = 0: out (n x l) = J[:, p_begin:p_end] in, with in the
+ * (p_end - p_begin) x l rows of the range; transpose = 1: out ((p_end -
+ * p_begin) x l) = J[:, p_begin:p_end]^T in, in n x l.  ld_in must be a
+ * multiple of 32; the range must start and end on unit boundaries (any pair
+ * of curvkit_topk_shard_rows boundaries qualifies). */
+int curvkit_dev_jacobian_apply(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                               int64_t n, int32_t precision, int64_t p_begin, int64_t p_end, int32_t transpose,
+                               const void* in, int64_t ld_in, int64_t l, void* out, int64_t ld_out, void* stream);
+
 /* The curvature GEMM engine on its own (fp32 storage): C[m][n] = alpha *
  * sum_k A(m,k) B(n,k) with A(m,k) = a[m*lda+k] if a_kmajor else a[k*lda+m]
  * (likewise B).  TF32/TF32X3 run the tcgen05 kernel, F32 the SIMT one. */

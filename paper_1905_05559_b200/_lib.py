@@ -53,6 +53,12 @@ SIGNATURES = {
     "curvkit_dev_opg_shard": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
     "curvkit_dev_gemm": [i64, i64, i64, vptr, i64, i32, vptr, i64, i32, vptr, i64, C.c_float, i32, vptr],
     "curvkit_dev_opg_topk": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
+    "curvkit_comm_unique_id": [C.POINTER(C.c_uint8)],
+    "curvkit_comm_init": [C.POINTER(C.c_uint8), i32, i32, C.POINTER(vptr)],
+    "curvkit_comm_destroy": [vptr],
+    "curvkit_topk_shard_rows": [_MP, i64, i64, C.POINTER(i64), C.POINTER(i64)],
+    "curvkit_dev_opg_topk_sharded": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr, vptr],
+    "curvkit_dev_jacobian_apply": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, i32, vptr, i64, i64, vptr, i64, vptr],
 }
 _RESTYPES = {"curvkit_last_error": C.c_char_p, "curvkit_version": C.c_char_p, "curvkit_launch_count": i64}
 

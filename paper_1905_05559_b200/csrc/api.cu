@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/curvkit_b200.h"
+#include "comm.cuh"
 #include "common.cuh"
 #include "curvature.cuh"
 #include "eigen.cuh"
@@ -642,6 +643,89 @@ int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t ld
         Opnd<float> B = b_kmajor ? kmaj(b, ldb) : mnmaj(b, ldb);
         if (precision == kTF32 || precision == k3xTF32) gemm_tf32_store(precision, s, m, n, k, A, B, c, ldc, alpha);
         else CurvGemm<float, EpiStore<float>>::run(precision, s, m, n, k, A, B, e);
+    });
+}
+
+struct curvkit_comm_s {
+    ck::Comm c;
+};
+
+int curvkit_comm_unique_id(uint8_t* id_out) {
+    return guard([&] {
+        if (!id_out) contract("comm_unique_id: null output");
+        ncclUniqueId id;
+        nccl_check(NcclApi::get().get_unique_id(&id), "ncclGetUniqueId");
+        static_assert(sizeof(id.internal) == CURVKIT_COMM_ID_BYTES, "NCCL unique id size");
+        std::memcpy(id_out, id.internal, CURVKIT_COMM_ID_BYTES);
+    });
+}
+
+int curvkit_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, curvkit_comm* out) {
+    return guard([&] {
+        if (!id || !out) contract("comm_init: null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) contract("comm_init: need 0 <= rank < nranks");
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, CURVKIT_COMM_ID_BYTES);
+        ncclComm_t c = nullptr;
+        nccl_check(NcclApi::get().comm_init_rank(&c, nranks, u, rank), "ncclCommInitRank");
+        *out = new curvkit_comm_s{ck::Comm{c, rank, nranks}};
+    });
+}
+
+int curvkit_comm_destroy(curvkit_comm comm) {
+    return guard([&] {
+        if (!comm) return;
+        if (comm->c.comm) nccl_check(NcclApi::get().comm_destroy(comm->c.comm), "ncclCommDestroy");
+        delete comm;
+    });
+}
+
+int curvkit_topk_shard_rows(const curvkit_model* model, int64_t nshards, int64_t shard, int64_t* p_begin,
+                            int64_t* p_end) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (nshards < 1 || shard < 0 || shard >= nshards) contract("topk_shard_rows: need 0 <= shard < nshards");
+        const TopkShard t = TopkShard::make(md, nshards, shard);
+        if (p_begin) *p_begin = t.p0;
+        if (p_end) *p_end = t.p1;
+    });
+}
+
+int curvkit_dev_jacobian_apply(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                               int64_t n, int32_t precision, int64_t p_begin, int64_t p_end, int32_t transpose,
+                               const void* in, int64_t ld_in, int64_t l, void* out, int64_t ld_out, void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1 || l < 1) contract("jacobian_apply: empty operand");
+        if (precision != kTF32) contract("jacobian_apply needs TF32 precision");
+        if (ld_in % 32 || (transpose && ld_in < l) || (!transpose && ld_in < l))
+            contract("jacobian_apply: the input pitch must be a multiple of 32 and >= l");
+        cudaStream_t s = dev_stream(stream);
+        const TopkShard sh = TopkShard::range(md, p_begin, p_end);
+        Cache<float> c;
+        forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
+        if (!kr_supported(md, c)) contract("jacobian_apply: unsupported cache layout");
+        KrOperands op(md, c, s);
+        if (transpose)
+            kr_apply_jt(md, c, op, sh, (const float*)in, ld_in, l, (float*)out, ld_out, s);
+        else
+            kr_apply_j(md, c, op, sh, (const float*)in, ld_in, l, (float*)out, ld_out, s);
+    });
+}
+
+int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params, const void* x,
+                                 const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
+                                 int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
+                                 void* stream, curvkit_comm comm) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk: empty dataset");
+        if (!comm) contract("opg_topk_sharded: null communicator");
+        cudaStream_t s = dev_stream(stream);
+        if (precision != kTF32) contract("sharded opg_topk needs TF32 precision");
+        Cache<float> c;
+        forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
+        dev_topk<float>(md, c, k, oversample, power_iters, seed, precision, (float*)q, (float*)lambda, s, &comm->c);
     });
 }
 

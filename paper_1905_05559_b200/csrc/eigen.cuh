@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "curvature.cuh"
 #include "gemm_tc.cuh"
+#include "comm.cuh"
 #include "kr.cuh"
 #include "gemm_simt.cuh"
 #include "model.cuh"
@@ -38,15 +39,17 @@ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t i) {
 
 // Omega[p][c] ~ N(0, 1): Box-Muller on the counter-based splitmix64 stream
 template <class T>
-__global__ void gaussian_kernel(T* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= rows * cols) return;
+__global__ void gaussian_kernel(T* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0) {
+    const int64_t loc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (loc >= rows * cols) return;
+    // entry (row0 + r, c) of the global sketch: a shard draws exactly its rows
+    const int64_t idx = row0 * cols + loc;
     const uint64_t pair = (uint64_t)idx >> 1;
     const double u1 = 1.0 - (double)(splitmix_at(seed, 2 * pair) >> 11) * 0x1.0p-53;
     const double u2 = (double)(splitmix_at(seed, 2 * pair + 1) >> 11) * 0x1.0p-53;
     const double r = sqrt(-2.0 * log(u1));
     const double th = 6.283185307179586476925286766559 * u2;
-    out[(idx / cols) * ld + idx % cols] = (T)((idx & 1) ? r * sin(th) : r * cos(th));
+    out[(loc / cols) * ld + loc % cols] = (T)((idx & 1) ? r * sin(th) : r * cos(th));
 }
 
 // W[c][d] += sum_{p in chunk} Y[p][c] * Y[p][d]   (fp64 accumulation)
@@ -272,6 +275,8 @@ struct EigenWork {
     int prec;
     const Cache<T>* c = nullptr;
     const KrOperands* kr = nullptr;  // set: J X / J^T T from the activations (J never formed)
+    TopkShard sh{};                  // parameter rows of this rank (all of them unsharded)
+    const Comm* comm = nullptr;      // sums J X partials and Grams across ranks
 
     // Y <- orth(Y) (CholeskyQR2, fp64 Gram): pass 1 writes Y Rinv into the
     // scratch Y2, pass 2 writes back into Y; no host round trip
@@ -288,6 +293,7 @@ struct EigenWork {
             dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
             gram_kernel<T><<<g, 256, 0, s>>>(src, ld, rows, l, chunk, dptr<double>(W));
             CK_LAUNCH();
+            if (comm) comm->sum(dptr<double>(W), (size_t)(l * l), s);  // Gram of all ranks' rows
             chol_inv_kernel<<<1, 256, 0, s>>>(dptr<double>(W), l, sizeof(T) == 4 ? 1e-7 : 1e-14, dptr<double>(Rinv));
             CK_LAUNCH();
             convert_to<T>(dptr<double>(Rinv), dptr<T>(Rt), l * l);
@@ -308,7 +314,8 @@ struct EigenWork {
         ProfScope ps("eig_apply_j", s, 2.0 * (double)n * md.P * l, kr ? 0.0 : (double)sizeof(T) * n * md.P);
         if constexpr (std::is_same_v<T, float>) {
             if (kr) {
-                kr_apply_j(md, *c, *kr, X, ldx, l, Tout, ldt, s);
+                kr_apply_j(md, *c, *kr, sh, X, ldx, l, Tout, ldt, s);
+                if (comm) comm->sum(Tout, (size_t)(n * ldt), s);  // J X = sum over ranks' rows
                 return;
             }
             if (prec == kTF32 || prec == k3xTF32) {  // split-K: only ceil(N/256) row tiles
@@ -325,7 +332,7 @@ struct EigenWork {
         ProfScope ps("eig_apply_jt", s, 2.0 * (double)n * md.P * l, kr ? 0.0 : (double)sizeof(T) * n * md.P);
         if constexpr (std::is_same_v<T, float>) {
             if (kr) {
-                kr_apply_jt(md, *c, *kr, Tn, ldt, l, Y, ldy, s);
+                kr_apply_jt(md, *c, *kr, sh, Tn, ldt, l, Y, ldy, s);
                 return;
             }
         }
@@ -334,12 +341,19 @@ struct EigenWork {
     }
 };
 
-// Core driver: leaves eigenvectors (P x k, row-major, ld k) in q_dev and
-// eigenvalues (k, descending) in lam_host.
+// Core driver: leaves eigenvectors (rows of this rank's shard x k, row-major,
+// ld k) in q_dev and eigenvalues (k, descending) in lam_host.  With a
+// communicator of nranks > 1 each rank holds the parameter rows of
+// TopkShard::make(md, nranks, rank); the only exchanges are all-reduces of
+// the N x l product J X and of the l x l Grams.
 template <class T>
 void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
-               uint64_t seed, int prec, T* q_dev, std::vector<double>& lam_host, cudaStream_t s) {
+               uint64_t seed, int prec, T* q_dev, std::vector<double>& lam_host, cudaStream_t s,
+               const Comm* comm = nullptr) {
     const int64_t n = c.n, P = md.P;
+    const bool sharded = comm && comm->nranks > 1;
+    const TopkShard sh = TopkShard::make(md, sharded ? comm->nranks : 1, sharded ? comm->rank : 0);
+    const int64_t R = sh.rows();
     if (k < 1 || k > std::min(n, P))
         throw CurvError(kContractError, "opg_topk: need 1 <= k <= min(N, P), got k = " + std::to_string(k));
     if (oversample < 0 || power_iters < 0) throw CurvError(kContractError, "opg_topk: negative oversample/power_iters");
@@ -350,29 +364,34 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     std::unique_ptr<KrOperands> krop;
     if constexpr (std::is_same_v<T, float>)
         if (prec == kTF32 && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
+    if (sharded && !krop) throw CurvError(kContractError, "sharded opg_topk needs TF32 precision");
     const int64_t ldj = krop ? 0 : round_up(P, 32);
     DevMem J((size_t)n * ldj * sizeof(T), s);
     if (!krop) jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
-    DevMem Y((size_t)P * ldl * sizeof(T), s), Om((size_t)P * ldl * sizeof(T), s), Y2((size_t)P * ldl * sizeof(T), s);
+    const size_t rbytes = (size_t)std::max<int64_t>(R, 1) * ldl * sizeof(T);
+    DevMem Y(rbytes, s), Om(rbytes, s), Y2(rbytes, s);
     DevMem Tn((size_t)n * ldl * sizeof(T), s);
+    CK_CUDA(cudaMemsetAsync(Tn.p, 0, (size_t)n * ldl * sizeof(T), s));
     {
-        ProfScope ps("eig_sketch", s, 0.0, (double)sizeof(T) * P * ldl);
-        CK_CUDA(cudaMemsetAsync(Om.p, 0, (size_t)P * ldl * sizeof(T), s));
-        gaussian_kernel<T><<<blocks_for(P * l), 256, 0, s>>>(dptr<T>(Om), P, l, ldl, seed);
-        CK_LAUNCH();
+        ProfScope ps("eig_sketch", s, 0.0, (double)sizeof(T) * R * ldl);
+        CK_CUDA(cudaMemsetAsync(Om.p, 0, rbytes, s));
+        if (R > 0) {
+            gaussian_kernel<T><<<blocks_for(R * l), 256, 0, s>>>(dptr<T>(Om), R, l, ldl, seed, sh.p0);
+            CK_LAUNCH();
+        }
     }
-    EigenWork<T> ew{md, s, prec, &c, krop.get()};
+    EigenWork<T> ew{md, s, prec, &c, krop.get(), sh, sharded ? comm : nullptr};
     T* X = dptr<T>(Om);
     for (int64_t it = 0; it <= power_iters; ++it) {
         ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
         ew.apply_jt(dptr<T>(J), ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
-        ew.orth(dptr<T>(Y), dptr<T>(Y2), P, l, ldl);
+        ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl);
         X = dptr<T>(Y);
     }
     // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q) with round-to-nearest TF32
     // operands (J stored rounded, Q rounded per GEMM): unbiased products.
     ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
-    ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l + 2.0 * (double)P * l * k, 0.0);
+    ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l + 2.0 * (double)R * l * k, 0.0);
     DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
     CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));
     {
@@ -406,7 +425,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     DevMem Vk((size_t)l * k * sizeof(T), s);
     CK_CUDA(cudaMemcpyAsync(Vk.p, vk.data(), l * k * sizeof(T), cudaMemcpyHostToDevice, s));
     EpiStore<T> e{q_dev, k, 0, T(1), T(0)};
-    gemm_simt<T>(s, P, k, l, 1, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
+    if (R > 0) gemm_simt<T>(s, R, k, l, 1, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
     CK_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -425,9 +444,9 @@ void host_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
 
 template <class T>
 void dev_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
-              uint64_t seed, int prec, T* q_dev, T* lam_dev, cudaStream_t s) {
+              uint64_t seed, int prec, T* q_dev, T* lam_dev, cudaStream_t s, const Comm* comm = nullptr) {
     std::vector<double> lam;
-    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s);
+    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s, comm);
     std::vector<T> hl(lam.begin(), lam.end());
     CK_CUDA(cudaMemcpyAsync(lam_dev, hl.data(), k * sizeof(T), cudaMemcpyHostToDevice, s));
     CK_CUDA(cudaStreamSynchronize(s));

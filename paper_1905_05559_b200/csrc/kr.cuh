@@ -41,7 +41,7 @@ namespace pair {
 
 struct KrArgs {
     int64_t mt;           // row tiles (JX: n-tiles of 256 examples; JT: i-tiles of 256 inputs)
-    int64_t nop;          // o pairs: ceil(T_{k+1} / 2)
+    int64_t nop;          // o pairs: ceil((oend - o0) / 2)
     int64_t chunk;        // JX: o pairs per work unit
     int64_t nk;           // k-blocks per o pair (JX: ceil(T_k / 32); JT: ceil(n / 32))
     int64_t tk, to, woff;  // T_k, T_{k+1}, first weight row of layer k in X / Y
@@ -53,6 +53,8 @@ struct KrArgs {
     int64_t rows;          // JX: n ; JT: T_k
     int64_t l;             // live columns of this 128-wide column tile
     int64_t ksplit;        // JT: example slabs (partial Y in slab ks of out)
+    int64_t o0, oend;      // output units o0 .. oend - 1 of the layer (a shard's range)
+    int64_t prow0;         // parameter row held at row 0 of X (JX) / Y (JT)
 };
 
 constexpr int KR_BN = 256;
@@ -149,7 +151,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                 unit_of(u, mi, op0, op1, kb0, kb1, sl);
                 const int64_t r0 = mi * 256 + 128 * rank;  // this CTA's A rows
                 for (int64_t op = op0; op < op1; ++op) {
-                    const int64_t o = 2 * op + rank;         // this CTA's output unit
+                    const int64_t o = ka.o0 + 2 * op + rank;  // this CTA's output unit
                     for (int64_t kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = stage_base + stage * C::STAGE_BYTES;
@@ -166,7 +168,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                             else mbar_arrive_cluster(fb);
                             load_tile2<128>(sa, &mapA, fb, 0, 0, r0, k0, pol);
                             // rows of X past this unit's T_k meet zero-filled A columns
-                            load_tile2<128>(sb, &mapB, fb, 1, b3d, 0, ka.woff + o * ka.tk + k0, pol);
+                            load_tile2<128>(sb, &mapB, fb, 1, b3d, 0, ka.woff + o * ka.tk + k0 - ka.prow0, pol);
                         }
                         if (++stage == NST) { stage = 0; phase ^= 1; }
                     }
@@ -220,10 +222,10 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         for (int64_t u = pair_id; u < nunits; u += npairs) {
             int64_t mi, op0, op1, kb0, kb1, sl;
             unit_of(u, mi, op0, op1, kb0, kb1, sl);
-            const int64_t o = 2 * op0 + rank;
+            const int64_t o = ka.o0 + 2 * op0 + rank;
             // delta_k^T row o, eight k-blocks ahead of the stages that need them
-            const float* drow = ka.delta + (o < ka.to ? o : 0) * ka.ldd + klo;
-            const float live = o < ka.to ? 1.f : 0.f;
+            const float* drow = ka.delta + (o < ka.oend ? o : ka.o0) * ka.ldd + klo;
+            const float live = o < ka.oend ? 1.f : 0.f;
             for (int64_t kbg = kb0; kbg < kb1; kbg += 8) {
                 float d0[8], d1[8];
 #pragma unroll
@@ -278,8 +280,8 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                     tc_fence_after();
 #pragma unroll
                     for (int x = 0; x < 2; ++x) {
-                        const int64_t o = 2 * op + x;
-                        const float dv = (live && o < ka.to) ? __ldg(ka.delta + nrow * ka.ldd + o) : 0.f;
+                        const int64_t o = ka.o0 + 2 * op + x;
+                        const float dv = (live && o < ka.oend) ? __ldg(ka.delta + nrow * ka.ldd + o) : 0.f;
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             float v[32];
@@ -304,13 +306,13 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                 tc_fence_after();
                 // TMEM columns 128*chalf.. hold output unit o; lane = input i,
                 // whose 32-column run of Y row (woff + o T_k + i) is contiguous
-                const int64_t o = 2 * op0 + chalf;
+                const int64_t o = ka.o0 + 2 * op0 + chalf;
                 const int64_t i = row0 + lane;
-                float* yrow = ka.out + sl * ka.slab + (ka.woff + o * ka.tk + i) * ka.ldo;
+                float* yrow = ka.out + sl * ka.slab + (ka.woff + o * ka.tk + i - ka.prow0) * ka.ldo;
                 const bool vec = (ka.ldo & 3) == 0;
                 for (int cb = 0; cb < 4; ++cb) {
                     const int64_t c0 = cb * 32;
-                    if (c0 >= ka.l || o >= ka.to) break;
+                    if (c0 >= ka.l || o >= ka.oend) break;
                     float v[32];
                     tmem_ld32(lane_base + (uint32_t)(acc * KR_BN + chalf * 128 + cb * 32), v);
                     if (i < ka.rows) {
@@ -421,45 +423,110 @@ void kr_launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, con
     CK_LAUNCH();
 }
 
-// T (n x l, ldt) = J X for X (P x l, ldx; ldx a multiple of 32)
-inline void kr_apply_j(const ModelDesc& md, const Cache<float>& c, const KrOperands& op, const float* X, int64_t ldx,
-                       int64_t l, float* T, int64_t ldt, cudaStream_t s) {
-    const int64_t n = c.n, P = md.P;
+// Contiguous parameter rows [p0, p1) of one rank of the sharded top-k
+// solver, cut at output-unit weight blocks (T_k rows each) and at 4-aligned
+// bias blocks, balanced by parameter count (the J X and J^T T work of a row is
+// proportional to it).  Per layer: the output units [oa, ob) whose weight
+// rows the rank owns and its biases [ba, bb).
+struct TopkShard {
+    int64_t p0 = 0, p1 = 0;
+    int64_t oa[kMaxLayers] = {}, ob[kMaxLayers] = {}, ba[kMaxLayers] = {}, bb[kMaxLayers] = {};
+    int64_t rows() const { return p1 - p0; }
+
+    // rows [p0, p1), which must start and end on unit boundaries
+    static TopkShard range(const ModelDesc& md, int64_t p0, int64_t p1) {
+        auto on_cut = [&](int64_t p) {
+            if (p == 0 || p == md.P) return true;
+            for (int k = 0; k < md.S; ++k) {
+                if (p >= md.woff[k] && p < md.boff[k]) return (p - md.woff[k]) % md.w[k] == 0;
+                if (p >= md.boff[k] && p <= md.boff[k] + md.w[k + 1]) return (p - md.boff[k]) % 4 == 0 || p == md.boff[k] + md.w[k + 1];
+            }
+            return false;
+        };
+        if (p0 < 0 || p1 > md.P || p0 > p1 || !on_cut(p0) || !on_cut(p1))
+            throw CurvError(kContractError, "parameter range must start and end on an output-unit weight block or a "
+                                            "4-aligned bias block");
+        TopkShard t;
+        t.p0 = p0;
+        t.p1 = p1;
+        for (int k = 0; k < md.S; ++k) {
+            const int64_t tk = md.w[k], to = md.w[k + 1];
+            auto units = [&](int64_t p) { return std::min(to, ceil_div(std::max<int64_t>(p - md.woff[k], 0), tk)); };
+            auto biases = [&](int64_t p) { return std::min(to, std::max<int64_t>(p - md.boff[k], 0)); };
+            t.oa[k] = units(p0);
+            t.ob[k] = units(p1);
+            t.ba[k] = biases(p0);
+            t.bb[k] = biases(p1);
+        }
+        return t;
+    }
+
+    static TopkShard make(const ModelDesc& md, int64_t nshards, int64_t shard) {
+        // unit boundaries in parameter order
+        std::vector<int64_t> cut;
+        for (int k = 0; k < md.S; ++k) {
+            for (int64_t o = 0; o < md.w[k + 1]; ++o) cut.push_back(md.woff[k] + o * md.w[k]);
+            for (int64_t b = 0; b < md.w[k + 1]; b += 4) cut.push_back(md.boff[k] + b);
+        }
+        cut.push_back(md.P);
+        auto bound = [&](int64_t s) -> int64_t {
+            if (s <= 0) return 0;
+            if (s >= nshards) return md.P;
+            const double target = (double)md.P * (double)s / (double)nshards;
+            return *std::lower_bound(cut.begin(), cut.end(), (int64_t)std::ceil(target));
+        };
+        return range(md, bound(shard), bound(shard + 1));
+    }
+};
+
+// T (n x l, ldt) = J[:, shard rows] X for X = the shard's rows (sh.rows() x l,
+// ldx a multiple of 32).  Unsharded: TopkShard::make(md, 1, 0).
+inline void kr_apply_j(const ModelDesc& md, const Cache<float>& c, const KrOperands& op, const TopkShard& sh,
+                       const float* X, int64_t ldx, int64_t l, float* T, int64_t ldt, cudaStream_t s) {
+    const int64_t n = c.n, R = sh.rows();
     const int64_t pairs = tc::num_sms() / 2;
     const int64_t mt = ceil_div(n, 256);
     // X rounded to nearest TF32 with zero padding columns
-    DevMem xr((size_t)P * ldx * sizeof(float), s);
-    tc::round_pad_kernel<<<(unsigned)std::min<int64_t>(ceil_div(P * ldx / 4, 256), 148 * 16), 256, 0, s>>>(
-        X, dptr<float>(xr), P, l, ldx);
+    DevMem xr((size_t)R * ldx * sizeof(float), s);
+    tc::round_pad_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * ldx / 4, 256), 148 * 16)),
+                           256, 0, s>>>(X, dptr<float>(xr), R, l, ldx);
     CK_LAUNCH();
     // work split: each layer's o pairs cut into chunks so ~8 units per SM pair
-    int64_t chunk[kMaxLayers], nslab = 0, base[kMaxLayers];
+    int64_t chunk[kMaxLayers] = {}, nslab = 0, base[kMaxLayers] = {}, bslab[kMaxLayers] = {};
     for (int k = 0; k < md.S; ++k) {
-        const int64_t nop = ceil_div(md.w[k + 1], 2);
-        const int64_t want = std::max<int64_t>(1, ceil_div(8 * pairs, mt));
-        chunk[k] = ceil_div(nop, std::min(nop, want));
+        const int64_t nop = ceil_div(sh.ob[k] - sh.oa[k], 2);
         base[k] = nslab;
-        nslab += ceil_div(nop, chunk[k]);
+        if (nop > 0) {
+            const int64_t want = std::max<int64_t>(1, ceil_div(8 * pairs, mt));
+            chunk[k] = ceil_div(nop, std::min(nop, want));
+            nslab += ceil_div(nop, chunk[k]);
+        }
     }
-    const int64_t bias_base = nslab;
-    nslab += md.S;
+    for (int k = 0; k < md.S; ++k) bslab[k] = sh.bb[k] > sh.ba[k] ? nslab++ : -1;
     const int64_t ldw = 128, slab = n * ldw;
+    if (nslab == 0) {  // a shard without rows contributes zeros
+        CK_CUDA(cudaMemset2DAsync(T, ldt * sizeof(float), 0, l * sizeof(float), n, s));
+        return;
+    }
     DevMem ws((size_t)(nslab * slab) * sizeof(float), s);
     for (int64_t c0 = 0; c0 < l; c0 += 128) {
         const int64_t lc = std::min<int64_t>(128, l - c0);
         const float* xc = dptr<float>(xr) + c0;
         const int b3 = ldx >= round_up(lc, 32) ? 1 : 0;
         for (int k = 0; k < md.S; ++k) {
-            const int64_t tk = md.w[k], to = md.w[k + 1];
-            CUtensorMap ma = tc::make_map(op.a[k], n, tk, c.lda[k], 0, 128);
-            CUtensorMap mb = tc::make_map(xc, lc, P, ldx, 1, 128, b3);
-            tc::pair::KrArgs ka{mt, ceil_div(to, 2), chunk[k], ceil_div(tk, tc::BK), tk, to, md.woff[k],
-                                c.delta[k], c.ldt[k], n, dptr<float>(ws) + base[k] * slab, ldw, slab, n, lc, 1};
-            kr_launch<false>(s, ma, mb, ka, 0, b3);
-            // bias tangents: delta_k Xb_k
-            gemm_tf32(kTF32, s, n, lc, to, pre_rounded(kmaj(op.d[k], c.ldt[k])),
-                      pre_rounded(mnmaj(xc + md.boff[k] * ldx, ldx)),
-                      EpiStore<float>{dptr<float>(ws) + (bias_base + k) * slab, ldw, 0, 1.f, 0.f});
+            const int64_t tk = md.w[k];
+            if (sh.ob[k] > sh.oa[k]) {
+                CUtensorMap ma = tc::make_map(op.a[k], n, tk, c.lda[k], 0, 128);
+                CUtensorMap mb = tc::make_map(xc, lc, R, ldx, 1, 128, b3);
+                tc::pair::KrArgs ka{mt, ceil_div(sh.ob[k] - sh.oa[k], 2), chunk[k], ceil_div(tk, tc::BK), tk,
+                                    md.w[k + 1], md.woff[k], c.delta[k], c.ldt[k], n,
+                                    dptr<float>(ws) + base[k] * slab, ldw, slab, n, lc, 1, sh.oa[k], sh.ob[k], sh.p0};
+                kr_launch<false>(s, ma, mb, ka, 0, b3);
+            }
+            if (bslab[k] >= 0)  // bias tangents: delta_k[:, ba..bb) Xb
+                gemm_tf32(kTF32, s, n, lc, sh.bb[k] - sh.ba[k], pre_rounded(kmaj(op.d[k] + sh.ba[k], c.ldt[k])),
+                          pre_rounded(mnmaj(xc + (md.boff[k] + sh.ba[k] - sh.p0) * ldx, ldx)),
+                          EpiStore<float>{dptr<float>(ws) + bslab[k] * slab, ldw, 0, 1.f, 0.f});
         }
         tc::slab_sum_kernel<<<(unsigned)ceil_div(n * (ldw / 4), 256), 256, 0, s>>>(dptr<float>(ws), ldw, slab,
                                                                                   (int)nslab, n, lc, 1.f, T + c0, ldt);
@@ -467,9 +534,10 @@ inline void kr_apply_j(const ModelDesc& md, const Cache<float>& c, const KrOpera
     }
 }
 
-// Y (P x l, ldy) = J^T T for T (n x l, ldtn; ldtn a multiple of 32)
-inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOperands& op, const float* Tn,
-                        int64_t ldtn, int64_t l, float* Y, int64_t ldy, cudaStream_t s) {
+// Y (shard rows x l, ldy) = J[:, shard rows]^T T for T (n x l, ldtn; ldtn a
+// multiple of 32)
+inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOperands& op, const TopkShard& sh,
+                        const float* Tn, int64_t ldtn, int64_t l, float* Y, int64_t ldy, cudaStream_t s) {
     const int64_t n = c.n;
     const int64_t pairs = tc::num_sms() / 2;
     for (int64_t c0 = 0; c0 < l; c0 += 128) {
@@ -478,31 +546,36 @@ inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOper
         const int b3 = ldtn >= round_up(lc, 32) ? 1 : 0;
         CUtensorMap mb = tc::make_map(tc0, lc, n, ldtn, 1, 128, b3);
         for (int k = 0; k < md.S; ++k) {
-            const int64_t tk = md.w[k], to = md.w[k + 1];
-            const int a3 = c.lda[k] >= round_up(tk, 32) ? 1 : 0;
-            CUtensorMap ma = tc::make_map(op.a[k], tk, n, c.lda[k], 1, 128, a3);
-            const int64_t mt = ceil_div(tk, 256), nop = ceil_div(to, 2), nk = ceil_div(n, tc::BK);
-            // few (i-tile, o-pair) units (a narrow layer): split the examples
-            // into slabs of partial products, summed in fixed order after
-            int64_t ks = 1;
-            if (mt * nop < 2 * pairs) ks = std::max<int64_t>(1, std::min(ceil_div(4 * pairs, mt * nop), nk / 8));
-            if (ks > 1) ks = ceil_div(nk, ceil_div(nk, ks));  // every slab non-empty
-            if (ks == 1) {
-                tc::pair::KrArgs ka{mt, nop, 1, nk, tk, to, md.woff[k], op.dT[k], op.ldn, n, Y + c0, ldy, 0, tk, lc, 1};
-                kr_launch<true>(s, ma, mb, ka, a3, b3);
-            } else {
-                const int64_t rows = to * tk, slab = rows * 128;
-                DevMem ws((size_t)(ks * slab) * sizeof(float), s);
-                tc::pair::KrArgs ka{mt, nop, 1, nk, tk, to, 0, op.dT[k], op.ldn, n, dptr<float>(ws), 128, slab, tk,
-                                    lc, ks};
-                kr_launch<true>(s, ma, mb, ka, a3, b3);
-                tc::slab_sum_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, s>>>(
-                    dptr<float>(ws), 128, slab, (int)ks, rows, lc, 1.f, Y + md.woff[k] * ldy + c0, ldy);
-                CK_LAUNCH();
+            const int64_t tk = md.w[k], oa = sh.oa[k], ob = sh.ob[k];
+            if (ob > oa) {
+                const int a3 = c.lda[k] >= round_up(tk, 32) ? 1 : 0;
+                CUtensorMap ma = tc::make_map(op.a[k], tk, n, c.lda[k], 1, 128, a3);
+                const int64_t mt = ceil_div(tk, 256), nop = ceil_div(ob - oa, 2), nk = ceil_div(n, tc::BK);
+                // few (i-tile, o-pair) units (a narrow layer): split the examples
+                // into slabs of partial products, summed in fixed order after
+                int64_t ks = 1;
+                if (mt * nop < 2 * pairs) ks = std::max<int64_t>(1, std::min(ceil_div(4 * pairs, mt * nop), nk / 8));
+                if (ks > 1) ks = ceil_div(nk, ceil_div(nk, ks));  // every slab non-empty
+                if (ks == 1) {
+                    tc::pair::KrArgs ka{mt, nop, 1, nk, tk, md.w[k + 1], md.woff[k], op.dT[k], op.ldn, n, Y + c0, ldy,
+                                        0, tk, lc, 1, oa, ob, sh.p0};
+                    kr_launch<true>(s, ma, mb, ka, a3, b3);
+                } else {
+                    // slab rows (o - oa) T_k + i: woff 0 and prow0 = oa T_k
+                    const int64_t rows = (ob - oa) * tk, slab = rows * 128;
+                    DevMem ws((size_t)(ks * slab) * sizeof(float), s);
+                    tc::pair::KrArgs ka{mt, nop, 1, nk, tk, md.w[k + 1], 0, op.dT[k], op.ldn, n, dptr<float>(ws),
+                                        128, slab, tk, lc, ks, oa, ob, oa * tk};
+                    kr_launch<true>(s, ma, mb, ka, a3, b3);
+                    tc::slab_sum_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, s>>>(
+                        dptr<float>(ws), 128, slab, (int)ks, rows, lc, 1.f,
+                        Y + (md.woff[k] + oa * tk - sh.p0) * ldy + c0, ldy);
+                    CK_LAUNCH();
+                }
             }
-            // bias rows: delta_k^T T (short M, long K: split over K)
-            gemm_tf32_store(kTF32, s, to, lc, n, pre_rounded(mnmaj(op.d[k], c.ldt[k])), mnmaj(tc0, ldtn),
-                            Y + md.boff[k] * ldy + c0, ldy);
+            if (sh.bb[k] > sh.ba[k])  // bias rows: delta_k[:, ba..bb)^T T (short M, long K: split over K)
+                gemm_tf32_store(kTF32, s, sh.bb[k] - sh.ba[k], lc, n, pre_rounded(mnmaj(op.d[k] + sh.ba[k], c.ldt[k])),
+                                mnmaj(tc0, ldtn), Y + (md.boff[k] + sh.ba[k] - sh.p0) * ldy + c0, ldy);
         }
     }
 }

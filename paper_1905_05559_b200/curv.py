@@ -429,3 +429,60 @@ def dev_opg_shard(spec, params, x, labels, n, row_begin, row_end, out, ldg, prec
     _lib.check(_lib.load().curvkit_dev_opg_shard(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
                                                   _prec(precision), row_begin, row_end, _ptr(out), ldg,
                                                   _stream(stream)))
+
+
+# ---- multi-GPU top-k (parameter-row shards, NCCL all-reduce of J X) --------
+
+def topk_shard_rows(spec: ModelSpec, nshards: int, shard: int):
+    """Parameter rows [begin, end) owned by `shard` in the sharded top-k solver
+    (whole output-unit weight blocks and 4-aligned bias blocks, balanced by
+    parameter count)."""
+    b, e = C.c_int64(), C.c_int64()
+    _lib.check(_lib.load().curvkit_topk_shard_rows(C.byref(spec._c()), nshards, shard, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+class Comm:
+    """One rank of an NCCL communicator owned by the library.  Build it with
+    `Comm.create(rank, world, broadcast)` where `broadcast(bytes) -> bytes`
+    ships rank 0's 128-byte id to every rank (e.g. over torch.distributed)."""
+
+    def __init__(self, handle, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _lib.check(_lib.load().curvkit_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def create(cls, rank: int, world: int, broadcast):
+        uid = broadcast(cls.unique_id() if rank == 0 else None)
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _lib.check(_lib.load().curvkit_comm_init(buf, world, rank, C.byref(h)))
+        return cls(h, rank, world)
+
+    def close(self):
+        if self.handle is not None:
+            _lib.check(_lib.load().curvkit_comm_destroy(self.handle))
+            self.handle = None
+
+
+def dev_opg_topk_sharded(spec, params, x, labels, n, k, oversample, power_iters, seed, q, lam, comm: Comm,
+                         precision="tf32", stream=None):
+    """Top-k eigenpairs of G with the parameter rows sharded over comm's ranks:
+    q receives this rank's rows (topk_shard_rows) x k, lam all k values."""
+    _lib.check(_lib.load().curvkit_dev_opg_topk_sharded(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n, k,
+                                                         oversample, power_iters, seed, _prec(precision), _ptr(q),
+                                                         _ptr(lam), _stream(stream), comm.handle))
+
+
+def dev_jacobian_apply(spec, params, x, labels, n, p_begin, p_end, inp, ld_in, l, out, ld_out, transpose=False,
+                       precision="tf32", stream=None):
+    """Matrix-free J[:, p_begin:p_end] @ inp (transpose=False) or its
+    transpose, with J never formed (TF32 Khatri-Rao kernels)."""
+    _lib.check(_lib.load().curvkit_dev_jacobian_apply(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
+                                                       _prec(precision), p_begin, p_end, 1 if transpose else 0,
+                                                       _ptr(inp), ld_in, l, _ptr(out), ld_out, _stream(stream)))
