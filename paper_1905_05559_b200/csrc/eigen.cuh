@@ -85,6 +85,206 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ Y, int6
     }
 }
 
+// W += Y^T Y over a chunk of rows (fp64): 64 x 64 output tiles of the lower
+// triangle (blockIdx.x: tile, blockIdx.y: row chunk), 4 x 4 register
+// micro-tiles per thread (rows tr + 16u, columns tc + 16v), the row panels
+// staged in shared memory as fp64.
+template <class T>
+__global__ void __launch_bounds__(256) gram64_kernel(const T* __restrict__ Y, int64_t ld, int64_t rows, int64_t l,
+                                                     int64_t chunk, double* __restrict__ W) {
+    __shared__ double As[32][64], Bs[32][64];
+    // lower tile (ci, di), di <= ci, from the triangular index
+    int ci = 0;
+    while ((ci + 1) * (ci + 2) / 2 <= (int)blockIdx.x) ++ci;
+    const int di = (int)blockIdx.x - ci * (ci + 1) / 2;
+    const int64_t c0 = ci * 64, d0 = di * 64;
+    const int64_t p0 = blockIdx.y * chunk, p1 = min(rows, p0 + chunk);
+    const int t = threadIdx.x, tr = t / 16, tc = t % 16;
+    double acc[4][4] = {};
+    // the next 32-row panel is fetched into registers while this one is used
+    T ra[8], rb[8];
+    auto fetch = [&](int64_t p) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int e = t + 256 * j, r = e / 64, cc = e % 64;
+            const int64_t pp = p + r;
+            ra[j] = (pp < p1 && c0 + cc < l) ? Y[pp * ld + c0 + cc] : T(0);
+            rb[j] = (pp < p1 && d0 + cc < l) ? Y[pp * ld + d0 + cc] : T(0);
+        }
+    };
+    if (p0 < p1) fetch(p0);
+    for (int64_t p = p0; p < p1; p += 32) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int e = t + 256 * j, r = e / 64, cc = e % 64;
+            As[r][cc] = (double)ra[j];
+            Bs[r][cc] = (double)rb[j];
+        }
+        __syncthreads();
+        if (p + 32 < p1) fetch(p + 32);
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // interleaved micro-tile: conflict-free rows of Bs
+                a[u] = As[r][tr + 16 * u];
+                b[u] = Bs[r][tc + 16 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t c = c0 + tr + 16 * u, d = d0 + tc + 16 * v;
+            if (c >= l || d >= l) continue;
+            if (ci == di) {
+                atomicAdd(&W[c * l + d], acc[u][v]);  // diagonal tile: both halves computed
+            } else {
+                atomicAdd(&W[c * l + d], acc[u][v]);
+                atomicAdd(&W[d * l + c], acc[u][v]);
+            }
+        }
+}
+
+// W += Y^T Y (fp64) on the FP64 tensor cores: mma.sync m8n8k4 f64.  A block
+// owns a 64 x 64 lower tile (blockIdx.x) over a row chunk (blockIdx.y); four
+// warps each accumulate a 32 x 32 quarter as 4 x 4 fragments of 8 x 8.  Both
+// MMA operands are plain elements of Y: A(c, p) = Y[p][c], B(p, d) = Y[p][d],
+// staged per 32-row panel in shared memory (fp64, odd pitch).
+__device__ __forceinline__ void dmma_8x8x4(double* c, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <class T>
+__global__ void __launch_bounds__(128) gram_dmma_kernel(const T* __restrict__ Y, int64_t ld, int64_t rows, int64_t l,
+                                                        int64_t chunk, double* __restrict__ W) {
+    constexpr int LD = 65;  // odd pitch (doubles): the 4 k-rows of a fragment hit different banks
+    __shared__ double As[32 * LD], Bs[32 * LD];
+    int ci = 0;
+    while ((ci + 1) * (ci + 2) / 2 <= (int)blockIdx.x) ++ci;
+    const int di = (int)blockIdx.x - ci * (ci + 1) / 2;
+    const int64_t c0 = ci * 64, d0 = di * 64;
+    const int64_t p0 = blockIdx.y * chunk, p1 = min(rows, p0 + chunk);
+    const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const int wc = (warp >> 1) * 32, wd = (warp & 1) * 32;  // warp quarter of the 64 x 64 tile
+    const int fr = lane >> 2, fk = lane & 3;                  // fragment row / k of this lane
+    double acc[4][4][2] = {};
+    T ra[16], rb[16];
+    auto fetch = [&](int64_t p) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int e = t + 128 * j, r = e / 64, cc = e % 64;
+            const int64_t pp = p + r;
+            ra[j] = (pp < p1 && c0 + cc < l) ? Y[pp * ld + c0 + cc] : T(0);
+            rb[j] = (pp < p1 && d0 + cc < l) ? Y[pp * ld + d0 + cc] : T(0);
+        }
+    };
+    if (p0 < p1) fetch(p0);
+    for (int64_t p = p0; p < p1; p += 32) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int e = t + 128 * j, r = e / 64, cc = e % 64;
+            As[r * LD + cc] = (double)ra[j];
+            Bs[r * LD + cc] = (double)rb[j];
+        }
+        __syncthreads();
+        if (p + 32 < p1) fetch(p + 32);
+#pragma unroll
+        for (int k4 = 0; k4 < 32; k4 += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                a[f] = As[(k4 + fk) * LD + wc + 8 * f + fr];  // A(c = wc + 8f + fr, k)
+                b[f] = Bs[(k4 + fk) * LD + wd + 8 * f + fr];  // B(k, d = wd + 8f + fr)
+            }
+#pragma unroll
+            for (int fa = 0; fa < 4; ++fa)
+#pragma unroll
+                for (int fb = 0; fb < 4; ++fb) dmma_8x8x4(acc[fa][fb], a[fa], b[fb]);
+        }
+        __syncthreads();
+    }
+    // D fragment: row fr, columns 2 fk + {0, 1}
+#pragma unroll
+    for (int fa = 0; fa < 4; ++fa)
+#pragma unroll
+        for (int fb = 0; fb < 4; ++fb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t c = c0 + wc + 8 * fa + fr, d = d0 + wd + 8 * fb + 2 * fk + h;
+                if (c >= l || d >= l) continue;
+                atomicAdd(&W[c * l + d], acc[fa][fb][h]);
+                if (ci != di) atomicAdd(&W[d * l + c], acc[fa][fb][h]);
+            }
+}
+
+// Shifted Cholesky W + shift I = R^T R and Rinv = R^{-1} in one CTA with the
+// l x l matrix in shared memory (l <= 160): right-looking factorisation, then
+// the in-place column-by-column inverse of the upper triangle.  The shift is
+// rel * trace(W) / l (shifted CholeskyQR keeps rank-deficient Grams defined).
+__global__ void __launch_bounds__(1024) chol_inv_smem_kernel(const double* __restrict__ Wg, int l, double rel,
+                                                             double* __restrict__ Rinv) {
+    extern __shared__ double R[];  // l x l, row-major
+    __shared__ double shift_s;
+    __shared__ double red[32];
+    const int t = threadIdx.x, nt = blockDim.x;
+    double part = 0.0;
+    for (int i = t; i < l * l; i += nt) {
+        const double v = Wg[i];
+        R[i] = v;
+        if (i / l == i % l) part += v;
+    }
+    for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    if ((t & 31) == 0) red[t >> 5] = part;
+    __syncthreads();
+    if (t == 0) {
+        double tr = 0.0;
+        for (int w = 0; w < nt / 32; ++w) tr += red[w];
+        shift_s = rel * tr / (double)l;
+    }
+    __syncthreads();
+    for (int i = t; i < l; i += nt) R[i * l + i] += shift_s;
+    __syncthreads();
+    // upper Cholesky: row j of R, then the trailing upper triangle
+    for (int j = 0; j < l; ++j) {
+        const double d = R[j * l + j];
+        const double rjj = sqrt(d > 0.0 ? d : 1e-300);
+        __syncthreads();
+        for (int c = j + 1 + t; c < l; c += nt) R[j * l + c] /= rjj;
+        if (t == 0) R[j * l + j] = rjj;
+        __syncthreads();
+        const int m = l - j - 1;
+        for (int idx = t; idx < m * m; idx += nt) {
+            const int r = j + 1 + idx / m, c = j + 1 + idx % m;
+            if (c >= r) R[r * l + c] -= R[j * l + r] * R[j * l + c];
+        }
+        __syncthreads();
+    }
+    // in-place inverse of the upper triangle, one column at a time:
+    // X[j][j] = 1 / R[j][j];  X[i][j] = -X[j][j] * sum_{i<=m<j} X[i][m] R[m][j]
+    for (int j = 0; j < l; ++j) {
+        const double xjj = 1.0 / R[j * l + j];
+        double v = 0.0;
+        if (t < j) {
+            for (int m = t; m < j; ++m) v += R[t * l + m] * R[m * l + j];
+            v *= -xjj;
+        }
+        __syncthreads();
+        if (t < j) R[t * l + j] = v;
+        if (t == 0) R[j * l + j] = xjj;
+        __syncthreads();
+    }
+    for (int i = t; i < l * l; i += nt) Rinv[i] = (i % l >= i / l) ? R[i] : 0.0;
+}
+
 // In-place upper Cholesky W = R^T R and Rinv = R^{-1}, one CTA (l <= 1024).
 // A diagonal shift rel * trace(W) / l keeps rank-deficient Grams
 // factorisable (shifted CholeskyQR); it is formed here, not on the host.
@@ -137,6 +337,7 @@ __global__ void chol_inv_kernel(double* W, int64_t l, double rel, double* Rinv) 
 // sqrt|a_pp a_qq|, or below 1e-18 ||A||_F); a sweep without rotations ends
 // the iteration (the threshold Jacobi method).  Out: A's diagonal holds the
 // eigenvalues, V (l x l, row-major) the eigenvectors by columns.
+template <class VT>
 __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int l, int max_sweeps,
                                                       int* sweeps_out, int a_in_smem) {
     extern __shared__ double sh[];
@@ -148,7 +349,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
     int* qq = pp + np;
     const int lda = a_in_smem ? l + ((l + 1) & 1) : l;  // odd pitch in shared memory
     double* A = a_in_smem ? sh + m + np + 1 : Ag;
-    double* Vt = V;  // transposed during the iteration
+    // transposed eigenvectors: fp64 in place in V, or fp32 in shared memory
+    // after A (the eigenvalues come from A's fp64 rotations either way)
+    VT* Vt;
+    if constexpr (sizeof(VT) == 8) Vt = reinterpret_cast<VT*>(V);
+    else Vt = reinterpret_cast<VT*>(A + l * lda);
     __shared__ int nrot;
     __shared__ double red[32];
     const int tx = threadIdx.x, ty = threadIdx.y, t = ty * blockDim.x + tx, nt = blockDim.x * blockDim.y;
@@ -158,7 +363,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
             const double v = Ag[r * l + c];
             part += v * v;
             if (a_in_smem) A[r * lda + c] = v;
-            Vt[r * l + c] = r == c ? 1.0 : 0.0;
+            Vt[r * l + c] = r == c ? VT(1) : VT(0);
         }
     for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
     if ((t & 31) == 0) red[t >> 5] = part;
@@ -209,9 +414,9 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
                     const double x = A[i * lda + a], y = A[i * lda + b];
                     A[i * lda + a] = c * x - s * y;
                     A[i * lda + b] = s * x + c * y;
-                    const double vx = Vt[a * l + i], vy = Vt[b * l + i];
-                    Vt[a * l + i] = c * vx - s * vy;
-                    Vt[b * l + i] = s * vx + c * vy;
+                    const VT vx = Vt[a * l + i], vy = Vt[b * l + i];
+                    Vt[a * l + i] = (VT)c * vx - (VT)s * vy;
+                    Vt[b * l + i] = (VT)s * vx + (VT)c * vy;
                 }
             }
             __syncthreads();
@@ -236,29 +441,41 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
         for (int r = ty; r < l; r += blockDim.y)
             for (int c = tx; c < l; c += blockDim.x) Ag[r * l + c] = A[r * lda + c];
     __syncthreads();
-    // Vt -> V in place (swap across the diagonal)
-    for (int r = ty; r < l; r += blockDim.y)
-        for (int c = tx; c < r; c += blockDim.x) {
-            const double x = Vt[r * l + c];
-            Vt[r * l + c] = Vt[c * l + r];
-            Vt[c * l + r] = x;
-        }
+    if constexpr (sizeof(VT) == 8) {  // Vt -> V in place (swap across the diagonal)
+        for (int r = ty; r < l; r += blockDim.y)
+            for (int c = tx; c < r; c += blockDim.x) {
+                const double x = Vt[r * l + c];
+                Vt[r * l + c] = Vt[c * l + r];
+                Vt[c * l + r] = x;
+            }
+    } else {
+        for (int r = ty; r < l; r += blockDim.y)
+            for (int c = tx; c < l; c += blockDim.x) V[r * l + c] = (double)Vt[c * l + r];
+    }
     if (t == 0) *sweeps_out = sweep;
 }
 
 // one-CTA symmetric eigensolve of the l x l matrix A (in place: diagonal =
 // eigenvalues, V = eigenvectors by columns)
-inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_t s) {
+// fp32_vectors: accumulate the rotations of the eigenvectors in fp32 shared
+// memory (enough for fp32 outputs), so no rotation touches global memory.
+inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_t s, bool fp32_vectors = false) {
     const int64_t m = l + (l & 1);
     const size_t base = (size_t)(m + m / 2 + 1) * sizeof(double);
-    const size_t with_a = base + (size_t)l * (l + 1) * sizeof(double);
-    const bool smem_a = with_a <= 200 * 1024;
+    const size_t with_a = base + (size_t)l * (l + 1 + ((l + 1) & 1)) * sizeof(double);
+    const size_t with_v = with_a + (size_t)l * l * sizeof(float);
     static bool attr = false;
     if (!attr) {
-        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    jacobi_kernel<<<1, dim3(128, 8), smem_a ? with_a : base, s>>>(A, V, (int)l, 60, sweeps, smem_a ? 1 : 0);
+    if (fp32_vectors && with_v <= 200 * 1024) {
+        jacobi_kernel<float><<<1, dim3(128, 8), with_v, s>>>(A, V, (int)l, 60, sweeps, 1);
+    } else {
+        const bool smem_a = with_a <= 200 * 1024;
+        jacobi_kernel<double><<<1, dim3(128, 8), smem_a ? with_a : base, s>>>(A, V, (int)l, 60, sweeps, smem_a ? 1 : 0);
+    }
     CK_LAUNCH();
 }
 
@@ -287,20 +504,52 @@ struct EigenWork {
         T* src = Y;
         T* dst = Y2;
         for (int pass = 0; pass < 2; ++pass) {
+            ProfScope p1("orth_gram", s, 0.0, 0.0);
             CK_CUDA(cudaMemsetAsync(W.p, 0, l * l * sizeof(double), s));
-            const int64_t ksplit = std::min<int64_t>(256, std::max<int64_t>(1, rows / 4096));
-            const int64_t chunk = ceil_div(rows, ksplit);
-            dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
-            gram_kernel<T><<<g, 256, 0, s>>>(src, ld, rows, l, chunk, dptr<double>(W));
-            CK_LAUNCH();
+            {
+                const int64_t lt = ceil_div(l, 64), tiles = lt * (lt + 1) / 2;
+                const int64_t ksplit = std::min<int64_t>(ceil_div(4 * 148, tiles), std::max<int64_t>(1, rows / 2048));
+                gram_dmma_kernel<T><<<dim3((unsigned)tiles, (unsigned)ksplit), 128, 0, s>>>(src, ld, rows, l,
+                                                                                        ceil_div(rows, ksplit),
+                                                                                        dptr<double>(W));
+                CK_LAUNCH();
+            }
             if (comm) comm->sum(dptr<double>(W), (size_t)(l * l), s);  // Gram of all ranks' rows
-            chol_inv_kernel<<<1, 256, 0, s>>>(dptr<double>(W), l, sizeof(T) == 4 ? 1e-7 : 1e-14, dptr<double>(Rinv));
-            CK_LAUNCH();
+            p1.end();
+            ProfScope p2("orth_chol", s, 0.0, 0.0);
+            chol_inv(dptr<double>(W), l, sizeof(T) == 4 ? 1e-7 : 1e-14, dptr<double>(Rinv));
             convert_to<T>(dptr<double>(Rinv), dptr<T>(Rt), l * l);
+            p2.end();
+            ProfScope p3("orth_apply", s, 0.0, 0.0);
             EpiStore<T> e{dst, ld, 0, T(1), T(0)};
-            gemm_simt<T>(s, rows, l, l, 1, kmaj(src, ld), mnmaj(dptr<T>(Rt), l), e);
+            bool done = false;
+            if constexpr (std::is_same_v<T, float>) {
+                if (prec == kTF32 && rows >= 512 && l % 4 == 0) {  // fp32-grade products on the tensor cores
+                    gemm_tf32(k3xTF32, s, rows, l, l, kmaj(src, ld), mnmaj(dptr<T>(Rt), l), e);
+                    done = true;
+                }
+            }
+            if (!done) gemm_simt<T>(s, rows, l, l, 1, kmaj(src, ld), mnmaj(dptr<T>(Rt), l), e);
+            p3.end();
             std::swap(src, dst);
         }
+    }
+
+    // shifted Cholesky + inverse of the l x l Gram (shared memory when it fits)
+    void chol_inv(double* W, int64_t l, double rel, double* Rinv) {
+        const size_t bytes = (size_t)l * l * sizeof(double);
+        if (bytes <= 200 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                CK_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024));
+                attr = true;
+            }
+            chol_inv_smem_kernel<<<1, 1024, bytes, s>>>(W, (int)l, rel, Rinv);
+        } else {
+            chol_inv_kernel<<<1, 256, 0, s>>>(W, l, rel, Rinv);
+        }
+        CK_LAUNCH();
     }
 
     template <class U>
@@ -407,11 +656,14 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     for (auto& v : hb) v /= (double)n;
     CK_CUDA(cudaMemcpyAsync(B.p, hb.data(), l * l * sizeof(double), cudaMemcpyHostToDevice, s));
     DevMem sw(sizeof(int), s);
-    jacobi_eig(dptr<double>(B), dptr<double>(V), l, dptr<int>(sw), s);
+    jacobi_eig(dptr<double>(B), dptr<double>(V), l, dptr<int>(sw), s, std::is_same_v<T, float>);
     std::vector<double> ha(l * l), hv(l * l);
     CK_CUDA(cudaMemcpyAsync(ha.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaMemcpyAsync(hv.data(), V.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+    int sweeps = 0;
+    CK_CUDA(cudaMemcpyAsync(&sweeps, sw.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
+    if (getenv("CURVKIT_TRACE")) fprintf(stderr, "[curvkit] Rayleigh-Ritz Jacobi: l = %lld, %d sweeps\n", (long long)l, sweeps);
     std::vector<int64_t> ord(l);
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return ha[a * l + a] > ha[b * l + b]; });
