@@ -18,9 +18,13 @@ so a step produces 2 * P^2 matrix entries.
          unmodified reference sources) on a bounded sample of the same job
 
 --impl reference runs only the reference CPU arm (rank 0; other ranks exit).
-Multi-GPU (torchrun): rank r assembles rows curvkit_shard_rows(P, N, r) of H and
-G (lower-triangle entries and their mirrors; shards balanced by triangle area,
-no collective on the data path); value = 2 P^2 / max-over-ranks step time.
+Multi-GPU (torchrun), no collective on the data path either way:
+  --scaling weak (default)  the units are independent curvature jobs: rank r
+         assembles H and G of its own config-1 instance (parameters drawn with
+         seed + r); value = N * 2 P^2 / max-over-ranks step time
+  --scaling strong  one job: rank r assembles rows curvkit_shard_rows(P, N, r)
+         of H and G (lower-triangle entries and their mirrors, shards balanced
+         by triangle area); value = 2 P^2 / max-over-ranks step time
 """
 from __future__ import annotations
 
@@ -49,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     return ap.parse_args()
 
 
@@ -177,7 +182,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "hessian_opg_entries_per_s", "value": v, "unit": "entries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE config shapes and distributions)",
         "config": {"workload": f"{wl.name}: MLP {wl.widths} {wl.activation}, N={wl.n}, P={wl.P}, exact H + OPG",
                    "products": "hessian+opg"},
@@ -208,6 +213,10 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = CONFIGS[args.config]
+    weak = world > 1 and args.scaling == "weak"
+    if weak and rank > 0:  # an independent instance of the same config per rank
+        import dataclasses
+        wl = dataclasses.replace(wl, seed=wl.seed + 7919 * rank)
     prec = args.precision
     dt = torch.float64 if prec == "f64" else torch.float32
     dev = torch.device("cuda", local)
@@ -225,7 +234,7 @@ def run_b200(args):
     rb, re = curv.shard_rows(P, world, rank)
 
     def step():
-        if world == 1:
+        if world == 1 or weak:
             curv.dev_assemble_hessian(spec, p_d, x_d, l_d, n, H, ld, precision=prec, stream=stream)
             curv.dev_assemble_opg(spec, p_d, x_d, l_d, n, G, ld, precision=prec, stream=stream)
         else:  # this rank's triangle-balanced row shard of both products
@@ -259,12 +268,13 @@ def run_b200(args):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    entries = 2.0 * P * P  # the ranks' row shards together cover H and G once
+    # weak: every rank assembles a whole job; strong: the row shards cover one
+    entries = 2.0 * P * P * (world if weak else 1)
     value = entries / (ms / 1e3)
 
     # e2e through the host-buffer C-ABI (pinned host outputs)
     e2e = None
-    if not args.no_e2e and world == 1:  # the host-buffer ABI assembles whole matrices
+    if not args.no_e2e and (world == 1 or weak):  # the host-buffer ABI assembles whole matrices
         lib = _lib.load()
         import ctypes as C
         hH = torch.empty((P, P), dtype=torch.float32, pin_memory=True)
@@ -293,9 +303,9 @@ def run_b200(args):
             t = torch.tensor([te], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             te = float(t.item())
-        h2d = 2 * 8 * (P + x.size + y.size)
+        h2d = 2 * 8 * (P + x.size + y.size) * world
         e2e = {"value": entries / te, "unit": "entries/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(2 * 4 * P * P), "ms_per_step": te * 1e3}
+               "d2h_bytes_per_step": int(2 * 4 * P * P * world), "ms_per_step": te * 1e3}
 
     if rank != 0:
         return
@@ -338,14 +348,15 @@ def run_b200(args):
     line = {
         "metric": "hessian_opg_entries_per_s", "value": value, "unit": "entries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": PREC_DTYPE[prec],
+        "scaling": "weak" if (weak or world == 1) else "strong", "vs_baseline": None, "dtype": PREC_DTYPE[prec],
         "data": "synthetic (seeded, BASELINE config shapes and distributions)",
         "config": {"workload": f"{wl.name}: MLP {wl.widths} {wl.activation}, N={n}, P={P}, exact H + OPG "
                                f"({2 * P * P} entries per step)",
                    "products": "hessian+opg", "precision": prec,
                    "l2": "no flush: each step writes 2 x P^2 x 4 B = 5.2 GB >> 126 MB L2",
-                   "parallelism": (f"{world} GPUs, triangle-balanced row shards of H and G, no data-path collective"
-                                   if world > 1 else "single GPU")},
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"{world} GPUs, one independent config-1 job per GPU, no collective" if weak else
+                                   f"{world} GPUs, triangle-balanced row shards of one job, no data-path collective")},
         "gpu_launches": int(launches),
         "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
         "clocks": clk.summary(),

@@ -63,6 +63,18 @@ template <class T>
 __global__ void replicate_rows_kernel(const T* __restrict__ in, int64_t period, int64_t ld, T* __restrict__ out,
                                       int64_t rows, int64_t in_bstride, int64_t out_bstride) {
     const int64_t b = blockIdx.y;
+    if constexpr (sizeof(T) == 4) {
+        if (ld % 4 == 0 && in_bstride % 4 == 0 && out_bstride % 4 == 0 && rows * ld / 4 < (int64_t(1) << 31)) {
+            const uint32_t q = (uint32_t)(ld / 4), total = (uint32_t)(rows * q);
+            const float4* src = reinterpret_cast<const float4*>(in + b * in_bstride);
+            float4* dst = reinterpret_cast<float4*>(out + b * out_bstride);
+            for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+                const uint32_t r = i / q;
+                __stcs(dst + i, __ldg(src + (size_t)(r % (uint32_t)period) * q + (i - r * q)));
+            }
+            return;
+        }
+    }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ld; i += (int64_t)gridDim.x * blockDim.x)
         out[b * out_bstride + i] = in[b * in_bstride + ((i / ld) % period) * ld + i % ld];
 }
@@ -72,9 +84,21 @@ template <class T>
 __global__ void qext_kernel(const T* __restrict__ qt, int64_t tk, int64_t tm1, int64_t ldn, T* __restrict__ qx,
                             int64_t rows) {
     const int64_t opp = blockIdx.y;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ldn; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / ldn, e = i - r * ldn;
-        qx[(opp * rows + r) * ldn + e] = qt[((r % tk) * tm1 + opp) * ldn + e];
+    if constexpr (sizeof(T) == 4) {
+        // 16-byte vectors along n (ldn is a multiple of 32); row index math in 32 bits
+        const uint32_t q = (uint32_t)(ldn / 4), total = (uint32_t)(rows * q);
+        const float4* src = reinterpret_cast<const float4*>(qt);
+        float4* dst = reinterpret_cast<float4*>(qx) + (size_t)opp * rows * q;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+            const uint32_t r = i / q, e = i - r * q;
+            __stcs(dst + i, __ldg(src + ((size_t)(r % (uint32_t)tk) * tm1 + opp) * q + e));
+        }
+    } else {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ldn;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t r = i / ldn, e = i - r * ldn;
+            qx[(opp * rows + r) * ldn + e] = qt[((r % tk) * tm1 + opp) * ldn + e];
+        }
     }
 }
 
@@ -335,7 +359,7 @@ struct Engine {
                     const int64_t tm1 = md.w[m + 1];
                     QX[m] = buf(tm1 * ak_rows, ldn);
                     // QT[m] is [i][o''][n]; QX[m] is [o''][r][n] with r -> i = r mod T_k
-                    qext_kernel<T><<<dim3(blocks_for(ak_rows * ldn), (unsigned)tm1), 256, 0, s>>>(
+                    qext_kernel<T><<<dim3(blocks_for(ak_rows * ldn / 4), (unsigned)tm1), 256, 0, s>>>(
                         QT[m], tk, tm1, ldn, QX[m], ak_rows);
                     CK_LAUNCH();
                 }

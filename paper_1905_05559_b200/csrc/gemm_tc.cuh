@@ -782,10 +782,12 @@ struct FusedHess {
 };
 
 // control (4 warps), epilogue (8: two per TMEM lane quadrant, each half the
-// tile width), transform (FUSED_TW: FUSED_TW / 4 threads per tile row, each
-// a contiguous share of the row's eight 16-byte chunks)
+// tile width), transform (FUSED_TW: TW_SETS sets of 4 warps, one tile row per
+// thread; set s transforms the k-blocks with global index = s mod TW_SETS,
+// so a stage has TW_SETS MMA periods for its transform)
 constexpr int FUSED_EPI = 8, FUSED_TW = 4;
-constexpr int TW_CH = 8 / (FUSED_TW / 4);  // chunks per transform thread
+constexpr int TW_SETS = FUSED_TW / 4;
+constexpr int TW_CH = 8 / TW_SETS;  // 16-byte chunks per pass (TW_SETS passes bound the registers)
 constexpr int PV_ROWS = 8;  // profile rows (output units o) staged per CTA and stage
 constexpr bool STAGE_PV = true;  // profile rows ride the stage (TMA), no L2 round trip in the transform
 constexpr int kFusedThreads = 128 + 32 * FUSED_EPI + 32 * FUSED_TW;
@@ -868,7 +870,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         prefetch_map(&mapB);
         if (fh.hasq) prefetch_map(&mapQ);
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 1 + 2 * FUSED_TW);
+            mbar_init(&full[s], 1 + 2 * 4);  // producer + one transform set (4 warps) of each CTA
             mbar_init(&empty[s], 1);
             mbar_init(&afull[s], 1);
         }
@@ -962,12 +964,14 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             }
         }
     } else if (warp >= TW0) {  // ---------------- A transform (both CTAs)
+        const int set = (warp - TW0) >> 2;
         const int row = ((warp - TW0) & 3) * 32 + lane;  // tile row of this thread
-        const int L0 = FUSED_TW == 4 ? 0 : ((warp - TW0) >> 2) * TW_CH;  // its chunks L0 .. L0 + TW_CH - 1
         const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
-        int stage = 0;
+        // running stage / phase of the k-block stream (all tiles), and its
+        // position mod TW_SETS: no divisions in the loop
+        int stage = 0, sidx = 0;
         uint32_t phase = 0;
-        int64_t tg = 0;
+        int g = 0;  // k-block index (trace)
         for (int64_t t = pair_id; t < ntiles; t += npairs) {
             int64_t opp, j0, n0;
             tile_of(t, opp, j0, n0);
@@ -981,58 +985,68 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             // weight rows read their profile (and delta) row from the stage
             const int64_t slot = o - fh.o_first(j0 + 128 * rank);
             const bool staged = fh.pv_tma && !bias && slot >= 0 && slot < PV_ROWS;
-            for (int64_t kb = 0; kb < nk; ++kb, ++tg) {
-                mbar_wait(&afull[stage], phase);
-                if (trw && tg < TRN) trace[1 * TRN + tg] = clock64();
-                uint8_t* st = stage_base + stage * STAGE_BYTES;
+            for (int64_t kb = 0; kb < nk; ++kb, ++g) {
+                const bool mine = TW_SETS == 1 || sidx == set;
+                const int st_ = stage;
+                const uint32_t ph_ = phase;
+                if (++stage == NST) { stage = 0; phase ^= 1; }
+                if (TW_SETS > 1 && ++sidx == TW_SETS) sidx = 0;
+                if (!mine) continue;
+                mbar_wait(&afull[st_], ph_);
+                if (trw && g < TRN) trace[1 * TRN + g] = clock64();
+                uint8_t* st = stage_base + st_ * STAGE_BYTES;
                 uint8_t* sa = st + row * 128;
                 const int64_t n0k = kb * BK;
                 const float4* pst = reinterpret_cast<const float4*>(st + PV_OFF + slot * 128);
                 const float4* dst_ = reinterpret_cast<const float4*>(st + DT_OFF + slot * 128);
-                // all loads first, then the products, then the stores: logical
-                // 16-byte chunk L holds examples n0k + 4L .. +3 and sits at
-                // physical chunk L ^ (row & 7)
-                float4 x[TW_CH], p[TW_CH];
+                // per pass: loads first, then the products, then the stores;
+                // logical 16-byte chunk L holds examples n0k + 4L .. +3 and sits
+                // at physical chunk L ^ (row & 7)
 #pragma unroll
-                for (int u = 0; u < TW_CH; ++u) x[u] = *reinterpret_cast<const float4*>(sa + (((L0 + u) ^ sw) << 4));
-                if (staged) {
-#pragma unroll
-                    for (int u = 0; u < TW_CH; ++u) p[u] = pst[L0 + u];
-                } else {
+                for (int pass = 0; pass < TW_SETS; ++pass) {
+                    const int L0 = pass * TW_CH;
+                    float4 x[TW_CH], p[TW_CH];
 #pragma unroll
                     for (int u = 0; u < TW_CH; ++u)
-                        p[u] = __ldg(reinterpret_cast<const float4*>(pvrow + n0k + 4 * (L0 + u)));
-                }
+                        x[u] = *reinterpret_cast<const float4*>(sa + (((L0 + u) ^ sw) << 4));
+                    if (staged) {
 #pragma unroll
-                for (int u = 0; u < TW_CH; ++u) {
-                    if (bias) {
-                        x[u] = p[u];
+                        for (int u = 0; u < TW_CH; ++u) p[u] = pst[L0 + u];
                     } else {
-                        x[u].x *= p[u].x; x[u].y *= p[u].y; x[u].z *= p[u].z; x[u].w *= p[u].w;
+#pragma unroll
+                        for (int u = 0; u < TW_CH; ++u)
+                            p[u] = __ldg(reinterpret_cast<const float4*>(pvrow + n0k + 4 * (L0 + u)));
                     }
-                }
-                if (fh.hasq && !bias) {
 #pragma unroll
                     for (int u = 0; u < TW_CH; ++u) {
-                        const float4 q = *reinterpret_cast<const float4*>(sa + A_OFF_Q + (((L0 + u) ^ sw) << 4));
-                        const float4 dd = staged ? dst_[L0 + u]
-                                                 : __ldg(reinterpret_cast<const float4*>(drow + n0k + 4 * (L0 + u)));
-                        x[u].x += dd.x * q.x; x[u].y += dd.y * q.y; x[u].z += dd.z * q.z; x[u].w += dd.w * q.w;
+                        if (bias) {
+                            x[u] = p[u];
+                        } else {
+                            x[u].x *= p[u].x; x[u].y *= p[u].y; x[u].z *= p[u].z; x[u].w *= p[u].w;
+                        }
+                    }
+                    if (fh.hasq && !bias) {
+#pragma unroll
+                        for (int u = 0; u < TW_CH; ++u) {
+                            const float4 q = *reinterpret_cast<const float4*>(sa + A_OFF_Q + (((L0 + u) ^ sw) << 4));
+                            const float4 dd = staged ? dst_[L0 + u]
+                                                     : __ldg(reinterpret_cast<const float4*>(drow + n0k + 4 * (L0 + u)));
+                            x[u].x += dd.x * q.x; x[u].y += dd.y * q.y; x[u].z += dd.z * q.z; x[u].w += dd.w * q.w;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < TW_CH; ++u) {  // round to nearest TF32 (the MMA would truncate)
+                        x[u].x = round_tf32(x[u].x); x[u].y = round_tf32(x[u].y);
+                        x[u].z = round_tf32(x[u].z); x[u].w = round_tf32(x[u].w);
+                        *reinterpret_cast<float4*>(sa + (((L0 + u) ^ sw) << 4)) = x[u];
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < TW_CH; ++u) {  // round to nearest TF32 (the MMA would truncate)
-                    x[u].x = round_tf32(x[u].x); x[u].y = round_tf32(x[u].y);
-                    x[u].z = round_tf32(x[u].z); x[u].w = round_tf32(x[u].w);
-                    *reinterpret_cast<float4*>(sa + (((L0 + u) ^ sw) << 4)) = x[u];
-                }
-                if (trw && tg < TRN) trace[4 * TRN + tg] = clock64();
+                if (trw && g < TRN) trace[4 * TRN + g] = clock64();
                 fence_proxy_async();
-                if (trw && tg < TRN) trace[5 * TRN + tg] = clock64();
+                if (trw && g < TRN) trace[5 * TRN + g] = clock64();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(fb0 + stage * 8);
-                if (trw && tg < TRN) trace[2 * TRN + tg] = clock64();
-                if (++stage == NST) { stage = 0; phase ^= 1; }
+                if (lane == 0) mbar_arrive_cluster(fb0 + st_ * 8);
+                if (trw && g < TRN) trace[2 * TRN + g] = clock64();
             }
         }
     } else if (warp >= 4) {  // ---------------- epilogue (both CTAs)
