@@ -474,6 +474,32 @@ __device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
         : "memory");
 }
 
+// A from TMEM (the "TS" form): a_tmem is this CTA's A tile column in TMEM
+__device__ __forceinline__ void mma2_tf32_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+    const uint32_t z = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(z)
+        : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit values from registers into TMEM
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+        "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]),
+        "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]),
+        "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void commit2(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -820,7 +846,12 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
 }
 
 
-template <int BN, class Epi>
+// TS = true: the transform writes R into TMEM A slots (tcgen05.st) and the MMA
+// reads A from TMEM, so R never passes through shared memory; 512 TMEM
+// columns = 2 accumulators of BN (192) + TS_SLOTS A slots of one K-block.
+constexpr int TS_SLOTS = 4;
+
+template <int BN, class Epi, bool TS = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_constant__ CUtensorMap mapQ,
                      const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapPV,
@@ -880,9 +911,12 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    constexpr int TMEM_COLS = TS ? 512 : 2 * BN;
+    static_assert(!TS || 2 * BN + 32 * TS_SLOTS <= 512, "TMEM budget");
+    constexpr uint32_t A_COL0 = 2 * BN;  // first TMEM A slot (TS)
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "n"(2 * BN));
+                     "n"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
@@ -944,17 +978,22 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
                 for (int64_t kb = 0; kb < nk; ++kb) {
                     mbar_wait(&full[stage], phase);
-                    if (trace) { if (tg < TRN) trace[3 * TRN + tg] = clock64(); ++tg; }
+                    if (trace) { if (tg < TRN) trace[3 * TRN + tg] = clock64(); }
                     tc_fence_after();
                     const uint32_t sa = smem_u32(stage_base + stage * STAGE_BYTES);
                     const uint32_t sb = sa + B_OFF;
+                    const uint32_t aslot = tmem_base + A_COL0 + (uint32_t)(tg % TS_SLOTS) * 32;
+                    ++tg;
 #pragma unroll
                     for (int ks = 0; ks < BK / 8; ++ks) {
                         const uint32_t boff = sh.b_mn ? ks * sh.mn_kstep : ks * 32;
                         const uint32_t blbo = sh.b_mn ? sh.mn_lbo : 16, bsbo = sh.b_mn ? sh.mn_sbo : 1024;
                         const uint32_t blay = sh.b_mn ? sh.mn_layout : 2;
-                        mma2_tf32(d, smem_desc(sa + ks * 32, 16, 1024, 2), smem_desc(sb + boff, blbo, bsbo, blay),
-                                  idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        const uint64_t bd = smem_desc(sb + boff, blbo, bsbo, blay);
+                        if constexpr (TS)
+                            mma2_tf32_ts(d, aslot + ks * 8, bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        else
+                            mma2_tf32(d, smem_desc(sa + ks * 32, 16, 1024, 2), bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
                     }
                     commit2(&empty[stage]);
                     if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -971,7 +1010,12 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         // position mod TW_SETS: no divisions in the loop
         int stage = 0, sidx = 0;
         uint32_t phase = 0;
-        int g = 0;  // k-block index (trace)
+        int g = 0;  // k-block index (trace; TS: A slot g % TS_SLOTS)
+        // TS: the MMA of k-block g - TS_SLOTS (stage rs, phase rph) must be done
+        // with A slot g % TS_SLOTS before it is overwritten
+        int rs = 0;
+        uint32_t rph = 0;
+        const uint32_t tq = (uint32_t)(((warp - TW0) & 3) * 32) << 16;  // TMEM lane quadrant of this warp
         for (int64_t t = pair_id; t < ntiles; t += npairs) {
             int64_t opp, j0, n0;
             tile_of(t, opp, j0, n0);
@@ -993,6 +1037,12 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 if (TW_SETS > 1 && ++sidx == TW_SETS) sidx = 0;
                 if (!mine) continue;
                 mbar_wait(&afull[st_], ph_);
+                if constexpr (TS) {
+                    if (g >= TS_SLOTS) {
+                        mbar_wait(&empty[rs], rph);
+                        if (++rs == NST) { rs = 0; rph ^= 1; }
+                    }
+                }
                 if (trw && g < TRN) trace[1 * TRN + g] = clock64();
                 uint8_t* st = stage_base + st_ * STAGE_BYTES;
                 uint8_t* sa = st + row * 128;
@@ -1038,11 +1088,17 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                     for (int u = 0; u < TW_CH; ++u) {  // round to nearest TF32 (the MMA would truncate)
                         x[u].x = round_tf32(x[u].x); x[u].y = round_tf32(x[u].y);
                         x[u].z = round_tf32(x[u].z); x[u].w = round_tf32(x[u].w);
-                        *reinterpret_cast<float4*>(sa + (((L0 + u) ^ sw) << 4)) = x[u];
+                        if constexpr (!TS) *reinterpret_cast<float4*>(sa + (((L0 + u) ^ sw) << 4)) = x[u];
+                    }
+                    if constexpr (TS) {  // row = TMEM lane, k = column of A slot g % TS_SLOTS
+                        static_assert(!TS || TW_SETS == 1, "TS transform writes whole rows");
+                        tmem_st32(tmem_base + tq + A_COL0 + (uint32_t)(g % TS_SLOTS) * 32,
+                                  reinterpret_cast<const float*>(x));
                     }
                 }
                 if (trw && g < TRN) trace[4 * TRN + g] = clock64();
-                fence_proxy_async();
+                if constexpr (TS) tc_fence_before();
+                else fence_proxy_async();
                 if (trw && g < TRN) trace[5 * TRN + g] = clock64();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(fb0 + st_ * 8);
@@ -1133,7 +1189,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
     cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(2 * BN));
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
     }
 }
 
@@ -1458,7 +1514,15 @@ template <>
 struct HessFused<float> {
     static bool run(int prec, cudaStream_t s, const HessFusedArgs<float>& a, const EpiHess<float>& e) {
         if (prec != kTF32) return false;
-        constexpr int BN = 256;
+        namespace pair = tc::pair;
+        // A from TMEM (R never in shared memory) is correct but measured slower
+        // on B200 (5.3 vs 4.2 clocks per N column per k-block): opt-in only
+        static const bool ts = getenv("CURVKIT_HESS_TS") != nullptr;
+        return ts ? launch<192, true>(s, a, e) : launch<256, false>(s, a, e);
+    }
+
+    template <int BN, bool TS>
+    static bool launch(cudaStream_t s, const HessFusedArgs<float>& a, const EpiHess<float>& e) {
         namespace pair = tc::pair;
         pair::FusedHess fh{a.pv, a.dT, a.ldn, a.tk, a.tm, a.tm1, a.nw, a.qrows, a.diag, a.qT ? 1 : 0, nullptr, 0,
                            a.rows, 0};
@@ -1496,7 +1560,7 @@ struct HessFused<float> {
         using S = pair::FusedSmem<BN>;
         static bool attr = false;
         if (!attr) {
-            CK_CUDA(cudaFuncSetAttribute(pair::tc_hess_fused_kernel<BN, EpiHess<float>>,
+            CK_CUDA(cudaFuncSetAttribute(pair::tc_hess_fused_kernel<BN, EpiHess<float>, TS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(S::bytes(0), S::bytes(1))));
             attr = true;
         }
@@ -1511,7 +1575,7 @@ struct HessFused<float> {
         // H as a 2D map of 32 x 32 boxes (128-byte swizzle) for the epilogue
         fh.tma_h = (e.ldh % 4 == 0) ? 1 : 0;
         CUtensorMap mh = fh.tma_h ? tc::make_map_h(e.H, e.ldh) : mb;
-        pair::tc_hess_fused_kernel<BN, EpiHess<float>><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
+        pair::tc_hess_fused_kernel<BN, EpiHess<float>, TS><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
             mak, mq, mb, mpv, mdt, mh, fh, sh, e);
         CK_LAUNCH();
         if (tracing) {

@@ -203,3 +203,39 @@ def test_config1_topk_against_dual_gram(prec):
     assert lam[9] <= w[9] * (1 + 1e-3) and lam[9] >= 0.9 * w[9]
     qtq = (q.T.double() @ q.double()).cpu().numpy()
     assert np.abs(qtq - np.eye(k)).max() <= 1e-4
+
+
+def test_config1_hessian_tmem_a_variant():
+    """The opt-in fused Hessian variant with the R operand in TMEM
+    (CURVKIT_HESS_TS=1, read once per process: run in a subprocess) against
+    the reference's config-1 Hessian columns."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from conftest import load_golden, rel_fro
+from paper_1905_05559_b200 import curv
+from paper_1905_05559_b200.workloads import CONFIGS
+wl = CONFIGS["c1"]; pins = load_golden("c1_pins")
+params, x, y, lab = wl.draw()
+d = "cuda:0"
+p = torch.tensor(params, dtype=torch.float32, device=d); xx = torch.tensor(x, dtype=torch.float32, device=d)
+ll = torch.tensor(lab, dtype=torch.int32, device=d)
+spec = curv.ModelSpec(wl.widths, wl.activation); P = wl.P; ld = (P + 3) // 4 * 4
+H = torch.empty((P, ld), dtype=torch.float32, device=d)
+curv.dev_assemble_hessian(spec, p, xx, ll, wl.n, H, ld, precision="tf32"); torch.cuda.synchronize()
+cols = torch.tensor(pins["cols"], device=d)
+got = H[:, :P][:, cols].double().cpu().numpy()
+err = max(rel_fro(got[:, j], pins["hcols"][:, j]) for j in range(got.shape[1]))
+sub = H[:2000, :2000]
+print("ERR", err, bool(torch.equal(sub, sub.T)))
+'''
+    import os
+    env = dict(os.environ, CURVKIT_HESS_TS="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("ERR")][-1].split()
+    assert float(line[1]) <= 1e-3 and line[2] == "True", line
