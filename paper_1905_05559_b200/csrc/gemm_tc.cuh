@@ -911,7 +911,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    constexpr int TMEM_COLS = TS ? 512 : 2 * BN;
+    constexpr int TMEM_COLS = (TS || 2 * BN > 256) ? 512 : 256;
     static_assert(!TS || 2 * BN + 32 * TS_SLOTS <= 512, "TMEM budget");
     constexpr uint32_t A_COL0 = 2 * BN;  // first TMEM A slot (TS)
     if (warp == 2) {
@@ -1518,7 +1518,11 @@ struct HessFused<float> {
         // A from TMEM (R never in shared memory) is correct but measured slower
         // on B200 (5.3 vs 4.2 clocks per N column per k-block): opt-in only
         static const bool ts = getenv("CURVKIT_HESS_TS") != nullptr;
-        return ts ? launch<192, true>(s, a, e) : launch<256, false>(s, a, e);
+        static const bool ss192 = getenv("CURVKIT_HESS_SS192") != nullptr;  // dev: control for the TS variant
+        if (ss192) return launch<192, false>(s, a, e);
+        if constexpr (pair::TW_SETS == 1)
+            if (ts) return launch<192, true>(s, a, e);
+        return launch<256, false>(s, a, e);
     }
 
     template <int BN, bool TS>
