@@ -113,6 +113,19 @@ int curvkit_assemble_opg_f32(const curvkit_model* model, const double* params, c
                              const double* y, int64_t n, const curvkit_curvature_config* cfg,
                              int32_t precision, float* g_out);
 
+/* curv::lanczos_topk (eigensolve.hpp:44) on the HvpOperator of
+ * (model, params, data, batch_size) (autodiff.hpp:72-86): the k
+ * algebraically largest eigenpairs of the Hessian, Lanczos with full
+ * reorthogonalisation, the Krylov basis resident on the device.  q_out: P x k
+ * (columns are eigenvectors), lambda_out: k descending, residuals_out: k
+ * true residuals ||H q_i - lambda_i q_i||.  Not converged within
+ * max_iterations: CURVKIT_CONVERGENCE_ERROR with the best residual estimates
+ * in residuals_out (the reference's ConvergenceError payload). */
+int curvkit_hessian_topk_lanczos(const curvkit_model* model, const double* params, const double* x, const double* y,
+                                 int64_t n, int64_t batch_size, int64_t k, int64_t max_iterations,
+                                 double residual_tol, uint64_t seed, int32_t precision, double* q_out,
+                                 double* lambda_out, double* residuals_out, int64_t* iterations_out);
+
 /* Top-k eigenpairs of the OPG G = (1/N) J^T J without forming G
  * (replaces curv::opg_eigs_incremental, eigensolve.hpp:75-76): randomized
  * range finder with `oversample` extra columns and `power_iters` power

@@ -162,8 +162,10 @@ class Ref(_Lib):
         lib.ref_hvp_operator_apply.argtypes = mdl + [i64, _dp, _dp]
         lib.ref_forward.argtypes = [_ip, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
         lib.ref_opg_eigs_incremental.argtypes = [_dp, i64, i64, i64, i64, _dp, _dp]
+        lib.ref_hessian_lanczos.argtypes = mdl + [i64, i64, i64, C.c_double, C.c_uint64, _dp, _dp, _dp,
+                                                  C.POINTER(i64)]
         for f in ("ref_hessian", "ref_opg", "ref_hessian_columns_sample", "ref_opg_rows_sample",
-                  "ref_hvp_operator_apply", "ref_forward", "ref_opg_eigs_incremental"):
+                  "ref_hvp_operator_apply", "ref_forward", "ref_opg_eigs_incremental", "ref_hessian_lanczos"):
             getattr(lib, f).restype = C.c_int
 
     def _err(self, rc):
@@ -199,6 +201,18 @@ class Ref(_Lib):
         self._call("hvp_operator_apply", w, L, a, m, _f64(params), _f64(x), _f64(y), x.shape[0],
                    batch, _f64(v), out)
         return out
+
+    def hessian_lanczos(self, spec, params, x, y, batch, k, max_iterations, residual_tol, seed):
+        """lanczos_topk on the reference HvpOperator: (q P x k, lambda, residuals, iterations)."""
+        w, L, a, m = self._m(spec)
+        P = self.param_count(w)
+        q = np.zeros((P, k))
+        lam = np.zeros(k)
+        res = np.zeros(k)
+        it = i64(0)
+        self._call("hessian_lanczos", w, L, a, m, _f64(params), _f64(x), _f64(y), x.shape[0], batch, k,
+                   max_iterations, residual_tol, seed, q, lam, res, C.byref(it))
+        return q, lam, res, int(it.value)
 
     def hessian_columns_sample(self, spec, params, x, y, c0, c1, lanes):
         w, L, a, m = self._m(spec)

@@ -256,4 +256,34 @@ int ref_opg_eigs_incremental(const double* J, int64_t n, int64_t p, int64_t bloc
     });
 }
 
+// lanczos_topk (eigensolve.cpp:46-160) on the HvpOperator of the data
+// (autodiff.hpp:72-86).  rc 4 (ConvergenceError): residuals receive the
+// best residuals the reference attaches.
+int ref_hessian_lanczos(const int64_t* w, int L, int act, int mode, const double* params, const double* x,
+                        const double* y, int64_t n, int64_t batch, int64_t k, int64_t max_iterations,
+                        double residual_tol, uint64_t seed, double* q, double* lambda, double* residuals,
+                        int64_t* iterations) {
+    return guard([&] {
+        ModelSpec s = make_spec(w, L, act, mode);
+        const std::size_t p = param_count(s);
+        HvpOperator op(s, make_params(s, params), make_batch(s, x, y, n), batch);
+        LanczosConfig cfg;
+        cfg.k = (std::size_t)k;
+        cfg.max_iterations = (std::size_t)max_iterations;
+        cfg.residual_tol = residual_tol;
+        cfg.seed = seed;
+        try {
+            LanczosResult r = lanczos_topk([&](const DenseVector& v) { return op.apply(v); }, p, cfg);
+            std::memcpy(q, r.pairs.q.data(), sizeof(double) * p * (std::size_t)k);
+            std::memcpy(lambda, r.pairs.lambda.data(), sizeof(double) * (std::size_t)k);
+            std::memcpy(residuals, r.residuals.data(), sizeof(double) * (std::size_t)k);
+            *iterations = (int64_t)r.iterations;
+        } catch (const ConvergenceError& e) {
+            for (std::size_t i = 0; i < e.best_residuals.size() && i < (std::size_t)k; ++i)
+                residuals[i] = e.best_residuals[i];
+            throw;
+        }
+    });
+}
+
 }  // extern "C"

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "curvature.cuh"
 #include "eigen.cuh"
+#include "lanczos.cuh"
 #include "gemm_tc.cuh"
 #include "model.cuh"
 #include "prof.cuh"
@@ -450,6 +451,46 @@ int curvkit_hvp_operator_apply(const curvkit_model* model, const double* params,
                      std::to_string(batch_size) + "; refusing to drop the remainder");
         if (is_f64(precision)) host_hvp<double>(md, params, x, y, n, v, nvec, precision, hv_out);
         else host_hvp<float>(md, params, x, y, n, v, nvec, precision, hv_out);
+    });
+}
+
+int curvkit_hessian_topk_lanczos(const curvkit_model* model, const double* params, const double* x, const double* y,
+                                 int64_t n, int64_t batch_size, int64_t k, int64_t max_iterations,
+                                 double residual_tol, uint64_t seed, int32_t precision, double* q_out,
+                                 double* lambda_out, double* residuals_out, int64_t* iterations_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        // the HvpOperator the reference hands to lanczos_topk (autodiff.cpp:523-537)
+        if (batch_size < 1) contract("HvpOperator: batch size must be >= 1");
+        if (n == 0) contract("HvpOperator: empty dataset");
+        if (n % batch_size != 0)
+            contract("HvpOperator: dataset size " + std::to_string(n) + " is not divisible by batch size " +
+                     std::to_string(batch_size) + "; refusing to drop the remainder");
+        // lanczos_topk's own preconditions (eigensolve.cpp:47-53), before any device work
+        if (md.P < 2) contract("lanczos_topk: operator dimension must be >= 2");
+        if (k < 1 || k >= md.P)
+            contract("lanczos_topk: need 1 <= k < p, got k = " + std::to_string(k) + ", p = " + std::to_string(md.P));
+        if (max_iterations < k) contract("lanczos_topk: max_iterations must be >= k");
+        if (!(residual_tol > 0.0)) contract("lanczos_topk: residual_tol must be > 0");
+        auto lab = labels_from_onehot(md, y, n);
+        cudaStream_t s = lib_stream();
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Resident<T> r;
+            upload_and_forward<T>(md, params, x, lab, n, r, s);
+            LanczosOut o = lanczos_topk<T>(md, dptr<T>(r.params), r.cache, k, max_iterations, residual_tol, seed,
+                                           precision, s);
+            if (iterations_out) *iterations_out = o.iterations;
+            if (residuals_out)
+                for (int64_t i = 0; i < (int64_t)o.residuals.size() && i < k; ++i) residuals_out[i] = o.residuals[i];
+            if (!o.converged)
+                throw CurvError(kConvergenceError, "lanczos_topk: not converged within " +
+                                                       std::to_string(std::min(max_iterations, md.P)) + " iterations");
+            if (q_out) std::copy(o.q.begin(), o.q.end(), q_out);
+            if (lambda_out) std::copy(o.lambda.begin(), o.lambda.end(), lambda_out);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
     });
 }
 

@@ -164,6 +164,7 @@ struct TcShape {
     int a_3d, b_3d;                     // MN-major operand loaded by one 3D TMA box
     int ksplit = 1;                     // pair kernel: K slabs per tile (Epi::block_split)
     int a_once = 0, b_once = 0;         // streamed operand: L2 evict_first
+    int group_m = 16;                   // rasterisation group (m-tiles per column sweep)
 };
 
 // Epilogues whose interior blocks are stored by TMA boxes (Epi::tma_block)
@@ -442,11 +443,12 @@ __device__ __forceinline__ void tma2_3d(void* dst, const CUtensorMap* map, uint3
 // column before moving right, so the ~74 tiles in flight share a few A and B
 // panels in L2.
 constexpr int64_t GROUP_M = 16;
-__device__ __forceinline__ void tile_coords(int64_t t, int64_t mt, int64_t nt, int64_t& mi, int64_t& ni) {
-    const int64_t per = GROUP_M * nt;
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t mt, int64_t nt, int64_t& mi, int64_t& ni,
+                                            int64_t group = GROUP_M) {
+    const int64_t per = group * nt;
     const int64_t g = t / per, local = t - g * per;
-    const int64_t gm = ::min(GROUP_M, mt - g * GROUP_M);
-    mi = g * GROUP_M + local % gm;
+    const int64_t gm = ::min(group, mt - g * group);
+    mi = g * group + local % gm;
     ni = local / gm;
 }
 
@@ -580,7 +582,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const int64_t nunits = ntiles * ksl;
     const int64_t kcb = ceil_div(nk, ksl);
     auto unit_of = [&](int64_t t, int64_t& mi, int64_t& ni, int64_t& kb0, int64_t& kb1) {
-        tile_coords(t % ntiles, mt, nt, mi, ni);
+        tile_coords(t % ntiles, mt, nt, mi, ni, sh.group_m);
         kb0 = (t / ntiles) * kcb;
         kb1 = ::min(nk, kb0 + kcb);
     };
@@ -1374,6 +1376,8 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     const int b3 = (!B.kmajor && B.ld >= round_up(N, 32)) ? 1 : 0;
     tc::TcShape sh{M, N, K, A.kmajor ? 0 : 1, B.kmajor ? 0 : 1, prec == k3xTF32 ? 3 : 1,
                    (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, a3, b3, ksplit, A.once, B.once};
+    static const int group_env = getenv("CURVKIT_GROUP_M") ? atoi(getenv("CURVKIT_GROUP_M")) : 0;  // dev knob
+    if (group_env > 0) sh.group_m = group_env;
     const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
     DevMem alo, blo, ahi, bhi;
     const float* pa = A.p;

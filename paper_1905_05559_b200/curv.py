@@ -317,6 +317,44 @@ def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 
     return EigenPairs(q, lam)
 
 
+@dataclass
+class LanczosConfig:  # eigensolve.hpp:25-30
+    k: int = 1
+    max_iterations: int = 0
+    residual_tol: float = 1e-6
+    seed: int = 0
+
+
+@dataclass
+class LanczosResult:  # eigensolve.hpp:32-36
+    pairs: EigenPairs
+    residuals: np.ndarray
+    iterations: int
+
+
+def hessian_lanczos_topk(spec: ModelSpec, params, dataset: Batch, batch_size: int, cfg: LanczosConfig,
+                         precision: str = "f64") -> LanczosResult:
+    """curv::lanczos_topk (eigensolve.hpp:44) applied to HvpOperator(spec,
+    params, dataset, batch_size): the k algebraically largest eigenpairs of
+    the Hessian, full reorthogonalisation, Krylov basis on the device.
+    Raises ConvergenceError (best residual estimates attached) when the
+    tolerance is not met within cfg.max_iterations."""
+    from .errors import ConvergenceError
+    P, params, x, y, n = _inputs(spec, params, dataset)
+    k = int(cfg.k)
+    q = np.empty((P, max(k, 1)))
+    lam = np.empty(max(k, 1))
+    res = np.zeros(max(k, 1))
+    it = C.c_int64(0)
+    rc = _lib.load().curvkit_hessian_topk_lanczos(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(batch_size), k,
+                                                   int(cfg.max_iterations), float(cfg.residual_tol), int(cfg.seed),
+                                                   _prec(precision), _p(q), _p(lam), _p(res), C.byref(it))
+    if rc == 4:
+        raise ConvergenceError(_lib.load().curvkit_last_error().decode(), res[:k].tolist())
+    _lib.check(rc)
+    return LanczosResult(EigenPairs(q, lam), res, int(it.value))
+
+
 # ---- low/full-rank operators from eigenpairs (eigensolve.hpp:78-93) ------------
 
 def low_rank_quadform(pairs: EigenPairs, x) -> float:
