@@ -135,6 +135,18 @@ int curvkit_opg_topk(const curvkit_model* model, const double* params, const dou
                      const double* y, int64_t n, int64_t k, int64_t oversample, int64_t power_iters,
                      uint64_t seed, int32_t precision, double* q_out, double* lambda_out);
 
+/* The same eigenpairs from a caller's per-example gradients, the input of
+ * curv::opg_eigs_incremental (eigensolve.hpp:75-76): j is n x p row-major
+ * (the row blocks stacked), G = (1/n) J^T J; q_out p x k, lambda_out k
+ * descending.  The device variant takes j with leading dimension ldj
+ * (ldj >= p, a multiple of 4) in the precision's storage type. */
+int curvkit_opg_topk_from_jacobian(const double* j, int64_t n, int64_t p, int64_t k, int64_t oversample,
+                                   int64_t power_iters, uint64_t seed, int32_t precision, double* q_out,
+                                   double* lambda_out);
+int curvkit_dev_opg_topk_from_jacobian(const void* j, int64_t ldj, int64_t n, int64_t p, int64_t k,
+                                       int64_t oversample, int64_t power_iters, uint64_t seed, int32_t precision,
+                                       void* q, void* lambda, void* stream);
+
 /* ---- device entry points ---------------------------------------------------
  * Device pointers in the precision's storage type (double for F64, float
  * otherwise): params P, x n x T_1 row-major, labels n int32 class indices.

@@ -359,6 +359,19 @@ void host_hvp(const ModelDesc& md, const double* params, const double* x, const 
     download<T, double>(dptr<T>(hd), md.P, nv, md.P, hv, s);
 }
 
+// opg_eigs_incremental's input contract (eigensolve.cpp:375-381): the rows of
+// J from the caller; top-k of G = (1/n) J^T J by the randomized range finder.
+template <class T>
+void topk_from_j(const T* J, int64_t ldj, int64_t n, int64_t p, int64_t k, int64_t oversample, int64_t power_iters,
+                 uint64_t seed, int prec, T* q_dev, std::vector<double>& lam, cudaStream_t s) {
+    if (n < 1 || p < 1) shape("opg_eigs: empty Jacobian");
+    ModelDesc md{};
+    md.P = p;  // no layers: the products run on the caller's J
+    Cache<T> c;
+    c.n = n;
+    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s, nullptr, J, ldj);
+}
+
 }  // namespace
 
 extern "C" {
@@ -767,6 +780,54 @@ int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params,
         Cache<float> c;
         forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
         dev_topk<float>(md, c, k, oversample, power_iters, seed, precision, (float*)q, (float*)lambda, s, &comm->c);
+    });
+}
+
+int curvkit_opg_topk_from_jacobian(const double* j, int64_t n, int64_t p, int64_t k, int64_t oversample,
+                                   int64_t power_iters, uint64_t seed, int32_t precision, double* q_out,
+                                   double* lambda_out) {
+    return guard([&] {
+        if (!j) contract("opg_eigs: null Jacobian");
+        cudaStream_t s = lib_stream();
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t ld = round_up(p, 32);
+            DevMem jd((size_t)n * p * sizeof(double), s), jt((size_t)n * ld * sizeof(T), s);
+            CK_CUDA(cudaMemcpyAsync(jd.p, j, (size_t)n * p * sizeof(double), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaMemsetAsync(jt.p, 0, (size_t)n * ld * sizeof(T), s));
+            convert_rows_kernel<double, T><<<blocks_for(n * p), 256, 0, s>>>(dptr<double>(jd), p, dptr<T>(jt), ld, n, p);
+            CK_LAUNCH();
+            DevMem q((size_t)p * k * sizeof(T), s);
+            std::vector<double> lam;
+            topk_from_j<T>(dptr<T>(jt), ld, n, p, k, oversample, power_iters, seed, precision, dptr<T>(q), lam, s);
+            std::vector<T> hq((size_t)p * k);
+            CK_CUDA(cudaMemcpyAsync(hq.data(), q.p, hq.size() * sizeof(T), cudaMemcpyDeviceToHost, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            for (size_t i = 0; i < hq.size(); ++i) q_out[i] = (double)hq[i];
+            for (int64_t i = 0; i < k; ++i) lambda_out[i] = lam[i];
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_dev_opg_topk_from_jacobian(const void* j, int64_t ldj, int64_t n, int64_t p, int64_t k,
+                                       int64_t oversample, int64_t power_iters, uint64_t seed, int32_t precision,
+                                       void* q, void* lambda, void* stream) {
+    return guard([&] {
+        if (!j) contract("opg_eigs: null Jacobian");
+        if (ldj < p || ldj % 4) contract("opg_eigs: ldj must be >= p and a multiple of 4");
+        cudaStream_t s = dev_stream(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            std::vector<double> lam;
+            topk_from_j<T>((const T*)j, ldj, n, p, k, oversample, power_iters, seed, precision, (T*)q, lam, s);
+            std::vector<T> hl(lam.begin(), lam.end());
+            CK_CUDA(cudaMemcpyAsync(lambda, hl.data(), k * sizeof(T), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
     });
 }
 

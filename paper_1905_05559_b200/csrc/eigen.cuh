@@ -485,6 +485,25 @@ __global__ void convert_d_kernel(const double* in, U* out, int64_t n) {
     if (i < n) out[i] = (U)in[i];
 }
 
+// dst (rows x cols, ldd; padding zeroed) = src rounded to nearest TF32
+template <class T>
+__global__ void copy_rn_kernel(const T* __restrict__ src, int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t rows,
+                               int64_t cols) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * ldd;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / ldd, c = i - r * ldd;
+        if constexpr (sizeof(T) == 4) dst[i] = c < cols ? round_tf32(src[r * lds + c]) : T(0);
+        else dst[i] = c < cols ? src[r * lds + c] : T(0);
+    }
+}
+
+template <class T>
+void convert_rows_rn(const T* src, int64_t lds, T* dst, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s) {
+    copy_rn_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(rows * ldd, 256), 148 * 64), 256, 0, s>>>(src, lds, dst,
+                                                                                                       ldd, rows, cols);
+    CK_LAUNCH();
+}
+
 template <class T>
 struct EigenWork {
     const ModelDesc& md;
@@ -598,7 +617,7 @@ struct EigenWork {
 template <class T>
 void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
                uint64_t seed, int prec, T* q_dev, std::vector<double>& lam_host, cudaStream_t s,
-               const Comm* comm = nullptr) {
+               const Comm* comm = nullptr, const T* Jext = nullptr, int64_t ldj_ext = 0) {
     const int64_t n = c.n, P = md.P;
     const bool sharded = comm && comm->nranks > 1;
     const TopkShard sh = TopkShard::make(md, sharded ? comm->nranks : 1, sharded ? comm->rank : 0);
@@ -610,13 +629,22 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     const int64_t ldl = round_up(l, 32);
     // TF32: J X and J^T T straight from the activations and deltas (kr.cuh);
     // otherwise the per-example gradients are formed once and stay in HBM
+    // a caller's J (opg_eigs_incremental's input): used as is, or -- TF32 --
+    // through one copy rounded to nearest TF32 (the products take it pre-rounded)
+    const bool ext = Jext != nullptr;
     std::unique_ptr<KrOperands> krop;
     if constexpr (std::is_same_v<T, float>)
-        if (prec == kTF32 && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
+        if (!ext && prec == kTF32 && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
     if (sharded && !krop) throw CurvError(kContractError, "sharded opg_topk needs TF32 precision");
-    const int64_t ldj = krop ? 0 : round_up(P, 32);
-    DevMem J((size_t)n * ldj * sizeof(T), s);
-    if (!krop) jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
+    const bool ext_copy = ext && prec == kTF32;
+    const int64_t ldj = ext && !ext_copy ? ldj_ext : (krop ? 0 : round_up(P, 32));
+    DevMem J((size_t)((ext && !ext_copy) ? 0 : n * ldj) * sizeof(T), s);
+    if (ext_copy) {
+        convert_rows_rn<T>(Jext, ldj_ext, dptr<T>(J), ldj, n, P, s);
+    } else if (!ext && !krop) {
+        jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
+    }
+    const T* Jp = (ext && !ext_copy) ? Jext : dptr<T>(J);
     const size_t rbytes = (size_t)std::max<int64_t>(R, 1) * ldl * sizeof(T);
     DevMem Y(rbytes, s), Om(rbytes, s), Y2(rbytes, s);
     DevMem Tn((size_t)n * ldl * sizeof(T), s);
@@ -632,14 +660,14 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     EigenWork<T> ew{md, s, prec, &c, krop.get(), sh, sharded ? comm : nullptr};
     T* X = dptr<T>(Om);
     for (int64_t it = 0; it <= power_iters; ++it) {
-        ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
-        ew.apply_jt(dptr<T>(J), ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
+        ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+        ew.apply_jt(Jp, ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
         ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl);
         X = dptr<T>(Y);
     }
     // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q) with round-to-nearest TF32
     // operands (J stored rounded, Q rounded per GEMM): unbiased products.
-    ew.apply_j(dptr<T>(J), ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+    ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
     ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l + 2.0 * (double)R * l * k, 0.0);
     DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
     CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));

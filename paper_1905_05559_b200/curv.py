@@ -355,6 +355,35 @@ def hessian_lanczos_topk(spec: ModelSpec, params, dataset: Batch, batch_size: in
     return LanczosResult(EigenPairs(q, lam), res, int(it.value))
 
 
+def opg_eigs_incremental(j_blocks, n_total: int, k: int, oversample: int = 20, power_iters: int = 2, seed: int = 0,
+                         precision: str = "f64") -> EigenPairs:
+    """Top-k eigenpairs of G = (1/n) J^T J from the caller's row blocks of J --
+    the input contract of curv::opg_eigs_incremental (eigensolve.hpp:75-76,
+    eigensolve.cpp:375-381) -- by the device randomized range finder."""
+    blocks = [np.ascontiguousarray(b, dtype=np.float64) for b in j_blocks]
+    if not blocks:
+        raise ContractError("opg_eigs_incremental: no row blocks")
+    p = blocks[0].shape[1]
+    if any(b.ndim != 2 or b.shape[1] != p or b.shape[0] < 1 for b in blocks):
+        raise ShapeError("opg_eigs_incremental: blocks must be b x P with b >= 1")
+    J = np.concatenate(blocks, axis=0)
+    if J.shape[0] != int(n_total):
+        raise ContractError("opg_eigs_incremental: n_total does not match the rows pushed")
+    q = np.empty((p, k))
+    lam = np.empty(k)
+    _lib.check(_lib.load().curvkit_opg_topk_from_jacobian(_p(J), J.shape[0], p, int(k), int(oversample),
+                                                           int(power_iters), int(seed), _prec(precision), _p(q),
+                                                           _p(lam)))
+    return EigenPairs(q, lam)
+
+
+def dev_opg_topk_from_jacobian(J, ldj, n, p, k, oversample, power_iters, seed, q, lam, precision="tf32",
+                               stream=None):
+    _lib.check(_lib.load().curvkit_dev_opg_topk_from_jacobian(_ptr(J), ldj, n, p, k, oversample, power_iters, seed,
+                                                               _prec(precision), _ptr(q), _ptr(lam),
+                                                               _stream(stream)))
+
+
 # ---- low/full-rank operators from eigenpairs (eigensolve.hpp:78-93) ------------
 
 def low_rank_quadform(pairs: EigenPairs, x) -> float:

@@ -239,3 +239,28 @@ print("ERR", err, bool(torch.equal(sub, sub.T)))
     assert out.returncode == 0, out.stderr[-2000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("ERR")][-1].split()
     assert float(line[1]) <= 1e-3 and line[2] == "True", line
+
+
+@pytest.mark.parametrize("prec", ["f64", "tf32"])
+def test_opg_eigs_from_jacobian_blocks(prec):
+    """opg_eigs_incremental's input contract: the caller's row blocks of J.
+    Against the reference's own streaming SVD (tests/golden/incremental_svd)
+    and, for stacked config-0 blocks, the reference's G."""
+    import os
+    from conftest import GOLDEN
+    g = np.load(os.path.join(GOLDEN, "incremental_svd.npz"))
+    J = g["J"]
+    pairs = curv.opg_eigs_incremental([J[:20], J[20:50], J[50:]], J.shape[0], 4, oversample=8, power_iters=2,
+                                      precision=prec)
+    tol = 1e-10 if prec == "f64" else 1e-3
+    np.testing.assert_allclose(pairs.lam, g["lam"], rtol=tol)
+    overlap = np.abs(np.sum(pairs.q * g["q"], axis=0))
+    assert np.all(overlap >= 1 - (1e-9 if prec == "f64" else 1e-3)), overlap
+    c0 = load_golden("config0")
+    Jc = c0["J"]
+    p2 = curv.opg_eigs_incremental([Jc[:50], Jc[50:100], Jc[100:]], Jc.shape[0], 5, oversample=10, power_iters=3,
+                                   precision=prec)
+    w = np.linalg.eigvalsh(c0["G"])[::-1][:5]
+    assert np.all(np.abs(p2.lam - w) <= (1e-9 if prec == "f64" else 1e-3) * np.abs(w))
+    with pytest.raises(curv.ContractError):
+        curv.opg_eigs_incremental([Jc[:50]], Jc.shape[0], 5)
