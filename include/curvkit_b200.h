@@ -113,6 +113,15 @@ int curvkit_assemble_opg_f32(const curvkit_model* model, const double* params, c
                              const double* y, int64_t n, const curvkit_curvature_config* cfg,
                              int32_t precision, float* g_out);
 
+/* curv::forward (model.hpp:66) for n examples: out n x T_L (softmax
+ * probabilities, or the raw output for raw_mean_output). */
+int curvkit_forward(const curvkit_model* model, const double* params, const double* x, int64_t n, int32_t precision,
+                    double* out);
+/* curv::cost (model.hpp:70): mean fused log-softmax cross-entropy over the
+ * batch (y one-hot, n x T_L), or the mean raw output (y may be NULL). */
+int curvkit_cost(const curvkit_model* model, const double* params, const double* x, const double* y, int64_t n,
+                 int32_t precision, double* cost_out);
+
 /* curv::lanczos_topk (eigensolve.hpp:44) on the HvpOperator of
  * (model, params, data, batch_size) (autodiff.hpp:72-86): the k
  * algebraically largest eigenpairs of the Hessian, Lanczos with full

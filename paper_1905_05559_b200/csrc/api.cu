@@ -372,6 +372,53 @@ void topk_from_j(const T* J, int64_t ldj, int64_t n, int64_t p, int64_t k, int64
     topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s, nullptr, J, ldj);
 }
 
+// per-example cost (model.cpp:216-256): fused log-softmax logsumexp(z) - z_y
+// on the logits in fp64, or the raw output (raw_mean_output)
+template <class T>
+__global__ void example_cost_kernel(const T* __restrict__ z, int64_t ldz, const T* __restrict__ out, int64_t ldo,
+                                    const int32_t* __restrict__ labels, int64_t n, int64_t tl, int mode,
+                                    double* __restrict__ cost) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    if (mode == kRawMean) {
+        cost[r] = (double)out[r * ldo];
+        return;
+    }
+    const T* zr = z + r * ldz;
+    double zmax = (double)zr[0];
+    for (int64_t m = 1; m < tl; ++m) zmax = fmax(zmax, (double)zr[m]);
+    double sum = 0.0;
+    for (int64_t m = 0; m < tl; ++m) sum += exp((double)zr[m] - zmax);
+    cost[r] = zmax + log(sum) - (double)zr[labels[r]];
+}
+
+template <class T>
+void host_forward_cost(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n, int prec,
+                       double* out, double* cost) {
+    if (n < 1) contract("cost: empty batch");
+    auto lab = labels_from_onehot(md, y, n);
+    cudaStream_t s = lib_stream();
+    Resident<T> r;
+    upload_and_forward<T>(md, params, x, lab, n, r, s);
+    const int S = md.S;
+    const int64_t tl = md.w[S];
+    if (out) download<T, double>(r.cache.a[S], r.cache.lda[S], n, tl, out, s);
+    if (cost) {
+        DevMem cd((size_t)n * sizeof(double), s);
+        example_cost_kernel<T><<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(
+            r.cache.z[S - 1], r.cache.ldt[S - 1], r.cache.a[S], r.cache.lda[S], dptr<int32_t>(r.labels), n, tl,
+            md.mode, dptr<double>(cd));
+        CK_LAUNCH();
+        std::vector<double> hc(n);
+        CK_CUDA(cudaMemcpyAsync(hc.data(), cd.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaStreamSynchronize(s));
+        double total = 0.0;
+        for (double v : hc) total += v;  // fixed order: deterministic
+        *cost = total / (double)n;
+    }
+    (void)prec;
+}
+
 }  // namespace
 
 extern "C" {
@@ -464,6 +511,35 @@ int curvkit_hvp_operator_apply(const curvkit_model* model, const double* params,
                      std::to_string(batch_size) + "; refusing to drop the remainder");
         if (is_f64(precision)) host_hvp<double>(md, params, x, y, n, v, nvec, precision, hv_out);
         else host_hvp<float>(md, params, x, y, n, v, nvec, precision, hv_out);
+    });
+}
+
+// curv::forward (model.cpp:178-199) for n examples at once: out n x T_L
+// (softmax probabilities, or the raw output for raw_mean_output).
+int curvkit_forward(const curvkit_model* model, const double* params, const double* x, int64_t n, int32_t precision,
+                    double* out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (!out) contract("forward: null output");
+        std::vector<double> y;
+        if (md.mode == kSoftmaxCE) {  // the forward pass needs no labels: any one-hot row
+            y.assign((size_t)n * md.w[md.L - 1], 0.0);
+            for (int64_t r = 0; r < n; ++r) y[r * md.w[md.L - 1]] = 1.0;
+        }
+        if (is_f64(precision)) host_forward_cost<double>(md, params, x, y.empty() ? nullptr : y.data(), n, precision, out, nullptr);
+        else host_forward_cost<float>(md, params, x, y.empty() ? nullptr : y.data(), n, precision, out, nullptr);
+    });
+}
+
+// curv::cost (model.cpp:216-256): mean fused log-softmax cross-entropy (or
+// mean raw output).
+int curvkit_cost(const curvkit_model* model, const double* params, const double* x, const double* y, int64_t n,
+                 int32_t precision, double* cost_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (!cost_out) contract("cost: null output");
+        if (is_f64(precision)) host_forward_cost<double>(md, params, x, y, n, precision, nullptr, cost_out);
+        else host_forward_cost<float>(md, params, x, y, n, precision, nullptr, cost_out);
     });
 }
 

@@ -204,6 +204,35 @@ def _inputs(spec: ModelSpec, params, batch: Batch):
     return P, params, x, y, n
 
 
+def forward(spec: ModelSpec, params, x, precision: str = "f64") -> np.ndarray:
+    """curv::forward (model.hpp:66): the network output (softmax
+    probabilities, or the raw output).  x: one example (T_1,) as in the
+    reference, or a batch (n, T_1) -> (n, T_L)."""
+    spec.validate()
+    params = _f64(params).reshape(-1)
+    if params.shape[0] != param_count(spec):
+        raise ShapeError(f"parameter vector has length {params.shape[0]}, model needs {param_count(spec)}")
+    x = _f64(x)
+    single = x.ndim == 1
+    xb = x.reshape(1, -1) if single else x
+    if xb.ndim != 2 or xb.shape[1] != spec.input_width():
+        raise ShapeError(f"forward: input has length {xb.shape[-1]}, model expects {spec.input_width()}")
+    out = np.empty((xb.shape[0], spec.output_width()))
+    _lib.check(_lib.load().curvkit_forward(C.byref(spec._c()), _p(params), _p(xb), xb.shape[0], _prec(precision),
+                                            _p(out)))
+    return out[0] if single else out
+
+
+def cost(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> float:
+    """curv::cost (model.hpp:70): mean cross-entropy (fused log-softmax) or
+    mean raw output over the batch."""
+    P, params, x, y, n = _inputs(spec, params, batch)
+    out = C.c_double()
+    _lib.check(_lib.load().curvkit_cost(C.byref(spec._c()), _p(params), _p(x), None if y is None else _p(y), n,
+                                         _prec(precision), C.byref(out)))
+    return out.value
+
+
 def assemble_jacobian(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> np.ndarray:
     """curvature.hpp:32-33: N x P, row n = gradient of C_n."""
     P, params, x, y, n = _inputs(spec, params, batch)

@@ -264,3 +264,24 @@ def test_opg_eigs_from_jacobian_blocks(prec):
     assert np.all(np.abs(p2.lam - w) <= (1e-9 if prec == "f64" else 1e-3) * np.abs(w))
     with pytest.raises(curv.ContractError):
         curv.opg_eigs_incremental([Jc[:50]], Jc.shape[0], 5)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("name", SMALL_CASES + ["config0", "linear_diag"])
+def test_forward_and_cost_match_oracle(name, prec):
+    """curv::forward and curv::cost (model.cpp:178-256) against the C oracle."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.oracle import Oracle
+    g = load_golden(name)
+    spec = spec_of(g)
+    orc = Oracle()
+    tol = 1e-12 if prec == "f64" else 1e-5
+    c_ref = orc.cost(g["spec"], g["params"], g["x"], g["y"])
+    c = curv.cost(spec, g["params"], curv.Batch(g["x"], g["y"]), precision=prec)
+    assert abs(c - c_ref) <= tol * max(1.0, abs(c_ref))
+    out = curv.forward(spec, g["params"], g["x"], precision=prec)
+    one = curv.forward(spec, g["params"], g["x"][0], precision=prec)
+    np.testing.assert_allclose(one, out[0], rtol=tol, atol=tol)
+    if spec.output_mode == curv.OutputMode.softmax_cross_entropy:
+        np.testing.assert_allclose(out.sum(axis=1), 1.0, atol=tol * 10)
