@@ -25,6 +25,7 @@
 #include <mutex>
 
 #include "curvature.cuh"
+#include "gemm_dmma.cuh"
 
 namespace ck {
 namespace tc {
