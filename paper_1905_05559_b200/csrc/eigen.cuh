@@ -516,13 +516,16 @@ struct EigenWork {
 
     // Y <- orth(Y) (CholeskyQR2, fp64 Gram): pass 1 writes Y Rinv into the
     // scratch Y2, pass 2 writes back into Y; no host round trip
-    void orth(T* Y, T* Y2, int64_t rows, int64_t l, int64_t ld) {
+    // passes = 1 (between power iterations: the fp64 Gram keeps the basis
+    // well conditioned) or 2 (CholeskyQR2, the final basis); returns the
+    // buffer holding the result (Y after 2 passes, Y2 after 1)
+    T* orth(T* Y, T* Y2, int64_t rows, int64_t l, int64_t ld, int passes = 2) {
         ProfScope ps("eig_orth", s, 2.0 * 2.0 * 2.0 * (double)rows * l * l, 2.0 * 2.0 * 2.0 * sizeof(T) * rows * ld);
         DevMem W((size_t)l * l * sizeof(double), s), Rinv((size_t)l * l * sizeof(double), s);
         DevMem Rt((size_t)l * l * sizeof(T), s);
         T* src = Y;
         T* dst = Y2;
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < passes; ++pass) {
             ProfScope p1("orth_gram", s, 0.0, 0.0);
             CK_CUDA(cudaMemsetAsync(W.p, 0, l * l * sizeof(double), s));
             {
@@ -552,6 +555,7 @@ struct EigenWork {
             p3.end();
             std::swap(src, dst);
         }
+        return src;
     }
 
     // shifted Cholesky + inverse of the l x l Gram (shared memory when it fits)
@@ -662,8 +666,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     for (int64_t it = 0; it <= power_iters; ++it) {
         ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
         ew.apply_jt(Jp, ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
-        ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl);
-        X = dptr<T>(Y);
+        X = ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl, it < power_iters ? 1 : 2);
     }
     // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q) with round-to-nearest TF32
     // operands (J stored rounded, Q rounded per GEMM): unbiased products.
