@@ -337,9 +337,12 @@ __global__ void chol_inv_kernel(double* W, int64_t l, double rel, double* Rinv) 
 // sqrt|a_pp a_qq|, or below 1e-18 ||A||_F); a sweep without rotations ends
 // the iteration (the threshold Jacobi method).  Out: A's diagonal holds the
 // eigenvalues, V (l x l, row-major) the eigenvectors by columns.
-template <class VT>
+template <class VT, bool SMEM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int l, int max_sweeps,
-                                                      int* sweeps_out, int a_in_smem) {
+                                                      int* sweeps_out, int a_in_smem_rt) {
+    // SMEM: A (and for fp32 vectors Vt) statically in shared memory, so every
+    // rotation is LDS/STS, never a generic access
+    const int a_in_smem = SMEM ? 1 : a_in_smem_rt;
     extern __shared__ double sh[];
     const int m = l + (l & 1);  // pad to even with a dummy index
     const int np = m / 2;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
     int* pp = reinterpret_cast<int*>(sh + m);
     int* qq = pp + np;
     const int lda = a_in_smem ? l + ((l + 1) & 1) : l;  // odd pitch in shared memory
-    double* A = a_in_smem ? sh + m + np + 1 : Ag;
+    double* A = SMEM ? sh + m + np + 1 : (a_in_smem ? sh + m + np + 1 : Ag);
     // transposed eigenvectors: fp64 in place in V, or fp32 in shared memory
     // after A (the eigenvalues come from A's fp64 rotations either way)
     VT* Vt;
@@ -466,15 +469,18 @@ inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_
     const size_t with_v = with_a + (size_t)l * l * sizeof(float);
     static bool attr = false;
     if (!attr) {
-        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+        CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
         attr = true;
     }
     if (fp32_vectors && with_v <= 200 * 1024) {
-        jacobi_kernel<float><<<1, dim3(128, 8), with_v, s>>>(A, V, (int)l, 60, sweeps, 1);
+        jacobi_kernel<float, true><<<1, dim3(128, 8), with_v, s>>>(A, V, (int)l, 60, sweeps, 1);
     } else {
         const bool smem_a = with_a <= 200 * 1024;
-        jacobi_kernel<double><<<1, dim3(128, 8), smem_a ? with_a : base, s>>>(A, V, (int)l, 60, sweeps, smem_a ? 1 : 0);
+        jacobi_kernel<double, false><<<1, dim3(128, 8), smem_a ? with_a : base, s>>>(A, V, (int)l, 60, sweeps,
+                                                                                  smem_a ? 1 : 0);
     }
     CK_LAUNCH();
 }

@@ -184,8 +184,9 @@ struct EpiSymLower {
     // tensor-core epilogue: 32 x 32 blocks strictly below the diagonal go out
     // as two TMA boxes (entry block at (row, col), mirror at (col, row))
     static constexpr bool kTmaStore = true;
+    int tma = 1;  // cleared by the launcher when C's pitch cannot be a TMA tensor (ldc % 4 != 0)
     __device__ bool tma_block(int64_t row0, int64_t col0, int64_t M, int64_t N, int64_t& gr0, int64_t& gc0) const {
-        if (row0 + 32 > M || col0 + 32 > N) return false;
+        if (!tma || row0 + 32 > M || col0 + 32 > N) return false;
         gr0 = row0 + roff;
         gc0 = col0;
         return gc0 + 31 < gr0;

@@ -1352,11 +1352,12 @@ void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const 
     const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN) * std::max(1, sh.ksplit);
     const int grid = 2 * (int)std::min<int64_t>(tiles, num_sms() / 2);
     CUtensorMap mc = a;  // unused unless the epilogue stores by TMA
+    Epi ee = e;
     if constexpr (EpiTma<Epi>::value) {
-        if (e.ldc % 4) throw CurvError(kContractError, "tensor-core symmetric store needs ldc % 4 == 0");
-        mc = make_map_h(e.c, e.ldc);
+        if (e.ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(e.c) & 15) == 0) mc = make_map_h(e.c, e.ldc);
+        else ee.tma = 0;  // pitch not TMA-addressable: scalar epilogue for every block
     }
-    pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, mc, sh, e);
+    pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, mc, sh, ee);
     CK_LAUNCH();
 }
 

@@ -285,3 +285,20 @@ def test_forward_and_cost_match_oracle(name, prec):
     np.testing.assert_allclose(one, out[0], rtol=tol, atol=tol)
     if spec.output_mode == curv.OutputMode.softmax_cross_entropy:
         np.testing.assert_allclose(out.sum(axis=1), 1.0, atol=tol * 10)
+
+
+def test_opg_odd_pitch_device_buffer():
+    """dev_assemble_opg (config 1: the CTA-pair SYRK with its TMA-box
+    epilogue) into a buffer whose pitch is not a multiple of 4, where no TMA
+    tensor is possible: the scalar epilogue must give the same G."""
+    torch = pytest.importorskip("torch")
+    wl = CONFIGS["c1"]
+    p, x, lab = _device_inputs(wl, torch, torch.float32)
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P = wl.P
+    G1 = torch.zeros((P, P + 2), device="cuda:0")  # P + 2 = 25452: TMA-addressable
+    curv.dev_assemble_opg(spec, p, x, lab, wl.n, G1, P + 2, precision="tf32")
+    G2 = torch.zeros((P, P + 1), device="cuda:0")  # odd pitch
+    curv.dev_assemble_opg(spec, p, x, lab, wl.n, G2, P + 1, precision="tf32")
+    torch.cuda.synchronize()
+    assert torch.equal(G1[:, :P], G2[:, :P])
