@@ -1583,7 +1583,7 @@ struct HessFused<float> {
             fh.trace = dptr<long long>(trbuf);
         }
         // H as a 2D map of 32 x 32 boxes (128-byte swizzle) for the epilogue
-        fh.tma_h = (e.ldh % 4 == 0) ? 1 : 0;
+        fh.tma_h = (e.ldh % 4 == 0 && (reinterpret_cast<uintptr_t>(e.H) & 15) == 0) ? 1 : 0;
         CUtensorMap mh = fh.tma_h ? tc::make_map_h(e.H, e.ldh) : mb;
         pair::tc_hess_fused_kernel<BN, EpiHess<float>, TS><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
             mak, mq, mb, mpv, mdt, mh, fh, sh, e);
