@@ -398,41 +398,61 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
                         const double th = 0.5 * (aqq - app) / apq;
                         double tt = 1.0 / (fabs(th) + sqrt(1.0 + th * th));
                         if (th < 0.0) tt = -tt;
-                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        c = rsqrt(1.0 + tt * tt);
                         s = tt * c;
-                        atomicAdd(&nrot, 1);
+                        nrot = 1;  // any rotation this sweep (a plain store: no atomic serialisation)
                     }
                 }
                 cs[k] = c;
                 sn[k] = s;
             }
             __syncthreads();
-            // A <- A J (columns a, b), Vt <- J^T Vt (rows a, b)
-            for (int k = ty; k < np; k += blockDim.y) {
-                const double s = sn[k];
-                if (s == 0.0) continue;
-                const int a = pp[k], b = qq[k];
-                const double c = cs[k];
-                for (int i = tx; i < l; i += blockDim.x) {
-                    const double x = A[i * lda + a], y = A[i * lda + b];
-                    A[i * lda + a] = c * x - s * y;
-                    A[i * lda + b] = s * x + c * y;
-                    const VT vx = Vt[a * l + i], vy = Vt[b * l + i];
-                    Vt[a * l + i] = (VT)c * vx - (VT)s * vy;
-                    Vt[b * l + i] = (VT)s * vx + (VT)c * vy;
+            // A <- J^T A J in one pass: for pair-indices (k, g), k <= g, the 2 x 2
+            // block A[{a_k, b_k}, {a_g, b_g}] becomes J_k^T B J_g (J = [[c, s], [-s, c]]),
+            // written with its mirror; the eigenvector rows a_k, b_k of Vt rotate
+            // in the same phase (rows and blocks are disjoint within a round)
+            {
+                const int nb = np * (np + 1) / 2;
+                for (int idx = t; idx < nb; idx += nt) {
+                    // triangular index -> (k, g), k <= g
+                    int k = (int)((sqrtf(8.f * idx + 1.f) - 1.f) * 0.5f);
+                    while ((k + 1) * (k + 2) / 2 <= idx) ++k;
+                    while (k * (k + 1) / 2 > idx) --k;
+                    const int g = idx - k * (k + 1) / 2;  // g <= k: block (g, k)
+                    const int ak = pp[g], bk = qq[g], ag = pp[k], bg = qq[k];
+                    const double ck = cs[g], sk = sn[g], cg = cs[k], sg = sn[k];
+                    if ((sk == 0.0 && sg == 0.0)) continue;
+                    const bool vk = bk < l, vg = bg < l;  // the padded dummy index is never stored
+                    double b00 = A[ak * lda + ag], b01 = vg ? A[ak * lda + bg] : 0.0;
+                    double b10 = vk ? A[bk * lda + ag] : 0.0, b11 = (vk && vg) ? A[bk * lda + bg] : 0.0;
+                    // right: columns (a_g, b_g) by J_g
+                    double t00 = cg * b00 - sg * b01, t01 = sg * b00 + cg * b01;
+                    double t10 = cg * b10 - sg * b11, t11 = sg * b10 + cg * b11;
+                    // left: rows (a_k, b_k) by J_k^T
+                    b00 = ck * t00 - sk * t10; b10 = sk * t00 + ck * t10;
+                    b01 = ck * t01 - sk * t11; b11 = sk * t01 + ck * t11;
+                    A[ak * lda + ag] = b00;
+                    if (vg) A[ak * lda + bg] = b01;
+                    if (vk) A[bk * lda + ag] = b10;
+                    if (vk && vg) A[bk * lda + bg] = b11;
+                    if (g != k) {  // mirror
+                        A[ag * lda + ak] = b00;
+                        if (vg) A[bg * lda + ak] = b01;
+                        if (vk) A[ag * lda + bk] = b10;
+                        if (vk && vg) A[bg * lda + bk] = b11;
+                    }
                 }
-            }
-            __syncthreads();
-            // A <- J^T A (rows a, b)
-            for (int k = ty; k < np; k += blockDim.y) {
-                const double s = sn[k];
-                if (s == 0.0) continue;
-                const int a = pp[k], b = qq[k];
-                const double c = cs[k];
-                for (int i = tx; i < l; i += blockDim.x) {
-                    const double x = A[a * lda + i], y = A[b * lda + i];
-                    A[a * lda + i] = c * x - s * y;
-                    A[b * lda + i] = s * x + c * y;
+                for (int k = ty; k < np; k += blockDim.y) {
+                    const double s = sn[k];
+                    if (s == 0.0) continue;
+                    const int a = pp[k], b = qq[k];
+                    if (b >= l) continue;
+                    const double c = cs[k];
+                    for (int i = tx; i < l; i += blockDim.x) {
+                        const VT vx = Vt[a * l + i], vy = Vt[b * l + i];
+                        Vt[a * l + i] = (VT)c * vx - (VT)s * vy;
+                        Vt[b * l + i] = (VT)s * vx + (VT)c * vy;
+                    }
                 }
             }
             __syncthreads();
@@ -460,6 +480,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(double* Ag, double* V, int
 
 // one-CTA symmetric eigensolve of the l x l matrix A (in place: diagonal =
 // eigenvalues, V = eigenvectors by columns)
+inline unsigned jacobi_ty() {  // dev knob: rows of 128 threads in the Jacobi CTA
+    static const unsigned ty = getenv("CURVKIT_JACOBI_TY") ? (unsigned)atoi(getenv("CURVKIT_JACOBI_TY")) : 8;
+    return ty;
+}
+
 // fp32_vectors: accumulate the rotations of the eigenvectors in fp32 shared
 // memory (enough for fp32 outputs), so no rotation touches global memory.
 inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_t s, bool fp32_vectors = false) {
@@ -476,7 +501,7 @@ inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_
         attr = true;
     }
     if (fp32_vectors && with_v <= 200 * 1024) {
-        jacobi_kernel<float, true><<<1, dim3(128, 8), with_v, s>>>(A, V, (int)l, 60, sweeps, 1);
+        jacobi_kernel<float, true><<<1, dim3(128, jacobi_ty()), with_v, s>>>(A, V, (int)l, 60, sweeps, 1);
     } else {
         const bool smem_a = with_a <= 200 * 1024;
         jacobi_kernel<double, false><<<1, dim3(128, 8), smem_a ? with_a : base, s>>>(A, V, (int)l, 60, sweeps,
