@@ -415,6 +415,44 @@ def dev_opg_topk_from_jacobian(J, ldj, n, p, k, oversample, power_iters, seed, q
 
 # ---- low/full-rank operators from eigenpairs (eigensolve.hpp:78-93) ------------
 
+def validate_eigen_pairs(pairs: EigenPairs, ortho_tol: float = 1e-8) -> None:
+    """curv::validate_eigen_pairs (eigensolve.cpp:11-29): lambda length,
+    descending order and column orthonormality within ortho_tol."""
+    q = np.asarray(pairs.q, dtype=np.float64)
+    lam = np.asarray(pairs.lam, dtype=np.float64)
+    p, k = q.shape
+    if lam.shape[0] != k:
+        raise ShapeError("EigenPairs: lambda length does not match column count")
+    if k > p:
+        raise ShapeError("EigenPairs: more columns than rows")
+    if np.any(lam[:-1] < lam[1:]):
+        raise ContractError("EigenPairs: eigenvalues not sorted descending")
+    if k and np.abs(q.T @ q - np.eye(k)).max() > ortho_tol:
+        raise ContractError("EigenPairs: columns are not orthonormal")
+
+
+def _check_dense_cap(p: int, memory_cap: int, who: str):  # eigensolve.cpp:255-260
+    if p > memory_cap:
+        raise ContractError(f"{who}: P = {p} exceeds the dense memory cap {memory_cap}; "
+                            "use the implicit quadform/apply forms instead")
+
+
+def low_rank_materialize(pairs: EigenPairs, memory_cap: int = 4096) -> np.ndarray:
+    """curv::low_rank_materialize (eigensolve.cpp): Q diag(lambda) Q^T."""
+    q = np.asarray(pairs.q, dtype=np.float64)
+    _check_dense_cap(q.shape[0], memory_cap, "low_rank_materialize")
+    return (q * np.asarray(pairs.lam)) @ q.T
+
+
+def full_rank_materialize(pairs: EigenPairs, lambda_tilde: float, memory_cap: int = 4096) -> np.ndarray:
+    """curv::full_rank_materialize: Q diag(lambda) Q^T + lambda_tilde (I - Q Q^T)."""
+    if not lambda_tilde > 0.0:
+        raise ContractError(f"full-rank approximation requires lambda_tilde > 0, got {lambda_tilde}")
+    q = np.asarray(pairs.q, dtype=np.float64)
+    _check_dense_cap(q.shape[0], memory_cap, "full_rank_materialize")
+    return low_rank_materialize(pairs, memory_cap) - lambda_tilde * (q @ q.T) + lambda_tilde * np.eye(q.shape[0])
+
+
 def low_rank_quadform(pairs: EigenPairs, x) -> float:
     t = pairs.q.T @ np.asarray(x, dtype=np.float64)
     return float(np.sum(pairs.lam * t * t))
