@@ -5,7 +5,7 @@
  * Drop-in boundary for the hot path of the reference curvkit library
  * (/root/reference/proj).  Every entry point below replaces one reference
  * C++ interface, cited beside it; argument meaning, flat parameter order
- * (model.hpp:52-55), row-major matrices and the error classes
+ * (model.hpp:44-46), row-major matrices and the error classes
  * (errors.hpp: ShapeError / ContractError / ConvergenceError) are the
  * reference's.  Only plain pointers and sizes cross the boundary.
  *
@@ -35,7 +35,7 @@ enum curvkit_status {
     CURVKIT_OUT_OF_MEMORY = 6
 };
 
-/* Activation (model.hpp:11) and OutputMode (model.hpp:21) as integers. */
+/* Activation (model.hpp:11) and OutputMode (model.hpp:20) as integers. */
 enum curvkit_activation { CURVKIT_IDENTITY = 0, CURVKIT_SIGMOID = 1, CURVKIT_TANH = 2, CURVKIT_RELU = 3 };
 enum curvkit_output_mode { CURVKIT_SOFTMAX_CROSS_ENTROPY = 0, CURVKIT_RAW_MEAN_OUTPUT = 1 };
 
@@ -46,7 +46,7 @@ enum curvkit_output_mode { CURVKIT_SOFTMAX_CROSS_ENTROPY = 0, CURVKIT_RAW_MEAN_O
  * hi+lo TF32 parts for fp32-grade products on tensor cores. */
 enum curvkit_precision { CURVKIT_F64 = 0, CURVKIT_F32 = 1, CURVKIT_TF32 = 2, CURVKIT_TF32X3 = 3 };
 
-/* curv::ModelSpec (model.hpp:27-38). */
+/* curv::ModelSpec (model.hpp:27-42). */
 typedef struct curvkit_model {
     int32_t num_layers;          /* L >= 2 */
     const int64_t* layer_widths; /* T_1 .. T_L */
@@ -73,7 +73,7 @@ int curvkit_param_count(const curvkit_model* model, int64_t* p_out);
  * params: P doubles (canonical order); x: n x T_1; y: n x T_L one-hot
  * (ignored in raw_mean_output mode, may be NULL there).                     */
 
-/* curv::assemble_jacobian (curvature.hpp:32-33): j_out n x P */
+/* curv::assemble_jacobian (curvature.hpp:35-36): j_out n x P */
 int curvkit_assemble_jacobian(const curvkit_model* model, const double* params, const double* x,
                               const double* y, int64_t n, int32_t precision, double* j_out);
 
@@ -81,18 +81,18 @@ int curvkit_assemble_jacobian(const curvkit_model* model, const double* params, 
 int curvkit_grad_batch(const curvkit_model* model, const double* params, const double* x,
                        const double* y, int64_t n, int32_t precision, double* grad_total_out);
 
-/* curv::hvp (autodiff.hpp:66-67), batched over nvec directions:
+/* curv::hvp (autodiff.hpp:60-65), batched over nvec directions:
  * v: nvec x P (one direction per row), hv_out: nvec x P */
 int curvkit_hvp(const curvkit_model* model, const double* params, const double* x, const double* y,
                 int64_t n, const double* v, int64_t nvec, int32_t precision, double* hv_out);
 
-/* curv::HvpOperator (autodiff.hpp:76-89) constructed with batch_size and
+/* curv::HvpOperator (autodiff.hpp:70-84) constructed with batch_size and
  * applied to nvec directions (rows of v). */
 int curvkit_hvp_operator_apply(const curvkit_model* model, const double* params, const double* x,
                                const double* y, int64_t n, int64_t batch_size, const double* v,
                                int64_t nvec, int32_t precision, double* hv_out);
 
-/* curv::assemble_hessian (curvature.hpp:27-29): h_out P x P, exactly
+/* curv::assemble_hessian (curvature.hpp:25-32): h_out P x P, exactly
  * symmetric.  asymmetry_out (may be NULL) receives max|H - H^T| before
  * symmetrization when verify != 0 (diagonal layer blocks assembled from
  * both triangles), else 0 (lower triangle mirrored by construction). */
@@ -100,7 +100,7 @@ int curvkit_assemble_hessian(const curvkit_model* model, const double* params, c
                              const double* y, int64_t n, const curvkit_curvature_config* cfg,
                              int32_t precision, int32_t verify, double* h_out, double* asymmetry_out);
 
-/* curv::assemble_opg (curvature.hpp:38-40): g_out P x P */
+/* curv::assemble_opg (curvature.hpp:37-42): g_out P x P */
 int curvkit_assemble_opg(const curvkit_model* model, const double* params, const double* x,
                          const double* y, int64_t n, const curvkit_curvature_config* cfg,
                          int32_t precision, double* g_out);
@@ -113,17 +113,17 @@ int curvkit_assemble_opg_f32(const curvkit_model* model, const double* params, c
                              const double* y, int64_t n, const curvkit_curvature_config* cfg,
                              int32_t precision, float* g_out);
 
-/* curv::forward (model.hpp:66) for n examples: out n x T_L (softmax
+/* curv::forward (model.hpp:80) for n examples: out n x T_L (softmax
  * probabilities, or the raw output for raw_mean_output). */
 int curvkit_forward(const curvkit_model* model, const double* params, const double* x, int64_t n, int32_t precision,
                     double* out);
-/* curv::cost (model.hpp:70): mean fused log-softmax cross-entropy over the
+/* curv::cost (model.hpp:84): mean fused log-softmax cross-entropy over the
  * batch (y one-hot, n x T_L), or the mean raw output (y may be NULL). */
 int curvkit_cost(const curvkit_model* model, const double* params, const double* x, const double* y, int64_t n,
                  int32_t precision, double* cost_out);
 
-/* curv::lanczos_topk (eigensolve.hpp:44) on the HvpOperator of
- * (model, params, data, batch_size) (autodiff.hpp:72-86): the k
+/* curv::lanczos_topk (eigensolve.hpp:36-45) on the HvpOperator of
+ * (model, params, data, batch_size) (autodiff.hpp:70-84): the k
  * algebraically largest eigenpairs of the Hessian, Lanczos with full
  * reorthogonalisation, the Krylov basis resident on the device.  q_out: P x k
  * (columns are eigenvectors), lambda_out: k descending, residuals_out: k
@@ -136,7 +136,7 @@ int curvkit_hessian_topk_lanczos(const curvkit_model* model, const double* param
                                  double* lambda_out, double* residuals_out, int64_t* iterations_out);
 
 /* Top-k eigenpairs of the OPG G = (1/N) J^T J without forming G
- * (replaces curv::opg_eigs_incremental, eigensolve.hpp:75-76): randomized
+ * (replaces curv::opg_eigs_incremental, eigensolve.hpp:80-81): randomized
  * range finder with `oversample` extra columns and `power_iters` power
  * iterations, Rayleigh-Ritz on the projected (k+oversample)^2 matrix.
  * q_out: P x k (columns are eigenvectors), lambda_out: k, descending. */
@@ -145,7 +145,7 @@ int curvkit_opg_topk(const curvkit_model* model, const double* params, const dou
                      uint64_t seed, int32_t precision, double* q_out, double* lambda_out);
 
 /* The same eigenpairs from a caller's per-example gradients, the input of
- * curv::opg_eigs_incremental (eigensolve.hpp:75-76): j is n x p row-major
+ * curv::opg_eigs_incremental (eigensolve.hpp:80-81): j is n x p row-major
  * (the row blocks stacked), G = (1/n) J^T J; q_out p x k, lambda_out k
  * descending.  The device variant takes j with leading dimension ldj
  * (ldj >= p, a multiple of 4) in the precision's storage type. */

@@ -241,7 +241,7 @@ int ref_sym_eig(const double* a, int64_t n, double* vals, double* vecs) {
     });
 }
 
-// opg_eigs_incremental over row blocks of J (eigensolve.cpp:375-381).
+// opg_eigs_incremental over row blocks of J (eigensolve.cpp:245-251).
 int ref_opg_eigs_incremental(const double* J, int64_t n, int64_t p, int64_t block, int64_t k,
                              double* q, double* lambda) {
     return guard([&] {
@@ -256,8 +256,8 @@ int ref_opg_eigs_incremental(const double* J, int64_t n, int64_t p, int64_t bloc
     });
 }
 
-// lanczos_topk (eigensolve.cpp:46-160) on the HvpOperator of the data
-// (autodiff.hpp:72-86).  rc 4 (ConvergenceError): residuals receive the
+// lanczos_topk (eigensolve.cpp:46-156) on the HvpOperator of the data
+// (autodiff.hpp:70-84).  rc 4 (ConvergenceError): residuals receive the
 // best residuals the reference attaches.
 int ref_hessian_lanczos(const int64_t* w, int L, int act, int mode, const double* params, const double* x,
                         const double* y, int64_t n, int64_t batch, int64_t k, int64_t max_iterations,

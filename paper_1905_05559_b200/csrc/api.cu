@@ -1,7 +1,7 @@
 // api.cu -- the C-ABI (include/curvkit_b200.h) over the B200 engine.
 //
 // Validation and error text follow the reference (model.cpp:80-87,
-// model.cpp:201-214, curvature.cpp:15-29, autodiff.cpp:523-537) so a caller
+// model.cpp:201-214, curvature.cpp:15-29, autodiff.cpp:266-280) so a caller
 // switching from curvkit sees the same contract errors for the same inputs.
 #include <atomic>
 #include <cstring>
@@ -359,7 +359,7 @@ void host_hvp(const ModelDesc& md, const double* params, const double* x, const 
     download<T, double>(dptr<T>(hd), md.P, nv, md.P, hv, s);
 }
 
-// opg_eigs_incremental's input contract (eigensolve.cpp:375-381): the rows of
+// opg_eigs_incremental's input contract (eigensolve.cpp:245-251): the rows of
 // J from the caller; top-k of G = (1/n) J^T J by the randomized range finder.
 template <class T>
 void topk_from_j(const T* J, int64_t ldj, int64_t n, int64_t p, int64_t k, int64_t oversample, int64_t power_iters,
@@ -503,7 +503,7 @@ int curvkit_hvp_operator_apply(const curvkit_model* model, const double* params,
                                double* hv_out) {
     return guard([&] {
         ModelDesc md = make_desc(model);
-        // autodiff.cpp:523-537; equal mini-batches average to the full mean
+        // autodiff.cpp:266-280; equal mini-batches average to the full mean
         if (batch_size < 1) contract("HvpOperator: batch size must be >= 1");
         if (n == 0) contract("HvpOperator: empty dataset");
         if (n % batch_size != 0)
@@ -549,7 +549,7 @@ int curvkit_hessian_topk_lanczos(const curvkit_model* model, const double* param
                                  double* lambda_out, double* residuals_out, int64_t* iterations_out) {
     return guard([&] {
         ModelDesc md = make_desc(model);
-        // the HvpOperator the reference hands to lanczos_topk (autodiff.cpp:523-537)
+        // the HvpOperator the reference hands to lanczos_topk (autodiff.cpp:266-280)
         if (batch_size < 1) contract("HvpOperator: batch size must be >= 1");
         if (n == 0) contract("HvpOperator: empty dataset");
         if (n % batch_size != 0)

@@ -1,6 +1,6 @@
 // curvature.cuh -- orchestration of the curvature products on one GPU.
 //
-//   hvp      batched Pearlmutter R-op (autodiff.cpp:415-501): every layer of
+//   hvp      batched Pearlmutter R-op (autodiff.cpp:158-244): every layer of
 //            the R-forward / R-backward pass and the final accumulation is
 //            a GEMM over (direction x example) rows.
 //   hessian  exact H (curvature.cpp:33-92).  Column p of H is the HVP on the

@@ -10,8 +10,8 @@
 // gradient matrix J, which stays in HBM.  orth() is CholeskyQR2 with the
 // l x l Gram matrices accumulated in fp64.
 //
-// Replaces the reference's streaming SVD (eigensolve.cpp:288-381); its
-// eigenvalue scaling sigma^2 / N (eigensolve.cpp:366-372) is the same
+// Replaces the reference's streaming SVD (eigensolve.cpp:158-251); its
+// eigenvalue scaling sigma^2 / N (eigensolve.cpp:236-242) is the same
 // quantity as lambda(B) here.
 #pragma once
 

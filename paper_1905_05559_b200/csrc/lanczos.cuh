@@ -1,16 +1,16 @@
-// lanczos.cuh -- curv::lanczos_topk (eigensolve.cpp:46-160) on the Hessian
+// lanczos.cuh -- curv::lanczos_topk (eigensolve.cpp:46-156) on the Hessian
 // operator, with the Krylov basis resident in HBM.
 //
 // Each step applies H by the device R-op engine (Engine::hvp: one batched
 // forward/backward R-pass), then alpha, the three-term recurrence and two
 // classical Gram-Schmidt passes against the whole basis (the reference's full
-// reorthogonalisation, eigensolve.cpp:72-74) as fp64-accumulating kernels.
+// reorthogonalisation, eigensolve.cpp:70-73) as fp64-accumulating kernels.
 // The tridiagonal Ritz problem is small and sequential: it is solved on the
 // host by implicit QL, rotating only the last row of the identity for the
-// convergence estimates beta * |y_{m,i}| (eigensolve.cpp:80-94), and fully
+// convergence estimates beta * |y_{m,i}| (eigensolve.cpp:78-94), and fully
 // once the estimates pass, when the Ritz vectors are formed by one GEMM and
 // confirmed against true residuals from a k-direction batched HVP
-// (eigensolve.cpp:96-126).  Start vectors and restarts use the reference's
+// (eigensolve.cpp:95-129).  Start vectors and restarts use the reference's
 // splitmix64 + Box-Muller stream (rng.hpp), so the Krylov sequence starts
 // where the reference's does.
 #pragma once
@@ -25,7 +25,7 @@
 
 namespace ck {
 
-// ---- host: the reference's Rng (rng.hpp:12-33, rng.cpp:8-20 Box-Muller) ---
+// ---- host: the reference's Rng (rng.hpp:10-31, rng.cpp:8-20 Box-Muller) ---
 struct HostRng {
     uint64_t state;
     bool has_spare = false;
@@ -181,7 +181,7 @@ struct LanczosOut {
 };
 
 // Top-k algebraically largest eigenpairs of H (batch-averaged Hessian of the
-// cached dataset) -- eigensolve.cpp:46-160 restated.
+// cached dataset) -- eigensolve.cpp:46-156 restated.
 template <class T>
 LanczosOut lanczos_topk(const ModelDesc& md, const T* params, const Cache<T>& c, int64_t k, int64_t max_iterations,
                         double tol, uint64_t seed, int prec, cudaStream_t s) {
@@ -203,7 +203,7 @@ LanczosOut lanczos_topk(const ModelDesc& md, const T* params, const Cache<T>& c,
     double* sc = dptr<double>(scal);
     const unsigned gb = (unsigned)ceil_div(P, 256);
     HostRng rng{seed};
-    // random_unit_vector (eigensolve.cpp:33-39), then for a restart one
+    // random_unit_vector (eigensolve.cpp:32-38), then for a restart one
     // Gram-Schmidt pass against the basis and the 0.5 norm test (:131-141)
     auto unit_random = [&](T* dst, bool against_basis, int64_t m) -> bool {
         std::vector<double> h(P);
@@ -307,7 +307,7 @@ LanczosOut lanczos_topk(const ModelDesc& md, const T* params, const Cache<T>& c,
                 // Qt[i][r] = sum_c Y[c][i] V[c][r]
                 EpiStore<T> e{dptr<T>(Qt), P, 0, T(1), T(0)};
                 gemm_simt<T>(s, k, P, m, 1, mnmaj(dptr<T>(Yd), k), mnmaj(V, P), e);
-                // normalise away the rounding drift of the basis product (eigensolve.cpp:105-109)
+                // normalise away the rounding drift of the basis product (eigensolve.cpp:107-112)
                 for (int64_t i = 0; i < k; ++i) {
                     T* qi = dptr<T>(Qt) + i * P;
                     lz_dots_kernel<T><<<1, 256, 0, s>>>(qi, P, qi, dptr<double>(nrm) + i);
@@ -345,7 +345,7 @@ LanczosOut lanczos_topk(const ModelDesc& md, const T* params, const Cache<T>& c,
         }
         if (m == max_steps) break;
         if (beta <= 1e-13 * std::max(opnorm, 1.0)) {
-            // invariant subspace: continue in a fresh random direction (eigensolve.cpp:131-143)
+            // invariant subspace: continue in a fresh random direction (eigensolve.cpp:134-143)
             while (!unit_random(V + (j + 1) * P, true, m)) {
             }
             betas.push_back(0.0);

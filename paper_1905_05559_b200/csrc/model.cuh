@@ -2,9 +2,9 @@
 // Pearlmutter R-op (HVP) and the basis-tangent Hessian factorization.
 //
 // Reference behaviour followed:
-//   forward_backward      autodiff.cpp:310-360
-//   per_example_grad_rows autodiff.cpp:384-400
-//   hvp_from_cache        autodiff.cpp:415-501
+//   forward_backward      autodiff.cpp:53-103
+//   per_example_grad_rows autodiff.cpp:127-143
+//   hvp_from_cache        autodiff.cpp:158-244
 //   assemble_hessian      curvature.cpp:33-92 (columns = HVPs on e_p)
 //
 // Layout in HBM (row-major everywhere, n = example index):
@@ -95,7 +95,7 @@ struct EpiForward {
     }
 };
 
-// softmax output + delta = p - y (autodiff.cpp:291-306, 342-350)
+// softmax output + delta = p - y (autodiff.cpp:34-49, 85-90)
 template <class T>
 __global__ void output_layer_kernel(const T* __restrict__ z, int64_t ldz, const int32_t* __restrict__ labels,
                                     int64_t n, int64_t tl, int mode, T* __restrict__ prob, int64_t ldp,
@@ -225,7 +225,7 @@ void forward_backward(const ModelDesc& md, const T* params, const int32_t* label
 }
 
 // ---------------------------------------------------------------------------
-// per-example gradients: J[n][p] (autodiff.cpp:384-400).  Pure HBM write
+// per-example gradients: J[n][p] (autodiff.cpp:127-143).  Pure HBM write
 // stream: every CTA owns one example row and walks it with 16-byte stores.
 // ---------------------------------------------------------------------------
 struct LayerTable {
@@ -374,7 +374,7 @@ __global__ void rop_act_kernel(const T* __restrict__ in, int64_t ldi, const T* _
 }
 
 // rdelta_out = p * (rz - p . rz) for each (profile, example) row; zero in
-// raw_mean_output mode (autodiff.cpp:448-461).
+// raw_mean_output mode (autodiff.cpp:190-205).
 template <class T>
 __global__ void rop_softmax_kernel(const T* __restrict__ rz, int64_t ldr, const T* __restrict__ prob, int64_t ldp,
                                    int64_t n, int64_t rows, int64_t tl, int mode, T* __restrict__ out, int64_t ldo) {

@@ -31,7 +31,7 @@ class Activation(IntEnum):  # model.hpp:11
     relu = 3
 
 
-class OutputMode(IntEnum):  # model.hpp:21
+class OutputMode(IntEnum):  # model.hpp:20
     softmax_cross_entropy = 0
     raw_mean_output = 1
 
@@ -46,7 +46,7 @@ def _enum(e, v):
 
 
 @dataclass
-class ModelSpec:  # model.hpp:27-38
+class ModelSpec:  # model.hpp:27-42
     layer_widths: list
     hidden_activation: Activation = Activation.tanh
     output_mode: OutputMode = OutputMode.softmax_cross_entropy
@@ -82,7 +82,7 @@ class ModelSpec:  # model.hpp:27-38
 
 
 @dataclass
-class Batch:  # model.hpp:49-54
+class Batch:  # model.hpp:58-64
     x: np.ndarray
     y: np.ndarray = None
 
@@ -108,13 +108,13 @@ class HessianResult:  # curvature.hpp:20-23
 
 
 @dataclass
-class GradResult:  # autodiff.hpp:15-18
+class GradResult:  # autodiff.hpp:14-17
     grad_total: np.ndarray
     n: int = 0
 
 
 @dataclass
-class EigenPairs:  # eigensolve.hpp:13-17
+class EigenPairs:  # eigensolve.hpp:14-17
     q: np.ndarray
     lam: np.ndarray = field(default=None)
 
@@ -205,7 +205,7 @@ def _inputs(spec: ModelSpec, params, batch: Batch):
 
 
 def forward(spec: ModelSpec, params, x, precision: str = "f64") -> np.ndarray:
-    """curv::forward (model.hpp:66): the network output (softmax
+    """curv::forward (model.hpp:80): the network output (softmax
     probabilities, or the raw output).  x: one example (T_1,) as in the
     reference, or a batch (n, T_1) -> (n, T_L)."""
     spec.validate()
@@ -224,7 +224,7 @@ def forward(spec: ModelSpec, params, x, precision: str = "f64") -> np.ndarray:
 
 
 def cost(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> float:
-    """curv::cost (model.hpp:70): mean cross-entropy (fused log-softmax) or
+    """curv::cost (model.hpp:84): mean cross-entropy (fused log-softmax) or
     mean raw output over the batch."""
     P, params, x, y, n = _inputs(spec, params, batch)
     out = C.c_double()
@@ -234,7 +234,7 @@ def cost(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> float
 
 
 def assemble_jacobian(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> np.ndarray:
-    """curvature.hpp:32-33: N x P, row n = gradient of C_n."""
+    """curvature.hpp:35-36: N x P, row n = gradient of C_n."""
     P, params, x, y, n = _inputs(spec, params, batch)
     out = np.empty((n, P))
     _lib.check(_lib.load().curvkit_assemble_jacobian(C.byref(spec._c()), _p(params), _p(x), _p(y), n,
@@ -243,7 +243,7 @@ def assemble_jacobian(spec: ModelSpec, params, batch: Batch, precision: str = "f
 
 
 def grad_batch(spec: ModelSpec, params, batch: Batch, precision: str = "f64") -> GradResult:
-    """autodiff.hpp:60: sum of per-example gradients in one batched pass."""
+    """autodiff.hpp:54: sum of per-example gradients in one batched pass."""
     P, params, x, y, n = _inputs(spec, params, batch)
     out = np.empty(P)
     _lib.check(_lib.load().curvkit_grad_batch(C.byref(spec._c()), _p(params), _p(x), _p(y), n,
@@ -252,14 +252,14 @@ def grad_batch(spec: ModelSpec, params, batch: Batch, precision: str = "f64") ->
 
 
 def per_example_grad(spec: ModelSpec, params, x, y=None, precision: str = "f64") -> np.ndarray:
-    """autodiff.hpp:55-56."""
+    """autodiff.hpp:49-50."""
     x = _f64(x).reshape(1, -1)
     y = None if y is None else _f64(y).reshape(1, -1)
     return grad_batch(spec, params, Batch(x, y), precision).grad_total
 
 
 def hvp(spec: ModelSpec, params, batch: Batch, v, precision: str = "f64") -> np.ndarray:
-    """autodiff.hpp:66-67: H_batch v (v may be P or nvec x P)."""
+    """autodiff.hpp:60-65: H_batch v (v may be P or nvec x P)."""
     P, params, x, y, n = _inputs(spec, params, batch)
     v = _f64(v)
     single = v.ndim == 1
@@ -273,7 +273,7 @@ def hvp(spec: ModelSpec, params, batch: Batch, v, precision: str = "f64") -> np.
 
 
 class HvpOperator:
-    """autodiff.hpp:76-89: v -> Hv over a fixed dataset with equal mini-batches."""
+    """autodiff.hpp:70-84: v -> Hv over a fixed dataset with equal mini-batches."""
 
     def __init__(self, spec: ModelSpec, params, data: Batch, batch_size: int, precision: str = "f64"):
         self.spec, self.data, self.batch_size, self.precision = spec, data, int(batch_size), precision
@@ -307,7 +307,7 @@ class HvpOperator:
 
 def assemble_hessian(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfig = None,
                      precision: str = "f64", verify: bool = True) -> HessianResult:
-    """curvature.hpp:27-29.  verify=True assembles each diagonal layer block
+    """curvature.hpp:25-32.  verify=True assembles each diagonal layer block
     from both triangles and reports the pre-symmetrization asymmetry like the
     reference; verify=False fills the lower triangle and mirrors it."""
     config = config or CurvatureConfig(batch_size_h=max(1, Batch(dataset.x).size()))
@@ -322,7 +322,7 @@ def assemble_hessian(spec: ModelSpec, params, dataset: Batch, config: CurvatureC
 
 def assemble_opg(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfig = None,
                  precision: str = "f64") -> np.ndarray:
-    """curvature.hpp:38-40: (1/N) J^T J, symmetric PSD."""
+    """curvature.hpp:37-42: (1/N) J^T J, symmetric PSD."""
     config = config or CurvatureConfig(batch_size_g=max(1, Batch(dataset.x).size()))
     P, params, x, y, n = _inputs(spec, params, dataset)
     g = np.empty((P, P))
@@ -335,7 +335,7 @@ def assemble_opg(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfi
 def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 20, power_iters: int = 2,
              seed: int = 0, precision: str = "f64") -> EigenPairs:
     """Top-k eigenpairs of G = (1/N) J^T J by a randomized range finder
-    (replaces eigensolve.hpp:75-76 opg_eigs_incremental).  Eigenvalues are
+    (replaces eigensolve.hpp:80-81 opg_eigs_incremental).  Eigenvalues are
     descending; columns of q are orthonormal eigenvectors."""
     P, params, x, y, n = _inputs(spec, params, dataset)
     q = np.empty((P, k))
@@ -347,7 +347,7 @@ def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 
 
 
 @dataclass
-class LanczosConfig:  # eigensolve.hpp:25-30
+class LanczosConfig:  # eigensolve.hpp:22-27
     k: int = 1
     max_iterations: int = 0
     residual_tol: float = 1e-6
@@ -355,7 +355,7 @@ class LanczosConfig:  # eigensolve.hpp:25-30
 
 
 @dataclass
-class LanczosResult:  # eigensolve.hpp:32-36
+class LanczosResult:  # eigensolve.hpp:29-33
     pairs: EigenPairs
     residuals: np.ndarray
     iterations: int
@@ -363,7 +363,7 @@ class LanczosResult:  # eigensolve.hpp:32-36
 
 def hessian_lanczos_topk(spec: ModelSpec, params, dataset: Batch, batch_size: int, cfg: LanczosConfig,
                          precision: str = "f64") -> LanczosResult:
-    """curv::lanczos_topk (eigensolve.hpp:44) applied to HvpOperator(spec,
+    """curv::lanczos_topk (eigensolve.hpp:36-45) applied to HvpOperator(spec,
     params, dataset, batch_size): the k algebraically largest eigenpairs of
     the Hessian, full reorthogonalisation, Krylov basis on the device.
     Raises ConvergenceError (best residual estimates attached) when the
@@ -387,8 +387,8 @@ def hessian_lanczos_topk(spec: ModelSpec, params, dataset: Batch, batch_size: in
 def opg_eigs_incremental(j_blocks, n_total: int, k: int, oversample: int = 20, power_iters: int = 2, seed: int = 0,
                          precision: str = "f64") -> EigenPairs:
     """Top-k eigenpairs of G = (1/n) J^T J from the caller's row blocks of J --
-    the input contract of curv::opg_eigs_incremental (eigensolve.hpp:75-76,
-    eigensolve.cpp:375-381) -- by the device randomized range finder."""
+    the input contract of curv::opg_eigs_incremental (eigensolve.hpp:80-81,
+    eigensolve.cpp:245-251) -- by the device randomized range finder."""
     blocks = [np.ascontiguousarray(b, dtype=np.float64) for b in j_blocks]
     if not blocks:
         raise ContractError("opg_eigs_incremental: no row blocks")
@@ -413,10 +413,10 @@ def dev_opg_topk_from_jacobian(J, ldj, n, p, k, oversample, power_iters, seed, q
                                                                _stream(stream)))
 
 
-# ---- low/full-rank operators from eigenpairs (eigensolve.hpp:78-93) ------------
+# ---- low/full-rank operators from eigenpairs (eigensolve.hpp:83-97) ------------
 
 def validate_eigen_pairs(pairs: EigenPairs, ortho_tol: float = 1e-8) -> None:
-    """curv::validate_eigen_pairs (eigensolve.cpp:11-29): lambda length,
+    """curv::validate_eigen_pairs (eigensolve.cpp:11-30): lambda length,
     descending order and column orthonormality within ortho_tol."""
     q = np.asarray(pairs.q, dtype=np.float64)
     lam = np.asarray(pairs.lam, dtype=np.float64)
@@ -431,7 +431,7 @@ def validate_eigen_pairs(pairs: EigenPairs, ortho_tol: float = 1e-8) -> None:
         raise ContractError("EigenPairs: columns are not orthonormal")
 
 
-def _check_dense_cap(p: int, memory_cap: int, who: str):  # eigensolve.cpp:255-260
+def _check_dense_cap(p: int, memory_cap: int, who: str):  # eigensolve.cpp:255-261
     if p > memory_cap:
         raise ContractError(f"{who}: P = {p} exceeds the dense memory cap {memory_cap}; "
                             "use the implicit quadform/apply forms instead")
@@ -463,7 +463,7 @@ def low_rank_apply(pairs: EigenPairs, x) -> np.ndarray:
     return pairs.q @ (pairs.lam * t)
 
 
-def default_lambda_tilde(pairs: EigenPairs) -> float:  # eigensolve.cpp:480-488
+def default_lambda_tilde(pairs: EigenPairs) -> float:  # eigensolve.cpp:350-358
     if len(pairs.lam) == 0:
         raise ContractError("default_lambda_tilde: no eigenvalues")
     lk = float(pairs.lam[-1])

@@ -3,7 +3,7 @@
 The paper and the reference measure no public dataset; BASELINE.json names
 five MLP configurations with synthetic input distributions.  This module
 draws them deterministically from a splitmix64 stream (the reference's own
-generator, /root/reference/proj/include/curv/rng.hpp:15-24), vectorised in
+generator, /root/reference/proj/include/curv/rng.hpp:14-19), vectorised in
 numpy so a 20000 x 1024 draw takes well under a second.
 
 Glorot-uniform weights follow the reference's init_params
@@ -33,12 +33,12 @@ def splitmix64(seed: int, count: int, offset: int = 0) -> np.ndarray:
 
 
 def uniform(seed: int, count: int) -> np.ndarray:
-    """rng.hpp:27 next_uniform(): (u64 >> 11) * 2^-53, in [0, 1)."""
+    """rng.hpp:22 next_uniform(): (u64 >> 11) * 2^-53, in [0, 1)."""
     return (splitmix64(seed, count) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
 
 def normal(seed: int, count: int) -> np.ndarray:
-    """rng.cpp:5-19 Box-Muller: pairs (cos, sin) from (1-u1, u2)."""
+    """rng.cpp:8-20 Box-Muller: pairs (cos, sin) from (1-u1, u2)."""
     npairs = (count + 1) // 2
     u = uniform(seed, 2 * npairs)
     u1 = 1.0 - u[0::2]

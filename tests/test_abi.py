@@ -90,7 +90,7 @@ def test_host_api_contract_errors():
 
 
 def test_low_full_rank_algebra_host():
-    # eigensolve.cpp:425-478 operator algebra on host-side eigenpairs
+    # eigensolve.cpp:295-348 operator algebra on host-side eigenpairs
     rng = np.random.default_rng(106)
     a = rng.normal(size=(30, 30)); a = a + a.T
     w, v = np.linalg.eigh(a)

@@ -34,7 +34,7 @@ def test_lanczos_matches_reference(name):
     k = int(g["k"])
     np.testing.assert_allclose(lam, g["lam"], rtol=1e-9, atol=1e-12)
     assert np.all(np.diff(lam) <= 0)
-    # orthonormal columns (validate_eigen_pairs, eigensolve.cpp:11-29) and the
+    # orthonormal columns (validate_eigen_pairs, eigensolve.cpp:11-30) and the
     # reference's vectors up to sign
     assert np.abs(q.T @ q - np.eye(k)).max() <= 1e-8
     overlap = np.abs(np.sum(q * g["q"], axis=0))
