@@ -179,6 +179,10 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
  * mirrored copies into a full-size output buffer; the shards of
  * curvkit_shard_rows(P, nshards, s, ...) for s = 0..nshards-1 write disjoint
  * entries whose union is the full matrix (rows balanced by triangle area).
+ * In TF32 mode a diagonal layer block is computed per symmetric orbit of four
+ * entries; there a shard takes the share of the block's
+ * orbit tiles that matches its share of the block's lower triangle, so the
+ * shards still write disjoint entries whose union is the block.
  * opg_shard needs row_begin % 4 == 0 (the boundaries of shard_rows are). */
 int curvkit_shard_rows(int64_t p, int64_t nshards, int64_t shard, int64_t* row_begin, int64_t* row_end);
 int curvkit_dev_hessian_shard(const curvkit_model* model, const void* params, const void* x,

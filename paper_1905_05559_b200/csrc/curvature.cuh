@@ -58,6 +58,28 @@ struct HessFused {
     static bool run(int, cudaStream_t, const HessFusedArgs<T>&, const EpiHess<T>&) { return false; }
 };
 
+// Diagonal layer block (k = m) by the symmetric Khatri-Rao product (symkr.cuh):
+// B[(o,i),(o'',c)] = alpha sum_n abar_i abar_c Pi[o][o''] written with its
+// four symmetric images.  TF32 only; returns false where it does not apply.
+template <class T>
+struct SymKrArgs {
+    const T* akT;        // abar_k^T [T_k + 1][ldn] (row T_k = ones)
+    const T* prof;       // H: profiles [U][U][ldn]; G: delta_k^T [U][ldn]
+    int delta_products;  // 1: Pi[o][o''] = delta_o * delta_o'' (OPG)
+    int64_t ldn, n, tk, U;
+    T* H;
+    int64_t ldh, woff, boff;
+    T alpha;
+    // row shard: the block's orbit tiles [floor(f0 T), floor(f1 T)) of T, f = the
+    // shard's share of the block's lower triangle (shards partition the orbits)
+    double f0 = 0.0, f1 = 1.0;
+};
+
+template <class T>
+struct SymKr {
+    static bool run(int, cudaStream_t, const SymKrArgs<T>&) { return false; }
+};
+
 // out[r][.] = in[r mod period][.]  (row replication for the extended tiles)
 template <class T>
 __global__ void replicate_rows_kernel(const T* __restrict__ in, int64_t period, int64_t ld, T* __restrict__ out,
@@ -225,6 +247,11 @@ struct Engine {
     //   Pm [T_{k+1}][n][ldt_m]       rdelta_m, m < k, same tangents
     //   Qm [T_k][n][ldt_m]           rdelta_m from the explicit delta*RW term
     size_t chunk_bytes = size_t(256) << 20;  // R operand chunk (streamed once from HBM)
+    // dev control: CURVKIT_NO_SYMKR=1 keeps diagonal blocks on the lower-triangle kernels
+    static bool sym_off() {
+        static const bool off = getenv("CURVKIT_NO_SYMKR") != nullptr;
+        return off;
+    }
 
     // Output entries of one (k, m, chunk) block that the assembly needs: all
     // of an off-diagonal block, the lower triangle (gc <= gr) of a diagonal one.
@@ -373,7 +400,21 @@ struct Engine {
                 // weight tangents through the fused kernel where it exists; the
                 // chunked R path below then only covers the bias tangents
                 int64_t jbeg = 0;
-                if (fused) {
+                if (fused && m == k && !verify && !sym_off()) {
+                    // diagonal block: one value per symmetric orbit (a row shard takes
+                    // its share of the block's lower triangle as a range of orbit tiles)
+                    auto tri = [&](int64_t r) {
+                        const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
+                        return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
+                    };
+                    const double f0 = tri(rlo), f1 = rhi >= md.woff[k] + Pk ? 1.0 : tri(rhi);
+                    const double orbits = (double)np * (np + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
+                    ProfScope ps("hess_symkr", s, 2.0 * (double)n * orbits * (f1 - f0),
+                                 (double)sizeof(T) * (double)Pk * Pk * (f1 - f0));
+                    SymKrArgs<T> sa{akT, GT, 0, ldn, n, tk, np, H, ldh, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
+                    if (SymKr<T>::run(prec, s, sa)) jbeg = Pk;
+                }
+                if (fused && jbeg < Pk) {
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                     HessFusedArgs<T> fa{akX, ak_rows, m == k ? nullptr : QX[m], ak_rows, tm1 * ak_rows,
                                         m == k ? GT : PT[m], dkT, c.a[m], c.lda[m], ldn, n, tk, tm, tm1, nw,

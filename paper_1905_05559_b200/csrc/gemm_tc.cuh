@@ -795,6 +795,8 @@ struct FusedHess {
     int pv_tma;         // profile / delta rows of a CTA's weight rows staged by TMA (else __ldg)
     long long* trace = nullptr;  // dev: pipeline event stamps (8 x 1024) of CTA 0
     int tma_h = 0;               // interior 32 x 32 blocks stored by TMA (mapH)
+    int dev = 0;                 // dev experiments (CURVKIT_DEV_FUSED): 1 no transform math, 2 no epilogue stores,
+                                 // 4 mirror boxes by TMA (else coalesced register stores)
     // first output unit o whose profile row the producer stages for a CTA
     // whose first tangent row is jr (rows jr .. jr + 127 use units o_first ..)
     __host__ __device__ int64_t o_first(int64_t jr) const {
@@ -1047,6 +1049,11 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                     }
                 }
                 if (trw && g < TRN) trace[1 * TRN + g] = clock64();
+                if (fh.dev & 1) {  // dev: pipeline without the transform's shared-memory work
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(fb0 + st_ * 8);
+                    continue;
+                }
                 uint8_t* st = stage_base + st_ * STAGE_BYTES;
                 uint8_t* sa = st + row * 128;
                 const int64_t n0k = kb * BK;
@@ -1133,7 +1140,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 if (col0 >= sh.N) break;
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
-                if (row0 < band_end) {
+                if (row0 < band_end && !(fh.dev & 2)) {
                     int64_t gr0, gc0;
                     // the slot is free once the previous box's TMA store has read it
                     if (lane == 0) bulk_wait_read();
@@ -1146,8 +1153,6 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                         *reinterpret_cast<float4*>(box + lane * 32 + ((q ^ (lane & 7)) << 2)) =
                             make_float4(sc * v[4 * q], sc * v[4 * q + 1], sc * v[4 * q + 2], sc * v[4 * q + 3]);
                     if (via_tma) {
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) v[c] *= epi.alpha;
                         fence_proxy_async();
                         __syncwarp();
                         if (lane == 0) {
@@ -1155,17 +1160,25 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                             bulk_commit();
                         }
                         if (epi.mirror) {
-                            if (lane == 0) bulk_wait_read();
-                            __syncwarp();
-                            // transposed box: row c holds this block's column c, element lane
+                            if (fh.dev & 4) {
+                                if (lane == 0) bulk_wait_read();
+                                __syncwarp();
+                                // transposed box: row c holds this block's column c, element lane
 #pragma unroll
-                            for (int c = 0; c < 32; ++c)
-                                box[c * 32 + ((((lane >> 2) ^ (c & 7)) << 2) | (lane & 3))] = v[c];
-                            fence_proxy_async();
-                            __syncwarp();
-                            if (lane == 0) {
-                                tma_store_2d(&mapH, box, (int32_t)gr0, (int32_t)gc0);
-                                bulk_commit();
+                                for (int c = 0; c < 32; ++c)
+                                    box[c * 32 + ((((lane >> 2) ^ (c & 7)) << 2) | (lane & 3))] = sc * v[c];
+                                fence_proxy_async();
+                                __syncwarp();
+                                if (lane == 0) {
+                                    tma_store_2d(&mapH, box, (int32_t)gr0, (int32_t)gc0);
+                                    bulk_commit();
+                                }
+                            } else {
+                                // mirrored block: H row gc0 + c gets this block's column c; the
+                                // 32 lanes write 128 contiguous bytes per row (no shared memory)
+                                float* mcol = epi.H + gc0 * epi.ldh + gr0 + lane;
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) __stcs(mcol + c * epi.ldh, sc * v[c]);
                             }
                         }
                     } else {
@@ -1574,7 +1587,8 @@ struct HessFused<float> {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(S::bytes(0), S::bytes(1))));
             attr = true;
         }
-        const int grid = 2 * (int)std::min<int64_t>(fh.ntiles, tc::num_sms() / 2);
+        int grid = 2 * (int)std::min<int64_t>(fh.ntiles, tc::num_sms() / 2);
+        if (const char* g = getenv("CURVKIT_DEV_GRID")) grid = std::min(grid, 2 * (atoi(g) / 2));  // dev: fewer SMs
         static const bool tracing = getenv("CURVKIT_TRACE") != nullptr;
         DevMem trbuf;
         if (tracing) {
@@ -1584,6 +1598,8 @@ struct HessFused<float> {
         }
         // H as a 2D map of 32 x 32 boxes (128-byte swizzle) for the epilogue
         fh.tma_h = (e.ldh % 4 == 0 && (reinterpret_cast<uintptr_t>(e.H) & 15) == 0) ? 1 : 0;
+        static const int dev = getenv("CURVKIT_DEV_FUSED") ? atoi(getenv("CURVKIT_DEV_FUSED")) : 0;
+        fh.dev = dev;
         CUtensorMap mh = fh.tma_h ? tc::make_map_h(e.H, e.ldh) : mb;
         pair::tc_hess_fused_kernel<BN, EpiHess<float>, TS><<<grid, pair::kFusedThreads, S::bytes(fh.hasq), s>>>(
             mak, mq, mb, mpv, mdt, mh, fh, sh, e);
@@ -1615,3 +1631,5 @@ struct CurvGemm<float, Epi> {
 };
 
 }  // namespace ck
+
+#include "symkr.cuh"

@@ -1,0 +1,471 @@
+// symkr.cuh -- diagonal curvature blocks by the symmetric Khatri-Rao product.
+//
+// A diagonal layer block (tangent step k = m) of H, and of G = (1/N) J^T J, is
+//
+//   B[(o, i), (o'', c)] = alpha * sum_n abar[n, i] abar[n, c] Pi[o][o''][n]
+//
+// with abar = a_k plus its ones column (index T_k stands for the bias of unit
+// o, row boff_k + o of H), Pi[o][o''] = the R-op profile G_k[o][o''] for H
+// (curvature.cpp:43-72 restated per DESIGN.md section 2) and delta_k[., o] *
+// delta_k[., o''] for G (the per-example gradient rows of
+// autodiff.cpp:127-143 are delta (x) abar).  Pi is symmetric in (o, o''), and
+// abar_i abar_c is symmetric in (i, c), so every value sits on an orbit of
+// four entries:
+//
+//   (o, i; o'', c)   (o'', c; o, i)   (o, c; o'', i)   (o'', i; o, c)
+//
+// The kernel computes one representative per orbit (i <= c in 16 x 16 blocks,
+// o <= o'' as packed columns) as a tensor-core GEMM
+//
+//   V[(i, c), j] = sum_n Z[(i, c), n] Pi_packed[j][n],   Z = abar_i * abar_c,
+//
+// i.e. half the multiply-adds of the lower-triangle GEMM, and writes each
+// value to its four places.  Z is formed in shared memory by four transform
+// warps from TMA-staged activation rows (8 + 16 rows per K-block instead of a
+// 128-row tile); Pi_packed is the TMA-loaded B operand.  CTA pair (cta_group::2,
+// M = 256 = 16 i x 16 c), N = up to 256 packed columns, TMEM double buffer.
+// The epilogue stages each 8-column chunk in two layouts and stores 4-D TMA
+// boxes (16 c x 8 i x E o'' or 8 i x 16 c x E o'') into H; the TMA clips
+// everything at index T_k, and the bias entries (index T_k) are written by
+// the lanes that hold them.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gemm_tc.cuh"
+
+namespace ck {
+namespace tc {
+namespace sym {
+using namespace ::ck::tc::pair;
+
+constexpr int EPI_W = 8, TW_W = 4, TW_SETS = 2;  // TW_SETS sets of 4 transform warps take alternate K-blocks
+constexpr int kThreads = 128 + 32 * EPI_W + 32 * TW_W * TW_SETS;
+constexpr int TW0 = 4 + EPI_W;
+constexpr int Z_BYTES = 128 * BK * 4;   // A operand (Z), 128 rows x 32 examples
+constexpr int B_BYTES = 128 * BK * 4;   // up to 128 packed profile rows per CTA
+constexpr int I_BYTES = 8 * BK * 4;     // abar^T rows of the CTA's 8 i
+constexpr int C_BYTES = 16 * BK * 4;    // abar^T rows of the 16 c
+constexpr int STAGE = Z_BYTES + B_BYTES + I_BYTES + C_BYTES;
+constexpr int CH = 8;                   // epilogue chunk (packed columns)
+constexpr int SLOT = CH * 128 * 4;      // one staging layout of one chunk
+constexpr int EPI_BYTES = 2 * 2 * 2 * SLOT;  // group x double buffer x layout
+constexpr int EPI_PAD = 4 * 1024;       // boxes of extent 8 may read past a slot
+constexpr int MAX_SMEM = 227 * 1024;
+constexpr int NST = std::min(8, (MAX_SMEM - 1024 - EPI_BYTES - EPI_PAD - 1024) / STAGE);
+constexpr int SMEM_BYTES = 1024 + NST * STAGE + EPI_BYTES + EPI_PAD + 1024;
+
+struct Params {
+    const int4* tiles;   // (ib, cb, nt, -): 16-blocks ib <= cb of abar indices, packed column tile nt
+    int64_t ntiles;
+    const int4* pairs;   // (o, o'', box kind, -) of packed column j
+    int64_t npairs, bn;  // packed columns, MMA N (multiple of 16, <= 256)
+    int64_t tk, nk;      // T_k (abar has T_k + 1 rows), K-blocks of 32 examples
+    int64_t U;           // T_{k+1}
+    float* H;
+    int64_t ldh, woff, boff;
+    float alpha;
+    int tma;             // H boxes by TMA (else every entry by the scalar path)
+    int dev;             // dev experiments (CURVKIT_DEV_SYMKR): 1 no transform, 2 no epilogue stores
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1, int32_t c2,
+                                             int32_t c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// H row / column of (unit o, abar index x): weight (o, x) or the bias of o
+__device__ __forceinline__ int64_t hidx(const Params& p, int64_t o, int64_t x) {
+    return x < p.tk ? p.woff + o * p.tk + x : p.boff + o;
+}
+
+// H maps: [0..3] = orbit types 1..4 with o''-extent 8, [4..7] with extent 1
+struct HMaps {
+    CUtensorMap m[8];
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant__ CUtensorMap mapAbar16,
+             const __grid_constant__ CUtensorMap mapPi, const __grid_constant__ HMaps hm, Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    constexpr int Z_OFF = 0, B_OFF = Z_BYTES, I_OFF = B_OFF + B_BYTES, C_OFF = I_OFF + I_BYTES;
+    uint8_t* epi_base = smem + NST * STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + EPI_BYTES + EPI_PAD);
+    uint64_t* full = bars;         // [8] leader: producer + 2 x 4 transform warps, B tx
+    uint64_t* empty = bars + 8;    // [8] both CTAs (multicast commit)
+    uint64_t* afull = bars + 16;   // [8] local: abar rows landed
+    uint64_t* tfull = bars + 24;   // [2]
+    uint64_t* tempty = bars + 26;  // [2] leader
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cta_rank();
+    const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
+    const int bn = (int)p.bn;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_map(&mapAbar8);
+        prefetch_map(&mapAbar16);
+        prefetch_map(&mapPi);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1 + 2 * TW_W);
+            mbar_init(&empty[s], 1);
+            mbar_init(&afull[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * EPI_W);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- producer
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint64_t pol = evict_last_policy();
+            for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
+                const int4 tl = __ldg(&p.tiles[t]);
+                const int32_t i0 = tl.x * 16 + 8 * (int)rank, c0 = tl.y * 16;
+                const int32_t b0 = (int32_t)(tl.z * p.bn + (p.bn / 2) * rank);
+                for (int64_t kb = 0; kb < p.nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* st = smem + stage * STAGE;
+                    const int32_t k0 = (int32_t)(kb * BK);
+                    mbar_expect_tx(&afull[stage], (uint32_t)(I_BYTES + C_BYTES));
+                    tma_load_2d(st + I_OFF, &mapAbar8, &afull[stage], k0, i0);
+                    tma_load_2d(st + C_OFF, &mapAbar16, &afull[stage], k0, c0);
+                    const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
+                    if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * (p.bn / 2) * BK * 4));
+                    tma2_2d(st + B_OFF, &mapPi, fb, k0, b0, pol);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            const uint32_t idesc = idesc2_tf32(bn, false, false);
+            for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+                for (int64_t kb = 0; kb < p.nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sz = smem_u32(smem + stage * STAGE + Z_OFF);
+                    const uint32_t sb = sz + B_OFF;
+#pragma unroll
+                    for (int ks = 0; ks < BK / 8; ++ks)
+                        mma2_tf32(d, smem_desc(sz + ks * 32, 16, 1024, 2), smem_desc(sb + ks * 32, 16, 1024, 2), idesc,
+                                  (kb > 0 || ks > 0) ? 1u : 0u);
+                    commit2(&empty[stage]);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+                commit2(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= TW0) {  // ---------------- Z transform (both CTAs)
+        const int set = (warp - TW0) / TW_W;
+        const int rho = ((warp - TW0) % TW_W) * 32 + lane;  // tile row: i = rho / 16, c = rho % 16
+        const int il = rho >> 4, cl = rho & 15;
+        const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
+        int stage = 0, sidx = 0;
+        uint32_t phase = 0;
+        for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
+            for (int64_t kb = 0; kb < p.nk; ++kb) {
+                const int st_ = stage;
+                const uint32_t ph_ = phase;
+                if (++stage == NST) { stage = 0; phase ^= 1; }
+                const bool mine = sidx == set;
+                if (++sidx == TW_SETS) sidx = 0;
+                // every set waits on every stage in order: a set that skipped stages
+                // could otherwise see a completed phase of the same parity one lap early
+                mbar_wait(&afull[st_], ph_);
+                if (!mine) continue;
+                uint8_t* st = smem + st_ * STAGE;
+                if (!(p.dev & 1)) {
+                    const uint8_t* ri = st + I_OFF + il * 128;
+                    const uint8_t* rc = st + C_OFF + cl * 128;
+                    uint8_t* rz = st + Z_OFF + rho * 128;
+                    float4 x[8], y[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        x[q] = *reinterpret_cast<const float4*>(ri + ((q ^ (il & 7)) << 4));
+                        y[q] = *reinterpret_cast<const float4*>(rc + ((q ^ (cl & 7)) << 4));
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<float4*>(rz + ((q ^ (rho & 7)) << 4)) =
+                            make_float4(round_tf32(x[q].x * y[q].x), round_tf32(x[q].y * y[q].y),
+                                        round_tf32(x[q].z * y[q].z), round_tf32(x[q].w * y[q].w));
+                    fence_proxy_async();
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(fb0 + st_ * 8);
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, 2 groups of 4 warps)
+        const int ew = warp - 4;
+        const int quad = warp % 4;   // TMEM lanes 32 quad .. + 31
+        const int grp = ew / 4;      // column half of the tile
+        const int rho = quad * 32 + lane;
+        const int il = rho >> 4, cl = rho & 15;
+        uint8_t* gbase = epi_base + grp * 4 * SLOT;  // [buf][layout][CH][128] floats
+        const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
+        const int half = bn / 2;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int chunk = 0;
+        for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
+            const int4 tl = __ldg(&p.tiles[t]);
+            const int64_t i0 = tl.x * 16 + 8 * (int)rank, c0 = tl.y * 16;
+            const int64_t ii = i0 + il, cc = c0 + cl;  // this lane's abar indices
+            const bool box_ok = p.tma && i0 < p.tk && c0 < p.tk && !(p.dev & 2);
+            // lanes holding a bias entry (index T_k) or, without TMA, any valid entry
+            const bool scalar = (ii <= p.tk && cc <= p.tk) && (ii == p.tk || cc == p.tk || !p.tma) && !(p.dev & 2);
+            const int64_t jt0 = (int64_t)tl.z * p.bn;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            for (int jj0 = grp * half; jj0 < (grp + 1) * half; jj0 += CH) {
+                const int64_t J0 = jt0 + jj0;
+                if (J0 >= p.npairs) break;  // uniform across the group
+                float v[CH];
+                tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + jj0), v);
+#pragma unroll
+                for (int e = 0; e < CH; ++e) v[e] *= p.alpha;
+                const int ncol = (int)(p.npairs - J0 < CH ? p.npairs - J0 : CH);
+                if (box_ok) {
+                    float* sA = reinterpret_cast<float*>(gbase + (chunk & 1) * 2 * SLOT);
+                    float* sB = sA + SLOT / 4;
+                    // lanes 0..7 of every warp issue boxes (warp quad = orbit type); each
+                    // waits for its own stores of two chunks ago before the buffer is reused
+                    if (lane < CH) bulk_wait_read1();
+                    named_sync(1 + grp, 128);
+#pragma unroll
+                    for (int e = 0; e < CH; ++e) {
+                        sA[e * 128 + rho] = v[e];            // [o''][i][c]
+                        sB[e * 128 + cl * 8 + il] = v[e];    // [o''][c][i]
+                    }
+                    fence_proxy_async();
+                    named_sync(1 + grp, 128);
+                    if (lane < ncol) {
+                        // kind 1: extent-8 box from this column (the run fills the chunk or
+                        // ends at U, where the TMA clips), 2: extent-1 box, 0: inside a box
+                        const int4 bx = __ldg(&p.pairs[J0 + lane]);
+                        if (bx.z) {
+                            const CUtensorMap* mp = &hm.m[(bx.z == 1 ? 0 : 4) + quad];
+                            const bool ic = quad == 0 || quad == 3;  // types 1, 4: [o''][i][c]
+                            const float* src = (ic ? sA : sB) + lane * 128;
+                            if (ic) tma_store_4d(mp, src, (int32_t)c0, (int32_t)i0, bx.y, bx.x);
+                            else tma_store_4d(mp, src, (int32_t)i0, (int32_t)c0, bx.y, bx.x);
+                        }
+                    }
+                    if (lane < CH) bulk_commit();  // one group per chunk and lane (wait_group.read 1 above)
+                    ++chunk;
+                }
+                if (scalar) {
+#pragma unroll
+                    for (int e = 0; e < CH; ++e) {
+                        if (e >= ncol) break;
+                        const int4 pr = __ldg(&p.pairs[J0 + e]);
+                        const int64_t r1 = hidx(p, pr.x, ii), c1 = hidx(p, pr.y, cc);
+                        const int64_t r3 = hidx(p, pr.x, cc), c3 = hidx(p, pr.y, ii);
+                        p.H[r1 * p.ldh + c1] = v[e];
+                        p.H[c1 * p.ldh + r1] = v[e];
+                        p.H[r3 * p.ldh + c3] = v[e];
+                        p.H[c3 * p.ldh + r3] = v[e];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (lane < CH) bulk_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
+}  // namespace sym
+
+// 4-D map of one orbit type over the diagonal block at H + woff * (ldh + 1):
+// dims (d0, d1, U, U) with element strides (1, s1, s2, s3), box (b0, b1, E, 1)
+inline CUtensorMap make_map_orbit(float* H, int64_t ldh, int64_t woff, int64_t d0, int64_t d1, int64_t U, int64_t s1,
+                                  int64_t s2, int64_t s3, int b0, int b1, int E) {
+    CUtensorMap m;
+    float* base = H + woff * ldh + woff;
+    cuuint64_t dims[4] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)U, (cuuint64_t)U};
+    cuuint64_t str[3] = {(cuuint64_t)s1 * 4, (cuuint64_t)s2 * 4, (cuuint64_t)s3 * 4};
+    cuuint32_t box[4] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)E, 1}, es[4] = {1, 1, 1, 1};
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (str[0] & 15) || (str[1] & 15) || (str[2] & 15))
+        throw CurvError(kCudaError, "orbit map: 16-byte alignment");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, str, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (orbit) failed: " + std::to_string((int)r));
+    return m;
+}
+
+// out[j][.] = tf32(src[(o_j * U + o''_j)][.])  -- packed profile rows
+__global__ void pack_profile_kernel(const float* __restrict__ src, const int4* __restrict__ pairs, int64_t U,
+                                    int64_t ldn, float* __restrict__ out, int64_t npairs) {
+    const int64_t j = blockIdx.y;
+    const int4 pr = pairs[j];
+    const float4* s = reinterpret_cast<const float4*>(src + (pr.x * U + pr.y) * ldn);
+    float4* d = reinterpret_cast<float4*>(out + j * ldn);
+    for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
+        float4 v = s[q];
+        v.x = round_tf32(v.x); v.y = round_tf32(v.y); v.z = round_tf32(v.z); v.w = round_tf32(v.w);
+        d[q] = v;
+    }
+}
+
+// out[j][n] = tf32(dT[o_j][n] * dT[o''_j][n])  -- OPG profiles delta_o delta_o''
+__global__ void pack_delta_products_kernel(const float* __restrict__ dT, const int4* __restrict__ pairs, int64_t ldn,
+                                           float* __restrict__ out, int64_t npairs) {
+    const int64_t j = blockIdx.y;
+    const int4 pr = pairs[j];
+    const float4* a = reinterpret_cast<const float4*>(dT + pr.x * ldn);
+    const float4* b = reinterpret_cast<const float4*>(dT + pr.y * ldn);
+    float4* d = reinterpret_cast<float4*>(out + j * ldn);
+    for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
+        const float4 x = a[q], y = b[q];
+        d[q] = make_float4(round_tf32(x.x * y.x), round_tf32(x.y * y.y), round_tf32(x.z * y.z), round_tf32(x.w * y.w));
+    }
+}
+
+}  // namespace tc
+
+template <>
+struct SymKr<float> {
+    // Applicability of the TMA orbit epilogue (else the scalar path writes all
+    // entries; the caller prefers the fused kernel then).
+    static bool tma_ok(const float* H, int64_t ldh, int64_t woff, int64_t tk) {
+        return ldh % 4 == 0 && woff % 4 == 0 && tk % 4 == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0;
+    }
+
+    static bool run(int prec, cudaStream_t s, const SymKrArgs<float>& a) {
+        if (prec != kTF32) return false;
+        if (!tma_ok(a.H, a.ldh, a.woff, a.tk)) return false;
+        namespace sym = tc::sym;
+        const int64_t U = a.U, tk = a.tk;
+        const int64_t np = U * (U + 1) / 2;
+        // packed columns (o <= o''), o-major
+        std::vector<int4> pairs;
+        pairs.reserve(np);
+        for (int64_t o = 0; o < U; ++o)
+            for (int64_t q = o; q < U; ++q) pairs.push_back(make_int4((int)o, (int)q, 0, 0));
+        // TMA box decomposition per 8-column chunk (chunks start at multiples of 8:
+        // tile widths are multiples of 16): runs of one o with consecutive o''
+        for (int64_t j0 = 0; j0 < np; j0 += sym::CH) {
+            const int64_t j1 = std::min<int64_t>(np, j0 + sym::CH);
+            for (int64_t e = j0; e < j1;) {
+                int64_t L = 1;
+                while (e + L < j1 && pairs[e + L].x == pairs[e].x) ++L;
+                const bool wide = L == sym::CH || pairs[e].y + L == U;
+                if (wide) pairs[e].z = 1;
+                else
+                    for (int64_t u = 0; u < L; ++u) pairs[e + u].z = 2;
+                e += L;
+            }
+        }
+        const int64_t ntn = ceil_div(np, 256);
+        const int64_t bn = round_up(ceil_div(np, ntn), 16);
+        const int64_t nb = ceil_div(tk + 1, 16);  // 16-blocks of abar indices
+        std::vector<int4> tiles;
+        for (int64_t ib = 0; ib < nb; ++ib)
+            for (int64_t cb = ib; cb < nb; ++cb)
+                for (int64_t nt = 0; nt < ntn; ++nt) tiles.push_back(make_int4((int)ib, (int)cb, (int)nt, 0));
+        {  // row shard: a contiguous range of the (equal-work) orbit tiles
+            const int64_t T = (int64_t)tiles.size();
+            const int64_t t0 = std::clamp<int64_t>((int64_t)std::floor(a.f0 * (double)T), 0, T);
+            const int64_t t1 = a.f1 >= 1.0 ? T : std::clamp<int64_t>((int64_t)std::floor(a.f1 * (double)T), t0, T);
+            tiles = std::vector<int4>(tiles.begin() + t0, tiles.begin() + t1);
+            if (tiles.empty()) return true;
+        }
+        DevMem dpairs(pairs.size() * sizeof(int4), s), dtiles(tiles.size() * sizeof(int4), s);
+        CK_CUDA(cudaMemcpyAsync(dpairs.p, pairs.data(), pairs.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+        CK_CUDA(cudaMemcpyAsync(dtiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+        // packed profiles (B operand, K-major rows of ldn examples), rounded to nearest TF32
+        DevMem pi((size_t)np * a.ldn * 4, s);
+        if (a.delta_products)
+            tc::pack_delta_products_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)np), 256, 0, s>>>(
+                a.prof, dptr<int4>(dpairs), a.ldn, dptr<float>(pi), np);
+        else
+            tc::pack_profile_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)np), 256, 0, s>>>(
+                a.prof, dptr<int4>(dpairs), U, a.ldn, dptr<float>(pi), np);
+        CK_LAUNCH();
+        CUtensorMap m8 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 8);
+        CUtensorMap m16 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 16);
+        CUtensorMap mpi = tc::make_map(dptr<float>(pi), np, a.n, a.ldn, 0, (int)(bn / 2));
+        tc::sym::HMaps hm;
+        const int64_t L = a.ldh;
+        for (int x = 0; x < 2; ++x) {
+            const int E = x == 0 ? 8 : 1;
+            // type 1: H[(o,i),(o'',c)]  d = (c, i, o'', o), strides (1, L, tk, tk L)
+            hm.m[4 * x + 0] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk, tk * L, 16, 8, E);
+            // type 2: H[(o'',c),(o,i)]  d = (i, c, o'', o), strides (1, L, tk L, tk)
+            hm.m[4 * x + 1] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk * L, tk, 8, 16, E);
+            // type 3: H[(o,c),(o'',i)]  d = (i, c, o'', o), strides (1, L, tk, tk L)
+            hm.m[4 * x + 2] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk, tk * L, 8, 16, E);
+            // type 4: H[(o'',i),(o,c)]  d = (c, i, o'', o), strides (1, L, tk L, tk)
+            hm.m[4 * x + 3] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk * L, tk, 16, 8, E);
+        }
+        sym::Params prm{dptr<int4>(dtiles), (int64_t)tiles.size(), dptr<int4>(dpairs), np, bn, tk,
+                        ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, 1, 0};
+        static const int dev = getenv("CURVKIT_DEV_SYMKR") ? atoi(getenv("CURVKIT_DEV_SYMKR")) : 0;
+        prm.dev = dev;
+        static bool attr = false;
+        if (!attr) {
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sym::SMEM_BYTES));
+            attr = true;
+        }
+        const int grid = 2 * (int)std::min<int64_t>((int64_t)tiles.size(), tc::num_sms() / 2);
+        sym::symkr_kernel<<<grid, sym::kThreads, sym::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        CK_LAUNCH();
+        return true;
+    }
+};
+
+}  // namespace ck
