@@ -293,6 +293,19 @@ void jacobian_full(const ModelDesc& md, const Cache<T>& c, DevMem& J, int64_t& l
     jacobian<T>(md, c, 0, c.n, dptr<T>(J), ldj, s, rn);
 }
 
+// G (rows [rb, re) of the lower triangle and their mirrors): the J-free
+// Khatri-Rao route in TF32 mode, else per-example gradients J and the SYRK
+template <class T>
+void opg_into(const ModelDesc& md, const Cache<T>& c, T* G, int64_t ldg, int prec, cudaStream_t s, int64_t rb = 0,
+              int64_t re = -1) {
+    Engine<T> eng{md, s, prec};
+    if (eng.opg_kr(c, G, ldg, rb, re < 0 ? INT64_MAX : re)) return;
+    DevMem J;
+    int64_t ldj;
+    jacobian_full<T>(md, c, J, ldj, s, prec == kTF32);
+    eng.opg(dptr<T>(J), ldj, c.n, G, ldg, rb, re);
+}
+
 template <class T, class U>
 void host_opg(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n,
               const curvkit_curvature_config* cfg, int prec, U* g_out) {
@@ -303,13 +316,9 @@ void host_opg(const ModelDesc& md, const double* params, const double* x, const 
     cudaStream_t s = lib_stream();
     Resident<T> r;
     upload_and_forward<T>(md, params, x, lab, n, r, s);
-    DevMem J;
-    int64_t ldj;
-    jacobian_full<T>(md, r.cache, J, ldj, s, prec == kTF32);
     const int64_t ldg = round_up(md.P, 4);
     DevMem G((size_t)md.P * ldg * sizeof(T), s);
-    Engine<T> eng{md, s, prec};
-    eng.opg(dptr<T>(J), ldj, n, dptr<T>(G), ldg);
+    opg_into<T>(md, r.cache, dptr<T>(G), ldg, prec, s);
     download<T, U>(dptr<T>(G), ldg, md.P, md.P, g_out, s);
 }
 
@@ -671,11 +680,7 @@ int curvkit_dev_assemble_opg(const curvkit_model* model, const void* params, con
             using T = decltype(tag);
             Cache<T> c;
             forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
-            DevMem J;
-            int64_t ldj;
-            jacobian_full<T>(md, c, J, ldj, s, precision == kTF32);
-            Engine<T> eng{md, s, precision};
-            eng.opg(dptr<T>(J), ldj, n, (T*)g, ldg);
+            opg_into<T>(md, c, (T*)g, ldg, precision, s);
         };
         if (is_f64(precision)) run(double{});
         else run(float{});
@@ -750,11 +755,7 @@ int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const 
             using T = decltype(tag);
             Cache<T> c;
             forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
-            DevMem J;
-            int64_t ldj;
-            jacobian_full<T>(md, c, J, ldj, s, precision == kTF32);
-            Engine<T> eng{md, s, precision};
-            eng.opg(dptr<T>(J), ldj, n, (T*)g, ldg, row_begin, row_end);
+            opg_into<T>(md, c, (T*)g, ldg, precision, s, row_begin, row_end);
         };
         if (is_f64(precision)) run(double{});
         else run(float{});

@@ -77,8 +77,18 @@ struct SymKrArgs {
 
 template <class T>
 struct SymKr {
+    static bool tma_ok(const T*, int64_t, int64_t, int64_t) { return false; }
     static bool run(int, cudaStream_t, const SymKrArgs<T>&) { return false; }
 };
+
+// PV[o][o''][n] = dk[o][n] * dm[o''][n]  (OPG profile of block (k, m))
+template <class T>
+__global__ void outer_delta_kernel(const T* __restrict__ dk, const T* __restrict__ dm, int64_t um, int64_t ldn,
+                                   T* __restrict__ pv) {
+    const int64_t o = blockIdx.z, oo = blockIdx.y;
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < ldn; n += (int64_t)gridDim.x * blockDim.x)
+        pv[(o * um + oo) * ldn + n] = dk[o * ldn + n] * dm[oo * ldn + n];
+}
 
 // out[r][.] = in[r mod period][.]  (row replication for the extended tiles)
 template <class T>
@@ -239,6 +249,70 @@ struct Engine {
         ProfScope ps("opg_gemm", s, 2.0 * entries * (double)n,
                      (double)sizeof(T) * ((double)n * re + 2.0 * entries));
         CurvGemm<T, EpiSymLower<T>>::run(prec, s, re - rb, re, n, pre_rounded(mnmaj(J + rb, ldj)), pre_rounded(mnmaj(J, ldj)), e);
+    }
+
+    // OPG without J (TF32): G[(k,o,i),(m,o'',c)] = (1/N) sum_n abar_k,i abar_m,c
+    // delta_k,o delta_m,o'' -- the per-example gradient rows are delta (x) abar
+    // (autodiff.cpp:127-143).  Diagonal blocks by the symmetric Khatri-Rao
+    // kernel (one value per orbit), blocks m < k by the fused block kernel with
+    // the profile delta_k,o delta_m,o'' and no Q term.  Same row-shard contract
+    // as opg(); returns false where the route does not apply (then J + SYRK).
+    bool opg_kr(const Cache<T>& c, T* G, int64_t ldg, int64_t rlo = 0, int64_t rhi = INT64_MAX) {
+        if (!(prec == kTF32 && sizeof(T) == 4) || sym_off()) return false;
+        const int S = md.S;
+        const int64_t n = c.n, ldn = round_up(n, 32);
+        std::vector<DevMem> keep;
+        auto buf = [&](int64_t rows, int64_t ld) {
+            keep.emplace_back((size_t)rows * ld * sizeof(T), s);
+            CK_CUDA(cudaMemsetAsync(keep.back().p, 0, (size_t)rows * ld * sizeof(T), s));
+            return dptr<T>(keep.back());
+        };
+        T* akT[kMaxLayers] = {};
+        T* dT[kMaxLayers] = {};
+        {
+            ProfScope prep("opg_prep", s, 0.0, 0.0);
+            for (int k = 0; k < S; ++k) {
+                akT[k] = buf(md.w[k] + 1, ldn);
+                transpose<T>(s, c.a[k], c.lda[k], 0, akT[k], ldn, 0, n, md.w[k] + 1, 1);
+                dT[k] = buf(md.w[k + 1], ldn);
+                transpose<T>(s, c.delta[k], c.ldt[k], 0, dT[k], ldn, 0, n, md.w[k + 1], 1);
+            }
+        }
+        for (int k = 0; k < S; ++k) {
+            const int64_t Pk = md.block_size(k), tk = md.w[k], uk = md.w[k + 1];
+            if (md.woff[k] + Pk <= rlo || md.woff[k] >= rhi) continue;
+            {
+                auto tri = [&](int64_t r) {
+                    const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
+                    return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
+                };
+                const double f0 = tri(rlo), f1 = rhi >= md.woff[k] + Pk ? 1.0 : tri(rhi);
+                const double orbits = (double)uk * (uk + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
+                ProfScope ps("opg_symkr", s, 2.0 * (double)n * orbits * (f1 - f0),
+                             (double)sizeof(T) * (double)Pk * Pk * (f1 - f0));
+                SymKrArgs<T> sa{akT[k], dT[k], 1, ldn, n, tk, uk, G, ldg, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
+                if (!SymKr<T>::run(prec, s, sa)) throw CurvError(kCudaError, "opg_kr: diagonal block kernel unavailable");
+            }
+            if (k == 0) continue;
+            const int64_t ak_rows = tk + 256;
+            T* akX = buf(ak_rows, ldn);
+            replicate_rows_kernel<T><<<dim3(blocks_for(ak_rows * ldn), 1), 256, 0, s>>>(akT[k], tk, ldn, akX, ak_rows, 0, 0);
+            CK_LAUNCH();
+            for (int m = k - 1; m >= 0; --m) {
+                const int64_t tm = md.w[m], um = md.w[m + 1];
+                T* pv = buf(uk * um, ldn);
+                outer_delta_kernel<T><<<dim3((unsigned)ceil_div(ldn, 256), (unsigned)um, (unsigned)uk), 256, 0, s>>>(
+                    dT[k], dT[m], um, ldn, pv);
+                CK_LAUNCH();
+                HessFusedArgs<T> fa{akX, ak_rows, nullptr, ak_rows, um * ak_rows, pv, dT[k], c.a[m], c.lda[m], ldn, n,
+                                    tk, tm, um, uk * tk, 0, Pk};
+                EpiHess<T> e{G, ldg, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n), 0, 1, rlo, rhi};
+                const double req = (double)Pk * um * (tm + 1);
+                ProfScope ps("opg_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * 2.0 * req);
+                if (!HessFused<T>::run(prec, s, fa, e)) throw CurvError(kCudaError, "opg_kr: block kernel unavailable");
+            }
+        }
+        return true;
     }
 
     // ---------------------------------------------------------------- hessian

@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "gemm_tc.cuh"
@@ -379,15 +380,16 @@ __global__ void pack_delta_products_kernel(const float* __restrict__ dT, const i
 
 template <>
 struct SymKr<float> {
-    // Applicability of the TMA orbit epilogue (else the scalar path writes all
-    // entries; the caller prefers the fused kernel then).
+    // Applicability of the TMA orbit epilogue (else the caller keeps the other kernels)
     static bool tma_ok(const float* H, int64_t ldh, int64_t woff, int64_t tk) {
         return ldh % 4 == 0 && woff % 4 == 0 && tk % 4 == 0 && (reinterpret_cast<uintptr_t>(H) & 15) == 0;
     }
 
     static bool run(int prec, cudaStream_t s, const SymKrArgs<float>& a) {
         if (prec != kTF32) return false;
-        if (!tma_ok(a.H, a.ldh, a.woff, a.tk)) return false;
+        // without TMA-addressable H (pitch or offset not 16-byte aligned) every
+        // entry takes the scalar path: slower, same values
+        const int tma = tma_ok(a.H, a.ldh, a.woff, a.tk) ? 1 : 0;
         namespace sym = tc::sym;
         const int64_t U = a.U, tk = a.tk;
         const int64_t np = U * (U + 1) / 2;
@@ -440,8 +442,9 @@ struct SymKr<float> {
         CUtensorMap m16 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 16);
         CUtensorMap mpi = tc::make_map(dptr<float>(pi), np, a.n, a.ldn, 0, (int)(bn / 2));
         tc::sym::HMaps hm;
+        std::memset(&hm, 0, sizeof hm);
         const int64_t L = a.ldh;
-        for (int x = 0; x < 2; ++x) {
+        for (int x = 0; tma && x < 2; ++x) {
             const int E = x == 0 ? 8 : 1;
             // type 1: H[(o,i),(o'',c)]  d = (c, i, o'', o), strides (1, L, tk, tk L)
             hm.m[4 * x + 0] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk, tk * L, 16, 8, E);
@@ -453,7 +456,7 @@ struct SymKr<float> {
             hm.m[4 * x + 3] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk * L, tk, 16, 8, E);
         }
         sym::Params prm{dptr<int4>(dtiles), (int64_t)tiles.size(), dptr<int4>(dpairs), np, bn, tk,
-                        ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, 1, 0};
+                        ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, tma, 0};
         static const int dev = getenv("CURVKIT_DEV_SYMKR") ? atoi(getenv("CURVKIT_DEV_SYMKR")) : 0;
         prm.dev = dev;
         static bool attr = false;

@@ -22,7 +22,8 @@ __host__ __device__ constexpr uint32_t idesc(int kind, int m, int n, bool a_mn, 
            ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-template <int CG, int KIND>
+// TS = 1: A operand from TMEM (columns 384.., cta_group::2 tf32 only)
+template <int CG, int KIND, int TS = 0>
 __global__ void __cluster_dims__(2, 1, 1) mma_rate(int reps, int n, int a_mn, int b_mn, long long* out) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bar;
@@ -57,7 +58,11 @@ __global__ void __cluster_dims__(2, 1, 1) mma_rate(int reps, int n, int a_mn, in
         long long t0 = clock64();
         for (int r = 0; r < reps; ++r) {
             const uint32_t d = tmem + (uint32_t)((r & 1) * 256);
-            if (CG == 2) {
+            if (TS) {
+                const uint32_t d2 = tmem + (uint32_t)((r & 1) * 192);
+                asm volatile("tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, {%4, %4, %4, %4, %4, %4, %4, %4}, 1;" ::"r"(d2),
+                             "r"(tmem + 384u + (uint32_t)((r & 3) * 32)), "l"(bd), "r"(id), "r"(z) : "memory");
+            } else if (CG == 2) {
                 if (KIND == 0)
                     asm volatile("tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%4, %4, %4, %4, %4, %4, %4, %4}, 1;" ::"r"(d),
                                  "l"(ad), "l"(bd), "r"(id), "r"(z) : "memory");
@@ -91,15 +96,15 @@ __global__ void __cluster_dims__(2, 1, 1) mma_rate(int reps, int n, int a_mn, in
     }
 }
 
-template <int CG, int KIND>
+template <int CG, int KIND, int TS = 0>
 void run(const char* name, int n, int a_mn, int b_mn, int grid) {
     long long* d;
     cudaMalloc(&d, grid * sizeof(long long));
     cudaMemset(d, 0, grid * sizeof(long long));
-    cudaFuncSetAttribute(mma_rate<CG, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(mma_rate<CG, KIND, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     const int reps = 4096;
-    mma_rate<CG, KIND><<<grid, 128, 64 * 1024>>>(reps, n, a_mn, b_mn, d);
-    mma_rate<CG, KIND><<<grid, 128, 64 * 1024>>>(reps, n, a_mn, b_mn, d);
+    mma_rate<CG, KIND, TS><<<grid, 128, 64 * 1024>>>(reps, n, a_mn, b_mn, d);
+    mma_rate<CG, KIND, TS><<<grid, 128, 64 * 1024>>>(reps, n, a_mn, b_mn, d);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[296] = {0};
     cudaMemcpy(h, d, grid * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -116,6 +121,9 @@ void run(const char* name, int n, int a_mn, int b_mn, int grid) {
 
 int main() {
     for (int grid : {2, 148}) {
+        run<2, 0, 1>("tf32 TS cta_group::2 N192", 192, 0, 0, grid);
+        run<2, 0, 1>("tf32 TS cta_group::2 N176", 176, 0, 0, grid);
+        run<2, 0, 0>("tf32 SS cta_group::2 N176", 176, 0, 0, grid);
         run<2, 0>("tf32 cta_group::2 KK", 256, 0, 0, grid);
         run<2, 0>("tf32 cta_group::2 K,MN", 256, 0, 1, grid);
         run<2, 0>("tf32 cta_group::2 MN,MN", 256, 1, 1, grid);
