@@ -254,9 +254,11 @@ struct Engine {
     // OPG without J (TF32): G[(k,o,i),(m,o'',c)] = (1/N) sum_n abar_k,i abar_m,c
     // delta_k,o delta_m,o'' -- the per-example gradient rows are delta (x) abar
     // (autodiff.cpp:127-143).  Diagonal blocks by the symmetric Khatri-Rao
-    // kernel (one value per orbit), blocks m < k by the fused block kernel with
-    // the profile delta_k,o delta_m,o'' and no Q term.  Same row-shard contract
-    // as opg(); returns false where the route does not apply (then J + SYRK).
+    // kernel (one value per orbit); the blocks m < k of a layer k form one
+    // rectangular tensor-core GEMM over J (or, where its rows are not
+    // 16-byte addressable, the fused block kernel with the profile
+    // delta_k,o delta_m,o'' and no Q term).  Same row-shard contract as opg();
+    // returns false where the route does not apply (then J + SYRK).
     bool opg_kr(const Cache<T>& c, T* G, int64_t ldg, int64_t rlo = 0, int64_t rhi = INT64_MAX) {
         if (!(prec == kTF32 && sizeof(T) == 4) || sym_off()) return false;
         const int S = md.S;
@@ -269,6 +271,8 @@ struct Engine {
         };
         T* akT[kMaxLayers] = {};
         T* dT[kMaxLayers] = {};
+        DevMem J;  // per-example gradients (rounded to TF32), only for the blocks m < k
+        int64_t ldj = 0;
         {
             ProfScope prep("opg_prep", s, 0.0, 0.0);
             for (int k = 0; k < S; ++k) {
@@ -294,6 +298,23 @@ struct Engine {
                 if (!SymKr<T>::run(prec, s, sa)) throw CurvError(kCudaError, "opg_kr: diagonal block kernel unavailable");
             }
             if (k == 0) continue;
+            // blocks m < k: one rectangular GEMM G[rows of k, columns of layers < k]
+            // = (1/N) J_k^T J_<k on the tensor cores (the SYRK engine), mirrored
+            const int64_t r0 = std::max(rlo, md.woff[k]), r1 = std::min(rhi, md.woff[k] + Pk);
+            if (r0 % 4 == 0) {
+                if (!J.p) {  // (jacobian() times itself as "jacobian")
+                    ldj = round_up(md.P, 32);
+                    J = DevMem((size_t)n * ldj * sizeof(T), s);
+                    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, true);
+                }
+                EpiSymLower<T> e{G, ldg, T(1) / T(n), r0};
+                ProfScope ps("opg_gemm", s, 2.0 * (double)(r1 - r0) * md.woff[k] * n,
+                             (double)sizeof(T) * 2.0 * (double)(r1 - r0) * md.woff[k]);
+                CurvGemm<T, EpiSymLower<T>>::run(prec, s, r1 - r0, md.woff[k], n,
+                                                 pre_rounded(mnmaj(dptr<T>(J) + r0, ldj)),
+                                                 pre_rounded(mnmaj(dptr<T>(J), ldj)), e);
+                continue;
+            }
             const int64_t ak_rows = tk + 256;
             T* akX = buf(ak_rows, ldn);
             replicate_rows_kernel<T><<<dim3(blocks_for(ak_rows * ldn), 1), 256, 0, s>>>(akT[k], tk, ldn, akX, ak_rows, 0, 0);

@@ -1,4 +1,5 @@
 """Dev driver: time the large BASELINE configs on one GPU.
+  c2: exact Hessian (P = 55050, H = 12 GB fp32)
   c3: full OPG (P = 109386, G = 48 GB fp32)     c4: top-100 OPG eigenpairs (P = 1.05 M)"""
 import sys, time, torch
 sys.path.insert(0, '.')
@@ -14,6 +15,18 @@ for name in which:
     ll = torch.tensor(lab, dtype=torch.int32, device=dev)
     spec = curv.ModelSpec(wl.widths, wl.activation)
     P = wl.P
+    if name == "c2":
+        ld = (P + 31) // 32 * 32
+        H = torch.empty((P, ld), dtype=torch.float32, device=dev)
+        for it in range(2):
+            if it == 1: curv.profile_begin()
+            torch.cuda.synchronize(); t = time.time()
+            curv.dev_assemble_hessian(spec, p, xx, ll, wl.n, H, ld, precision="tf32")
+            torch.cuda.synchronize()
+            print(name, "hessian", it, "%.1f ms" % ((time.time() - t) * 1e3), flush=True)
+        print("  ", {k: (round(v["ms"], 2), v["launches"], round(v["flops"] / v["ms"] / 1e9, 1) if v["flops"] else None) for k, v in curv.profile_end().items()})
+        print("   sym", torch.equal(H[:1024, :1024], H[:1024, :1024].T), "H[0,0]", H[0, 0].item(), "mem GB", torch.cuda.max_memory_allocated() / 1e9)
+        del H
     if name == "c3":
         ld = (P + 31) // 32 * 32
         G = torch.empty((P, ld), dtype=torch.float32, device=dev)
