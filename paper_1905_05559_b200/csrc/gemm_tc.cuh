@@ -127,6 +127,26 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// One lane of a converged warp.  The MMA issuers run as whole warps with
+// warp-uniform descriptors and issue from the elected lane: a single-lane
+// issuer makes ptxas wrap every tcgen05.mma in a uniform-register waterfall
+// (ELECT / R2UR.BROADCAST / BRA.U.ANY), which measured ~200 clocks per MMA,
+// well below the tensor pipe's rate (tools/mma_loop.cu).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
+__device__ __forceinline__ void mma_tf32_e(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (elect_one()) mma_tf32(d, a, b, idesc, acc);
+    __syncwarp();
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+    if (elect_one()) mma_commit(bar);
+    __syncwarp();
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     uint32_t r[32];
     asm volatile(
@@ -290,7 +310,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
+        {  // ---------------- MMA issuer (whole warp; elected lane issues)
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -320,18 +340,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
                         const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
                         const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
                         const uint32_t accf = (kb > 0 || ks > 0) ? 1u : 0u;
-                        mma_tf32(d, ahi, bhi, idesc, accf);
+                        mma_tf32_e(d, ahi, bhi, idesc, accf);
                         if (split == 2) {
                             const uint64_t alo = smem_desc(sa + A_BYTES + aoff, albo, asbo, alay);
                             const uint64_t blo = smem_desc(sb + B_BYTES + boff, blbo, bsbo, blay);
-                            mma_tf32(d, ahi, blo, idesc, 1u);
-                            mma_tf32(d, alo, bhi, idesc, 1u);
+                            mma_tf32_e(d, ahi, blo, idesc, 1u);
+                            mma_tf32_e(d, alo, bhi, idesc, 1u);
                         }
                     }
-                    mma_commit(&empty[stage]);
+                    mma_commit_e(&empty[stage]);
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&tfull[acc]);
+                mma_commit_e(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -511,6 +531,20 @@ __device__ __forceinline__ void commit2(uint64_t* bar) {
         : "memory");
 }
 
+// issue from the elected lane of a converged warp (see elect_one)
+__device__ __forceinline__ void mma2_tf32_e(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (elect_one()) mma2_tf32(d, a, b, idesc, acc);
+    __syncwarp();
+}
+__device__ __forceinline__ void mma2_tf32_ts_e(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (elect_one()) mma2_tf32_ts(d, a, b, idesc, acc);
+    __syncwarp();
+}
+__device__ __forceinline__ void commit2_e(uint64_t* bar) {
+    if (elect_one()) commit2(bar);
+    __syncwarp();
+}
+
 __host__ __device__ constexpr uint32_t idesc2_tf32(int n, bool a_mn, bool b_mn) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
            ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -651,7 +685,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader only)
+        if (rank == 0) {  // ---------------- MMA issuer (leader CTA, whole warp; elected lane issues)
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -679,16 +713,16 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         const uint32_t alay = sh.a_mn ? sh.mn_layout : 2, blay = sh.b_mn ? sh.mn_layout : 2;
                         const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
                         const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
-                        mma2_tf32(d, ahi, bhi, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                        mma2_tf32_e(d, ahi, bhi, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                         if (split == 2) {
-                            mma2_tf32(d, ahi, smem_desc(sb + S::B_BYTES + boff, blbo, bsbo, blay), idesc, 1u);
-                            mma2_tf32(d, smem_desc(sa + S::A_BYTES + aoff, albo, asbo, alay), bhi, idesc, 1u);
+                            mma2_tf32_e(d, ahi, smem_desc(sb + S::B_BYTES + boff, blbo, bsbo, blay), idesc, 1u);
+                            mma2_tf32_e(d, smem_desc(sa + S::A_BYTES + aoff, albo, asbo, alay), bhi, idesc, 1u);
                         }
                     }
-                    commit2(&empty[stage]);
+                    commit2_e(&empty[stage]);
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
-                commit2(&tfull[acc]);
+                commit2_e(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -967,7 +1001,7 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+        if (rank == 0) {  // ---------------- MMA issuer (leader CTA, whole warp; elected lane issues)
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -996,14 +1030,14 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                         const uint32_t blay = sh.b_mn ? sh.mn_layout : 2;
                         const uint64_t bd = smem_desc(sb + boff, blbo, bsbo, blay);
                         if constexpr (TS)
-                            mma2_tf32_ts(d, aslot + ks * 8, bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                            mma2_tf32_ts_e(d, aslot + ks * 8, bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
                         else
-                            mma2_tf32(d, smem_desc(sa + ks * 32, 16, 1024, 2), bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                            mma2_tf32_e(d, smem_desc(sa + ks * 32, 16, 1024, 2), bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
                     }
-                    commit2(&empty[stage]);
+                    commit2_e(&empty[stage]);
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
-                commit2(&tfull[acc]);
+                commit2_e(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }

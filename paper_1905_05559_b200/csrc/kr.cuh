@@ -176,7 +176,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+        if (rank == 0) {  // ---------------- MMA issuer (leader CTA, whole warp; elected lane issues)
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -199,12 +199,12 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                             const uint64_t ad = JT ? smem_desc(sa + ks * mn_kstep, mn_lbo, mn_sbo, 1)
                                                    : smem_desc(sa + ks * 32, 16, 1024, 2);
                             const uint64_t bd = smem_desc(sb + ks * mn_kstep, mn_lbo, mn_sbo, 1);
-                            mma2_tf32(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                            mma2_tf32_e(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                         }
-                        commit2(&empty[stage]);
+                        commit2_e(&empty[stage]);
                         if (++stage == NST) { stage = 0; phase ^= 1; }
                     }
-                    commit2(&tfull[acc]);
+                    commit2_e(&tfull[acc]);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
             }

@@ -69,7 +69,7 @@ struct Params {
     int64_t ldh, woff, boff;
     float alpha;
     int tma;             // H boxes by TMA (else every entry by the scalar path)
-    int dev;             // dev experiments (CURVKIT_DEV_SYMKR): 1 no transform, 2 no epilogue stores
+    int dev;             // dev experiments (CURVKIT_DEV_SYMKR): 1 no transform, 2 no epilogue stores, 32 MMA loop alone (+64 no per-K-block commits)
 };
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -150,7 +150,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
     const uint32_t tmem_base = *tmem_holder;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- producer
+        if (lane == 0 && !(p.dev & 32)) {  // ---------------- producer
             int stage = 0;
             uint32_t phase = 0;
             const uint64_t pol = evict_last_policy();
@@ -173,33 +173,41 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (leader)
+        if (rank == 0) {  // ---------------- MMA issuer (leader CTA, whole warp, elected lane issues)
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
             const uint32_t idesc = idesc2_tf32(bn, false, false);
+            const uint64_t zdesc0 = smem_desc(smem_u32(smem) + Z_OFF, 16, 1024, 2);
+            const uint64_t bdesc0 = smem_desc(smem_u32(smem) + B_OFF, 16, 1024, 2);
             for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(acc * 256);
                 for (int64_t kb = 0; kb < p.nk; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    if (!(p.dev & 32)) mbar_wait(&full[stage], phase);  // dev 32: the MMA loop alone (no data)
                     tc_fence_after();
-                    const uint32_t sz = smem_u32(smem + stage * STAGE + Z_OFF);
-                    const uint32_t sb = sz + B_OFF;
+                    const uint64_t off = (uint64_t)((stage * STAGE) >> 4);  // descriptor address field: 16-byte units
 #pragma unroll
-                    for (int ks = 0; ks < BK / 8; ++ks)
-                        mma2_tf32(d, smem_desc(sz + ks * 32, 16, 1024, 2), smem_desc(sb + ks * 32, 16, 1024, 2), idesc,
-                                  (kb > 0 || ks > 0) ? 1u : 0u);
-                    commit2(&empty[stage]);
+                    for (int ks = 0; ks < BK / 8; ++ks) {
+                        if (elect_one())
+                            mma2_tf32(d, zdesc0 + off + 2 * ks, bdesc0 + off + 2 * ks, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        __syncwarp();
+                    }
+                    if (!(p.dev & 64)) {  // dev 64: no per-K-block commit
+                        if (elect_one()) commit2(&empty[stage]);
+                        __syncwarp();
+                    }
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
-                commit2(&tfull[acc]);
+                if (elect_one()) commit2(&tfull[acc]);
+                __syncwarp();
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else if (warp >= TW0) {  // ---------------- Z transform (both CTAs)
+        if (p.dev & 32) goto done;
         const int set = (warp - TW0) / TW_W;
         const int rho = ((warp - TW0) % TW_W) * 32 + lane;  // tile row: i = rho / 16, c = rho % 16
         const int il = rho >> 4, cl = rho & 15;
@@ -319,6 +327,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
         }
         if (lane < CH) bulk_wait_all();
     }
+done:
     tc_fence_before();
     __syncthreads();
     cluster_sync();
