@@ -13,8 +13,9 @@ for r in rows:
     name = r["Kernel Name"]
     short = re.sub(r"\(.*", "", name).replace("void ", "")
     short = re.sub(r"<.*", "", short)
-    if "kr_kernel" in name or "tc_gemm_pair_kernel" in name or "tc_hess_fused_kernel" in name:
-        short += re.search(r"<[^(]*", name).group(0)[:48]
+    if "kr_kernel" in name or "tc_gemm_pair_kernel" in name or "tc_hess_fused_kernel" in name or "symkr" in name:
+        m = re.search(r"<[^(]*", name)
+        short += m.group(0)[:48] if m else ""
     a = agg.setdefault(short, [0, 0.0])
     a[0] += 1
     a[1] += float(r["Metric Value"]) / 1e3
