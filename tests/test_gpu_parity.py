@@ -157,6 +157,31 @@ def test_config1_hessian_and_opg_pins(prec):
         assert rel_fro(gr[j], pins["grows"][j]) <= tol
 
 
+def test_config3_opg_pins_tf32():
+    """BASELINE config 3 at full size (P = 109 386, N = 10 000, G = 48 GB):
+    six reference OPG rows (tests/golden/make_c3_pins.py) -- layer-0 weights
+    (symmetric Khatri-Rao kernel), its bias, layer-1 weights and the output
+    bias (rectangular J GEMM) -- and exact symmetry."""
+    torch = pytest.importorskip("torch")
+    wl = CONFIGS["c3"]
+    pins = load_golden("c3_pins")
+    p, x, lab = _device_inputs(wl, torch, torch.float32)
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P = wl.P
+    ld = (P + 3) // 4 * 4
+    G = torch.empty((P, ld), dtype=torch.float32, device="cuda:0")
+    curv.dev_assemble_opg(spec, p, x, lab, wl.n, G, ld, precision="tf32")
+    torch.cuda.synchronize()
+    rows = torch.tensor(pins["rows"], device="cuda:0")
+    gr = G[rows, :P].double().cpu().numpy()
+    for j in range(gr.shape[0]):
+        assert rel_fro(gr[j], pins["grows"][j].astype(np.float64)) <= 1e-3, (int(pins["rows"][j]), rel_fro(gr[j], pins["grows"][j]))
+    cols = G[:, rows].T.double().cpu().numpy()  # columns = rows by symmetry
+    assert np.array_equal(cols, gr)
+    del G
+    torch.cuda.empty_cache()
+
+
 def test_config2_hessian_pins_tf32():
     torch = pytest.importorskip("torch")
     wl = CONFIGS["c2"]
@@ -302,3 +327,51 @@ def test_opg_odd_pitch_device_buffer():
     curv.dev_assemble_opg(spec, p, x, lab, wl.n, G2, P + 1, precision="tf32")
     torch.cuda.synchronize()
     assert torch.equal(G1[:, :P], G2[:, :P])
+
+
+def test_config4_topk_against_exact_spectrum():
+    """BASELINE config 4 at full size (P = 1 055 242, N = 20 000): the device
+    randomized range finder against the exact nonzero spectrum of G, from the
+    dual Gram (1/N) J J^T (20 000 x 20 000, FP32 SGEMM, fp64 eigvalsh; J is
+    84 GB and formed only for this check).  Rayleigh-Ritz values are lower
+    bounds of the true eigenvalues; the spectrum is flat (lambda_1/lambda_100 =
+    1.3), so with the BASELINE's 2 power iterations they sit ~10% low and
+    converge with more iterations: at 16, the top 10 are within 1e-3
+    (DESIGN.md section 5)."""
+    torch = pytest.importorskip("torch")
+    wl = CONFIGS["c4"]
+    p, x, lab = _device_inputs(wl, torch, torch.float32)
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P, n, k = wl.P, wl.n, wl.eig_k
+    lams = {}
+    for it in (wl.power_iters, 16):
+        q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
+        lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
+        curv.dev_opg_topk(spec, p, x, lab, n, k, wl.oversample, it, 7, q, lam, precision="tf32")
+        torch.cuda.synchronize()
+        lams[it] = lam.double().cpu().numpy()
+        del q
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        ldj = (P + 31) // 32 * 32
+        J = torch.empty((n, ldj), dtype=torch.float32, device="cuda:0")
+        curv.dev_assemble_jacobian(spec, p, x, lab, n, J, ldj, precision="f32")
+        K = torch.empty((n, n), dtype=torch.float64, device="cuda:0")
+        for i0 in range(0, n, 2000):
+            K[i0:i0 + 2000] = (J[i0:i0 + 2000, :P] @ J[:, :P].T).double()
+        del J
+        torch.cuda.empty_cache()
+        K = (K + K.T) / (2.0 * n)
+        ev = torch.linalg.eigvalsh(K).flip(0)[:k].cpu().numpy()
+        del K
+        torch.cuda.empty_cache()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+    for it, lam in lams.items():
+        assert np.all(np.diff(lam) <= 1e-6 * lam[0])            # descending
+        assert np.all(lam <= ev * (1 + 1e-4)), it                  # Ritz values bound from below
+    e2 = np.abs(lams[wl.power_iters] - ev) / ev
+    e16 = np.abs(lams[16] - ev) / ev
+    assert np.all(e16 <= e2 + 1e-4)                                # more iterations, closer
+    assert e16[:10].max() <= 1e-3, e16[:10]

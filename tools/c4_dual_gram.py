@@ -1,0 +1,51 @@
+"""Dev / parity evidence at full size for BASELINE config 4 (P = 1 055 242,
+N = 20 000): the top-k eigenvalues of G = (1/N) J^T J from the device
+randomized range finder against the exact nonzero spectrum of G, taken from
+the dual Gram K = (1/N) J J^T (20 000 x 20 000; FP32 SGEMM without TF32, fp64
+eigvalsh).  J (84 GB fp32) is formed only for this check.
+    python tools/c4_dual_gram.py [power_iters ...]"""
+import sys, time, json
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from paper_1905_05559_b200 import curv
+from paper_1905_05559_b200.workloads import CONFIGS
+
+torch.backends.cuda.matmul.allow_tf32 = False
+wl = CONFIGS["c4"]
+params, x, y, lab = wl.draw()
+dev = "cuda:0"
+p = torch.tensor(params, dtype=torch.float32, device=dev)
+xx = torch.tensor(x, dtype=torch.float32, device=dev)
+ll = torch.tensor(lab, dtype=torch.int32, device=dev)
+spec = curv.ModelSpec(wl.widths, wl.activation)
+P, n, k = wl.P, wl.n, wl.eig_k
+iters = [int(a) for a in sys.argv[1:]] or [wl.power_iters]
+lams = {}
+for it in iters:
+    q = torch.empty((P, k), dtype=torch.float32, device=dev)
+    lam = torch.empty(k, dtype=torch.float32, device=dev)
+    curv.dev_opg_topk(spec, p, xx, ll, n, k, wl.oversample, it, 7, q, lam, precision="tf32")
+    torch.cuda.synchronize()
+    lams[it] = lam.double().cpu().numpy()
+    del q
+t = time.time()
+ldj = (P + 31) // 32 * 32
+J = torch.empty((n, ldj), dtype=torch.float32, device=dev)
+curv.dev_assemble_jacobian(spec, p, xx, ll, n, J, ldj, precision="f32")
+K = torch.empty((n, n), dtype=torch.float64, device=dev)
+bs = 2000
+for i0 in range(0, n, bs):  # row blocks of K in fp32 SGEMM, accumulated into fp64
+    K[i0:i0 + bs] = (J[i0:i0 + bs, :P] @ J[:, :P].T).double()
+del J
+torch.cuda.empty_cache()
+K = (K + K.T) / (2.0 * n)
+ev = torch.linalg.eigvalsh(K).flip(0)[:k].cpu().numpy()
+print(f"dual Gram + eigvalsh: {time.time() - t:.1f} s")
+out = {"lambda_exact_top10": ev[:10].tolist(), "lambda_exact_k": float(ev[k - 1])}
+for it, l in lams.items():
+    rel = np.abs(l - ev) / ev
+    out[f"power_iters={it}"] = {"max_rel_err_top10": float(rel[:10].max()), "max_rel_err_top50": float(rel[:50].max()),
+                                "max_rel_err_all": float(rel.max()), "median_rel_err": float(np.median(rel)),
+                                "n_within_1e-3": int((rel <= 1e-3).sum())}
+print(json.dumps(out, indent=1))
