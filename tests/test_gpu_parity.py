@@ -336,15 +336,15 @@ def test_config4_topk_against_exact_spectrum():
     84 GB and formed only for this check).  Rayleigh-Ritz values are lower
     bounds of the true eigenvalues; the spectrum is flat (lambda_1/lambda_100 =
     1.3), so with the BASELINE's 2 power iterations they sit ~10% low and
-    converge with more iterations: at 16, the top 10 are within 1e-3
-    (DESIGN.md section 5)."""
+    converge with more iterations: at 64 all 100 are within 1e-3 (DESIGN.md
+    section 5)."""
     torch = pytest.importorskip("torch")
     wl = CONFIGS["c4"]
     p, x, lab = _device_inputs(wl, torch, torch.float32)
     spec = curv.ModelSpec(wl.widths, wl.activation)
     P, n, k = wl.P, wl.n, wl.eig_k
     lams = {}
-    for it in (wl.power_iters, 16):
+    for it in (wl.power_iters, 64):
         q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
         lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
         curv.dev_opg_topk(spec, p, x, lab, n, k, wl.oversample, it, 7, q, lam, precision="tf32")
@@ -372,6 +372,6 @@ def test_config4_topk_against_exact_spectrum():
         assert np.all(np.diff(lam) <= 1e-6 * lam[0])            # descending
         assert np.all(lam <= ev * (1 + 1e-4)), it                  # Ritz values bound from below
     e2 = np.abs(lams[wl.power_iters] - ev) / ev
-    e16 = np.abs(lams[16] - ev) / ev
-    assert np.all(e16 <= e2 + 1e-4)                                # more iterations, closer
-    assert e16[:10].max() <= 1e-3, e16[:10]
+    e64 = np.abs(lams[64] - ev) / ev
+    assert np.all(e64 <= e2 + 1e-4)                                # more iterations, closer
+    assert e64.max() <= 1e-3, (e64.max(), int(e64.argmax()))       # the north_star's bar, all 100
