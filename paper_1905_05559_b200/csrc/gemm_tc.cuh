@@ -1074,8 +1074,10 @@ tc_hess_fused_kernel(const __grid_constant__ CUtensorMap mapAk, const __grid_con
                 const uint32_t ph_ = phase;
                 if (++stage == NST) { stage = 0; phase ^= 1; }
                 if (TW_SETS > 1 && ++sidx == TW_SETS) sidx = 0;
-                if (!mine) continue;
+                // every set waits on every stage in order: a set that skipped stages
+                // could see a completed phase of the same parity one lap early
                 mbar_wait(&afull[st_], ph_);
+                if (!mine) continue;
                 if constexpr (TS) {
                     if (g >= TS_SLOTS) {
                         mbar_wait(&empty[rs], rph);
