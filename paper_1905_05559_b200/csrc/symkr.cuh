@@ -45,18 +45,28 @@ using namespace ::ck::tc::pair;
 constexpr int EPI_W = 8, TW_W = 4, TW_SETS = 2;  // TW_SETS sets of 4 transform warps take alternate K-blocks
 constexpr int kThreads = 128 + 32 * EPI_W + 32 * TW_W * TW_SETS;
 constexpr int TW0 = 4 + EPI_W;
-constexpr int Z_BYTES = 128 * BK * 4;   // A operand (Z), 128 rows x 32 examples
+constexpr int Z_BYTES = 128 * BK * 4;   // A operand (Z), 128 rows x 32 examples (shared-memory form)
 constexpr int B_BYTES = 128 * BK * 4;   // up to 128 packed profile rows per CTA
 constexpr int I_BYTES = 8 * BK * 4;     // abar^T rows of the CTA's 8 i
 constexpr int C_BYTES = 16 * BK * 4;    // abar^T rows of the 16 c
-constexpr int STAGE = Z_BYTES + B_BYTES + I_BYTES + C_BYTES;
 constexpr int CH = 8;                   // epilogue chunk (packed columns)
 constexpr int SLOT = CH * 128 * 4;      // one staging layout of one chunk
 constexpr int EPI_BYTES = 2 * 2 * 2 * SLOT;  // group x double buffer x layout
 constexpr int EPI_PAD = 4 * 1024;       // boxes of extent 8 may read past a slot
 constexpr int MAX_SMEM = 227 * 1024;
-constexpr int NST = std::min(8, (MAX_SMEM - 1024 - EPI_BYTES - EPI_PAD - 1024) / STAGE);
-constexpr int SMEM_BYTES = 1024 + NST * STAGE + EPI_BYTES + EPI_PAD + 1024;
+// ZT (Z in TMEM): the transform writes Z with tcgen05.st into NZ slots of 32
+// columns and the MMA reads A from TMEM (tcgen05.mma [d], [a], b), so Z never
+// passes through shared memory; slot reuse is gated by an MMA commit (zfree).
+constexpr int NZ = 4;
+constexpr int ZSLOT0 = 512 - 32 * NZ;   // first Z column; accumulators at 0 and bn
+template <bool ZT>
+struct Cfg {
+    static constexpr int STAGE = (ZT ? 0 : Z_BYTES) + B_BYTES + I_BYTES + C_BYTES;
+    static constexpr int NST = std::min(8, (MAX_SMEM - 1024 - EPI_BYTES - EPI_PAD - 1024) / STAGE);
+    static constexpr int SMEM_BYTES = 1024 + NST * STAGE + EPI_BYTES + EPI_PAD + 1024;
+    static constexpr int MAX_BN = ZT ? ZSLOT0 / 2 / 16 * 16 : 256;
+    static constexpr int ACC_STRIDE = ZT ? 0 : 256;  // 0: accumulator acc at acc * bn
+};
 
 struct Params {
     const int4* tiles;   // (ib, cb, nt, -): 16-blocks ib <= cb of abar indices, packed column tile nt
@@ -104,12 +114,15 @@ struct HMaps {
     CUtensorMap m[8];
 };
 
+template <bool ZT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant__ CUtensorMap mapAbar16,
              const __grid_constant__ CUtensorMap mapPi, const __grid_constant__ HMaps hm, Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    constexpr int Z_OFF = 0, B_OFF = Z_BYTES, I_OFF = B_OFF + B_BYTES, C_OFF = I_OFF + I_BYTES;
+    using K = Cfg<ZT>;
+    constexpr int STAGE = K::STAGE, NST = K::NST;
+    constexpr int Z_OFF = 0, B_OFF = ZT ? 0 : Z_BYTES, I_OFF = B_OFF + B_BYTES, C_OFF = I_OFF + I_BYTES;
     uint8_t* epi_base = smem + NST * STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + EPI_BYTES + EPI_PAD);
     uint64_t* full = bars;         // [8] leader: producer + 2 x 4 transform warps, B tx
@@ -117,7 +130,8 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
     uint64_t* afull = bars + 16;   // [8] local: abar rows landed
     uint64_t* tfull = bars + 24;   // [2]
     uint64_t* tempty = bars + 26;  // [2] leader
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
+    uint64_t* zfree = bars + 28;   // [NZ] both CTAs (ZT): the MMA of the slot's K-block is done
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28 + NZ);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cta_rank();
@@ -137,6 +151,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 2 * EPI_W);
         }
+        for (int z = 0; z < NZ; ++z) mbar_init(&zfree[z], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -181,23 +196,34 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
             const uint32_t idesc = idesc2_tf32(bn, false, false);
             const uint64_t zdesc0 = smem_desc(smem_u32(smem) + Z_OFF, 16, 1024, 2);
             const uint64_t bdesc0 = smem_desc(smem_u32(smem) + B_OFF, 16, 1024, 2);
+            int zs = 0;
             for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+                const uint32_t d = tmem_base + (uint32_t)(acc * (K::ACC_STRIDE ? K::ACC_STRIDE : bn));
                 for (int64_t kb = 0; kb < p.nk; ++kb) {
                     if (!(p.dev & 32)) mbar_wait(&full[stage], phase);  // dev 32: the MMA loop alone (no data)
                     tc_fence_after();
                     const uint64_t off = (uint64_t)((stage * STAGE) >> 4);  // descriptor address field: 16-byte units
 #pragma unroll
                     for (int ks = 0; ks < BK / 8; ++ks) {
-                        if (elect_one())
-                            mma2_tf32(d, zdesc0 + off + 2 * ks, bdesc0 + off + 2 * ks, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        if (elect_one()) {
+                            if constexpr (ZT)
+                                mma2_tf32_ts(d, tmem_base + (uint32_t)(ZSLOT0 + zs * 32 + ks * 8), bdesc0 + off + 2 * ks,
+                                             idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                            else
+                                mma2_tf32(d, zdesc0 + off + 2 * ks, bdesc0 + off + 2 * ks, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        }
                         __syncwarp();
                     }
                     if (!(p.dev & 64)) {  // dev 64: no per-K-block commit
                         if (elect_one()) commit2(&empty[stage]);
                         __syncwarp();
+                    }
+                    if constexpr (ZT) {
+                        if (elect_one()) commit2(&zfree[zs]);
+                        __syncwarp();
+                        if (++zs == NZ) zs = 0;
                     }
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
@@ -214,8 +240,9 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
         const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
         int stage = 0, sidx = 0;
         uint32_t phase = 0;
+        int64_t g = 0;  // K-block counter (ZT: Z slot g mod NZ)
         for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
-            for (int64_t kb = 0; kb < p.nk; ++kb) {
+            for (int64_t kb = 0; kb < p.nk; ++kb, ++g) {
                 const int st_ = stage;
                 const uint32_t ph_ = phase;
                 if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -226,9 +253,29 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                 mbar_wait(&afull[st_], ph_);
                 if (!mine) continue;
                 uint8_t* st = smem + st_ * STAGE;
-                if (!(p.dev & 1)) {
-                    const uint8_t* ri = st + I_OFF + il * 128;
-                    const uint8_t* rc = st + C_OFF + cl * 128;
+                const uint8_t* ri = st + I_OFF + il * 128;
+                const uint8_t* rc = st + C_OFF + cl * 128;
+                if constexpr (ZT) {
+                    const int zs = (int)(g % NZ);
+                    // slot reuse: the MMA of K-block g - NZ is done (phase g / NZ - 1 of zfree[zs];
+                    // exact: that barrier cannot run ahead of this set's own K-block g)
+                    if (g >= NZ) mbar_wait(&zfree[zs], (uint32_t)(((g / NZ) - 1) & 1));
+                    if (!(p.dev & 1)) {
+                        float z[32];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 x = *reinterpret_cast<const float4*>(ri + ((q ^ (il & 7)) << 4));
+                            const float4 y = *reinterpret_cast<const float4*>(rc + ((q ^ (cl & 7)) << 4));
+                            z[4 * q] = round_tf32(x.x * y.x);
+                            z[4 * q + 1] = round_tf32(x.y * y.y);
+                            z[4 * q + 2] = round_tf32(x.z * y.z);
+                            z[4 * q + 3] = round_tf32(x.w * y.w);
+                        }
+                        // row rho of this CTA's Z = TMEM lane rho, K = the slot's 32 columns
+                        tmem_st32(tmem_base + ((uint32_t)(rho & ~31) << 16) + (uint32_t)(ZSLOT0 + zs * 32), z);
+                    }
+                    tc_fence_before();
+                } else if (!(p.dev & 1)) {
                     uint8_t* rz = st + Z_OFF + rho * 128;
                     float4 x[8], y[8];
 #pragma unroll
@@ -273,7 +320,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                 const int64_t J0 = jt0 + jj0;
                 if (J0 >= p.npairs) break;  // uniform across the group
                 float v[CH];
-                tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256 + jj0), v);
+                tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * (K::ACC_STRIDE ? K::ACC_STRIDE : bn) + jj0), v);
 #pragma unroll
                 for (int e = 0; e < CH; ++e) v[e] *= p.alpha;
                 const int ncol = (int)(p.npairs - J0 < CH ? p.npairs - J0 : CH);
@@ -421,8 +468,12 @@ struct SymKr<float> {
                 e += L;
             }
         }
-        const int64_t ntn = ceil_div(np, 256);
-        const int64_t bn = round_up(ceil_div(np, ntn), 16);
+        // Z in shared memory (default) or in TMEM (CURVKIT_SYMKR_TS=1: correct, but measured
+        // slower on B200 -- c1 1.08 vs 0.92 ms, c2 9.2 vs 8.6 ms, c3 97.7 vs 85.7 ms)
+        static const bool zt = getenv("CURVKIT_SYMKR_TS") != nullptr;
+        const int64_t max_bn = zt ? sym::Cfg<true>::MAX_BN : sym::Cfg<false>::MAX_BN;
+        const int64_t ntn = ceil_div(np, max_bn);
+        const int64_t bn = round_up(ceil_div(np, ntn), 16);  // <= max_bn
         const int64_t nb = ceil_div(tk + 1, 16);  // 16-blocks of abar indices
         // Tile order = write locality: the ~74 tiles in flight walk an SB x SB square
         // of (ib, cb) blocks, so both the c-contiguous (types 1, 4) and the
@@ -483,11 +534,17 @@ struct SymKr<float> {
         prm.dev = dev;
         static bool attr = false;
         if (!attr) {
-            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sym::SMEM_BYTES));
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         sym::Cfg<true>::SMEM_BYTES));
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         sym::Cfg<false>::SMEM_BYTES));
             attr = true;
         }
         const int grid = 2 * (int)std::min<int64_t>((int64_t)tiles.size(), tc::num_sms() / 2);
-        sym::symkr_kernel<<<grid, sym::kThreads, sym::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        if (zt)
+            sym::symkr_kernel<true><<<grid, sym::kThreads, sym::Cfg<true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        else
+            sym::symkr_kernel<false><<<grid, sym::kThreads, sym::Cfg<false>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
         CK_LAUNCH();
         return true;
     }
