@@ -342,7 +342,10 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                         // kind 1: extent-8 box from this column (the run fills the chunk or
                         // ends at U, where the TMA clips), 2: extent-1 box, 0: inside a box
                         const int4 bx = __ldg(&p.pairs[J0 + lane]);
-                        if (bx.z) {
+                        // dev 256: skip types 2, 3 (32-byte rows); dev 512: skip types 1, 4 (64-byte rows)
+                        const bool skip_t = ((p.dev & 256) && (quad == 1 || quad == 2)) ||
+                                            ((p.dev & 512) && (quad == 0 || quad == 3));
+                        if (bx.z && !skip_t) {
                             const CUtensorMap* mp = &hm.m[(bx.z == 1 ? 0 : 4) + quad];
                             const bool ic = quad == 0 || quad == 3;  // types 1, 4: [o''][i][c]
                             const float* src = (ic ? sA : sB) + lane * 128;
