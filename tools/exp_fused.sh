@@ -1,4 +1,3 @@
 timeout 120 python tools/hess_c1_once.py c1 5 2>&1 | tail -1 | grep -o "'hess_symkr': ([^)]*)" || echo "c1 run failed/hung"
 timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_shards.py -x -q -m gpu -k "hessian or config1 or config2 or union or opg" 2>&1 | tail -2
-CURVKIT_SYMKR_PAIRX=0 timeout 120 python tools/hess_c1_once.py c1 5 2>&1 | tail -1 | grep -o "'hess_symkr': ([^)]*)"
 timeout 300 python tools/run_configs.py c2 2>&1 | grep -o "'hess_symkr': ([^)]*)"
