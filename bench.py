@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--precision", default="tf32", choices=list(PREC_DTYPE))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     return ap.parse_args()
 
@@ -330,6 +330,10 @@ def run_b200(args):
             roof = {"bound": "hbm", "achieved": achieved, "unit": "GB/s", "kernel": dom, "peak": pk["hbm_gbs"],
                     "frac": achieved / pk["hbm_gbs"], "share_of_step": r["ms"] / args.steps / ms,
                     "per_launch_ms": per_launch_ms, "traffic": None}
+        if dom in ("hess_symkr", "opg_symkr"):
+            roof["note"] = ("flops = 2 N per symmetric-orbit value (the kernel's algorithmic work, DESIGN.md section 4); "
+                            "at config 1 the kernel is bound by its TMA output stores (32/64-byte rows, "
+                            "profiles/r01_c1_symkr_ncu_summary.txt), at configs 2/3 by the tensor pipe (~0.9 of peak)")
         tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tfile):
             roof["traffic"] = json.load(open(tfile)).get(dom)
