@@ -81,6 +81,59 @@ struct SymKr {
     static bool run(int, cudaStream_t, const SymKrArgs<T>&) { return false; }
 };
 
+// ---- symmetric orbits without the tensor-core kernel (f32 SIMT, f64 DMMA) ----
+// The same one-value-per-orbit scheme as symkr.cuh for the non-TF32 modes:
+// Z[(i,c)][n] = abar_i abar_c is materialised for a chunk of pairs i <= c,
+// V = Z Pi_packed^T runs on the precision's GEMM engine, and the epilogue
+// writes each value to its four places.
+
+// Z[q][n] = akT[i_q][n] * akT[c_q][n]
+template <class T>
+__global__ void orbit_z_kernel(const T* __restrict__ akT, int64_t ldn, const int2* __restrict__ ic, int64_t q0,
+                               int64_t nq, int64_t n, T* __restrict__ z) {
+    const int64_t q = q0 + blockIdx.y;
+    if (blockIdx.y >= nq) return;
+    const int2 p = ic[q];
+    const T* a = akT + p.x * ldn;
+    const T* b = akT + p.y * ldn;
+    T* out = z + (int64_t)blockIdx.y * ldn;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[i] * b[i];
+}
+
+// packed profiles: out[j][n] = src[(o_j U + o''_j)][n] (H) or dk[o_j][n] dk[o''_j][n] (OPG)
+template <class T>
+__global__ void orbit_pack_kernel(const T* __restrict__ src, const int2* __restrict__ oo, int64_t U, int64_t ldn,
+                                  int64_t n, int delta_products, T* __restrict__ out) {
+    const int2 p = oo[blockIdx.y];
+    T* d = out + (int64_t)blockIdx.y * ldn;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = delta_products ? src[p.x * ldn + i] * src[p.y * ldn + i] : src[(p.x * U + p.y) * ldn + i];
+}
+
+// GEMM row m = pair q0 + m, column j = packed (o, o''): the value goes to
+// (o,i; o'',c), (o'',c; o,i), (o,c; o'',i), (o'',i; o,c) of the block
+template <class T>
+struct EpiOrbit {
+    T* H;
+    int64_t ldh, woff, boff, tk;
+    T alpha;
+    const int2* ic;  // pairs (i, c), i <= c, indexed by q0 + m
+    int64_t q0;
+    const int2* oo;  // packed (o, o'')
+    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
+    __device__ int64_t idx(int64_t o, int64_t x) const { return x < tk ? woff + o * tk + x : boff + o; }
+    __device__ void operator()(int, int64_t m, int64_t j, T acc) const {
+        const int2 p = ic[q0 + m], u = oo[j];
+        const T v = alpha * acc;
+        const int64_t r1 = idx(u.x, p.x), c1 = idx(u.y, p.y), r3 = idx(u.x, p.y), c3 = idx(u.y, p.x);
+        H[r1 * ldh + c1] = v;
+        H[c1 * ldh + r1] = v;
+        H[r3 * ldh + c3] = v;
+        H[c3 * ldh + r3] = v;
+    }
+};
+
 // PV[o][o''][n] = dk[o][n] * dm[o''][n]  (OPG profile of block (k, m))
 template <class T>
 __global__ void outer_delta_kernel(const T* __restrict__ dk, const T* __restrict__ dm, int64_t um, int64_t ldn,
@@ -251,6 +304,49 @@ struct Engine {
         CurvGemm<T, EpiSymLower<T>>::run(prec, s, re - rb, re, n, pre_rounded(mnmaj(J + rb, ldj)), pre_rounded(mnmaj(J, ldj)), e);
     }
 
+    // Diagonal block of layer k by symmetric orbits on the precision's GEMM engine
+    // (f32 SIMT, f64 DMMA); prof = profiles [U][U][ldn] (H) or delta_k^T [U][ldn]
+    // (OPG, delta_products).  A row shard takes the pair range matching its share
+    // of the block's lower triangle (orbits partition the entries).
+    void orbit_block(int k, const T* akT, const T* prof, int delta_products, int64_t ldn, int64_t n, T* H, int64_t ldh,
+                     int64_t rlo, int64_t rhi) {
+        const int64_t tk = md.w[k], U = md.w[k + 1], Pk = md.block_size(k);
+        std::vector<int2> ic, oo;
+        for (int64_t i = 0; i <= tk; ++i)
+            for (int64_t c = i; c <= tk; ++c) ic.push_back(make_int2((int)i, (int)c));
+        for (int64_t o = 0; o < U; ++o)
+            for (int64_t q = o; q < U; ++q) oo.push_back(make_int2((int)o, (int)q));
+        const int64_t nq = (int64_t)ic.size(), np = (int64_t)oo.size();
+        auto tri = [&](int64_t r) {
+            const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
+            return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
+        };
+        const int64_t qa = rlo <= md.woff[k] ? 0 : std::min<int64_t>(nq, (int64_t)(tri(rlo) * (double)nq));
+        const int64_t qb = rhi >= md.woff[k] + Pk ? nq : std::min<int64_t>(nq, (int64_t)(tri(rhi) * (double)nq));
+        if (qa >= qb) return;
+        DevMem dic(ic.size() * sizeof(int2), s), doo(oo.size() * sizeof(int2), s);
+        CK_CUDA(cudaMemcpyAsync(dic.p, ic.data(), ic.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        CK_CUDA(cudaMemcpyAsync(doo.p, oo.data(), oo.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        DevMem pi((size_t)np * ldn * sizeof(T), s);
+        orbit_pack_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)np), 256, 0, s>>>(
+            prof, dptr<int2>(doo), U, ldn, n, delta_products, dptr<T>(pi));
+        CK_LAUNCH();
+        // Z in chunks of at most ~512 MB
+        const int64_t chunk = std::clamp<int64_t>((int64_t(512) << 20) / ((int64_t)ldn * (int64_t)sizeof(T)), 64, 32768);  // grid.y
+        DevMem z((size_t)std::min(chunk, qb - qa) * ldn * sizeof(T), s);
+        for (int64_t q0 = qa; q0 < qb; q0 += chunk) {
+            const int64_t nqc = std::min(chunk, qb - q0);
+            orbit_z_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)nqc), 256, 0, s>>>(
+                akT, ldn, dptr<int2>(dic), q0, nqc, n, dptr<T>(z));
+            CK_LAUNCH();
+            EpiOrbit<T> e{H, ldh, md.woff[k], md.boff[k], tk, T(1) / T(n), dptr<int2>(dic), q0, dptr<int2>(doo)};
+            if constexpr (sizeof(T) == 4)  // f32: SIMT (the TF32 modes take symkr.cuh)
+                gemm_simt<T>(s, nqc, np, n, 1, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
+            else  // f64: FP64 tensor cores
+                CurvGemm<T, EpiOrbit<T>>::run(prec, s, nqc, np, n, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
+        }
+    }
+
     // OPG without J (TF32): G[(k,o,i),(m,o'',c)] = (1/N) sum_n abar_k,i abar_m,c
     // delta_k,o delta_m,o'' -- the per-example gradient rows are delta (x) abar
     // (autodiff.cpp:127-143).  Diagonal blocks by the symmetric Khatri-Rao
@@ -260,7 +356,8 @@ struct Engine {
     // delta_k,o delta_m,o'' and no Q term).  Same row-shard contract as opg();
     // returns false where the route does not apply (then J + SYRK).
     bool opg_kr(const Cache<T>& c, T* G, int64_t ldg, int64_t rlo = 0, int64_t rhi = INT64_MAX) {
-        if (!(prec == kTF32 && sizeof(T) == 4) || sym_off()) return false;
+        const bool tc = prec == kTF32 && sizeof(T) == 4;
+        if (!(tc || prec == kF32 || prec == kF64) || sym_off()) return false;
         const int S = md.S;
         const int64_t n = c.n, ldn = round_up(n, 32);
         std::vector<DevMem> keep;
@@ -294,25 +391,28 @@ struct Engine {
                 const double orbits = (double)uk * (uk + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
                 ProfScope ps("opg_symkr", s, 2.0 * (double)n * orbits * (f1 - f0),
                              (double)sizeof(T) * (double)Pk * Pk * (f1 - f0));
-                SymKrArgs<T> sa{akT[k], dT[k], 1, ldn, n, tk, uk, G, ldg, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
-                if (!SymKr<T>::run(prec, s, sa)) throw CurvError(kCudaError, "opg_kr: diagonal block kernel unavailable");
+                if (tc) {
+                    SymKrArgs<T> sa{akT[k], dT[k], 1, ldn, n, tk, uk, G, ldg, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
+                    if (!SymKr<T>::run(prec, s, sa)) throw CurvError(kCudaError, "opg_kr: diagonal block kernel unavailable");
+                } else {
+                    orbit_block(k, akT[k], dT[k], 1, ldn, n, G, ldg, rlo, rhi);
+                }
             }
             if (k == 0) continue;
             // blocks m < k: one rectangular GEMM G[rows of k, columns of layers < k]
             // = (1/N) J_k^T J_<k on the tensor cores (the SYRK engine), mirrored
             const int64_t r0 = std::max(rlo, md.woff[k]), r1 = std::min(rhi, md.woff[k] + Pk);
-            if (r0 % 4 == 0) {
+            if (r0 % 4 == 0 || !tc) {
                 if (!J.p) {  // (jacobian() times itself as "jacobian")
                     ldj = round_up(md.P, 32);
                     J = DevMem((size_t)n * ldj * sizeof(T), s);
-                    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, true);
+                    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, tc);
                 }
                 EpiSymLower<T> e{G, ldg, T(1) / T(n), r0};
                 ProfScope ps("opg_gemm", s, 2.0 * (double)(r1 - r0) * md.woff[k] * n,
                              (double)sizeof(T) * 2.0 * (double)(r1 - r0) * md.woff[k]);
-                CurvGemm<T, EpiSymLower<T>>::run(prec, s, r1 - r0, md.woff[k], n,
-                                                 pre_rounded(mnmaj(dptr<T>(J) + r0, ldj)),
-                                                 pre_rounded(mnmaj(dptr<T>(J), ldj)), e);
+                auto opj = [&](const T* p) { return tc ? pre_rounded(mnmaj(p, ldj)) : mnmaj(p, ldj); };
+                CurvGemm<T, EpiSymLower<T>>::run(prec, s, r1 - r0, md.woff[k], n, opj(dptr<T>(J) + r0), opj(dptr<T>(J)), e);
                 continue;
             }
             const int64_t ak_rows = tk + 256;
@@ -508,6 +608,12 @@ struct Engine {
                                  (double)sizeof(T) * (double)Pk * Pk * (f1 - f0));
                     SymKrArgs<T> sa{akT, GT, 0, ldn, n, tk, np, H, ldh, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
                     if (SymKr<T>::run(prec, s, sa)) jbeg = Pk;
+                }
+                if (!fused && (prec == kF32 || prec == kF64) && m == k && !verify && !sym_off()) {
+                    const double orbits = (double)np * (np + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
+                    ProfScope ps("hess_orbit", s, 2.0 * (double)n * orbits, (double)sizeof(T) * (double)Pk * Pk);
+                    orbit_block(k, akT, GT, 0, ldn, n, H, ldh, rlo, rhi);
+                    jbeg = Pk;
                 }
                 if (fused && jbeg < Pk) {
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
