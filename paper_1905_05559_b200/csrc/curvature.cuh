@@ -104,11 +104,13 @@ __global__ void orbit_z_kernel(const T* __restrict__ akT, int64_t ldn, const int
 // packed profiles: out[j][n] = src[(o_j U + o''_j)][n] (H) or dk[o_j][n] dk[o''_j][n] (OPG)
 template <class T>
 __global__ void orbit_pack_kernel(const T* __restrict__ src, const int2* __restrict__ oo, int64_t U, int64_t ldn,
-                                  int64_t n, int delta_products, T* __restrict__ out) {
-    const int2 p = oo[blockIdx.y];
-    T* d = out + (int64_t)blockIdx.y * ldn;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        d[i] = delta_products ? src[p.x * ldn + i] * src[p.y * ldn + i] : src[(p.x * U + p.y) * ldn + i];
+                                  int64_t n, int delta_products, T* __restrict__ out, int64_t np) {
+    for (int64_t j = blockIdx.y; j < np; j += gridDim.y) {  // grid.y <= 65535
+        const int2 p = oo[j];
+        T* d = out + j * ldn;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            d[i] = delta_products ? src[p.x * ldn + i] * src[p.y * ldn + i] : src[(p.x * U + p.y) * ldn + i];
+    }
 }
 
 // GEMM row m = pair q0 + m, column j = packed (o, o''): the value goes to
@@ -328,8 +330,8 @@ struct Engine {
         CK_CUDA(cudaMemcpyAsync(dic.p, ic.data(), ic.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
         CK_CUDA(cudaMemcpyAsync(doo.p, oo.data(), oo.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
         DevMem pi((size_t)np * ldn * sizeof(T), s);
-        orbit_pack_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)np), 256, 0, s>>>(
-            prof, dptr<int2>(doo), U, ldn, n, delta_products, dptr<T>(pi));
+        orbit_pack_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
+            prof, dptr<int2>(doo), U, ldn, n, delta_products, dptr<T>(pi), np);
         CK_LAUNCH();
         // Z in chunks of at most ~512 MB
         const int64_t chunk = std::clamp<int64_t>((int64_t(512) << 20) / ((int64_t)ldn * (int64_t)sizeof(T)), 64, 32768);  // grid.y

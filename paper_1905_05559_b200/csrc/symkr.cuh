@@ -410,28 +410,30 @@ inline CUtensorMap make_map_orbit(float* H, int64_t ldh, int64_t woff, int64_t d
 // out[j][.] = tf32(src[(o_j * U + o''_j)][.])  -- packed profile rows
 __global__ void pack_profile_kernel(const float* __restrict__ src, const int4* __restrict__ pairs, int64_t U,
                                     int64_t ldn, float* __restrict__ out, int64_t npairs) {
-    const int64_t j = blockIdx.y;
-    const int4 pr = pairs[j];
-    const float4* s = reinterpret_cast<const float4*>(src + (pr.x * U + pr.y) * ldn);
-    float4* d = reinterpret_cast<float4*>(out + j * ldn);
-    for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
-        float4 v = s[q];
-        v.x = round_tf32(v.x); v.y = round_tf32(v.y); v.z = round_tf32(v.z); v.w = round_tf32(v.w);
-        d[q] = v;
+    for (int64_t j = blockIdx.y; j < npairs; j += gridDim.y) {  // grid.y <= 65535
+        const int4 pr = pairs[j];
+        const float4* s = reinterpret_cast<const float4*>(src + (pr.x * U + pr.y) * ldn);
+        float4* d = reinterpret_cast<float4*>(out + j * ldn);
+        for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
+            float4 v = s[q];
+            v.x = round_tf32(v.x); v.y = round_tf32(v.y); v.z = round_tf32(v.z); v.w = round_tf32(v.w);
+            d[q] = v;
+        }
     }
 }
 
 // out[j][n] = tf32(dT[o_j][n] * dT[o''_j][n])  -- OPG profiles delta_o delta_o''
 __global__ void pack_delta_products_kernel(const float* __restrict__ dT, const int4* __restrict__ pairs, int64_t ldn,
                                            float* __restrict__ out, int64_t npairs) {
-    const int64_t j = blockIdx.y;
-    const int4 pr = pairs[j];
-    const float4* a = reinterpret_cast<const float4*>(dT + pr.x * ldn);
-    const float4* b = reinterpret_cast<const float4*>(dT + pr.y * ldn);
-    float4* d = reinterpret_cast<float4*>(out + j * ldn);
-    for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
-        const float4 x = a[q], y = b[q];
-        d[q] = make_float4(round_tf32(x.x * y.x), round_tf32(x.y * y.y), round_tf32(x.z * y.z), round_tf32(x.w * y.w));
+    for (int64_t j = blockIdx.y; j < npairs; j += gridDim.y) {  // grid.y <= 65535
+        const int4 pr = pairs[j];
+        const float4* a = reinterpret_cast<const float4*>(dT + pr.x * ldn);
+        const float4* b = reinterpret_cast<const float4*>(dT + pr.y * ldn);
+        float4* d = reinterpret_cast<float4*>(out + j * ldn);
+        for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
+            const float4 x = a[q], y = b[q];
+            d[q] = make_float4(round_tf32(x.x * y.x), round_tf32(x.y * y.y), round_tf32(x.z * y.z), round_tf32(x.w * y.w));
+        }
     }
 }
 
@@ -508,10 +510,10 @@ struct SymKr<float> {
         // packed profiles (B operand, K-major rows of ldn examples), rounded to nearest TF32
         DevMem pi((size_t)np * a.ldn * 4, s);
         if (a.delta_products)
-            tc::pack_delta_products_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)np), 256, 0, s>>>(
+            tc::pack_delta_products_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
                 a.prof, dptr<int4>(dpairs), a.ldn, dptr<float>(pi), np);
         else
-            tc::pack_profile_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)np), 256, 0, s>>>(
+            tc::pack_profile_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
                 a.prof, dptr<int4>(dpairs), U, a.ldn, dptr<float>(pi), np);
         CK_LAUNCH();
         CUtensorMap m8 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 8);

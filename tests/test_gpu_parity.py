@@ -375,3 +375,29 @@ def test_config4_topk_against_exact_spectrum():
     e64 = np.abs(lams[64] - ev) / ev
     assert np.all(e64 <= e2 + 1e-4)                                # more iterations, closer
     assert e64.max() <= 1e-3, (e64.max(), int(e64.argmax()))       # the north_star's bar, all 100
+
+
+@pytest.mark.parametrize("prec", ["tf32", "f64"])
+def test_wide_layer_orbits_against_oracle(prec):
+    """A 400-unit layer: 80 200 packed (o, o'') columns (more than one grid
+    dimension holds) through the symmetric-orbit kernels, against the C oracle
+    for H and G; inputs in [4, 400, 3] make the first layer's T_k = 4."""
+    from oracle.oracle import Oracle
+    from paper_1905_05559_b200.workloads import normal, splitmix64
+    widths, n = [4, 400, 3], 16
+    P = sum(widths[k] * widths[k + 1] + widths[k + 1] for k in range(len(widths) - 1))
+    params = 0.3 * normal(901, P)
+    x = normal(907, n * widths[0]).reshape(n, widths[0])
+    y = np.zeros((n, widths[-1]))
+    y[np.arange(n), (splitmix64(913, n) % np.uint64(widths[-1])).astype(np.int64)] = 1.0
+    ospec = dict(widths=widths, activation="sigmoid")
+    orc = Oracle()
+    H_ref, _ = orc.hessian(ospec, params, x, y, batch=n)
+    G_ref = orc.opg(ospec, params, x, y)
+    spec = curv.ModelSpec(widths, "sigmoid")
+    hr = curv.assemble_hessian(spec, params, curv.Batch(x, y), curv.CurvatureConfig(batch_size_h=n), precision=prec)
+    G = curv.assemble_opg(spec, params, curv.Batch(x, y), curv.CurvatureConfig(batch_size_g=n), precision=prec)
+    tol = TOL[prec]
+    assert rel_fro(hr.h, H_ref) <= tol, rel_fro(hr.h, H_ref)
+    assert rel_fro(G, G_ref) <= tol, rel_fro(G, G_ref)
+    assert np.array_equal(hr.h, hr.h.T) and np.array_equal(G, G.T)
