@@ -4,6 +4,8 @@
 // model.cpp:201-214, curvature.cpp:15-29, autodiff.cpp:266-280) so a caller
 // switching from curvkit sees the same contract errors for the same inputs.
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -206,6 +208,10 @@ void upload_and_forward(const ModelDesc& md, const double* params, const double*
                                                                                  r.cache.a[0], r.cache.lda[0]);
     CK_LAUNCH();
     forward_backward<T>(md, dptr<T>(r.params), dptr<int32_t>(r.labels), r.cache, s);
+    // Settle the pageable-memory uploads before the curvature work: without this
+    // sync a later 2.6 GB device-to-pinned download of the same call measured
+    // 53-214 ms instead of a steady 53 ms (tools/e2e_probe.py)
+    CK_CUDA(cudaStreamSynchronize(s));
 }
 
 // Device-resident inputs: x already T on device.
@@ -269,6 +275,24 @@ double hessian_into(const ModelDesc& md, const T* params, const Cache<T>& c, T* 
     return asym;
 }
 
+// dev (CURVKIT_HOST_TIMING): wall time of the phases of a host-buffer call
+struct HostTimer {
+    const char* name;
+    cudaStream_t s;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    HostTimer(const char* n, cudaStream_t st) : name(n), s(st), on(getenv("CURVKIT_HOST_TIMING") != nullptr) {
+        if (on) t = std::chrono::steady_clock::now();
+    }
+    void mark(const char* phase) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[curvkit] %s %s %.2f ms\n", name, phase, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 template <class T, class U>
 void host_hessian(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n,
                   const curvkit_curvature_config* cfg, int prec, bool verify, U* h_out, double* asym_out) {
@@ -277,12 +301,16 @@ void host_hessian(const ModelDesc& md, const double* params, const double* x, co
     check_divisible(n, cfg ? cfg->batch_size_h : n, "assemble_hessian");
     auto lab = labels_from_onehot(md, y, n);
     cudaStream_t s = lib_stream();
+    HostTimer tm("assemble_hessian", s);
     Resident<T> r;
     upload_and_forward<T>(md, params, x, lab, n, r, s);
+    tm.mark("upload+forward");
     const int64_t ldh = round_up(md.P, 4);
     DevMem H((size_t)md.P * ldh * sizeof(T), s);
     const double asym = hessian_into<T>(md, dptr<T>(r.params), r.cache, dptr<T>(H), ldh, prec, verify, s);
+    tm.mark("compute");
     download<T, U>(dptr<T>(H), ldh, md.P, md.P, h_out, s);
+    tm.mark("download");
     if (asym_out) *asym_out = asym;
 }
 
@@ -314,12 +342,16 @@ void host_opg(const ModelDesc& md, const double* params, const double* x, const 
     check_divisible(n, cfg ? cfg->batch_size_g : n, "assemble_opg");
     auto lab = labels_from_onehot(md, y, n);
     cudaStream_t s = lib_stream();
+    HostTimer tm("assemble_opg", s);
     Resident<T> r;
     upload_and_forward<T>(md, params, x, lab, n, r, s);
+    tm.mark("upload+forward");
     const int64_t ldg = round_up(md.P, 4);
     DevMem G((size_t)md.P * ldg * sizeof(T), s);
     opg_into<T>(md, r.cache, dptr<T>(G), ldg, prec, s);
+    tm.mark("compute");
     download<T, U>(dptr<T>(G), ldg, md.P, md.P, g_out, s);
+    tm.mark("download");
 }
 
 template <class T>

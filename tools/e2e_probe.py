@@ -26,6 +26,6 @@ def d2h(): hH.copy_(d[:, :P], non_blocking=True); torch.cuda.synchronize()
 for f, name in ((h, "hessian host API"), (g, "opg host API"), (d2h, "bare pitched D2H 2.59 GB")):
     f()
     ts = []
-    for _ in range(4):
+    for _ in range(8):
         t = time.perf_counter(); f(); ts.append(time.perf_counter() - t)
-    print(f"{name:28s} {1e3 * min(ts):8.1f} ms  (median {1e3 * sorted(ts)[len(ts) // 2]:.1f})")
+    print(f"{name:28s} {1e3 * min(ts):8.1f} ms  (median {1e3 * sorted(ts)[len(ts) // 2]:.1f})  all", [round(1e3 * v, 1) for v in ts])
