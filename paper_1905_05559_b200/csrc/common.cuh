@@ -9,8 +9,10 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 
 namespace ck {
 
@@ -139,6 +141,27 @@ __device__ __forceinline__ T act_second(int a, T z) {
         }
         default: return T(0);
     }
+}
+
+// Read-only launch tables (tile lists, packed index pairs) keyed by content:
+// uploaded once per device and kept for the life of the process, so repeated
+// calls of the same shape launch without a pageable host-to-device copy.
+inline const void* cached_upload(const void* host, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, void*> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::string key(reinterpret_cast<const char*>(&dev), sizeof dev);
+    key.append(reinterpret_cast<const char*>(host), bytes);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    void* d = nullptr;
+    if (cudaMalloc(&d, bytes ? bytes : 1) != cudaSuccess) throw std::runtime_error("cached_upload: cudaMalloc failed");
+    if (bytes && cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("cached_upload: cudaMemcpy failed");
+    cache.emplace(std::move(key), d);
+    return d;
 }
 
 }  // namespace ck

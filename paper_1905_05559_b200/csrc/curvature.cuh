@@ -326,12 +326,11 @@ struct Engine {
         const int64_t qa = rlo <= md.woff[k] ? 0 : std::min<int64_t>(nq, (int64_t)(tri(rlo) * (double)nq));
         const int64_t qb = rhi >= md.woff[k] + Pk ? nq : std::min<int64_t>(nq, (int64_t)(tri(rhi) * (double)nq));
         if (qa >= qb) return;
-        DevMem dic(ic.size() * sizeof(int2), s), doo(oo.size() * sizeof(int2), s);
-        CK_CUDA(cudaMemcpyAsync(dic.p, ic.data(), ic.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-        CK_CUDA(cudaMemcpyAsync(doo.p, oo.data(), oo.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        const int2* dic = static_cast<const int2*>(cached_upload(ic.data(), ic.size() * sizeof(int2)));
+        const int2* doo = static_cast<const int2*>(cached_upload(oo.data(), oo.size() * sizeof(int2)));
         DevMem pi((size_t)np * ldn * sizeof(T), s);
         orbit_pack_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
-            prof, dptr<int2>(doo), U, ldn, n, delta_products, dptr<T>(pi), np);
+            prof, doo, U, ldn, n, delta_products, dptr<T>(pi), np);
         CK_LAUNCH();
         // Z in chunks of at most ~512 MB
         const int64_t chunk = std::clamp<int64_t>((int64_t(512) << 20) / ((int64_t)ldn * (int64_t)sizeof(T)), 64, 32768);  // grid.y
@@ -339,9 +338,9 @@ struct Engine {
         for (int64_t q0 = qa; q0 < qb; q0 += chunk) {
             const int64_t nqc = std::min(chunk, qb - q0);
             orbit_z_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)nqc), 256, 0, s>>>(
-                akT, ldn, dptr<int2>(dic), q0, nqc, n, dptr<T>(z));
+                akT, ldn, dic, q0, nqc, n, dptr<T>(z));
             CK_LAUNCH();
-            EpiOrbit<T> e{H, ldh, md.woff[k], md.boff[k], tk, T(1) / T(n), dptr<int2>(dic), q0, dptr<int2>(doo)};
+            EpiOrbit<T> e{H, ldh, md.woff[k], md.boff[k], tk, T(1) / T(n), dic, q0, doo};
             if constexpr (sizeof(T) == 4)  // f32: SIMT (the TF32 modes take symkr.cuh)
                 gemm_simt<T>(s, nqc, np, n, 1, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
             else  // f64: FP64 tensor cores

@@ -1602,9 +1602,7 @@ struct HessFused<float> {
                         list.push_back(make_int4((int)o, (int)j0, (int)n0, 0));
             }
         if (list.empty()) return true;
-        DevMem tl(list.size() * sizeof(int4), s);
-        CK_CUDA(cudaMemcpyAsync(tl.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-        fh.tiles = dptr<int4>(tl);
+        fh.tiles = static_cast<const int4*>(cached_upload(list.data(), list.size() * sizeof(int4)));
         fh.ntiles = (int64_t)list.size();
         const int b3 = a.lda_m >= round_up(N, 32) ? 1 : 0;
         tc::TcShape sh{0, N, a.n, 0, 1, 1, (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, 0, b3};

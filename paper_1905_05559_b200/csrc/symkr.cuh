@@ -504,17 +504,16 @@ struct SymKr<float> {
             tiles = std::vector<int4>(tiles.begin() + t0, tiles.begin() + t1);
             if (tiles.empty()) return true;
         }
-        DevMem dpairs(pairs.size() * sizeof(int4), s), dtiles(tiles.size() * sizeof(int4), s);
-        CK_CUDA(cudaMemcpyAsync(dpairs.p, pairs.data(), pairs.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-        CK_CUDA(cudaMemcpyAsync(dtiles.p, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+        const int4* dpairs = static_cast<const int4*>(cached_upload(pairs.data(), pairs.size() * sizeof(int4)));
+        const int4* dtiles = static_cast<const int4*>(cached_upload(tiles.data(), tiles.size() * sizeof(int4)));
         // packed profiles (B operand, K-major rows of ldn examples), rounded to nearest TF32
         DevMem pi((size_t)np * a.ldn * 4, s);
         if (a.delta_products)
             tc::pack_delta_products_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
-                a.prof, dptr<int4>(dpairs), a.ldn, dptr<float>(pi), np);
+                a.prof, dpairs, a.ldn, dptr<float>(pi), np);
         else
             tc::pack_profile_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
-                a.prof, dptr<int4>(dpairs), U, a.ldn, dptr<float>(pi), np);
+                a.prof, dpairs, U, a.ldn, dptr<float>(pi), np);
         CK_LAUNCH();
         CUtensorMap m8 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 8);
         CUtensorMap m16 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 16);
@@ -533,7 +532,7 @@ struct SymKr<float> {
             // type 4: H[(o'',i),(o,c)]  d = (c, i, o'', o), strides (1, L, tk L, tk)
             hm.m[4 * x + 3] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk * L, tk, 16, 8, E);
         }
-        sym::Params prm{dptr<int4>(dtiles), (int64_t)tiles.size(), dptr<int4>(dpairs), np, bn, tk,
+        sym::Params prm{dtiles, (int64_t)tiles.size(), dpairs, np, bn, tk,
                         ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, tma, 0};
         static const int dev = getenv("CURVKIT_DEV_SYMKR") ? atoi(getenv("CURVKIT_DEV_SYMKR")) : 0;
         prm.dev = dev;
