@@ -334,6 +334,12 @@ def run_b200(args):
             roof["note"] = ("flops = 2 N per symmetric-orbit value (the kernel's algorithmic work, DESIGN.md section 4); "
                             "at config 1 the kernel is bound by its TMA output stores (32/64-byte rows, "
                             "profiles/r01_c1_symkr_ncu_summary.txt), at configs 2/3 by the tensor pipe (~0.9 of peak)")
+            # the same launches counted as the lower-triangle product a symmetry-blind kernel runs
+            # (2 N per lower entry of the diagonal blocks): the rate the orbit scheme delivers
+            if world == 1 or weak:  # whole diagonal blocks per rank
+                ws = wl.widths
+                lower = sum(pk * (pk + 1) / 2.0 for pk in (ws[k + 1] * (ws[k] + 1) for k in range(len(ws) - 1)))
+                roof["reference_count_tflops"] = 2.0 * n * lower * args.steps / (r["ms"] / 1e3) / 1e12
         tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tfile):
             roof["traffic"] = json.load(open(tfile)).get(dom)
