@@ -3,7 +3,7 @@ N = 20 000): the top-k eigenvalues of G = (1/N) J^T J from the device
 randomized range finder against the exact nonzero spectrum of G, taken from
 the dual Gram K = (1/N) J J^T (20 000 x 20 000; FP32 SGEMM without TF32, fp64
 eigvalsh).  J (84 GB fp32) is formed only for this check.
-    python tools/c4_dual_gram.py [power_iters ...]"""
+    python tools/c4_dual_gram.py [power_iters[:oversample] ...]"""
 import sys, time, json
 import numpy as np
 import torch
@@ -20,14 +20,18 @@ xx = torch.tensor(x, dtype=torch.float32, device=dev)
 ll = torch.tensor(lab, dtype=torch.int32, device=dev)
 spec = curv.ModelSpec(wl.widths, wl.activation)
 P, n, k = wl.P, wl.n, wl.eig_k
-iters = [int(a) for a in sys.argv[1:]] or [wl.power_iters]
+runs = [tuple(int(v) for v in a.split(":")) for a in sys.argv[1:]] or [(wl.power_iters,)]
 lams = {}
-for it in iters:
+for r in runs:
+    it, ov = r[0], (r[1] if len(r) > 1 else wl.oversample)
     q = torch.empty((P, k), dtype=torch.float32, device=dev)
     lam = torch.empty(k, dtype=torch.float32, device=dev)
-    curv.dev_opg_topk(spec, p, xx, ll, n, k, wl.oversample, it, 7, q, lam, precision="tf32")
+    curv.dev_opg_topk(spec, p, xx, ll, n, k, ov, it, 7, q, lam, precision="tf32")
     torch.cuda.synchronize()
-    lams[it] = lam.double().cpu().numpy()
+    t0 = time.time()
+    curv.dev_opg_topk(spec, p, xx, ll, n, k, ov, it, 7, q, lam, precision="tf32")
+    torch.cuda.synchronize()
+    lams[f"{it}:{ov}"] = (lam.double().cpu().numpy(), time.time() - t0)
     del q
 t = time.time()
 ldj = (P + 31) // 32 * 32
@@ -43,9 +47,9 @@ K = (K + K.T) / (2.0 * n)
 ev = torch.linalg.eigvalsh(K).flip(0)[:k].cpu().numpy()
 print(f"dual Gram + eigvalsh: {time.time() - t:.1f} s")
 out = {"lambda_exact_top10": ev[:10].tolist(), "lambda_exact_k": float(ev[k - 1])}
-for it, l in lams.items():
+for key, (l, secs) in lams.items():
     rel = np.abs(l - ev) / ev
-    out[f"power_iters={it}"] = {"max_rel_err_top10": float(rel[:10].max()), "max_rel_err_top50": float(rel[:50].max()),
+    out[f"power_iters:oversample={key}"] = {"seconds": round(secs, 3),"max_rel_err_top10": float(rel[:10].max()), "max_rel_err_top50": float(rel[:50].max()),
                                 "max_rel_err_all": float(rel.max()), "median_rel_err": float(np.median(rel)),
                                 "n_within_1e-3": int((rel <= 1e-3).sum())}
 print(json.dumps(out, indent=1))
