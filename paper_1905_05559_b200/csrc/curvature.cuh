@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "model.cuh"
+#include "orbit_dmma.cuh"
 #include "prof.cuh"
 
 namespace ck {
@@ -312,6 +313,10 @@ struct Engine {
     // of the block's lower triangle (orbits partition the entries).
     void orbit_block(int k, const T* akT, const T* prof, int delta_products, int64_t ldn, int64_t n, T* H, int64_t ldh,
                      int64_t rlo, int64_t rhi) {
+        if constexpr (sizeof(T) == 8) {
+            orbit_block_f64(k, akT, prof, delta_products, ldn, n, H, ldh, rlo, rhi);
+            return;
+        }
         const int64_t tk = md.w[k], U = md.w[k + 1], Pk = md.block_size(k);
         std::vector<int2> ic, oo;
         for (int64_t i = 0; i <= tk; ++i)
@@ -345,6 +350,53 @@ struct Engine {
                 gemm_simt<T>(s, nqc, np, n, 1, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
             else  // f64: FP64 tensor cores
                 CurvGemm<T, EpiOrbit<T>>::run(prec, s, nqc, np, n, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
+        }
+    }
+
+    // f64: pairs in 8 x 8 (i, c) blocks, one 64-row DMMA tile per block, staged
+    // epilogue with 64-byte runs (orbit_dmma_kernel, gemm_dmma.cuh)
+    void orbit_block_f64(int k, const T* akT, const T* prof, int delta_products, int64_t ldn, int64_t n, T* H,
+                         int64_t ldh, int64_t rlo, int64_t rhi) {
+        const int64_t tk = md.w[k], U = md.w[k + 1], Pk = md.block_size(k);
+        const int64_t nb = ceil_div(tk + 1, 8);
+        std::vector<int2> blocks, ic, oo;
+        for (int64_t ib = 0; ib < nb; ++ib)
+            for (int64_t cb = ib; cb < nb; ++cb) blocks.push_back(make_int2((int)ib, (int)cb));
+        for (const int2& b : blocks)
+            for (int il = 0; il < 8; ++il)
+                for (int cl = 0; cl < 8; ++cl)  // padding rows read row T_k (masked at the store)
+                    ic.push_back(make_int2((int)std::min<int64_t>(8 * b.x + il, tk), (int)std::min<int64_t>(8 * b.y + cl, tk)));
+        for (int64_t o = 0; o < U; ++o)
+            for (int64_t q = o; q < U; ++q) oo.push_back(make_int2((int)o, (int)q));
+        const int64_t nbk = (int64_t)blocks.size(), np = (int64_t)oo.size();
+        auto tri = [&](int64_t r) {
+            const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
+            return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
+        };
+        const int64_t ba = rlo <= md.woff[k] ? 0 : std::min<int64_t>(nbk, (int64_t)(tri(rlo) * (double)nbk));
+        const int64_t bb = rhi >= md.woff[k] + Pk ? nbk : std::min<int64_t>(nbk, (int64_t)(tri(rhi) * (double)nbk));
+        if (ba >= bb) return;
+        const int2* dblocks = static_cast<const int2*>(cached_upload(blocks.data(), blocks.size() * sizeof(int2)));
+        const int2* dic = static_cast<const int2*>(cached_upload(ic.data(), ic.size() * sizeof(int2)));
+        const int2* doo = static_cast<const int2*>(cached_upload(oo.data(), oo.size() * sizeof(int2)));
+        DevMem pi((size_t)np * ldn * sizeof(T), s);
+        orbit_pack_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
+            prof, doo, U, ldn, n, delta_products, dptr<T>(pi), np);
+        CK_LAUNCH();
+        // Z chunks of whole blocks (<= ~512 MB, <= 32768 rows: grid.y of orbit_z_kernel)
+        const int64_t cblk = std::clamp<int64_t>((int64_t(512) << 20) / (64 * ldn * (int64_t)sizeof(T)), 1, 512);
+        DevMem z((size_t)std::min(cblk, bb - ba) * 64 * ldn * sizeof(T), s);
+        for (int64_t b0 = ba; b0 < bb; b0 += cblk) {
+            const int64_t nbc = std::min(cblk, bb - b0);
+            orbit_z_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)(64 * nbc)), 256, 0, s>>>(
+                akT, ldn, dic, 64 * b0, 64 * nbc, n, dptr<T>(z));
+            CK_LAUNCH();
+            if constexpr (sizeof(T) == 8) {
+                OrbitArgs oa{dptr<double>(z), dptr<double>(pi), ldn, np, n, dblocks + b0, doo, H, ldh, md.woff[k],
+                             md.boff[k], tk, 1.0 / (double)n};
+                orbit_dmma_kernel<<<dim3((unsigned)nbc, (unsigned)ceil_div(np, 64)), 128, 0, s>>>(oa);
+                CK_LAUNCH();
+            }
         }
     }
 

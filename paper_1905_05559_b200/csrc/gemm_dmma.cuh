@@ -12,14 +12,10 @@
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "orbit_dmma.cuh"
 
 namespace ck {
 
-__device__ __forceinline__ void dmma8x8x4(double* c, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c[0]), "+d"(c[1])
-                 : "d"(a), "d"(b));
-}
 
 template <class Epi>
 __global__ void __launch_bounds__(128) gemm_dmma_kernel(int64_t M, int64_t N, int64_t K, Opnd<double> A,
