@@ -82,11 +82,10 @@ struct SymKr {
     static bool run(int, cudaStream_t, const SymKrArgs<T>&) { return false; }
 };
 
-// ---- symmetric orbits without the tensor-core kernel (f32 SIMT, f64 DMMA) ----
-// The same one-value-per-orbit scheme as symkr.cuh for the non-TF32 modes:
-// Z[(i,c)][n] = abar_i abar_c is materialised for a chunk of pairs i <= c,
-// V = Z Pi_packed^T runs on the precision's GEMM engine, and the epilogue
-// writes each value to its four places.
+// ---- symmetric orbits in the f32 / f64 modes (Engine::orbit_block) ----
+// The same one-value-per-orbit scheme as symkr.cuh: Z[(i,c)][n] = abar_i abar_c
+// is materialised for a chunk of pair blocks, V = Z Pi_packed^T runs on the
+// FP64 tensor cores / FFMA (orbit_dmma.cuh), each value goes to its four places.
 
 // Z[q][n] = akT[i_q][n] * akT[c_q][n]
 template <class T>
@@ -113,29 +112,6 @@ __global__ void orbit_pack_kernel(const T* __restrict__ src, const int2* __restr
             d[i] = delta_products ? src[p.x * ldn + i] * src[p.y * ldn + i] : src[(p.x * U + p.y) * ldn + i];
     }
 }
-
-// GEMM row m = pair q0 + m, column j = packed (o, o''): the value goes to
-// (o,i; o'',c), (o'',c; o,i), (o,c; o'',i), (o'',i; o,c) of the block
-template <class T>
-struct EpiOrbit {
-    T* H;
-    int64_t ldh, woff, boff, tk;
-    T alpha;
-    const int2* ic;  // pairs (i, c), i <= c, indexed by q0 + m
-    int64_t q0;
-    const int2* oo;  // packed (o, o'')
-    __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
-    __device__ int64_t idx(int64_t o, int64_t x) const { return x < tk ? woff + o * tk + x : boff + o; }
-    __device__ void operator()(int, int64_t m, int64_t j, T acc) const {
-        const int2 p = ic[q0 + m], u = oo[j];
-        const T v = alpha * acc;
-        const int64_t r1 = idx(u.x, p.x), c1 = idx(u.y, p.y), r3 = idx(u.x, p.y), c3 = idx(u.y, p.x);
-        H[r1 * ldh + c1] = v;
-        H[c1 * ldh + r1] = v;
-        H[r3 * ldh + c3] = v;
-        H[c3 * ldh + r3] = v;
-    }
-};
 
 // PV[o][o''][n] = dk[o][n] * dm[o''][n]  (OPG profile of block (k, m))
 template <class T>
@@ -307,55 +283,14 @@ struct Engine {
         CurvGemm<T, EpiSymLower<T>>::run(prec, s, re - rb, re, n, pre_rounded(mnmaj(J + rb, ldj)), pre_rounded(mnmaj(J, ldj)), e);
     }
 
-    // Diagonal block of layer k by symmetric orbits on the precision's GEMM engine
-    // (f32 SIMT, f64 DMMA); prof = profiles [U][U][ldn] (H) or delta_k^T [U][ldn]
-    // (OPG, delta_products).  A row shard takes the pair range matching its share
-    // of the block's lower triangle (orbits partition the entries).
-    void orbit_block(int k, const T* akT, const T* prof, int delta_products, int64_t ldn, int64_t n, T* H, int64_t ldh,
-                     int64_t rlo, int64_t rhi) {
-        if constexpr (sizeof(T) == 8) {
-            orbit_block_f64(k, akT, prof, delta_products, ldn, n, H, ldh, rlo, rhi);
-            return;
-        }
-        const int64_t tk = md.w[k], U = md.w[k + 1], Pk = md.block_size(k);
-        std::vector<int2> ic, oo;
-        for (int64_t i = 0; i <= tk; ++i)
-            for (int64_t c = i; c <= tk; ++c) ic.push_back(make_int2((int)i, (int)c));
-        for (int64_t o = 0; o < U; ++o)
-            for (int64_t q = o; q < U; ++q) oo.push_back(make_int2((int)o, (int)q));
-        const int64_t nq = (int64_t)ic.size(), np = (int64_t)oo.size();
-        auto tri = [&](int64_t r) {
-            const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
-            return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
-        };
-        const int64_t qa = rlo <= md.woff[k] ? 0 : std::min<int64_t>(nq, (int64_t)(tri(rlo) * (double)nq));
-        const int64_t qb = rhi >= md.woff[k] + Pk ? nq : std::min<int64_t>(nq, (int64_t)(tri(rhi) * (double)nq));
-        if (qa >= qb) return;
-        const int2* dic = static_cast<const int2*>(cached_upload(ic.data(), ic.size() * sizeof(int2)));
-        const int2* doo = static_cast<const int2*>(cached_upload(oo.data(), oo.size() * sizeof(int2)));
-        DevMem pi((size_t)np * ldn * sizeof(T), s);
-        orbit_pack_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
-            prof, doo, U, ldn, n, delta_products, dptr<T>(pi), np);
-        CK_LAUNCH();
-        // Z in chunks of at most ~512 MB
-        const int64_t chunk = std::clamp<int64_t>((int64_t(512) << 20) / ((int64_t)ldn * (int64_t)sizeof(T)), 64, 32768);  // grid.y
-        DevMem z((size_t)std::min(chunk, qb - qa) * ldn * sizeof(T), s);
-        for (int64_t q0 = qa; q0 < qb; q0 += chunk) {
-            const int64_t nqc = std::min(chunk, qb - q0);
-            orbit_z_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)nqc), 256, 0, s>>>(
-                akT, ldn, dic, q0, nqc, n, dptr<T>(z));
-            CK_LAUNCH();
-            EpiOrbit<T> e{H, ldh, md.woff[k], md.boff[k], tk, T(1) / T(n), dic, q0, doo};
-            if constexpr (sizeof(T) == 4)  // f32: SIMT (the TF32 modes take symkr.cuh)
-                gemm_simt<T>(s, nqc, np, n, 1, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
-            else  // f64: FP64 tensor cores
-                CurvGemm<T, EpiOrbit<T>>::run(prec, s, nqc, np, n, kmaj(dptr<T>(z), ldn), kmaj(dptr<T>(pi), ldn), e);
-        }
-    }
-
-    // f64: pairs in 8 x 8 (i, c) blocks, one 64-row DMMA tile per block, staged
-    // epilogue with 64-byte runs (orbit_dmma_kernel, gemm_dmma.cuh)
-    void orbit_block_f64(int k, const T* akT, const T* prof, int delta_products, int64_t ldn, int64_t n, T* H,
+    // Diagonal block of layer k by symmetric orbits in the f32 / f64 modes (the
+    // TF32 modes take symkr.cuh).  prof = profiles [U][U][ldn] (H) or delta_k^T
+    // [U][ldn] (OPG, delta_products).  Z = abar_i abar_c is materialised for
+    // pairs in 8 x 8 (i, c) blocks, one 64-row tile per block (orbit_dmma_kernel
+    // f64 / orbit_simt_kernel f32, orbit_dmma.cuh), the tile staged in shared
+    // memory and written as runs of 8 for all four orbit images.  A row shard
+    // takes the block range matching its share of the block's lower triangle.
+    void orbit_block(int k, const T* akT, const T* prof, int delta_products, int64_t ldn, int64_t n, T* H,
                          int64_t ldh, int64_t rlo, int64_t rhi) {
         const int64_t tk = md.w[k], U = md.w[k + 1], Pk = md.block_size(k);
         const int64_t nb = ceil_div(tk + 1, 8);
@@ -391,12 +326,13 @@ struct Engine {
             orbit_z_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)(64 * nbc)), 256, 0, s>>>(
                 akT, ldn, dic, 64 * b0, 64 * nbc, n, dptr<T>(z));
             CK_LAUNCH();
-            if constexpr (sizeof(T) == 8) {
-                OrbitArgs oa{dptr<double>(z), dptr<double>(pi), ldn, np, n, dblocks + b0, doo, H, ldh, md.woff[k],
-                             md.boff[k], tk, 1.0 / (double)n};
+            OrbitArgs<T> oa{dptr<T>(z), dptr<T>(pi), ldn, np, n, dblocks + b0, doo, H, ldh, md.woff[k],
+                            md.boff[k], tk, T(1) / T(n)};
+            if constexpr (sizeof(T) == 8)
                 orbit_dmma_kernel<<<dim3((unsigned)nbc, (unsigned)ceil_div(np, 64)), 128, 0, s>>>(oa);
-                CK_LAUNCH();
-            }
+            else
+                orbit_simt_kernel<<<dim3((unsigned)nbc, (unsigned)ceil_div(np, 64)), 128, 0, s>>>(oa);
+            CK_LAUNCH();
         }
     }
 
