@@ -350,6 +350,7 @@ def run_b200(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
+            reference_sample(wl, os.cpu_count() or 1)  # warm-up sample (page faults, thread start), as the reference arm
             r = reference_sample(wl, os.cpu_count() or 1)
             cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # noqa: BLE001
