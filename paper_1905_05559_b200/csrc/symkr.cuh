@@ -46,7 +46,11 @@ constexpr int EPI_W = 8, TW_W = 4, TW_SETS = 2;  // TW_SETS sets of 4 transform 
 constexpr int kThreads = 128 + 32 * EPI_W + 32 * TW_W * TW_SETS;
 constexpr int TW0 = 4 + EPI_W;
 constexpr int Z_BYTES = 128 * BK * 4;   // A operand (Z), 128 rows x 32 examples (shared-memory form)
-constexpr int B_BYTES = 128 * BK * 4;   // up to 128 packed profile rows per CTA
+#ifndef CURVKIT_SYMKR_BROWS
+#define CURVKIT_SYMKR_BROWS 128
+#endif
+constexpr int B_ROWS = CURVKIT_SYMKR_BROWS;  // packed profile rows per CTA and stage (MMA N <= 2 B_ROWS)
+constexpr int B_BYTES = B_ROWS * BK * 4;
 constexpr int I_BYTES = 8 * BK * 4;     // abar^T rows of the CTA's 8 i
 constexpr int C_BYTES = 16 * BK * 4;    // abar^T rows of the 16 c
 constexpr int CH = 8;                   // epilogue chunk (packed columns)
@@ -64,7 +68,7 @@ struct Cfg {
     static constexpr int STAGE = (ZT ? 0 : Z_BYTES) + B_BYTES + I_BYTES + C_BYTES;
     static constexpr int NST = std::min(8, (MAX_SMEM - 1024 - EPI_BYTES - EPI_PAD - 1024) / STAGE);
     static constexpr int SMEM_BYTES = 1024 + NST * STAGE + EPI_BYTES + EPI_PAD + 1024;
-    static constexpr int MAX_BN = ZT ? ZSLOT0 / 2 / 16 * 16 : 256;
+    static constexpr int MAX_BN = ZT ? std::min(ZSLOT0 / 2 / 16 * 16, 2 * B_ROWS) : 2 * B_ROWS;
     static constexpr int ACC_STRIDE = ZT ? 0 : 256;  // 0: accumulator acc at acc * bn
 };
 
@@ -102,6 +106,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Tile row rho (TMEM lane, Z row) -> (i, c) within the CTA's 8 x 16 block.  A warp
+// covers 4 i x 8 c and each half-warp 2 i x 8 c, so the transform's abar loads touch
+// 8 distinct c rows per half-warp (one shared-memory wavefront per LDS.128).
+__device__ __forceinline__ void row_ic(int rho, int& il, int& cl) {
+    const int w = rho >> 5;
+    il = 4 * (w >> 1) + ((rho >> 3) & 3);
+    cl = (rho & 7) + 8 * (w & 1);
 }
 
 // H row / column of (unit o, abar index x): weight (o, x) or the bias of o
@@ -235,8 +248,9 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
     } else if (warp >= TW0) {  // ---------------- Z transform (both CTAs)
         if (p.dev & 32) goto done;
         const int set = (warp - TW0) / TW_W;
-        const int rho = ((warp - TW0) % TW_W) * 32 + lane;  // tile row: i = rho / 16, c = rho % 16
-        const int il = rho >> 4, cl = rho & 15;
+        const int rho = ((warp - TW0) % TW_W) * 32 + lane;  // tile row (row_ic)
+        int il, cl;
+        row_ic(rho, il, cl);
         const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
         int stage = 0, sidx = 0;
         uint32_t phase = 0;
@@ -299,7 +313,8 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
         const int quad = warp % 4;   // TMEM lanes 32 quad .. + 31
         const int grp = ew / 4;      // column half of the tile
         const int rho = quad * 32 + lane;
-        const int il = rho >> 4, cl = rho & 15;
+        int il, cl;
+        row_ic(rho, il, cl);
         uint8_t* gbase = epi_base + grp * 4 * SLOT;  // [buf][layout][CH][128] floats
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         const int half = bn / 2;
@@ -333,7 +348,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                     named_sync(1 + grp, 128);
 #pragma unroll
                     for (int e = 0; e < CH; ++e) {
-                        sA[e * 128 + rho] = v[e];            // [o''][i][c]
+                        sA[e * 128 + il * 16 + cl] = v[e];  // [o''][i][c]
                         sB[e * 128 + cl * 8 + il] = v[e];    // [o''][c][i]
                     }
                     fence_proxy_async();
