@@ -117,6 +117,20 @@ __device__ __forceinline__ void row_ic(int rho, int& il, int& cl) {
     cl = (rho & 7) + 8 * (w & 1);
 }
 
+// Split TMEM load: issue now, wait later (the wait passes the registers through,
+// so the compiler cannot read them before the data has landed)
+__device__ __forceinline__ void tmem_ld8_issue(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait8(uint32_t (&r)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+                 :
+                 : "memory");
+}
+
 // H row / column of (unit o, abar index x): weight (o, x) or the bias of o
 __device__ __forceinline__ int64_t hidx(const Params& p, int64_t o, int64_t x) {
     return x < p.tk ? p.woff + o * p.tk + x : p.boff + o;
@@ -331,13 +345,19 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
             const int64_t jt0 = (int64_t)tl.z * p.bn;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            for (int jj0 = grp * half; jj0 < (grp + 1) * half; jj0 += CH) {
+            // chunk n + 1's TMEM load is in flight while chunk n is staged and stored
+            const uint32_t tacc = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * (K::ACC_STRIDE ? K::ACC_STRIDE : bn));
+            const int jend = (grp + 1) * half;
+            uint32_t r[CH];
+            if (jt0 + grp * half < p.npairs) tmem_ld8_issue(tacc + (uint32_t)(grp * half), r);
+            for (int jj0 = grp * half; jj0 < jend; jj0 += CH) {
                 const int64_t J0 = jt0 + jj0;
                 if (J0 >= p.npairs) break;  // uniform across the group
                 float v[CH];
-                tmem_ld8(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * (K::ACC_STRIDE ? K::ACC_STRIDE : bn) + jj0), v);
+                tmem_ld_wait8(r);
 #pragma unroll
-                for (int e = 0; e < CH; ++e) v[e] *= p.alpha;
+                for (int e = 0; e < CH; ++e) v[e] = __uint_as_float(r[e]) * p.alpha;
+                if (jj0 + CH < jend && J0 + CH < p.npairs) tmem_ld8_issue(tacc + (uint32_t)(jj0 + CH), r);
                 const int ncol = (int)(p.npairs - J0 < CH ? p.npairs - J0 : CH);
                 if (box_ok) {
                     float* sA = reinterpret_cast<float*>(gbase + (chunk & 1) * 2 * SLOT);
