@@ -174,6 +174,22 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
                          int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
                          void* stream);
 
+/* The same eigenpairs by Chebyshev-filtered subspace iteration: after the
+ * sketch Y = G Omega, filter_steps rounds each apply the degree-filter_degree
+ * Chebyshev polynomial of G that damps [0, theta_l] (theta_l = the smallest
+ * Ritz value of the current basis) and re-orthonormalize (on steep spectra a
+ * round's degree is lowered so that the filtered columns stay within ~2e4 in
+ * scale; the budget of filter_steps x filter_degree operator applications is
+ * kept).  Same outputs and
+ * contract as curvkit_dev_opg_topk; filter_steps x filter_degree operator
+ * applications reach the accuracy of many more power iterations on flat
+ * spectra.  An extension beside the randomized
+ * replacement of curv::opg_eigs_incremental (eigensolve.hpp:80-81). */
+int curvkit_dev_opg_topk_filtered(const curvkit_model* model, const void* params, const void* x,
+                                  const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
+                                  int64_t filter_steps, int64_t filter_degree, uint64_t seed, int32_t precision,
+                                  void* q, void* lambda, void* stream);
+
 /* Row shards for multi-GPU runs (no collective on the data path).  A shard
  * assembles the lower-triangle entries of rows [row_begin, row_end) and their
  * mirrored copies into a full-size output buffer; the shards of

@@ -53,6 +53,7 @@ SIGNATURES = {
     "curvkit_dev_opg_shard": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
     "curvkit_dev_gemm": [i64, i64, i64, vptr, i64, i32, vptr, i64, i32, vptr, i64, C.c_float, i32, vptr],
     "curvkit_dev_opg_topk": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
+    "curvkit_dev_opg_topk_filtered": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
     "curvkit_comm_unique_id": [C.POINTER(C.c_uint8)],
     "curvkit_comm_init": [C.POINTER(C.c_uint8), i32, i32, C.POINTER(vptr)],
     "curvkit_comm_destroy": [vptr],

@@ -958,4 +958,25 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
     });
 }
 
+int curvkit_dev_opg_topk_filtered(const curvkit_model* model, const void* params, const void* x,
+                                  const int32_t* labels, int64_t n, int64_t k, int64_t oversample, int64_t filter_steps,
+                                  int64_t filter_degree, uint64_t seed, int32_t precision, void* q, void* lambda,
+                                  void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk_filtered: empty dataset");
+        if (filter_degree < 1) contract("opg_topk_filtered: filter_degree must be >= 1");
+        cudaStream_t s = dev_stream(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            dev_topk<T>(md, c, k, oversample, 0, seed, precision, (T*)q, (T*)lambda, s, nullptr, filter_steps,
+                        filter_degree);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
 }  // extern "C"

@@ -649,10 +649,31 @@ struct EigenWork {
 // communicator of nranks > 1 each rank holds the parameter rows of
 // TopkShard::make(md, nranks, rank); the only exchanges are all-reduces of
 // the N x l product J X and of the l x l Grams.
+// C <- sc C + sb B + sa A on the first l columns of R rows (one Chebyshev
+// three-term step; A may be null)
+template <class T>
+__global__ void cheb_combine_kernel(T* __restrict__ C, const T* __restrict__ B, const T* __restrict__ A, int64_t rows,
+                                    int64_t ld, int64_t l, T sc, T sb, T sa) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * l; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / l, j = r * ld + (i - r * l);
+        T v = sc * C[j] + sb * B[j];
+        if (A) v += sa * A[j];
+        C[j] = v;
+    }
+}
+
+// Filter: cheb_degree > 0 replaces the power iterations by cheb_steps rounds of
+// Chebyshev-filtered subspace iteration (power_iters is then unused).  Each
+// round takes the smallest Ritz value theta_l of the current basis as the
+// upper end b of the damped interval [0, b] (G is PSD) and applies
+// T_d((2 G - b) / b) by the three-term recurrence, d = cheb_degree operator
+// applications; eigenvalues above b grow like cosh(d acosh(2 lambda / b - 1)),
+// against (lambda / lambda')^d for d power iterations.
 template <class T>
 void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
                uint64_t seed, int prec, T* q_dev, std::vector<double>& lam_host, cudaStream_t s,
-               const Comm* comm = nullptr, const T* Jext = nullptr, int64_t ldj_ext = 0) {
+               const Comm* comm = nullptr, const T* Jext = nullptr, int64_t ldj_ext = 0, int64_t cheb_steps = 0,
+               int64_t cheb_degree = 0) {
     const int64_t n = c.n, P = md.P;
     const bool sharded = comm && comm->nranks > 1;
     const TopkShard sh = TopkShard::make(md, sharded ? comm->nranks : 1, sharded ? comm->rank : 0);
@@ -660,6 +681,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     if (k < 1 || k > std::min(n, P))
         throw CurvError(kContractError, "opg_topk: need 1 <= k <= min(N, P), got k = " + std::to_string(k));
     if (oversample < 0 || power_iters < 0) throw CurvError(kContractError, "opg_topk: negative oversample/power_iters");
+    if (cheb_steps < 0 || cheb_degree < 0) throw CurvError(kContractError, "opg_topk: negative filter steps/degree");
     const int64_t l = std::min(k + oversample, P);
     const int64_t ldl = round_up(l, 32);
     // TF32: J X and J^T T straight from the activations and deltas (kr.cuh);
@@ -693,39 +715,98 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         }
     }
     EigenWork<T> ew{md, s, prec, &c, krop.get(), sh, sharded ? comm : nullptr};
+    // Rayleigh-Ritz on the orthonormal basis X: B = (1/N) (J X)^T (J X) with
+    // round-to-nearest TF32 operands (J stored rounded, X rounded per GEMM):
+    // unbiased products.  Leaves the Ritz values on B's diagonal (ha) and the
+    // vectors in hv (both l x l, host).
+    DevMem Bm((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
+    std::vector<double> ha(l * l), hv(l * l);
+    auto ritz = [&](const T* X) {
+        ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+        ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l, 0.0);
+        CK_CUDA(cudaMemsetAsync(Bm.p, 0, l * l * sizeof(double), s));
+        {
+            const int64_t ksplit = std::min<int64_t>(256, std::max<int64_t>(1, n / 2048));
+            dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
+            gram_kernel<T><<<g, 256, 0, s>>>(dptr<T>(Tn), ldl, n, l, ceil_div(n, ksplit), dptr<double>(Bm));
+            CK_LAUNCH();
+        }
+        ProfScope pj("eig_ritz_eig", s, 0.0, 0.0);
+        std::vector<double> hb(l * l);
+        CK_CUDA(cudaMemcpyAsync(hb.data(), Bm.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaStreamSynchronize(s));
+        for (auto& v : hb) v /= (double)n;
+        CK_CUDA(cudaMemcpyAsync(Bm.p, hb.data(), l * l * sizeof(double), cudaMemcpyHostToDevice, s));
+        DevMem sw(sizeof(int), s);
+        jacobi_eig(dptr<double>(Bm), dptr<double>(V), l, dptr<int>(sw), s, std::is_same_v<T, float>);
+        CK_CUDA(cudaMemcpyAsync(ha.data(), Bm.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaMemcpyAsync(hv.data(), V.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+        int sweeps = 0;
+        CK_CUDA(cudaMemcpyAsync(&sweeps, sw.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaStreamSynchronize(s));
+        if (getenv("CURVKIT_TRACE"))
+            fprintf(stderr, "[curvkit] Rayleigh-Ritz Jacobi: l = %lld, %d sweeps\n", (long long)l, sweeps);
+    };
     T* X = dptr<T>(Om);
-    for (int64_t it = 0; it <= power_iters; ++it) {
+    if (cheb_degree == 0) {
+        for (int64_t it = 0; it <= power_iters; ++it) {
+            ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
+            ew.apply_jt(Jp, ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
+            X = ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl, it < power_iters ? 1 : 2);
+        }
+    } else {
         ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
         ew.apply_jt(Jp, ldj, n, dptr<T>(Tn), ldl, l, dptr<T>(Y), ldl);
-        X = ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl, it < power_iters ? 1 : 2);
+        X = ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl, 2);  // -> Y
+        T* bufs[3] = {dptr<T>(Y), dptr<T>(Om), dptr<T>(Y2)};
+        const int64_t budget = cheb_steps * cheb_degree;  // operator applications
+        for (int64_t used = 0; used < budget;) {
+            ritz(X);
+            double b = INFINITY, top = 0.0;
+            for (int64_t j = 0; j < l; ++j) {
+                b = std::min(b, ha[j * l + j]);
+                top = std::max(top, ha[j * l + j]);
+            }
+            if (!(b > 0.0)) break;  // basis already spans G's range (rank < l)
+            // the filter grows the top Ritz direction by T_d(2 top / b - 1) against <= 1
+            // on [0, b]: keep that range within ~2e4 (fp32 basis, CholeskyQR2) by
+            // lowering this round's degree on steep spectra (degree 1 = a shifted
+            // power step); the application budget stays steps x degree
+            int64_t deg = cheb_degree;
+            const double x1 = 2.0 * top / b - 1.0;
+            if (x1 > 1.0) deg = std::clamp<int64_t>((int64_t)std::floor(9.9 / std::acosh(x1)), 1, cheb_degree);
+            deg = std::min(deg, budget - used);
+            used += deg;
+            const double e = b / 2.0, cc = b / 2.0;  // [0, b] -> [-1, 1]
+            ProfScope pf("eig_cheb_filter", s, 0.0, 0.0);
+            T* Bp = X;
+            T* Ap = nullptr;
+            int free_idx[2], nf = 0;
+            for (T* q : bufs)
+                if (q != X) free_idx[nf++] = (int)(std::find(bufs, bufs + 3, q) - bufs);
+            T* Cp = bufs[free_idx[0]];
+            T* Dp = bufs[free_idx[1]];  // the third buffer
+            for (int64_t d = 1; d <= deg; ++d) {
+                ew.apply_j(Jp, ldj, n, Bp, ldl, l, dptr<T>(Tn), ldl);
+                ew.apply_jt(Jp, ldj, n, dptr<T>(Tn), ldl, l, Cp, ldl);  // C = J^T J B = N G B
+                const double sc = (d == 1 ? 1.0 : 2.0) / (e * (double)n), sb = -(d == 1 ? 1.0 : 2.0) * cc / e;
+                if (R > 0) {
+                    cheb_combine_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(R * l, 256), 148 * 32), 256, 0, s>>>(
+                        Cp, Bp, d == 1 ? nullptr : Ap, R, ldl, l, (T)sc, (T)sb, (T)-1.0);
+                    CK_LAUNCH();
+                }
+                // rotate (A, B, C) <- (B, C, A or the third buffer)
+                T* nextC = d == 1 ? Dp : Ap;
+                Ap = Bp;
+                Bp = Cp;
+                Cp = nextC;
+            }
+            pf.end();
+            T* scratch = Ap;  // free after the last step
+            X = ew.orth(Bp, scratch, R, l, ldl, 2);  // 2 passes: the filtered columns differ in scale
+        }
     }
-    // Rayleigh-Ritz: B = (1/N) (J Q)^T (J Q) with round-to-nearest TF32
-    // operands (J stored rounded, Q rounded per GEMM): unbiased products.
-    ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
-    ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l + 2.0 * (double)R * l * k, 0.0);
-    DevMem B((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
-    CK_CUDA(cudaMemsetAsync(B.p, 0, l * l * sizeof(double), s));
-    {
-        const int64_t ksplit = std::min<int64_t>(256, std::max<int64_t>(1, n / 2048));
-        dim3 g((unsigned)ceil_div(l, 32), (unsigned)ceil_div(l, 32), (unsigned)ksplit);
-        gram_kernel<T><<<g, 256, 0, s>>>(dptr<T>(Tn), ldl, n, l, ceil_div(n, ksplit), dptr<double>(B));
-        CK_LAUNCH();
-    }
-    ProfScope pj("eig_ritz_eig", s, 0.0, 0.0);
-    std::vector<double> hb(l * l);
-    CK_CUDA(cudaMemcpyAsync(hb.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK_CUDA(cudaStreamSynchronize(s));
-    for (auto& v : hb) v /= (double)n;
-    CK_CUDA(cudaMemcpyAsync(B.p, hb.data(), l * l * sizeof(double), cudaMemcpyHostToDevice, s));
-    DevMem sw(sizeof(int), s);
-    jacobi_eig(dptr<double>(B), dptr<double>(V), l, dptr<int>(sw), s, std::is_same_v<T, float>);
-    std::vector<double> ha(l * l), hv(l * l);
-    CK_CUDA(cudaMemcpyAsync(ha.data(), B.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK_CUDA(cudaMemcpyAsync(hv.data(), V.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
-    int sweeps = 0;
-    CK_CUDA(cudaMemcpyAsync(&sweeps, sw.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK_CUDA(cudaStreamSynchronize(s));
-    if (getenv("CURVKIT_TRACE")) fprintf(stderr, "[curvkit] Rayleigh-Ritz Jacobi: l = %lld, %d sweeps\n", (long long)l, sweeps);
+    ritz(X);
     std::vector<int64_t> ord(l);
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return ha[a * l + a] > ha[b * l + b]; });
@@ -735,7 +816,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         lam_host[j] = ha[ord[j] * l + ord[j]];
         for (int64_t r = 0; r < l; ++r) vk[r * k + j] = (T)hv[r * l + ord[j]];
     }
-    pj.end();
+    ProfScope pr("eig_ritz", s, 2.0 * (double)R * l * k, 0.0);
     DevMem Vk((size_t)l * k * sizeof(T), s);
     CK_CUDA(cudaMemcpyAsync(Vk.p, vk.data(), l * k * sizeof(T), cudaMemcpyHostToDevice, s));
     EpiStore<T> e{q_dev, k, 0, T(1), T(0)};
@@ -758,9 +839,11 @@ void host_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
 
 template <class T>
 void dev_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
-              uint64_t seed, int prec, T* q_dev, T* lam_dev, cudaStream_t s, const Comm* comm = nullptr) {
+              uint64_t seed, int prec, T* q_dev, T* lam_dev, cudaStream_t s, const Comm* comm = nullptr,
+              int64_t cheb_steps = 0, int64_t cheb_degree = 0) {
     std::vector<double> lam;
-    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s, comm);
+    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s, comm, nullptr, 0, cheb_steps,
+                 cheb_degree);
     std::vector<T> hl(lam.begin(), lam.end());
     CK_CUDA(cudaMemcpyAsync(lam_dev, hl.data(), k * sizeof(T), cudaMemcpyHostToDevice, s));
     CK_CUDA(cudaStreamSynchronize(s));

@@ -523,6 +523,15 @@ def dev_opg_topk(spec, params, x, labels, n, k, oversample, power_iters, seed, q
                                                  _stream(stream)))
 
 
+def dev_opg_topk_filtered(spec, params, x, labels, n, k, oversample, filter_steps, filter_degree, seed, q, lam,
+                          precision="tf32", stream=None):
+    """Top-k of G by Chebyshev-filtered subspace iteration (curvkit_dev_opg_topk_filtered):
+    filter_steps rounds of a degree-filter_degree filter instead of power iterations."""
+    _lib.check(_lib.load().curvkit_dev_opg_topk_filtered(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
+                                                          k, oversample, filter_steps, filter_degree, seed,
+                                                          _prec(precision), _ptr(q), _ptr(lam), _stream(stream)))
+
+
 def launch_count() -> int:
     return int(_lib.load().curvkit_launch_count())
 

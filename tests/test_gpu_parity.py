@@ -351,6 +351,16 @@ def test_config4_topk_against_exact_spectrum():
         torch.cuda.synchronize()
         lams[it] = lam.double().cpu().numpy()
         del q
+    # Chebyshev-filtered subspace iteration: 3 rounds of degree 6 (18 operator
+    # applications instead of 64 power iterations)
+    q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
+    lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
+    curv.dev_opg_topk_filtered(spec, p, x, lab, n, k, wl.oversample, 3, 6, 7, q, lam, precision="tf32")
+    torch.cuda.synchronize()
+    lams["cheb3x6"] = lam.double().cpu().numpy()
+    qtq = (q.T @ q).double().cpu().numpy()
+    assert np.abs(qtq - np.eye(k)).max() <= 1e-4
+    del q
     old = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     try:
@@ -375,6 +385,37 @@ def test_config4_topk_against_exact_spectrum():
     e64 = np.abs(lams[64] - ev) / ev
     assert np.all(e64 <= e2 + 1e-4)                                # more iterations, closer
     assert e64.max() <= 1e-3, (e64.max(), int(e64.argmax()))       # the north_star's bar, all 100
+    ec = np.abs(lams["cheb3x6"] - ev) / ev
+    assert ec.max() <= 1e-3, (ec.max(), int(ec.argmax()))         # the same bar from 18 applications
+
+
+@pytest.mark.parametrize("prec", ["f64", "tf32"])
+def test_filtered_topk_matches_dense_eig(prec):
+    """Chebyshev-filtered top-k (curvkit_dev_opg_topk_filtered) against the
+    dense eigendecomposition of the reference's config-0 G."""
+    torch = pytest.importorskip("torch")
+    g = load_golden("config0")
+    spec = spec_of(g)
+    dt = torch.float64 if prec == "f64" else torch.float32
+    dev = "cuda:0"
+    P, n, k = g["G"].shape[0], g["x"].shape[0], 5
+    p = torch.tensor(g["params"], dtype=dt, device=dev)
+    x = torch.tensor(g["x"], dtype=dt, device=dev)
+    lab = torch.tensor(np.argmax(g["y"], axis=1), dtype=torch.int32, device=dev)
+    qd = torch.empty((P, k), dtype=dt, device=dev)
+    lamd = torch.empty(k, dtype=dt, device=dev)
+    curv.dev_opg_topk_filtered(spec, p, x, lab, n, k, 10, 2, 4, 3, qd, lamd, precision=prec)
+    torch.cuda.synchronize()
+    lam = lamd.double().cpu().numpy()
+    q = qd.double().cpu().numpy()
+    w = np.linalg.eigvalsh(g["G"])[::-1]
+    assert np.all(np.abs(lam - w[:k]) <= 1e-3 * np.abs(w[:k])), (lam, w[:k])
+    assert np.all(np.diff(lam) <= 0)
+    assert np.abs(q.T @ q - np.eye(k)).max() <= (1e-8 if prec == "f64" else 1e-4)
+    r = g["G"] @ q - q * lam
+    assert np.linalg.norm(r) <= 1e-3 * np.linalg.norm(g["G"])
+    with pytest.raises(curv.ContractError):
+        curv.dev_opg_topk_filtered(spec, p, x, lab, n, k, 10, 2, 0, 3, qd, lamd, precision=prec)
 
 
 @pytest.mark.parametrize("prec", ["tf32", "f64"])

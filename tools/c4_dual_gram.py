@@ -3,7 +3,8 @@ N = 20 000): the top-k eigenvalues of G = (1/N) J^T J from the device
 randomized range finder against the exact nonzero spectrum of G, taken from
 the dual Gram K = (1/N) J J^T (20 000 x 20 000; FP32 SGEMM without TF32, fp64
 eigvalsh).  J (84 GB fp32) is formed only for this check.
-    python tools/c4_dual_gram.py [power_iters[:oversample] ...]"""
+    python tools/c4_dual_gram.py [power_iters[:oversample] | f:steps:degree[:oversample] ...]
+(f: Chebyshev-filtered subspace iteration, curvkit_dev_opg_topk_filtered)"""
 import sys, time, json
 import numpy as np
 import torch
@@ -20,18 +21,27 @@ xx = torch.tensor(x, dtype=torch.float32, device=dev)
 ll = torch.tensor(lab, dtype=torch.int32, device=dev)
 spec = curv.ModelSpec(wl.widths, wl.activation)
 P, n, k = wl.P, wl.n, wl.eig_k
-runs = [tuple(int(v) for v in a.split(":")) for a in sys.argv[1:]] or [(wl.power_iters,)]
+runs = sys.argv[1:] or [str(wl.power_iters)]
 lams = {}
-for r in runs:
-    it, ov = r[0], (r[1] if len(r) > 1 else wl.oversample)
+for a in runs:
+    f = a.startswith("f:")
+    r = [int(v) for v in (a[2:] if f else a).split(":")]
     q = torch.empty((P, k), dtype=torch.float32, device=dev)
     lam = torch.empty(k, dtype=torch.float32, device=dev)
-    curv.dev_opg_topk(spec, p, xx, ll, n, k, ov, it, 7, q, lam, precision="tf32")
+    if f:
+        st, deg, ov = r[0], r[1], (r[2] if len(r) > 2 else wl.oversample)
+        call = lambda: curv.dev_opg_topk_filtered(spec, p, xx, ll, n, k, ov, st, deg, 7, q, lam, precision="tf32")
+        key = f"filtered {st}x{deg}:{ov}"
+    else:
+        it, ov = r[0], (r[1] if len(r) > 1 else wl.oversample)
+        call = lambda: curv.dev_opg_topk(spec, p, xx, ll, n, k, ov, it, 7, q, lam, precision="tf32")
+        key = f"power {it}:{ov}"
+    call()
     torch.cuda.synchronize()
     t0 = time.time()
-    curv.dev_opg_topk(spec, p, xx, ll, n, k, ov, it, 7, q, lam, precision="tf32")
+    call()
     torch.cuda.synchronize()
-    lams[f"{it}:{ov}"] = (lam.double().cpu().numpy(), time.time() - t0)
+    lams[key] = (lam.double().cpu().numpy(), time.time() - t0)
     del q
 t = time.time()
 ldj = (P + 31) // 32 * 32
@@ -49,7 +59,7 @@ print(f"dual Gram + eigvalsh: {time.time() - t:.1f} s")
 out = {"lambda_exact_top10": ev[:10].tolist(), "lambda_exact_k": float(ev[k - 1])}
 for key, (l, secs) in lams.items():
     rel = np.abs(l - ev) / ev
-    out[f"power_iters:oversample={key}"] = {"seconds": round(secs, 3),"max_rel_err_top10": float(rel[:10].max()), "max_rel_err_top50": float(rel[:50].max()),
+    out[key] = {"seconds": round(secs, 3),"max_rel_err_top10": float(rel[:10].max()), "max_rel_err_top50": float(rel[:50].max()),
                                 "max_rel_err_all": float(rel.max()), "median_rel_err": float(np.median(rel)),
                                 "n_within_1e-3": int((rel <= 1e-3).sum())}
 print(json.dumps(out, indent=1))
