@@ -473,6 +473,12 @@ struct Engine {
                 CK_CUDA(cudaMemsetAsync(keep.back().p, 0, (size_t)rows * ld * sizeof(T), s));
                 return dptr<T>(keep.back());
             };
+            // for the n-contiguous copies below: transpose, replicate_rows and qext
+            // write every element of their rows, the padding included (zeros)
+            auto buf_full = [&](int64_t rows, int64_t ld) {
+                keep.emplace_back((size_t)rows * ld * sizeof(T), s);
+                return dptr<T>(keep.back());
+            };
             ProfScope prof_stage("hess_profiles", s, 0.0, 0.0);
             T* G = buf(np * n, c.ldt[k]);
             T* rzp[kMaxLayers] = {};
@@ -541,19 +547,19 @@ struct Engine {
             // a 32-multiple pitch keeps every K-block of 32 examples inside a row
             const int64_t ldn = round_up(n, 32);
             const int64_t tk = md.w[k];
-            T* akT = buf(tk + 1, ldn);
+            T* akT = buf_full(tk + 1, ldn);
             transpose<T>(s, c.a[k], c.lda[k], 0, akT, ldn, 0, n, tk + 1, 1);
-            T* dkT = buf(np, ldn);
+            T* dkT = buf_full(np, ldn);
             transpose<T>(s, c.delta[k], c.ldt[k], 0, dkT, ldn, 0, n, np, 1);
-            T* GT = buf(np * np, ldn);
+            T* GT = buf_full(np * np, ldn);
             transpose<T>(s, G, c.ldt[k], n * c.ldt[k], GT, ldn, np * ldn, n, np, np);
             T* PT[kMaxLayers] = {};
             T* QT[kMaxLayers] = {};
             for (int m = k - 1; m >= 0; --m) {
                 const int64_t tm1 = md.w[m + 1];
-                PT[m] = buf(np * tm1, ldn);
+                PT[m] = buf_full(np * tm1, ldn);
                 transpose<T>(s, Pm[m], c.ldt[m], n * c.ldt[m], PT[m], ldn, tm1 * ldn, n, tm1, np);
-                QT[m] = buf(tk * tm1, ldn);
+                QT[m] = buf_full(tk * tm1, ldn);
                 transpose<T>(s, Qm[m], c.ldt[m], n * c.ldt[m], QT[m], ldn, tm1 * ldn, n, tm1, tk);
             }
             // Extended copies for the fused TF32 kernel: a 128-row activation
@@ -562,19 +568,22 @@ struct Engine {
             const int64_t ak_rows = tk + 256;
             T* akX = nullptr;
             T* QX[kMaxLayers] = {};
-            if (fused) {
-                akX = buf(ak_rows, ldn);
+            // built before the block loop when a fused block is certain (m < k, or a
+            // diagonal block without the symmetric kernel), else on first use
+            auto build_ext = [&]() {
+                akX = buf_full(ak_rows, ldn);
                 replicate_rows_kernel<T><<<dim3(blocks_for(ak_rows * ldn), 1), 256, 0, s>>>(akT, tk, ldn, akX, ak_rows, 0, 0);
                 CK_LAUNCH();
                 for (int m = k - 1; m >= 0; --m) {
                     const int64_t tm1 = md.w[m + 1];
-                    QX[m] = buf(tm1 * ak_rows, ldn);
+                    QX[m] = buf_full(tm1 * ak_rows, ldn);
                     // QT[m] is [i][o''][n]; QX[m] is [o''][r][n] with r -> i = r mod T_k
                     qext_kernel<T><<<dim3(blocks_for(ak_rows * ldn / 4), (unsigned)tm1), 256, 0, s>>>(
                         QT[m], tk, tm1, ldn, QX[m], ak_rows);
                     CK_LAUNCH();
                 }
-            }
+            };
+            if (fused && (k > 0 || verify || sym_off())) build_ext();
             prep_stage.end();
             // blocks (k, m), m <= k
             const int64_t Pk = md.block_size(k);
@@ -605,6 +614,7 @@ struct Engine {
                     jbeg = Pk;
                 }
                 if (fused && jbeg < Pk) {
+                    if (!akX) build_ext();
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                     HessFusedArgs<T> fa{akX, ak_rows, m == k ? nullptr : QX[m], ak_rows, tm1 * ak_rows,
                                         m == k ? GT : PT[m], dkT, c.a[m], c.lda[m], ldn, n, tk, tm, tm1, nw,
