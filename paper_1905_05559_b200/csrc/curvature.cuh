@@ -468,9 +468,10 @@ struct Engine {
             const int64_t np = md.w[k + 1];
             if (md.woff[k] + md.block_size(k) <= rlo || md.woff[k] >= rhi) continue;
             std::vector<DevMem> keep;
+            // R-op profile buffers: every kernel below writes its output's logical
+            // extent and reads only logical extents (checked with CURVKIT_POISON)
             auto buf = [&](int64_t rows, int64_t ld) {
                 keep.emplace_back((size_t)rows * ld * sizeof(T), s);
-                CK_CUDA(cudaMemsetAsync(keep.back().p, 0, (size_t)rows * ld * sizeof(T), s));
                 return dptr<T>(keep.back());
             };
             // for the n-contiguous copies below: transpose, replicate_rows and qext

@@ -31,6 +31,10 @@ struct DevMem {
     DevMem() = default;
     DevMem(size_t b, cudaStream_t st) : bytes(b), s(st) {
         if (b) CK_CUDA(cudaMallocAsync(&p, b, st));
+        // dev check (CURVKIT_POISON=1): new buffers start as NaN bytes, so a read of
+        // anything no kernel or memset wrote shows up in the parity tests
+        static const bool poison = getenv("CURVKIT_POISON") != nullptr;
+        if (b && poison) CK_CUDA(cudaMemsetAsync(p, 0xFF, b, st));
     }
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
