@@ -350,9 +350,10 @@ struct Engine {
         const int S = md.S;
         const int64_t n = c.n, ldn = round_up(n, 32);
         std::vector<DevMem> keep;
+        // every buffer here is written in full, padding included (transposes pad
+        // with zeros; replicate_rows and outer_delta copy or multiply whole rows)
         auto buf = [&](int64_t rows, int64_t ld) {
             keep.emplace_back((size_t)rows * ld * sizeof(T), s);
-            CK_CUDA(cudaMemsetAsync(keep.back().p, 0, (size_t)rows * ld * sizeof(T), s));
             return dptr<T>(keep.back());
         };
         T* akT[kMaxLayers] = {};
