@@ -228,6 +228,13 @@ int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params,
                                  const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
                                  int64_t power_iters, uint64_t seed, int32_t precision, void* q, void* lambda,
                                  void* stream, curvkit_comm comm);
+/* curvkit_dev_opg_topk_sharded with the Chebyshev filter of
+ * curvkit_dev_opg_topk_filtered (same exchanges: all-reduces of J X and of
+ * the l x l Grams; the recurrence itself is row-local). */
+int curvkit_dev_opg_topk_sharded_filtered(const curvkit_model* model, const void* params, const void* x,
+                                          const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
+                                          int64_t filter_steps, int64_t filter_degree, uint64_t seed,
+                                          int32_t precision, void* q, void* lambda, void* stream, curvkit_comm comm);
 
 /* Matrix-free Jacobian operator on a parameter-row range (TF32, J never
  * formed): transpose = 0: out (n x l) = J[:, p_begin:p_end] in, with in the

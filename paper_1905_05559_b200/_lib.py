@@ -59,6 +59,8 @@ SIGNATURES = {
     "curvkit_comm_destroy": [vptr],
     "curvkit_topk_shard_rows": [_MP, i64, i64, C.POINTER(i64), C.POINTER(i64)],
     "curvkit_dev_opg_topk_sharded": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr, vptr],
+    "curvkit_dev_opg_topk_sharded_filtered": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr,
+                                              vptr],
     "curvkit_dev_jacobian_apply": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, i32, vptr, i64, i64, vptr, i64, vptr],
     "curvkit_forward": [_MP, dptr, dptr, i64, i32, dptr],
     "curvkit_cost": [_MP, dptr, dptr, dptr, i64, i32, dptr],

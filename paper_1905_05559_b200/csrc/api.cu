@@ -892,6 +892,24 @@ int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params,
     });
 }
 
+int curvkit_dev_opg_topk_sharded_filtered(const curvkit_model* model, const void* params, const void* x,
+                                          const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
+                                          int64_t filter_steps, int64_t filter_degree, uint64_t seed,
+                                          int32_t precision, void* q, void* lambda, void* stream, curvkit_comm comm) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk: empty dataset");
+        if (!comm) contract("opg_topk_sharded: null communicator");
+        if (filter_degree < 1) contract("opg_topk_filtered: filter_degree must be >= 1");
+        cudaStream_t s = dev_stream(stream);
+        if (precision != kTF32) contract("sharded opg_topk needs TF32 precision");
+        Cache<float> c;
+        forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
+        dev_topk<float>(md, c, k, oversample, 0, seed, precision, (float*)q, (float*)lambda, s, &comm->c, filter_steps,
+                        filter_degree);
+    });
+}
+
 int curvkit_opg_topk_from_jacobian(const double* j, int64_t n, int64_t p, int64_t k, int64_t oversample,
                                    int64_t power_iters, uint64_t seed, int32_t precision, double* q_out,
                                    double* lambda_out) {

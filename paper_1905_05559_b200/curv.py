@@ -622,6 +622,14 @@ def dev_opg_topk_sharded(spec, params, x, labels, n, k, oversample, power_iters,
                                                          _ptr(lam), _stream(stream), comm.handle))
 
 
+def dev_opg_topk_sharded_filtered(spec, params, x, labels, n, k, oversample, filter_steps, filter_degree, seed, q, lam,
+                                  comm: Comm, precision="tf32", stream=None):
+    """dev_opg_topk_sharded with the Chebyshev filter of dev_opg_topk_filtered."""
+    _lib.check(_lib.load().curvkit_dev_opg_topk_sharded_filtered(
+        C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n, k, oversample, filter_steps, filter_degree, seed,
+        _prec(precision), _ptr(q), _ptr(lam), _stream(stream), comm.handle))
+
+
 def dev_jacobian_apply(spec, params, x, labels, n, p_begin, p_end, inp, ld_in, l, out, ld_out, transpose=False,
                        precision="tf32", stream=None):
     """Matrix-free J[:, p_begin:p_end] @ inp (transpose=False) or its

@@ -76,6 +76,44 @@ def _sharded_range_finder(J, rows, k, l, iters, seed, allreduce):
     return lam
 
 
+def _cholqr2(y, allreduce):
+    for _ in range(2):                 # CholeskyQR2: Gram all-reduced, rows local
+        w = allreduce(y.T @ y)
+        r = np.linalg.cholesky(w).T
+        y = np.linalg.solve(r.T, y.T).T
+    return y
+
+
+def _sharded_filtered(J, rows, k, l, steps, degree, seed, allreduce):
+    """The Chebyshev-filtered solver's exchange pattern (eigen.cuh topk_core,
+    cheb_degree > 0): sketch, then rounds of Ritz values (all-reduced J X),
+    a row-local three-term recurrence on [0, theta_l], CholeskyQR2."""
+    n, P = J.shape
+    b, e = rows
+    Jr = J[:, b:e]
+    x = _cholqr2(Jr.T @ allreduce(Jr @ np.random.default_rng(seed).standard_normal((P, l))[b:e]), allreduce)
+    used = 0
+    while used < steps * degree:
+        t = allreduce(Jr @ x)
+        th = np.linalg.eigvalsh(t.T @ t / n)
+        lo, top = th.min(), th.max()
+        deg = degree
+        if 2 * top / lo - 1 > 1:
+            deg = int(np.clip(np.floor(9.9 / np.arccosh(2 * top / lo - 1)), 1, degree))
+        deg = min(deg, steps * degree - used)
+        used += deg
+        c = e_ = lo / 2
+        a, bb = None, x
+        for d in range(1, deg + 1):
+            cc = Jr.T @ allreduce(Jr @ bb)          # N G B, local rows
+            f = 1.0 if d == 1 else 2.0
+            nxt = f / (e_ * n) * cc - f * c / e_ * bb - (a if d > 1 else 0.0)
+            a, bb = bb, nxt
+        x = _cholqr2(bb, allreduce)
+    t = allreduce(Jr @ x)
+    return np.linalg.eigvalsh(t.T @ t / n)[::-1][:k]
+
+
 def _gloo_topk_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
@@ -101,8 +139,11 @@ def _gloo_topk_worker(rank, world, port, q):
     rows = curv.topk_shard_rows(spec, world, rank)
     lam = _sharded_range_finder(J, rows, 4, 10, 2, 11, allreduce)
     full = _sharded_range_finder(J, (0, J.shape[1]), 4, 10, 2, 11, lambda a: a)
+    flam = _sharded_filtered(J, rows, 4, 10, 2, 3, 11, allreduce)
+    ffull = _sharded_filtered(J, (0, J.shape[1]), 4, 10, 2, 3, 11, lambda a: a)
     if rank == 0:
-        q.put((lam.tolist(), full.tolist(), rows))
+        exact = np.linalg.eigvalsh(J.T @ J / n)[::-1][:4]
+        q.put((lam.tolist(), full.tolist(), rows, flam.tolist(), ffull.tolist(), exact.tolist()))
     dist.destroy_process_group()
 
 
@@ -114,12 +155,14 @@ def test_gloo_two_ranks_sharded_range_finder():
     procs = [ctx.Process(target=_gloo_topk_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    lam, full, rows = q.get(timeout=180)
+    lam, full, rows, flam, ffull, exact = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert 0 < rows[1]
     np.testing.assert_allclose(lam, full, rtol=1e-10)
+    np.testing.assert_allclose(flam, ffull, rtol=1e-10)     # filtered: sharded == unsharded
+    np.testing.assert_allclose(ffull, exact, rtol=1e-6)     # and converged (6 applications)
 
 
 # ---- GPU -------------------------------------------------------------------
@@ -185,6 +228,26 @@ def test_sharded_entry_one_rank_equals_unsharded():
         q1 = torch.empty((wl.P, k), device="cuda:0")
         l1 = torch.empty(k, device="cuda:0")
         curv.dev_opg_topk_sharded(spec, p32, x32, lab, wl.n, k, 10, 2, 3, q1, l1, comm)
+    finally:
+        comm.close()
+    torch.cuda.synchronize()
+    assert torch.equal(l0, l1) and torch.equal(q0, q1)
+
+
+@pytest.mark.gpu
+def test_sharded_filtered_one_rank_equals_unsharded():
+    torch = pytest.importorskip("torch")
+    wl, spec, (p64, x64), lab = _c1(torch)
+    p32, x32 = p64.float(), x64.float()
+    k = 12
+    q0 = torch.empty((wl.P, k), device="cuda:0")
+    l0 = torch.empty(k, device="cuda:0")
+    curv.dev_opg_topk_filtered(spec, p32, x32, lab, wl.n, k, 10, 2, 3, 3, q0, l0)
+    comm = curv.Comm.create(0, 1, lambda b: b)
+    try:
+        q1 = torch.empty((wl.P, k), device="cuda:0")
+        l1 = torch.empty(k, device="cuda:0")
+        curv.dev_opg_topk_sharded_filtered(spec, p32, x32, lab, wl.n, k, 10, 2, 3, 3, q1, l1, comm)
     finally:
         comm.close()
     torch.cuda.synchronize()
