@@ -190,7 +190,7 @@ __global__ void finalize_kernel(const T* __restrict__ ws, int64_t splits, int64_
 template <class T, class Epi>
 void model_gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<T> A, Opnd<T> B, const Epi& e) {
     const int64_t tiles = ceil_div(M, 64) * ceil_div(N, 64);
-    int64_t splits = std::min<int64_t>(ceil_div(2 * 148, tiles), K / 64);
+    int64_t splits = std::min<int64_t>(ceil_div(2 * 148, tiles), K / 32);
     if (splits < 2) {
         gemm_simt<T>(s, M, N, K, 1, A, B, e);
         return;
