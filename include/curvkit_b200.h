@@ -144,6 +144,12 @@ int curvkit_opg_topk(const curvkit_model* model, const double* params, const dou
                      const double* y, int64_t n, int64_t k, int64_t oversample, int64_t power_iters,
                      uint64_t seed, int32_t precision, double* q_out, double* lambda_out);
 
+/* The same eigenpairs by Chebyshev-filtered subspace iteration
+ * (curvkit_dev_opg_topk_filtered) through host buffers. */
+int curvkit_opg_topk_filtered(const curvkit_model* model, const double* params, const double* x, const double* y,
+                              int64_t n, int64_t k, int64_t oversample, int64_t filter_steps, int64_t filter_degree,
+                              uint64_t seed, int32_t precision, double* q_out, double* lambda_out);
+
 /* The same eigenpairs from a caller's per-example gradients, the input of
  * curv::opg_eigs_incremental (eigensolve.hpp:80-81): j is n x p row-major
  * (the row blocks stacked), G = (1/n) J^T J; q_out p x k, lambda_out k

@@ -45,6 +45,7 @@ SIGNATURES = {
     "curvkit_assemble_hessian_f32": [_MP, dptr, dptr, dptr, i64, _CP, i32, fptr],
     "curvkit_assemble_opg_f32": [_MP, dptr, dptr, dptr, i64, _CP, i32, fptr],
     "curvkit_opg_topk": [_MP, dptr, dptr, dptr, i64, i64, i64, i64, u64, i32, dptr, dptr],
+    "curvkit_opg_topk_filtered": [_MP, dptr, dptr, dptr, i64, i64, i64, i64, i64, u64, i32, dptr, dptr],
     "curvkit_dev_assemble_hessian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_opg": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_jacobian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],

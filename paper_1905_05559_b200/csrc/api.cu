@@ -683,6 +683,29 @@ int curvkit_opg_topk(const curvkit_model* model, const double* params, const dou
     });
 }
 
+int curvkit_opg_topk_filtered(const curvkit_model* model, const double* params, const double* x, const double* y,
+                              int64_t n, int64_t k, int64_t oversample, int64_t filter_steps, int64_t filter_degree,
+                              uint64_t seed, int32_t precision, double* q_out, double* lambda_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk_filtered: empty dataset");
+        if (filter_degree < 1) contract("opg_topk_filtered: filter_degree must be >= 1");
+        auto lab = labels_from_onehot(md, y, n);
+        cudaStream_t s = lib_stream();
+        if (is_f64(precision)) {
+            Resident<double> r;
+            upload_and_forward<double>(md, params, x, lab, n, r, s);
+            host_topk<double>(md, r.cache, k, oversample, 0, seed, precision, q_out, lambda_out, s, filter_steps,
+                              filter_degree);
+        } else {
+            Resident<float> r;
+            upload_and_forward<float>(md, params, x, lab, n, r, s);
+            host_topk<float>(md, r.cache, k, oversample, 0, seed, precision, q_out, lambda_out, s, filter_steps,
+                             filter_degree);
+        }
+    });
+}
+
 // ---- device entry points -----------------------------------------------------
 int curvkit_dev_assemble_hessian(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
                                  int64_t n, int32_t precision, void* h, int64_t ldh, void* stream) {

@@ -826,10 +826,12 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
 
 template <class T>
 void host_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
-               uint64_t seed, int prec, double* q_out, double* lambda_out, cudaStream_t s) {
+               uint64_t seed, int prec, double* q_out, double* lambda_out, cudaStream_t s, int64_t cheb_steps = 0,
+               int64_t cheb_degree = 0) {
     DevMem q((size_t)md.P * k * sizeof(T), s);
     std::vector<double> lam;
-    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, dptr<T>(q), lam, s);
+    topk_core<T>(md, c, k, oversample, power_iters, seed, prec, dptr<T>(q), lam, s, nullptr, nullptr, 0, cheb_steps,
+                 cheb_degree);
     std::vector<T> hq((size_t)md.P * k);
     CK_CUDA(cudaMemcpyAsync(hq.data(), q.p, hq.size() * sizeof(T), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));

@@ -333,16 +333,23 @@ def assemble_opg(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfi
 
 
 def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 20, power_iters: int = 2,
-             seed: int = 0, precision: str = "f64") -> EigenPairs:
+             seed: int = 0, precision: str = "f64", filter_steps: int = 0, filter_degree: int = 0) -> EigenPairs:
     """Top-k eigenpairs of G = (1/N) J^T J by a randomized range finder
     (replaces eigensolve.hpp:80-81 opg_eigs_incremental).  Eigenvalues are
-    descending; columns of q are orthonormal eigenvectors."""
+    descending; columns of q are orthonormal eigenvectors.  filter_degree > 0
+    replaces the power iterations by filter_steps rounds of a Chebyshev
+    filter of that degree (curvkit_opg_topk_filtered)."""
     P, params, x, y, n = _inputs(spec, params, dataset)
     q = np.empty((P, k))
     lam = np.empty(k)
-    _lib.check(_lib.load().curvkit_opg_topk(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
-                                             int(oversample), int(power_iters), int(seed), _prec(precision),
-                                             _p(q), _p(lam)))
+    if filter_degree > 0:
+        _lib.check(_lib.load().curvkit_opg_topk_filtered(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
+                                                          int(oversample), int(filter_steps), int(filter_degree),
+                                                          int(seed), _prec(precision), _p(q), _p(lam)))
+    else:
+        _lib.check(_lib.load().curvkit_opg_topk(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
+                                                 int(oversample), int(power_iters), int(seed), _prec(precision),
+                                                 _p(q), _p(lam)))
     return EigenPairs(q, lam)
 
 

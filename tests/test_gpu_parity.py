@@ -390,6 +390,18 @@ def test_config4_topk_against_exact_spectrum():
 
 
 @pytest.mark.parametrize("prec", ["f64", "tf32"])
+def test_opg_eigs_filtered_host_mirror(prec):
+    g = load_golden("config0")
+    spec = spec_of(g)
+    k = 5
+    pairs = curv.opg_eigs(spec, g["params"], curv.Batch(g["x"], g["y"]), k, oversample=10, seed=3, precision=prec,
+                          filter_steps=2, filter_degree=4)
+    w = np.linalg.eigvalsh(g["G"])[::-1]
+    assert np.all(np.abs(pairs.lam - w[:k]) <= 1e-3 * np.abs(w[:k]))
+    assert np.abs(pairs.q.T @ pairs.q - np.eye(k)).max() <= (1e-8 if prec == "f64" else 1e-4)
+
+
+@pytest.mark.parametrize("prec", ["f64", "tf32"])
 def test_filtered_topk_matches_dense_eig(prec):
     """Chebyshev-filtered top-k (curvkit_dev_opg_topk_filtered) against the
     dense eigendecomposition of the reference's config-0 G."""
