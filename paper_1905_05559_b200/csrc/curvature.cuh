@@ -362,11 +362,12 @@ struct Engine {
         int64_t ldj = 0;
         {
             ProfScope prep("opg_prep", s, 0.0, 0.0);
+            TransposeBatch<T> tb(s);  // all layers' copies in one launch (flushed at scope end)
             for (int k = 0; k < S; ++k) {
                 akT[k] = buf(md.w[k] + 1, ldn);
-                transpose<T>(s, c.a[k], c.lda[k], 0, akT[k], ldn, 0, n, md.w[k] + 1, 1);
+                tb.add(c.a[k], c.lda[k], 0, akT[k], ldn, 0, n, md.w[k] + 1, 1);
                 dT[k] = buf(md.w[k + 1], ldn);
-                transpose<T>(s, c.delta[k], c.ldt[k], 0, dT[k], ldn, 0, n, md.w[k + 1], 1);
+                tb.add(c.delta[k], c.ldt[k], 0, dT[k], ldn, 0, n, md.w[k + 1], 1);
             }
         }
         for (int k = 0; k < S; ++k) {
@@ -545,25 +546,27 @@ struct Engine {
             }
             prof_stage.end();
             ProfScope prep_stage("hess_prep", s, 0.0, 0.0);
+            TransposeBatch<T> tb(s);  // the copies below in one launch
             // n-contiguous copies for the R generator (all reads 16-byte vectors);
             // a 32-multiple pitch keeps every K-block of 32 examples inside a row
             const int64_t ldn = round_up(n, 32);
             const int64_t tk = md.w[k];
             T* akT = buf_full(tk + 1, ldn);
-            transpose<T>(s, c.a[k], c.lda[k], 0, akT, ldn, 0, n, tk + 1, 1);
+            tb.add(c.a[k], c.lda[k], 0, akT, ldn, 0, n, tk + 1, 1);
             T* dkT = buf_full(np, ldn);
-            transpose<T>(s, c.delta[k], c.ldt[k], 0, dkT, ldn, 0, n, np, 1);
+            tb.add(c.delta[k], c.ldt[k], 0, dkT, ldn, 0, n, np, 1);
             T* GT = buf_full(np * np, ldn);
-            transpose<T>(s, G, c.ldt[k], n * c.ldt[k], GT, ldn, np * ldn, n, np, np);
+            tb.add(G, c.ldt[k], n * c.ldt[k], GT, ldn, np * ldn, n, np, np);
             T* PT[kMaxLayers] = {};
             T* QT[kMaxLayers] = {};
             for (int m = k - 1; m >= 0; --m) {
                 const int64_t tm1 = md.w[m + 1];
                 PT[m] = buf_full(np * tm1, ldn);
-                transpose<T>(s, Pm[m], c.ldt[m], n * c.ldt[m], PT[m], ldn, tm1 * ldn, n, tm1, np);
+                tb.add(Pm[m], c.ldt[m], n * c.ldt[m], PT[m], ldn, tm1 * ldn, n, tm1, np);
                 QT[m] = buf_full(tk * tm1, ldn);
-                transpose<T>(s, Qm[m], c.ldt[m], n * c.ldt[m], QT[m], ldn, tm1 * ldn, n, tm1, tk);
+                tb.add(Qm[m], c.ldt[m], n * c.ldt[m], QT[m], ldn, tm1 * ldn, n, tm1, tk);
             }
+            tb.flush();
             // Extended copies for the fused TF32 kernel: a 128-row activation
             // tile starting anywhere in [0, T_k) reads rows r -> r mod T_k.
             const bool fused = prec == kTF32 && sizeof(T) == 4;

@@ -516,13 +516,13 @@ __global__ void __launch_bounds__(256) rgen_kernel(RGenArgs<T> g) {
 
 // out[b][c][r] = in[b][r][c]  (rows x cols per batch; 32x32 smem tiles)
 template <class T>
-__global__ void transpose_kernel(const T* __restrict__ in, int64_t ldi, int64_t bsi, T* __restrict__ out,
-                                 int64_t ldo, int64_t bso, int64_t rows, int64_t cols) {
+__device__ __forceinline__ void transpose_tile(const T* __restrict__ in, int64_t ldi, int64_t bsi, T* __restrict__ out,
+                                               int64_t ldo, int64_t bso, int64_t rows, int64_t cols, int64_t bx,
+                                               int64_t by, int64_t bz) {
     __shared__ T tile[32][33];
-    const int64_t b = blockIdx.z;
-    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
-    const T* ip = in + b * bsi;
-    T* op = out + b * bso;
+    const int64_t r0 = bx * 32, c0 = by * 32;
+    const T* ip = in + bz * bsi;
+    T* op = out + bz * bso;
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
         const int64_t r = r0 + y, c = c0 + threadIdx.x;
         tile[y][threadIdx.x] = (r < rows && c < cols) ? ip[r * ldi + c] : T(0);
@@ -533,6 +533,61 @@ __global__ void transpose_kernel(const T* __restrict__ in, int64_t ldi, int64_t 
         if (c < cols && r < ldo) op[c * ldo + r] = r < rows ? tile[threadIdx.x][y] : T(0);
     }
 }
+
+template <class T>
+__global__ void transpose_kernel(const T* __restrict__ in, int64_t ldi, int64_t bsi, T* __restrict__ out,
+                                 int64_t ldo, int64_t bso, int64_t rows, int64_t cols) {
+    transpose_tile<T>(in, ldi, bsi, out, ldo, bso, rows, cols, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// Several independent transposes in one launch (the per-layer n-contiguous
+// copies of the curvature prep): block b belongs to the last job whose
+// first block is <= b.
+template <class T>
+struct TransposeJobs {
+    static constexpr int kMax = 8;
+    struct Job {
+        const T* in;
+        T* out;
+        int64_t ldi, bsi, ldo, bso, rows, cols, bx, by, block0;
+    } j[kMax];
+    int n = 0;
+    int64_t blocks = 0;
+};
+
+template <class T>
+__global__ void transpose_jobs_kernel(const __grid_constant__ TransposeJobs<T> J) {
+    const int64_t b = blockIdx.x;
+    int q = 0;
+    while (q + 1 < J.n && b >= J.j[q + 1].block0) ++q;
+    const auto& t = J.j[q];
+    const int64_t lb = b - t.block0;
+    transpose_tile<T>(t.in, t.ldi, t.bsi, t.out, t.ldo, t.bso, t.rows, t.cols, lb % t.bx, (lb / t.bx) % t.by,
+                      lb / (t.bx * t.by));
+}
+
+// same arguments as transpose(); jobs are launched together by flush()
+template <class T>
+struct TransposeBatch {
+    cudaStream_t s;
+    TransposeJobs<T> J{};
+    explicit TransposeBatch(cudaStream_t st) : s(st) {}
+    void add(const T* in, int64_t ldi, int64_t bsi, T* out, int64_t ldo, int64_t bso, int64_t rows, int64_t cols,
+             int64_t batch) {
+        if (J.n == TransposeJobs<T>::kMax) flush();
+        auto& t = J.j[J.n++];
+        t = {in, out, ldi, bsi, ldo, bso, rows, cols, ceil_div(ldo, 32), ceil_div(cols, 32), J.blocks};
+        J.blocks += t.bx * t.by * batch;
+    }
+    void flush() {
+        if (J.n == 0) return;
+        transpose_jobs_kernel<T><<<(unsigned)J.blocks, dim3(32, 8), 0, s>>>(J);
+        CK_LAUNCH();
+        J.n = 0;
+        J.blocks = 0;
+    }
+    ~TransposeBatch() { flush(); }
+};
 
 template <class T>
 void transpose(cudaStream_t s, const T* in, int64_t ldi, int64_t bsi, T* out, int64_t ldo, int64_t bso, int64_t rows,
