@@ -1602,6 +1602,10 @@ struct HessFused<float> {
                         list.push_back(make_int4((int)o, (int)j0, (int)n0, 0));
             }
         if (list.empty()) return true;
+        // partial-width column tiles (the bias column's tail, N = T_m + 1) last: the
+        // persistent pairs' final round then gets the short tiles (the transform
+        // cost of a tile does not shrink with its width)
+        std::stable_partition(list.begin(), list.end(), [&](const int4& t) { return t.z + BN <= N; });
         fh.tiles = static_cast<const int4*>(cached_upload(list.data(), list.size() * sizeof(int4)));
         fh.ntiles = (int64_t)list.size();
         const int b3 = a.lda_m >= round_up(N, 32) ? 1 : 0;
