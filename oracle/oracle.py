@@ -164,8 +164,12 @@ class Ref(_Lib):
         lib.ref_opg_eigs_incremental.argtypes = [_dp, i64, i64, i64, i64, _dp, _dp]
         lib.ref_hessian_lanczos.argtypes = mdl + [i64, i64, i64, C.c_double, C.c_uint64, _dp, _dp, _dp,
                                                   C.POINTER(i64)]
+        lib.ref_opg_rows_from_jacobian.argtypes = [_dp, i64, i64, i64, i64, i64, _dp]
+        lib.ref_hessian_sketch.argtypes = mdl + [_dp, i64, i64, _dp]
+        lib.ref_opg_sketch.argtypes = mdl + [_dp, i64, i64, _dp]
         for f in ("ref_hessian", "ref_opg", "ref_hessian_columns_sample", "ref_opg_rows_sample",
-                  "ref_hvp_operator_apply", "ref_forward", "ref_opg_eigs_incremental", "ref_hessian_lanczos"):
+                  "ref_hvp_operator_apply", "ref_forward", "ref_opg_eigs_incremental", "ref_hessian_lanczos",
+                  "ref_opg_rows_from_jacobian", "ref_hessian_sketch", "ref_opg_sketch"):
             getattr(lib, f).restype = C.c_int
 
     def _err(self, rc):
@@ -228,6 +232,31 @@ class Ref(_Lib):
         out = np.zeros((r1 - r0, P))
         self._call("opg_rows_sample", w, L, a, m, _f64(params), _f64(x), _f64(y), x.shape[0],
                    r0, r1, lanes, out)
+        return out
+
+    def opg_rows_from_jacobian(self, J, r0, r1, lanes):
+        """Rows [r0, r1) of G by the reference's rank-1 loop on a held Jacobian."""
+        n, p = J.shape
+        out = np.zeros((r1 - r0, p))
+        self._call("opg_rows_from_jacobian", J, n, p, r0, r1, lanes, out)
+        return out
+
+    def hessian_sketch(self, spec, params, x, y, omega, lanes):
+        """H @ omega (P x k) by k reference HVPs of the dataset-averaged cost."""
+        w, L, a, m = self._m(spec)
+        omega = _f64(omega)
+        out = np.zeros_like(omega)
+        self._call("hessian_sketch", w, L, a, m, _f64(params), _f64(x), _f64(y), x.shape[0], omega,
+                   omega.shape[1], lanes, out)
+        return out
+
+    def opg_sketch(self, spec, params, x, y, omega, block=256):
+        """G @ omega (P x k) = (1/N) J^T (J omega), J from the reference, streamed in row blocks."""
+        w, L, a, m = self._m(spec)
+        omega = _f64(omega)
+        out = np.zeros_like(omega)
+        self._call("opg_sketch", w, L, a, m, _f64(params), _f64(x), _f64(y), x.shape[0], omega,
+                   omega.shape[1], block, out)
         return out
 
     def opg_eigs_incremental(self, J, block, k):

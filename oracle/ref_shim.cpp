@@ -233,6 +233,108 @@ int ref_opg_rows_sample(const int64_t* w, int L, int act, int mode, const double
     });
 }
 
+// The reference's rank-1 update loop of assemble_opg (curvature.cpp:116-123)
+// restricted to rows [r0, r1) of G, on a Jacobian the caller already holds
+// (n x p, e.g. from ref_jacobian), split over `lanes` threads by row.  The
+// CPU arm times this on a bounded row sample; the Jacobian is timed once.
+int ref_opg_rows_from_jacobian(const double* J, int64_t n, int64_t p, int64_t r0, int64_t r1, int64_t lanes,
+                               double* out) {
+    return guard([&] {
+        const double inv_rows = 1.0 / static_cast<double>(n);
+        const std::size_t nr = r1 - r0;
+        std::memset(out, 0, sizeof(double) * nr * p);
+        lanes = std::max<int64_t>(1, lanes);
+        auto work = [&](std::size_t lane) {
+            for (int64_t ex = 0; ex < n; ++ex) {
+                const double* row = J + ex * p;
+                for (std::size_t i = r0 + lane; i < (std::size_t)r1; i += lanes) {
+                    if (row[i] == 0.0) continue;
+                    double* grow = out + (i - r0) * p;
+                    for (int64_t j = 0; j < p; ++j) grow[j] += (row[i] * row[j]) * inv_rows;
+                }
+            }
+        };
+        std::vector<std::thread> th;
+        for (int64_t l = 0; l < lanes; ++l) th.emplace_back(work, l);
+        for (auto& t : th) t.join();
+    });
+}
+
+// Sketches of the reference's full matrices without forming them, for
+// whole-matrix parity pins at full BASELINE sizes (tests/golden/make_sketch_pins.py):
+//   H Omega: column j is the reference HVP of the dataset-averaged cost on
+//            omega[:, j] (autodiff.cpp:158-244 through HvpOperator, one
+//            mini-batch = the dataset), columns over `lanes` threads;
+//   G Omega: (1/N) J^T (J Omega) with J from the reference's assemble_jacobian
+//            (curvature.cpp:94-100) on consecutive example blocks of `block`
+//            rows, i.e. G = (1/N) J^T J of assemble_opg for equal batches.
+// omega and out are P x k row-major.
+int ref_hessian_sketch(const int64_t* w, int L, int act, int mode, const double* params, const double* x,
+                       const double* y, int64_t n, const double* omega, int64_t k, int64_t lanes, double* out) {
+    return guard([&] {
+        ModelSpec s = make_spec(w, L, act, mode);
+        const std::size_t p = param_count(s);
+        const HvpOperator op(s, make_params(s, params), make_batch(s, x, y, n), (std::size_t)n);
+        lanes = std::max<int64_t>(1, lanes);
+        std::exception_ptr err;
+        std::mutex m;
+        auto work = [&](std::size_t lane) {
+            try {
+                for (int64_t j = lane; j < k; j += lanes) {
+                    DenseVector v(p, 0.0);
+                    for (std::size_t r = 0; r < p; ++r) v[r] = omega[r * k + j];
+                    const DenseVector hv = op.apply(v);
+                    for (std::size_t r = 0; r < p; ++r) out[r * k + j] = hv[r];
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> g(m);
+                if (!err) err = std::current_exception();
+            }
+        };
+        std::vector<std::thread> th;
+        for (int64_t l = 0; l < lanes; ++l) th.emplace_back(work, l);
+        for (auto& t : th) t.join();
+        if (err) std::rethrow_exception(err);
+    });
+}
+
+int ref_opg_sketch(const int64_t* w, int L, int act, int mode, const double* params, const double* x,
+                   const double* y, int64_t n, const double* omega, int64_t k, int64_t block, double* out) {
+    return guard([&] {
+        ModelSpec s = make_spec(w, L, act, mode);
+        const std::size_t p = param_count(s);
+        const ParamVector pv = make_params(s, params);
+        const Batch data = make_batch(s, x, y, n);
+        std::memset(out, 0, sizeof(double) * p * k);
+        std::vector<double> t;
+        for (int64_t b0 = 0; b0 < n; b0 += block) {
+            const int64_t nb = std::min(block, n - b0);
+            const DenseMatrix jb = assemble_jacobian(s, pv, slice_batch(data, b0, nb));
+            t.assign((std::size_t)nb * k, 0.0);
+            for (int64_t e = 0; e < nb; ++e) {  // T = J_b Omega
+                const double* row = jb.row(e);
+                double* tr = t.data() + e * k;
+                for (std::size_t r = 0; r < p; ++r) {
+                    if (row[r] == 0.0) continue;
+                    const double* om = omega + r * k;
+                    for (int64_t j = 0; j < k; ++j) tr[j] += row[r] * om[j];
+                }
+            }
+            for (int64_t e = 0; e < nb; ++e) {  // out += J_b^T T
+                const double* row = jb.row(e);
+                const double* tr = t.data() + e * k;
+                for (std::size_t r = 0; r < p; ++r) {
+                    if (row[r] == 0.0) continue;
+                    double* o = out + r * k;
+                    for (int64_t j = 0; j < k; ++j) o[j] += row[r] * tr[j];
+                }
+            }
+        }
+        const double inv = 1.0 / static_cast<double>(n);
+        for (std::size_t i = 0; i < p * (std::size_t)k; ++i) out[i] *= inv;
+    });
+}
+
 int ref_sym_eig(const double* a, int64_t n, double* vals, double* vecs) {
     return guard([&] {
         SymEig e = sym_eig(DenseMatrix(n, n, std::vector<double>(a, a + n * n)));
