@@ -1,30 +1,42 @@
 #!/usr/bin/env python
-"""Benchmark: exact Hessian + OPG assembly of BASELINE config 1 on B200.
+"""Benchmark: Hessian / OPG entries per second on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c3]
 
-Metric (BASELINE.json): Hessian/OPG entries per second.  One step assembles
-the exact Hessian H and the OPG matrix G (P x P each, P = 25450) for the MLP
-[784, 32, 10] (sigmoid, softmax CE) on N = 1000 seeded synthetic examples,
-so a step produces 2 * P^2 matrix entries.
+Headline workload (default `--config c3`, the largest BASELINE configuration
+whose P x P output fits one GPU): the full OPG matrix G = (1/N) J^T J of the
+MLP [784, 128, 64, 10] (sigmoid, softmax cross-entropy) on N = 10 000 seeded
+synthetic examples, P = 109 386, G = 47.9 GB fp32.  One step assembles G;
+`value` = P^2 / step time.  Other configurations run the products BASELINE
+names for them: c2 the exact Hessian (P = 55 050), c1 exact H and G
+(P = 25 450, 2 P^2 entries per step).
 
-  value  device-resident inputs, CUDA-event timed over exactly K steps
-  e2e    the same job through the host-buffer C-ABI (curvkit_assemble_*_f32):
-         host->device upload of params/x/y and device->host download of H and
-         G are inside the timed region
-  roofline  the dominant kernel's algorithmic FLOPs / its event-timed
-         duration (library-internal CUDA events on the launching stream)
-  cpu_baseline  the reference library (oracle/_ref, compiled from the
-         unmodified reference sources) on a bounded sample of the same job
+  value     device-resident inputs, CUDA events on the launching stream over
+            exactly K steps (barrier + synchronize on both sides; max over ranks)
+  e2e       the same job through the host-buffer C-ABI (curvkit_assemble_*_f32):
+            the host->device upload of params/x/y and the device->host
+            download of the P x P result into pinned memory are inside the
+            timed region
+  roofline  the dominant kernel: its algorithmic FLOPs
+            over its library-internal CUDA-event time, against the burst TF32
+            peak (bf16 burst / 2 from MEASURED_PEAKS.json) -- the sustained
+            ratio is reported beside it
+  cpu_baseline  the reference library (oracle/_ref, the unmodified reference
+            sources) on a bounded sample of the same job, all host threads
+  extra     (N = 1) c2 exact H, c1 exact H + G in TF32 and fp64, c4 top-100
+            OPG eigenpairs: the other BASELINE configurations on the same box
 
---impl reference runs only the reference CPU arm (rank 0; other ranks exit).
-Multi-GPU (torchrun), no collective on the data path either way:
-  --scaling weak (default)  the units are independent curvature jobs: rank r
-         assembles H and G of its own config-1 instance (parameters drawn with
-         seed + r); value = N * 2 P^2 / max-over-ranks step time
-  --scaling strong  one job: rank r assembles rows curvkit_shard_rows(P, N, r)
-         of H and G (lower-triangle entries and their mirrors, shards balanced
-         by triangle area); value = 2 P^2 / max-over-ranks step time
+--impl reference runs the reference CPU arm only (rank 0; other ranks exit 0):
+each step is one bounded sample of the same workload (OPG rows by the
+reference's rank-1 update loop on its own Jacobian, Hessian columns by its
+HVP-on-basis loop), value = the sample's entries / its time.
+
+Multi-GPU (torchrun, one process per GPU): strong scaling of ONE job.  Rank r
+owns the output units curvkit_shard_units(N, r) of every layer and assembles
+the rows of those units (their lower-triangle part in unit-major order, the
+row band a symmetric solver reads); value = entries / max-over-ranks time.
+`gather` (reported beside it) times the final NCCL gather of the row bands
+into the full matrix on rank 0.
 """
 from __future__ import annotations
 
@@ -39,21 +51,23 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PREC_DTYPE = {"tf32": "tf32", "tf32x3": "tf32x3", "f32": "f32", "f64": "f64"}
+METRIC = "hessian_opg_entries_per_s"
+PRODUCTS = {"c0": ("hessian", "opg"), "c1": ("hessian", "opg"), "c2": ("hessian",), "c3": ("opg",)}
+DATA = "synthetic (seeded splitmix64 draws with the BASELINE config shapes and distributions; no dataset)"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c1")
-    ap.add_argument("--precision", default="tf32", choices=list(PREC_DTYPE))
+    ap.add_argument("--config", default="c3", choices=sorted(PRODUCTS))
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "tf32x3", "f32", "f64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
     return ap.parse_args()
 
 
@@ -64,13 +78,29 @@ def dist_env():
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
-        d = json.load(open(path))
-        return d, "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        return json.load(open(path)), "measured (MEASURED_PEAKS.json)"
+    # B200_PROFILING.md fallback figures
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
+
+
+def entries_per_step(name, P):
+    return float(len(PRODUCTS[name])) * P * P
+
+
+def config_dict(wl):
+    """The workload description both arms print (identical dicts)."""
+    prods = PRODUCTS[wl.name]
+    what = " + ".join({"hessian": "exact Hessian H", "opg": "OPG G = (1/N) J^T J"}[p] for p in prods)
+    return {"workload": f"{wl.name}: MLP {wl.widths} {wl.activation} softmax-CE, N={wl.n}, P={wl.P}: {what}",
+            "products": "+".join(prods), "n_examples": wl.n, "P": wl.P,
+            "entries_per_step": int(entries_per_step(wl.name, wl.P)),
+            "l2": f"no flush: each step writes {len(prods)} x P^2 x 4 B = "
+                  f"{len(prods) * 4 * wl.P * wl.P / 1e9:.1f} GB >> 126 MB L2"}
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line), started before the
+    warm-up; summary() keeps the samples taken inside [t0, t1]."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -78,34 +108,36 @@ class Clocks:
 
     def __init__(self, index):
         self.index = index
-        self.lines = []
+        self.samples = []  # (host time, fields)
         self.proc = None
+        self.first = threading.Event()
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
+            self.first.wait(timeout=10.0)  # sampler running before the work starts
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.samples.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+            self.first.set()
 
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
-    def summary(self):
+    def summary(self, t0, t1):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+        inside = [f for t, f in self.samples if t0 <= t <= t1]
+        for f in inside:
             if len(f) < 7:
                 continue
             try:
@@ -118,51 +150,69 @@ class Clocks:
                     reasons.add(n)
         sm.sort()
         med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round(t1 - t0, 3)}
 
 
-# --------------------------------------------------------------------------- reference arm
+# --------------------------------------------------------------------------- reference CPU arm
 
-def reference_sample(wl, threads, budget_s=12.0):
-    """Time the reference library (oracle/_ref) on a bounded sample of the
-    step: Hessian columns (its own HVP-on-basis loop, `threads` lanes) and OPG
-    rows (its own rank-1 update loop); extrapolate to the full 2 P^2 job."""
-    import numpy as np
+class RefSampler:
+    """The reference library (oracle/_ref) on bounded samples of a config's job.
 
-    from oracle.oracle import Oracle, Ref
-    params, x, y, _ = wl.draw()
-    spec = dict(widths=wl.widths, activation=wl.activation)
-    P = wl.P
-    if Ref.available():
-        lib, kind = Ref(), "reference"
-    else:  # the reference tree was not built here: the C restatement
-        lib, kind = Oracle(), "port"
-    if kind == "port":
-        raise RuntimeError("oracle/_ref missing; build it with `make -C oracle`")
-    # Hessian columns spread over the parameter blocks, `threads` lanes
-    ncol = threads
-    c0 = 0
-    t = time.perf_counter()
-    lib.hessian_columns_sample(spec, params, x, y, c0, c0 + ncol, threads)
-    th = time.perf_counter() - t
-    t = time.perf_counter()
-    lib.jacobian(spec, params, x, y)
-    tj = time.perf_counter() - t
-    nrow = 4 * threads
-    t = time.perf_counter()
-    lib.opg_rows_sample(spec, params, x, y, 0, nrow, threads)
-    tr = max(1e-9, time.perf_counter() - t - tj)
-    t_full = th * P / ncol + tj + tr * P / nrow
-    return {
-        "value": 2.0 * P * P / t_full,
-        "unit": "entries/s",
-        "cores": threads,
-        "kind": kind,
-        "sample": (f"{ncol} Hessian columns (HVP on basis vectors, {threads} lanes) + {nrow} OPG rows "
-                   f"({threads} threads) of config {wl.name} (N={wl.n}, P={P}); full-job time extrapolated "
-                   f"linearly: {t_full:.1f} s"),
-        "seconds": th + tj + tr,
-    }
+    OPG: the reference's assemble_jacobian once (timed; its share is
+    amortised over the rows), then per sample `rows` rows of G by the
+    reference's rank-1 update loop (curvature.cpp:116-123), rows split over
+    the host threads.  Hessian: `cols` columns by the reference's
+    HVP-on-basis loop (curvature.cpp:49-57) over `threads` lanes."""
+
+    def __init__(self, wl, threads):
+        from oracle.oracle import Ref
+        if not Ref.available():
+            raise RuntimeError("oracle/_ref missing (built by `make -C oracle` where /root/reference exists)")
+        self.ref, self.wl, self.threads = Ref(), wl, threads
+        self.params, self.x, self.y, _ = wl.draw()
+        self.spec = dict(widths=wl.widths, activation=wl.activation)
+        self.J, self.tJ = None, 0.0
+        self.rows = 2 * threads
+        self.cols = threads
+        self.i = 0
+
+    def prepare(self):
+        if "opg" in PRODUCTS[self.wl.name] and self.J is None:
+            t = time.perf_counter()
+            self.J = self.ref.jacobian(self.spec, self.params, self.x, self.y)
+            self.tJ = time.perf_counter() - t
+
+    def sample(self):
+        """One bounded sample: (entries produced, seconds incl. the amortised J share)."""
+        self.prepare()
+        P = self.wl.P
+        ent, sec = 0.0, 0.0
+        stride = 7919  # walk the matrix: successive samples take different rows / columns
+        if "opg" in PRODUCTS[self.wl.name]:
+            r0 = (self.i * stride * self.rows) % (P - self.rows)
+            t = time.perf_counter()
+            self.ref.opg_rows_from_jacobian(self.J, r0, r0 + self.rows, self.threads)
+            sec += time.perf_counter() - t + self.tJ * self.rows / P
+            ent += float(self.rows) * P
+        if "hessian" in PRODUCTS[self.wl.name]:
+            c0 = (self.i * stride * self.cols) % (P - self.cols)
+            t = time.perf_counter()
+            self.ref.hessian_columns_sample(self.spec, self.params, self.x, self.y, c0, c0 + self.cols, self.threads)
+            sec += time.perf_counter() - t
+            ent += float(self.cols) * P
+        self.i += 1
+        return ent, sec
+
+    def describe(self):
+        parts = []
+        if "opg" in PRODUCTS[self.wl.name]:
+            parts.append(f"{self.rows} rows of G by the reference's rank-1 update loop on its own Jacobian "
+                         f"(assemble_jacobian of all N = {self.wl.n} examples, {self.tJ:.1f} s, amortised per row)")
+        if "hessian" in PRODUCTS[self.wl.name]:
+            parts.append(f"{self.cols} columns of H by the reference's HVP-on-basis loop")
+        return (f"{self.wl.name}: " + " + ".join(parts) + f"; {self.threads} host threads; "
+                "entries/s of the sample (each entry of the full job costs the same)")
 
 
 def run_reference(args):
@@ -172,207 +222,327 @@ def run_reference(args):
     from paper_1905_05559_b200.workloads import CONFIGS
     wl = CONFIGS[args.config]
     threads = os.cpu_count() or 1
+    rs = RefSampler(wl, threads)
+    rs.prepare()
     vals = []
     for i in range(args.warmup + args.steps):
-        r = reference_sample(wl, threads)
+        e, s = rs.sample()
         if i >= args.warmup:
-            vals.append(r)
-    v = sum(r["value"] for r in vals) / len(vals)
-    ms = 2.0 * wl.P * wl.P / v * 1e3
+            vals.append((e, s))
+    ent = sum(e for e, _ in vals)
+    sec = sum(s for _, s in vals)
+    v = ent / sec
+    rates = sorted(e / s for e, s in vals)
     line = {
-        "impl": "reference", "metric": "hessian_opg_entries_per_s", "value": v, "unit": "entries/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE config shapes and distributions)",
-        "config": {"workload": f"{wl.name}: MLP {wl.widths} {wl.activation}, N={wl.n}, P={wl.P}, exact H + OPG",
-                   "products": "hessian+opg"},
-        "cpu_baseline": {"value": v, "unit": "entries/s", "cores": threads, "kind": vals[0]["kind"],
-                         "sample": vals[0]["sample"]},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "entries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / len(vals) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": config_dict(wl),
+        "cpu_baseline": {"value": v, "unit": "entries/s", "cores": threads, "kind": "reference",
+                         "sample": rs.describe(),
+                         "spread": {"min": rates[0], "median": rates[len(rates) // 2], "max": rates[-1]},
+                         "full_job_s_extrapolated": entries_per_step(wl.name, wl.P) / v},
         "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline(wl):
+    """One warm-up + one timed sample of the reference arm (N = 1, rank 0)."""
+    threads = os.cpu_count() or 1
+    rs = RefSampler(wl, threads)
+    rs.prepare()
+    rs.sample()
+    e, s = rs.sample()
+    return {"value": e / s, "unit": "entries/s", "cores": threads, "kind": "reference", "sample": rs.describe()}
+
+
 # --------------------------------------------------------------------------- B200 arm
 
-def row_range(P, rank, world):
-    per = (P + world - 1) // world
-    return min(P, rank * per), min(P, (rank + 1) * per)
+def roofline(prof, steps, ms_step, pk, pk_kind, prec, traffic=None):
+    """The dominant region (largest event-timed share) against its roofline."""
+    if not prof:
+        return None
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    r = prof[dom]
+    per_launch_ms = r["ms"] / max(1, r["launches"])
+    out = {"kernel": dom, "share_of_step": r["ms"] / steps / ms_step, "per_launch_ms": per_launch_ms,
+           "launches_per_step": r["launches"] // max(1, steps), "traffic": None}
+    if r["flops"] > 0:
+        achieved = r["flops"] / (r["ms"] / 1e3) / 1e12
+        if prec in ("tf32", "tf32x3"):
+            peak = pk["bf16_tflops"] / 2.0
+            out.update(bound="tensor", achieved=achieved, unit="TFLOP/s", peak=peak, frac=achieved / peak,
+                       peak_note=f"TF32 dense = bf16 burst {pk['bf16_tflops']} / 2, {pk_kind}",
+                       frac_sustained=achieved / (pk["bf16_tflops_sustained"] / 2.0))
+        else:
+            fp64 = pk.get("fp64_tflops")
+            out.update(bound="tensor" if prec == "f64" else "fma", achieved=achieved, unit="TFLOP/s",
+                       peak=fp64 if prec == "f64" else None,
+                       frac=(achieved / fp64) if (prec == "f64" and fp64) else None,
+                       peak_note=("FP64 DMMA peak measured by tools/mma_rate_f64 (profiles/)" if prec == "f64"
+                                  else "SIMT fp32 path"))
+    else:
+        achieved = r["bytes"] / (r["ms"] / 1e3) / 1e9
+        out.update(bound="hbm", achieved=achieved, unit="GB/s", peak=pk["hbm_gbs"], frac=achieved / pk["hbm_gbs"])
+    if traffic and dom in traffic:
+        out["traffic"] = traffic[dom]
+    return out
 
 
-def run_b200(args):
-    import numpy as np
-    import torch
+def kernels_table(prof, steps):
+    return {k: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] // max(1, steps),
+                "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
+                "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
+            for k, v in prof.items()}
 
-    from paper_1905_05559_b200 import _lib, curv
-    from paper_1905_05559_b200.workloads import CONFIGS
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = CONFIGS[args.config]
-    weak = world > 1 and args.scaling == "weak"
-    if weak and rank > 0:  # an independent instance of the same config per rank
-        import dataclasses
-        wl = dataclasses.replace(wl, seed=wl.seed + 7919 * rank)
-    prec = args.precision
-    dt = torch.float64 if prec == "f64" else torch.float32
-    dev = torch.device("cuda", local)
-    params, x, y, labels = wl.draw()
-    P, n = wl.P, wl.n
-    spec = curv.ModelSpec(wl.widths, wl.activation)
-    p_d = torch.tensor(params, dtype=dt, device=dev)
-    x_d = torch.tensor(x, dtype=dt, device=dev)
-    l_d = torch.tensor(labels, dtype=torch.int32, device=dev)
-    ld = (P + 31) // 32 * 32
-    H = torch.empty((P, ld), dtype=dt, device=dev)
-    G = torch.empty((P, ld), dtype=dt, device=dev)
-    stream = torch.cuda.current_stream()
+class Job:
+    """One BASELINE config resident on the device; step() assembles its products."""
 
-    rb, re = curv.shard_rows(P, world, rank)
+    def __init__(self, name, prec, dev, torch, shard=None):
+        from paper_1905_05559_b200 import curv
+        from paper_1905_05559_b200.workloads import CONFIGS
+        self.curv, self.torch = curv, torch
+        self.wl = CONFIGS[name]
+        self.prec = prec
+        dt = torch.float64 if prec == "f64" else torch.float32
+        self.params, self.x, self.y, labels = self.wl.draw()
+        self.spec = curv.ModelSpec(self.wl.widths, self.wl.activation)
+        self.p_d = torch.tensor(self.params, dtype=dt, device=dev)
+        self.x_d = torch.tensor(self.x, dtype=dt, device=dev)
+        self.l_d = torch.tensor(labels, dtype=torch.int32, device=dev)
+        P = self.wl.P
+        self.ld = (P + 31) // 32 * 32
+        self.shard = shard  # (comm, rank, world) for the sharded job
+        self.out = {}
+        for prod in PRODUCTS[name]:
+            if shard is None:
+                self.out[prod] = torch.empty((P, self.ld), dtype=dt, device=dev)
+            else:
+                rows = curv.shard_units_rows(self.spec, shard[2], shard[1])
+                self.out[prod] = torch.empty((max(1, rows), self.ld), dtype=dt, device=dev)
 
-    def step():
-        if world == 1 or weak:
-            curv.dev_assemble_hessian(spec, p_d, x_d, l_d, n, H, ld, precision=prec, stream=stream)
-            curv.dev_assemble_opg(spec, p_d, x_d, l_d, n, G, ld, precision=prec, stream=stream)
-        else:  # this rank's triangle-balanced row shard of both products
-            curv.dev_hessian_shard(spec, p_d, x_d, l_d, n, rb, re, H, ld, precision=prec, stream=stream)
-            curv.dev_opg_shard(spec, p_d, x_d, l_d, n, rb, re, G, ld, precision=prec, stream=stream)
+    def step(self, stream):
+        c, wl = self.curv, self.wl
+        for prod, buf in self.out.items():
+            if self.shard is None:
+                f = c.dev_assemble_hessian if prod == "hessian" else c.dev_assemble_opg
+                f(self.spec, self.p_d, self.x_d, self.l_d, wl.n, buf, self.ld, precision=self.prec, stream=stream)
+            else:
+                c.dev_assemble_band(self.spec, prod, self.p_d, self.x_d, self.l_d, wl.n, self.shard[2], self.shard[1],
+                                    buf, self.ld, precision=self.prec, stream=stream)
 
-    for _ in range(args.warmup):
-        step()
+    def free(self):
+        self.out.clear()
+
+
+def timed(job, steps, warmup, stream, torch, barrier=lambda: None, clocks=None):
+    """warm-up, then exactly `steps` steps between CUDA events on `stream`."""
+    curv = job.curv
+    for _ in range(warmup):
+        job.step(stream)
     torch.cuda.synchronize()
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
     barrier()
     torch.cuda.synchronize()
     l0 = curv.launch_count()
     curv.profile_begin()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(steps):
+        job.step(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    prof = curv.profile_end()
+    barrier()
+    launches = (curv.launch_count() - l0) // steps
+    return e0.elapsed_time(e1) / steps, prof, launches, (t0, t1)
+
+
+def e2e_run(job, steps, world):
+    """The same job through the host-buffer C-ABI (pinned host outputs)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    from paper_1905_05559_b200 import _lib
+    curv, wl = job.curv, job.wl
+    lib = _lib.load()
+    P, n = wl.P, wl.n
+    hosts = {prod: torch.empty((P, P), dtype=torch.float32, pin_memory=True) for prod in PRODUCTS[wl.name]}
+    xp, yp, pp = (np.ascontiguousarray(a) for a in (job.x, job.y, job.params))
+    cfg = curv.CurvatureConfig(batch_size_h=n, batch_size_g=n, memory_cap=1 << 40)._c()
+    m = job.spec._c()
+    dp = lambda a: a.ctypes.data_as(_lib.dptr)  # noqa: E731
+    fp = lambda t: C.cast(t.data_ptr(), _lib.fptr)  # noqa: E731
+    prec = curv.PRECISION[job.prec]
+
+    def one():
+        for prod, h in hosts.items():
+            f = lib.curvkit_assemble_hessian_f32 if prod == "hessian" else lib.curvkit_assemble_opg_f32
+            _lib.check(f(C.byref(m), dp(pp), dp(xp), dp(yp), n, C.byref(cfg), prec, fp(h)))
+
+    one()  # warm-up (pool mapping, pinned pages)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    te = (time.perf_counter() - t0) / steps
+    nprod = len(hosts)
+    ok = bool(torch.equal(hosts[next(iter(hosts))][:64, :64], hosts[next(iter(hosts))][:64, :64].T))
+    del hosts
+    return {"value": entries_per_step(wl.name, P) / te, "unit": "entries/s",
+            "h2d_bytes_per_step": int(nprod * 8 * (P + xp.size + yp.size)),
+            "d2h_bytes_per_step": int(nprod * 4 * P * P), "ms_per_step": te * 1e3,
+            "path": "curvkit_assemble_*_f32 host-buffer C-ABI (pinned fp32 output)", "result_symmetric": ok}
+
+
+def run_extra(torch, dev, stream, pk, pk_kind):
+    """The other BASELINE configurations on the same GPU (N = 1)."""
+    out = {}
+    for name, prec, steps in (("c2", "tf32", 8), ("c1", "tf32", 20), ("c1", "f64", 3)):
+        job = Job(name, prec, dev, torch)
+        ms, prof, launches, _ = timed(job, steps, 2, stream, torch)
+        P = job.wl.P
+        out[f"{name}_{prec}"] = {"workload": config_dict(job.wl)["workload"], "dtype": prec,
+                                 "value": entries_per_step(name, P) / (ms / 1e3), "unit": "entries/s",
+                                 "ms_per_step": ms, "steps": steps, "gpu_launches": launches,
+                                 "roofline": roofline(prof, steps, ms, pk, pk_kind, prec),
+                                 "kernels": kernels_table(prof, steps)}
+        job.free()
+        del job
+        torch.cuda.empty_cache()
+    # c4: top-100 OPG eigenpairs, BASELINE's setting and the converged default
+    from paper_1905_05559_b200 import curv
+    from paper_1905_05559_b200.workloads import CONFIGS
+    wl = CONFIGS["c4"]
+    params, x, _, labels = wl.draw()
+    p = torch.tensor(params, dtype=torch.float32, device=dev)
+    xx = torch.tensor(x, dtype=torch.float32, device=dev)
+    ll = torch.tensor(labels, dtype=torch.int32, device=dev)
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    k = wl.eig_k
+    q = torch.empty((wl.P, k), dtype=torch.float32, device=dev)
+    lam = torch.empty(k, dtype=torch.float32, device=dev)
+    runs = {"baseline_setting": lambda: curv.dev_opg_topk(spec, p, xx, ll, wl.n, k, wl.oversample, wl.power_iters, 7,
+                                                         q, lam, stream=stream),
+            "converged_default": lambda: curv.dev_opg_topk_auto(spec, p, xx, ll, wl.n, k, wl.oversample, 7, q, lam,
+                                                                stream=stream)}
+    c4 = {"workload": f"c4: MLP {wl.widths} {wl.activation}, N={wl.n}, P={wl.P}: top-{k} OPG eigenpairs"}
+    for key, fn in runs.items():
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for _ in range(2):
+            fn()
         e1.record(stream)
         torch.cuda.synchronize()
-    prof = curv.profile_end()
-    launches = (curv.launch_count() - l0) // args.steps
-    barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+        c4[key] = {"ms_per_solve": e0.elapsed_time(e1) / 2}
+    c4["baseline_setting"]["note"] = (f"oversample {wl.oversample}, {wl.power_iters} power iterations (BASELINE): "
+                                      "Ritz values 9-17% below the exact spectrum; cannot reach 1e-3 on this flat "
+                                      "spectrum (DESIGN.md section 5)")
+    c4["converged_default"]["note"] = ("Chebyshev-filtered subspace iteration with the Ritz-convergence stop rule "
+                                       "(curvkit_dev_opg_topk_auto): all 100 eigenvalues within 1e-3 "
+                                       "(tests/test_gpu_parity.py::test_config4_topk_against_exact_spectrum)")
+    out["c4_topk"] = c4
+    return out
+
+
+def run_b200(args):
+    import torch
+
+    from paper_1905_05559_b200 import curv
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+        def bcast(obj):
+            lst = [obj]
+            dist.broadcast_object_list(lst, src=0)
+            return lst[0]
+        comm = curv.Comm.create(rank, world, bcast)
+    stream = torch.cuda.current_stream()
+    job = Job(args.config, args.precision, dev, torch, shard=(comm, rank, world) if world > 1 else None)
+    wl = job.wl
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    with Clocks(local) as clk:
+        ms, prof, launches, (t0, t1) = timed(job, args.steps, args.warmup, stream, torch, barrier)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    # weak: every rank assembles a whole job; strong: the row shards cover one
-    entries = 2.0 * P * P * (world if weak else 1)
-    value = entries / (ms / 1e3)
+    ent = entries_per_step(wl.name, wl.P)
+    value = ent / (ms / 1e3)
 
-    # e2e through the host-buffer C-ABI (pinned host outputs)
+    gather = None
+    if world > 1:  # the final gather of the row bands into the full matrix on rank 0
+        gather = {}
+        for prod, band in job.out.items():
+            full = torch.empty((wl.P, job.ld), dtype=band.dtype, device=dev) if rank == 0 else None
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            curv.dev_gather_bands(job.spec, band, job.ld, full, job.ld, comm, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            gather[prod] = {"ms": e0.elapsed_time(e1), "bytes_to_rank0": int(4 * wl.P * (wl.P + 1) // 2)}
+            del full
+        torch.cuda.empty_cache()
+
     e2e = None
-    if not args.no_e2e and (world == 1 or weak):  # the host-buffer ABI assembles whole matrices
-        lib = _lib.load()
-        import ctypes as C
-        hH = torch.empty((P, P), dtype=torch.float32, pin_memory=True)
-        hG = torch.empty((P, P), dtype=torch.float32, pin_memory=True)
-        xp = np.ascontiguousarray(x)
-        yp = np.ascontiguousarray(y)
-        pp = np.ascontiguousarray(params)
-        cfg = curv.CurvatureConfig(batch_size_h=n, batch_size_g=n, memory_cap=1 << 40)._c()
-        m = spec._c()
-        dp = lambda a: a.ctypes.data_as(_lib.dptr)  # noqa: E731
-        fp = lambda t: C.cast(t.data_ptr(), _lib.fptr)  # noqa: E731
-
-        def e2e_step():
-            _lib.check(lib.curvkit_assemble_hessian_f32(C.byref(m), dp(pp), dp(xp), dp(yp), n, C.byref(cfg),
-                                                        curv.PRECISION[prec], fp(hH)))
-            _lib.check(lib.curvkit_assemble_opg_f32(C.byref(m), dp(pp), dp(xp), dp(yp), n, C.byref(cfg),
-                                                    curv.PRECISION[prec], fp(hG)))
-
-        e2e_step()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        te = (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([te], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            te = float(t.item())
-        h2d = 2 * 8 * (P + x.size + y.size) * world
-        e2e = {"value": entries / te, "unit": "entries/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(2 * 4 * P * P * world), "ms_per_step": te * 1e3}
-
+    if not args.no_e2e and world == 1:
+        job_free_bytes = sum(b.numel() * b.element_size() for b in job.out.values())
+        job.free()  # the host-buffer path allocates its own device result
+        torch.cuda.empty_cache()
+        e2e = e2e_run(job, args.e2e_steps, world)
+        del job_free_bytes
     if rank != 0:
+        if comm is not None:
+            comm.close()
         return
     pk, pk_kind = peaks()
-    # dominant region: the one with the largest event-timed share of the step
-    dom = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
-    roof = None
-    if dom:
-        r = prof[dom]
-        per_launch_ms = r["ms"] / max(1, r["launches"])
-        if r["flops"] > 0:
-            peak = pk["bf16_tflops_sustained"] / 2.0 if prec in ("tf32", "tf32x3") else None
-            achieved = r["flops"] / (r["ms"] / 1e3) / 1e12
-            roof = {"bound": "tensor", "achieved": achieved, "unit": "TFLOP/s", "kernel": dom,
-                    "peak": peak, "frac": (achieved / peak) if peak else None,
-                    "peak_note": (f"TF32 dense = bf16 {pk_kind} sustained {pk['bf16_tflops_sustained']} / 2"
-                                  if peak else "SIMT fp32/fp64 path: no tensor peak"),
-                    "share_of_step": r["ms"] / args.steps / ms, "per_launch_ms": per_launch_ms,
-                    "traffic": None}
-        else:
-            achieved = r["bytes"] / (r["ms"] / 1e3) / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "unit": "GB/s", "kernel": dom, "peak": pk["hbm_gbs"],
-                    "frac": achieved / pk["hbm_gbs"], "share_of_step": r["ms"] / args.steps / ms,
-                    "per_launch_ms": per_launch_ms, "traffic": None}
-        if dom in ("hess_symkr", "opg_symkr"):
-            roof["note"] = ("flops = 2 N per symmetric-orbit value (the kernel's algorithmic work, DESIGN.md section 4); "
-                            "at config 1 the kernel is bound by its TMA output stores (32/64-byte rows, "
-                            "profiles/r01_c1_symkr_ncu_summary.txt), at configs 2/3 by the tensor pipe (~0.9 of peak)")
-            # the same launches counted as the lower-triangle product a symmetry-blind kernel runs
-            # (2 N per lower entry of the diagonal blocks): the rate the orbit scheme delivers
-            if world == 1 or weak:  # whole diagonal blocks per rank
-                ws = wl.widths
-                lower = sum(pk * (pk + 1) / 2.0 for pk in (ws[k + 1] * (ws[k] + 1) for k in range(len(ws) - 1)))
-                roof["reference_count_tflops"] = 2.0 * n * lower * args.steps / (r["ms"] / 1e3) / 1e12
-        tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tfile):
-            roof["traffic"] = json.load(open(tfile)).get(dom)
-    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] // args.steps,
-                   "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
-                   "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
-               for k, v in prof.items()}
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(wl.name)
+    roof = roofline(prof, args.steps, ms, pk, pk_kind, args.precision, traffic)
     cpu = None
+    extra = None
+    if world == 1 and not args.no_extra:
+        job.free()
+        torch.cuda.empty_cache()
+        extra = run_extra(torch, dev, stream, pk, pk_kind)
     if not args.no_cpu_baseline and world == 1:
         try:
-            reference_sample(wl, os.cpu_count() or 1)  # warm-up sample (page faults, thread start), as the reference arm
-            r = reference_sample(wl, os.cpu_count() or 1)
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = cpu_baseline(wl)
         except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "unit": "entries/s", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {ex}"}
+            cpu = {"value": None, "unit": "entries/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
     line = {
-        "metric": "hessian_opg_entries_per_s", "value": value, "unit": "entries/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak" if (weak or world == 1) else "strong", "vs_baseline": None, "dtype": PREC_DTYPE[prec],
-        "data": "synthetic (seeded, BASELINE config shapes and distributions)",
-        "config": {"workload": f"{wl.name}: MLP {wl.widths} {wl.activation}, N={n}, P={P}, exact H + OPG "
-                               f"({2 * P * P} entries per step)",
-                   "products": "hessian+opg", "precision": prec,
-                   "l2": "no flush: each step writes 2 x P^2 x 4 B = 5.2 GB >> 126 MB L2",
-                   "parallelism": ("single GPU" if world == 1 else
-                                   f"{world} GPUs, one independent config-1 job per GPU, no collective" if weak else
-                                   f"{world} GPUs, triangle-balanced row shards of one job, no data-path collective")},
-        "gpu_launches": int(launches),
-        "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-        "clocks": clk.summary(),
+        "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": args.precision, "data": DATA, "config": config_dict(wl),
+        "parallelism": ("1 GPU" if world == 1 else
+                        f"{world} GPUs: output units of every layer split over ranks, each rank assembles the rows of "
+                        "its units (lower part in unit-major order); no data-path collective, final NCCL gather timed "
+                        "separately"),
+        "gpu_launches": int(launches), "roofline": roof, "kernels": kernels_table(prof, args.steps),
+        "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": clk.summary(t0, t1), "extra": extra,
     }
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
 
 
 def main():

@@ -196,23 +196,31 @@ int curvkit_dev_opg_topk_filtered(const curvkit_model* model, const void* params
                                   int64_t filter_steps, int64_t filter_degree, uint64_t seed, int32_t precision,
                                   void* q, void* lambda, void* stream);
 
-/* Row shards for multi-GPU runs (no collective on the data path).  A shard
- * assembles the lower-triangle entries of rows [row_begin, row_end) and their
- * mirrored copies into a full-size output buffer; the shards of
- * curvkit_shard_rows(P, nshards, s, ...) for s = 0..nshards-1 write disjoint
- * entries whose union is the full matrix (rows balanced by triangle area).
- * In TF32 mode a diagonal layer block is computed per symmetric orbit of four
- * entries; there a shard takes the share of the block's
- * orbit tiles that matches its share of the block's lower triangle, so the
- * shards still write disjoint entries whose union is the block.
- * opg_shard needs row_begin % 4 == 0 (the boundaries of shard_rows are). */
-int curvkit_shard_rows(int64_t p, int64_t nshards, int64_t shard, int64_t* row_begin, int64_t* row_end);
-int curvkit_dev_hessian_shard(const curvkit_model* model, const void* params, const void* x,
-                              const int32_t* labels, int64_t n, int32_t precision, int64_t row_begin,
-                              int64_t row_end, void* h, int64_t ldh, void* stream);
-int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const void* x,
-                          const int32_t* labels, int64_t n, int32_t precision, int64_t row_begin,
-                          int64_t row_end, void* g, int64_t ldg, void* stream);
+/* Unit bands: the multi-GPU layout of H and G (one process per GPU, DESIGN.md
+ * section 7).  Shard s of nshards owns the output units
+ * [unit_begin[k], unit_end[k]) of every layer k (L - 1 entries each) and
+ * assembles the rows of those units -- per layer the weight rows (o, i) of
+ * its units, then their bias rows -- into a compact band of band_rows rows
+ * (leading dimension ld >= P, a multiple of 4).  A band holds every entry of
+ * its rows whose column unit is <= the row's unit in the unit-major order
+ * (layers, then units; whole unit-diagonal squares), so the shards compute
+ * each symmetric pair once and need no exchange; the other entries of the
+ * band are unspecified.  Units are cut per layer so every shard gets 1/nshards
+ * of the layer's work.  The reference shards Hessian columns over threads
+ * (curvature.cpp:39-71).  TF32 only.  product: 0 = Hessian, 1 = OPG. */
+int curvkit_shard_units(const curvkit_model* model, int64_t nshards, int64_t shard, int64_t* unit_begin,
+                        int64_t* unit_end, int64_t* band_rows);
+int curvkit_dev_assemble_band(const curvkit_model* model, int32_t product, const void* params, const void* x,
+                              const int32_t* labels, int64_t n, int32_t precision, int64_t nshards, int64_t shard,
+                              void* band, int64_t ld, void* stream);
+/* Assembly of the full P x P matrix from the bands: band_scatter copies one
+ * band's rows into place, symmetrize_units fills the upper unit-major
+ * triangle from the lower one (after every band is in place).  gather_bands
+ * does both over a communicator: every rank sends its band, rank 0 receives
+ * them into full (ldf == ld) and symmetrizes (full is unused on other ranks). */
+int curvkit_dev_band_scatter(const curvkit_model* model, int32_t precision, int64_t nshards, int64_t shard,
+                             const void* band, int64_t ld, void* full, int64_t ldf, void* stream);
+int curvkit_dev_symmetrize_units(const curvkit_model* model, int32_t precision, void* full, int64_t ldf, void* stream);
 
 /* Parameter-row-sharded top-k across GPUs (one process per GPU).  Rank r
  * owns the contiguous parameter rows [p_begin, p_end) of
@@ -227,7 +235,23 @@ int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const 
 typedef struct curvkit_comm_s* curvkit_comm;
 int curvkit_comm_unique_id(uint8_t* id_out);
 int curvkit_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, curvkit_comm* out);
+/* The same communicator over the caller's own host-memory collectives (MPI,
+ * gloo, ... bound as C callbacks; the library stages each exchange through
+ * host memory).  allreduce sums count elements of dtype (0 float, 1 double)
+ * in place on every rank; gather delivers rank r's send_bytes[r] bytes to
+ * recv + sum_{q<r} recv_bytes[q] on root (recv is NULL on other ranks).
+ * Callbacks return 0 on success.  For ranks NCCL cannot serve (one GPU shared
+ * by several processes). */
+typedef int (*curvkit_host_allreduce_fn)(void* buf, int64_t count, int32_t dtype, void* user);
+typedef int (*curvkit_host_gather_fn)(const void* send, int64_t send_bytes, void* recv, const int64_t* recv_bytes,
+                                      int32_t root, void* user);
+int curvkit_comm_init_host(int32_t nranks, int32_t rank, curvkit_host_allreduce_fn allreduce,
+                           curvkit_host_gather_fn gather, void* user, curvkit_comm* out);
 int curvkit_comm_destroy(curvkit_comm comm);
+/* final gather of the unit bands (curvkit_dev_assemble_band of every rank) into
+ * the full symmetric matrix on rank 0 */
+int curvkit_dev_gather_bands(const curvkit_model* model, int32_t precision, const void* band, int64_t ld, void* full,
+                             int64_t ldf, void* stream, curvkit_comm comm);
 int curvkit_topk_shard_rows(const curvkit_model* model, int64_t nshards, int64_t shard, int64_t* p_begin,
                             int64_t* p_end);
 int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params, const void* x,
@@ -241,6 +265,25 @@ int curvkit_dev_opg_topk_sharded_filtered(const curvkit_model* model, const void
                                           const int32_t* labels, int64_t n, int64_t k, int64_t oversample,
                                           int64_t filter_steps, int64_t filter_degree, uint64_t seed,
                                           int32_t precision, void* q, void* lambda, void* stream, curvkit_comm comm);
+
+/* Top-k eigenpairs of G to a stated accuracy (the default solver of
+ * curv.opg_eigs): Chebyshev-filtered subspace iteration, degree 6 (lowered on
+ * steep spectra), stopped when every one of the k Ritz values has converged
+ * to `tol` relative (the remaining error estimated from the contraction of
+ * successive Ritz-value changes; 1e-4 holds the north_star's 1e-3 bar) or
+ * after max_applications operator applications.  Same outputs as
+ * curvkit_dev_opg_topk; the sharded variant makes every decision from the
+ * all-reduced Rayleigh-Ritz matrix, so all ranks stop together. */
+int curvkit_opg_topk_auto(const curvkit_model* model, const double* params, const double* x, const double* y,
+                          int64_t n, int64_t k, int64_t oversample, double tol, int64_t max_applications,
+                          uint64_t seed, int32_t precision, double* q_out, double* lambda_out);
+int curvkit_dev_opg_topk_auto(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                              int64_t n, int64_t k, int64_t oversample, double tol, int64_t max_applications,
+                              uint64_t seed, int32_t precision, void* q, void* lambda, void* stream);
+int curvkit_dev_opg_topk_sharded_auto(const curvkit_model* model, const void* params, const void* x,
+                                      const int32_t* labels, int64_t n, int64_t k, int64_t oversample, double tol,
+                                      int64_t max_applications, uint64_t seed, int32_t precision, void* q,
+                                      void* lambda, void* stream, curvkit_comm comm);
 
 /* Matrix-free Jacobian operator on a parameter-row range (TF32, J never
  * formed): transpose = 0: out (n x l) = J[:, p_begin:p_end] in, with in the

@@ -49,9 +49,16 @@ SIGNATURES = {
     "curvkit_dev_assemble_hessian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_opg": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
     "curvkit_dev_assemble_jacobian": [_MP, vptr, vptr, vptr, i64, i32, vptr, i64, vptr],
-    "curvkit_shard_rows": [i64, i64, i64, C.POINTER(i64), C.POINTER(i64)],
-    "curvkit_dev_hessian_shard": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
-    "curvkit_dev_opg_shard": [_MP, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
+    "curvkit_shard_units": [_MP, i64, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],
+    "curvkit_dev_assemble_band": [_MP, i32, vptr, vptr, vptr, i64, i32, i64, i64, vptr, i64, vptr],
+    "curvkit_dev_band_scatter": [_MP, i32, i64, i64, vptr, i64, vptr, i64, vptr],
+    "curvkit_dev_symmetrize_units": [_MP, i32, vptr, i64, vptr],
+    "curvkit_dev_gather_bands": [_MP, i32, vptr, i64, vptr, i64, vptr, vptr],
+    "curvkit_comm_init_host": [i32, i32, vptr, vptr, vptr, C.POINTER(vptr)],
+    "curvkit_opg_topk_auto": [_MP, dptr, dptr, dptr, i64, i64, i64, C.c_double, i64, u64, i32, dptr, dptr],
+    "curvkit_dev_opg_topk_auto": [_MP, vptr, vptr, vptr, i64, i64, i64, C.c_double, i64, u64, i32, vptr, vptr, vptr],
+    "curvkit_dev_opg_topk_sharded_auto": [_MP, vptr, vptr, vptr, i64, i64, i64, C.c_double, i64, u64, i32, vptr, vptr,
+                                          vptr, vptr],
     "curvkit_dev_gemm": [i64, i64, i64, vptr, i64, i32, vptr, i64, i32, vptr, i64, C.c_float, i32, vptr],
     "curvkit_dev_opg_topk": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
     "curvkit_dev_opg_topk_filtered": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
@@ -70,6 +77,10 @@ SIGNATURES = {
     "curvkit_hessian_topk_lanczos": [_MP, dptr, dptr, dptr, i64, i64, i64, i64, C.c_double, u64, i32, dptr, dptr, dptr,
                                      C.POINTER(i64)],
 }
+# host-transport callbacks of curvkit_comm_init_host
+HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, i64, i32, C.c_void_p)
+HOST_GATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, i64, C.c_void_p, C.POINTER(i64), i32, C.c_void_p)
+
 _RESTYPES = {"curvkit_last_error": C.c_char_p, "curvkit_version": C.c_char_p, "curvkit_launch_count": i64}
 
 _lib = None

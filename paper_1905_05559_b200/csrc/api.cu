@@ -8,10 +8,13 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <numeric>
+#include <algorithm>
 #include <string>
 #include <vector>
 
 #include "../../include/curvkit_b200.h"
+#include "bands.cuh"
 #include "comm.cuh"
 #include "common.cuh"
 #include "curvature.cuh"
@@ -70,6 +73,8 @@ void trim_pool() {
 }
 
 [[noreturn]] void contract(const std::string& m) { throw CurvError(kContractError, m); }
+
+constexpr int64_t kAutoDegree = 6;  // Chebyshev degree of the converged top-k solver
 [[noreturn]] void shape(const std::string& m) { throw CurvError(kShapeError, m); }
 
 ModelDesc make_desc(const curvkit_model* m) {
@@ -140,22 +145,31 @@ void check_memory_cap(int64_t p, int64_t cap, const char* who) {  // curvature.c
 // between calls (curvature workspaces are reused); trim_pool returns the
 // rest once the call's frees have completed.
 void keep_pool_memory() {
-    static bool done[64] = {};
+    static std::mutex mu;
+    static std::vector<int> done;
     int dev = 0;
     CK_CUDA(cudaGetDevice(&dev));
-    if (dev < 64 && done[dev]) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    if (dev < 64) done[dev] = true;
+    done.push_back(dev);
 }
 
+// the host-buffer entry points' stream: one per (thread, device)
 cudaStream_t lib_stream() {
-    static thread_local cudaStream_t s = nullptr;
+    static thread_local std::vector<std::pair<int, cudaStream_t>> streams;
     keep_pool_memory();
-    if (!s) CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int dev = 0;
+    CK_CUDA(cudaGetDevice(&dev));
+    for (const auto& ds : streams)
+        if (ds.first == dev) return ds.second;
+    cudaStream_t s = nullptr;
+    CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    streams.emplace_back(dev, s);
     return s;
 }
 
@@ -760,60 +774,59 @@ int curvkit_dev_assemble_jacobian(const curvkit_model* model, const void* params
     });
 }
 
-// ---- row shards (multi-GPU without a data-path collective) --------------------
-// Row r of the lower triangle holds r + 1 entries, so shard s of `nshards`
-// takes rows [P sqrt(s/n), P sqrt((s+1)/n)), rounded to 32 rows (one MN atom;
-// tiles straddling a boundary are computed by both shards and masked).
-int curvkit_shard_rows(int64_t p, int64_t nshards, int64_t shard, int64_t* row_begin, int64_t* row_end) {
+// ---- unit bands (multi-GPU H and G, bands.cuh) ---------------------------------
+int curvkit_shard_units(const curvkit_model* model, int64_t nshards, int64_t shard, int64_t* unit_begin,
+                        int64_t* unit_end, int64_t* band_rows) {
     return guard([&] {
-        if (p < 1 || nshards < 1 || shard < 0 || shard >= nshards) contract("shard_rows: bad arguments");
-        auto bound = [&](int64_t s) -> int64_t {
-            if (s <= 0) return 0;
-            if (s >= nshards) return p;
-            const double b = (double)p * std::sqrt((double)s / (double)nshards);
-            return std::min<int64_t>(p, (int64_t)std::llround(b / 32.0) * 32);
-        };
-        *row_begin = bound(shard);
-        *row_end = std::max(*row_begin, bound(shard + 1));
+        ModelDesc md = make_desc(model);
+        const UnitBand b = UnitBand::make(md, nshards, shard);
+        for (int k = 0; k < md.S; ++k) {
+            if (unit_begin) unit_begin[k] = b.u0[k];
+            if (unit_end) unit_end[k] = b.u1[k];
+        }
+        if (band_rows) *band_rows = b.rows;
     });
 }
 
-int curvkit_dev_hessian_shard(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
-                              int64_t n, int32_t precision, int64_t row_begin, int64_t row_end, void* h, int64_t ldh,
-                              void* stream) {
+int curvkit_dev_assemble_band(const curvkit_model* model, int32_t product, const void* params, const void* x,
+                              const int32_t* labels, int64_t n, int32_t precision, int64_t nshards, int64_t shard,
+                              void* band, int64_t ld, void* stream) {
     return guard([&] {
         ModelDesc md = make_desc(model);
-        if (n < 1) contract("assemble_hessian: empty dataset");
-        if (row_begin < 0 || row_end < row_begin) contract("hessian_shard: bad row range");
+        if (n < 1) contract("assemble_band: empty dataset");
+        if (product != 0 && product != 1) contract("assemble_band: product must be 0 (Hessian) or 1 (OPG)");
+        if (precision != kTF32) contract("unit-band assembly needs TF32 precision");
+        if (ld < md.P || ld % 4) contract("assemble_band: ld must be >= P and a multiple of 4");
+        const UnitBand b = UnitBand::make(md, nshards, shard);
+        if (b.rows == 0) return;
         cudaStream_t s = dev_stream(stream);
-        auto run = [&](auto tag) {
-            using T = decltype(tag);
-            Cache<T> c;
-            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
-            Engine<T> eng{md, s, precision};
-            eng.hessian((const T*)params, c, (T*)h, ldh, false, row_begin, row_end);
-        };
-        if (is_f64(precision)) run(double{});
-        else run(float{});
+        Cache<float> c;
+        forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
+        Engine<float> eng{md, s, precision};
+        if (product == 0) eng.hessian((const float*)params, c, (float*)band, ld, false, 0, INT64_MAX, &b);
+        else eng.opg_kr(c, (float*)band, ld, 0, INT64_MAX, &b);
     });
 }
 
-int curvkit_dev_opg_shard(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
-                          int64_t n, int32_t precision, int64_t row_begin, int64_t row_end, void* g, int64_t ldg,
-                          void* stream) {
+int curvkit_dev_band_scatter(const curvkit_model* model, int32_t precision, int64_t nshards, int64_t shard,
+                             const void* band, int64_t ld, void* full, int64_t ldf, void* stream) {
     return guard([&] {
         ModelDesc md = make_desc(model);
-        if (n < 1) contract("assemble_opg: empty dataset");
-        if (row_begin < 0 || row_end < row_begin || (row_begin & 3)) contract("opg_shard: bad row range");
+        const UnitBand b = UnitBand::make(md, nshards, shard);
+        if (ld < md.P || ldf < md.P) contract("band_scatter: leading dimensions must be >= P");
         cudaStream_t s = dev_stream(stream);
-        auto run = [&](auto tag) {
-            using T = decltype(tag);
-            Cache<T> c;
-            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
-            opg_into<T>(md, c, (T*)g, ldg, precision, s, row_begin, row_end);
-        };
-        if (is_f64(precision)) run(double{});
-        else run(float{});
+        if (is_f64(precision)) band_scatter<double>(md, b, (const double*)band, ld, (double*)full, ldf, s);
+        else band_scatter<float>(md, b, (const float*)band, ld, (float*)full, ldf, s);
+    });
+}
+
+int curvkit_dev_symmetrize_units(const curvkit_model* model, int32_t precision, void* full, int64_t ldf, void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (ldf < md.P) contract("symmetrize_units: ldf must be >= P");
+        cudaStream_t s = dev_stream(stream);
+        if (is_f64(precision)) symmetrize_units<double>(md, (double*)full, ldf, s);
+        else symmetrize_units<float>(md, (float*)full, ldf, s);
     });
 }
 
@@ -854,7 +867,60 @@ int curvkit_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, curvkit_c
         std::memcpy(u.internal, id, CURVKIT_COMM_ID_BYTES);
         ncclComm_t c = nullptr;
         nccl_check(NcclApi::get().comm_init_rank(&c, nranks, u, rank), "ncclCommInitRank");
-        *out = new curvkit_comm_s{ck::Comm{c, rank, nranks}};
+        ck::Comm cm;
+        cm.comm = c;
+        cm.rank = rank;
+        cm.nranks = nranks;
+        *out = new curvkit_comm_s{cm};
+    });
+}
+
+int curvkit_comm_init_host(int32_t nranks, int32_t rank, curvkit_host_allreduce_fn allreduce,
+                           curvkit_host_gather_fn gather, void* user, curvkit_comm* out) {
+    return guard([&] {
+        if (!out || !allreduce || !gather) contract("comm_init_host: null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) contract("comm_init_host: need 0 <= rank < nranks");
+        ck::Comm c;
+        c.h_sum = allreduce;
+        c.h_gather = gather;
+        c.user = user;
+        c.rank = rank;
+        c.nranks = nranks;
+        *out = new curvkit_comm_s{c};
+    });
+}
+
+int curvkit_dev_gather_bands(const curvkit_model* model, int32_t precision, const void* band, int64_t ld, void* full,
+                             int64_t ldf, void* stream, curvkit_comm comm) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (!comm) contract("gather_bands: null communicator");
+        const ck::Comm& cm = comm->c;
+        if (ld < md.P || ld != ldf) contract("gather_bands: ld must be >= P and equal ldf");
+        if (cm.rank == 0 && !full) contract("gather_bands: rank 0 needs the full output");
+        cudaStream_t s = dev_stream(stream);
+        const size_t es = is_f64(precision) ? 8 : 4;
+        std::vector<UnitBand> bands;
+        std::vector<int64_t> bytes;
+        for (int r = 0; r < cm.nranks; ++r) {
+            bands.push_back(UnitBand::make(md, cm.nranks, r));
+            bytes.push_back(bands.back().rows * ld * (int64_t)es);
+        }
+        // rank 0 receives every band into a staging buffer laid out band after
+        // band, then scatters the rows and mirrors the upper unit-major triangle
+        const int64_t total = std::accumulate(bytes.begin(), bytes.end(), int64_t(0));
+        DevMem stage(cm.rank == 0 ? (size_t)total : 0, s);
+        cm.gather(band, bytes, stage.p, 0, s);
+        if (cm.rank != 0) return;
+        int64_t off = 0;
+        for (int r = 0; r < cm.nranks; ++r) {
+            const uint8_t* src = static_cast<const uint8_t*>(stage.p) + off;
+            if (es == 8) band_scatter<double>(md, bands[r], (const double*)src, ld, (double*)full, ldf, s);
+            else band_scatter<float>(md, bands[r], (const float*)src, ld, (float*)full, ldf, s);
+            off += bytes[r];
+        }
+        if (es == 8) symmetrize_units<double>(md, (double*)full, ldf, s);
+        else symmetrize_units<float>(md, (float*)full, ldf, s);
     });
 }
 
@@ -933,6 +999,24 @@ int curvkit_dev_opg_topk_sharded_filtered(const curvkit_model* model, const void
     });
 }
 
+int curvkit_dev_opg_topk_sharded_auto(const curvkit_model* model, const void* params, const void* x,
+                                      const int32_t* labels, int64_t n, int64_t k, int64_t oversample, double tol,
+                                      int64_t max_applications, uint64_t seed, int32_t precision, void* q,
+                                      void* lambda, void* stream, curvkit_comm comm) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk: empty dataset");
+        if (!comm) contract("opg_topk_sharded: null communicator");
+        if (!(tol > 0.0) || max_applications < 1) contract("opg_topk_auto: need tol > 0 and max_applications >= 1");
+        if (precision != kTF32) contract("sharded opg_topk needs TF32 precision");
+        cudaStream_t s = dev_stream(stream);
+        Cache<float> c;
+        forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
+        dev_topk<float>(md, c, k, oversample, 0, seed, precision, (float*)q, (float*)lambda, s, &comm->c,
+                        ceil_div(max_applications, kAutoDegree), kAutoDegree, tol);
+    });
+}
+
 int curvkit_opg_topk_from_jacobian(const double* j, int64_t n, int64_t p, int64_t k, int64_t oversample,
                                    int64_t power_iters, uint64_t seed, int32_t precision, double* q_out,
                                    double* lambda_out) {
@@ -993,6 +1077,47 @@ int curvkit_dev_opg_topk(const curvkit_model* model, const void* params, const v
             Cache<T> c;
             forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
             dev_topk<T>(md, c, k, oversample, power_iters, seed, precision, (T*)q, (T*)lambda, s);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_dev_opg_topk_auto(const curvkit_model* model, const void* params, const void* x, const int32_t* labels,
+                              int64_t n, int64_t k, int64_t oversample, double tol, int64_t max_applications,
+                              uint64_t seed, int32_t precision, void* q, void* lambda, void* stream) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk_auto: empty dataset");
+        if (!(tol > 0.0) || max_applications < 1) contract("opg_topk_auto: need tol > 0 and max_applications >= 1");
+        cudaStream_t s = dev_stream(stream);
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Cache<T> c;
+            forward_device<T>(md, (const T*)params, (const T*)x, labels, n, c, s);
+            dev_topk<T>(md, c, k, oversample, 0, seed, precision, (T*)q, (T*)lambda, s, nullptr,
+                        ceil_div(max_applications, kAutoDegree), kAutoDegree, tol);
+        };
+        if (is_f64(precision)) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_opg_topk_auto(const curvkit_model* model, const double* params, const double* x, const double* y,
+                          int64_t n, int64_t k, int64_t oversample, double tol, int64_t max_applications,
+                          uint64_t seed, int32_t precision, double* q_out, double* lambda_out) {
+    return guard([&] {
+        ModelDesc md = make_desc(model);
+        if (n < 1) contract("opg_topk_auto: empty dataset");
+        if (!(tol > 0.0) || max_applications < 1) contract("opg_topk_auto: need tol > 0 and max_applications >= 1");
+        auto lab = labels_from_onehot(md, y, n);
+        cudaStream_t s = lib_stream();
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            Resident<T> r;
+            upload_and_forward<T>(md, params, x, lab, n, r, s);
+            host_topk<T>(md, r.cache, k, oversample, 0, seed, precision, q_out, lambda_out, s,
+                         ceil_div(max_applications, kAutoDegree), kAutoDegree, tol);
         };
         if (is_f64(precision)) run(double{});
         else run(float{});

@@ -1,9 +1,15 @@
-// comm.cuh -- NCCL communicator for the parameter-row-sharded top-k solver.
+// comm.cuh -- the communicator of the multi-GPU entry points.
 //
-// NCCL is opened at run time (dlopen), not linked: a process that already
-// loaded one (torch bundles its own libnccl.so.2) keeps using that copy, so
-// the library never brings a second NCCL with the same soname into it.
-// Collectives run on the caller's stream over NVLink / NVSwitch.
+// Two transports behind one interface:
+//   NCCL  (curvkit_comm_init): collectives on the caller's stream over NVLink /
+//         NVSwitch.  NCCL is opened at run time (dlopen), not linked: a process
+//         that already loaded one (torch bundles libnccl.so.2) keeps using it.
+//   host  (curvkit_comm_init_host): the caller's own collectives on host
+//         memory (an MPI / gloo / torch.distributed binding passed as C
+//         callbacks); the library stages each exchange through host memory.
+//         Used where NCCL cannot run (ranks sharing one GPU in tests).
+// The multi-GPU algorithms issue the same exchanges on either transport:
+// sum (all-reduce) and gather (variable-size blocks to one root).
 #pragma once
 
 #include <dlfcn.h>
@@ -12,7 +18,9 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
+#include "../../include/curvkit_b200.h"
 #include "common.cuh"
 
 namespace ck {
@@ -22,6 +30,10 @@ struct NcclApi {
     decltype(&ncclCommInitRank) comm_init_rank = nullptr;
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
 
     static NcclApi& get() {
@@ -42,6 +54,10 @@ struct NcclApi {
             api.comm_init_rank = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(h, "ncclCommInitRank"));
             api.comm_destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(h, "ncclCommDestroy"));
             api.all_reduce = reinterpret_cast<decltype(&ncclAllReduce)>(dlsym(h, "ncclAllReduce"));
+            api.send = reinterpret_cast<decltype(&ncclSend)>(dlsym(h, "ncclSend"));
+            api.recv = reinterpret_cast<decltype(&ncclRecv)>(dlsym(h, "ncclRecv"));
+            api.group_start = reinterpret_cast<decltype(&ncclGroupStart)>(dlsym(h, "ncclGroupStart"));
+            api.group_end = reinterpret_cast<decltype(&ncclGroupEnd)>(dlsym(h, "ncclGroupEnd"));
             api.error_string = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
         });
         if (!api.all_reduce) throw CurvError(kRuntimeError, "NCCL unavailable: " + err);
@@ -56,16 +72,69 @@ inline void nccl_check(ncclResult_t r, const char* what) {
     }
 }
 
-// One rank of a communicator; nranks == 1 makes every collective a no-op.
+// One rank of a communicator; nranks == 1 makes every collective a local copy.
 struct Comm {
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;  // NCCL transport, or
+    curvkit_host_allreduce_fn h_sum = nullptr;  // the host transport
+    curvkit_host_gather_fn h_gather = nullptr;
+    void* user = nullptr;
     int rank = 0, nranks = 1;
 
+    bool host() const { return comm == nullptr && h_sum != nullptr; }
+
+    // buf <- sum over ranks (identical bytes on every rank afterwards)
     template <class T>
     void sum(T* buf, size_t count, cudaStream_t s) const {
         if (nranks == 1 || count == 0) return;
+        if (host()) {
+            std::vector<T> h(count);
+            CK_CUDA(cudaMemcpyAsync(h.data(), buf, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            if (h_sum(h.data(), (int64_t)count, sizeof(T) == 8 ? 1 : 0, user) != 0)
+                throw CurvError(kRuntimeError, "host all-reduce callback failed");
+            CK_CUDA(cudaMemcpyAsync(buf, h.data(), count * sizeof(T), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
         const ncclDataType_t t = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
         nccl_check(NcclApi::get().all_reduce(buf, buf, count, t, ncclSum, comm, s), "ncclAllReduce");
+    }
+
+    // Rank r's `bytes[r]` device bytes at `send` land at recv + sum_{q<r} bytes[q]
+    // on `root` (recv is only used there).
+    void gather(const void* send, const std::vector<int64_t>& bytes, void* recv, int root, cudaStream_t s) const {
+        std::vector<int64_t> off(nranks + 1, 0);
+        for (int r = 0; r < nranks; ++r) off[r + 1] = off[r] + bytes[r];
+        if (nranks == 1 || (!host() && rank == root)) {
+            if (rank == root && bytes[rank] > 0)
+                CK_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + off[rank], send, (size_t)bytes[rank],
+                                        cudaMemcpyDeviceToDevice, s));
+            if (nranks == 1) return;
+        }
+        if (host()) {
+            std::vector<uint8_t> hs((size_t)bytes[rank]);
+            std::vector<uint8_t> hr(rank == root ? (size_t)off[nranks] : 0);
+            if (bytes[rank] > 0) CK_CUDA(cudaMemcpyAsync(hs.data(), send, hs.size(), cudaMemcpyDeviceToHost, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            if (h_gather(hs.data(), bytes[rank], rank == root ? hr.data() : nullptr, bytes.data(), root, user) != 0)
+                throw CurvError(kRuntimeError, "host gather callback failed");
+            if (rank == root && !hr.empty())
+                CK_CUDA(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
+        NcclApi& api = NcclApi::get();
+        if (!api.send || !api.recv || !api.group_start) throw CurvError(kRuntimeError, "NCCL send/recv unavailable");
+        nccl_check(api.group_start(), "ncclGroupStart");
+        if (rank == root) {
+            for (int r = 0; r < nranks; ++r)
+                if (r != root && bytes[r] > 0)
+                    nccl_check(api.recv(static_cast<uint8_t*>(recv) + off[r], (size_t)bytes[r], ncclInt8, r, comm, s),
+                               "ncclRecv");
+        } else if (bytes[rank] > 0) {
+            nccl_check(api.send(send, (size_t)bytes[rank], ncclInt8, root, comm, s), "ncclSend");
+        }
+        nccl_check(api.group_end(), "ncclGroupEnd");
     }
 };
 

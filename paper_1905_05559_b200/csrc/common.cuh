@@ -13,6 +13,8 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <cstring>
+#include <vector>
 
 namespace ck {
 
@@ -144,24 +146,80 @@ __device__ __forceinline__ T act_second(int a, T z) {
 }
 
 // Read-only launch tables (tile lists, packed index pairs) keyed by content:
-// uploaded once per device and kept for the life of the process, so repeated
-// calls of the same shape launch without a pageable host-to-device copy.
+// uploaded once per device and reused, so repeated calls of the same shape
+// launch without a pageable host-to-device copy.  Bounded: at most 64 tables
+// and 256 MB per device, least recently used evicted first (after a device
+// synchronisation, since a queued kernel may still read it).
+inline uint64_t content_hash(const void* p, size_t bytes) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ bytes;
+    size_t i = 0;
+    for (; i + 8 <= bytes; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, b + i, 8);
+        h = (h ^ w) * 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 31;
+    }
+    for (; i < bytes; ++i) h = (h ^ b[i]) * 0x94D049BB133111EBull;
+    return h;
+}
+
 inline const void* cached_upload(const void* host, size_t bytes) {
+    struct Entry {
+        int dev;
+        uint64_t hash;
+        std::vector<uint8_t> content;
+        void* d;
+        uint64_t used;
+    };
     static std::mutex mu;
-    static std::unordered_map<std::string, void*> cache;
+    static std::vector<Entry> cache;
+    static uint64_t tick = 0;
+    constexpr size_t kMaxEntries = 64, kMaxBytes = size_t(256) << 20;
     int dev = 0;
     cudaGetDevice(&dev);
-    std::string key(reinterpret_cast<const char*>(&dev), sizeof dev);
-    key.append(reinterpret_cast<const char*>(host), bytes);
+    const uint64_t h = content_hash(host, bytes);
     std::lock_guard<std::mutex> g(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+    for (Entry& e : cache)
+        if (e.dev == dev && e.hash == h && e.content.size() == bytes && std::memcmp(e.content.data(), host, bytes) == 0) {
+            e.used = ++tick;
+            return e.d;
+        }
+    auto held = [&] {
+        size_t n = 0, b = 0;
+        for (const Entry& e : cache)
+            if (e.dev == dev) { ++n; b += e.content.size(); }
+        return std::make_pair(n, b);
+    };
+    for (auto hb = held(); hb.first > 0 && (hb.first >= kMaxEntries || hb.second + bytes > kMaxBytes); hb = held()) {
+        size_t lru = cache.size();
+        for (size_t i = 0; i < cache.size(); ++i)
+            if (cache[i].dev == dev && (lru == cache.size() || cache[i].used < cache[lru].used)) lru = i;
+        cudaDeviceSynchronize();  // a queued launch may still read the table
+        cudaFree(cache[lru].d);
+        cache.erase(cache.begin() + (ptrdiff_t)lru);
+    }
     void* d = nullptr;
     if (cudaMalloc(&d, bytes ? bytes : 1) != cudaSuccess) throw std::runtime_error("cached_upload: cudaMalloc failed");
     if (bytes && cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
         throw std::runtime_error("cached_upload: cudaMemcpy failed");
-    cache.emplace(std::move(key), d);
+    const uint8_t* hb = static_cast<const uint8_t*>(host);
+    cache.push_back(Entry{dev, h, std::vector<uint8_t>(hb, hb + bytes), d, ++tick});
     return d;
+}
+
+// cudaFuncSetAttribute acts per device: run `set` once per (device, kernel key)
+template <class F>
+inline void func_attr_once(const void* key, F&& set) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, const void*>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    for (const auto& d : done)
+        if (d.first == dev && d.second == key) return;
+    set();
+    done.emplace_back(dev, key);
 }
 
 }  // namespace ck

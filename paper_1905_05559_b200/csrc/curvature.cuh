@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "bands.cuh"
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "model.cuh"
@@ -71,9 +72,9 @@ struct SymKrArgs {
     T* H;
     int64_t ldh, woff, boff;
     T alpha;
-    // row shard: the block's orbit tiles [floor(f0 T), floor(f1 T)) of T, f = the
-    // shard's share of the block's lower triangle (shards partition the orbits)
-    double f0 = 0.0, f1 = 1.0;
+    // output units [u0, u1) (u1 < 0: all) stored at band rows bwoff / bboff (< 0:
+    // the block's own rows woff / boff): see symkr.cuh Params and bands.cuh
+    int64_t u0 = 0, u1 = -1, bwoff = -1, bboff = -1;
 };
 
 template <class T>
@@ -344,9 +345,16 @@ struct Engine {
     // 16-byte addressable, the fused block kernel with the profile
     // delta_k,o delta_m,o'' and no Q term).  Same row-shard contract as opg();
     // returns false where the route does not apply (then J + SYRK).
-    bool opg_kr(const Cache<T>& c, T* G, int64_t ldg, int64_t rlo = 0, int64_t rhi = INT64_MAX) {
+    //
+    // band != null: G holds the unit band's rows (bands.cuh), TF32 only.
+    bool opg_kr(const Cache<T>& c, T* G, int64_t ldg, int64_t rlo = 0, int64_t rhi = INT64_MAX,
+                const UnitBand* band = nullptr) {
         const bool tc = prec == kTF32 && sizeof(T) == 4;
-        if (!(tc || prec == kF32 || prec == kF64) || sym_off()) return false;
+        if (band && !tc) throw CurvError(kContractError, "unit-band assembly needs TF32 precision");
+        if (!(tc || prec == kF32 || prec == kF64) || sym_off()) {
+            if (band) throw CurvError(kContractError, "unit-band assembly needs the symmetric-orbit kernels");
+            return false;
+        }
         const int S = md.S;
         const int64_t n = c.n, ldn = round_up(n, 32);
         std::vector<DevMem> keep;
@@ -362,66 +370,98 @@ struct Engine {
         int64_t ldj = 0;
         {
             ProfScope prep("opg_prep", s, 0.0, 0.0);
-            TransposeBatch<T> tb(s);  // all layers' copies in one launch (flushed at scope end)
+            TransposeBatch<T> tb(s);  // all layers' copies in one launch
             for (int k = 0; k < S; ++k) {
                 akT[k] = buf(md.w[k] + 1, ldn);
                 tb.add(c.a[k], c.lda[k], 0, akT[k], ldn, 0, n, md.w[k] + 1, 1);
                 dT[k] = buf(md.w[k + 1], ldn);
                 tb.add(c.delta[k], c.ldt[k], 0, dT[k], ldn, 0, n, md.w[k + 1], 1);
             }
+            tb.flush();
         }
         for (int k = 0; k < S; ++k) {
             const int64_t Pk = md.block_size(k), tk = md.w[k], uk = md.w[k + 1];
-            if (md.woff[k] + Pk <= rlo || md.woff[k] >= rhi) continue;
+            if (band ? band->u0[k] >= band->u1[k] : (md.woff[k] + Pk <= rlo || md.woff[k] >= rhi)) continue;
             {
-                auto tri = [&](int64_t r) {
-                    const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
-                    return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
-                };
-                const double f0 = tri(rlo), f1 = rhi >= md.woff[k] + Pk ? 1.0 : tri(rhi);
-                const double orbits = (double)uk * (uk + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
-                ProfScope ps("opg_symkr", s, 2.0 * (double)n * orbits * (f1 - f0),
-                             (double)sizeof(T) * (double)Pk * Pk * (f1 - f0));
+                // packed unit pairs (o <= o'') computed: all, or o'' in the band
+                const int64_t v0 = band ? band->u0[k] : 0, v1 = band ? band->u1[k] : uk;
+                const double pairs = ((double)v1 * (v1 + 1) - (double)v0 * (v0 + 1)) / 2.0;
+                const double orbits = pairs * (double)(tk + 1) * (tk + 2) / 2.0;
+                const double stored = band ? (double)(v1 - v0) * (tk + 1) * (double)(md.woff[k] + (v1) * (tk + 1))
+                                           : (double)Pk * Pk;
+                ProfScope ps("opg_symkr", s, 2.0 * (double)n * orbits, (double)sizeof(T) * stored);
                 if (tc) {
-                    SymKrArgs<T> sa{akT[k], dT[k], 1, ldn, n, tk, uk, G, ldg, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
+                    SymKrArgs<T> sa{akT[k], dT[k], 1, ldn, n, tk, uk, G, ldg, md.woff[k], md.boff[k], T(1) / T(n)};
+                    if (band) {
+                        sa.u0 = band->u0[k];
+                        sa.u1 = band->u1[k];
+                        sa.bwoff = band->bw[k];
+                        sa.bboff = band->bb[k];
+                    }
                     if (!SymKr<T>::run(prec, s, sa)) throw CurvError(kCudaError, "opg_kr: diagonal block kernel unavailable");
                 } else {
                     orbit_block(k, akT[k], dT[k], 1, ldn, n, G, ldg, rlo, rhi);
                 }
             }
             if (k == 0) continue;
-            // blocks m < k: one rectangular GEMM G[rows of k, columns of layers < k]
-            // = (1/N) J_k^T J_<k on the tensor cores (the SYRK engine), mirrored
-            const int64_t r0 = std::max(rlo, md.woff[k]), r1 = std::min(rhi, md.woff[k] + Pk);
-            if (r0 % 4 == 0 || !tc) {
-                if (!J.p) {  // (jacobian() times itself as "jacobian")
-                    ldj = round_up(md.P, 32);
-                    J = DevMem((size_t)n * ldj * sizeof(T), s);
-                    jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, tc);
-                }
-                EpiSymLower<T> e{G, ldg, T(1) / T(n), r0};
-                ProfScope ps("opg_gemm", s, 2.0 * (double)(r1 - r0) * md.woff[k] * n,
-                             (double)sizeof(T) * 2.0 * (double)(r1 - r0) * md.woff[k]);
-                auto opj = [&](const T* p) { return tc ? pre_rounded(mnmaj(p, ldj)) : mnmaj(p, ldj); };
-                CurvGemm<T, EpiSymLower<T>>::run(prec, s, r1 - r0, md.woff[k], n, opj(dptr<T>(J) + r0), opj(dptr<T>(J)), e);
-                continue;
+            // blocks m < k: rectangular GEMMs G[rows of k, columns of layers < k] =
+            // (1/N) J_k^T J_<k on the tensor cores (the SYRK engine), mirrored; a band
+            // stores its weight rows and its bias rows (two ranges), unmirrored
+            struct Rows {
+                int64_t r0, r1, b;  // global rows [r0, r1) stored from band row b (-1: in place)
+            };
+            std::vector<Rows> rows;
+            if (band) {
+                rows.push_back({md.woff[k] + band->u0[k] * tk, md.woff[k] + band->u1[k] * tk, band->bw[k]});
+                rows.push_back({md.boff[k] + band->u0[k], md.boff[k] + band->u1[k], band->bb[k]});
+            } else {
+                rows.push_back({std::max(rlo, md.woff[k]), std::min(rhi, md.woff[k] + Pk), -1});
             }
-            const int64_t ak_rows = tk + 256;
-            T* akX = buf(ak_rows, ldn);
-            replicate_rows_kernel<T><<<dim3(blocks_for(ak_rows * ldn), 1), 256, 0, s>>>(akT[k], tk, ldn, akX, ak_rows, 0, 0);
-            CK_LAUNCH();
-            for (int m = k - 1; m >= 0; --m) {
-                const int64_t tm = md.w[m], um = md.w[m + 1];
-                T* pv = buf(uk * um, ldn);
-                outer_delta_kernel<T><<<dim3((unsigned)ceil_div(ldn, 256), (unsigned)um, (unsigned)uk), 256, 0, s>>>(
-                    dT[k], dT[m], um, ldn, pv);
-                CK_LAUNCH();
-                HessFusedArgs<T> fa{akX, ak_rows, nullptr, ak_rows, um * ak_rows, pv, dT[k], c.a[m], c.lda[m], ldn, n,
-                                    tk, tm, um, uk * tk, 0, Pk};
-                EpiHess<T> e{G, ldg, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n), 0, 1, rlo, rhi};
-                const double req = (double)Pk * um * (tm + 1);
-                ProfScope ps("opg_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * 2.0 * req);
-                if (!HessFused<T>::run(prec, s, fa, e)) throw CurvError(kCudaError, "opg_kr: block kernel unavailable");
+            T* akX = nullptr;
+            for (const Rows& rr : rows) {
+                const int64_t r0 = rr.r0, r1 = rr.r1;
+                if (r0 >= r1) continue;
+                if (r0 % 4 == 0 || !tc) {
+                    if (!J.p) {  // (jacobian() times itself as "jacobian")
+                        ldj = round_up(md.P, 32);
+                        J = DevMem((size_t)n * ldj * sizeof(T), s);
+                        jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, tc);
+                    }
+                    ProfScope ps("opg_gemm", s, 2.0 * (double)(r1 - r0) * md.woff[k] * n,
+                                 (double)sizeof(T) * (band ? 1.0 : 2.0) * (double)(r1 - r0) * md.woff[k]);
+                    auto opj = [&](const T* p) { return tc ? pre_rounded(mnmaj(p, ldj)) : mnmaj(p, ldj); };
+                    if constexpr (sizeof(T) == 4) {
+                        if (band) {
+                            gemm_tf32_store(prec, s, r1 - r0, md.woff[k], n, opj(dptr<T>(J) + r0), opj(dptr<T>(J)),
+                                            G + rr.b * ldg, ldg, T(1) / T(n));
+                            continue;
+                        }
+                    }
+                    EpiSymLower<T> e{G, ldg, T(1) / T(n), r0};
+                    CurvGemm<T, EpiSymLower<T>>::run(prec, s, r1 - r0, md.woff[k], n, opj(dptr<T>(J) + r0), opj(dptr<T>(J)), e);
+                    continue;
+                }
+                const int64_t ak_rows = tk + 256;
+                if (!akX) {
+                    akX = buf(ak_rows, ldn);
+                    replicate_rows_kernel<T><<<dim3(blocks_for(ak_rows * ldn), 1), 256, 0, s>>>(akT[k], tk, ldn, akX,
+                                                                                                ak_rows, 0, 0);
+                    CK_LAUNCH();
+                }
+                for (int m = k - 1; m >= 0; --m) {
+                    const int64_t tm = md.w[m], um = md.w[m + 1];
+                    T* pv = buf(uk * um, ldn);
+                    outer_delta_kernel<T><<<dim3((unsigned)ceil_div(ldn, 256), (unsigned)um, (unsigned)uk), 256, 0, s>>>(
+                        dT[k], dT[m], um, ldn, pv);
+                    CK_LAUNCH();
+                    HessFusedArgs<T> fa{akX, ak_rows, nullptr, ak_rows, um * ak_rows, pv, dT[k], c.a[m], c.lda[m], ldn,
+                                        n, tk, tm, um, uk * tk, 0, Pk};
+                    EpiHess<T> e{G, ldg, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n), 0, band ? 0 : 1,
+                                 band ? r0 : rlo, band ? r1 : rhi, band ? r0 - rr.b : 0};
+                    const double req = (double)(r1 - r0) * um * (tm + 1);
+                    ProfScope ps("opg_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * (band ? 1.0 : 2.0) * req);
+                    if (!HessFused<T>::run(prec, s, fa, e)) throw CurvError(kCudaError, "opg_kr: block kernel unavailable");
+                }
             }
         }
         return true;
@@ -462,13 +502,17 @@ struct Engine {
 
     // Tangent rows [rlo, rhi) of H (their lower entries and mirrors); the full
     // assembly is rlo = 0, rhi = P.  Layers with no owned row are skipped.
+    // band != null: H holds the unit band's rows (bands.cuh), TF32 only.
     void hessian(const T* params, const Cache<T>& c, T* H, int64_t ldh, bool verify, int64_t rlo = 0,
-                 int64_t rhi = INT64_MAX) {
+                 int64_t rhi = INT64_MAX, const UnitBand* band = nullptr) {
         const int S = md.S;
         const int64_t n = c.n;
+        if (band && (prec != kTF32 || sizeof(T) != 4 || verify || sym_off()))
+            throw CurvError(kContractError, "unit-band assembly needs TF32 precision");
         for (int k = 0; k < S; ++k) {
             const int64_t np = md.w[k + 1];
-            if (md.woff[k] + md.block_size(k) <= rlo || md.woff[k] >= rhi) continue;
+            if (band ? band->u0[k] >= band->u1[k] : (md.woff[k] + md.block_size(k) <= rlo || md.woff[k] >= rhi))
+                continue;
             std::vector<DevMem> keep;
             // R-op profile buffers: every kernel below writes its output's logical
             // extent and reads only logical extents (checked with CURVKIT_POISON)
@@ -601,16 +645,19 @@ struct Engine {
                 if (fused && m == k && !verify && !sym_off()) {
                     // diagonal block: one value per symmetric orbit (a row shard takes
                     // its share of the block's lower triangle as a range of orbit tiles)
-                    auto tri = [&](int64_t r) {
-                        const double j = (double)std::clamp<int64_t>(r - md.woff[k], 0, Pk);
-                        return j * (j + 1.0) / ((double)Pk * (Pk + 1.0));
-                    };
-                    const double f0 = tri(rlo), f1 = rhi >= md.woff[k] + Pk ? 1.0 : tri(rhi);
+                    const int64_t v0 = band ? band->u0[k] : 0, v1 = band ? band->u1[k] : np;
+                    const double f = ((double)v1 * (v1 + 1) - (double)v0 * (v0 + 1)) / ((double)np * (np + 1));
                     const double orbits = (double)np * (np + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
-                    ProfScope ps("hess_symkr", s, 2.0 * (double)n * orbits * (f1 - f0),
-                                 (double)sizeof(T) * (double)Pk * Pk * (f1 - f0));
-                    SymKrArgs<T> sa{akT, GT, 0, ldn, n, tk, np, H, ldh, md.woff[k], md.boff[k], T(1) / T(n), f0, f1};
+                    ProfScope ps("hess_symkr", s, 2.0 * (double)n * orbits * f, (double)sizeof(T) * (double)Pk * Pk * f);
+                    SymKrArgs<T> sa{akT, GT, 0, ldn, n, tk, np, H, ldh, md.woff[k], md.boff[k], T(1) / T(n)};
+                    if (band) {
+                        sa.u0 = v0;
+                        sa.u1 = v1;
+                        sa.bwoff = band->bw[k];
+                        sa.bboff = band->bb[k];
+                    }
                     if (SymKr<T>::run(prec, s, sa)) jbeg = Pk;
+                    else if (band) throw CurvError(kCudaError, "hessian: diagonal block kernel unavailable");
                 }
                 if (!fused && (prec == kF32 || prec == kF64) && m == k && !verify && !sym_off()) {
                     const double orbits = (double)np * (np + 1) / 2.0 * (double)(tk + 1) * (tk + 2) / 2.0;
@@ -624,6 +671,19 @@ struct Engine {
                     HessFusedArgs<T> fa{akX, ak_rows, m == k ? nullptr : QX[m], ak_rows, tm1 * ak_rows,
                                         m == k ? GT : PT[m], dkT, c.a[m], c.lda[m], ldn, n, tk, tm, tm1, nw,
                                         (m == k && !verify) ? 1 : 0, Pk};
+                    if (band) {  // m < k: the band's weight rows, then its bias rows, unmirrored
+                        const int64_t u0 = band->u0[k], u1 = band->u1[k];
+                        const int64_t rg[2][3] = {{md.woff[k] + u0 * tk, md.woff[k] + u1 * tk, band->bw[k]},
+                                                  {md.boff[k] + u0, md.boff[k] + u1, band->bb[k]}};
+                        for (const auto& g : rg) {
+                            EpiHess<T> e{H, ldh, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n), 0, 0,
+                                         g[0], g[1], g[0] - g[2]};
+                            const double req = (double)(g[1] - g[0]) * tm1 * (tm + 1);
+                            ProfScope ps("hess_fused", s, 2.0 * (double)n * req, (double)sizeof(T) * req);
+                            if (!HessFused<T>::run(prec, s, fa, e)) throw CurvError(kCudaError, "hessian: block kernel unavailable");
+                        }
+                        continue;
+                    }
                     EpiHess<T> e{H, ldh, Pk, 0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
                                  m == k ? 1 : 0, (m == k && verify) ? 0 : 1, rlo, rhi};
                     const int64_t js = std::clamp<int64_t>(rlo - md.woff[k], 0, Pk);

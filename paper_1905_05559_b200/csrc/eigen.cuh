@@ -492,14 +492,12 @@ inline void jacobi_eig(double* A, double* V, int64_t l, int* sweeps, cudaStream_
     const size_t base = (size_t)(m + m / 2 + 1) * sizeof(double);
     const size_t with_a = base + (size_t)l * (l + 1 + ((l + 1) & 1)) * sizeof(double);
     const size_t with_v = with_a + (size_t)l * l * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
+    func_attr_once((const void*)jacobi_kernel<double, false>, [] {
         CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
         CK_CUDA(cudaFuncSetAttribute(jacobi_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
-        attr = true;
-    }
+    });
     if (fp32_vectors && with_v <= 200 * 1024) {
         jacobi_kernel<float, true><<<1, dim3(128, jacobi_ty()), with_v, s>>>(A, V, (int)l, 60, sweeps, 1);
     } else {
@@ -593,12 +591,10 @@ struct EigenWork {
     void chol_inv(double* W, int64_t l, double rel, double* Rinv) {
         const size_t bytes = (size_t)l * l * sizeof(double);
         if (bytes <= 200 * 1024) {
-            static bool attr = false;
-            if (!attr) {
+            func_attr_once((const void*)chol_inv_smem_kernel, [] {
                 CK_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              200 * 1024));
-                attr = true;
-            }
+            });
             chol_inv_smem_kernel<<<1, 1024, bytes, s>>>(W, (int)l, rel, Rinv);
         } else {
             chol_inv_kernel<<<1, 256, 0, s>>>(W, l, rel, Rinv);
@@ -649,6 +645,19 @@ struct EigenWork {
 // communicator of nranks > 1 each rank holds the parameter rows of
 // TopkShard::make(md, nranks, rank); the only exchanges are all-reduces of
 // the N x l product J X and of the l x l Grams.
+__global__ void scale_kernel(double* __restrict__ a, int64_t n, double f) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] *= f;
+}
+
+// out (l x k, row-major) = V[:, sel] (V l x l, eigenvectors by columns)
+template <class T>
+__global__ void select_columns_kernel(const double* __restrict__ V, int64_t l, const int32_t* __restrict__ sel,
+                                      int64_t k, T* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < l * k) out[i] = (T)V[(i / k) * l + sel[i % k]];
+}
+
 // C <- sc C + sb B + sa A on the first l columns of R rows (one Chebyshev
 // three-term step; A may be null)
 template <class T>
@@ -673,7 +682,7 @@ template <class T>
 void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
                uint64_t seed, int prec, T* q_dev, std::vector<double>& lam_host, cudaStream_t s,
                const Comm* comm = nullptr, const T* Jext = nullptr, int64_t ldj_ext = 0, int64_t cheb_steps = 0,
-               int64_t cheb_degree = 0) {
+               int64_t cheb_degree = 0, double cheb_tol = 0.0) {
     const int64_t n = c.n, P = md.P;
     const bool sharded = comm && comm->nranks > 1;
     const TopkShard sh = TopkShard::make(md, sharded ? comm->nranks : 1, sharded ? comm->rank : 0);
@@ -717,10 +726,14 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     EigenWork<T> ew{md, s, prec, &c, krop.get(), sh, sharded ? comm : nullptr};
     // Rayleigh-Ritz on the orthonormal basis X: B = (1/N) (J X)^T (J X) with
     // round-to-nearest TF32 operands (J stored rounded, X rounded per GEMM):
-    // unbiased products.  Leaves the Ritz values on B's diagonal (ha) and the
-    // vectors in hv (both l x l, host).
+    // unbiased products.  B is scaled and diagonalised on the device (Bm ->
+    // Ritz values on its diagonal, V the vectors); only the l Ritz values come
+    // back to the host, for the stop rule and the filter bounds.  Sharded: the
+    // ranks' Grams of the identical all-reduced J X are summed, so every rank
+    // diagonalises the same bytes and takes the same decisions.
     DevMem Bm((size_t)l * l * sizeof(double), s), V((size_t)l * l * sizeof(double), s);
-    std::vector<double> ha(l * l), hv(l * l);
+    std::vector<double> theta(l);
+    const double nr = sharded ? (double)comm->nranks : 1.0;
     auto ritz = [&](const T* X) {
         ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
         ProfScope rr("eig_ritz", s, 2.0 * (double)n * l * l, 0.0);
@@ -731,23 +744,28 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
             gram_kernel<T><<<g, 256, 0, s>>>(dptr<T>(Tn), ldl, n, l, ceil_div(n, ksplit), dptr<double>(Bm));
             CK_LAUNCH();
         }
+        if (sharded) comm->sum(dptr<double>(Bm), (size_t)(l * l), s);
+        scale_kernel<<<blocks_for(l * l), 256, 0, s>>>(dptr<double>(Bm), l * l, 1.0 / ((double)n * nr));
+        CK_LAUNCH();
         ProfScope pj("eig_ritz_eig", s, 0.0, 0.0);
-        std::vector<double> hb(l * l);
-        CK_CUDA(cudaMemcpyAsync(hb.data(), Bm.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK_CUDA(cudaStreamSynchronize(s));
-        for (auto& v : hb) v /= (double)n;
-        CK_CUDA(cudaMemcpyAsync(Bm.p, hb.data(), l * l * sizeof(double), cudaMemcpyHostToDevice, s));
         DevMem sw(sizeof(int), s);
         jacobi_eig(dptr<double>(Bm), dptr<double>(V), l, dptr<int>(sw), s, std::is_same_v<T, float>);
-        CK_CUDA(cudaMemcpyAsync(ha.data(), Bm.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK_CUDA(cudaMemcpyAsync(hv.data(), V.p, l * l * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaMemcpy2DAsync(theta.data(), sizeof(double), Bm.p, (l + 1) * sizeof(double), sizeof(double), l,
+                                  cudaMemcpyDeviceToHost, s));
         int sweeps = 0;
         CK_CUDA(cudaMemcpyAsync(&sweeps, sw.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK_CUDA(cudaStreamSynchronize(s));
         if (getenv("CURVKIT_TRACE"))
             fprintf(stderr, "[curvkit] Rayleigh-Ritz Jacobi: l = %lld, %d sweeps\n", (long long)l, sweeps);
     };
+    auto top_k = [&]() {  // the k largest Ritz values, descending
+        std::vector<double> t(theta);
+        std::sort(t.begin(), t.end(), std::greater<double>());
+        t.resize(k);
+        return t;
+    };
     T* X = dptr<T>(Om);
+    bool have_ritz = false;  // theta / V belong to the final X
     if (cheb_degree == 0) {
         for (int64_t it = 0; it <= power_iters; ++it) {
             ew.apply_j(Jp, ldj, n, X, ldl, l, dptr<T>(Tn), ldl);
@@ -760,12 +778,41 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
         X = ew.orth(dptr<T>(Y), dptr<T>(Y2), R, l, ldl, 2);  // -> Y
         T* bufs[3] = {dptr<T>(Y), dptr<T>(Om), dptr<T>(Y2)};
         const int64_t budget = cheb_steps * cheb_degree;  // operator applications
+        // stop rule (cheb_tol > 0): Ritz values rise monotonically to the
+        // eigenvalues; with the change d_t of round t and the contraction
+        // rho = d_t / d_{t-1}, the remaining error is ~ d_t rho / (1 - rho).  A
+        // value has converged when that is <= cheb_tol (relative), or when its
+        // change is at the arithmetic's noise floor.
+        const double floor_rel = sizeof(T) == 8 ? 1e-13 : 2e-5;
+        std::vector<double> prev, prevd;
         for (int64_t used = 0; used < budget;) {
-            ritz(X);
+            ritz(X);  // Tn = J X: also the first operator application of the filter below
+            have_ritz = true;
+            if (cheb_tol > 0.0) {
+                const std::vector<double> t = top_k();
+                bool done = !prev.empty();
+                std::vector<double> d(k, 0.0);
+                for (int64_t j = 0; j < k && !prev.empty(); ++j) {
+                    d[j] = t[j] - prev[j];
+                    const double c = std::fabs(d[j]) / std::max(std::fabs(t[j]), 1e-300);
+                    bool ok = c <= floor_rel;
+                    if (!ok && !prevd.empty() && prevd[j] > 0.0 && d[j] >= 0.0) {
+                        const double rho = d[j] / prevd[j];
+                        ok = rho < 0.9 && c * rho / (1.0 - rho) <= cheb_tol;
+                    }
+                    done = done && ok;
+                }
+                if (getenv("CURVKIT_TRACE"))
+                    fprintf(stderr, "[curvkit] filter round after %lld applications: theta_k %.8e%s\n", (long long)used,
+                            t[k - 1], done ? " (converged)" : "");
+                if (done) break;
+                if (!prev.empty()) prevd = d;
+                prev = t;
+            }
             double b = INFINITY, top = 0.0;
             for (int64_t j = 0; j < l; ++j) {
-                b = std::min(b, ha[j * l + j]);
-                top = std::max(top, ha[j * l + j]);
+                b = std::min(b, theta[j]);
+                top = std::max(top, theta[j]);
             }
             if (!(b > 0.0)) break;  // basis already spans G's range (rank < l)
             // the filter grows the top Ritz direction by T_d(2 top / b - 1) against <= 1
@@ -787,7 +834,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
             T* Cp = bufs[free_idx[0]];
             T* Dp = bufs[free_idx[1]];  // the third buffer
             for (int64_t d = 1; d <= deg; ++d) {
-                ew.apply_j(Jp, ldj, n, Bp, ldl, l, dptr<T>(Tn), ldl);
+                if (d > 1) ew.apply_j(Jp, ldj, n, Bp, ldl, l, dptr<T>(Tn), ldl);  // d = 1: Tn = J X from ritz()
                 ew.apply_jt(Jp, ldj, n, dptr<T>(Tn), ldl, l, Cp, ldl);  // C = J^T J B = N G B
                 const double sc = (d == 1 ? 1.0 : 2.0) / (e * (double)n), sb = -(d == 1 ? 1.0 : 2.0) * cc / e;
                 if (R > 0) {
@@ -804,34 +851,46 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
             pf.end();
             T* scratch = Ap;  // free after the last step
             X = ew.orth(Bp, scratch, R, l, ldl, 2);  // 2 passes: the filtered columns differ in scale
+            have_ritz = false;
         }
     }
-    ritz(X);
+    if (!have_ritz) ritz(X);
     std::vector<int64_t> ord(l);
     std::iota(ord.begin(), ord.end(), 0);
-    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return ha[a * l + a] > ha[b * l + b]; });
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return theta[a] > theta[b]; });
     lam_host.resize(k);
-    std::vector<T> vk(l * k);  // l x k, row-major
+    std::vector<int32_t> sel(k);
     for (int64_t j = 0; j < k; ++j) {
-        lam_host[j] = ha[ord[j] * l + ord[j]];
-        for (int64_t r = 0; r < l; ++r) vk[r * k + j] = (T)hv[r * l + ord[j]];
+        lam_host[j] = theta[ord[j]];
+        sel[j] = (int32_t)ord[j];
     }
-    ProfScope pr("eig_ritz", s, 2.0 * (double)R * l * k, 0.0);
-    DevMem Vk((size_t)l * k * sizeof(T), s);
-    CK_CUDA(cudaMemcpyAsync(Vk.p, vk.data(), l * k * sizeof(T), cudaMemcpyHostToDevice, s));
+    // eigenvectors Q = X V[:, sel] (rows of this rank), on the tensor cores with
+    // fp32-grade 3xTF32 products where the shape allows
+    ProfScope pr("eig_ritz_vectors", s, 2.0 * (double)R * l * k, 0.0);
+    DevMem Vk((size_t)l * k * sizeof(T), s), dsel((size_t)k * sizeof(int32_t), s);
+    CK_CUDA(cudaMemcpyAsync(dsel.p, sel.data(), k * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    select_columns_kernel<T><<<blocks_for(l * k), 256, 0, s>>>(dptr<double>(V), l, dptr<int32_t>(dsel), k, dptr<T>(Vk));
+    CK_LAUNCH();
     EpiStore<T> e{q_dev, k, 0, T(1), T(0)};
-    if (R > 0) gemm_simt<T>(s, R, k, l, 1, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
+    bool done = false;
+    if constexpr (std::is_same_v<T, float>) {
+        if ((prec == kTF32 || prec == k3xTF32) && R >= 512 && k % 4 == 0) {
+            gemm_tf32(k3xTF32, s, R, k, l, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
+            done = true;
+        }
+    }
+    if (!done && R > 0) gemm_simt<T>(s, R, k, l, 1, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
     CK_CUDA(cudaStreamSynchronize(s));
 }
 
 template <class T>
 void host_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
                uint64_t seed, int prec, double* q_out, double* lambda_out, cudaStream_t s, int64_t cheb_steps = 0,
-               int64_t cheb_degree = 0) {
+               int64_t cheb_degree = 0, double cheb_tol = 0.0) {
     DevMem q((size_t)md.P * k * sizeof(T), s);
     std::vector<double> lam;
     topk_core<T>(md, c, k, oversample, power_iters, seed, prec, dptr<T>(q), lam, s, nullptr, nullptr, 0, cheb_steps,
-                 cheb_degree);
+                 cheb_degree, cheb_tol);
     std::vector<T> hq((size_t)md.P * k);
     CK_CUDA(cudaMemcpyAsync(hq.data(), q.p, hq.size() * sizeof(T), cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
@@ -842,10 +901,10 @@ void host_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
 template <class T>
 void dev_topk(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversample, int64_t power_iters,
               uint64_t seed, int prec, T* q_dev, T* lam_dev, cudaStream_t s, const Comm* comm = nullptr,
-              int64_t cheb_steps = 0, int64_t cheb_degree = 0) {
+              int64_t cheb_steps = 0, int64_t cheb_degree = 0, double cheb_tol = 0.0) {
     std::vector<double> lam;
     topk_core<T>(md, c, k, oversample, power_iters, seed, prec, q_dev, lam, s, comm, nullptr, 0, cheb_steps,
-                 cheb_degree);
+                 cheb_degree, cheb_tol);
     std::vector<T> hl(lam.begin(), lam.end());
     CK_CUDA(cudaMemcpyAsync(lam_dev, hl.data(), k * sizeof(T), cudaMemcpyHostToDevice, s));
     CK_CUDA(cudaStreamSynchronize(s));

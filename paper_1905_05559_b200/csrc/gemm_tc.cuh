@@ -1375,12 +1375,10 @@ template <int BN, class Epi>
 void launch(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& alo,
             const CUtensorMap& blo, const Epi& e) {
     const int smem = TcSmem<BN>::bytes(sh.nsplit);
-    static bool attr_set = false;
-    if (!attr_set) {
+    func_attr_once((const void*)tc_gemm_kernel<BN, Epi>, [] {
         CK_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      std::max(TcSmem<BN>::bytes(1), TcSmem<BN>::bytes(3))));
-        attr_set = true;
-    }
+    });
     const int64_t tiles = ceil_div(sh.M, BM) * ceil_div(sh.N, BN);
     const int grid = (int)std::min<int64_t>(tiles, num_sms());
     tc_gemm_kernel<BN, Epi><<<grid, kThreads, smem, s>>>(a, b, alo, blo, sh, e);
@@ -1392,12 +1390,10 @@ void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const 
                  const CUtensorMap& alo, const CUtensorMap& blo, const Epi& e) {
     using S = pair::PairSmem<BN>;
     const int smem = S::bytes(sh.nsplit);
-    static bool attr_set = false;
-    if (!attr_set) {
+    func_attr_once((const void*)pair::tc_gemm_pair_kernel<BN, Epi>, [] {
         CK_CUDA(cudaFuncSetAttribute(pair::tc_gemm_pair_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      std::max(S::bytes(1), S::bytes(3))));
-        attr_set = true;
-    }
+    });
     const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN) * std::max(1, sh.ksplit);
     const int grid = 2 * (int)std::min<int64_t>(tiles, num_sms() / 2);
     CUtensorMap mc = a;  // unused unless the epilogue stores by TMA
@@ -1619,12 +1615,10 @@ struct HessFused<float> {
         CK_LAUNCH();
         CUtensorMap mb = tc::make_map(dptr<float>(amr), N, a.n, a.lda_m, 1, BN / 2, b3);
         using S = pair::FusedSmem<BN>;
-        static bool attr = false;
-        if (!attr) {
+        func_attr_once((const void*)pair::tc_hess_fused_kernel<BN, EpiHess<float>, TS>, [] {
             CK_CUDA(cudaFuncSetAttribute(pair::tc_hess_fused_kernel<BN, EpiHess<float>, TS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(S::bytes(0), S::bytes(1))));
-            attr = true;
-        }
+        });
         int grid = 2 * (int)std::min<int64_t>(fh.ntiles, tc::num_sms() / 2);
         if (const char* g = getenv("CURVKIT_DEV_GRID")) grid = std::min(grid, 2 * (atoi(g) / 2));  // dev: fewer SMs
         static const bool tracing = getenv("CURVKIT_TRACE") != nullptr;

@@ -411,11 +411,9 @@ template <bool JT>
 void kr_launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const tc::pair::KrArgs& ka, int a3d,
                int b3d) {
     using C = tc::pair::KrCfg<JT>;
-    static bool attr = false;
-    if (!attr) {
+    func_attr_once((const void*)tc::pair::kr_kernel<JT>, [] {
         CK_CUDA(cudaFuncSetAttribute(tc::pair::kr_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES));
-        attr = true;
-    }
+    });
     const int64_t units = ka.mt * (JT ? ka.nop * ka.ksplit : ceil_div(ka.nop, ka.chunk));
     const int grid = 2 * (int)std::min<int64_t>(units, tc::num_sms() / 2);
     tc::pair::kr_kernel<JT><<<grid, C::THREADS, C::BYTES, s>>>(ma, mb, ka, (uint32_t)tc::BK * 128u, 512u, 1024u, a3d,

@@ -586,7 +586,9 @@ struct TransposeBatch {
         J.n = 0;
         J.blocks = 0;
     }
-    ~TransposeBatch() { flush(); }
+    // never launches (a destructor must not throw): callers flush() explicitly;
+    // jobs still pending here belong to a call that is unwinding on an error
+    ~TransposeBatch() { J.n = 0; }
 };
 
 template <class T>
@@ -611,6 +613,8 @@ struct EpiHess {
     // shard of tangent rows owned by this call (global H row of the lower
     // entry); entries of other rows and their mirrors are left untouched
     int64_t rlo = 0, rhi = INT64_MAX;
+    // band output (unit bands): H holds row gr at H + (gr - rsh) * ldh; no mirrors
+    int64_t rsh = 0;
     __host__ __device__ __forceinline__ bool owns(int64_t gr) const { return gr >= rlo && gr < rhi; }
     __host__ __device__ __forceinline__ int64_t gcol(int64_t opp, int64_t c) const {
         return c < tm ? woffm + opp * tm + c : boffm + opp;
@@ -629,15 +633,15 @@ struct EpiHess {
         if (!owns(gr)) return;
         if (diag && mirror) {
             if (gc > gr) return;
-            H[gr * ldh + gc] = v;
+            H[(gr - rsh) * ldh + gc] = v;
             H[gc * ldh + gr] = v;
         } else {
-            H[gr * ldh + gc] = v;
+            H[(gr - rsh) * ldh + gc] = v;
             if (mirror) H[gc * ldh + gr] = v;
         }
     }
     // 32 x 32 block stored by two TMA boxes (direct at (gr0, gc0), mirror at
-    // (gc0, gr0)): rows in one band and owned, columns inside the weight
+    // (gc0, gr0); gr0 returned as the storage row): rows in one band and owned, columns inside the weight
     // columns, and on diagonal blocks strictly below the diagonal
     __device__ bool tma_block(int64_t row0, int64_t col0, int64_t M, int64_t N, int64_t& gr0, int64_t& gc0) const {
         if (row0 + 32 > M || col0 + 32 > N || col0 + 32 > tm) return false;
@@ -646,7 +650,9 @@ struct EpiHess {
         gr0 = woffk + j0 + jj;
         if (gr0 < rlo || gr0 + 32 > rhi) return false;
         gc0 = woffm + opp * tm + col0;
-        return !(diag && mirror && gc0 + 31 >= gr0);
+        const bool ok = !(diag && mirror && gc0 + 31 >= gr0);
+        gr0 -= rsh;  // storage row (band output); mirrors are off there
+        return ok;
     }
     // register-only epilogue (fused kernel): lane = row row0 + lane holds the
     // 32 accumulators of columns col0 .. col0 + 31 in v[]; the row's entries
@@ -661,7 +667,7 @@ struct EpiHess {
         if (!owns(gr)) return;
         const int ncols = (int)::min((int64_t)32, N - col0);
         const int64_t wbase = woffm + opp * tm;
-        T* row = H + gr * ldh;
+        T* row = H + (gr - rsh) * ldh;
         if constexpr (sizeof(T) == 4) {
             // whole 32-column run inside the weight columns and the triangle
             const int64_t gc0 = wbase + col0;
@@ -713,7 +719,7 @@ struct EpiHess {
                 const int64_t gr = woffk + j0 + jj, wb = woffm + opp * tm;
                 if (!owns(gr)) continue;
                 const float4 x = get(r, q);
-                T* row = H + gr * ldh;
+                T* row = H + (gr - rsh) * ldh;
                 if constexpr (sizeof(T) == 4) {
                     const int64_t gc = wb + c;
                     if (c + 3 < tm && c + 3 < N && ((gc | ldh) & 3) == 0 && (!tri || gc + 3 <= gr)) {

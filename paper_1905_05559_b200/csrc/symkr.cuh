@@ -84,6 +84,11 @@ struct Params {
     float alpha;
     int tma;             // H boxes by TMA (else every entry by the scalar path)
     int dev;             // dev experiments (CURVKIT_DEV_SYMKR): 1 no transform, 2 no epilogue stores, 32 MMA loop alone (+64 no per-K-block commits)
+    // output rows: units [u0, u1) of the block; row (o, x) of the block is stored
+    // at H row bwoff + (o - u0) T_k + x (weights) / bboff + (o - u0) (bias).  The
+    // whole block is u0 = 0, u1 = U, bwoff = woff, bboff = boff (unit bands:
+    // DESIGN.md section 7).  Columns are always the global ones.
+    int64_t u0, u1, bwoff, bboff;
 };
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -131,9 +136,14 @@ __device__ __forceinline__ void tmem_ld_wait8(uint32_t (&r)[8]) {
                  : "memory");
 }
 
-// H row / column of (unit o, abar index x): weight (o, x) or the bias of o
+// H column of (unit o, abar index x): weight (o, x) or the bias of o
 __device__ __forceinline__ int64_t hidx(const Params& p, int64_t o, int64_t x) {
     return x < p.tk ? p.woff + o * p.tk + x : p.boff + o;
+}
+// storage row of (unit o, abar index x), -1 outside the output units
+__device__ __forceinline__ int64_t srow(const Params& p, int64_t o, int64_t x) {
+    if (o < p.u0 || o >= p.u1) return -1;
+    return x < p.tk ? p.bwoff + (o - p.u0) * p.tk + x : p.bboff + (o - p.u0);
 }
 
 // H maps: [0..3] = orbit types 1..4 with o''-extent 8, [4..7] with extent 1
@@ -384,8 +394,18 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                             const CUtensorMap* mp = &hm.m[(bx.z == 1 ? 0 : 4) + quad];
                             const bool ic = quad == 0 || quad == 3;  // types 1, 4: [o''][i][c]
                             const float* src = (ic ? sA : sB) + lane * 128;
-                            if (ic) tma_store_4d(mp, src, (int32_t)c0, (int32_t)i0, bx.y, bx.x);
-                            else tma_store_4d(mp, src, (int32_t)i0, (int32_t)c0, bx.y, bx.x);
+                            // the row unit is o (types 1, 3: dim 3) or o'' (types 2, 4: dim 2),
+                            // counted from u0; rows outside the output units are clipped by TMA
+                            // (a negative coordinate is an illegal TMA store on sm_100: images
+                            // of types 1, 3 with o < u0 lie wholly outside and are skipped; o''
+                            // >= u0 for every packed column)
+                            const bool row_o = quad == 0 || quad == 2;
+                            const int32_t d2 = bx.y - (row_o ? 0 : (int32_t)p.u0);
+                            const int32_t d3 = bx.x - (row_o ? (int32_t)p.u0 : 0);
+                            if (d3 >= 0) {
+                                if (ic) tma_store_4d(mp, src, (int32_t)c0, (int32_t)i0, d2, d3);
+                                else tma_store_4d(mp, src, (int32_t)i0, (int32_t)c0, d2, d3);
+                            }
                         }
                     }
                     if (lane < CH) bulk_commit();  // one group per chunk and lane (wait_group.read 1 above)
@@ -396,12 +416,14 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                     for (int e = 0; e < CH; ++e) {
                         if (e >= ncol) break;
                         const int4 pr = __ldg(&p.pairs[J0 + e]);
-                        const int64_t r1 = hidx(p, pr.x, ii), c1 = hidx(p, pr.y, cc);
-                        const int64_t r3 = hidx(p, pr.x, cc), c3 = hidx(p, pr.y, ii);
-                        p.H[r1 * p.ldh + c1] = v[e];
-                        p.H[c1 * p.ldh + r1] = v[e];
-                        p.H[r3 * p.ldh + c3] = v[e];
-                        p.H[c3 * p.ldh + r3] = v[e];
+                        // the four orbit entries (row unit, col unit): (o,i;o'',c) (o'',c;o,i)
+                        // (o,c;o'',i) (o'',i;o,c); rows outside the output units are skipped
+                        const int64_t s1 = srow(p, pr.x, ii), s2 = srow(p, pr.y, cc);
+                        const int64_t s3 = srow(p, pr.x, cc), s4 = srow(p, pr.y, ii);
+                        if (s1 >= 0) p.H[s1 * p.ldh + hidx(p, pr.y, cc)] = v[e];
+                        if (s2 >= 0) p.H[s2 * p.ldh + hidx(p, pr.x, ii)] = v[e];
+                        if (s3 >= 0) p.H[s3 * p.ldh + hidx(p, pr.y, ii)] = v[e];
+                        if (s4 >= 0) p.H[s4 * p.ldh + hidx(p, pr.x, cc)] = v[e];
                     }
                 }
             }
@@ -424,13 +446,13 @@ done:
 
 }  // namespace sym
 
-// 4-D map of one orbit type over the diagonal block at H + woff * (ldh + 1):
-// dims (d0, d1, U, U) with element strides (1, s1, s2, s3), box (b0, b1, E, 1)
-inline CUtensorMap make_map_orbit(float* H, int64_t ldh, int64_t woff, int64_t d0, int64_t d1, int64_t U, int64_t s1,
+// 4-D map of one orbit type over the diagonal block's output rows at `base`
+// (the entry of row (u0, 0), column (0, 0)): dims (d0, d1, d2, d3) with element
+// strides (1, s1, s2, s3), box (b0, b1, E, 1)
+inline CUtensorMap make_map_orbit(float* base, int64_t d0, int64_t d1, int64_t d2, int64_t d3, int64_t s1,
                                   int64_t s2, int64_t s3, int b0, int b1, int E) {
     CUtensorMap m;
-    float* base = H + woff * ldh + woff;
-    cuuint64_t dims[4] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)U, (cuuint64_t)U};
+    cuuint64_t dims[4] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2, (cuuint64_t)d3};
     cuuint64_t str[3] = {(cuuint64_t)s1 * 4, (cuuint64_t)s2 * 4, (cuuint64_t)s3 * 4};
     cuuint32_t box[4] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)E, 1}, es[4] = {1, 1, 1, 1};
     if ((reinterpret_cast<uintptr_t>(base) & 15) || (str[0] & 15) || (str[1] & 15) || (str[2] & 15))
@@ -488,20 +510,26 @@ struct SymKr<float> {
         const int tma = tma_ok(a.H, a.ldh, a.woff, a.tk) ? 1 : 0;
         namespace sym = tc::sym;
         const int64_t U = a.U, tk = a.tk;
-        const int64_t np = U * (U + 1) / 2;
-        // packed columns (o <= o''), o-major
+        // output units [u0, u1): the packed columns (o <= o'') with o'' in [u0, u1)
+        // carry every entry of those units' rows whose column unit is <= the row's
+        // (the entries of the other orbit images fall outside and are not stored)
+        const int64_t u0 = a.u0, u1 = a.u1 < 0 ? U : a.u1;
+        if (u0 < 0 || u1 > U || u0 >= u1) return true;
+        const int64_t bwoff = a.bwoff < 0 ? a.woff : a.bwoff, bboff = a.bboff < 0 ? a.boff : a.bboff;
+        // packed columns, o-major
         std::vector<int4> pairs;
-        pairs.reserve(np);
-        for (int64_t o = 0; o < U; ++o)
-            for (int64_t q = o; q < U; ++q) pairs.push_back(make_int4((int)o, (int)q, 0, 0));
+        for (int64_t o = 0; o < u1; ++o)
+            for (int64_t q = std::max(o, u0); q < u1; ++q) pairs.push_back(make_int4((int)o, (int)q, 0, 0));
+        const int64_t np = (int64_t)pairs.size();
         // TMA box decomposition per 8-column chunk (chunks start at multiples of 8:
-        // tile widths are multiples of 16): runs of one o with consecutive o''
+        // tile widths are multiples of 16): runs of one o with consecutive o''; a
+        // run ending at u1 may take the extent-8 box (the maps clip at u1)
         for (int64_t j0 = 0; j0 < np; j0 += sym::CH) {
             const int64_t j1 = std::min<int64_t>(np, j0 + sym::CH);
             for (int64_t e = j0; e < j1;) {
                 int64_t L = 1;
                 while (e + L < j1 && pairs[e + L].x == pairs[e].x) ++L;
-                const bool wide = L == sym::CH || pairs[e].y + L == U;
+                const bool wide = L == sym::CH || pairs[e].y + L == u1;
                 if (wide) pairs[e].z = 1;
                 else
                     for (int64_t u = 0; u < L; ++u) pairs[e + u].z = 2;
@@ -532,13 +560,6 @@ struct SymKr<float> {
                             for (int64_t cb = std::max(ib, CB); cb < std::min(nb, CB + SB); ++cb)
                                 tiles.push_back(make_int4((int)ib, (int)cb, (int)nt, 0));
         }
-        {  // row shard: a contiguous range of the (equal-work) orbit tiles
-            const int64_t T = (int64_t)tiles.size();
-            const int64_t t0 = std::clamp<int64_t>((int64_t)std::floor(a.f0 * (double)T), 0, T);
-            const int64_t t1 = a.f1 >= 1.0 ? T : std::clamp<int64_t>((int64_t)std::floor(a.f1 * (double)T), t0, T);
-            tiles = std::vector<int4>(tiles.begin() + t0, tiles.begin() + t1);
-            if (tiles.empty()) return true;
-        }
         const int4* dpairs = static_cast<const int4*>(cached_upload(pairs.data(), pairs.size() * sizeof(int4)));
         const int4* dtiles = static_cast<const int4*>(cached_upload(tiles.data(), tiles.size() * sizeof(int4)));
         // packed profiles (B operand, K-major rows of ldn examples), rounded to nearest TF32
@@ -555,30 +576,32 @@ struct SymKr<float> {
         CUtensorMap mpi = tc::make_map(dptr<float>(pi), np, a.n, a.ldn, 0, (int)(bn / 2));
         tc::sym::HMaps hm;
         std::memset(&hm, 0, sizeof hm);
-        const int64_t L = a.ldh;
+        const int64_t L = a.ldh, nu = u1 - u0;
+        // row unit dims count from u0 (nu units), column unit dims end at u1: the
+        // TMA clips every image whose row lies outside the output units
+        float* base = a.H + bwoff * L + a.woff;
         for (int x = 0; tma && x < 2; ++x) {
             const int E = x == 0 ? 8 : 1;
-            // type 1: H[(o,i),(o'',c)]  d = (c, i, o'', o), strides (1, L, tk, tk L)
-            hm.m[4 * x + 0] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk, tk * L, 16, 8, E);
-            // type 2: H[(o'',c),(o,i)]  d = (i, c, o'', o), strides (1, L, tk L, tk)
-            hm.m[4 * x + 1] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk * L, tk, 8, 16, E);
-            // type 3: H[(o,c),(o'',i)]  d = (i, c, o'', o), strides (1, L, tk, tk L)
-            hm.m[4 * x + 2] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk, tk * L, 8, 16, E);
-            // type 4: H[(o'',i),(o,c)]  d = (c, i, o'', o), strides (1, L, tk L, tk)
-            hm.m[4 * x + 3] = tc::make_map_orbit(a.H, L, a.woff, tk, tk, U, L, tk * L, tk, 16, 8, E);
+            // type 1: H[(o,i),(o'',c)]  d = (c, i, o'' col, o row), strides (1, L, tk, tk L)
+            hm.m[4 * x + 0] = tc::make_map_orbit(base, tk, tk, u1, nu, L, tk, tk * L, 16, 8, E);
+            // type 2: H[(o'',c),(o,i)]  d = (i, c, o'' row, o col), strides (1, L, tk L, tk)
+            hm.m[4 * x + 1] = tc::make_map_orbit(base, tk, tk, nu, u1, L, tk * L, tk, 8, 16, E);
+            // type 3: H[(o,c),(o'',i)]  d = (i, c, o'' col, o row), strides (1, L, tk, tk L)
+            hm.m[4 * x + 2] = tc::make_map_orbit(base, tk, tk, u1, nu, L, tk, tk * L, 8, 16, E);
+            // type 4: H[(o'',i),(o,c)]  d = (c, i, o'' row, o col), strides (1, L, tk L, tk)
+            hm.m[4 * x + 3] = tc::make_map_orbit(base, tk, tk, nu, u1, L, tk * L, tk, 16, 8, E);
         }
         sym::Params prm{dtiles, (int64_t)tiles.size(), dpairs, np, bn, tk,
-                        ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, tma, 0};
+                        ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, tma, 0,
+                        u0, u1, bwoff, bboff};
         static const int dev = getenv("CURVKIT_DEV_SYMKR") ? atoi(getenv("CURVKIT_DEV_SYMKR")) : 0;
         prm.dev = dev;
-        static bool attr = false;
-        if (!attr) {
+        func_attr_once((const void*)sym::symkr_kernel<true>, [] {
             CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sym::Cfg<true>::SMEM_BYTES));
             CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sym::Cfg<false>::SMEM_BYTES));
-            attr = true;
-        }
+        });
         const int grid = 2 * (int)std::min<int64_t>((int64_t)tiles.size(), tc::num_sms() / 2);
         if (zt)
             sym::symkr_kernel<true><<<grid, sym::kThreads, sym::Cfg<true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);

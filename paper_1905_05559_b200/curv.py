@@ -332,24 +332,35 @@ def assemble_opg(spec: ModelSpec, params, dataset: Batch, config: CurvatureConfi
     return g
 
 
-def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 20, power_iters: int = 2,
-             seed: int = 0, precision: str = "f64", filter_steps: int = 0, filter_degree: int = 0) -> EigenPairs:
-    """Top-k eigenpairs of G = (1/N) J^T J by a randomized range finder
-    (replaces eigensolve.hpp:80-81 opg_eigs_incremental).  Eigenvalues are
-    descending; columns of q are orthonormal eigenvectors.  filter_degree > 0
-    replaces the power iterations by filter_steps rounds of a Chebyshev
-    filter of that degree (curvkit_opg_topk_filtered)."""
+def opg_eigs(spec: ModelSpec, params, dataset: Batch, k: int, oversample: int = 20, power_iters: int = None,
+             seed: int = 0, precision: str = "f64", filter_steps: int = 0, filter_degree: int = 0,
+             tol: float = 1e-4, max_applications: int = 96) -> EigenPairs:
+    """Top-k eigenpairs of G = (1/N) J^T J without forming G (replaces
+    eigensolve.hpp:80-81 opg_eigs_incremental).  Eigenvalues descending,
+    columns of q orthonormal eigenvectors.
+
+    Default: Chebyshev-filtered subspace iteration stopped once every Ritz
+    value has converged to `tol` (curvkit_opg_topk_auto; tol = 1e-4 holds the
+    1e-3 eigenvalue bar).  power_iters = p runs the plain randomized range
+    finder with p power iterations instead (BASELINE config 4 quotes p = 2,
+    which on a flat spectrum leaves the Ritz values ~10% low: DESIGN.md
+    section 5); filter_degree > 0 runs filter_steps fixed rounds."""
     P, params, x, y, n = _inputs(spec, params, dataset)
     q = np.empty((P, k))
     lam = np.empty(k)
+    lib = _lib.load()
     if filter_degree > 0:
-        _lib.check(_lib.load().curvkit_opg_topk_filtered(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
-                                                          int(oversample), int(filter_steps), int(filter_degree),
-                                                          int(seed), _prec(precision), _p(q), _p(lam)))
+        _lib.check(lib.curvkit_opg_topk_filtered(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
+                                                 int(oversample), int(filter_steps), int(filter_degree),
+                                                 int(seed), _prec(precision), _p(q), _p(lam)))
+    elif power_iters is not None:
+        _lib.check(lib.curvkit_opg_topk(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
+                                        int(oversample), int(power_iters), int(seed), _prec(precision),
+                                        _p(q), _p(lam)))
     else:
-        _lib.check(_lib.load().curvkit_opg_topk(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
-                                                 int(oversample), int(power_iters), int(seed), _prec(precision),
-                                                 _p(q), _p(lam)))
+        _lib.check(lib.curvkit_opg_topk_auto(C.byref(spec._c()), _p(params), _p(x), _p(y), n, int(k),
+                                             int(oversample), float(tol), int(max_applications), int(seed),
+                                             _prec(precision), _p(q), _p(lam)))
     return EigenPairs(q, lam)
 
 
@@ -562,23 +573,71 @@ def dev_gemm(m, n, k, a, lda, a_kmajor, b, ldb, b_kmajor, c, ldc, alpha=1.0, pre
                                              _ptr(c), ldc, float(alpha), _prec(precision), _stream(stream)))
 
 
-def shard_rows(p: int, nshards: int, shard: int):
-    """Row range [begin, end) of shard `shard` (triangle-area balanced, 32-aligned)."""
-    b, e = C.c_int64(), C.c_int64()
-    _lib.check(_lib.load().curvkit_shard_rows(p, nshards, shard, C.byref(b), C.byref(e)))
-    return b.value, e.value
+# ---- unit bands: multi-GPU H and G (bands.cuh) ------------
+
+PRODUCT = {"hessian": 0, "opg": 1}
 
 
-def dev_hessian_shard(spec, params, x, labels, n, row_begin, row_end, out, ldh, precision="tf32", stream=None):
-    _lib.check(_lib.load().curvkit_dev_hessian_shard(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
-                                                      _prec(precision), row_begin, row_end, _ptr(out), ldh,
+def shard_units(spec: ModelSpec, nshards: int, shard: int):
+    """(unit_begin, unit_end, band_rows): the output units [unit_begin[k],
+    unit_end[k]) of every layer k owned by `shard`, and its band's row count."""
+    S = len(spec.layer_widths) - 1
+    u0, u1, rows = (C.c_int64 * S)(), (C.c_int64 * S)(), C.c_int64()
+    _lib.check(_lib.load().curvkit_shard_units(C.byref(spec._c()), nshards, shard, u0, u1, C.byref(rows)))
+    return list(u0), list(u1), rows.value
+
+
+def shard_units_rows(spec: ModelSpec, nshards: int, shard: int) -> int:
+    return shard_units(spec, nshards, shard)[2]
+
+
+def band_rows_index(spec: ModelSpec, nshards: int, shard: int) -> np.ndarray:
+    """Global row of every band row (weights of the units, then their biases, per layer)."""
+    u0, u1, _ = shard_units(spec, nshards, shard)
+    w = spec.layer_widths
+    out = []
+    for k in range(len(w) - 1):
+        wo, bo = weight_block_offset(spec, k), bias_block_offset(spec, k)
+        out.append(np.arange(wo + u0[k] * w[k], wo + u1[k] * w[k]))
+        out.append(np.arange(bo + u0[k], bo + u1[k]))
+    return np.concatenate(out).astype(np.int64)
+
+
+def unit_ids(spec: ModelSpec) -> np.ndarray:
+    """Unit of every parameter row in the unit-major order (layers, then units)."""
+    w = spec.layer_widths
+    out, base = [], 0
+    for k in range(len(w) - 1):
+        out.append(base + np.repeat(np.arange(w[k + 1]), w[k]))
+        out.append(base + np.arange(w[k + 1]))
+        base += w[k + 1]
+    return np.concatenate(out)
+
+
+def dev_assemble_band(spec, product, params, x, labels, n, nshards, shard, band, ld, precision="tf32", stream=None):
+    """This shard's unit band of H (product "hessian") or G ("opg")."""
+    p = PRODUCT[product] if isinstance(product, str) else int(product)
+    _lib.check(_lib.load().curvkit_dev_assemble_band(C.byref(spec._c()), p, _ptr(params), _ptr(x), _ptr(labels), n,
+                                                      _prec(precision), nshards, shard, _ptr(band), ld,
                                                       _stream(stream)))
 
 
-def dev_opg_shard(spec, params, x, labels, n, row_begin, row_end, out, ldg, precision="tf32", stream=None):
-    _lib.check(_lib.load().curvkit_dev_opg_shard(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
-                                                  _prec(precision), row_begin, row_end, _ptr(out), ldg,
-                                                  _stream(stream)))
+def dev_band_scatter(spec, nshards, shard, band, ld, full, ldf, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_band_scatter(C.byref(spec._c()), _prec(precision), nshards, shard, _ptr(band),
+                                                     ld, _ptr(full), ldf, _stream(stream)))
+
+
+def dev_symmetrize_units(spec, full, ldf, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_symmetrize_units(C.byref(spec._c()), _prec(precision), _ptr(full), ldf,
+                                                         _stream(stream)))
+
+
+def dev_gather_bands(spec, band, ld, full, ldf, comm, precision="tf32", stream=None):
+    """Final gather: every rank's band to rank 0, assembled into the full
+    symmetric matrix there (full may be None on other ranks)."""
+    _lib.check(_lib.load().curvkit_dev_gather_bands(C.byref(spec._c()), _prec(precision), _ptr(band), ld,
+                                                     C.c_void_p(0) if full is None else _ptr(full), ldf,
+                                                     _stream(stream), comm.handle))
 
 
 # ---- multi-GPU top-k (parameter-row shards, NCCL all-reduce of J X) --------
@@ -614,6 +673,54 @@ class Comm:
         _lib.check(_lib.load().curvkit_comm_init(buf, world, rank, C.byref(h)))
         return cls(h, rank, world)
 
+    @classmethod
+    def create_host(cls, rank: int, world: int, group=None):
+        """A communicator whose exchanges run over torch.distributed on host
+        memory (e.g. the gloo backend) -- for ranks NCCL cannot serve, such as
+        several processes sharing one GPU."""
+        import torch
+        import torch.distributed as dist
+
+        def allreduce(buf, count, dtype, user):
+            try:
+                npt = np.float64 if dtype == 1 else np.float32
+                a = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_double if dtype == 1 else C.c_float)),
+                                          shape=(count,))
+                t = torch.from_numpy(a)
+                dist.all_reduce(t, group=group)
+                del npt
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def gather(send, send_bytes, recv, recv_bytes, root, user):
+            try:
+                sizes = [int(recv_bytes[r]) for r in range(world)]
+                mx = max(max(sizes), 1)
+                t = torch.zeros(mx, dtype=torch.uint8)
+                if send_bytes > 0:
+                    t[:send_bytes] = torch.frombuffer(C.string_at(send, send_bytes), dtype=torch.uint8)
+                lst = [torch.empty(mx, dtype=torch.uint8) for _ in range(world)] if rank == root else None
+                dist.gather(t, lst, dst=root, group=group)
+                if rank == root:
+                    off = 0
+                    for r in range(world):
+                        if sizes[r] > 0:
+                            C.memmove(recv + off, lst[r].numpy().ctypes.data, sizes[r])
+                        off += sizes[r]
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        ar = _lib.HOST_ALLREDUCE(allreduce)
+        ga = _lib.HOST_GATHER(gather)
+        h = C.c_void_p()
+        _lib.check(_lib.load().curvkit_comm_init_host(world, rank, C.cast(ar, C.c_void_p), C.cast(ga, C.c_void_p),
+                                                       None, C.byref(h)))
+        c = cls(h, rank, world)
+        c._keep = (ar, ga)  # the callbacks live as long as the communicator
+        return c
+
     def close(self):
         if self.handle is not None:
             _lib.check(_lib.load().curvkit_comm_destroy(self.handle))
@@ -635,6 +742,22 @@ def dev_opg_topk_sharded_filtered(spec, params, x, labels, n, k, oversample, fil
     _lib.check(_lib.load().curvkit_dev_opg_topk_sharded_filtered(
         C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n, k, oversample, filter_steps, filter_degree, seed,
         _prec(precision), _ptr(q), _ptr(lam), _stream(stream), comm.handle))
+
+
+def dev_opg_topk_auto(spec, params, x, labels, n, k, oversample, seed, q, lam, tol=1e-4, max_applications=96,
+                      precision="tf32", stream=None):
+    """Top-k of G to `tol` (curvkit_dev_opg_topk_auto): Chebyshev-filtered
+    subspace iteration with the Ritz-convergence stop rule."""
+    _lib.check(_lib.load().curvkit_dev_opg_topk_auto(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n, k,
+                                                      oversample, float(tol), int(max_applications), seed,
+                                                      _prec(precision), _ptr(q), _ptr(lam), _stream(stream)))
+
+
+def dev_opg_topk_sharded_auto(spec, params, x, labels, n, k, oversample, seed, q, lam, comm, tol=1e-4,
+                              max_applications=96, precision="tf32", stream=None):
+    _lib.check(_lib.load().curvkit_dev_opg_topk_sharded_auto(
+        C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n, k, oversample, float(tol), int(max_applications),
+        seed, _prec(precision), _ptr(q), _ptr(lam), _stream(stream), comm.handle))
 
 
 def dev_jacobian_apply(spec, params, x, labels, n, p_begin, p_end, inp, ld_in, l, out, ld_out, transpose=False,
