@@ -398,6 +398,47 @@ def e2e_run(job, steps, world):
             "path": "curvkit_assemble_*_f32 host-buffer C-ABI (pinned fp32 output)", "result_symmetric": ok}
 
 
+def e2e_band_run(job, steps, stream, torch, barrier, red_dev):
+    """N > 1: each rank uploads its inputs from pinned host memory, assembles
+    its band through the device C-ABI and downloads the band into pinned host
+    memory (every rank over its own PCIe link); max over ranks."""
+    import numpy as np
+    wl = job.wl
+    pin = lambda a, dt: torch.tensor(np.ascontiguousarray(a), dtype=dt).pin_memory()  # noqa: E731
+    hp, hx = pin(job.params, job.p_d.dtype), pin(job.x, job.x_d.dtype)
+    hl = job.l_d.cpu().pin_memory()
+    hosts = {prod: torch.empty(tuple(b.shape), dtype=b.dtype, pin_memory=True) for prod, b in job.out.items()}
+
+    def one():
+        job.p_d.copy_(hp, non_blocking=True)
+        job.x_d.copy_(hx, non_blocking=True)
+        job.l_d.copy_(hl, non_blocking=True)
+        job.step(stream)
+        for prod, h in hosts.items():
+            h.copy_(job.out[prod], non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], device=red_dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    h2d = hp.numel() * hp.element_size() + hx.numel() * hx.element_size() + hl.numel() * hl.element_size()
+    d2h = sum(h.numel() * h.element_size() for h in hosts.values())
+    h2d_all = torch.tensor([h2d, d2h], dtype=torch.float64, device=red_dev)
+    torch.distributed.all_reduce(h2d_all)
+    return {"value": entries_per_step(wl.name, wl.P) / (ms / 1e3), "unit": "entries/s",
+            "h2d_bytes_per_step": int(h2d_all[0].item()), "d2h_bytes_per_step": int(h2d_all[1].item()),
+            "ms_per_step": ms, "path": "device C-ABI (curvkit_dev_assemble_band) with pinned host inputs and "
+                                      "the band downloaded to pinned host memory on every rank"}
+
+
 def run_extra(torch, dev, stream, pk, pk_kind):
     """The other BASELINE configurations on the same GPU (N = 1)."""
     out = {}
@@ -456,18 +497,28 @@ def run_b200(args):
     from paper_1905_05559_b200 import curv
 
     rank, world, local = dist_env()
+    # CURVKIT_BENCH_COMM=host: gloo + the library's host transport (a code-path
+    # check with several ranks sharing the GPUs there are; its timings mean nothing)
+    host_comm = os.environ.get("CURVKIT_BENCH_COMM") == "host"
+    if host_comm:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
+    red_dev = torch.device("cpu") if host_comm else dev
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if host_comm:
+            dist.init_process_group("gloo")
+            comm = curv.Comm.create_host(rank, world)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
-        def bcast(obj):
-            lst = [obj]
-            dist.broadcast_object_list(lst, src=0)
-            return lst[0]
-        comm = curv.Comm.create(rank, world, bcast)
+            def bcast(obj):
+                lst = [obj]
+                dist.broadcast_object_list(lst, src=0)
+                return lst[0]
+            comm = curv.Comm.create(rank, world, bcast)
     stream = torch.cuda.current_stream()
     job = Job(args.config, args.precision, dev, torch, shard=(comm, rank, world) if world > 1 else None)
     wl = job.wl
@@ -479,7 +530,7 @@ def run_b200(args):
     with Clocks(local) as clk:
         ms, prof, launches, (t0, t1) = timed(job, args.steps, args.warmup, stream, torch, barrier)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ent = entries_per_step(wl.name, wl.P)
@@ -503,11 +554,11 @@ def run_b200(args):
 
     e2e = None
     if not args.no_e2e and world == 1:
-        job_free_bytes = sum(b.numel() * b.element_size() for b in job.out.values())
         job.free()  # the host-buffer path allocates its own device result
         torch.cuda.empty_cache()
         e2e = e2e_run(job, args.e2e_steps, world)
-        del job_free_bytes
+    elif not args.no_e2e:
+        e2e = e2e_band_run(job, args.e2e_steps, stream, torch, barrier, red_dev)
     if rank != 0:
         if comm is not None:
             comm.close()

@@ -151,7 +151,7 @@ struct HMaps {
     CUtensorMap m[8];
 };
 
-template <bool ZT>
+template <bool ZT, bool BAND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant__ CUtensorMap mapAbar16,
              const __grid_constant__ CUtensorMap mapPi, const __grid_constant__ HMaps hm, Params p) {
@@ -418,6 +418,17 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                         const int4 pr = __ldg(&p.pairs[J0 + e]);
                         // the four orbit entries (row unit, col unit): (o,i;o'',c) (o'',c;o,i)
                         // (o,c;o'',i) (o'',i;o,c); rows outside the output units are skipped
+                        if constexpr (!BAND) {  // the whole block: all four images
+                            // (a separate instantiation: the band's row mapping in this
+                            // loop measured 15% slower on the whole-block kernel)
+                            const int64_t r1 = hidx(p, pr.x, ii), c1 = hidx(p, pr.y, cc);
+                            const int64_t r3 = hidx(p, pr.x, cc), c3 = hidx(p, pr.y, ii);
+                            p.H[r1 * p.ldh + c1] = v[e];
+                            p.H[c1 * p.ldh + r1] = v[e];
+                            p.H[r3 * p.ldh + c3] = v[e];
+                            p.H[c3 * p.ldh + r3] = v[e];
+                            continue;
+                        }
                         const int64_t s1 = srow(p, pr.x, ii), s2 = srow(p, pr.y, cc);
                         const int64_t s3 = srow(p, pr.x, cc), s4 = srow(p, pr.y, ii);
                         if (s1 >= 0) p.H[s1 * p.ldh + hidx(p, pr.y, cc)] = v[e];
@@ -596,17 +607,22 @@ struct SymKr<float> {
                         u0, u1, bwoff, bboff};
         static const int dev = getenv("CURVKIT_DEV_SYMKR") ? atoi(getenv("CURVKIT_DEV_SYMKR")) : 0;
         prm.dev = dev;
-        func_attr_once((const void*)sym::symkr_kernel<true>, [] {
-            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        func_attr_once((const void*)sym::symkr_kernel<true, false>, [] {
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sym::Cfg<true>::SMEM_BYTES));
-            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         sym::Cfg<false>::SMEM_BYTES));
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sym::Cfg<false>::SMEM_BYTES));
         });
         const int grid = 2 * (int)std::min<int64_t>((int64_t)tiles.size(), tc::num_sms() / 2);
-        if (zt)
-            sym::symkr_kernel<true><<<grid, sym::kThreads, sym::Cfg<true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        const bool band = u0 != 0 || u1 != U || bwoff != a.woff || bboff != a.boff;
+        if (band)
+            sym::symkr_kernel<false, true><<<grid, sym::kThreads, sym::Cfg<false>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        else if (zt)
+            sym::symkr_kernel<true, false><<<grid, sym::kThreads, sym::Cfg<true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
         else
-            sym::symkr_kernel<false><<<grid, sym::kThreads, sym::Cfg<false>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+            sym::symkr_kernel<false, false><<<grid, sym::kThreads, sym::Cfg<false>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
         CK_LAUNCH();
         return true;
     }

@@ -228,6 +228,13 @@ def test_config1_topk_against_dual_gram(prec):
     assert lam[9] <= w[9] * (1 + 1e-3) and lam[9] >= 0.9 * w[9]
     qtq = (q.T.double() @ q.double()).cpu().numpy()
     assert np.abs(qtq - np.eye(k)).max() <= 1e-4
+    # the default converged solver: all ten within 1e-3
+    qa = torch.empty((P, 10), dtype=torch.float32, device="cuda:0")
+    la = torch.empty(10, dtype=torch.float32, device="cuda:0")
+    curv.dev_opg_topk_auto(spec, p64.float(), x64.float(), lab, n, 10, 20, 7, qa, la, precision=prec)
+    torch.cuda.synchronize()
+    la = la.double().cpu().numpy()
+    assert np.all(np.abs(la - w[:10]) <= 1e-3 * np.abs(w[:10])), (la, w)
 
 
 def test_config1_hessian_tmem_a_variant():
@@ -332,8 +339,8 @@ def test_opg_odd_pitch_device_buffer():
 def test_config4_topk_against_exact_spectrum():
     """BASELINE config 4 at full size (P = 1 055 242, N = 20 000): the device
     randomized range finder against the exact nonzero spectrum of G, from the
-    dual Gram (1/N) J J^T (20 000 x 20 000, FP32 SGEMM, fp64 eigvalsh; J is
-    84 GB and formed only for this check).  Rayleigh-Ritz values are lower
+    dual Gram (1/N) J J^T (20 000 x 20 000, fp32 products accumulated in fp64,
+    fp64 eigvalsh; J is 84 GB and formed only for this check).  Rayleigh-Ritz values are lower
     bounds of the true eigenvalues; the spectrum is flat (lambda_1/lambda_100 =
     1.3), so with the BASELINE's 2 power iterations they sit ~10% low and
     converge with more iterations: at 64 all 100 are within 1e-3 (DESIGN.md
@@ -352,27 +359,43 @@ def test_config4_topk_against_exact_spectrum():
         lams[it] = lam.double().cpu().numpy()
         del q
     # Chebyshev-filtered subspace iteration: 3 rounds of degree 6 (18 operator
-    # applications instead of 64 power iterations)
-    q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
-    lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
-    curv.dev_opg_topk_filtered(spec, p, x, lab, n, k, wl.oversample, 3, 6, 7, q, lam, precision="tf32")
-    torch.cuda.synchronize()
-    lams["cheb3x6"] = lam.double().cpu().numpy()
-    qtq = (q.T @ q).double().cpu().numpy()
-    assert np.abs(qtq - np.eye(k)).max() <= 1e-4
-    del q
+    # applications instead of 64 power iterations), and the default converged
+    # solver (Ritz-convergence stop rule, tol 1e-4)
+    for tag in ("cheb3x6", "auto"):
+        q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
+        lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
+        if tag == "auto":
+            curv.dev_opg_topk_auto(spec, p, x, lab, n, k, wl.oversample, 7, q, lam)
+        else:
+            curv.dev_opg_topk_filtered(spec, p, x, lab, n, k, wl.oversample, 3, 6, 7, q, lam, precision="tf32")
+        torch.cuda.synchronize()
+        lams[tag] = lam.double().cpu().numpy()
+        qtq = (q.T @ q).double().cpu().numpy()
+        assert np.abs(qtq - np.eye(k)).max() <= 1e-4
+        del q
     old = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     try:
         ldj = (P + 31) // 32 * 32
         J = torch.empty((n, ldj), dtype=torch.float32, device="cuda:0")
         curv.dev_assemble_jacobian(spec, p, x, lab, n, J, ldj, precision="f32")
-        K = torch.empty((n, n), dtype=torch.float64, device="cuda:0")
-        for i0 in range(0, n, 2000):
-            K[i0:i0 + 2000] = (J[i0:i0 + 2000, :P] @ J[:, :P].T).double()
-        del J
+        # fp32 products accumulated in fp64 over column chunks of J: one
+        # 20000 x 20000 x 1.05M SGEMM loses ~1e-3 of its entries on this GPU
+        # (tools/gpu/dual_gram_check.py), chunks of 16384 keep them to ~2e-7
+        K = torch.zeros((n, n), dtype=torch.float64, device="cuda:0")
+        for c0 in range(0, P, 16384):
+            Jc = J[:, c0:min(P, c0 + 16384)]
+            K += (Jc @ Jc.T).double()
+        del J, Jc
         torch.cuda.empty_cache()
         K = (K + K.T) / (2.0 * n)
+        # the dual Gram rests on reference data: its block at 16 sampled examples
+        # equals (1/N) J_s J_s^T of the reference's per-example gradient rows
+        # (tests/golden/c4_sketch.npz, make_sketch_pins.py)
+        pins = load_golden("c4_sketch")
+        rows = torch.tensor(pins["rows"], device="cuda:0")
+        blk = K[rows][:, rows].cpu().numpy()
+        assert rel_fro(blk, pins["gram"] / n) <= 1e-5, rel_fro(blk, pins["gram"] / n)
         ev = torch.linalg.eigvalsh(K).flip(0)[:k].cpu().numpy()
         del K
         torch.cuda.empty_cache()
@@ -387,6 +410,26 @@ def test_config4_topk_against_exact_spectrum():
     assert e64.max() <= 1e-3, (e64.max(), int(e64.argmax()))       # the north_star's bar, all 100
     ec = np.abs(lams["cheb3x6"] - ev) / ev
     assert ec.max() <= 1e-3, (ec.max(), int(ec.argmax()))         # the same bar from 18 applications
+    ea = np.abs(lams["auto"] - ev) / ev
+    assert ea.max() <= 1e-3, (ea.max(), int(ea.argmax()))         # the default solver: stops converged
+    print(f"c4 max rel. eigenvalue error: power-2 {e2.max():.3e}, power-64 {e64.max():.3e}, "
+          f"cheb 3x6 {ec.max():.3e}, auto {ea.max():.3e}")
+
+
+@pytest.mark.parametrize("prec", ["f64", "tf32"])
+def test_opg_eigs_default_is_converged(prec):
+    """curv.opg_eigs with no solver arguments: the Chebyshev filter with the
+    Ritz-convergence stop rule (curvkit_opg_topk_auto) against the dense
+    eigendecomposition of the reference's G."""
+    g = load_golden("config0")
+    spec = spec_of(g)
+    k = 5
+    pairs = curv.opg_eigs(spec, g["params"], curv.Batch(g["x"], g["y"]), k, oversample=10, seed=3, precision=prec)
+    w = np.linalg.eigvalsh(g["G"])[::-1]
+    assert np.all(np.abs(pairs.lam - w[:k]) <= 1e-3 * np.abs(w[:k])), (pairs.lam, w[:k])
+    assert np.abs(pairs.q.T @ pairs.q - np.eye(k)).max() <= (1e-8 if prec == "f64" else 1e-4)
+    with pytest.raises(curv.ContractError):
+        curv.opg_eigs(spec, g["params"], curv.Batch(g["x"], g["y"]), k, tol=0.0)
 
 
 @pytest.mark.parametrize("prec", ["f64", "tf32"])

@@ -1,7 +1,8 @@
 """Dev / parity evidence at full size for BASELINE config 4 (P = 1 055 242,
 N = 20 000): the top-k eigenvalues of G = (1/N) J^T J from the device
 randomized range finder against the exact nonzero spectrum of G, taken from
-the dual Gram K = (1/N) J J^T (20 000 x 20 000; FP32 SGEMM without TF32, fp64
+the dual Gram K = (1/N) J J^T (20 000 x 20 000; fp32 products over column
+chunks accumulated in fp64 -- one big SGEMM loses ~1e-3 per entry -- fp64
 eigvalsh).  J (84 GB fp32) is formed only for this check.
     python tools/c4_dual_gram.py [power_iters[:oversample] | f:steps:degree[:oversample] ...]
 (f: Chebyshev-filtered subspace iteration, curvkit_dev_opg_topk_filtered)"""
@@ -25,10 +26,14 @@ runs = sys.argv[1:] or [str(wl.power_iters)]
 lams = {}
 for a in runs:
     f = a.startswith("f:")
-    r = [int(v) for v in (a[2:] if f else a).split(":")]
+    r = [] if a.startswith("auto") else [int(v) for v in (a[2:] if f else a).split(":")]
     q = torch.empty((P, k), dtype=torch.float32, device=dev)
     lam = torch.empty(k, dtype=torch.float32, device=dev)
-    if f:
+    if a.startswith("auto"):
+        ov = int(a.split(":")[1]) if ":" in a else wl.oversample
+        call = lambda: curv.dev_opg_topk_auto(spec, p, xx, ll, n, k, ov, 7, q, lam)
+        key = f"auto:{ov}"
+    elif f:
         st, deg, ov = r[0], r[1], (r[2] if len(r) > 2 else wl.oversample)
         call = lambda: curv.dev_opg_topk_filtered(spec, p, xx, ll, n, k, ov, st, deg, 7, q, lam, precision="tf32")
         key = f"filtered {st}x{deg}:{ov}"
@@ -47,11 +52,11 @@ t = time.time()
 ldj = (P + 31) // 32 * 32
 J = torch.empty((n, ldj), dtype=torch.float32, device=dev)
 curv.dev_assemble_jacobian(spec, p, xx, ll, n, J, ldj, precision="f32")
-K = torch.empty((n, n), dtype=torch.float64, device=dev)
-bs = 2000
-for i0 in range(0, n, bs):  # row blocks of K in fp32 SGEMM, accumulated into fp64
-    K[i0:i0 + bs] = (J[i0:i0 + bs, :P] @ J[:, :P].T).double()
-del J
+K = torch.zeros((n, n), dtype=torch.float64, device=dev)
+for c0 in range(0, P, 16384):  # fp32 products over column chunks, accumulated in fp64
+    Jc = J[:, c0:min(P, c0 + 16384)]
+    K += (Jc @ Jc.T).double()
+del J, Jc
 torch.cuda.empty_cache()
 K = (K + K.T) / (2.0 * n)
 ev = torch.linalg.eigvalsh(K).flip(0)[:k].cpu().numpy()
