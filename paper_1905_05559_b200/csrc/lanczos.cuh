@@ -52,6 +52,8 @@ struct HostRng {
 };
 
 // ---- host: symmetric tridiagonal eigensolver (implicit QL, Wilkinson shift)
+// The textbook routine (Numerical Recipes `tqli`; the reference uses the same
+// algorithm in linalg.cpp:262-315 for its Lanczos Ritz solve).
 // d (m) diagonal, e (m-1) off-diagonal.  z: nz x m rows that receive every
 // rotation (identity -> eigenvectors; the last row of the identity -> the
 // last components of the eigenvectors).  On return d holds the eigenvalues;

@@ -1,7 +1,7 @@
 // Dev microbenchmark: the symkr MMA issue loop in isolation (cta_group::2,
 // kind::tf32, M = 256, N = bn, 4 MMAs per 32-example K-block advancing inside
 // the 128-byte swizzle atom, NST rotating smem stages, optional commit per
-// K-block).  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_loop tools/mma_loop.cu
+// K-block).  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/dev/mma_loop tools/dev/mma_loop.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
