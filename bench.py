@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(PRODUCTS))
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "tf32x3", "f32", "f64"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "f16s", "tf32x3", "f32", "f64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
@@ -276,13 +276,16 @@ def roofline(prof, steps, ms_step, pk, pk_kind, prec, traffic=None):
            "launches_per_step": r["launches"] // max(1, steps), "traffic": None}
     if r["flops"] > 0:
         achieved = r["flops"] / (r["ms"] / 1e3) / 1e12
-        if prec in ("tf32", "tf32x3"):
-            burst, sus = pk["bf16_tflops"] / 2.0, pk["bf16_tflops_sustained"] / 2.0
+        if prec in ("tf32", "tf32x3", "f16s"):
+            # f16s runs its dominant kernels on the fp16 datapath: the bf16/fp16 peak itself
+            div, what = (1.0, "fp16 dense = bf16") if prec == "f16s" else (2.0, "TF32 dense = bf16")
+            burst, sus = pk["bf16_tflops"] / div, pk["bf16_tflops_sustained"] / div
             long_region = steps * ms_step >= 1000.0
             peak = sus if long_region else burst
-            kind = (f"sustained: TF32 dense = bf16 sustained {pk['bf16_tflops_sustained']} / 2 (timed region "
+            dv = f" / {div:g}" if div != 1.0 else ""
+            kind = (f"sustained: {what} sustained {pk['bf16_tflops_sustained']}{dv} (timed region "
                     f"{steps * ms_step / 1e3:.1f} s >= 1 s)" if long_region else
-                    f"burst: TF32 dense = bf16 burst {pk['bf16_tflops']} / 2 (timed region "
+                    f"burst: {what} burst {pk['bf16_tflops']}{dv} (timed region "
                     f"{steps * ms_step:.0f} ms < 1 s)")
             out.update(bound="tensor", achieved=achieved, unit="TFLOP/s", peak=peak, frac=achieved / peak,
                        peak_note=f"{kind}, {pk_kind}", frac_burst=achieved / burst, frac_sustained=achieved / sus)

@@ -43,8 +43,12 @@ enum curvkit_output_mode { CURVKIT_SOFTMAX_CROSS_ENTROPY = 0, CURVKIT_RAW_MEAN_O
  * (linalg.hpp DenseMatrix of double); F64 reproduces it, F32 uses exact
  * fp32 FMAs, TF32 runs the curvature GEMMs on tcgen05 tensor cores
  * (kind::tf32, fp32 accumulate in TMEM), TF32X3 splits operands into
- * hi+lo TF32 parts for fp32-grade products on tensor cores. */
-enum curvkit_precision { CURVKIT_F64 = 0, CURVKIT_F32 = 1, CURVKIT_TF32 = 2, CURVKIT_TF32X3 = 3 };
+ * hi+lo TF32 parts for fp32-grade products on tensor cores.  F16S is the
+ * TF32 precision class on the fp16 tensor datapath: operands scaled by exact
+ * powers of two and rounded to fp16 (the 11-bit TF32 significand), exact
+ * products accumulated in fp32 (kind::f16), scales undone exactly; kernels
+ * without an fp16 form run TF32 in this mode.  Same tolerance class as TF32. */
+enum curvkit_precision { CURVKIT_F64 = 0, CURVKIT_F32 = 1, CURVKIT_TF32 = 2, CURVKIT_TF32X3 = 3, CURVKIT_F16S = 4 };
 
 /* curv::ModelSpec (model.hpp:27-42). */
 typedef struct curvkit_model {

@@ -179,7 +179,7 @@ cudaStream_t dev_stream(void* stream) {
 }
 
 bool is_f64(int prec) {
-    if (prec < kF64 || prec > k3xTF32) contract("unknown precision");
+    if (prec < kF64 || prec > kF16S) contract("unknown precision");
     return prec == kF64;
 }
 
@@ -344,7 +344,7 @@ void opg_into(const ModelDesc& md, const Cache<T>& c, T* G, int64_t ldg, int pre
     if (eng.opg_kr(c, G, ldg, rb, re < 0 ? INT64_MAX : re)) return;
     DevMem J;
     int64_t ldj;
-    jacobian_full<T>(md, c, J, ldj, s, prec == kTF32);
+    jacobian_full<T>(md, c, J, ldj, s, tf32_class(prec));
     eng.opg(dptr<T>(J), ldj, c.n, G, ldg, rb, re);
 }
 
@@ -795,7 +795,7 @@ int curvkit_dev_assemble_band(const curvkit_model* model, int32_t product, const
         ModelDesc md = make_desc(model);
         if (n < 1) contract("assemble_band: empty dataset");
         if (product != 0 && product != 1) contract("assemble_band: product must be 0 (Hessian) or 1 (OPG)");
-        if (precision != kTF32) contract("unit-band assembly needs TF32 precision");
+        if (!tf32_class(precision)) contract("unit-band assembly needs TF32 precision");
         if (ld < md.P || ld % 4) contract("assemble_band: ld must be >= P and a multiple of 4");
         const UnitBand b = UnitBand::make(md, nshards, shard);
         if (b.rows == 0) return;
@@ -840,7 +840,7 @@ int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t ld
         EpiStore<float> e{c, ldc, 0, alpha, 0.f};
         Opnd<float> A = a_kmajor ? kmaj(a, lda) : mnmaj(a, lda);
         Opnd<float> B = b_kmajor ? kmaj(b, ldb) : mnmaj(b, ldb);
-        if (precision == kTF32 || precision == k3xTF32) gemm_tf32_store(precision, s, m, n, k, A, B, c, ldc, alpha);
+        if (tf32_class(precision) || precision == k3xTF32) gemm_tf32_store(tc_form(precision), s, m, n, k, A, B, c, ldc, alpha);
         else CurvGemm<float, EpiStore<float>>::run(precision, s, m, n, k, A, B, e);
     });
 }
@@ -949,7 +949,7 @@ int curvkit_dev_jacobian_apply(const curvkit_model* model, const void* params, c
     return guard([&] {
         ModelDesc md = make_desc(model);
         if (n < 1 || l < 1) contract("jacobian_apply: empty operand");
-        if (precision != kTF32) contract("jacobian_apply needs TF32 precision");
+        if (!tf32_class(precision)) contract("jacobian_apply needs TF32 precision");
         if (ld_in % 32 || (transpose && ld_in < l) || (!transpose && ld_in < l))
             contract("jacobian_apply: the input pitch must be a multiple of 32 and >= l");
         cudaStream_t s = dev_stream(stream);
@@ -974,7 +974,7 @@ int curvkit_dev_opg_topk_sharded(const curvkit_model* model, const void* params,
         if (n < 1) contract("opg_topk: empty dataset");
         if (!comm) contract("opg_topk_sharded: null communicator");
         cudaStream_t s = dev_stream(stream);
-        if (precision != kTF32) contract("sharded opg_topk needs TF32 precision");
+        if (!tf32_class(precision)) contract("sharded opg_topk needs TF32 precision");
         Cache<float> c;
         forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
         dev_topk<float>(md, c, k, oversample, power_iters, seed, precision, (float*)q, (float*)lambda, s, &comm->c);
@@ -991,7 +991,7 @@ int curvkit_dev_opg_topk_sharded_filtered(const curvkit_model* model, const void
         if (!comm) contract("opg_topk_sharded: null communicator");
         if (filter_degree < 1) contract("opg_topk_filtered: filter_degree must be >= 1");
         cudaStream_t s = dev_stream(stream);
-        if (precision != kTF32) contract("sharded opg_topk needs TF32 precision");
+        if (!tf32_class(precision)) contract("sharded opg_topk needs TF32 precision");
         Cache<float> c;
         forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
         dev_topk<float>(md, c, k, oversample, 0, seed, precision, (float*)q, (float*)lambda, s, &comm->c, filter_steps,
@@ -1008,7 +1008,7 @@ int curvkit_dev_opg_topk_sharded_auto(const curvkit_model* model, const void* pa
         if (n < 1) contract("opg_topk: empty dataset");
         if (!comm) contract("opg_topk_sharded: null communicator");
         if (!(tol > 0.0) || max_applications < 1) contract("opg_topk_auto: need tol > 0 and max_applications >= 1");
-        if (precision != kTF32) contract("sharded opg_topk needs TF32 precision");
+        if (!tf32_class(precision)) contract("sharded opg_topk needs TF32 precision");
         cudaStream_t s = dev_stream(stream);
         Cache<float> c;
         forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);

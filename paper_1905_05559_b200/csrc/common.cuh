@@ -37,7 +37,17 @@ enum OutMode : int { kSoftmaxCE = 0, kRawMean = 1 };
 // kTF32 runs tcgen05 kind::tf32 MMAs with fp32 accumulation in TMEM;
 // k3xTF32 splits each fp32 operand into a TF32 hi part and a TF32 lo part
 // and accumulates hi*hi + hi*lo + lo*hi (fp32-grade products).
-enum Precision : int { kF64 = 0, kF32 = 1, kTF32 = 2, k3xTF32 = 3 };
+// kF16S is the TF32 precision class on the fp16 datapath: operands are
+// scaled by exact powers of two into fp16 range and rounded to nearest fp16
+// -- the same 11-bit significand as TF32 -- and the tcgen05 kind::f16 MMA
+// accumulates their exact products in fp32; the scales are undone in the
+// epilogue (exact).  Twice the TF32 tensor rate at half the operand bytes.
+// Kernels without an fp16 variant run their TF32 form in this mode.
+enum Precision : int { kF64 = 0, kF32 = 1, kTF32 = 2, k3xTF32 = 3, kF16S = 4 };
+// the tensor-core (TF32-precision) class: TF32 or F16S
+__host__ __device__ inline bool tf32_class(int p) { return p == kTF32 || p == kF16S; }
+// what a kernel without an fp16 form runs
+__host__ __device__ inline int tc_form(int p) { return p == kF16S ? (int)kTF32 : p; }
 
 struct CurvError : std::runtime_error {
     int code;

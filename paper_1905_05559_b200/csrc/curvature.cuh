@@ -349,7 +349,7 @@ struct Engine {
     // band != null: G holds the unit band's rows (bands.cuh), TF32 only.
     bool opg_kr(const Cache<T>& c, T* G, int64_t ldg, int64_t rlo = 0, int64_t rhi = INT64_MAX,
                 const UnitBand* band = nullptr) {
-        const bool tc = prec == kTF32 && sizeof(T) == 4;
+        const bool tc = tf32_class(prec) && sizeof(T) == 4;
         if (band && !tc) throw CurvError(kContractError, "unit-band assembly needs TF32 precision");
         if (!(tc || prec == kF32 || prec == kF64) || sym_off()) {
             if (band) throw CurvError(kContractError, "unit-band assembly needs the symmetric-orbit kernels");
@@ -507,7 +507,7 @@ struct Engine {
                  int64_t rhi = INT64_MAX, const UnitBand* band = nullptr) {
         const int S = md.S;
         const int64_t n = c.n;
-        if (band && (prec != kTF32 || sizeof(T) != 4 || verify || sym_off()))
+        if (band && (!tf32_class(prec) || sizeof(T) != 4 || verify || sym_off()))
             throw CurvError(kContractError, "unit-band assembly needs TF32 precision");
         for (int k = 0; k < S; ++k) {
             const int64_t np = md.w[k + 1];
@@ -613,7 +613,7 @@ struct Engine {
             tb.flush();
             // Extended copies for the fused TF32 kernel: a 128-row activation
             // tile starting anywhere in [0, T_k) reads rows r -> r mod T_k.
-            const bool fused = prec == kTF32 && sizeof(T) == 4;
+            const bool fused = tf32_class(prec) && sizeof(T) == 4;
             const int64_t ak_rows = tk + 256;
             T* akX = nullptr;
             T* QX[kMaxLayers] = {};

@@ -575,7 +575,7 @@ struct EigenWork {
             EpiStore<T> e{dst, ld, 0, T(1), T(0)};
             bool done = false;
             if constexpr (std::is_same_v<T, float>) {
-                if (prec == kTF32 && rows >= 512 && l % 4 == 0) {  // fp32-grade products on the tensor cores
+                if (tf32_class(prec) && rows >= 512 && l % 4 == 0) {  // fp32-grade products on the tensor cores
                     gemm_tf32(k3xTF32, s, rows, l, l, kmaj(src, ld), mnmaj(dptr<T>(Rt), l), e);
                     done = true;
                 }
@@ -617,7 +617,7 @@ struct EigenWork {
                 if (comm) comm->sum(Tout, (size_t)(n * ldt), s);  // J X = sum over ranks' rows
                 return;
             }
-            if (prec == kTF32 || prec == k3xTF32) {  // split-K: only ceil(N/256) row tiles
+            if (tf32_class(prec) || prec == k3xTF32) {  // split-K: only ceil(N/256) row tiles
                 gemm_tf32_store(prec, s, n, l, md.P, read_once(pre_rounded(kmaj(J, ldj))), mnmaj(X, ldx), Tout,
                                 ldt);
                 return;
@@ -700,15 +700,15 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     const bool ext = Jext != nullptr;
     std::unique_ptr<KrOperands> krop;
     if constexpr (std::is_same_v<T, float>)
-        if (!ext && prec == kTF32 && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
+        if (!ext && tf32_class(prec) && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
     if (sharded && !krop) throw CurvError(kContractError, "sharded opg_topk needs TF32 precision");
-    const bool ext_copy = ext && prec == kTF32;
+    const bool ext_copy = ext && tf32_class(prec);
     const int64_t ldj = ext && !ext_copy ? ldj_ext : (krop ? 0 : round_up(P, 32));
     DevMem J((size_t)((ext && !ext_copy) ? 0 : n * ldj) * sizeof(T), s);
     if (ext_copy) {
         convert_rows_rn<T>(Jext, ldj_ext, dptr<T>(J), ldj, n, P, s);
     } else if (!ext && !krop) {
-        jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, prec == kTF32);  // TF32: stored pre-rounded
+        jacobian<T>(md, c, 0, n, dptr<T>(J), ldj, s, tf32_class(prec));  // TF32: stored pre-rounded
     }
     const T* Jp = (ext && !ext_copy) ? Jext : dptr<T>(J);
     const size_t rbytes = (size_t)std::max<int64_t>(R, 1) * ldl * sizeof(T);
@@ -874,7 +874,7 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     EpiStore<T> e{q_dev, k, 0, T(1), T(0)};
     bool done = false;
     if constexpr (std::is_same_v<T, float>) {
-        if ((prec == kTF32 || prec == k3xTF32) && R >= 512 && k % 4 == 0) {
+        if ((tf32_class(prec) || prec == k3xTF32) && R >= 512 && k % 4 == 0) {
             gemm_tf32(k3xTF32, s, R, k, l, kmaj(X, ldl), mnmaj(dptr<T>(Vk), k), e);
             done = true;
         }

@@ -497,6 +497,18 @@ __device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
         : "memory");
 }
 
+// kind::f16: fp16 A and B (K = 16 per instruction, the same 32 bytes of a
+// 128-byte swizzle row as one K = 8 tf32 step), fp32 accumulate
+__device__ __forceinline__ void mma2_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    const uint32_t z = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(z)
+        : "memory");
+}
+
 // A from TMEM (the "TS" form): a_tmem is this CTA's A tile column in TMEM
 __device__ __forceinline__ void mma2_tf32_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
                                              uint32_t acc) {
@@ -543,6 +555,12 @@ __device__ __forceinline__ void mma2_tf32_ts_e(uint32_t d, uint32_t a, uint64_t 
 __device__ __forceinline__ void commit2_e(uint64_t* bar) {
     if (elect_one()) commit2(bar);
     __syncwarp();
+}
+
+// kind::f16 instruction descriptor, M = 256 (pair): D f32, A/B f16 (format 0)
+__host__ __device__ constexpr uint32_t idesc2_f16(int n, bool a_mn, bool b_mn) {
+    return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(256 >> 4) << 24);
 }
 
 __host__ __device__ constexpr uint32_t idesc2_tf32(int n, bool a_mn, bool b_mn) {
@@ -1564,7 +1582,7 @@ inline void gemm_tf32_store(int prec, cudaStream_t s, int64_t M, int64_t N, int6
 template <>
 struct HessFused<float> {
     static bool run(int prec, cudaStream_t s, const HessFusedArgs<float>& a, const EpiHess<float>& e) {
-        if (prec != kTF32) return false;
+        if (!tf32_class(prec)) return false;
         namespace pair = tc::pair;
         // A from TMEM (R never in shared memory) is correct but measured slower
         // on B200 (5.3 vs 4.2 clocks per N column per k-block): opt-in only
@@ -1657,7 +1675,7 @@ template <class Epi>
 struct CurvGemm<float, Epi> {
     static void run(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<float> A, Opnd<float> B,
                     const Epi& e) {
-        if (prec == kTF32 || prec == k3xTF32) gemm_tf32(prec, s, M, N, K, A, B, e);
+        if (tf32_class(prec) || prec == k3xTF32) gemm_tf32(tc_form(prec), s, M, N, K, A, B, e);
         else gemm_simt<float>(s, M, N, K, 1, A, B, e);
     }
 };

@@ -35,6 +35,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "gemm_tc.cuh"
 
 namespace ck {
@@ -51,8 +53,6 @@ constexpr int Z_BYTES = 128 * BK * 4;   // A operand (Z), 128 rows x 32 examples
 #endif
 constexpr int B_ROWS = CURVKIT_SYMKR_BROWS;  // packed profile rows per CTA and stage (MMA N <= 2 B_ROWS)
 constexpr int B_BYTES = B_ROWS * BK * 4;
-constexpr int I_BYTES = 8 * BK * 4;     // abar^T rows of the CTA's 8 i
-constexpr int C_BYTES = 16 * BK * 4;    // abar^T rows of the 16 c
 constexpr int CH = 8;                   // epilogue chunk (packed columns)
 constexpr int SLOT = CH * 128 * 4;      // one staging layout of one chunk
 constexpr int EPI_BYTES = 2 * 2 * 2 * SLOT;  // group x double buffer x layout
@@ -63,8 +63,17 @@ constexpr int MAX_SMEM = 227 * 1024;
 // passes through shared memory; slot reuse is gated by an MMA commit (zfree).
 constexpr int NZ = 4;
 constexpr int ZSLOT0 = 512 - 32 * NZ;   // first Z column; accumulators at 0 and bn
-template <bool ZT>
+// F16 (precision kF16S): Z and the packed profile are fp16, so one 128-byte
+// operand row holds KB = 64 examples (4 kind::f16 MMAs of K = 16); the fp32
+// abar^T rows of a K-block arrive as two 128-byte TMA boxes (examples
+// [k0, k0 + 32) and [k0 + 32, k0 + 64)), each in its own 1 KB swizzle atom.
+template <bool ZT, bool F16 = false>
 struct Cfg {
+    static constexpr int KB = F16 ? 64 : 32;           // examples per K-block
+    static constexpr int HALVES = F16 ? 2 : 1;         // 32-example abar boxes per K-block
+    static constexpr int I_HALF = 8 * BK * 4, C_HALF = 16 * BK * 4;
+    static constexpr int I_BYTES = HALVES * I_HALF;    // abar^T rows of the CTA's 8 i
+    static constexpr int C_BYTES = HALVES * C_HALF;    // abar^T rows of the 16 c
     static constexpr int STAGE = (ZT ? 0 : Z_BYTES) + B_BYTES + I_BYTES + C_BYTES;
     static constexpr int NST = std::min(8, (MAX_SMEM - 1024 - EPI_BYTES - EPI_PAD - 1024) / STAGE);
     static constexpr int SMEM_BYTES = 1024 + NST * STAGE + EPI_BYTES + EPI_PAD + 1024;
@@ -89,6 +98,10 @@ struct Params {
     // whole block is u0 = 0, u1 = U, bwoff = woff, bboff = boff (unit bands:
     // DESIGN.md section 7).  Columns are always the global ones.
     int64_t u0, u1, bwoff, bboff;
+    // F16: power-of-two scales, Z row (i, c) = abar_i abar_c zscale[i] zscale[c]
+    // (abar indices, padded to whole 16-blocks) and packed column j = Pi_j / pscale[j]
+    const float* zscale;
+    const float* pscale;
 };
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -136,6 +149,17 @@ __device__ __forceinline__ void tmem_ld_wait8(uint32_t (&r)[8]) {
                  : "memory");
 }
 
+// inverse of row_ic: the tile row (TMEM lane, Z row) of (il, cl)
+__device__ __forceinline__ int ic_row(int il, int cl) { return 32 * (2 * (il >> 2) + (cl >> 3)) + 8 * (il & 3) + (cl & 7); }
+
+__device__ __forceinline__ float4 scale4(float4 v, float s) { return make_float4(v.x * s, v.y * s, v.z * s, v.w * s); }
+
+// two fp32 -> packed fp16x2 (round to nearest even), the first in the low half
+__device__ __forceinline__ uint32_t h2_bits(float lo, float hi) {
+    const __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // H column of (unit o, abar index x): weight (o, x) or the bias of o
 __device__ __forceinline__ int64_t hidx(const Params& p, int64_t o, int64_t x) {
     return x < p.tk ? p.woff + o * p.tk + x : p.boff + o;
@@ -151,15 +175,16 @@ struct HMaps {
     CUtensorMap m[8];
 };
 
-template <bool ZT, bool BAND>
+template <bool ZT, bool BAND, bool F16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant__ CUtensorMap mapAbar16,
              const __grid_constant__ CUtensorMap mapPi, const __grid_constant__ HMaps hm, Params p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    using K = Cfg<ZT>;
+    using K = Cfg<ZT, F16>;
+    static_assert(!(ZT && F16), "Z in TMEM is a TF32-only variant");
     constexpr int STAGE = K::STAGE, NST = K::NST;
-    constexpr int Z_OFF = 0, B_OFF = ZT ? 0 : Z_BYTES, I_OFF = B_OFF + B_BYTES, C_OFF = I_OFF + I_BYTES;
+    constexpr int Z_OFF = 0, B_OFF = ZT ? 0 : Z_BYTES, I_OFF = B_OFF + B_BYTES, C_OFF = I_OFF + K::I_BYTES;
     uint8_t* epi_base = smem + NST * STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + EPI_BYTES + EPI_PAD);
     uint64_t* full = bars;         // [8] leader: producer + 2 x 4 transform warps, B tx
@@ -213,10 +238,13 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                 for (int64_t kb = 0; kb < p.nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* st = smem + stage * STAGE;
-                    const int32_t k0 = (int32_t)(kb * BK);
-                    mbar_expect_tx(&afull[stage], (uint32_t)(I_BYTES + C_BYTES));
-                    tma_load_2d(st + I_OFF, &mapAbar8, &afull[stage], k0, i0);
-                    tma_load_2d(st + C_OFF, &mapAbar16, &afull[stage], k0, c0);
+                    const int32_t k0 = (int32_t)(kb * K::KB);
+                    mbar_expect_tx(&afull[stage], (uint32_t)(K::I_BYTES + K::C_BYTES));
+#pragma unroll
+                    for (int h = 0; h < K::HALVES; ++h) {
+                        tma_load_2d(st + I_OFF + h * K::I_HALF, &mapAbar8, &afull[stage], k0 + 32 * h, i0);
+                        tma_load_2d(st + C_OFF + h * K::C_HALF, &mapAbar16, &afull[stage], k0 + 32 * h, c0);
+                    }
                     const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
                     if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * (p.bn / 2) * BK * 4));
                     tma2_2d(st + B_OFF, &mapPi, fb, k0, b0, pol);
@@ -230,7 +258,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            const uint32_t idesc = idesc2_tf32(bn, false, false);
+            const uint32_t idesc = F16 ? idesc2_f16(bn, false, false) : idesc2_tf32(bn, false, false);
             const uint64_t zdesc0 = smem_desc(smem_u32(smem) + Z_OFF, 16, 1024, 2);
             const uint64_t bdesc0 = smem_desc(smem_u32(smem) + B_OFF, 16, 1024, 2);
             int zs = 0;
@@ -248,6 +276,8 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                             if constexpr (ZT)
                                 mma2_tf32_ts(d, tmem_base + (uint32_t)(ZSLOT0 + zs * 32 + ks * 8), bdesc0 + off + 2 * ks,
                                              idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                            else if constexpr (F16)
+                                mma2_f16(d, zdesc0 + off + 2 * ks, bdesc0 + off + 2 * ks, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
                             else
                                 mma2_tf32(d, zdesc0 + off + 2 * ks, bdesc0 + off + 2 * ks, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
                         }
@@ -279,7 +309,18 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
         int stage = 0, sidx = 0;
         uint32_t phase = 0;
         int64_t g = 0;  // K-block counter (ZT: Z slot g mod NZ)
+        // blocked (shared-memory Z) form: thread = (chunk tq, 2 i of pair tip, 4 c of quad tcq)
+        const int tid = ((warp - TW0) % TW_W) * 32 + lane;
+        const int tq = tid & 7, tip = (tid >> 3) & 3, tcq = tid >> 5;
         for (int64_t t = pair_id; t < p.ntiles; t += npairs) {
+            float zsx[2] = {1.f, 1.f}, zsy[4] = {1.f, 1.f, 1.f, 1.f};  // F16: the exact power-of-two zscale
+            if constexpr (F16) {
+                const int4 tl = __ldg(&p.tiles[t]);
+#pragma unroll
+                for (int a = 0; a < 2; ++a) zsx[a] = __ldg(&p.zscale[tl.x * 16 + 8 * (int)rank + 2 * tip + a]);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) zsy[b] = __ldg(&p.zscale[tl.y * 16 + 4 * tcq + b]);
+            }
             for (int64_t kb = 0; kb < p.nk; ++kb, ++g) {
                 const int st_ = stage;
                 const uint32_t ph_ = phase;
@@ -314,18 +355,72 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                     }
                     tc_fence_before();
                 } else if (!(p.dev & 1)) {
-                    uint8_t* rz = st + Z_OFF + rho * 128;
-                    float4 x[8], y[8];
+                    // Blocked: thread (group gq, chunk q) forms Z chunk q of the 2 i x 4 c
+                    // rows of its group from 2 + 4 abar chunks, so every activation
+                    // chunk it loads serves 4 (x) or 2 (y) Z rows -- the loads were two
+                    // per Z chunk, and the shared-memory load wavefronts bounded the
+                    // K-block period.  A quarter-warp is one group's 8 chunks: its loads
+                    // and stores hit 8 distinct 16-byte bank slots.
+                    uint8_t* zb = st + Z_OFF;
+                    if constexpr (F16) {
+                        // Z chunk q (8 fp16) = examples 8q .. 8q + 7 = fp32 chunks 2(q % 4)
+                        // and 2(q % 4) + 1 of abar box h = q / 4; box h = 1 reads its chunks
+                        // in the other order, so a quarter-warp's first load covers slots
+                        // {0,2,4,6} (box 0) and {1,3,5,7} (box 1) without conflicts
+                        const int h = tq >> 2, ca = 2 * (tq & 3) + h, cb = 2 * (tq & 3) + 1 - h;
+                        float4 x0[2], x1[2], y0[4], y1[4];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        x[q] = *reinterpret_cast<const float4*>(ri + ((q ^ (il & 7)) << 4));
-                        y[q] = *reinterpret_cast<const float4*>(rc + ((q ^ (cl & 7)) << 4));
+                        for (int a = 0; a < 2; ++a) {
+                            const int il = 2 * tip + a;
+                            const uint8_t* r = st + I_OFF + h * K::I_HALF + il * 128;
+                            const float4 u = *reinterpret_cast<const float4*>(r + ((ca ^ (il & 7)) << 4));
+                            const float4 v = *reinterpret_cast<const float4*>(r + ((cb ^ (il & 7)) << 4));
+                            x0[a] = scale4(h ? v : u, zsx[a]);
+                            x1[a] = scale4(h ? u : v, zsx[a]);
+                        }
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int cl = 4 * tcq + b;
+                            const uint8_t* r = st + C_OFF + h * K::C_HALF + cl * 128;
+                            const float4 u = *reinterpret_cast<const float4*>(r + ((ca ^ (cl & 7)) << 4));
+                            const float4 v = *reinterpret_cast<const float4*>(r + ((cb ^ (cl & 7)) << 4));
+                            y0[b] = scale4(h ? v : u, zsy[b]);
+                            y1[b] = scale4(h ? u : v, zsy[b]);
+                        }
+#pragma unroll
+                        for (int a = 0; a < 2; ++a)
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const int rho = ic_row(2 * tip + a, 4 * tcq + b);
+                                uint4 w;
+                                w.x = h2_bits(x0[a].x * y0[b].x, x0[a].y * y0[b].y);
+                                w.y = h2_bits(x0[a].z * y0[b].z, x0[a].w * y0[b].w);
+                                w.z = h2_bits(x1[a].x * y1[b].x, x1[a].y * y1[b].y);
+                                w.w = h2_bits(x1[a].z * y1[b].z, x1[a].w * y1[b].w);
+                                *reinterpret_cast<uint4*>(zb + rho * 128 + ((tq ^ (rho & 7)) << 4)) = w;
+                            }
+                    } else {
+                        float4 x[2], y[4];
+#pragma unroll
+                        for (int a = 0; a < 2; ++a) {
+                            const int il = 2 * tip + a;
+                            x[a] = *reinterpret_cast<const float4*>(st + I_OFF + il * 128 + ((tq ^ (il & 7)) << 4));
+                        }
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int cl = 4 * tcq + b;
+                            y[b] = *reinterpret_cast<const float4*>(st + C_OFF + cl * 128 + ((tq ^ (cl & 7)) << 4));
+                        }
+#pragma unroll
+                        for (int a = 0; a < 2; ++a)
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const int rho = ic_row(2 * tip + a, 4 * tcq + b);
+                                *reinterpret_cast<float4*>(zb + rho * 128 + ((tq ^ (rho & 7)) << 4)) =
+                                    make_float4(round_tf32(x[a].x * y[b].x), round_tf32(x[a].y * y[b].y),
+                                                round_tf32(x[a].z * y[b].z), round_tf32(x[a].w * y[b].w));
+                            }
                     }
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        *reinterpret_cast<float4*>(rz + ((q ^ (rho & 7)) << 4)) =
-                            make_float4(round_tf32(x[q].x * y[q].x), round_tf32(x[q].y * y[q].y),
-                                        round_tf32(x[q].z * y[q].z), round_tf32(x[q].w * y[q].w));
                     fence_proxy_async();
                 }
                 __syncwarp();
@@ -353,6 +448,11 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
             // lanes holding a bias entry (index T_k) or, without TMA, any valid entry
             const bool scalar = (ii <= p.tk && cc <= p.tk) && (ii == p.tk || cc == p.tk || !p.tma) && !(p.dev & 2);
             const int64_t jt0 = (int64_t)tl.z * p.bn;
+            // F16: undo the power-of-two scales (exact): alpha / (zscale[i] zscale[c]) per
+            // lane, / pscale... per column (pscale holds the inverse column scale)
+            float rsc = p.alpha;
+            if constexpr (F16)
+                rsc = p.alpha / (__ldg(&p.zscale[i0 + il]) * __ldg(&p.zscale[c0 + cl]));
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             // chunk n + 1's TMEM load is in flight while chunk n is staged and stored
@@ -365,8 +465,14 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                 if (J0 >= p.npairs) break;  // uniform across the group
                 float v[CH];
                 tmem_ld_wait8(r);
+                if constexpr (F16) {
 #pragma unroll
-                for (int e = 0; e < CH; ++e) v[e] = __uint_as_float(r[e]) * p.alpha;
+                    for (int e = 0; e < CH; ++e)
+                        v[e] = __uint_as_float(r[e]) * rsc * (J0 + e < p.npairs ? __ldg(&p.pscale[J0 + e]) : 0.f);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < CH; ++e) v[e] = __uint_as_float(r[e]) * rsc;
+                }
                 if (jj0 + CH < jend && J0 + CH < p.npairs) tmem_ld8_issue(tacc + (uint32_t)(jj0 + CH), r);
                 const int ncol = (int)(p.npairs - J0 < CH ? p.npairs - J0 : CH);
                 if (box_ok) {
@@ -505,6 +611,86 @@ __global__ void pack_delta_products_kernel(const float* __restrict__ dT, const i
     }
 }
 
+// ---- F16 operands (precision kF16S) ----------------------------------------
+// Exact power-of-two scales put every operand into fp16's normal range with
+// headroom: |abar_i zscale[i]| < 2^7 (so |Z| < 2^14) and |Pi_j| / pscale[j]
+// < 2^14, products < 2^28 in the fp32 accumulator.  Values below 2^-14 of
+// the scaled range (2^-28 of a row's largest) lose significand bits to fp16
+// subnormals -- ~1e-9 relative contributions, far below the 2^-12 rounding
+// of the 11-bit significand every operand shares with TF32.
+
+__device__ __forceinline__ float block_absmax(float m, float* red) {
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) red[0] = m;
+    }
+    __syncthreads();
+    m = red[0];
+    __syncthreads();
+    return m;
+}
+
+// 2^(cap - e) with max|x| < 2^e: |x| * scale < 2^cap (1 for an all-zero row)
+__device__ __forceinline__ float pow2_scale(float m, int cap) {
+    if (!(m > 0.f) || isinf(m)) return 1.f;
+    int e;
+    frexpf(m, &e);
+    return ldexpf(1.f, max(-126, min(127, cap - e)));
+}
+
+// zscale[i] for the abar^T rows (rows >= `rows`: 1); one CTA per row
+__global__ void zscale_kernel(const float* __restrict__ akT, int64_t rows, int64_t n, int64_t ldn,
+                              float* __restrict__ zscale, int64_t padded) {
+    __shared__ float red[32];
+    for (int64_t r = blockIdx.x; r < padded; r += gridDim.x) {
+        float m = 0.f;
+        if (r < rows)
+            for (int64_t q = threadIdx.x; q < n; q += blockDim.x) m = fmaxf(m, fabsf(akT[r * ldn + q]));
+        m = block_absmax(m, red);
+        if (threadIdx.x == 0) zscale[r] = r < rows ? pow2_scale(m, 7) : 1.f;
+    }
+}
+
+// out[j][.] = fp16(Pi_j[.] * w_j), pscale[j] = 1 / w_j; Pi_j = the profile row
+// (o_j U + o''_j) or delta_o delta_o''; one CTA per packed column, two passes
+template <bool DELTA>
+__global__ void pack_h_kernel(const float* __restrict__ src, const int4* __restrict__ pairs, int64_t U, int64_t n,
+                              int64_t ldn, __half* __restrict__ out, float* __restrict__ pscale, int64_t npairs) {
+    __shared__ float red[32];
+    for (int64_t j = blockIdx.x; j < npairs; j += gridDim.x) {
+        const int4 pr = pairs[j];
+        const float* a = DELTA ? src + pr.x * ldn : src + (pr.x * U + pr.y) * ldn;
+        const float* b = src + pr.y * ldn;
+        auto val = [&](int64_t q) { return q < n ? (DELTA ? a[q] * b[q] : a[q]) : 0.f; };
+        float m = 0.f;
+        for (int64_t q = threadIdx.x; q < n; q += blockDim.x) m = fmaxf(m, fabsf(val(q)));
+        m = block_absmax(m, red);
+        const float w = pow2_scale(m, 14);
+        if (threadIdx.x == 0) pscale[j] = 1.f / w;
+        __half2* d = reinterpret_cast<__half2*>(out + j * ldn);
+        for (int64_t q = threadIdx.x; q < ldn / 2; q += blockDim.x)
+            d[q] = __floats2half2_rn(val(2 * q) * w, val(2 * q + 1) * w);
+    }
+}
+
+// 2-D fp16 K-major map (rows x K, pitch ld halves), box (64, box_rows), 128-byte swizzle
+inline CUtensorMap make_map_h(const __half* p, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows}, es[2] = {1, 1};
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || (strides[0] & 15))
+        throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(p), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (f16) failed: " + std::to_string((int)r));
+    return m;
+}
+
 }  // namespace tc
 
 template <>
@@ -515,7 +701,8 @@ struct SymKr<float> {
     }
 
     static bool run(int prec, cudaStream_t s, const SymKrArgs<float>& a) {
-        if (prec != kTF32) return false;
+        if (!tf32_class(prec)) return false;
+        const bool f16 = prec == kF16S;
         // without TMA-addressable H (pitch or offset not 16-byte aligned) every
         // entry takes the scalar path: slower, same values
         const int tma = tma_ok(a.H, a.ldh, a.woff, a.tk) ? 1 : 0;
@@ -549,7 +736,8 @@ struct SymKr<float> {
         }
         // Z in shared memory (default) or in TMEM (CURVKIT_SYMKR_TS=1: correct, but measured
         // slower on B200 -- c1 1.08 vs 0.92 ms, c2 9.2 vs 8.6 ms, c3 97.7 vs 85.7 ms)
-        static const bool zt = getenv("CURVKIT_SYMKR_TS") != nullptr;
+        static const bool zt_env = getenv("CURVKIT_SYMKR_TS") != nullptr;
+        const bool zt = zt_env && !f16;
         const int64_t max_bn = zt ? sym::Cfg<true>::MAX_BN : sym::Cfg<false>::MAX_BN;
         const int64_t ntn = ceil_div(np, max_bn);
         const int64_t bn = round_up(ceil_div(np, ntn), 16);  // <= max_bn
@@ -574,8 +762,19 @@ struct SymKr<float> {
         const int4* dpairs = static_cast<const int4*>(cached_upload(pairs.data(), pairs.size() * sizeof(int4)));
         const int4* dtiles = static_cast<const int4*>(cached_upload(tiles.data(), tiles.size() * sizeof(int4)));
         // packed profiles (B operand, K-major rows of ldn examples), rounded to nearest TF32
-        DevMem pi((size_t)np * a.ldn * 4, s);
-        if (a.delta_products)
+        // (F16: scaled and rounded to nearest fp16, with the column scales)
+        DevMem pi((size_t)np * a.ldn * (f16 ? 2 : 4), s);
+        DevMem psc(f16 ? (size_t)np * 4 : 0, s), zsc(f16 ? (size_t)nb * 16 * 4 : 0, s);
+        if (f16) {
+            const unsigned g = (unsigned)std::min<int64_t>(np, 8 * tc::num_sms());
+            if (a.delta_products)
+                tc::pack_h_kernel<true><<<g, 256, 0, s>>>(a.prof, dpairs, U, a.n, a.ldn, dptr<__half>(pi), dptr<float>(psc), np);
+            else
+                tc::pack_h_kernel<false><<<g, 256, 0, s>>>(a.prof, dpairs, U, a.n, a.ldn, dptr<__half>(pi), dptr<float>(psc), np);
+            CK_LAUNCH();
+            tc::zscale_kernel<<<(unsigned)std::min<int64_t>(nb * 16, 4096), 256, 0, s>>>(a.akT, tk + 1, a.n, a.ldn,
+                                                                                         dptr<float>(zsc), nb * 16);
+        } else if (a.delta_products)
             tc::pack_delta_products_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
                 a.prof, dpairs, a.ldn, dptr<float>(pi), np);
         else
@@ -584,7 +783,8 @@ struct SymKr<float> {
         CK_LAUNCH();
         CUtensorMap m8 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 8);
         CUtensorMap m16 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 16);
-        CUtensorMap mpi = tc::make_map(dptr<float>(pi), np, a.n, a.ldn, 0, (int)(bn / 2));
+        CUtensorMap mpi = f16 ? tc::make_map_h(dptr<__half>(pi), np, a.n, a.ldn, (int)(bn / 2))
+                              : tc::make_map(dptr<float>(pi), np, a.n, a.ldn, 0, (int)(bn / 2));
         tc::sym::HMaps hm;
         std::memset(&hm, 0, sizeof hm);
         const int64_t L = a.ldh, nu = u1 - u0;
@@ -603,8 +803,9 @@ struct SymKr<float> {
             hm.m[4 * x + 3] = tc::make_map_orbit(base, tk, tk, nu, u1, L, tk * L, tk, 16, 8, E);
         }
         sym::Params prm{dtiles, (int64_t)tiles.size(), dpairs, np, bn, tk,
-                        ceil_div(a.n, tc::BK), U, a.H, a.ldh, a.woff, a.boff, a.alpha, tma, 0,
-                        u0, u1, bwoff, bboff};
+                        ceil_div(a.n, f16 ? (int64_t)sym::Cfg<false, true>::KB : (int64_t)tc::BK), U, a.H, a.ldh,
+                        a.woff, a.boff, a.alpha, tma, 0, u0, u1, bwoff, bboff,
+                        f16 ? dptr<float>(zsc) : nullptr, f16 ? dptr<float>(psc) : nullptr};
         static const int dev = getenv("CURVKIT_DEV_SYMKR") ? atoi(getenv("CURVKIT_DEV_SYMKR")) : 0;
         prm.dev = dev;
         func_attr_once((const void*)sym::symkr_kernel<true, false>, [] {
@@ -614,10 +815,18 @@ struct SymKr<float> {
                                          sym::Cfg<false>::SMEM_BYTES));
             CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sym::Cfg<false>::SMEM_BYTES));
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sym::Cfg<false, true>::SMEM_BYTES));
+            CK_CUDA(cudaFuncSetAttribute(sym::symkr_kernel<false, true, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sym::Cfg<false, true>::SMEM_BYTES));
         });
         const int grid = 2 * (int)std::min<int64_t>((int64_t)tiles.size(), tc::num_sms() / 2);
         const bool band = u0 != 0 || u1 != U || bwoff != a.woff || bboff != a.boff;
-        if (band)
+        if (f16 && band)
+            sym::symkr_kernel<false, true, true><<<grid, sym::kThreads, sym::Cfg<false, true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        else if (f16)
+            sym::symkr_kernel<false, false, true><<<grid, sym::kThreads, sym::Cfg<false, true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
+        else if (band)
             sym::symkr_kernel<false, true><<<grid, sym::kThreads, sym::Cfg<false>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);
         else if (zt)
             sym::symkr_kernel<true, false><<<grid, sym::kThreads, sym::Cfg<true>::SMEM_BYTES, s>>>(m8, m16, mpi, hm, prm);

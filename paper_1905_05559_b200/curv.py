@@ -21,7 +21,7 @@ import numpy as np
 from . import _lib
 from .errors import ContractError, ShapeError
 
-PRECISION = {"f64": 0, "f32": 1, "tf32": 2, "tf32x3": 3}
+PRECISION = {"f64": 0, "f32": 1, "tf32": 2, "tf32x3": 3, "f16s": 4}
 
 
 class Activation(IntEnum):  # model.hpp:11

@@ -12,7 +12,7 @@ from paper_1905_05559_b200.workloads import CONFIGS
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"f64": 1e-10, "f32": 1e-5, "tf32": 1e-3, "tf32x3": 1e-5}
+TOL = {"f64": 1e-10, "f32": 1e-5, "tf32": 1e-3, "tf32x3": 1e-5, "f16s": 1e-3}
 PRECS = list(TOL)
 
 
