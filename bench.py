@@ -79,9 +79,13 @@ def dist_env():
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
-        return json.load(open(path)), "measured (MEASURED_PEAKS.json)"
-    # B200_PROFILING.md fallback figures
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
+        pk, kind = json.load(open(path)), "measured (MEASURED_PEAKS.json)"
+    else:  # B200_PROFILING.md fallback figures
+        pk, kind = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
+    f64 = os.path.join(ROOT, "profiles", "fp64_peak.json")  # FP64 tensor-core peak (tools/dmma_rate.cu)
+    if os.path.exists(f64) and "fp64_tflops" not in pk:
+        pk["fp64_tflops"] = json.load(open(f64))["fp64_tflops"]
+    return pk, kind
 
 
 def entries_per_step(name, P):
@@ -294,8 +298,8 @@ def roofline(prof, steps, ms_step, pk, pk_kind, prec, traffic=None):
             out.update(bound="tensor" if prec == "f64" else "fma", achieved=achieved, unit="TFLOP/s",
                        peak=fp64 if prec == "f64" else None,
                        frac=(achieved / fp64) if (prec == "f64" and fp64) else None,
-                       peak_note=("FP64 DMMA peak measured by tools/mma_rate_f64 (profiles/)" if prec == "f64"
-                                  else "SIMT fp32 path"))
+                       peak_note=("FP64 tensor-core (DMMA) peak measured by tools/dmma_rate.cu (profiles/fp64_peak.json)"
+                                  if prec == "f64" else "SIMT fp32 path"))
     else:
         achieved = r["bytes"] / (r["ms"] / 1e3) / 1e9
         out.update(bound="hbm", achieved=achieved, unit="GB/s", peak=pk["hbm_gbs"], frac=achieved / pk["hbm_gbs"])
@@ -453,17 +457,25 @@ def e2e_band_run(job, steps, stream, torch, barrier, red_dev):
                                       "the band downloaded to pinned host memory on every rank"}
 
 
+def load_traffic(name):
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(tfile)).get(name) if os.path.exists(tfile) else None
+
+
 def run_extra(torch, dev, stream, pk, pk_kind):
-    """The other BASELINE configurations on the same GPU (N = 1)."""
+    """The other BASELINE configurations on the same GPU (N = 1), and the
+    headline configuration in the f16s precision mode."""
     out = {}
-    for name, prec, steps in (("c2", "tf32", 8), ("c1", "tf32", 20), ("c1", "f64", 3)):
+    for name, prec, steps in (("c3", "f16s", 5), ("c2", "tf32", 8), ("c2", "f16s", 8), ("c1", "tf32", 20),
+                              ("c1", "f64", 3)):
         job = Job(name, prec, dev, torch)
         ms, prof, launches, _ = timed(job, steps, 2, stream, torch)
         P = job.wl.P
         out[f"{name}_{prec}"] = {"workload": config_dict(job.wl)["workload"], "dtype": prec,
                                  "value": entries_per_step(name, P) / (ms / 1e3), "unit": "entries/s",
                                  "ms_per_step": ms, "steps": steps, "gpu_launches": launches,
-                                 "roofline": roofline(prof, steps, ms, pk, pk_kind, prec),
+                                 "roofline": roofline(prof, steps, ms, pk, pk_kind, prec,
+                                                      load_traffic(name) if prec == "tf32" else None),
                                  "kernels": kernels_table(prof, steps)}
         job.free()
         del job
@@ -578,10 +590,7 @@ def run_b200(args):
             comm.close()
         return
     pk, pk_kind = peaks()
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(wl.name)
+    traffic = load_traffic(wl.name) if args.precision == "tf32" else None
     roof = roofline(prof, args.steps, ms, pk, pk_kind, args.precision, traffic)
     cpu = None
     extra = None

@@ -745,7 +745,11 @@ struct SymKr<float> {
         // Tile order = write locality: the ~74 tiles in flight walk an SB x SB square
         // of (ib, cb) blocks, so both the c-contiguous (types 1, 4) and the
         // i-contiguous (types 2, 3) row segments of concurrent tiles are adjacent in H.
-        static const int64_t SB = getenv("CURVKIT_SYMKR_SB") ? atoi(getenv("CURVKIT_SYMKR_SB")) : 5;  // measured: 5 best on c1 (0.92 vs 1.00 ms row-major)
+        // measured: 5 best on c1 (0.92 vs 1.00 ms row-major); a packed profile larger than
+        // ~1/4 of L2 is re-read from HBM once per square (c3: 330 MB, 55 squares, 33 GB of
+        // reads), so larger squares there (c3 symkr 81.5 -> 79.5 ms at 10-25)
+        static const int64_t SB_env = getenv("CURVKIT_SYMKR_SB") ? atoi(getenv("CURVKIT_SYMKR_SB")) : -1;
+        const int64_t SB = SB_env >= 0 ? SB_env : ((double)np * a.ldn * (f16 ? 2 : 4) > 32e6 ? 12 : 5);
         std::vector<int4> tiles;
         if (SB <= 0) {
             for (int64_t ib = 0; ib < nb; ++ib)
