@@ -200,6 +200,25 @@ int curvkit_dev_opg_topk_filtered(const curvkit_model* model, const void* params
                                   int64_t filter_steps, int64_t filter_degree, uint64_t seed, int32_t precision,
                                   void* q, void* lambda, void* stream);
 
+/* Streaming OPG eigensolver: curv::IncrementalOpgEigs (eigensolve.hpp:52-78,
+ * eigensolve.cpp:158-243) with the reference's algorithm and update windows
+ * (rows are buffered until at least k are waiting; [diag(sigma) V^T; rows] is
+ * re-factorised and truncated to rank k), the P-length work on the device in
+ * fp64.  create: ContractError unless 1 <= k <= p.  push_block: rows x p
+ * row-major fp64 (host) / rows x ld (device, ld >= p); ContractError for an
+ * empty block.  rows_seen / updates as the class's accessors.  finalize:
+ * q (p x k row-major) and lambda (k, descending) = sigma^2 / n_total; the
+ * reference's ContractErrors for a row-count mismatch, leftover buffered rows
+ * and no update.  The handle owns device memory until destroy. */
+typedef struct curvkit_incr_opg_s* curvkit_incr_opg;
+int curvkit_incr_opg_create(int64_t p, int64_t k, curvkit_incr_opg* out);
+int curvkit_incr_opg_push_block(curvkit_incr_opg h, const double* block, int64_t rows);
+int curvkit_incr_opg_dev_push_block(curvkit_incr_opg h, const void* block, int64_t rows, int64_t ld, void* stream);
+int curvkit_incr_opg_counts(curvkit_incr_opg h, int64_t* rows_seen, int64_t* updates);
+int curvkit_incr_opg_finalize(curvkit_incr_opg h, int64_t n_total, double* q_out, double* lambda_out);
+int curvkit_incr_opg_dev_finalize(curvkit_incr_opg h, int64_t n_total, void* q, void* lambda, void* stream);
+int curvkit_incr_opg_destroy(curvkit_incr_opg h);
+
 /* Unit bands: the multi-GPU layout of H and G (one process per GPU, DESIGN.md
  * section 7).  Shard s of nshards owns the output units
  * [unit_begin[k], unit_end[k]) of every layer k (L - 1 entries each) and

@@ -65,6 +65,13 @@ SIGNATURES = {
     "curvkit_comm_unique_id": [C.POINTER(C.c_uint8)],
     "curvkit_comm_init": [C.POINTER(C.c_uint8), i32, i32, C.POINTER(vptr)],
     "curvkit_comm_destroy": [vptr],
+    "curvkit_incr_opg_create": [i64, i64, C.POINTER(vptr)],
+    "curvkit_incr_opg_push_block": [vptr, dptr, i64],
+    "curvkit_incr_opg_dev_push_block": [vptr, vptr, i64, i64, vptr],
+    "curvkit_incr_opg_counts": [vptr, C.POINTER(i64), C.POINTER(i64)],
+    "curvkit_incr_opg_finalize": [vptr, i64, dptr, dptr],
+    "curvkit_incr_opg_dev_finalize": [vptr, i64, vptr, vptr, vptr],
+    "curvkit_incr_opg_destroy": [vptr],
     "curvkit_topk_shard_rows": [_MP, i64, i64, C.POINTER(i64), C.POINTER(i64)],
     "curvkit_dev_opg_topk_sharded": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr, vptr],
     "curvkit_dev_opg_topk_sharded_filtered": [_MP, vptr, vptr, vptr, i64, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr,

@@ -21,6 +21,7 @@
 #include "eigen.cuh"
 #include "lanczos.cuh"
 #include "gemm_tc.cuh"
+#include "incremental.cuh"
 #include "model.cuh"
 #include "prof.cuh"
 
@@ -843,6 +844,66 @@ int curvkit_dev_gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t ld
         if (tf32_class(precision) || precision == k3xTF32) gemm_tf32_store(tc_form(precision), s, m, n, k, A, B, c, ldc, alpha);
         else CurvGemm<float, EpiStore<float>>::run(precision, s, m, n, k, A, B, e);
     });
+}
+
+struct curvkit_incr_opg_s {
+    ck::IncrOpg st;
+    int dev;
+};
+
+int curvkit_incr_opg_create(int64_t p, int64_t k, curvkit_incr_opg* out) {
+    return guard([&] {
+        if (!out) contract("incr_opg_create: null output");
+        ck::IncrOpg st(p, k);  // the reference's k range check, before any device work
+        int dev = 0;
+        CK_CUDA(cudaGetDevice(&dev));
+        *out = new curvkit_incr_opg_s{std::move(st), dev};
+    });
+}
+
+int curvkit_incr_opg_push_block(curvkit_incr_opg h, const double* block, int64_t rows) {
+    return guard([&] {
+        if (!h) contract("incr_opg_push_block: null handle");
+        if (rows >= 1 && !block) contract("incr_opg_push_block: null block");
+        CK_CUDA(cudaSetDevice(h->dev));
+        h->st.push(block, rows, h->st.p, cudaMemcpyHostToDevice, lib_stream());
+    });
+}
+
+int curvkit_incr_opg_dev_push_block(curvkit_incr_opg h, const void* block, int64_t rows, int64_t ld, void* stream) {
+    return guard([&] {
+        if (!h) contract("incr_opg_push_block: null handle");
+        if (rows >= 1 && !block) contract("incr_opg_push_block: null block");
+        h->st.push(static_cast<const double*>(block), rows, ld, cudaMemcpyDeviceToDevice, dev_stream(stream));
+    });
+}
+
+int curvkit_incr_opg_counts(curvkit_incr_opg h, int64_t* rows_seen, int64_t* updates) {
+    return guard([&] {
+        if (!h) contract("incr_opg_counts: null handle");
+        if (rows_seen) *rows_seen = h->st.rows_seen;
+        if (updates) *updates = h->st.updates;
+    });
+}
+
+int curvkit_incr_opg_finalize(curvkit_incr_opg h, int64_t n_total, double* q_out, double* lambda_out) {
+    return guard([&] {
+        if (!h) contract("incr_opg_finalize: null handle");
+        CK_CUDA(cudaSetDevice(h->dev));
+        h->st.finalize(n_total, q_out, lambda_out, cudaMemcpyDeviceToHost, lib_stream());
+    });
+}
+
+int curvkit_incr_opg_dev_finalize(curvkit_incr_opg h, int64_t n_total, void* q, void* lambda, void* stream) {
+    return guard([&] {
+        if (!h) contract("incr_opg_finalize: null handle");
+        h->st.finalize(n_total, static_cast<double*>(q), static_cast<double*>(lambda), cudaMemcpyDeviceToDevice,
+                       dev_stream(stream));
+    });
+}
+
+int curvkit_incr_opg_destroy(curvkit_incr_opg h) {
+    return guard([&] { delete h; });
 }
 
 struct curvkit_comm_s {

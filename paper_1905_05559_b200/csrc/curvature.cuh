@@ -665,7 +665,11 @@ struct Engine {
                     orbit_block(k, akT, GT, 0, ldn, n, H, ldh, rlo, rhi);
                     jbeg = Pk;
                 }
-                if (fused && jbeg < Pk) {
+                // dev A/B (CURVKIT_HESS_RGEN): blocks m < k through R generated into HBM
+                // and the pair GEMM instead of the fused kernel
+                static const bool rgen_env = getenv("CURVKIT_HESS_RGEN") != nullptr;
+                const bool rgen_tc = fused && rgen_env && m < k && !band;
+                if (fused && jbeg < Pk && !rgen_tc) {
                     if (!akX) build_ext();
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
                     HessFusedArgs<T> fa{akX, ak_rows, m == k ? nullptr : QX[m], ak_rows, tm1 * ak_rows,
@@ -693,7 +697,7 @@ struct Engine {
                     if (HessFused<T>::run(prec, s, fa, e)) jbeg = Pk;
                 }
                 const int64_t tm = md.w[m], tm1 = md.w[m + 1];
-                int64_t J = (int64_t)(chunk_bytes / ((size_t)tm1 * ldr * sizeof(T)));
+                int64_t J = (int64_t)((rgen_tc ? size_t(2) << 30 : chunk_bytes) / ((size_t)tm1 * ldr * sizeof(T)));
                 J = std::max<int64_t>(128, J / 128 * 128);
                 J = std::min<int64_t>(J, round_up(Pk - jbeg, 128));
                 DevMem rbuf((size_t)tm1 * J * ldr * sizeof(T), s);
@@ -706,7 +710,7 @@ struct Engine {
                     if (m == k && !verify && j0 + Jc - 1 < tm * tm1) opp_hi = std::min(tm1, (j0 + Jc - 1) / tm + 1);
                     const int64_t rows = opp_hi * Jc;
                     RGenArgs<T> g{m == k ? GT : PT[m], m == k ? nullptr : QT[m], akT, dkT, ldn, n, tk, np, tm1,
-                                  j0, Jc, rows, dptr<T>(rbuf), ldr};
+                                  j0, Jc, rows, dptr<T>(rbuf), ldr, rgen_tc ? 1 : 0};
                     {
                         ProfScope ps("hess_rgen", s, 0.0, (double)sizeof(T) * rows * ldr);
                         const int64_t work = rows * (ldr / 4);
@@ -718,8 +722,9 @@ struct Engine {
                     // algorithmic work is counted only while profiling (host loop)
                     const double req = Profiler::get().on ? hess_required_entries(k, m, j0, Jc) : 0.0;
                     ProfScope ps("hess_gemm", s, 2.0 * (double)n * req, (double)sizeof(T) * ((double)rows * ldr + req));
-                    CurvGemm<T, EpiHess<T>>::run(prec, s, rows, tm + 1, n, kmaj(dptr<T>(rbuf), ldr),
-                                                 mnmaj(c.a[m], c.lda[m]), e);
+                    Opnd<T> ra = kmaj(dptr<T>(rbuf), ldr);
+                    if (rgen_tc) ra = pre_rounded(ra);
+                    CurvGemm<T, EpiHess<T>>::run(prec, s, rows, tm + 1, n, ra, mnmaj(c.a[m], c.lda[m]), e);
                 }
             }
         }

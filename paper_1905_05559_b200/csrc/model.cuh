@@ -484,6 +484,7 @@ struct RGenArgs {
     int64_t j0, J, rows;          // rows = (o'' rows generated) * J
     T* R;
     int64_t ldr;
+    int round = 0;                // store R rounded to nearest TF32 (the tensor-core GEMM's A operand)
 };
 
 // One thread per 4 consecutive examples of one R row: every read and the
@@ -508,6 +509,11 @@ __global__ void __launch_bounds__(256) rgen_kernel(RGenArgs<T> g) {
                 const V d = *reinterpret_cast<const V*>(g.dkT + o * g.ldn + e);
                 const V qv = *reinterpret_cast<const V*>(g.q + (i * g.tm1 + opp) * g.ldn + e);
                 p.x += d.x * qv.x; p.y += d.y * qv.y; p.z += d.z * qv.z; p.w += d.w * qv.w;
+            }
+        }
+        if constexpr (sizeof(T) == 4) {
+            if (g.round) {
+                p.x = round_tf32(p.x); p.y = round_tf32(p.y); p.z = round_tf32(p.z); p.w = round_tf32(p.w);
             }
         }
         *reinterpret_cast<V*>(g.R + r * g.ldr + e) = p;

@@ -424,6 +424,59 @@ def opg_eigs_incremental(j_blocks, n_total: int, k: int, oversample: int = 20, p
     return EigenPairs(q, lam)
 
 
+class IncrementalOpgEigs:
+    """curv::IncrementalOpgEigs (eigensolve.hpp:52-78): streaming eigenpairs of
+    G = (1/N) J^T J from row blocks of J, with the reference's algorithm and
+    update windows; the factorisations run on the device in fp64
+    (curvkit_incr_opg_*).  push_block takes b x P float64 rows (numpy, or a
+    CUDA torch tensor); finalize(n_total) returns EigenPairs."""
+
+    def __init__(self, p: int, k: int):
+        self.p, self.k = int(p), int(k)
+        h = C.c_void_p()
+        _lib.check(_lib.load().curvkit_incr_opg_create(self.p, self.k, C.byref(h)))
+        self._h = h
+
+    def push_block(self, block) -> None:
+        if hasattr(block, "data_ptr") and getattr(block, "is_cuda", False):
+            if block.dim() != 2 or block.shape[1] != self.p or block.dtype.itemsize != 8 or block.stride(1) != 1:
+                raise ShapeError(f"IncrementalOpgEigs: block must be b x {self.p} float64 with unit column stride")
+            _lib.check(_lib.load().curvkit_incr_opg_dev_push_block(self._h, block.data_ptr(), block.shape[0],
+                                                                   block.stride(0), None))
+            return
+        b = np.ascontiguousarray(block, dtype=np.float64)
+        if b.ndim != 2 or b.shape[1] != self.p:
+            raise ShapeError(f"IncrementalOpgEigs: block has {b.shape[-1] if b.ndim else 0} columns, "
+                             f"expected {self.p}")
+        _lib.check(_lib.load().curvkit_incr_opg_push_block(self._h, _p(b), b.shape[0]))
+
+    def _counts(self):
+        r, u = C.c_int64(0), C.c_int64(0)
+        _lib.check(_lib.load().curvkit_incr_opg_counts(self._h, C.byref(r), C.byref(u)))
+        return int(r.value), int(u.value)
+
+    def rows_seen(self) -> int:
+        return self._counts()[0]
+
+    def updates(self) -> int:
+        return self._counts()[1]
+
+    def finalize(self, n_total: int) -> EigenPairs:
+        q = np.empty((self.p, self.k))
+        lam = np.empty(self.k)
+        _lib.check(_lib.load().curvkit_incr_opg_finalize(self._h, int(n_total), _p(q), _p(lam)))
+        return EigenPairs(q, lam)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().curvkit_incr_opg_destroy(h)
+            except Exception:  # noqa: BLE001 -- interpreter teardown
+                pass
+            self._h = None
+
+
 def dev_opg_topk_from_jacobian(J, ldj, n, p, k, oversample, power_iters, seed, q, lam, precision="tf32",
                                stream=None):
     _lib.check(_lib.load().curvkit_dev_opg_topk_from_jacobian(_ptr(J), ldj, n, p, k, oversample, power_iters, seed,
