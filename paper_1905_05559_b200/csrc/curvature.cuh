@@ -632,7 +632,9 @@ struct Engine {
                     CK_LAUNCH();
                 }
             };
-            if (fused && (k > 0 || verify || sym_off())) build_ext();
+            // (blocks m < k take R in HBM unless banded or CURVKIT_HESS_FUSED, below)
+            static const bool fused_env = getenv("CURVKIT_HESS_FUSED") != nullptr;
+            if (fused && ((k > 0 && (band || fused_env)) || verify || sym_off())) build_ext();
             prep_stage.end();
             // blocks (k, m), m <= k
             const int64_t Pk = md.block_size(k);
@@ -665,10 +667,13 @@ struct Engine {
                     orbit_block(k, akT, GT, 0, ldn, n, H, ldh, rlo, rhi);
                     jbeg = Pk;
                 }
-                // dev A/B (CURVKIT_HESS_RGEN): blocks m < k through R generated into HBM
-                // and the pair GEMM instead of the fused kernel
-                static const bool rgen_env = getenv("CURVKIT_HESS_RGEN") != nullptr;
-                const bool rgen_tc = fused && rgen_env && m < k && !band;
+                // Blocks m < k (TF32 class, whole blocks): R generated into HBM in 2 GB
+                // chunks (rounded to TF32, write-bound) and the pair GEMM (~570 TF/s)
+                // instead of the fused kernel, whose k-block pipeline runs at ~0.34 of
+                // the TF32 peak for reasons DESIGN.md section 4 did not isolate (c2:
+                // 7.2 -> 5.2 ms).  Unit bands keep the fused kernel (its epilogue
+                // writes band rows); CURVKIT_HESS_FUSED=1 selects it everywhere.
+                const bool rgen_tc = fused && !fused_env && m < k && !band;
                 if (fused && jbeg < Pk && !rgen_tc) {
                     if (!akX) build_ext();
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
@@ -713,8 +718,9 @@ struct Engine {
                                   j0, Jc, rows, dptr<T>(rbuf), ldr, rgen_tc ? 1 : 0};
                     {
                         ProfScope ps("hess_rgen", s, 0.0, (double)sizeof(T) * rows * ldr);
-                        const int64_t work = rows * (ldr / 4);
-                        rgen_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 16), 256, 0, s>>>(g);
+                        const dim3 grid((unsigned)ceil_div(ldr / 4, 256),
+                                        (unsigned)std::min<int64_t>(opp_hi * ceil_div(Jc, RGEN_SEG), 65535));
+                        rgen_kernel<T><<<grid, 256, 0, s>>>(g);
                         CK_LAUNCH();
                     }
                     EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),

@@ -50,6 +50,35 @@ __global__ void incr_rows_to_cols_kernel(const double* __restrict__ blk, int64_t
     }
 }
 
+// sig[c] = || U[:, c] ||_2 over the p rows of U (p x k, ld), one CTA per column
+// (fixed-order block reduction: deterministic)
+__global__ void incr_colnorm_kernel(const double* __restrict__ u, int64_t ld, int64_t p, double* __restrict__ sig) {
+    __shared__ double red[32];
+    const int64_t c = blockIdx.x;
+    double acc = 0.0;
+    for (int64_t r = threadIdx.x; r < p; r += blockDim.x) {
+        const double x = u[r * ld + c];
+        acc += x * x;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) sig[c] = sqrt(acc);
+    }
+}
+
+// U[r][c] *= inv[c]
+__global__ void incr_scale_cols_kernel(double* __restrict__ u, int64_t ld, int64_t p, int64_t k,
+                                       const double* __restrict__ inv) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= p * k) return;
+    const int64_t r = idx / k, c = idx - r * k;
+    u[r * ld + c] *= inv[c];
+}
+
 struct IncrOpg {
     int64_t p = 0, k = 0;
     int64_t rows_seen = 0, updates = 0, buffered = 0;
@@ -123,28 +152,57 @@ struct IncrOpg {
         std::iota(ord.begin(), ord.end(), 0);
         std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return lam[a] > lam[b]; });
         const int64_t keep = std::min(k, m);
-        std::vector<double> sig(keep);
-        for (int64_t c = 0; c < keep; ++c) sig[c] = std::sqrt(std::max(lam[ord[c]], 0.0));
-        const double rank_tol = 1e-12 * std::max(sig[0], 1e-300);
-        // selection, scaled: B[c][j] = V[j][ord c] / sigma_c (0 for rank-deficient columns)
-        std::vector<double> bsel((size_t)keep * m, 0.0);
+        // U = M^T V[:, top keep] (fp64 tensor cores); sigma_c = ||U_c|| (a direction in
+        // the numerical null space of M^T gives ~eps ||M^T||, as the reference's
+        // one-sided Jacobi does -- the Gram eigenvalue alone would say ~sqrt(eps))
+        std::vector<double> bsel((size_t)keep * m);
         for (int64_t c = 0; c < keep; ++c)
-            if (sig[c] > rank_tol)
-                for (int64_t j = 0; j < m; ++j) bsel[(size_t)c * m + j] = vh[(size_t)j * m + ord[c]] / sig[c];
-        DevMem bs((size_t)keep * m * sizeof(double), s);
+            for (int64_t j = 0; j < m; ++j) bsel[(size_t)c * m + j] = vh[(size_t)j * m + ord[c]];
+        DevMem bs((size_t)keep * m * sizeof(double), s), sd((size_t)keep * sizeof(double), s);
         CK_CUDA(cudaMemcpyAsync(bs.p, bsel.data(), bsel.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         DevMem nb((size_t)p * k * sizeof(double), s);
         if (keep < k) CK_CUDA(cudaMemsetAsync(nb.p, 0, (size_t)p * k * sizeof(double), s));
-        // basis[r][c] = sum_j MT[r][j] B[c][j]   (fp64 tensor cores)
         EpiStore<double> e{dptr<double>(nb), k, 0, 1.0, 0.0};
         gemm_dmma(s, p, keep, m, 1, kmaj(dptr<double>(mt), m), kmaj(dptr<double>(bs), m), e);
-        basis = std::move(nb);
-        for (int64_t c = 0; c < keep; ++c) {
-            if (sig[c] > rank_tol) continue;
-            complete_rank_deficient(keep, s);  // the whole tail at once (host)
-            for (int64_t t = c; t < keep; ++t) sig[t] = 0.0;
-            break;
+        incr_colnorm_kernel<<<(unsigned)keep, 256, 0, s>>>(dptr<double>(nb), k, p, dptr<double>(sd));
+        CK_LAUNCH();
+        std::vector<double> sig(keep);
+        CK_CUDA(cudaMemcpyAsync(sig.data(), sd.p, keep * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaStreamSynchronize(s));
+        // descending by the accurate norms (the Gram order can swap near-ties)
+        std::vector<int64_t> perm(keep);
+        std::iota(perm.begin(), perm.end(), 0);
+        std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return sig[a] > sig[b]; });
+        bool permuted = false;
+        for (int64_t c = 0; c < keep; ++c) permuted |= perm[c] != c;
+        if (permuted) {  // reorder the columns of U by a second pass of the small GEMM
+            std::vector<double> b2((size_t)keep * m), s2(keep);
+            for (int64_t c = 0; c < keep; ++c) {
+                std::copy(bsel.begin() + (size_t)perm[c] * m, bsel.begin() + (size_t)(perm[c] + 1) * m,
+                          b2.begin() + (size_t)c * m);
+                s2[c] = sig[perm[c]];
+            }
+            CK_CUDA(cudaMemcpyAsync(bs.p, b2.data(), b2.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+            gemm_dmma(s, p, keep, m, 1, kmaj(dptr<double>(mt), m), kmaj(dptr<double>(bs), m), e);
+            sig = s2;
         }
+        const double rank_tol = 1e-12 * std::max(sig[0], 1e-300);
+        std::vector<double> inv(keep);
+        int64_t first_def = keep;
+        for (int64_t c = 0; c < keep; ++c) {
+            if (sig[c] > rank_tol) {
+                inv[c] = 1.0 / sig[c];
+            } else {
+                inv[c] = 0.0;
+                sig[c] = 0.0;
+                first_def = std::min(first_def, c);
+            }
+        }
+        CK_CUDA(cudaMemcpyAsync(sd.p, inv.data(), keep * sizeof(double), cudaMemcpyHostToDevice, s));
+        incr_scale_cols_kernel<<<blocks_for(p * keep), 256, 0, s>>>(dptr<double>(nb), k, p, keep, dptr<double>(sd));
+        CK_LAUNCH();
+        basis = std::move(nb);
+        if (first_def < keep) complete_rank_deficient(first_def, keep, s);  // host, rare
         sigma = sig;
         has_state = true;
         ++updates;
@@ -154,17 +212,10 @@ struct IncrOpg {
     // Columns c >= the first rank-deficient one: canonical directions e_cand
     // orthogonalised against the accepted columns, first with norm > 0.5
     // (eigensolve.cpp:203-218).
-    void complete_rank_deficient(int64_t keep, cudaStream_t s) {
+    void complete_rank_deficient(int64_t first, int64_t keep, cudaStream_t s) {
         std::vector<double> h((size_t)p * k);
         CK_CUDA(cudaMemcpyAsync(h.data(), basis.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK_CUDA(cudaStreamSynchronize(s));
-        // the accepted columns are those with a nonzero column (bsel rows were zeroed)
-        int64_t first = keep;
-        for (int64_t c = 0; c < keep; ++c) {
-            double nrm = 0.0;
-            for (int64_t r = 0; r < p; ++r) nrm += h[(size_t)r * k + c] * h[(size_t)r * k + c];
-            if (nrm == 0.0) { first = c; break; }
-        }
         for (int64_t c = first; c < keep; ++c) {
             for (int64_t cand = 0; cand < p; ++cand) {
                 std::vector<double> v(p, 0.0);
