@@ -18,6 +18,13 @@
 
 namespace ck {
 
+// Epilogues that split each entry into a direct and a mirrored store
+// (Epi::store_direct / Epi::store_mirror; together they equal Epi::operator())
+template <class E, class = void>
+struct EpiSplit : std::false_type {};
+template <class E>
+struct EpiSplit<E, std::void_t<decltype(&E::store_direct)>> : std::true_type {};
+
 
 template <class Epi>
 __global__ void __launch_bounds__(128, 4) gemm_dmma_kernel(int64_t M, int64_t N, int64_t K, Opnd<double> A,
@@ -85,15 +92,38 @@ __global__ void __launch_bounds__(128, 4) gemm_dmma_kernel(int64_t M, int64_t N,
         __syncthreads();
     }
     // D fragment: row fr, columns 2 fk + {0, 1}
+    if constexpr (EpiSplit<Epi>::value) {
+        // staged: the tile in shared memory, then the direct entries row by row
+        // and the mirrored entries column by column, so both store streams are
+        // 512-byte runs (per-element mirror stores walk down a column of H)
+        constexpr int SP = BN + 1;
+        double* S = smem;  // 64 x 65 <= the two K-panel buffers (after the last barrier)
 #pragma unroll
-    for (int fa = 0; fa < 4; ++fa)
+        for (int fa = 0; fa < 4; ++fa)
 #pragma unroll
-        for (int fb = 0; fb < 4; ++fb)
+            for (int fb = 0; fb < 4; ++fb)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t gm = m0 + wm + 8 * fa + fr, gn = n0 + wn + 8 * fb + 2 * fk + h;
-                if (gm < M && gn < N) epi(bz, gm, gn, acc[fa][fb][h]);
-            }
+                for (int h = 0; h < 2; ++h) S[(wm + 8 * fa + fr) * SP + wn + 8 * fb + 2 * fk + h] = acc[fa][fb][h];
+        __syncthreads();
+        for (int idx = t; idx < BM * BN; idx += 128) {
+            const int r = idx / BN, c = idx % BN;
+            if (m0 + r < M && n0 + c < N) epi.store_direct(bz, m0 + r, n0 + c, S[r * SP + c]);
+        }
+        for (int idx = t; idx < BM * BN; idx += 128) {
+            const int c = idx / BM, r = idx % BM;
+            if (m0 + r < M && n0 + c < N) epi.store_mirror(bz, m0 + r, n0 + c, S[r * SP + c]);
+        }
+    } else {
+#pragma unroll
+        for (int fa = 0; fa < 4; ++fa)
+#pragma unroll
+            for (int fb = 0; fb < 4; ++fb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t gm = m0 + wm + 8 * fa + fr, gn = n0 + wn + 8 * fb + 2 * fk + h;
+                    if (gm < M && gn < N) epi(bz, gm, gn, acc[fa][fb][h]);
+                }
+    }
 }
 
 template <class Epi>

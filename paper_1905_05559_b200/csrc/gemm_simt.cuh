@@ -201,6 +201,15 @@ struct EpiSymLower {
         c[m * ldc + n] = v;
         c[n * ldc + m] = v;
     }
+    // the two stores of operator() separately (staged fp64 epilogue)
+    __device__ void store_direct(int, int64_t m, int64_t n, T acc) const {
+        m += roff;
+        if (n <= m) c[m * ldc + n] = alpha * acc;
+    }
+    __device__ void store_mirror(int, int64_t m, int64_t n, T acc) const {
+        m += roff;
+        if (n <= m) c[n * ldc + m] = alpha * acc;
+    }
     __device__ void block(int64_t row0, int64_t col0, int64_t M, int64_t N, const float (*buf)[36], const float* v,
                           int lane) const {
         {  // lower entries (col <= row): 16-byte vectors along rows

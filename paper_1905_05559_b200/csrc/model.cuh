@@ -666,6 +666,20 @@ struct EpiHess {
             if (mirror) H[gc * ldh + gr] = v;
         }
     }
+    // the two stores of operator() separately (staged fp64 epilogue)
+    __device__ void store_direct(int, int64_t r, int64_t c, T acc) const {
+        const int64_t opp = r / J, jj = r - opp * J;
+        const int64_t gr = woffk + j0 + jj, gc = gcol(opp, c);
+        if (!owns(gr) || (diag && mirror && gc > gr)) return;
+        H[(gr - rsh) * ldh + gc] = alpha * acc;
+    }
+    __device__ void store_mirror(int, int64_t r, int64_t c, T acc) const {
+        if (!mirror) return;
+        const int64_t opp = r / J, jj = r - opp * J;
+        const int64_t gr = woffk + j0 + jj, gc = gcol(opp, c);
+        if (!owns(gr) || (diag && gc > gr)) return;
+        H[gc * ldh + gr] = alpha * acc;
+    }
     // 32 x 32 block stored by two TMA boxes (direct at (gr0, gc0), mirror at
     // (gc0, gr0); gr0 returned as the storage row): rows in one band and owned, columns inside the weight
     // columns, and on diagonal blocks strictly below the diagonal
