@@ -77,6 +77,24 @@ struct SymKrArgs {
     int64_t u0 = 0, u1 = -1, bwoff = -1, bboff = -1;
 };
 
+// kF16S OPG rectangles (blocks m < k): J^T in fp16 with an exact power-of-two
+// scale per parameter row (symkr.cuh), multiplied on the fp16 datapath
+struct JtF16Args {
+    int S;
+    const float* akT[kMaxLayers];  // abar_k^T [T_k + 1][ldn] (row T_k = ones)
+    const float* dT[kMaxLayers];   // delta_k^T [T_{k+1}][ldn]
+    int64_t w[kMaxLayers + 1], woff[kMaxLayers], boff[kMaxLayers];
+    int64_t P, n, ldn;
+};
+template <class T>
+struct OpgF16 {
+    // J^T (P x ldn fp16) and the inverse row scales (P floats); false: no fp16 form
+    static bool build(cudaStream_t, const JtF16Args&, DevMem&, DevMem&) { return false; }
+    // G rows [r0, r1) x columns [0, cols) = alpha J^T[r0:r1] J^T[0:cols]^T, mirrored
+    static void rect(cudaStream_t, int64_t, int64_t, int64_t, int64_t, const DevMem&, int64_t, const DevMem&, T*,
+                     int64_t, T) {}
+};
+
 template <class T>
 struct SymKr {
     static bool tma_ok(const T*, int64_t, int64_t, int64_t) { return false; }
@@ -368,6 +386,7 @@ struct Engine {
         T* dT[kMaxLayers] = {};
         DevMem J;  // per-example gradients (rounded to TF32), only for the blocks m < k
         int64_t ldj = 0;
+        DevMem jt16, jt16inv;  // F16S: J^T in fp16 and its inverse row scales
         {
             ProfScope prep("opg_prep", s, 0.0, 0.0);
             TransposeBatch<T> tb(s);  // all layers' copies in one launch
@@ -421,6 +440,31 @@ struct Engine {
             for (const Rows& rr : rows) {
                 const int64_t r0 = rr.r0, r1 = rr.r1;
                 if (r0 >= r1) continue;
+                // F16S: the whole-block rectangle on the fp16 datapath (J^T in fp16, built once)
+                if (prec == kF16S && !band && r1 - r0 >= 512 && md.woff[k] > 64) {
+                    if (!jt16.p) {
+                        JtF16Args ja{};
+                        ja.S = md.S;
+                        for (int q = 0; q < md.S; ++q) {
+                            ja.akT[q] = reinterpret_cast<const float*>(akT[q]);
+                            ja.dT[q] = reinterpret_cast<const float*>(dT[q]);
+                            ja.woff[q] = md.woff[q];
+                            ja.boff[q] = md.boff[q];
+                        }
+                        for (int q = 0; q <= md.S; ++q) ja.w[q] = md.w[q];
+                        ja.P = md.P;
+                        ja.n = n;
+                        ja.ldn = ldn;
+                        ProfScope pj("opg_jt16", s, 0.0, 2.0 * (double)md.P * ldn);
+                        if (!OpgF16<T>::build(s, ja, jt16, jt16inv)) jt16 = DevMem();
+                    }
+                    if (jt16.p) {
+                        ProfScope ps("opg_gemm", s, 2.0 * (double)(r1 - r0) * md.woff[k] * n,
+                                     (double)sizeof(T) * 2.0 * (double)(r1 - r0) * md.woff[k]);
+                        OpgF16<T>::rect(s, r0, r1, md.woff[k], n, jt16, ldn, jt16inv, G, ldg, T(1) / T(n));
+                        continue;
+                    }
+                }
                 if (r0 % 4 == 0 || !tc) {
                     if (!J.p) {  // (jacobian() times itself as "jacobian")
                         ldj = round_up(md.P, 32);

@@ -20,6 +20,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -186,6 +187,12 @@ struct TcShape {
     int ksplit = 1;                     // pair kernel: K slabs per tile (Epi::block_split)
     int a_once = 0, b_once = 0;         // streamed operand: L2 evict_first
     int group_m = 16;                   // rasterisation group (m-tiles per column sweep)
+    // pair kernel, precision kF16S: K-major fp16 operands (64 per 128-byte row,
+    // kind::f16), scaled by exact powers of two; the epilogue multiplies entry
+    // (r, c) by rsc[r] * csc[c] (the inverse scales) before storing
+    int f16 = 0;
+    const float* rsc = nullptr;
+    const float* csc = nullptr;
 };
 
 // Epilogues whose interior blocks are stored by TMA boxes (Epi::tma_block)
@@ -628,7 +635,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int64_t mt = ceil_div(sh.M, 256), nt = ceil_div(sh.N, BN);
     const int64_t ntiles = mt * nt;
-    const int64_t nk = ceil_div(sh.K, BK);
+    const int KBE = sh.f16 ? 2 * BK : BK;  // K elements per 128-byte operand row
+    const int64_t nk = ceil_div(sh.K, KBE);
     // work unit t = (K slab t / ntiles, tile t % ntiles): concurrent units
     // share a K slab, so the B rows they stream stay in L2
     const int64_t ksl = sh.ksplit > 1 ? sh.ksplit : 1;
@@ -691,7 +699,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                     else mbar_arrive_cluster(fb);
                     uint8_t* sa = stage_base + stage * STAGE_BYTES;
                     uint8_t* sb = sa + S::A_BYTES * split;
-                    const int64_t k0 = kb * BK;
+                    const int64_t k0 = kb * KBE;
                     load_tile2<128>(sa, &mapA, fb, sh.a_mn, sh.a_3d, am0, k0, pa);
                     load_tile2<BN / 2>(sb, &mapB, fb, sh.b_mn, sh.b_3d, bn0, k0, pb);
                     if (split == 2) {
@@ -715,7 +723,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 if (epi.skip(0, m0, n0, 256, BN)) continue;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t idesc = idesc2_tf32(tile_ntile(n0), sh.a_mn, sh.b_mn);
+                const uint32_t idesc = sh.f16 ? idesc2_f16(tile_ntile(n0), false, false)
+                                              : idesc2_tf32(tile_ntile(n0), sh.a_mn, sh.b_mn);
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
                 for (int64_t kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&full[stage], phase);
@@ -731,6 +740,11 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         const uint32_t alay = sh.a_mn ? sh.mn_layout : 2, blay = sh.b_mn ? sh.mn_layout : 2;
                         const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
                         const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
+                        if (sh.f16) {  // K-major fp16: K = 16 per MMA, the same 32 bytes per step
+                            if (elect_one()) mma2_f16(d, ahi, bhi, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                            __syncwarp();
+                            continue;
+                        }
                         mma2_tf32_e(d, ahi, bhi, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                         if (split == 2) {
                             mma2_tf32_e(d, ahi, smem_desc(sb + S::B_BYTES + boff, blbo, bsbo, blay), idesc, 1u);
@@ -767,6 +781,11 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 if (col0 >= sh.N) break;
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
+                if (sh.rsc) {  // undo the operands' power-of-two scales (exact)
+                    const float rs = row0 + lane < sh.M ? sh.rsc[row0 + lane] : 0.f;
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v[c] *= rs * (col0 + c < sh.N ? __ldg(&sh.csc[col0 + c]) : 0.f);
+                }
                 if (row0 < sh.M) {
                     if constexpr (EpiTma<Epi>::value) {
                         // the slot is free once the previous box's TMA store has read it
@@ -1318,6 +1337,20 @@ inline CUtensorMap make_map(const float* p, int64_t rows, int64_t K, int64_t ld,
     return m;
 }
 
+// 2-D fp16 K-major map (rows x K, pitch ld halves), box (64, box_rows), 128-byte swizzle
+inline CUtensorMap make_map_f16(const __half* p, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows}, es[2] = {1, 1};
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || (strides[0] & 15))
+        throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(p), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (f16) failed: " + std::to_string((int)r));
+    return m;
+}
+
 // 3D fp32 map without swizzle over p[(c * d1 + b) * ld0 + a] -- dims
 // (d0, d1, d2), dim-2 stride s2 elements -- box (b0, b1, b2)
 inline CUtensorMap make_map_plain3(const float* p, int64_t d0, int64_t d1, int64_t d2, int64_t s2, int b0, int b1,
@@ -1511,6 +1544,25 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     if (bn == 256) tc::launch<256>(s, sh, ma, mb, mal, mbl, e);
     else if (bn == 128) tc::launch<128>(s, sh, ma, mb, mal, mbl, e);
     else tc::launch<64>(s, sh, ma, mb, mal, mbl, e);
+}
+
+// kF16S GEMM on the CTA-pair kernel: K-major fp16 operands A (M x K, lda) and
+// B (N x K, ldb) pre-scaled by exact powers of two, entry (r, c) multiplied by
+// rsc[r] * csc[c] before the epilogue.  M >= 512 and N > 64 (pair tiles).
+template <class Epi>
+void gemm_f16(cudaStream_t s, int64_t M, int64_t N, int64_t K, const __half* A, int64_t lda, const __half* B,
+              int64_t ldb, const float* rsc, const float* csc, const Epi& e) {
+    if (M <= 0 || N <= 0) return;
+    if (M < 512 || N <= 64) throw CurvError(kRuntimeError, "gemm_f16: needs M >= 512 and N > 64");
+    tc::TcShape sh{M, N, K, 0, 0, 1, (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, 0, 0};
+    sh.f16 = 1;
+    sh.rsc = rsc;
+    sh.csc = csc;
+    const int bn = N >= 192 ? 256 : 128;
+    CUtensorMap ma = tc::make_map_f16(A, M, K, lda, tc::BM);
+    CUtensorMap mb = tc::make_map_f16(B, N, K, ldb, bn / 2);
+    if (bn == 256) tc::launch_pair<256>(s, sh, ma, mb, ma, mb, e);
+    else tc::launch_pair<128>(s, sh, ma, mb, ma, mb, e);
 }
 
 namespace tc {

@@ -677,21 +677,70 @@ __global__ void pack_h_kernel(const float* __restrict__ src, const int4* __restr
     }
 }
 
-// 2-D fp16 K-major map (rows x K, pitch ld halves), box (64, box_rows), 128-byte swizzle
-inline CUtensorMap make_map_h(const __half* p, int64_t rows, int64_t K, int64_t ld, int box_rows) {
-    CUtensorMap m;
-    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows}, es[2] = {1, 1};
-    if ((reinterpret_cast<uintptr_t>(p) & 15) || (strides[0] & 15))
-        throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(p), dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (f16) failed: " + std::to_string((int)r));
-    return m;
+// jt[p][n] = fp16(delta_k[n][o] abar_k[n][x] * t_{k,o} u_{k,x}), inv[p] = 1 / (t u)
+// for parameter row p = weight (k, o, x < T_k) or bias (k, o; x = T_k, the ones
+// row); t and u are the per-row power-of-two scales of delta_k^T and abar_k^T
+// (zscale_kernel), so |jt| < 2^14.  8 examples (one 16-byte store) per thread.
+__global__ void jt_f16_kernel(JtF16Args a, const float* __restrict__ us, const float* __restrict__ ts,
+                              int64_t us_ld, int64_t ts_ld, __half* __restrict__ jt, float* __restrict__ inv) {
+    const int64_t q8 = a.ldn / 8;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t p = blockIdx.y; p < a.P; p += gridDim.y) {
+        int k = 0;
+        while (k + 1 < a.S && p >= a.woff[k + 1]) ++k;
+        const int64_t tk = a.w[k], nwk = a.w[k + 1] * tk;
+        const int64_t rel = p - a.woff[k];
+        const int64_t o = rel < nwk ? rel / tk : rel - nwk, x = rel < nwk ? rel - o * tk : tk;
+        const float sc = ts[k * ts_ld + o] * us[k * us_ld + x];
+        if (e == 0) inv[p] = 1.f / sc;
+        if (e >= q8) continue;
+        const float4* d = reinterpret_cast<const float4*>(a.dT[k] + o * a.ldn) + 2 * e;
+        const float4* b = reinterpret_cast<const float4*>(a.akT[k] + x * a.ldn) + 2 * e;
+        const float4 d0 = d[0], d1 = d[1], b0 = b[0], b1 = b[1];
+        uint4 wv;
+        wv.x = sym::h2_bits((d0.x * b0.x) * sc, (d0.y * b0.y) * sc);
+        wv.y = sym::h2_bits((d0.z * b0.z) * sc, (d0.w * b0.w) * sc);
+        wv.z = sym::h2_bits((d1.x * b1.x) * sc, (d1.y * b1.y) * sc);
+        wv.w = sym::h2_bits((d1.z * b1.z) * sc, (d1.w * b1.w) * sc);
+        reinterpret_cast<uint4*>(jt + p * a.ldn)[e] = wv;
+    }
 }
 
 }  // namespace tc
+
+template <>
+struct OpgF16<float> {
+    static bool build(cudaStream_t s, const JtF16Args& a, DevMem& jt, DevMem& inv) {
+        if (a.ldn % 8 != 0) return false;
+        int64_t ul = 0, tl = 0;
+        for (int k = 0; k < a.S; ++k) {
+            ul = std::max(ul, a.w[k] + 1);
+            tl = std::max(tl, a.w[k + 1]);
+        }
+        DevMem us((size_t)a.S * ul * 4, s), ts((size_t)a.S * tl * 4, s);
+        for (int k = 0; k < a.S; ++k) {
+            tc::zscale_kernel<<<(unsigned)std::min<int64_t>(a.w[k] + 1, 4096), 256, 0, s>>>(
+                a.akT[k], a.w[k] + 1, a.n, a.ldn, dptr<float>(us) + k * ul, a.w[k] + 1);
+            CK_LAUNCH();
+            tc::zscale_kernel<<<(unsigned)std::min<int64_t>(a.w[k + 1], 4096), 256, 0, s>>>(
+                a.dT[k], a.w[k + 1], a.n, a.ldn, dptr<float>(ts) + k * tl, a.w[k + 1]);
+            CK_LAUNCH();
+        }
+        jt = DevMem((size_t)a.P * a.ldn * 2, s);
+        inv = DevMem((size_t)a.P * 4, s);
+        dim3 g((unsigned)ceil_div(a.ldn / 8, 128), (unsigned)std::min<int64_t>(a.P, 65535));
+        tc::jt_f16_kernel<<<g, 128, 0, s>>>(a, dptr<float>(us), dptr<float>(ts), ul, tl, dptr<__half>(jt),
+                                           dptr<float>(inv));
+        CK_LAUNCH();
+        return true;
+    }
+    static void rect(cudaStream_t s, int64_t r0, int64_t r1, int64_t cols, int64_t n, const DevMem& jt, int64_t ldn,
+                     const DevMem& inv, float* G, int64_t ldg, float alpha) {
+        EpiSymLower<float> e{G, ldg, alpha, r0};
+        gemm_f16(s, r1 - r0, cols, n, dptr<__half>(jt) + r0 * ldn, ldn, dptr<__half>(jt), ldn,
+                 dptr<float>(inv) + r0, dptr<float>(inv), e);
+    }
+};
 
 template <>
 struct SymKr<float> {
@@ -787,7 +836,7 @@ struct SymKr<float> {
         CK_LAUNCH();
         CUtensorMap m8 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 8);
         CUtensorMap m16 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 16);
-        CUtensorMap mpi = f16 ? tc::make_map_h(dptr<__half>(pi), np, a.n, a.ldn, (int)(bn / 2))
+        CUtensorMap mpi = f16 ? tc::make_map_f16(dptr<__half>(pi), np, a.n, a.ldn, (int)(bn / 2))
                               : tc::make_map(dptr<float>(pi), np, a.n, a.ldn, 0, (int)(bn / 2));
         tc::sym::HMaps hm;
         std::memset(&hm, 0, sizeof hm);

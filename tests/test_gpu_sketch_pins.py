@@ -115,7 +115,7 @@ def test_config4_jacobian_rows_match_reference(prec):
     np.testing.assert_allclose(norms, pins["norms"], rtol=1e-5)
 
 
-@pytest.mark.parametrize("name,product", [("c1", "hessian"), ("c1", "opg"), ("c2", "hessian")])
+@pytest.mark.parametrize("name,product", [("c1", "hessian"), ("c1", "opg"), ("c2", "hessian"), ("c3", "opg")])
 def test_f16s_equals_tf32_arithmetic(name, product):
     """f16s rounds every operand to the same 11-bit significand as tf32 (exact
     power-of-two scales), so the two modes differ only by ties (nearest-even vs
