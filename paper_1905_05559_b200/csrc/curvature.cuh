@@ -95,6 +95,27 @@ struct OpgF16 {
                      int64_t, T) {}
 };
 
+// kF16S Hessian blocks m < k through R in HBM (symkr.cuh): R rows in fp16 with
+// an exact power-of-two scale from a per-row bound, a_m^T in fp16 with per-index
+// scales, the fp16 pair GEMM
+struct HessF16Args {
+    const float* prof;  // P_m transposed [T_{k+1}][T_{m+1}][ldn]
+    const float* q;     // Q_m transposed [T_k][T_{m+1}][ldn]
+    const float* akT;   // a_k^T [T_k + 1][ldn]
+    const float* dkT;   // delta_k^T [T_{k+1}][ldn]
+    const float* am;    // a_m [n][lda_m] (column T_m = ones)
+    int64_t lda_m, ldn, n, tk, np, tm, tm1;
+};
+template <class T>
+struct HessF16 {
+    struct Prep {
+        DevMem amax, dmax, pmax, qmax, am16, aminv;
+    };
+    static bool prepare(cudaStream_t, const HessF16Args&, Prep&) { return false; }
+    static void chunk(cudaStream_t, const HessF16Args&, const Prep&, int64_t, int64_t, int64_t, DevMem&, DevMem&,
+                      const EpiHess<T>&, double) {}
+};
+
 template <class T>
 struct SymKr {
     static bool tma_ok(const T*, int64_t, int64_t, int64_t) { return false; }
@@ -746,6 +767,17 @@ struct Engine {
                     if (HessFused<T>::run(prec, s, fa, e)) jbeg = Pk;
                 }
                 const int64_t tm = md.w[m], tm1 = md.w[m + 1];
+                // F16S: the same chunks with R in fp16 and the fp16 GEMM
+                typename HessF16<T>::Prep hp;
+                HessF16Args ha{};
+                bool f16r = false;
+                if (rgen_tc && prec == kF16S && tm + 1 > 64 && jbeg < Pk) {
+                    ha = HessF16Args{reinterpret_cast<const float*>(PT[m]), reinterpret_cast<const float*>(QT[m]),
+                                     reinterpret_cast<const float*>(akT), reinterpret_cast<const float*>(dkT),
+                                     reinterpret_cast<const float*>(c.a[m]), c.lda[m], ldn, n, tk, np, tm, tm1};
+                    ProfScope pp("hess_prep16", s, 0.0, 0.0);
+                    f16r = HessF16<T>::prepare(s, ha, hp);
+                }
                 int64_t J = (int64_t)((rgen_tc ? size_t(2) << 30 : chunk_bytes) / ((size_t)tm1 * ldr * sizeof(T)));
                 J = std::max<int64_t>(128, J / 128 * 128);
                 J = std::min<int64_t>(J, round_up(Pk - jbeg, 128));
@@ -758,6 +790,14 @@ struct Engine {
                     int64_t opp_hi = tm1;
                     if (m == k && !verify && j0 + Jc - 1 < tm * tm1) opp_hi = std::min(tm1, (j0 + Jc - 1) / tm + 1);
                     const int64_t rows = opp_hi * Jc;
+                    if (f16r && rows >= 512) {
+                        EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
+                                     m == k ? 1 : 0, (m == k && verify) ? 0 : 1, rlo, rhi};
+                        const double req = Profiler::get().on ? hess_required_entries(k, m, j0, Jc) : 0.0;
+                        DevMem r16, rinv;
+                        HessF16<T>::chunk(s, ha, hp, j0, Jc, opp_hi, r16, rinv, e, req);
+                        continue;
+                    }
                     RGenArgs<T> g{m == k ? GT : PT[m], m == k ? nullptr : QT[m], akT, dkT, ldn, n, tk, np, tm1,
                                   j0, Jc, rows, dptr<T>(rbuf), ldr, rgen_tc ? 1 : 0};
                     {

@@ -608,7 +608,7 @@ struct PairSmem {
     }
 };
 
-template <int BN, class Epi>
+template <int BN, class Epi, bool F16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ CUtensorMap mapAlo, const __grid_constant__ CUtensorMap mapBlo,
@@ -635,7 +635,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
     const int64_t pair_id = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int64_t mt = ceil_div(sh.M, 256), nt = ceil_div(sh.N, BN);
     const int64_t ntiles = mt * nt;
-    const int KBE = sh.f16 ? 2 * BK : BK;  // K elements per 128-byte operand row
+    const int KBE = F16 ? 2 * BK : BK;  // K elements per 128-byte operand row
     const int64_t nk = ceil_div(sh.K, KBE);
     // work unit t = (K slab t / ntiles, tile t % ntiles): concurrent units
     // share a K slab, so the B rows they stream stay in L2
@@ -723,8 +723,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 if (epi.skip(0, m0, n0, 256, BN)) continue;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t idesc = sh.f16 ? idesc2_f16(tile_ntile(n0), false, false)
-                                              : idesc2_tf32(tile_ntile(n0), sh.a_mn, sh.b_mn);
+                const uint32_t idesc = F16 ? idesc2_f16(tile_ntile(n0), false, false)
+                                           : idesc2_tf32(tile_ntile(n0), sh.a_mn, sh.b_mn);
                 const uint32_t d = tmem_base + (uint32_t)(acc * BN);
                 for (int64_t kb = kb0; kb < kb1; ++kb) {
                     mbar_wait_cluster(&full[stage], phase);
@@ -740,7 +740,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                         const uint32_t alay = sh.a_mn ? sh.mn_layout : 2, blay = sh.b_mn ? sh.mn_layout : 2;
                         const uint64_t ahi = smem_desc(sa + aoff, albo, asbo, alay);
                         const uint64_t bhi = smem_desc(sb + boff, blbo, bsbo, blay);
-                        if (sh.f16) {  // K-major fp16: K = 16 per MMA, the same 32 bytes per step
+                        if constexpr (F16) {  // K-major fp16: K = 16 per MMA, the same 32 bytes per step
                             if (elect_one()) mma2_f16(d, ahi, bhi, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
                             __syncwarp();
                             continue;
@@ -781,7 +781,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 if (col0 >= sh.N) break;
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cb * 32), v);
-                if (sh.rsc) {  // undo the operands' power-of-two scales (exact)
+                if constexpr (F16) {  // undo the operands' power-of-two scales (exact)
                     const float rs = row0 + lane < sh.M ? sh.rsc[row0 + lane] : 0.f;
 #pragma unroll
                     for (int c = 0; c < 32; ++c) v[c] *= rs * (col0 + c < sh.N ? __ldg(&sh.csc[col0 + c]) : 0.f);
@@ -1436,13 +1436,13 @@ void launch(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const CUten
     CK_LAUNCH();
 }
 
-template <int BN, class Epi>
+template <int BN, class Epi, bool F16 = false>
 void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const CUtensorMap& b,
                  const CUtensorMap& alo, const CUtensorMap& blo, const Epi& e) {
     using S = pair::PairSmem<BN>;
     const int smem = S::bytes(sh.nsplit);
-    func_attr_once((const void*)pair::tc_gemm_pair_kernel<BN, Epi>, [] {
-        CK_CUDA(cudaFuncSetAttribute(pair::tc_gemm_pair_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    func_attr_once((const void*)pair::tc_gemm_pair_kernel<BN, Epi, F16>, [] {
+        CK_CUDA(cudaFuncSetAttribute(pair::tc_gemm_pair_kernel<BN, Epi, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      std::max(S::bytes(1), S::bytes(3))));
     });
     const int64_t tiles = ceil_div(sh.M, 256) * ceil_div(sh.N, BN) * std::max(1, sh.ksplit);
@@ -1453,7 +1453,7 @@ void launch_pair(cudaStream_t s, const TcShape& sh, const CUtensorMap& a, const 
         if (e.ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(e.c) & 15) == 0) mc = make_map_h(e.c, e.ldc);
         else ee.tma = 0;  // pitch not TMA-addressable: scalar epilogue for every block
     }
-    pair::tc_gemm_pair_kernel<BN, Epi><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, mc, sh, ee);
+    pair::tc_gemm_pair_kernel<BN, Epi, F16><<<grid, pair::kThreads2, smem, s>>>(a, b, alo, blo, mc, sh, ee);
     CK_LAUNCH();
 }
 
@@ -1561,8 +1561,8 @@ void gemm_f16(cudaStream_t s, int64_t M, int64_t N, int64_t K, const __half* A, 
     const int bn = N >= 192 ? 256 : 128;
     CUtensorMap ma = tc::make_map_f16(A, M, K, lda, tc::BM);
     CUtensorMap mb = tc::make_map_f16(B, N, K, ldb, bn / 2);
-    if (bn == 256) tc::launch_pair<256>(s, sh, ma, mb, ma, mb, e);
-    else tc::launch_pair<128>(s, sh, ma, mb, ma, mb, e);
+    if (bn == 256) tc::launch_pair<256, Epi, true>(s, sh, ma, mb, ma, mb, e);
+    else tc::launch_pair<128, Epi, true>(s, sh, ma, mb, ma, mb, e);
 }
 
 namespace tc {

@@ -706,7 +706,140 @@ __global__ void jt_f16_kernel(JtF16Args a, const float* __restrict__ us, const f
     }
 }
 
+// out[r] = max |src[r][0 .. n)|, one CTA per row
+__global__ void row_absmax_kernel(const float* __restrict__ src, int64_t rows, int64_t n, int64_t ld,
+                                  float* __restrict__ out) {
+    __shared__ float red[32];
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        float m = 0.f;
+        for (int64_t q = threadIdx.x; q < n; q += blockDim.x) m = fmaxf(m, fabsf(src[r * ld + q]));
+        m = block_absmax(m, red);
+        if (threadIdx.x == 0) out[r] = m;
+    }
+}
+
+// a_m^T in fp16: out[c][e] = fp16(a[e][c] u_c), u_c = the power-of-two scale of
+// column c (|a u| < 2^7), inv[c] = 1 / u_c; one CTA per column (c < cols)
+__global__ void am_f16_kernel(const float* __restrict__ a, int64_t lda, int64_t cols, int64_t n, int64_t ldn,
+                              __half* __restrict__ out, float* __restrict__ inv) {
+    __shared__ float red[32];
+    for (int64_t c = blockIdx.x; c < cols; c += gridDim.x) {
+        float m = 0.f;
+        for (int64_t e = threadIdx.x; e < n; e += blockDim.x) m = fmaxf(m, fabsf(a[e * lda + c]));
+        m = block_absmax(m, red);
+        const float u = pow2_scale(m, 7);
+        if (threadIdx.x == 0) inv[c] = 1.f / u;
+        for (int64_t e = threadIdx.x; e < ldn; e += blockDim.x)
+            out[c * ldn + e] = __float2half_rn(e < n ? a[e * lda + c] * u : 0.f);
+    }
+}
+
+// R rows of one chunk in fp16 (see rgen_kernel for the row layout and the
+// register reuse): row r = (o'', tangent j) scaled by s_r = 2^(14 - e) with
+// |R| <= max|a_i| max|P[o][o'']| + max|delta_o| max|Q[i][o'']| < 2^e (bias rows:
+// max|P|); rinv[r] = 1 / s_r.  8 examples (one 16-byte store) per thread.
+__global__ void rgen_f16_kernel(HessF16Args g, const float* __restrict__ amax, const float* __restrict__ dmax,
+                                const float* __restrict__ pmax, const float* __restrict__ qmax, int64_t j0, int64_t J,
+                                int64_t nopp, __half* __restrict__ R, float* __restrict__ rinv) {
+    constexpr int SEG = 32;
+    const int64_t q8 = g.ldn / 8;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nw = g.np * g.tk;
+    const int64_t segs = ceil_div(J, SEG);
+    for (int64_t sg = blockIdx.y; sg < nopp * segs; sg += gridDim.y) {
+        const int64_t opp = sg / segs, jj0 = (sg - opp * segs) * SEG;
+        const int64_t jj1 = jj0 + SEG < J ? jj0 + SEG : J;
+        int64_t last_o = -1;
+        float4 p0{}, p1{}, d0{}, d1{};  // the profile and delta vectors of the current unit o
+        for (int64_t jj = jj0; jj < jj1; ++jj) {
+            const int64_t j = j0 + jj;
+            const bool wt = j < nw;
+            const int64_t o = wt ? j / g.tk : j - nw;
+            const int64_t i = wt ? j - o * g.tk : 0;
+            const float bound = wt ? amax[i] * pmax[o * g.tm1 + opp] + dmax[o] * qmax[i * g.tm1 + opp]
+                                   : pmax[o * g.tm1 + opp];
+            const float sc = pow2_scale(bound, 14);
+            const int64_t r = opp * J + jj;
+            if (e == 0) rinv[r] = 1.f / sc;
+            if (e >= q8) continue;
+            if (o != last_o || !wt) {
+                const float4* pp = reinterpret_cast<const float4*>(g.prof + (o * g.tm1 + opp) * g.ldn) + 2 * e;
+                p0 = pp[0];
+                p1 = pp[1];
+                if (wt) {
+                    const float4* dp = reinterpret_cast<const float4*>(g.dkT + o * g.ldn) + 2 * e;
+                    d0 = dp[0];
+                    d1 = dp[1];
+                }
+                last_o = wt ? o : -1;
+            }
+            float4 v0 = p0, v1 = p1;
+            if (wt) {
+                const float4* ap = reinterpret_cast<const float4*>(g.akT + i * g.ldn) + 2 * e;
+                const float4* qp = reinterpret_cast<const float4*>(g.q + (i * g.tm1 + opp) * g.ldn) + 2 * e;
+                const float4 a0 = ap[0], a1 = ap[1], q0 = qp[0], q1 = qp[1];
+                v0.x *= a0.x; v0.y *= a0.y; v0.z *= a0.z; v0.w *= a0.w;
+                v1.x *= a1.x; v1.y *= a1.y; v1.z *= a1.z; v1.w *= a1.w;
+                v0.x += d0.x * q0.x; v0.y += d0.y * q0.y; v0.z += d0.z * q0.z; v0.w += d0.w * q0.w;
+                v1.x += d1.x * q1.x; v1.y += d1.y * q1.y; v1.z += d1.z * q1.z; v1.w += d1.w * q1.w;
+            }
+            uint4 w;
+            w.x = sym::h2_bits(v0.x * sc, v0.y * sc);
+            w.y = sym::h2_bits(v0.z * sc, v0.w * sc);
+            w.z = sym::h2_bits(v1.x * sc, v1.y * sc);
+            w.w = sym::h2_bits(v1.z * sc, v1.w * sc);
+            reinterpret_cast<uint4*>(R + r * g.ldn)[e] = w;
+        }
+    }
+}
+
 }  // namespace tc
+
+template <>
+struct HessF16<float> {
+    struct Prep {
+        DevMem amax, dmax, pmax, qmax, am16, aminv;
+    };
+    static bool prepare(cudaStream_t s, const HessF16Args& a, Prep& p) {
+        if (a.ldn % 8 != 0 || !a.q) return false;
+        p.amax = DevMem((size_t)(a.tk + 1) * 4, s);
+        p.dmax = DevMem((size_t)a.np * 4, s);
+        p.pmax = DevMem((size_t)a.np * a.tm1 * 4, s);
+        p.qmax = DevMem((size_t)a.tk * a.tm1 * 4, s);
+        auto rmax = [&](const float* src, int64_t rows, DevMem& out) {
+            tc::row_absmax_kernel<<<(unsigned)std::min<int64_t>(rows, 8192), 256, 0, s>>>(src, rows, a.n, a.ldn,
+                                                                                        dptr<float>(out));
+            CK_LAUNCH();
+        };
+        rmax(a.akT, a.tk + 1, p.amax);
+        rmax(a.dkT, a.np, p.dmax);
+        rmax(a.prof, a.np * a.tm1, p.pmax);
+        rmax(a.q, a.tk * a.tm1, p.qmax);
+        p.am16 = DevMem((size_t)(a.tm + 1) * a.ldn * 2, s);
+        p.aminv = DevMem((size_t)(a.tm + 1) * 4, s);
+        tc::am_f16_kernel<<<(unsigned)std::min<int64_t>(a.tm + 1, 8192), 256, 0, s>>>(
+            a.am, a.lda_m, a.tm + 1, a.n, a.ldn, dptr<__half>(p.am16), dptr<float>(p.aminv));
+        CK_LAUNCH();
+        return true;
+    }
+    static void chunk(cudaStream_t s, const HessF16Args& a, const Prep& p, int64_t j0, int64_t Jc, int64_t nopp,
+                      DevMem& r16, DevMem& rinv, const EpiHess<float>& e, double req) {
+        const int64_t rows = nopp * Jc;
+        r16 = DevMem((size_t)rows * a.ldn * 2, s);
+        rinv = DevMem((size_t)rows * 4, s);
+        {
+            ProfScope pr("hess_rgen", s, 0.0, 2.0 * (double)rows * a.ldn);
+            const dim3 g((unsigned)ceil_div(a.ldn / 8, 128), (unsigned)std::min<int64_t>(nopp * ceil_div(Jc, 32), 65535));
+            tc::rgen_f16_kernel<<<g, 128, 0, s>>>(a, dptr<float>(p.amax), dptr<float>(p.dmax), dptr<float>(p.pmax),
+                                                  dptr<float>(p.qmax), j0, Jc, nopp, dptr<__half>(r16),
+                                                  dptr<float>(rinv));
+            CK_LAUNCH();
+        }
+        ProfScope pg("hess_gemm", s, 2.0 * (double)a.n * req, 4.0 * req);
+        gemm_f16(s, rows, a.tm + 1, a.n, dptr<__half>(r16), a.ldn, dptr<__half>(p.am16), a.ldn, dptr<float>(rinv),
+                 dptr<float>(p.aminv), e);
+    }
+};
 
 template <>
 struct OpgF16<float> {
