@@ -580,9 +580,11 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // TMA store of one smem box; bulk-group bookkeeping
+// output boxes stream through L2 with evict_first (the operands keep their lines:
+// config 3's symmetric kernel re-read half as much of its B operand from HBM)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
-                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(evict_first_policy())
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }

@@ -109,10 +109,12 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 
+// the output streams through L2 with evict_first: the packed profile (the B
+// operand, re-read by every tile square) keeps its lines
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1, int32_t c2,
-                                             int32_t c3) {
-    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
-                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                                             int32_t c3, uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;"
+                 ::"l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
                  : "memory");
 }
 
@@ -435,6 +437,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
         int il, cl;
         row_ic(rho, il, cl);
         uint8_t* gbase = epi_base + grp * 4 * SLOT;  // [buf][layout][CH][128] floats
+        const uint64_t spol = evict_first_policy();
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         const int half = bn / 2;
         int acc = 0;
@@ -509,8 +512,8 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                             const int32_t d2 = bx.y - (row_o ? 0 : (int32_t)p.u0);
                             const int32_t d3 = bx.x - (row_o ? (int32_t)p.u0 : 0);
                             if (d3 >= 0) {
-                                if (ic) tma_store_4d(mp, src, (int32_t)c0, (int32_t)i0, d2, d3);
-                                else tma_store_4d(mp, src, (int32_t)i0, (int32_t)c0, d2, d3);
+                                if (ic) tma_store_4d(mp, src, (int32_t)c0, (int32_t)i0, d2, d3, spol);
+                                else tma_store_4d(mp, src, (int32_t)i0, (int32_t)c0, d2, d3, spol);
                             }
                         }
                     }
