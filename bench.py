@@ -464,6 +464,43 @@ def load_traffic(name):
     return json.load(open(tfile)).get(name) if os.path.exists(tfile) else None
 
 
+def band_balance(torch, dev, stream):
+    """Load balance of the multi-GPU split, measured on this one GPU: every
+    rank's unit band of config 3's G (curvkit_dev_assemble_band, the exact work
+    rank r of W runs, with its replicated forward/backward and J) timed in
+    turn.  projected_speedup = the 1-GPU step / the slowest band: what W GPUs
+    reach before the final gather, without the NVLink exchange (which the
+    assembly itself does not need)."""
+    from paper_1905_05559_b200 import curv
+    job = Job("c3", "tf32", dev, torch)
+    wl = job.wl
+    ms1, _, _, _ = timed(job, 3, 2, stream, torch)
+    job.free()
+    torch.cuda.empty_cache()
+    out = {"one_gpu_ms": ms1}
+    for W in (2, 4, 8):
+        times = []
+        for r in range(W):
+            rows = curv.shard_units_rows(job.spec, W, r)
+            band = torch.empty((max(1, rows), job.ld), dtype=torch.float32, device=dev)
+            f = lambda: curv.dev_assemble_band(job.spec, "opg", job.p_d, job.x_d, job.l_d, wl.n, W, r, band,  # noqa: E731
+                                               job.ld, precision="tf32", stream=stream)
+            f()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                f()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 3)
+            del band
+            torch.cuda.empty_cache()
+        out[f"W{W}"] = {"band_ms": [round(t, 2) for t in times], "max_band_ms": max(times),
+                        "projected_speedup": ms1 / max(times), "projected_efficiency": ms1 / max(times) / W}
+    return out
+
+
 def run_extra(torch, dev, stream, pk, pk_kind):
     """The other BASELINE configurations on the same GPU (N = 1), and the
     headline configuration in the f16s precision mode."""
@@ -482,6 +519,7 @@ def run_extra(torch, dev, stream, pk, pk_kind):
         job.free()
         del job
         torch.cuda.empty_cache()
+    out["c3_band_balance"] = band_balance(torch, dev, stream)
     # c4: top-100 OPG eigenpairs, BASELINE's setting and the converged default
     from paper_1905_05559_b200 import curv
     from paper_1905_05559_b200.workloads import CONFIGS

@@ -32,7 +32,7 @@ struct UnitBand {
     int64_t bw[kMaxLayers] = {}, bb[kMaxLayers] = {};  // band row of weight row (u0, 0) / of bias u0
     int64_t rows = 0;
 
-    // Units cut per layer so every shard gets 1/W of the layer's work: the
+    // Units cut per layer (at multiples of 4) so every shard gets ~1/W of the layer's work: the
     // diagonal block grows with the packed unit pairs below a unit,
     // u (u + 1) / 2 orbit columns of (T_k + 1)(T_k + 2) / 2 values, the blocks
     // left of it linearly, u (T_k + 1) rows of woff_k columns.  (Bias rows whose
@@ -57,7 +57,11 @@ struct UnitBand {
                     else lo = mid + 1;
                 }
                 if (lo > 0 && target - cost(lo - 1) < cost(lo) - target) --lo;  // the nearer neighbour
-                return lo;
+                // cuts on multiples of 4 units: every band row range then starts 16-byte
+                // aligned, so the bias rows take the J GEMM too (an unaligned start sent
+                // them to the fused block kernel: 1.5-1.8 ms of a 15 ms band at c3, W = 8)
+                const int64_t q = (lo + 2) / 4 * 4;
+                return q < U ? q : U;
             };
             b.u0[k] = bound(r);
             b.u1[k] = std::max(b.u0[k], bound(r + 1));
