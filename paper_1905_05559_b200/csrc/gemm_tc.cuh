@@ -1531,7 +1531,8 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
     // CTA-pair (cta_group::2) tiles of 256 x bn when M gives every pair work;
     // each CTA then stages only bn/2 rows of B.
     static const bool no_pair = getenv("CURVKIT_NO_PAIR") != nullptr;
-    const bool use_pair = (!no_pair && bn >= 128 && M >= 512) || ksplit > 1;
+    // (M = 256 exactly fills one pair tile: a 4-unit band of a 64-input layer, config 3 W = 8)
+    const bool use_pair = (!no_pair && bn >= 128 && (M >= 512 || M == 256)) || ksplit > 1;
     if (ksplit > 1 && (bn < 128 || M < 512)) throw CurvError(kRuntimeError, "split-K needs the CTA-pair kernel");
     const int box_b = use_pair ? bn / 2 : bn;
     CUtensorMap ma = tc::make_map(pa, M, K, A.ld, sh.a_mn, tc::BM, a3);
