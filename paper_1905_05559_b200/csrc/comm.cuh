@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -112,15 +113,36 @@ struct Comm {
             if (nranks == 1) return;
         }
         if (host()) {
-            std::vector<uint8_t> hs((size_t)bytes[rank]);
-            std::vector<uint8_t> hr(rank == root ? (size_t)off[nranks] : 0);
-            if (bytes[rank] > 0) CK_CUDA(cudaMemcpyAsync(hs.data(), send, hs.size(), cudaMemcpyDeviceToHost, s));
-            CK_CUDA(cudaStreamSynchronize(s));
-            if (h_gather(hs.data(), bytes[rank], rank == root ? hr.data() : nullptr, bytes.data(), root, user) != 0)
-                throw CurvError(kRuntimeError, "host gather callback failed");
-            if (rank == root && !hr.empty())
-                CK_CUDA(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, s));
-            CK_CUDA(cudaStreamSynchronize(s));
+            // in pieces of at most 256 MB per rank (bands of config 3 are tens of GB):
+            // every rank makes the same number of callback calls, piece c of rank r
+            // being bytes [c * PIECE, min(bytes[r], (c + 1) * PIECE)) of its block
+            constexpr int64_t PIECE = int64_t(256) << 20;
+            int64_t mx = 0;
+            for (int r = 0; r < nranks; ++r) mx = std::max(mx, bytes[r]);
+            const int64_t npieces = std::max<int64_t>(1, ceil_div(mx, PIECE));
+            std::vector<uint8_t> hs((size_t)std::min(bytes[rank], PIECE));
+            std::vector<uint8_t> hr;
+            std::vector<int64_t> sz(nranks), po(nranks + 1);
+            for (int64_t c = 0; c < npieces; ++c) {
+                po[0] = 0;
+                for (int r = 0; r < nranks; ++r) {
+                    sz[r] = std::clamp<int64_t>(bytes[r] - c * PIECE, 0, PIECE);
+                    po[r + 1] = po[r] + sz[r];
+                }
+                if (sz[rank] > 0)
+                    CK_CUDA(cudaMemcpyAsync(hs.data(), static_cast<const uint8_t*>(send) + c * PIECE, (size_t)sz[rank],
+                                            cudaMemcpyDeviceToHost, s));
+                CK_CUDA(cudaStreamSynchronize(s));
+                if (rank == root) hr.resize((size_t)po[nranks]);
+                if (h_gather(hs.data(), sz[rank], rank == root ? hr.data() : nullptr, sz.data(), root, user) != 0)
+                    throw CurvError(kRuntimeError, "host gather callback failed");
+                if (rank == root)
+                    for (int r = 0; r < nranks; ++r)
+                        if (sz[r] > 0)
+                            CK_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + off[r] + c * PIECE, hr.data() + po[r],
+                                                    (size_t)sz[r], cudaMemcpyHostToDevice, s));
+                CK_CUDA(cudaStreamSynchronize(s));
+            }
             return;
         }
         NcclApi& api = NcclApi::get();

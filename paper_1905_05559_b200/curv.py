@@ -751,8 +751,9 @@ class Comm:
                 sizes = [int(recv_bytes[r]) for r in range(world)]
                 mx = max(max(sizes), 1)
                 t = torch.zeros(mx, dtype=torch.uint8)
-                if send_bytes > 0:
-                    t[:send_bytes] = torch.frombuffer(C.string_at(send, send_bytes), dtype=torch.uint8)
+                if send_bytes > 0:  # a view of the library's host buffer (no bytes copy)
+                    t[:send_bytes] = torch.from_numpy(
+                        np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(int(send_bytes),)))
                 lst = [torch.empty(mx, dtype=torch.uint8) for _ in range(world)] if rank == root else None
                 dist.gather(t, lst, dst=root, group=group)
                 if rank == root:
