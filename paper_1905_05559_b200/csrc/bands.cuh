@@ -32,39 +32,64 @@ struct UnitBand {
     int64_t bw[kMaxLayers] = {}, bb[kMaxLayers] = {};  // band row of weight row (u0, 0) / of bias u0
     int64_t rows = 0;
 
-    // Units cut per layer (at multiples of 4) so every shard gets ~1/W of the layer's work: the
-    // diagonal block grows with the packed unit pairs below a unit,
-    // u (u + 1) / 2 orbit columns of (T_k + 1)(T_k + 2) / 2 values, the blocks
-    // left of it linearly, u (T_k + 1) rows of woff_k columns.  (Bias rows whose
-    // start is not 16-byte aligned take the fused block kernel instead of the
-    // J GEMM: the cut stays at unit granularity.)
+    // Unit cuts.  A unit's cost in layer k: the diagonal block grows with the
+    // packed unit pairs below it, u (u + 1) / 2 orbit columns of
+    // (T_k + 1)(T_k + 2) / 2 values, the blocks left of it linearly, u (T_k + 1)
+    // rows of woff_k columns -- 2 N flops per value or entry either way.  Every
+    // layer but the most expensive one is cut so each shard gets ~1/W of it; the
+    // most expensive layer (config 3: layer 0, 92% of the work) is then cut so
+    // each shard's TOTAL is ~1/W, absorbing the lumps of the small layers (10
+    // units over 8 shards).  Cuts fall on multiples of 4 units: every band row
+    // range then starts 16-byte aligned, so the bias rows take the J GEMM too
+    // (an unaligned start sent them to the fused block kernel: 1.5-1.8 ms of a
+    // 15 ms band at c3, W = 8) -- except in the first layer, which has no
+    // rectangle rows and keeps unit granularity (a 4-unit step of its largest
+    // units is ~3% of the whole job).
+    static double layer_cost(const ModelDesc& md, int k, int64_t u) {
+        const int64_t tk = md.w[k];
+        const double orb = (double)(tk + 1) * (double)(tk + 2) / 2.0, rect = (double)(tk + 1) * (double)md.woff[k];
+        return (double)u * (u + 1) / 2.0 * orb + (double)u * rect;
+    }
+    // smallest u on a multiple of 4 nearest to cost_k(u) = target, in [0, U]
+    static int64_t cut_for(const ModelDesc& md, int k, double target) {
+        const int64_t U = md.w[k + 1];
+        int64_t lo = 0, hi = U;  // smallest u with cost(u) >= target
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (layer_cost(md, k, mid) >= target) hi = mid;
+            else lo = mid + 1;
+        }
+        if (lo > 0 && target - layer_cost(md, k, lo - 1) < layer_cost(md, k, lo) - target) --lo;  // nearer
+        if (md.woff[k] == 0) return lo;  // no rectangle rows in the first layer: any unit aligns
+        const int64_t q = (lo + 2) / 4 * 4;
+        return q < U ? q : U;
+    }
     static UnitBand make(const ModelDesc& md, int64_t W, int64_t r) {
         if (W < 1 || r < 0 || r >= W) throw CurvError(kContractError, "shard_units: need 0 <= shard < nshards");
         UnitBand b;
         b.S = md.S;
+        // cut[k][s]: first unit of shard s in layer k (s = 0 .. W)
+        std::vector<std::vector<int64_t>> cut(md.S, std::vector<int64_t>(W + 1));
+        int a = 0;
+        double total = 0.0;
         for (int k = 0; k < md.S; ++k) {
-            const int64_t U = md.w[k + 1], tk = md.w[k];
-            const double orb = (double)(tk + 1) * (double)(tk + 2) / 2.0, rect = (double)(tk + 1) * (double)md.woff[k];
-            auto cost = [&](int64_t u) { return (double)u * (u + 1) / 2.0 * orb + (double)u * rect; };
-            auto bound = [&](int64_t s) -> int64_t {
-                if (s <= 0) return 0;
-                if (s >= W) return U;
-                const double target = cost(U) * (double)s / (double)W;
-                int64_t lo = 0, hi = U;  // smallest u with cost(u) >= target
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) / 2;
-                    if (cost(mid) >= target) hi = mid;
-                    else lo = mid + 1;
-                }
-                if (lo > 0 && target - cost(lo - 1) < cost(lo) - target) --lo;  // the nearer neighbour
-                // cuts on multiples of 4 units: every band row range then starts 16-byte
-                // aligned, so the bias rows take the J GEMM too (an unaligned start sent
-                // them to the fused block kernel: 1.5-1.8 ms of a 15 ms band at c3, W = 8)
-                const int64_t q = (lo + 2) / 4 * 4;
-                return q < U ? q : U;
-            };
-            b.u0[k] = bound(r);
-            b.u1[k] = std::max(b.u0[k], bound(r + 1));
+            const int64_t U = md.w[k + 1];
+            const double ck = layer_cost(md, k, U);
+            total += ck;
+            if (ck > layer_cost(md, a, md.w[a + 1])) a = k;
+            for (int64_t s = 0; s <= W; ++s)
+                cut[k][s] = s == 0 ? 0 : s == W ? U : cut_for(md, k, ck * (double)s / (double)W);
+        }
+        for (int64_t s = 1; s < W; ++s) {  // the absorbing layer
+            double other = 0.0;
+            for (int k = 0; k < md.S; ++k)
+                if (k != a) other += layer_cost(md, k, cut[k][s]);
+            const double t = std::max(0.0, total * (double)s / (double)W - other);
+            cut[a][s] = std::max(cut[a][s - 1], cut_for(md, a, t));
+        }
+        for (int k = 0; k < md.S; ++k) {
+            b.u0[k] = cut[k][r];
+            b.u1[k] = std::max(b.u0[k], cut[k][r + 1]);
         }
         for (int k = 0; k < md.S; ++k) {
             const int64_t nu = b.u1[k] - b.u0[k];

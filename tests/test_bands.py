@@ -48,17 +48,23 @@ def _layer_cost(widths, k, u0, u1):
 def test_shard_units_partition(widths, act, world):
     spec = curv.ModelSpec(widths, act)
     P = curv.param_count(spec)
+    L = len(widths) - 1
     parts = [curv.shard_units(spec, world, r) for r in range(world)]
-    for k in range(len(widths) - 1):
+    total = sum(_layer_cost(widths, k, 0, widths[k + 1])[0] for k in range(L))
+    # cut quantum: 1 unit in the first layer (no rectangle rows), 4 elsewhere
+    slack = 2 * sum((1 if k == 0 else 4) * _layer_cost(widths, k, 0, widths[k + 1])[1] for k in range(L))
+    for k in range(L):
         U = widths[k + 1]
         assert parts[0][0][k] == 0 and parts[-1][1][k] == U
         for a, b in zip(parts, parts[1:]):
             assert a[1][k] == b[0][k]
-        total, _ = _layer_cost(widths, k, 0, U)
         for u0, u1, _ in parts:
-            share, unit = _layer_cost(widths, k, u0[k], u1[k])
-            assert share <= total / world + 4 * unit + 1e-9   # balanced to within the 4-unit cut quantum
-            assert u0[k] % 4 == 0 or u0[k] == U  # band row ranges start 16-byte aligned (or are empty)
+            assert u0[k] <= u1[k]
+            if k > 0:
+                assert u0[k] % 4 == 0 or u0[k] == U  # band row ranges start 16-byte aligned (or are empty)
+    for u0, u1, _ in parts:  # every shard's total work within the cut quanta of 1/W
+        share = sum(_layer_cost(widths, k, u0[k], u1[k])[0] for k in range(L))
+        assert share <= total / world + slack + 1e-9
     rows = np.concatenate([curv.band_rows_index(spec, world, r) for r in range(world)])
     assert sorted(rows.tolist()) == list(range(P))
     assert sum(p[2] for p in parts) == P
