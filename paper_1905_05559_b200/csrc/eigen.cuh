@@ -700,7 +700,8 @@ void topk_core(const ModelDesc& md, const Cache<T>& c, int64_t k, int64_t oversa
     const bool ext = Jext != nullptr;
     std::unique_ptr<KrOperands> krop;
     if constexpr (std::is_same_v<T, float>)
-        if (!ext && tf32_class(prec) && kr_supported(md, c)) krop = std::make_unique<KrOperands>(md, c, s);
+        if (!ext && tf32_class(prec) && kr_supported(md, c))
+            krop = std::make_unique<KrOperands>(md, c, s, prec == kF16S);
     if (sharded && !krop) throw CurvError(kContractError, "sharded opg_topk needs TF32 precision");
     const bool ext_copy = ext && tf32_class(prec);
     const int64_t ldj = ext && !ext_copy ? ldj_ext : (krop ? 0 : round_up(P, 32));

@@ -55,6 +55,10 @@ struct KrArgs {
     int64_t ksplit;        // JT: example slabs (partial Y in slab ks of out)
     int64_t o0, oend;      // output units o0 .. oend - 1 of the layer (a shard's range)
     int64_t prow0;         // parameter row held at row 0 of X (JX) / Y (JT)
+    // F16 (precision kF16S, J X): inverse power-of-two scales of the fp16
+    // operands -- per example row of a_k and per column c of X^T
+    const float* rinv = nullptr;
+    const float* cinv = nullptr;
 };
 
 constexpr int KR_BN = 256;
@@ -71,11 +75,17 @@ struct KrCfg {
     static constexpr int BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 1024;
 };
 
-template <bool JT>
+// F16 (J X only): A = a_k in fp16 (K-major over the inputs i, rows scaled by
+// 1 / rinv), B = X^T in fp16 (K-major over the parameter rows, columns scaled
+// by 1 / cinv); 64 inputs per 128-byte operand row, kind::f16 MMAs; the
+// epilogue undoes both scales on the summed row (exact).
+template <bool JT, bool F16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KrCfg<JT>::THREADS, 1)
 kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, KrArgs ka,
           uint32_t mn_lbo, uint32_t mn_sbo, uint32_t mn_kstep, int a3d, int b3d) {
     using C = KrCfg<JT>;
+    static_assert(!(JT && F16), "the fp16 form is J X only");
+    constexpr int KBE = F16 ? 2 * BK : BK;  // K elements per 128-byte operand row
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int NST = C::STAGES;
@@ -157,7 +167,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                         uint8_t* sa = stage_base + stage * C::STAGE_BYTES;
                         uint8_t* sb = sa + C::A_BYTES;
                         const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
-                        const int64_t k0 = kb * BK;
+                        const int64_t k0 = kb * KBE;
                         if constexpr (JT) {
                             if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * C::A_BYTES));
                             load_tile2<128>(sa, &mapA, fb, 1, a3d, r0, k0, pol);
@@ -168,7 +178,10 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                             else mbar_arrive_cluster(fb);
                             load_tile2<128>(sa, &mapA, fb, 0, 0, r0, k0, pol);
                             // rows of X past this unit's T_k meet zero-filled A columns
-                            load_tile2<128>(sb, &mapB, fb, 1, b3d, 0, ka.woff + o * ka.tk + k0 - ka.prow0, pol);
+                            if constexpr (F16)  // X^T: K-major, rows = columns c of X
+                                load_tile2<128>(sb, &mapB, fb, 0, 0, 0, ka.woff + o * ka.tk + k0 - ka.prow0, pol);
+                            else
+                                load_tile2<128>(sb, &mapB, fb, 1, b3d, 0, ka.woff + o * ka.tk + k0 - ka.prow0, pol);
                         }
                         if (++stage == NST) { stage = 0; phase ^= 1; }
                     }
@@ -181,7 +194,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            const uint32_t idesc = idesc2_tf32(KR_BN, JT, true);
+            const uint32_t idesc = F16 ? idesc2_f16(KR_BN, false, false) : idesc2_tf32(KR_BN, JT, true);
             for (int64_t u = pair_id; u < nunits; u += npairs) {
                 int64_t mi, op0, op1, kb0, kb1, sl;
                 unit_of(u, mi, op0, op1, kb0, kb1, sl);
@@ -198,8 +211,14 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                         for (int ks = 0; ks < BK / 8; ++ks) {
                             const uint64_t ad = JT ? smem_desc(sa + ks * mn_kstep, mn_lbo, mn_sbo, 1)
                                                    : smem_desc(sa + ks * 32, 16, 1024, 2);
-                            const uint64_t bd = smem_desc(sb + ks * mn_kstep, mn_lbo, mn_sbo, 1);
-                            mma2_tf32_e(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                            if constexpr (F16) {  // both K-major: K = 16 per MMA in the same 32 bytes
+                                const uint64_t bd = smem_desc(sb + ks * 32, 16, 1024, 2);
+                                if (elect_one()) mma2_f16(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                                __syncwarp();
+                            } else {
+                                const uint64_t bd = smem_desc(sb + ks * mn_kstep, mn_lbo, mn_sbo, 1);
+                                mma2_tf32_e(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                            }
                         }
                         commit2_e(&empty[stage]);
                         if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -296,6 +315,11 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
                 if (live) {
+                    if constexpr (F16) {  // undo the operand scales: row n, columns c
+                        const float rs = __ldg(ka.rinv + nrow);
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) sum[j] *= rs * __ldg(ka.cinv + chalf * 64 + j);
+                    }
                     float4* dst = reinterpret_cast<float4*>(ka.out + sl * ka.slab + nrow * ka.ldo + chalf * 64);
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
@@ -363,6 +387,56 @@ __global__ void round_pad_kernel(const float* __restrict__ in, float* __restrict
     }
 }
 
+// ---- F16 operands of J X (precision kF16S) ----------------------------------
+// out[n][i] = fp16(a[n][i] w_n) for i < tk (0 up to ld16), w_n = 2^(7 - e) with
+// max_i |a[n][i]| < 2^e, winv[n] = 1 / w_n; one CTA per example row
+__global__ void a16_kernel(const float* __restrict__ a, int64_t lda, int64_t n, int64_t tk, int64_t ld16,
+                           __half* __restrict__ out, float* __restrict__ winv) {
+    __shared__ float red[32];
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        float m = 0.f;
+        for (int64_t i = threadIdx.x; i < tk; i += blockDim.x) m = fmaxf(m, fabsf(a[r * lda + i]));
+        m = block_absmax(m, red);
+        const float w = pow2_scale(m, 7);
+        if (threadIdx.x == 0) winv[r] = 1.f / w;
+        for (int64_t i = threadIdx.x; i < ld16; i += blockDim.x)
+            out[r * ld16 + i] = __float2half_rn(i < tk ? a[r * lda + i] * w : 0.f);
+    }
+}
+
+// bits[c] = max over rows of |X[p][c]| (float bits; non-negative floats order as
+// unsigned ints), c < l; thread c of a block walks a chunk of rows
+__global__ void colmax_kernel(const float* __restrict__ X, int64_t ldx, int64_t R, int64_t l, int64_t rows_per_block,
+                              unsigned* __restrict__ bits) {
+    const int64_t c = threadIdx.x;
+    if (c >= l) return;
+    const int64_t p0 = blockIdx.x * rows_per_block, p1 = min(R, p0 + rows_per_block);
+    float m = 0.f;
+    for (int64_t p = p0; p < p1; ++p) m = fmaxf(m, fabsf(X[p * ldx + c]));
+    atomicMax(bits + c, __float_as_uint(m));
+}
+
+// XT[c][p] = fp16(X[p][c0 + c] z_c) for c < lc, p < R (0 up to ld16), z_c =
+// 2^(14 - e) with max_p |X[p][c]| < 2^e; zinv[c] = 1 / z_c.  32 x 32 tiles.
+__global__ void xt16_kernel(const float* __restrict__ X, int64_t ldx, int64_t R, int64_t lc, int64_t c0,
+                            const unsigned* __restrict__ bits, __half* __restrict__ XT, int64_t ld16,
+                            float* __restrict__ zinv) {
+    __shared__ float t[32][33];
+    const int64_t p0 = (int64_t)blockIdx.x * 32, cb = (int64_t)blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t p = p0 + y, c = cb + threadIdx.x;
+        t[y][threadIdx.x] = (p < R && c < lc) ? X[p * ldx + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t c = cb + y, p = p0 + threadIdx.x;
+        if (c >= lc || p >= ld16) continue;
+        const float z = pow2_scale(__uint_as_float(bits[c0 + c]), 14);
+        if (blockIdx.x == 0 && threadIdx.x == 0) zinv[c] = 1.f / z;
+        XT[c * ld16 + p] = __float2half_rn(t[threadIdx.x][y] * z);
+    }
+}
+
 }  // namespace tc
 
 // Rounded (to nearest TF32) copies of the activations and deltas of every
@@ -373,8 +447,14 @@ struct KrOperands {
     const float* d[kMaxLayers] = {};
     const float* dT[kMaxLayers] = {};  // delta_k^T (T_{k+1} x ldn, not rounded), zero padded
     int64_t ldn = 0;
+    // F16 (kF16S): a_k in fp16 with per-example scales, for the J X products
+    bool f16 = false;
+    DevMem mem16;
+    const __half* a16[kMaxLayers] = {};
+    const float* winv[kMaxLayers] = {};
+    int64_t lda16[kMaxLayers] = {};
 
-    KrOperands(const ModelDesc& md, const Cache<float>& c, cudaStream_t s) {
+    KrOperands(const ModelDesc& md, const Cache<float>& c, cudaStream_t s, bool with_f16 = false) {
         ldn = round_up(c.n, 32);
         size_t total = 0;
         for (int k = 0; k < md.S; ++k) total += (size_t)c.n * (c.lda[k] + c.ldt[k]) + (size_t)md.w[k + 1] * ldn;
@@ -397,6 +477,26 @@ struct KrOperands {
             dT[k] = p;
             p += (size_t)md.w[k + 1] * ldn;
         }
+        if (!with_f16) return;
+        f16 = true;
+        size_t bytes = 0;
+        for (int k = 0; k < md.S; ++k) {
+            lda16[k] = round_up(md.w[k], 64);
+            bytes += (size_t)c.n * lda16[k] * 2 + (size_t)round_up(c.n, 4) * 4;
+        }
+        mem16 = DevMem(bytes, s);
+        uint8_t* q = static_cast<uint8_t*>(mem16.p);
+        for (int k = 0; k < md.S; ++k) {
+            __half* h = reinterpret_cast<__half*>(q);
+            q += (size_t)c.n * lda16[k] * 2;
+            float* w = reinterpret_cast<float*>(q);
+            q += (size_t)round_up(c.n, 4) * 4;
+            tc::a16_kernel<<<(unsigned)std::min<int64_t>(c.n, 65535), 128, 0, s>>>(c.a[k], c.lda[k], c.n, md.w[k],
+                                                                                 lda16[k], h, w);
+            CK_LAUNCH();
+            a16[k] = h;
+            winv[k] = w;
+        }
     }
 };
 
@@ -407,17 +507,18 @@ inline bool kr_supported(const ModelDesc& md, const Cache<float>& c) {
     return true;
 }
 
-template <bool JT>
+template <bool JT, bool F16 = false>
 void kr_launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const tc::pair::KrArgs& ka, int a3d,
                int b3d) {
     using C = tc::pair::KrCfg<JT>;
-    func_attr_once((const void*)tc::pair::kr_kernel<JT>, [] {
-        CK_CUDA(cudaFuncSetAttribute(tc::pair::kr_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES));
+    func_attr_once((const void*)tc::pair::kr_kernel<JT, F16>, [] {
+        CK_CUDA(cudaFuncSetAttribute(tc::pair::kr_kernel<JT, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     C::BYTES));
     });
     const int64_t units = ka.mt * (JT ? ka.nop * ka.ksplit : ceil_div(ka.nop, ka.chunk));
     const int grid = 2 * (int)std::min<int64_t>(units, tc::num_sms() / 2);
-    tc::pair::kr_kernel<JT><<<grid, C::THREADS, C::BYTES, s>>>(ma, mb, ka, (uint32_t)tc::BK * 128u, 512u, 1024u, a3d,
-                                                               b3d);
+    tc::pair::kr_kernel<JT, F16><<<grid, C::THREADS, C::BYTES, s>>>(ma, mb, ka, (uint32_t)tc::BK * 128u, 512u, 1024u,
+                                                                    a3d, b3d);
     CK_LAUNCH();
 }
 
@@ -507,19 +608,53 @@ inline void kr_apply_j(const ModelDesc& md, const Cache<float>& c, const KrOpera
         return;
     }
     DevMem ws((size_t)(nslab * slab) * sizeof(float), s);
+    // F16: X^T in fp16 with power-of-two column scales, per 128-column tile
+    DevMem cbits, xt16, zinv;
+    const int64_t ldR = round_up(R, 64);
+    if (op.f16) {
+        cbits = DevMem((size_t)l * 4, s);
+        CK_CUDA(cudaMemsetAsync(cbits.p, 0, (size_t)l * 4, s));
+        const int64_t rpb = 512;
+        tc::colmax_kernel<<<(unsigned)ceil_div(R, rpb), (unsigned)round_up(l, 32), 0, s>>>(X, ldx, R, l, rpb,
+                                                                                         dptr<unsigned>(cbits));
+        CK_LAUNCH();
+        xt16 = DevMem((size_t)128 * ldR * 2, s);
+        zinv = DevMem((size_t)128 * 4, s);
+    }
     for (int64_t c0 = 0; c0 < l; c0 += 128) {
         const int64_t lc = std::min<int64_t>(128, l - c0);
         const float* xc = dptr<float>(xr) + c0;
         const int b3 = ldx >= round_up(lc, 32) ? 1 : 0;
+        if (op.f16) {
+            CK_CUDA(cudaMemsetAsync(zinv.p, 0, (size_t)128 * 4, s));  // columns >= lc: scale 0
+            tc::xt16_kernel<<<dim3((unsigned)ceil_div(ldR, 32), (unsigned)ceil_div(lc, 32)), dim3(32, 8), 0, s>>>(
+                X, ldx, R, lc, c0, dptr<unsigned>(cbits), dptr<__half>(xt16), ldR, dptr<float>(zinv));
+            CK_LAUNCH();
+        }
         for (int k = 0; k < md.S; ++k) {
             const int64_t tk = md.w[k];
             if (sh.ob[k] > sh.oa[k]) {
-                CUtensorMap ma = tc::make_map(op.a[k], n, tk, c.lda[k], 0, 128);
-                CUtensorMap mb = tc::make_map(xc, lc, R, ldx, 1, 128, b3);
                 tc::pair::KrArgs ka{mt, ceil_div(sh.ob[k] - sh.oa[k], 2), chunk[k], ceil_div(tk, tc::BK), tk,
-                                    md.w[k + 1], md.woff[k], c.delta[k], c.ldt[k], n,
-                                    dptr<float>(ws) + base[k] * slab, ldw, slab, n, lc, 1, sh.oa[k], sh.ob[k], sh.p0};
-                kr_launch<false>(s, ma, mb, ka, 0, b3);
+                                    md.w[k + 1], md.woff[k],
+                                    c.delta[k], c.ldt[k], n, dptr<float>(ws) + base[k] * slab, ldw, slab, n, lc, 1,
+                                    sh.oa[k], sh.ob[k], sh.p0};
+                // the fp16 form reads X^T from parameter row woff + o T_k: TMA needs that
+                // start 16-byte (8-half) aligned, else the TF32 form (a 4-input layer)
+                const bool f16k = op.f16 && tk % 8 == 0 && (md.woff[k] - sh.p0) % 8 == 0;
+                if (f16k) {
+                    ka.nk = ceil_div(tk, 2 * tc::BK);
+                    ka.rinv = op.winv[k];
+                    ka.cinv = dptr<float>(zinv);
+                    // K extent = the zero-padded row (a 4-input layer's 8-byte rows are below
+                    // TMA's 16-byte minimum: the load faulted as an illegal instruction)
+                    CUtensorMap ma = tc::make_map_f16(op.a16[k], n, op.lda16[k], op.lda16[k], 128);
+                    CUtensorMap mb = tc::make_map_f16(dptr<__half>(xt16), lc, R, ldR, 128);
+                    kr_launch<false, true>(s, ma, mb, ka, 0, 0);
+                } else {
+                    CUtensorMap ma = tc::make_map(op.a[k], n, tk, c.lda[k], 0, 128);
+                    CUtensorMap mb = tc::make_map(xc, lc, R, ldx, 1, 128, b3);
+                    kr_launch<false>(s, ma, mb, ka, 0, b3);
+                }
             }
             if (bslab[k] >= 0)  // bias tangents: delta_k[:, ba..bb) Xb
                 gemm_tf32(kTF32, s, n, lc, sh.bb[k] - sh.ba[k], pre_rounded(kmaj(op.d[k] + sh.ba[k], c.ldt[k])),

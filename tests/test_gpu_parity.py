@@ -101,7 +101,7 @@ def test_hvp_symmetry_linearity():
     assert rel_fro(HC, a * HU + b * HV) <= 1e-9
 
 
-@pytest.mark.parametrize("prec", ["f64", "tf32"])
+@pytest.mark.parametrize("prec", ["f64", "tf32", "f16s"])
 def test_opg_topk_matches_dense_eig(prec):
     g = load_golden("config0")
     spec = spec_of(g)
@@ -199,7 +199,7 @@ def test_config2_hessian_pins_tf32():
         assert rel_fro(got[:, j], pins["hcols"][:, j]) <= 1e-3, j
 
 
-@pytest.mark.parametrize("prec", ["tf32", "f32"])
+@pytest.mark.parametrize("prec", ["tf32", "f32", "f16s"])
 def test_config1_topk_against_dual_gram(prec):
     """Top-k of G at config-1 size (P = 23860, N = 4096): the K-split J X
     product and the device CholeskyQR2 path.  The nonzero spectrum of
@@ -361,11 +361,12 @@ def test_config4_topk_against_exact_spectrum():
     # Chebyshev-filtered subspace iteration: 3 rounds of degree 6 (18 operator
     # applications instead of 64 power iterations), and the default converged
     # solver (Ritz-convergence stop rule, tol 1e-4)
-    for tag in ("cheb3x6", "auto"):
+    for tag in ("cheb3x6", "auto", "auto_f16s"):
         q = torch.empty((P, k), dtype=torch.float32, device="cuda:0")
         lam = torch.empty(k, dtype=torch.float32, device="cuda:0")
-        if tag == "auto":
-            curv.dev_opg_topk_auto(spec, p, x, lab, n, k, wl.oversample, 7, q, lam)
+        if tag.startswith("auto"):
+            curv.dev_opg_topk_auto(spec, p, x, lab, n, k, wl.oversample, 7, q, lam,
+                                   precision="f16s" if tag == "auto_f16s" else "tf32")
         else:
             curv.dev_opg_topk_filtered(spec, p, x, lab, n, k, wl.oversample, 3, 6, 7, q, lam, precision="tf32")
         torch.cuda.synchronize()
@@ -412,8 +413,10 @@ def test_config4_topk_against_exact_spectrum():
     assert ec.max() <= 1e-3, (ec.max(), int(ec.argmax()))         # the same bar from 18 applications
     ea = np.abs(lams["auto"] - ev) / ev
     assert ea.max() <= 1e-3, (ea.max(), int(ea.argmax()))         # the default solver: stops converged
+    ef = np.abs(lams["auto_f16s"] - ev) / ev
+    assert ef.max() <= 1e-3, (ef.max(), int(ef.argmax()))         # the same in the F16S mode
     print(f"c4 max rel. eigenvalue error: power-2 {e2.max():.3e}, power-64 {e64.max():.3e}, "
-          f"cheb 3x6 {ec.max():.3e}, auto {ea.max():.3e}")
+          f"cheb 3x6 {ec.max():.3e}, auto {ea.max():.3e}, auto f16s {ef.max():.3e}")
 
 
 @pytest.mark.parametrize("prec", ["f64", "tf32"])

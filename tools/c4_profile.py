@@ -9,6 +9,7 @@ sys.path.insert(0, ".")
 from paper_1905_05559_b200 import curv  # noqa: E402
 from paper_1905_05559_b200.workloads import CONFIGS  # noqa: E402
 
+prec = sys.argv[1] if len(sys.argv) > 1 else "tf32"
 wl = CONFIGS["c4"]
 params, x, _, labels = wl.draw()
 dev = "cuda:0"
@@ -19,8 +20,9 @@ spec = curv.ModelSpec(wl.widths, wl.activation)
 k = wl.eig_k
 q = torch.empty((wl.P, k), dtype=torch.float32, device=dev)
 lam = torch.empty(k, dtype=torch.float32, device=dev)
-runs = {"baseline": lambda: curv.dev_opg_topk(spec, p, xx, ll, wl.n, k, wl.oversample, wl.power_iters, 7, q, lam),
-        "auto": lambda: curv.dev_opg_topk_auto(spec, p, xx, ll, wl.n, k, wl.oversample, 7, q, lam)}
+runs = {"baseline": lambda: curv.dev_opg_topk(spec, p, xx, ll, wl.n, k, wl.oversample, wl.power_iters, 7, q, lam,
+                                              precision=prec),
+        "auto": lambda: curv.dev_opg_topk_auto(spec, p, xx, ll, wl.n, k, wl.oversample, 7, q, lam, precision=prec)}
 for name, fn in runs.items():
     fn()
     torch.cuda.synchronize()
@@ -32,7 +34,7 @@ for name, fn in runs.items():
     torch.cuda.synchronize()
     prof = curv.profile_end()
     tot = e0.elapsed_time(e1)
-    print(f"== {name}: {tot:.1f} ms")
+    print(f"== {name} ({prec}): {tot:.1f} ms")
     for r, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]):
         tf = v["flops"] / (v["ms"] / 1e3) / 1e12 if v["flops"] else 0
         print(f"  {r:24s} {v['ms']:8.2f} ms  {v['launches']:5d} launches  {tf:7.1f} TF/s")
