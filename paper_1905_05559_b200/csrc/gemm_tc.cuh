@@ -458,6 +458,16 @@ __device__ __forceinline__ void tma2_2d(void* dst, const CUtensorMap* map, uint3
         "l"(map), "r"(bar_leader), "r"(c0), "r"(c1), "l"(pol)
         : "memory");
 }
+// one box written to the same offset in every CTA of `mask`, completing bytes
+// on each destination CTA's barrier at the offset of `bar`
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void tma2_3d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
                                         int32_t c1, int32_t c2, uint64_t pol) {
     asm volatile(

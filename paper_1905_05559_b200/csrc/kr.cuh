@@ -59,15 +59,22 @@ struct KrArgs {
     // operands -- per example row of a_k and per column c of X^T
     const float* rinv = nullptr;
     const float* cinv = nullptr;
+    // F16 J^T T: max |delta_k[:, o]| per unit and max |T[:, c]| per column of this
+    // tile: the operand scale of unit o, column c is pow2_scale(dmax tmax, 14)
+    const float* dmax = nullptr;
+    const float* tmax = nullptr;
 };
 
 constexpr int KR_BN = 256;
 
-template <bool JT>
+// JT F16: the B stage holds the raw fp32 T^T tile (128 columns c x 64
+// examples, two 128-byte boxes) plus 256 bytes of delta_o; the transform
+// overwrites box 0 with the fp16 operand row by row (each thread one row c)
+template <bool JT, bool F16 = false>
 struct KrCfg {
     static constexpr int THREADS = 128 + 32 * EPI_WARPS + (JT ? 128 : 0);
     static constexpr int A_BYTES = 128 * BK * 4;
-    static constexpr int B_BYTES = (KR_BN / 2) * BK * 4;
+    static constexpr int B_BYTES = (JT && F16) ? 2 * (KR_BN / 2) * BK * 4 + 1024 : (KR_BN / 2) * BK * 4;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int EPI_BYTES = 0;  // epilogues store from registers
     static constexpr int STAGES_ = (227 * 1024 - 1024 - EPI_BYTES - 1024) / STAGE_BYTES;
@@ -80,11 +87,11 @@ struct KrCfg {
 // by 1 / cinv); 64 inputs per 128-byte operand row, kind::f16 MMAs; the
 // epilogue undoes both scales on the summed row (exact).
 template <bool JT, bool F16 = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KrCfg<JT>::THREADS, 1)
-kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, KrArgs ka,
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KrCfg<JT, F16>::THREADS, 1)
+kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+          const __grid_constant__ CUtensorMap mapDelta, KrArgs ka,
           uint32_t mn_lbo, uint32_t mn_sbo, uint32_t mn_kstep, int a3d, int b3d) {
-    using C = KrCfg<JT>;
-    static_assert(!(JT && F16), "the fp16 form is J X only");
+    using C = KrCfg<JT, F16>;
     constexpr int KBE = F16 ? 2 * BK : BK;  // K elements per 128-byte operand row
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -168,7 +175,19 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                         uint8_t* sb = sa + C::A_BYTES;
                         const uint32_t fb = map_to_leader(smem_u32(&full[stage]));
                         const int64_t k0 = kb * KBE;
-                        if constexpr (JT) {
+                        if constexpr (JT && F16) {
+                            // A = a_k^T in fp16 (K-major over examples); raw T^T boxes + delta_o
+                            if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * C::A_BYTES));
+                            load_tile2<128>(sa, &mapA, fb, 0, 0, r0, k0, pol);
+                            // both CTAs scale the same T^T tile: each loads one of its two
+                            // boxes into both (the peer's stage is free: the pair MMA that
+                            // last read it has committed to both CTAs' empty barriers)
+                            mbar_expect_tx(&bfull[stage], (uint32_t)(2 * 16384 + 256));
+                            tma_load_2d_mc(sb + rank * 16384, &mapB, &bfull[stage], (int32_t)(k0 + 32 * rank), 0,
+                                           (uint16_t)3);
+                            tma_load_2d(sb + 32768, &mapDelta, &bfull[stage], (int32_t)k0,
+                                        (int32_t)(o < ka.oend ? o : ka.o0));
+                        } else if constexpr (JT) {
                             if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * C::A_BYTES));
                             load_tile2<128>(sa, &mapA, fb, 1, a3d, r0, k0, pol);
                             mbar_expect_tx(&bfull[stage], (uint32_t)C::B_BYTES);
@@ -209,8 +228,8 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                         const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
                         for (int ks = 0; ks < BK / 8; ++ks) {
-                            const uint64_t ad = JT ? smem_desc(sa + ks * mn_kstep, mn_lbo, mn_sbo, 1)
-                                                   : smem_desc(sa + ks * 32, 16, 1024, 2);
+                            const uint64_t ad = (JT && !F16) ? smem_desc(sa + ks * mn_kstep, mn_lbo, mn_sbo, 1)
+                                                             : smem_desc(sa + ks * 32, 16, 1024, 2);
                             if constexpr (F16) {  // both K-major: K = 16 per MMA in the same 32 bytes
                                 const uint64_t bd = smem_desc(sb + ks * 32, 16, 1024, 2);
                                 if (elect_one()) mma2_f16(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
@@ -226,6 +245,46 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                     commit2_e(&tfull[acc]);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
+            }
+        }
+    } else if (JT && F16 && warp >= TW0) {  // ---------------- fp16 B rows (both CTAs)
+        // thread t = column c of this CTA's unit o: row c of the raw T^T tile
+        // (examples k0 .. k0 + 63 in two 128-byte boxes) times delta_o (staged
+        // 256 bytes), scaled by the power of two of (o, c), rounded to fp16 and
+        // written back as row c of box 0 (each thread reads its row first)
+        const int c = threadIdx.x - TW0 * 32;
+        const uint32_t fb0 = map_to_leader(smem_u32(&full[0]));
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t u = pair_id; u < nunits; u += npairs) {
+            int64_t mi, op0, op1, kb0, kb1, sl;
+            unit_of(u, mi, op0, op1, kb0, kb1, sl);
+            const int64_t o = ka.o0 + 2 * op0 + rank;
+            const float sc = (o < ka.oend && c < ka.l) ? pow2_scale(__ldg(ka.dmax + o) * __ldg(ka.tmax + c), 14) : 0.f;
+            for (int64_t kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(&bfull[stage], phase);
+                uint8_t* sb = stage_base + stage * C::STAGE_BYTES + C::A_BYTES;
+                const float4* dl = reinterpret_cast<const float4*>(sb + 32768);
+                float4 x[16];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        x[8 * h + q] = *reinterpret_cast<const float4*>(sb + h * 16384 + c * 128 + ((q ^ (c & 7)) << 4));
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {  // output chunk q = examples 8q .. 8q + 7 = raw chunks 2q, 2q + 1
+                    const float4 a0 = x[2 * q], a1 = x[2 * q + 1], d0 = dl[2 * q], d1 = dl[2 * q + 1];
+                    uint4 w;
+                    w.x = sym::h2_bits(a0.x * d0.x * sc, a0.y * d0.y * sc);
+                    w.y = sym::h2_bits(a0.z * d0.z * sc, a0.w * d0.w * sc);
+                    w.z = sym::h2_bits(a1.x * d1.x * sc, a1.y * d1.y * sc);
+                    w.w = sym::h2_bits(a1.z * d1.z * sc, a1.w * d1.w * sc);
+                    *reinterpret_cast<uint4*>(sb + c * 128 + ((q ^ (c & 7)) << 4)) = w;
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(fb0 + stage * 8);
+                if (++stage == NST) { stage = 0; phase ^= 1; }
             }
         }
     } else if (JT && warp >= TW0) {  // ---------------- T-tile scaling (both CTAs)
@@ -334,11 +393,18 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                 const int64_t i = row0 + lane;
                 float* yrow = ka.out + sl * ka.slab + (ka.woff + o * ka.tk + i - ka.prow0) * ka.ldo;
                 const bool vec = (ka.ldo & 3) == 0;
+                const float ri = (F16 && i < ka.rows) ? __ldg(ka.rinv + i) : 1.f;
+                const float dm = (F16 && o < ka.oend) ? __ldg(ka.dmax + o) : 0.f;
                 for (int cb = 0; cb < 4; ++cb) {
                     const int64_t c0 = cb * 32;
                     if (c0 >= ka.l || o >= ka.oend) break;
                     float v[32];
                     tmem_ld32(lane_base + (uint32_t)(acc * KR_BN + chalf * 128 + cb * 32), v);
+                    if constexpr (F16) {  // undo the operand scales (exact): row i, (unit o, column c)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            v[j] *= c0 + j < ka.l ? ri / pow2_scale(dm * __ldg(ka.tmax + c0 + j), 14) : 0.f;
+                    }
                     if (i < ka.rows) {
                         if (vec && c0 + 32 <= ka.l) {
 #pragma unroll
@@ -408,12 +474,34 @@ __global__ void a16_kernel(const float* __restrict__ a, int64_t lda, int64_t n, 
 // unsigned ints), c < l; thread c of a block walks a chunk of rows
 __global__ void colmax_kernel(const float* __restrict__ X, int64_t ldx, int64_t R, int64_t l, int64_t rows_per_block,
                               unsigned* __restrict__ bits) {
-    const int64_t c = threadIdx.x;
+    const int64_t c = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
     if (c >= l) return;
     const int64_t p0 = blockIdx.x * rows_per_block, p1 = min(R, p0 + rows_per_block);
     float m = 0.f;
     for (int64_t p = p0; p < p1; ++p) m = fmaxf(m, fabsf(X[p * ldx + c]));
     atomicMax(bits + c, __float_as_uint(m));
+}
+
+inline void colmax(cudaStream_t s, const float* X, int64_t ldx, int64_t R, int64_t l, unsigned* bits) {
+    const int64_t rpb = 512, bx = std::min<int64_t>(round_up(l, 32), 256);
+    colmax_kernel<<<dim3((unsigned)ceil_div(R, rpb), (unsigned)ceil_div(l, bx)), (unsigned)bx, 0, s>>>(X, ldx, R, l,
+                                                                                                   rpb, bits);
+    CK_LAUNCH();
+}
+
+// 2-D fp32 map without swizzle over rows x K (pitch ld), box (box_k, 1): one
+// row segment (delta_k^T row o of the F16 J^T T stages)
+inline CUtensorMap make_map_rowseg(const float* p, int64_t rows, int64_t K, int64_t ld, int box_k) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows}, strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_k, 1}, es[2] = {1, 1};
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || (strides[0] & 15))
+        throw CurvError(kCudaError, "TMA operand must be 16-byte aligned with a 16-byte row pitch");
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CurvError(kCudaError, "cuTensorMapEncodeTiled (row) failed: " + std::to_string((int)r));
+    return m;
 }
 
 // XT[c][p] = fp16(X[p][c0 + c] z_c) for c < lc, p < R (0 up to ld16), z_c =
@@ -453,6 +541,12 @@ struct KrOperands {
     const __half* a16[kMaxLayers] = {};
     const float* winv[kMaxLayers] = {};
     int64_t lda16[kMaxLayers] = {};
+    // ... and for J^T T: a_k^T in fp16 (T_k x ldn16) with per-input scales,
+    // and max |delta_k[:, o]| per output unit
+    const __half* aT16[kMaxLayers] = {};
+    const float* uinv[kMaxLayers] = {};
+    const float* dmax[kMaxLayers] = {};
+    int64_t ldn16 = 0;
 
     KrOperands(const ModelDesc& md, const Cache<float>& c, cudaStream_t s, bool with_f16 = false) {
         ldn = round_up(c.n, 32);
@@ -480,9 +574,11 @@ struct KrOperands {
         if (!with_f16) return;
         f16 = true;
         size_t bytes = 0;
+        ldn16 = round_up(c.n, 64);
         for (int k = 0; k < md.S; ++k) {
             lda16[k] = round_up(md.w[k], 64);
             bytes += (size_t)c.n * lda16[k] * 2 + (size_t)round_up(c.n, 4) * 4;
+            bytes += (size_t)md.w[k] * ldn16 * 2 + (size_t)round_up(md.w[k], 4) * 4 + (size_t)round_up(md.w[k + 1], 4) * 4;
         }
         mem16 = DevMem(bytes, s);
         uint8_t* q = static_cast<uint8_t*>(mem16.p);
@@ -497,6 +593,23 @@ struct KrOperands {
             a16[k] = h;
             winv[k] = w;
         }
+        for (int k = 0; k < md.S; ++k) {
+            __half* h = reinterpret_cast<__half*>(q);
+            q += (size_t)md.w[k] * ldn16 * 2;
+            float* u = reinterpret_cast<float*>(q);
+            q += (size_t)round_up(md.w[k], 4) * 4;
+            float* dm = reinterpret_cast<float*>(q);
+            q += (size_t)round_up(md.w[k + 1], 4) * 4;
+            tc::am_f16_kernel<<<(unsigned)std::min<int64_t>(md.w[k], 8192), 256, 0, s>>>(c.a[k], c.lda[k], md.w[k], c.n,
+                                                                                       ldn16, h, u);
+            CK_LAUNCH();
+            tc::row_absmax_kernel<<<(unsigned)std::min<int64_t>(md.w[k + 1], 8192), 256, 0, s>>>(dT[k], md.w[k + 1], c.n,
+                                                                                               ldn, dm);
+            CK_LAUNCH();
+            aT16[k] = h;
+            uinv[k] = u;
+            dmax[k] = dm;
+        }
     }
 };
 
@@ -509,16 +622,16 @@ inline bool kr_supported(const ModelDesc& md, const Cache<float>& c) {
 
 template <bool JT, bool F16 = false>
 void kr_launch(cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, const tc::pair::KrArgs& ka, int a3d,
-               int b3d) {
-    using C = tc::pair::KrCfg<JT>;
+               int b3d, const CUtensorMap* mdl = nullptr) {
+    using C = tc::pair::KrCfg<JT, F16>;
     func_attr_once((const void*)tc::pair::kr_kernel<JT, F16>, [] {
         CK_CUDA(cudaFuncSetAttribute(tc::pair::kr_kernel<JT, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      C::BYTES));
     });
     const int64_t units = ka.mt * (JT ? ka.nop * ka.ksplit : ceil_div(ka.nop, ka.chunk));
     const int grid = 2 * (int)std::min<int64_t>(units, tc::num_sms() / 2);
-    tc::pair::kr_kernel<JT, F16><<<grid, C::THREADS, C::BYTES, s>>>(ma, mb, ka, (uint32_t)tc::BK * 128u, 512u, 1024u,
-                                                                    a3d, b3d);
+    tc::pair::kr_kernel<JT, F16><<<grid, C::THREADS, C::BYTES, s>>>(ma, mb, mdl ? *mdl : mb, ka,
+                                                                    (uint32_t)tc::BK * 128u, 512u, 1024u, a3d, b3d);
     CK_LAUNCH();
 }
 
@@ -615,9 +728,7 @@ inline void kr_apply_j(const ModelDesc& md, const Cache<float>& c, const KrOpera
         cbits = DevMem((size_t)l * 4, s);
         CK_CUDA(cudaMemsetAsync(cbits.p, 0, (size_t)l * 4, s));
         const int64_t rpb = 512;
-        tc::colmax_kernel<<<(unsigned)ceil_div(R, rpb), (unsigned)round_up(l, 32), 0, s>>>(X, ldx, R, l, rpb,
-                                                                                         dptr<unsigned>(cbits));
-        CK_LAUNCH();
+        tc::colmax(s, X, ldx, R, l, dptr<unsigned>(cbits));
         xt16 = DevMem((size_t)128 * ldR * 2, s);
         zinv = DevMem((size_t)128 * 4, s);
     }
@@ -673,17 +784,46 @@ inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOper
                         const float* Tn, int64_t ldtn, int64_t l, float* Y, int64_t ldy, cudaStream_t s) {
     const int64_t n = c.n;
     const int64_t pairs = tc::num_sms() / 2;
+    // F16: T^T per 128-column tile in fp32 (the kernel scales it by delta_o and
+    // rounds to fp16 in shared memory) and max |T[:, c]| per column
+    DevMem tbits, tt;
+    if (op.f16) {
+        tbits = DevMem((size_t)l * 4, s);
+        CK_CUDA(cudaMemsetAsync(tbits.p, 0, (size_t)l * 4, s));
+        tc::colmax(s, Tn, ldtn, n, l, dptr<unsigned>(tbits));
+        tt = DevMem((size_t)128 * op.ldn * 4, s);
+    }
     for (int64_t c0 = 0; c0 < l; c0 += 128) {
         const int64_t lc = std::min<int64_t>(128, l - c0);
         const float* tc0 = Tn + c0;
         const int b3 = ldtn >= round_up(lc, 32) ? 1 : 0;
         CUtensorMap mb = tc::make_map(tc0, lc, n, ldtn, 1, 128, b3);
+        CUtensorMap mb16;
+        if (op.f16) {
+            transpose<float>(s, tc0, ldtn, 0, dptr<float>(tt), op.ldn, 0, n, lc, 1);
+            mb16 = tc::make_map(dptr<float>(tt), lc, n, op.ldn, 0, 128);
+        }
         for (int k = 0; k < md.S; ++k) {
             const int64_t tk = md.w[k], oa = sh.oa[k], ob = sh.ob[k];
             if (ob > oa) {
                 const int a3 = c.lda[k] >= round_up(tk, 32) ? 1 : 0;
-                CUtensorMap ma = tc::make_map(op.a[k], tk, n, c.lda[k], 1, 128, a3);
-                const int64_t mt = ceil_div(tk, 256), nop = ceil_div(ob - oa, 2), nk = ceil_div(n, tc::BK);
+                const bool f16 = op.f16;
+                CUtensorMap ma = f16 ? tc::make_map_f16(op.aT16[k], tk, n, op.ldn16, 128)
+                                     : tc::make_map(op.a[k], tk, n, c.lda[k], 1, 128, a3);
+                CUtensorMap mdl;
+                if (f16) mdl = tc::make_map_rowseg(op.dT[k], md.w[k + 1], n, op.ldn, 64);
+                auto launch = [&](tc::pair::KrArgs& ka) {
+                    if (f16) {
+                        ka.rinv = op.uinv[k];
+                        ka.dmax = op.dmax[k];
+                        ka.tmax = reinterpret_cast<const float*>(dptr<unsigned>(tbits)) + c0;
+                        kr_launch<true, true>(s, ma, mb16, ka, 0, 0, &mdl);
+                    } else {
+                        kr_launch<true>(s, ma, mb, ka, a3, b3);
+                    }
+                };
+                const int64_t mt = ceil_div(tk, 256), nop = ceil_div(ob - oa, 2),
+                              nk = ceil_div(n, f16 ? 2 * tc::BK : tc::BK);
                 // few (i-tile, o-pair) units (a narrow layer): split the examples
                 // into slabs of partial products, summed in fixed order after
                 int64_t ks = 1;
@@ -692,14 +832,14 @@ inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOper
                 if (ks == 1) {
                     tc::pair::KrArgs ka{mt, nop, 1, nk, tk, md.w[k + 1], md.woff[k], op.dT[k], op.ldn, n, Y + c0, ldy,
                                         0, tk, lc, 1, oa, ob, sh.p0};
-                    kr_launch<true>(s, ma, mb, ka, a3, b3);
+                    launch(ka);
                 } else {
                     // slab rows (o - oa) T_k + i: woff 0 and prow0 = oa T_k
                     const int64_t rows = (ob - oa) * tk, slab = rows * 128;
                     DevMem ws((size_t)(ks * slab) * sizeof(float), s);
                     tc::pair::KrArgs ka{mt, nop, 1, nk, tk, md.w[k + 1], 0, op.dT[k], op.ldn, n, dptr<float>(ws),
                                         128, slab, tk, lc, ks, oa, ob, oa * tk};
-                    kr_launch<true>(s, ma, mb, ka, a3, b3);
+                    launch(ka);
                     tc::slab_sum_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, s>>>(
                         dptr<float>(ws), 128, slab, (int)ks, rows, lc, 1.f,
                         Y + (md.woff[k] + oa * tk - sh.p0) * ldy + c0, ldy);
