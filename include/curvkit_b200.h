@@ -308,8 +308,9 @@ int curvkit_dev_opg_topk_sharded_auto(const curvkit_model* model, const void* pa
                                       int64_t max_applications, uint64_t seed, int32_t precision, void* q,
                                       void* lambda, void* stream, curvkit_comm comm);
 
-/* Matrix-free Jacobian operator on a parameter-row range (TF32, J never
- * formed): transpose = 0: out (n x l) = J[:, p_begin:p_end] in, with in the
+/* Matrix-free Jacobian operator on a parameter-row range (TF32 class: TF32,
+ * TF32X3 or F16S -- the F16S products run the fp16 datapath on exactly scaled
+ * operands; J never formed): transpose = 0: out (n x l) = J[:, p_begin:p_end] in, with in the
  * (p_end - p_begin) x l rows of the range; transpose = 1: out ((p_end -
  * p_begin) x l) = J[:, p_begin:p_end]^T in, in n x l.  ld_in must be a
  * multiple of 32; the range must start and end on unit boundaries (any pair

@@ -1018,7 +1018,7 @@ int curvkit_dev_jacobian_apply(const curvkit_model* model, const void* params, c
         Cache<float> c;
         forward_device<float>(md, (const float*)params, (const float*)x, labels, n, c, s);
         if (!kr_supported(md, c)) contract("jacobian_apply: unsupported cache layout");
-        KrOperands op(md, c, s);
+        KrOperands op(md, c, s, precision == kF16S);
         if (transpose)
             kr_apply_jt(md, c, op, sh, (const float*)in, ld_in, l, (float*)out, ld_out, s);
         else

@@ -271,7 +271,7 @@ __device__ __forceinline__ T jac_entry(const LayerTable& t, const CachePtrs<T>& 
 
 template <class T>
 __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T> cp, int64_t P, T* __restrict__ J,
-                                                       int64_t ldj, int64_t row0, int rn_tf32) {
+                                                       int64_t ldj, int64_t row0, int rn_tf32, int vec) {
     const int64_t row = row0 + blockIdx.y;
     T* out = J + (int64_t)blockIdx.y * ldj;
     constexpr int V = 16 / sizeof(T);
@@ -286,14 +286,14 @@ __global__ void __launch_bounds__(256) jacobian_kernel(LayerTable t, CachePtrs<T
                 for (int u = 0; u < V; ++u) v[u] = round_tf32(v[u]);
             }
         }
-        if (c0 + V <= ldj) {
+        if (vec && c0 + V <= P) {  // 16-byte aligned rows: vector stores (the pitch padding untouched)
             if constexpr (sizeof(T) == 4) {
                 *reinterpret_cast<float4*>(out + c0) = make_float4(v[0], v[1], v[2], v[3]);
             } else {
                 *reinterpret_cast<double2*>(out + c0) = make_double2(v[0], v[1]);
             }
         } else {
-            for (int u = 0; u < V && c0 + u < ldj; ++u) out[c0 + u] = v[u];
+            for (int u = 0; u < V && c0 + u < P; ++u) out[c0 + u] = v[u];
         }
     }
 }
@@ -342,7 +342,7 @@ void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows
     LayerTable t = make_table(md, c.lda, c.ldt);
     CachePtrs<T> cp;
     for (int k = 0; k < md.S; ++k) { cp.a[k] = c.a[k]; cp.delta[k] = c.delta[k]; }
-    bool structured = (ldj % 4 == 0);
+    bool structured = (ldj % 4 == 0) && (reinterpret_cast<uintptr_t>(J) & 15) == 0;
     for (int k = 0; k < md.S; ++k) structured = structured && md.w[k] % 4 == 0 && md.woff[k] % 4 == 0;
     if (structured) {
         for (int64_t r = 0; r < rows; r += (int64_t)1 << 30) {
@@ -354,11 +354,13 @@ void jacobian(const ModelDesc& md, const Cache<T>& c, int64_t row0, int64_t rows
         return;
     }
     const int64_t per_block = 256 * (16 / sizeof(T));
+    // any pitch: vector stores only where every row start is 16-byte aligned
+    const int vec = (ldj * (int64_t)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(J) & 15) == 0;
     const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(md.P, per_block), 64);
     for (int64_t r = 0; r < rows; r += 65535) {
         const int64_t rr = std::min<int64_t>(65535, rows - r);
         jacobian_kernel<T><<<dim3(gx, (unsigned)rr), 256, 0, s>>>(t, cp, md.P, J + r * ldj, ldj, row0 + r,
-                                                                   rn_tf32 ? 1 : 0);
+                                                                   rn_tf32 ? 1 : 0, vec);
         CK_LAUNCH();
     }
 }

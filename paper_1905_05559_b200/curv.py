@@ -817,7 +817,8 @@ def dev_opg_topk_sharded_auto(spec, params, x, labels, n, k, oversample, seed, q
 def dev_jacobian_apply(spec, params, x, labels, n, p_begin, p_end, inp, ld_in, l, out, ld_out, transpose=False,
                        precision="tf32", stream=None):
     """Matrix-free J[:, p_begin:p_end] @ inp (transpose=False) or its
-    transpose, with J never formed (TF32 Khatri-Rao kernels)."""
+    transpose, with J never formed (tcgen05 Khatri-Rao kernels; precision
+    "tf32" or "f16s")."""
     _lib.check(_lib.load().curvkit_dev_jacobian_apply(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
                                                        _prec(precision), p_begin, p_end, 1 if transpose else 0,
                                                        _ptr(inp), ld_in, l, _ptr(out), ld_out, _stream(stream)))
