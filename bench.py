@@ -537,7 +537,9 @@ def run_extra(torch, dev, stream, pk, pk_kind):
     runs = {"baseline_setting": lambda: curv.dev_opg_topk(spec, p, xx, ll, wl.n, k, wl.oversample, wl.power_iters, 7,
                                                          q, lam, stream=stream),
             "converged_default": lambda: curv.dev_opg_topk_auto(spec, p, xx, ll, wl.n, k, wl.oversample, 7, q, lam,
-                                                                stream=stream)}
+                                                                stream=stream),
+            "converged_f16s": lambda: curv.dev_opg_topk_auto(spec, p, xx, ll, wl.n, k, wl.oversample, 7, q, lam,
+                                                             precision="f16s", stream=stream)}
     c4 = {"workload": f"c4: MLP {wl.widths} {wl.activation}, N={wl.n}, P={wl.P}: top-{k} OPG eigenpairs"}
     for key, fn in runs.items():
         fn()
@@ -555,6 +557,9 @@ def run_extra(torch, dev, stream, pk, pk_kind):
     c4["converged_default"]["note"] = ("Chebyshev-filtered subspace iteration with the Ritz-convergence stop rule "
                                        "(curvkit_dev_opg_topk_auto): all 100 eigenvalues within 1e-3 "
                                        "(tests/test_gpu_parity.py::test_config4_topk_against_exact_spectrum)")
+    c4["converged_f16s"]["note"] = ("the converged solver with the J X / J^T T products on the fp16 datapath "
+                                    "(F16S: exactly scaled TF32-class operands); all 100 eigenvalues within 1e-3 "
+                                    "(same test, auto_f16s)")
     out["c4_topk"] = c4
     return out
 

@@ -41,7 +41,7 @@ namespace pair {
 
 struct KrArgs {
     int64_t mt;           // row tiles (JX: n-tiles of 256 examples; JT: i-tiles of 256 inputs)
-    int64_t nop;          // o pairs: ceil((oend - o0) / 2)
+    int64_t nop;          // o pairs: ceil((oend - o0) / 2) (JT F16: o quads, ceil((oend - o0) / 4))
     int64_t chunk;        // JX: o pairs per work unit
     int64_t nk;           // k-blocks per o pair (JX: ceil(T_k / 32); JT: ceil(n / 32))
     int64_t tk, to, woff;  // T_k, T_{k+1}, first weight row of layer k in X / Y
@@ -67,14 +67,18 @@ struct KrArgs {
 
 constexpr int KR_BN = 256;
 
-// JT F16: the B stage holds the raw fp32 T^T tile (128 columns c x 64
-// examples, two 128-byte boxes) plus 256 bytes of delta_o; the transform
-// overwrites box 0 with the fp16 operand row by row (each thread one row c)
+// JT F16 ("quad" units: each CTA of the pair computes TWO output units
+// o, o + 2 against the same A and T tiles, i.e. four units per pair and two
+// N = 256 MMAs per k-step into the whole TMEM): the B stage holds the raw fp32
+// T^T tile (128 columns c x 64 examples, two 128-byte boxes), the second
+// unit's fp16 operand (16 KB) and the two delta_o rows (256 bytes each); the
+// transform writes the first unit's operand over box 0, row by row (each
+// thread one row c, read before written)
 template <bool JT, bool F16 = false>
 struct KrCfg {
     static constexpr int THREADS = 128 + 32 * EPI_WARPS + (JT ? 128 : 0);
     static constexpr int A_BYTES = 128 * BK * 4;
-    static constexpr int B_BYTES = (JT && F16) ? 2 * (KR_BN / 2) * BK * 4 + 1024 : (KR_BN / 2) * BK * 4;
+    static constexpr int B_BYTES = (JT && F16) ? 3 * (KR_BN / 2) * BK * 4 + 1024 : (KR_BN / 2) * BK * 4;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int EPI_BYTES = 0;  // epilogues store from registers
     static constexpr int STAGES_ = (227 * 1024 - 1024 - EPI_BYTES - 1024) / STAGE_BYTES;
@@ -93,6 +97,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           uint32_t mn_lbo, uint32_t mn_sbo, uint32_t mn_kstep, int a3d, int b3d) {
     using C = KrCfg<JT, F16>;
     constexpr int KBE = F16 ? 2 * BK : BK;  // K elements per 128-byte operand row
+    constexpr bool QUAD = JT && F16;        // two units per CTA, no accumulator double buffer
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int NST = C::STAGES;
@@ -168,7 +173,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                 unit_of(u, mi, op0, op1, kb0, kb1, sl);
                 const int64_t r0 = mi * 256 + 128 * rank;  // this CTA's A rows
                 for (int64_t op = op0; op < op1; ++op) {
-                    const int64_t o = ka.o0 + 2 * op + rank;  // this CTA's output unit
+                    const int64_t o = ka.o0 + (QUAD ? 4 : 2) * op + rank;  // this CTA's (first) output unit
                     for (int64_t kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sa = stage_base + stage * C::STAGE_BYTES;
@@ -182,11 +187,13 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                             // both CTAs scale the same T^T tile: each loads one of its two
                             // boxes into both (the peer's stage is free: the pair MMA that
                             // last read it has committed to both CTAs' empty barriers)
-                            mbar_expect_tx(&bfull[stage], (uint32_t)(2 * 16384 + 256));
+                            mbar_expect_tx(&bfull[stage], (uint32_t)(2 * 16384 + 512));
                             tma_load_2d_mc(sb + rank * 16384, &mapB, &bfull[stage], (int32_t)(k0 + 32 * rank), 0,
                                            (uint16_t)3);
-                            tma_load_2d(sb + 32768, &mapDelta, &bfull[stage], (int32_t)k0,
+                            tma_load_2d(sb + 49152, &mapDelta, &bfull[stage], (int32_t)k0,
                                         (int32_t)(o < ka.oend ? o : ka.o0));
+                            tma_load_2d(sb + 49152 + 256, &mapDelta, &bfull[stage], (int32_t)k0,
+                                        (int32_t)(o + 2 < ka.oend ? o + 2 : ka.o0));
                         } else if constexpr (JT) {
                             if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * C::A_BYTES));
                             load_tile2<128>(sa, &mapA, fb, 1, a3d, r0, k0, pol);
@@ -220,7 +227,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                 for (int64_t op = op0; op < op1; ++op) {
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
-                    const uint32_t d = tmem_base + (uint32_t)(acc * KR_BN);
+                    const uint32_t d = tmem_base + (uint32_t)(acc * KR_BN);  // QUAD: acc = 0, columns 0 .. 511
                     for (int64_t kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
@@ -232,7 +239,12 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                                                              : smem_desc(sa + ks * 32, 16, 1024, 2);
                             if constexpr (F16) {  // both K-major: K = 16 per MMA in the same 32 bytes
                                 const uint64_t bd = smem_desc(sb + ks * 32, 16, 1024, 2);
-                                if (elect_one()) mma2_f16(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                                if (elect_one()) {
+                                    mma2_f16(d, ad, bd, idesc, (kb > kb0 || ks > 0) ? 1u : 0u);
+                                    if constexpr (QUAD)  // the second unit pair: B at +32 KB, columns 256 ..
+                                        mma2_f16(d + KR_BN, ad, smem_desc(sb + 32768 + ks * 32, 16, 1024, 2), idesc,
+                                                 (kb > kb0 || ks > 0) ? 1u : 0u);
+                                }
                                 __syncwarp();
                             } else {
                                 const uint64_t bd = smem_desc(sb + ks * mn_kstep, mn_lbo, mn_sbo, 1);
@@ -243,7 +255,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                         if (++stage == NST) { stage = 0; phase ^= 1; }
                     }
                     commit2_e(&tfull[acc]);
-                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                    if (QUAD || ++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
             }
         }
@@ -259,12 +271,14 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         for (int64_t u = pair_id; u < nunits; u += npairs) {
             int64_t mi, op0, op1, kb0, kb1, sl;
             unit_of(u, mi, op0, op1, kb0, kb1, sl);
-            const int64_t o = ka.o0 + 2 * op0 + rank;
-            const float sc = (o < ka.oend && c < ka.l) ? pow2_scale(__ldg(ka.dmax + o) * __ldg(ka.tmax + c), 14) : 0.f;
+            const int64_t o = ka.o0 + 4 * op0 + rank;  // units o (box 0) and o + 2 (+32 KB)
+            const float tm = c < ka.l ? __ldg(ka.tmax + c) : 0.f;
+            const float sc0 = o < ka.oend ? pow2_scale(__ldg(ka.dmax + o) * tm, 14) : 0.f;
+            const float sc1 = o + 2 < ka.oend ? pow2_scale(__ldg(ka.dmax + o + 2) * tm, 14) : 0.f;
             for (int64_t kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&bfull[stage], phase);
                 uint8_t* sb = stage_base + stage * C::STAGE_BYTES + C::A_BYTES;
-                const float4* dl = reinterpret_cast<const float4*>(sb + 32768);
+                const float4* dl = reinterpret_cast<const float4*>(sb + 49152);
                 float4 x[16];
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
@@ -272,14 +286,18 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                     for (int q = 0; q < 8; ++q)
                         x[8 * h + q] = *reinterpret_cast<const float4*>(sb + h * 16384 + c * 128 + ((q ^ (c & 7)) << 4));
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {  // output chunk q = examples 8q .. 8q + 7 = raw chunks 2q, 2q + 1
-                    const float4 a0 = x[2 * q], a1 = x[2 * q + 1], d0 = dl[2 * q], d1 = dl[2 * q + 1];
-                    uint4 w;
-                    w.x = sym::h2_bits(a0.x * d0.x * sc, a0.y * d0.y * sc);
-                    w.y = sym::h2_bits(a0.z * d0.z * sc, a0.w * d0.w * sc);
-                    w.z = sym::h2_bits(a1.x * d1.x * sc, a1.y * d1.y * sc);
-                    w.w = sym::h2_bits(a1.z * d1.z * sc, a1.w * d1.w * sc);
-                    *reinterpret_cast<uint4*>(sb + c * 128 + ((q ^ (c & 7)) << 4)) = w;
+                for (int u = 0; u < 2; ++u) {
+                    const float sc = u ? sc1 : sc0;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {  // output chunk q = examples 8q .. 8q + 7 = raw chunks 2q, 2q + 1
+                        const float4 a0 = x[2 * q], a1 = x[2 * q + 1], d0 = dl[16 * u + 2 * q], d1 = dl[16 * u + 2 * q + 1];
+                        uint4 w;
+                        w.x = sym::h2_bits(a0.x * d0.x * sc, a0.y * d0.y * sc);
+                        w.y = sym::h2_bits(a0.z * d0.z * sc, a0.w * d0.w * sc);
+                        w.z = sym::h2_bits(a1.x * d1.x * sc, a1.y * d1.y * sc);
+                        w.w = sym::h2_bits(a1.z * d1.z * sc, a1.w * d1.w * sc);
+                        *reinterpret_cast<uint4*>(sb + u * 32768 + c * 128 + ((q ^ (c & 7)) << 4)) = w;
+                    }
                 }
                 fence_proxy_async();
                 __syncwarp();
@@ -387,19 +405,23 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
             } else {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
-                // TMEM columns 128*chalf.. hold output unit o; lane = input i,
-                // whose 32-column run of Y row (woff + o T_k + i) is contiguous
-                const int64_t o = ka.o0 + 2 * op0 + chalf;
+                // TMEM columns 128*chalf.. hold output unit o (QUAD: columns
+                // 256 u + 128 chalf.. unit o0 + 4 op + 2 u + chalf); lane = input
+                // i, whose 32-column run of Y row (woff + o T_k + i) is contiguous
                 const int64_t i = row0 + lane;
-                float* yrow = ka.out + sl * ka.slab + (ka.woff + o * ka.tk + i - ka.prow0) * ka.ldo;
                 const bool vec = (ka.ldo & 3) == 0;
                 const float ri = (F16 && i < ka.rows) ? __ldg(ka.rinv + i) : 1.f;
-                const float dm = (F16 && o < ka.oend) ? __ldg(ka.dmax + o) : 0.f;
+#pragma unroll 1
+                for (int u = 0; u < (QUAD ? 2 : 1); ++u)
+#pragma unroll 1
                 for (int cb = 0; cb < 4; ++cb) {
+                    const int64_t o = ka.o0 + (QUAD ? 4 : 2) * op0 + 2 * u + chalf;
+                    float* yrow = ka.out + sl * ka.slab + (ka.woff + o * ka.tk + i - ka.prow0) * ka.ldo;
+                    const float dm = (F16 && o < ka.oend) ? __ldg(ka.dmax + o) : 0.f;
                     const int64_t c0 = cb * 32;
                     if (c0 >= ka.l || o >= ka.oend) break;
                     float v[32];
-                    tmem_ld32(lane_base + (uint32_t)(acc * KR_BN + chalf * 128 + cb * 32), v);
+                    tmem_ld32(lane_base + (uint32_t)(acc * KR_BN + u * KR_BN + chalf * 128 + cb * 32), v);
                     if constexpr (F16) {  // undo the operand scales (exact): row i, (unit o, column c)
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -421,7 +443,7 @@ kr_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(te_leader + acc * 8);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (QUAD || ++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
     }
@@ -822,7 +844,8 @@ inline void kr_apply_jt(const ModelDesc& md, const Cache<float>& c, const KrOper
                         kr_launch<true>(s, ma, mb, ka, a3, b3);
                     }
                 };
-                const int64_t mt = ceil_div(tk, 256), nop = ceil_div(ob - oa, 2),
+                // (F16: units of four output units, two per CTA)
+                const int64_t mt = ceil_div(tk, 256), nop = ceil_div(ob - oa, f16 ? 4 : 2),
                               nk = ceil_div(n, f16 ? 2 * tc::BK : tc::BK);
                 // few (i-tile, o-pair) units (a narrow layer): split the examples
                 // into slabs of partial products, summed in fixed order after
