@@ -932,6 +932,8 @@ int curvkit_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, curvkit_c
         cm.comm = c;
         cm.rank = rank;
         cm.nranks = nranks;
+        const char* lb = getenv("CURVKIT_COMM_LOOPBACK");
+        cm.loopback = nranks == 1 && lb && lb[0] == '1';
         *out = new curvkit_comm_s{cm};
     });
 }

@@ -80,13 +80,17 @@ struct Comm {
     curvkit_host_gather_fn h_gather = nullptr;
     void* user = nullptr;
     int rank = 0, nranks = 1;
+    // One-rank NCCL communicators opened under CURVKIT_COMM_LOOPBACK=1 still issue
+    // their collectives (an in-place all-reduce over one rank, a send/recv pair
+    // to itself): the NCCL calls of the multi-GPU paths run on a one-GPU box.
+    bool loopback = false;
 
     bool host() const { return comm == nullptr && h_sum != nullptr; }
 
     // buf <- sum over ranks (identical bytes on every rank afterwards)
     template <class T>
     void sum(T* buf, size_t count, cudaStream_t s) const {
-        if (nranks == 1 || count == 0) return;
+        if ((nranks == 1 && !loopback) || count == 0) return;
         if (host()) {
             std::vector<T> h(count);
             CK_CUDA(cudaMemcpyAsync(h.data(), buf, count * sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -106,6 +110,16 @@ struct Comm {
     void gather(const void* send, const std::vector<int64_t>& bytes, void* recv, int root, cudaStream_t s) const {
         std::vector<int64_t> off(nranks + 1, 0);
         for (int r = 0; r < nranks; ++r) off[r + 1] = off[r] + bytes[r];
+        if (nranks == 1 && loopback && !host()) {
+            NcclApi& api = NcclApi::get();
+            if (!api.send || !api.recv || !api.group_start) throw CurvError(kRuntimeError, "NCCL send/recv unavailable");
+            if (bytes[0] <= 0) return;
+            nccl_check(api.group_start(), "ncclGroupStart");
+            nccl_check(api.recv(recv, (size_t)bytes[0], ncclInt8, 0, comm, s), "ncclRecv");
+            nccl_check(api.send(send, (size_t)bytes[0], ncclInt8, 0, comm, s), "ncclSend");
+            nccl_check(api.group_end(), "ncclGroupEnd");
+            return;
+        }
         if (nranks == 1 || (!host() && rank == root)) {
             if (rank == root && bytes[rank] > 0)
                 CK_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + off[rank], send, (size_t)bytes[rank],

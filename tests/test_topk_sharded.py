@@ -252,3 +252,42 @@ def test_sharded_filtered_one_rank_equals_unsharded():
         comm.close()
     torch.cuda.synchronize()
     assert torch.equal(l0, l1) and torch.equal(q0, q1)
+
+
+@pytest.mark.gpu
+def test_nccl_loopback_one_rank(monkeypatch):
+    """The NCCL calls themselves on a one-GPU box: under CURVKIT_COMM_LOOPBACK=1 a
+    one-rank NCCL communicator issues its all-reduces (sharded top-k) and the
+    send/recv pair of the final band gather instead of short-cutting them; the
+    results equal the communication-free ones bitwise (a one-rank sum and a
+    self send are copies)."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("CURVKIT_COMM_LOOPBACK", "1")
+    wl, spec, (p64, x64), lab = _c1(torch)
+    p32, x32 = p64.float(), x64.float()
+    k = 12
+    q0 = torch.empty((wl.P, k), device="cuda:0")
+    l0 = torch.empty(k, device="cuda:0")
+    curv.dev_opg_topk_filtered(spec, p32, x32, lab, wl.n, k, 10, 2, 3, 3, q0, l0)
+    P = wl.P
+    ld = (P + 31) // 32 * 32
+    comm = curv.Comm.create(0, 1, lambda b: b)
+    try:
+        n0 = curv.launch_count()
+        q1 = torch.empty((wl.P, k), device="cuda:0")
+        l1 = torch.empty(k, device="cuda:0")
+        curv.dev_opg_topk_sharded_filtered(spec, p32, x32, lab, wl.n, k, 10, 2, 3, 3, q1, l1, comm)
+        band = torch.full((curv.shard_units_rows(spec, 1, 0), ld), float("nan"), device="cuda:0")
+        curv.dev_assemble_band(spec, "opg", p32, x32, lab, wl.n, 1, 0, band, ld)
+        full = torch.full((P, ld), float("nan"), device="cuda:0")
+        curv.dev_gather_bands(spec, band, ld, full, ld, comm)
+        assert curv.launch_count() > n0
+    finally:
+        comm.close()
+    torch.cuda.synchronize()
+    assert torch.equal(l0, l1) and torch.equal(q0, q1)
+    local = torch.full((P, ld), float("nan"), device="cuda:0")
+    curv.dev_band_scatter(spec, 1, 0, band, ld, local, ld)
+    curv.dev_symmetrize_units(spec, local, ld)
+    torch.cuda.synchronize()
+    assert not torch.isnan(full[:, :P]).any() and torch.equal(full[:, :P], local[:, :P])
