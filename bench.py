@@ -464,17 +464,19 @@ def load_traffic(name):
     return json.load(open(tfile)).get(name) if os.path.exists(tfile) else None
 
 
-def band_balance(torch, dev, stream):
+def band_balance(torch, dev, stream, name="c3"):
     """Load balance of the multi-GPU split, measured on this one GPU: every
-    rank's unit band of config 3's G (curvkit_dev_assemble_band, the exact work
-    rank r of W runs, with its replicated forward/backward and J) timed in
-    turn.  projected_speedup = the 1-GPU step / the slowest band: what W GPUs
+    rank's unit band of config 3's G or config 2's H (curvkit_dev_assemble_band,
+    the exact work rank r of W runs, with its replicated forward/backward and,
+    for G, J) timed in turn.  projected_speedup = the 1-GPU step / the slowest band: what W GPUs
     reach before the final gather, without the NVLink exchange (which the
     assembly itself does not need)."""
     from paper_1905_05559_b200 import curv
-    job = Job("c3", "tf32", dev, torch)
+    job = Job(name, "tf32", dev, torch)
     wl = job.wl
-    ms1, _, _, _ = timed(job, 10, 2, stream, torch)  # ~1 s: the power-capped steady state
+    product = PRODUCTS[name][0]
+    ms1, _, _, _ = timed(job, 10, 2, stream, torch)
+    ms1, _, _, _ = timed(job, max(10, int(1000.0 / ms1)), 0, stream, torch)  # ~1 s: the power-capped steady state
     job.free()
     torch.cuda.empty_cache()
     out = {"one_gpu_ms": ms1, "method": "each band timed over >= 1 s of back-to-back assemblies (the steady, "
@@ -484,11 +486,11 @@ def band_balance(torch, dev, stream):
         for r in range(W):
             rows = curv.shard_units_rows(job.spec, W, r)
             band = torch.empty((max(1, rows), job.ld), dtype=torch.float32, device=dev)
-            f = lambda: curv.dev_assemble_band(job.spec, "opg", job.p_d, job.x_d, job.l_d, wl.n, W, r, band,  # noqa: E731
+            f = lambda: curv.dev_assemble_band(job.spec, product, job.p_d, job.x_d, job.l_d, wl.n, W, r, band,  # noqa: E731
                                                job.ld, precision="tf32", stream=stream)
             f()
             torch.cuda.synchronize()
-            reps = max(3, int(1000.0 / max(1.0, ms1 / W)))
+            reps = max(3, int(1000.0 / max(0.25, ms1 / W)))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(reps):
@@ -521,7 +523,8 @@ def run_extra(torch, dev, stream, pk, pk_kind):
         job.free()
         del job
         torch.cuda.empty_cache()
-    out["c3_band_balance"] = band_balance(torch, dev, stream)
+    out["c3_band_balance"] = band_balance(torch, dev, stream, "c3")
+    out["c2_band_balance"] = band_balance(torch, dev, stream, "c2")
     # c4: top-100 OPG eigenpairs, BASELINE's setting and the converged default
     from paper_1905_05559_b200 import curv
     from paper_1905_05559_b200.workloads import CONFIGS

@@ -75,6 +75,9 @@ struct SymKrArgs {
     // output units [u0, u1) (u1 < 0: all) stored at band rows bwoff / bboff (< 0:
     // the block's own rows woff / boff): see symkr.cuh Params and bands.cuh
     int64_t u0 = 0, u1 = -1, bwoff = -1, bboff = -1;
+    // >= 0: prof holds only the tangents of units prof_t0, prof_t0 + 1, ... and
+    // Pi[o][o''] is read as prof[(o'' - prof_t0) U + o] (the profile is symmetric)
+    int64_t prof_t0 = -1;
 };
 
 // kF16S OPG rectangles (blocks m < k): J^T in fp16 with an exact power-of-two
@@ -591,40 +594,47 @@ struct Engine {
                 keep.emplace_back((size_t)rows * ld * sizeof(T), s);
                 return dptr<T>(keep.back());
             };
+            // Unit bands run the R-op only for the tangents of their own units
+            // [t0, t1): P[o][.] and PV[o][.] are needed for the rows of unit o alone
+            // (the symmetric kernel reads PV[o''][o] for its packed columns o <= o'',
+            // o'' in the band); Q_m does not depend on the row's unit.
+            static const bool fused_env = getenv("CURVKIT_HESS_FUSED") != nullptr;
+            const bool band_rgen = band && !fused_env;
+            const int64_t t0 = band_rgen ? band->u0[k] : 0, nt = band_rgen ? band->u1[k] - band->u0[k] : np;
             ProfScope prof_stage("hess_profiles", s, 0.0, 0.0);
-            T* G = buf(np * n, c.ldt[k]);
+            T* G = buf(nt * n, c.ldt[k]);
             T* rzp[kMaxLayers] = {};
             if (k == S - 1) {
-                profile_output_kernel<T><<<blocks_for(np * n * np), 256, 0, s>>>(c.a[S], c.lda[S], np, n, md.mode, G,
-                                                                                  c.ldt[k]);
+                profile_output_kernel<T><<<blocks_for(nt * n * np), 256, 0, s>>>(c.a[S], c.lda[S], np, n, md.mode, G,
+                                                                                  c.ldt[k], t0, nt);
                 CK_LAUNCH();
             } else {
                 // R-forward above the tangent layer
-                rzp[k + 1] = buf(np * n, c.ldt[k + 1]);
-                profile_first_rz_kernel<T><<<blocks_for(np * n * md.w[k + 2]), 256, 0, s>>>(
+                rzp[k + 1] = buf(nt * n, c.ldt[k + 1]);
+                profile_first_rz_kernel<T><<<blocks_for(nt * n * md.w[k + 2]), 256, 0, s>>>(
                     c.z[k], c.ldt[k], params + md.woff[k + 1], md.w[k + 1], md.w[k + 2], n, md.act, rzp[k + 1],
-                    c.ldt[k + 1]);
+                    c.ldt[k + 1], t0, nt);
                 CK_LAUNCH();
                 for (int kp = k + 1; kp + 1 < S; ++kp) {
-                    T* ra = buf(np * n, c.lda[kp + 1]);
-                    rop_act_kernel<T><<<blocks_for(np * n * md.w[kp + 1]), 256, 0, s>>>(
-                        rzp[kp], c.ldt[kp], c.z[kp], c.ldt[kp], n, np * n, md.w[kp + 1], md.act, ra, c.lda[kp + 1]);
+                    T* ra = buf(nt * n, c.lda[kp + 1]);
+                    rop_act_kernel<T><<<blocks_for(nt * n * md.w[kp + 1]), 256, 0, s>>>(
+                        rzp[kp], c.ldt[kp], c.z[kp], c.ldt[kp], n, nt * n, md.w[kp + 1], md.act, ra, c.lda[kp + 1]);
                     CK_LAUNCH();
-                    rzp[kp + 1] = buf(np * n, c.ldt[kp + 1]);
+                    rzp[kp + 1] = buf(nt * n, c.ldt[kp + 1]);
                     EpiStore<T> e{rzp[kp + 1], c.ldt[kp + 1], 0, T(1), T(0)};
-                    gemm_simt<T>(s, np * n, md.w[kp + 2], md.w[kp + 1], 1, kmaj(ra, c.lda[kp + 1]),
+                    gemm_simt<T>(s, nt * n, md.w[kp + 2], md.w[kp + 1], 1, kmaj(ra, c.lda[kp + 1]),
                                  kmaj(params + md.woff[kp + 1], md.w[kp + 1]), e);
                 }
                 // R-backward down to the tangent layer
-                T* rdn = buf(np * n, c.ldt[S - 1]);
-                rop_softmax_kernel<T><<<blocks_for(np * n, 128), 128, 0, s>>>(
-                    rzp[S - 1], c.ldt[S - 1], c.a[S], c.lda[S], n, np * n, md.w[S], md.mode, rdn, c.ldt[S - 1]);
+                T* rdn = buf(nt * n, c.ldt[S - 1]);
+                rop_softmax_kernel<T><<<blocks_for(nt * n, 128), 128, 0, s>>>(
+                    rzp[S - 1], c.ldt[S - 1], c.a[S], c.lda[S], n, nt * n, md.w[S], md.mode, rdn, c.ldt[S - 1]);
                 CK_LAUNCH();
                 for (int kp = S - 2; kp >= k; --kp) {
-                    T* out = kp == k ? G : buf(np * n, c.ldt[kp]);
+                    T* out = kp == k ? G : buf(nt * n, c.ldt[kp]);
                     EpiRback<T> e{out, c.ldt[kp], c.z[kp], c.up[kp], c.ldt[kp], rzp[kp], c.ldt[kp], n, md.act,
-                                  kp == k ? 1 : 0, 1, 0};
-                    gemm_simt<T>(s, np * n, md.w[kp + 1], md.w[kp + 2], 1, kmaj(rdn, c.ldt[kp + 1]),
+                                  kp == k ? 1 : 0, 1, 0, t0};
+                    gemm_simt<T>(s, nt * n, md.w[kp + 1], md.w[kp + 2], 1, kmaj(rdn, c.ldt[kp + 1]),
                                  mnmaj(params + md.woff[kp + 1], md.w[kp + 1]), e);
                     rdn = out;
                 }
@@ -636,9 +646,9 @@ struct Engine {
                 const int64_t nq = md.w[k];
                 T* prevP = G;
                 for (int m = k - 1; m >= 0; --m) {
-                    Pm[m] = buf(np * n, c.ldt[m]);
+                    Pm[m] = buf(nt * n, c.ldt[m]);
                     EpiRback<T> e{Pm[m], c.ldt[m], c.z[m], nullptr, c.ldt[m], nullptr, 0, n, md.act, 0, 1, 0};
-                    gemm_simt<T>(s, np * n, md.w[m + 1], md.w[m + 2], 1, kmaj(prevP, c.ldt[m + 1]),
+                    gemm_simt<T>(s, nt * n, md.w[m + 1], md.w[m + 2], 1, kmaj(prevP, c.ldt[m + 1]),
                                  mnmaj(params + md.woff[m + 1], md.w[m + 1]), e);
                     prevP = Pm[m];
                 }
@@ -664,14 +674,14 @@ struct Engine {
             tb.add(c.a[k], c.lda[k], 0, akT, ldn, 0, n, tk + 1, 1);
             T* dkT = buf_full(np, ldn);
             tb.add(c.delta[k], c.ldt[k], 0, dkT, ldn, 0, n, np, 1);
-            T* GT = buf_full(np * np, ldn);
-            tb.add(G, c.ldt[k], n * c.ldt[k], GT, ldn, np * ldn, n, np, np);
+            T* GT = buf_full(nt * np, ldn);
+            tb.add(G, c.ldt[k], n * c.ldt[k], GT, ldn, np * ldn, n, np, nt);
             T* PT[kMaxLayers] = {};
             T* QT[kMaxLayers] = {};
             for (int m = k - 1; m >= 0; --m) {
                 const int64_t tm1 = md.w[m + 1];
-                PT[m] = buf_full(np * tm1, ldn);
-                tb.add(Pm[m], c.ldt[m], n * c.ldt[m], PT[m], ldn, tm1 * ldn, n, tm1, np);
+                PT[m] = buf_full(nt * tm1, ldn);
+                tb.add(Pm[m], c.ldt[m], n * c.ldt[m], PT[m], ldn, tm1 * ldn, n, tm1, nt);
                 QT[m] = buf_full(tk * tm1, ldn);
                 tb.add(Qm[m], c.ldt[m], n * c.ldt[m], QT[m], ldn, tm1 * ldn, n, tm1, tk);
             }
@@ -697,9 +707,8 @@ struct Engine {
                     CK_LAUNCH();
                 }
             };
-            // (blocks m < k take R in HBM unless banded or CURVKIT_HESS_FUSED, below)
-            static const bool fused_env = getenv("CURVKIT_HESS_FUSED") != nullptr;
-            if (fused && ((k > 0 && (band || fused_env)) || verify || sym_off())) build_ext();
+            // (blocks m < k take R in HBM unless CURVKIT_HESS_FUSED, below)
+            if (fused && ((k > 0 && fused_env) || verify || sym_off())) build_ext();
             prep_stage.end();
             // blocks (k, m), m <= k
             const int64_t Pk = md.block_size(k);
@@ -722,6 +731,7 @@ struct Engine {
                         sa.u1 = v1;
                         sa.bwoff = band->bw[k];
                         sa.bboff = band->bb[k];
+                        if (band_rgen) sa.prof_t0 = t0;
                     }
                     if (SymKr<T>::run(prec, s, sa)) jbeg = Pk;
                     else if (band) throw CurvError(kCudaError, "hessian: diagonal block kernel unavailable");
@@ -736,9 +746,11 @@ struct Engine {
                 // chunks (rounded to TF32, write-bound) and the pair GEMM (~570 TF/s)
                 // instead of the fused kernel, whose k-block pipeline runs at ~0.34 of
                 // the TF32 peak for reasons DESIGN.md section 4 did not isolate (c2:
-                // 7.2 -> 5.2 ms).  Unit bands keep the fused kernel (its epilogue
-                // writes band rows); CURVKIT_HESS_FUSED=1 selects it everywhere.
-                const bool rgen_tc = fused && !fused_env && m < k && !band;
+                // 7.2 -> 5.2 ms), unit bands included (the chunks then cover the band's
+                // weight and bias tangent rows).  CURVKIT_HESS_FUSED=1 selects the
+                // fused kernel everywhere.
+                const bool rgen_tc = fused && !fused_env && m < k;
+                if (band && m == k) continue;  // the symmetric kernel wrote the band's diagonal block
                 if (fused && jbeg < Pk && !rgen_tc) {
                     if (!akX) build_ext();
                     const int64_t tm = md.w[m], tm1 = md.w[m + 1];
@@ -771,19 +783,37 @@ struct Engine {
                 typename HessF16<T>::Prep hp;
                 HessF16Args ha{};
                 bool f16r = false;
-                if (rgen_tc && prec == kF16S && tm + 1 > 64 && jbeg < Pk) {
+                if (rgen_tc && !band && prec == kF16S && tm + 1 > 64 && jbeg < Pk) {
                     ha = HessF16Args{reinterpret_cast<const float*>(PT[m]), reinterpret_cast<const float*>(QT[m]),
                                      reinterpret_cast<const float*>(akT), reinterpret_cast<const float*>(dkT),
                                      reinterpret_cast<const float*>(c.a[m]), c.lda[m], ldn, n, tk, np, tm, tm1};
                     ProfScope pp("hess_prep16", s, 0.0, 0.0);
                     f16r = HessF16<T>::prepare(s, ha, hp);
                 }
+                // tangent-row ranges of block k to generate: everything left (whole
+                // assembly), or the band's weight rows and bias rows, stored at the
+                // band's row offsets without mirrors
+                struct JRange { int64_t lo, hi, rlo, rhi, rsh; };
+                std::vector<JRange> ranges;
+                if (band) {
+                    const int64_t u0 = band->u0[k], u1 = band->u1[k];
+                    ranges.push_back({u0 * tk, u1 * tk, md.woff[k] + u0 * tk, md.woff[k] + u1 * tk,
+                                      md.woff[k] + u0 * tk - band->bw[k]});
+                    ranges.push_back({nw + u0, nw + u1, md.boff[k] + u0, md.boff[k] + u1, md.boff[k] + u0 - band->bb[k]});
+                } else {
+                    ranges.push_back({jbeg, Pk, rlo, rhi, 0});
+                }
+                int64_t span = 0;
+                for (const JRange& r : ranges) span = std::max(span, r.hi - r.lo);
                 int64_t J = (int64_t)((rgen_tc ? size_t(2) << 30 : chunk_bytes) / ((size_t)tm1 * ldr * sizeof(T)));
                 J = std::max<int64_t>(128, J / 128 * 128);
-                J = std::min<int64_t>(J, round_up(Pk - jbeg, 128));
-                DevMem rbuf((size_t)tm1 * J * ldr * sizeof(T), s);
-                for (int64_t j0 = jbeg; j0 < Pk; j0 += J) {
-                    const int64_t Jc = std::min<int64_t>(J, Pk - j0);
+                J = std::min<int64_t>(J, round_up(span, 128));
+                DevMem rbuf(span > 0 ? (size_t)tm1 * J * ldr * sizeof(T) : 0, s);
+                for (const JRange& jr : ranges)
+                for (int64_t j0 = jr.lo; j0 < jr.hi; j0 += J) {
+                    const int64_t Jc = std::min<int64_t>(J, jr.hi - j0);
+                    const int64_t rlo = jr.rlo, rhi = jr.rhi;
+                    const int mirror = band ? 0 : ((m == k && verify) ? 0 : 1);
                     if (md.woff[k] + j0 + Jc <= rlo || md.woff[k] + j0 >= rhi) continue;  // no owned row
                     // R rows (o'', jj) whose block entries are all above the
                     // diagonal are neither generated nor multiplied
@@ -792,14 +822,14 @@ struct Engine {
                     const int64_t rows = opp_hi * Jc;
                     if (f16r && rows >= 512) {
                         EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
-                                     m == k ? 1 : 0, (m == k && verify) ? 0 : 1, rlo, rhi};
+                                     m == k ? 1 : 0, mirror, rlo, rhi, jr.rsh};
                         const double req = Profiler::get().on ? hess_required_entries(k, m, j0, Jc) : 0.0;
                         DevMem r16, rinv;
                         HessF16<T>::chunk(s, ha, hp, j0, Jc, opp_hi, r16, rinv, e, req);
                         continue;
                     }
                     RGenArgs<T> g{m == k ? GT : PT[m], m == k ? nullptr : QT[m], akT, dkT, ldn, n, tk, np, tm1,
-                                  j0, Jc, rows, dptr<T>(rbuf), ldr, rgen_tc ? 1 : 0};
+                                  j0, Jc, rows, dptr<T>(rbuf), ldr, rgen_tc ? 1 : 0, t0};
                     {
                         ProfScope ps("hess_rgen", s, 0.0, (double)sizeof(T) * rows * ldr);
                         const dim3 grid((unsigned)ceil_div(ldr / 4, 256),
@@ -808,7 +838,7 @@ struct Engine {
                         CK_LAUNCH();
                     }
                     EpiHess<T> e{H, ldh, Jc, j0, md.woff[k], md.woff[m], md.boff[m], tm, T(1) / T(n),
-                                 m == k ? 1 : 0, (m == k && verify) ? 0 : 1, rlo, rhi};
+                                 m == k ? 1 : 0, mirror, rlo, rhi, jr.rsh};
                     // algorithmic work is counted only while profiling (host loop)
                     const double req = Profiler::get().on ? hess_required_entries(k, m, j0, Jc) : 0.0;
                     ProfScope ps("hess_gemm", s, 2.0 * (double)n * req, (double)sizeof(T) * ((double)rows * ldr + req));

@@ -416,6 +416,7 @@ struct EpiRback {
     int unit_prof;  // 1: rz is e_{row/n} (profile tangent layer)
     int finalize;   // 0: store raw acc (first of two GEMMs); 1: acc(+out) then apply
     int accum;
+    int64_t o0 = 0;  // unit_prof: row block b holds the tangent of unit o0 + b (unit bands)
     __device__ bool skip(int, int64_t, int64_t, int64_t, int64_t) const { return false; }
     __device__ void operator()(int, int64_t r, int64_t c, T acc) const {
         T v = acc;
@@ -424,7 +425,7 @@ struct EpiRback {
             const int64_t e = r % n;
             const T zz = z[e * ldz + c];
             T rzv = T(0);
-            if (unit_prof) rzv = (c == r / n) ? T(1) : T(0);
+            if (unit_prof) rzv = (c == o0 + r / n) ? T(1) : T(0);
             else if (rz) rzv = rz[r * ldr + c];
             v = v * act_deriv<T>(act, zz) + (up ? up[e * ldz + c] * act_second<T>(act, zz) * rzv : T(0));
         }
@@ -432,25 +433,26 @@ struct EpiRback {
     }
 };
 
-// prof[o][n][t] = act'(z_k[n][o]) * W_{k+1}[t][o]   (R-forward one step above
-// the tangent layer for rz_k = e_o)
+// prof[o - o0][n][t] = act'(z_k[n][o]) * W_{k+1}[t][o]   (R-forward one step above
+// the tangent layer for rz_k = e_o), tangents o in [o0, o0 + no)
 template <class T>
 __global__ void profile_first_rz_kernel(const T* __restrict__ zk, int64_t ldz, const T* __restrict__ W1,
                                         int64_t t1, int64_t t2, int64_t n, int act, T* __restrict__ out,
-                                        int64_t ldo) {
+                                        int64_t ldo, int64_t o0, int64_t no) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= t1 * n * t2) return;
-    const int64_t t = idx % t2, r = idx / t2, o = r / n, e = r % n;
+    if (idx >= no * n * t2) return;
+    const int64_t t = idx % t2, r = idx / t2, o = o0 + r / n, e = r % n;
     out[r * ldo + t] = act_deriv<T>(act, zk[e * ldz + o]) * W1[t * t1 + o];
 }
 
-// G_{S-1}[o][n][t] = p_t (delta_{to} - p_o): output-layer Hessian columns
+// G_{S-1}[o - o0][n][t] = p_t (delta_{to} - p_o): output-layer Hessian columns,
+// tangents o in [o0, o0 + no)
 template <class T>
 __global__ void profile_output_kernel(const T* __restrict__ prob, int64_t ldp, int64_t tl, int64_t n, int mode,
-                                      T* __restrict__ out, int64_t ldo) {
+                                      T* __restrict__ out, int64_t ldo, int64_t o0, int64_t no) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= tl * n * tl) return;
-    const int64_t t = idx % tl, r = idx / tl, o = r / n, e = r % n;
+    if (idx >= no * n * tl) return;
+    const int64_t t = idx % tl, r = idx / tl, o = o0 + r / n, e = r % n;
     T v = T(0);
     if (mode == kSoftmaxCE) {
         const T pt = prob[e * ldp + t], po = prob[e * ldp + o];
@@ -477,7 +479,7 @@ __global__ void profile_q_kernel(const T* __restrict__ z, int64_t ldz, int64_t t
 // ---------------------------------------------------------------------------
 template <class T>
 struct RGenArgs {
-    const T* prof;  // G (m == k) or Pm, transposed: [T_{k+1}][T_{m+1}][ldn]
+    const T* prof;  // G (m == k) or Pm, transposed: [T_{k+1} - o0][T_{m+1}][ldn]
     const T* q;     // Qm transposed [T_k][T_{m+1}][ldn], or null
     const T* akT;   // a_k transposed [T_k + 1][ldn]
     const T* dkT;   // delta_k transposed [T_{k+1}][ldn]
@@ -487,6 +489,7 @@ struct RGenArgs {
     T* R;
     int64_t ldr;
     int round = 0;                // store R rounded to nearest TF32 (the tensor-core GEMM's A operand)
+    int64_t o0 = 0;               // prof holds the tangents of units o0, o0 + 1, ... (unit bands)
 };
 
 // CTA (x: a 256-wide slice of the 4-example groups along n, y: a segment of
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(256) rgen_kernel(RGenArgs<T> g) {
             const int64_t o = wt ? j / g.tink : j - nw;
             const int64_t i = wt ? j - o * g.tink : 0;
             if (o != last_o || !wt) {
-                p = reinterpret_cast<const V*>(g.prof + (o * g.tm1 + opp) * g.ldn)[e];
+                p = reinterpret_cast<const V*>(g.prof + ((o - g.o0) * g.tm1 + opp) * g.ldn)[e];
                 if (g.q) d = reinterpret_cast<const V*>(g.dkT + o * g.ldn)[e];
                 last_o = wt ? o : -1;
             }

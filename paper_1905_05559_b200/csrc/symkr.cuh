@@ -584,12 +584,15 @@ inline CUtensorMap make_map_orbit(float* base, int64_t d0, int64_t d1, int64_t d
     return m;
 }
 
-// out[j][.] = tf32(src[(o_j * U + o''_j)][.])  -- packed profile rows
+// out[j][.] = tf32(src[(o_j * U + o''_j)][.])  -- packed profile rows; t0 >= 0: src
+// holds the tangents of units t0, t0 + 1, ... only and the symmetric entry
+// src[((o''_j - t0) * U + o_j)] is read instead (unit bands)
 __global__ void pack_profile_kernel(const float* __restrict__ src, const int4* __restrict__ pairs, int64_t U,
-                                    int64_t ldn, float* __restrict__ out, int64_t npairs) {
+                                    int64_t ldn, float* __restrict__ out, int64_t npairs, int64_t t0) {
     for (int64_t j = blockIdx.y; j < npairs; j += gridDim.y) {  // grid.y <= 65535
         const int4 pr = pairs[j];
-        const float4* s = reinterpret_cast<const float4*>(src + (pr.x * U + pr.y) * ldn);
+        const int64_t row = t0 < 0 ? pr.x * U + pr.y : (pr.y - t0) * U + pr.x;
+        const float4* s = reinterpret_cast<const float4*>(src + row * ldn);
         float4* d = reinterpret_cast<float4*>(out + j * ldn);
         for (int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < ldn / 4; q += gridDim.x * blockDim.x) {
             float4 v = s[q];
@@ -662,11 +665,13 @@ __global__ void zscale_kernel(const float* __restrict__ akT, int64_t rows, int64
 // (o_j U + o''_j) or delta_o delta_o''; one CTA per packed column, two passes
 template <bool DELTA>
 __global__ void pack_h_kernel(const float* __restrict__ src, const int4* __restrict__ pairs, int64_t U, int64_t n,
-                              int64_t ldn, __half* __restrict__ out, float* __restrict__ pscale, int64_t npairs) {
+                              int64_t ldn, __half* __restrict__ out, float* __restrict__ pscale, int64_t npairs,
+                              int64_t t0) {
     __shared__ float red[32];
     for (int64_t j = blockIdx.x; j < npairs; j += gridDim.x) {
         const int4 pr = pairs[j];
-        const float* a = DELTA ? src + pr.x * ldn : src + (pr.x * U + pr.y) * ldn;
+        const float* a = DELTA ? src + pr.x * ldn
+                               : src + (t0 < 0 ? pr.x * U + pr.y : (pr.y - t0) * U + pr.x) * ldn;
         const float* b = src + pr.y * ldn;
         auto val = [&](int64_t q) { return q < n ? (DELTA ? a[q] * b[q] : a[q]) : 0.f; };
         float m = 0.f;
@@ -957,9 +962,10 @@ struct SymKr<float> {
         if (f16) {
             const unsigned g = (unsigned)std::min<int64_t>(np, 8 * tc::num_sms());
             if (a.delta_products)
-                tc::pack_h_kernel<true><<<g, 256, 0, s>>>(a.prof, dpairs, U, a.n, a.ldn, dptr<__half>(pi), dptr<float>(psc), np);
+                tc::pack_h_kernel<true><<<g, 256, 0, s>>>(a.prof, dpairs, U, a.n, a.ldn, dptr<__half>(pi), dptr<float>(psc), np, -1);
             else
-                tc::pack_h_kernel<false><<<g, 256, 0, s>>>(a.prof, dpairs, U, a.n, a.ldn, dptr<__half>(pi), dptr<float>(psc), np);
+                tc::pack_h_kernel<false><<<g, 256, 0, s>>>(a.prof, dpairs, U, a.n, a.ldn, dptr<__half>(pi), dptr<float>(psc), np,
+                                                           a.prof_t0);
             CK_LAUNCH();
             tc::zscale_kernel<<<(unsigned)std::min<int64_t>(nb * 16, 4096), 256, 0, s>>>(a.akT, tk + 1, a.n, a.ldn,
                                                                                          dptr<float>(zsc), nb * 16);
@@ -968,7 +974,7 @@ struct SymKr<float> {
                 a.prof, dpairs, a.ldn, dptr<float>(pi), np);
         else
             tc::pack_profile_kernel<<<dim3((unsigned)ceil_div(a.ldn / 4, 256), (unsigned)std::min<int64_t>(np, 65535)), 256, 0, s>>>(
-                a.prof, dpairs, U, a.ldn, dptr<float>(pi), np);
+                a.prof, dpairs, U, a.ldn, dptr<float>(pi), np, a.prof_t0);
         CK_LAUNCH();
         CUtensorMap m8 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 8);
         CUtensorMap m16 = tc::make_map(a.akT, tk + 1, a.n, a.ldn, 0, 16);
