@@ -319,6 +319,43 @@ int curvkit_dev_jacobian_apply(const curvkit_model* model, const void* params, c
                                int64_t n, int32_t precision, int64_t p_begin, int64_t p_end, int32_t transpose,
                                const void* in, int64_t ld_in, int64_t l, void* out, int64_t ld_out, void* stream);
 
+/* ---- operators on eigenpairs (eigensolve.hpp:14-20, 83-101) -------------------
+ * Q is p x k (row-major: pairs.q), lambda k values.  full_rank = 0: the
+ * low-rank operator A = Q diag(lambda) Q^T (curv::low_rank_materialize /
+ * low_rank_apply / low_rank_quadform, eigensolve.cpp:278-307); full_rank = 1:
+ * its full-rank extension A = Q diag(lambda) Q^T + lambda_tilde (I - Q Q^T)
+ * (curv::full_rank_materialize / full_rank_apply / full_rank_quadform,
+ * eigensolve.cpp:309-348; ContractError unless lambda_tilde > 0).
+ *
+ * curvkit_eig_validate: curv::validate_eigen_pairs (eigensolve.cpp:11-30):
+ * ShapeError when lambda_len != k or k > p; ContractError when lambda is not
+ * descending or max |Q^T Q - I| > ortho_tol (fp64 Gram on the device).
+ *
+ * curvkit_eig_materialize: h_out (p x p, dense) = A; ContractError when
+ * p > memory_cap (eigensolve.cpp:255-261).  One symmetric tensor-core GEMM
+ * (lower tiles, mirrored: the result is exactly symmetric).
+ *
+ * curvkit_eig_apply: for each of the nvec vectors x[v] (x is nvec x p
+ * row-major; x_len = the caller's vector length, ShapeError unless it equals
+ * p): y_out[v] = A x[v] (skipped when y_out is null) and quad_out[v] =
+ * x[v]^T A x[v] (skipped when null).  Two passes over Q per four vectors.
+ *
+ * The device variants take q (leading dimension ldq), lambda, x, y and h in
+ * the precision's storage type; quad is always fp64 (device memory). */
+int curvkit_eig_validate(int64_t p, int64_t k, const double* q, const double* lambda, int64_t lambda_len,
+                         double ortho_tol);
+int curvkit_eig_materialize(int64_t p, int64_t k, const double* q, const double* lambda, int32_t full_rank,
+                            double lambda_tilde, int64_t memory_cap, int32_t precision, double* h_out);
+int curvkit_eig_apply(int64_t p, int64_t k, const double* q, const double* lambda, int32_t full_rank,
+                      double lambda_tilde, int64_t nvec, const double* x, int64_t x_len, int32_t precision,
+                      double* y_out, double* quad_out);
+int curvkit_dev_eig_materialize(int64_t p, int64_t k, const void* q, int64_t ldq, const void* lambda,
+                                int32_t full_rank, double lambda_tilde, int32_t precision, void* h, int64_t ldh,
+                                void* stream);
+int curvkit_dev_eig_apply(int64_t p, int64_t k, const void* q, int64_t ldq, const void* lambda, int32_t full_rank,
+                          double lambda_tilde, int64_t nvec, const void* x, int64_t ldx, void* y, int64_t ldy,
+                          double* quad, int32_t precision, void* stream);
+
 /* The curvature GEMM engine on its own (fp32 storage): C[m][n] = alpha *
  * sum_k A(m,k) B(n,k) with A(m,k) = a[m*lda+k] if a_kmajor else a[k*lda+m]
  * (likewise B).  TF32/TF32X3 run the tcgen05 kernel, F32 the SIMT one. */

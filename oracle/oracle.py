@@ -167,6 +167,12 @@ class Ref(_Lib):
         lib.ref_opg_rows_from_jacobian.argtypes = [_dp, i64, i64, i64, i64, i64, _dp]
         lib.ref_hessian_sketch.argtypes = mdl + [_dp, i64, i64, _dp]
         lib.ref_opg_sketch.argtypes = mdl + [_dp, i64, i64, _dp]
+        lib.ref_eig_ops.argtypes = [_dp, _dp, i64, i64, C.c_int, C.c_double, i64, C.c_void_p, i64, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]
+        lib.ref_validate_eigen_pairs.argtypes = [_dp, i64, i64, _dp, i64, C.c_double]
+        lib.ref_default_lambda_tilde.argtypes = [_dp, i64, C.POINTER(C.c_double)]
+        for f in ("ref_eig_ops", "ref_validate_eigen_pairs", "ref_default_lambda_tilde"):
+            getattr(lib, f).restype = C.c_int
         for f in ("ref_hessian", "ref_opg", "ref_hessian_columns_sample", "ref_opg_rows_sample",
                   "ref_hvp_operator_apply", "ref_forward", "ref_opg_eigs_incremental", "ref_hessian_lanczos",
                   "ref_opg_rows_from_jacobian", "ref_hessian_sketch", "ref_opg_sketch"):
@@ -266,3 +272,58 @@ class Ref(_Lib):
         lam = np.zeros(k)
         self._call("opg_eigs_incremental", J, n, p, block, k, q, lam)
         return lam, q
+
+    def eig_ops(self, q, lam, x=None, lambda_tilde=None, materialize=False, memory_cap=4096):
+        """The reference's low-rank (lambda_tilde None) or full-rank operators
+        (eigensolve.cpp:278-348): returns (H or None, A x or None, x^T A x or None)."""
+        q, lam = _f64(q), _f64(lam)
+        p, k = q.shape
+        full = lambda_tilde is not None
+        h = np.zeros((p, p)) if materialize else None
+        xv = _f64(x) if x is not None else None
+        y = np.zeros(xv.shape[0]) if xv is not None else None
+        quad = C.c_double() if xv is not None else None
+        vp = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None  # noqa: E731
+        self._call("eig_ops", q, lam, p, k, 1 if full else 0, float(lambda_tilde) if full else 0.0, memory_cap,
+                   vp(xv), xv.shape[0] if xv is not None else 0, vp(h), vp(y),
+                   C.cast(C.byref(quad), C.c_void_p) if quad is not None else None)
+        return h, y, (quad.value if quad is not None else None)
+
+    def validate_eigen_pairs(self, q, lam, ortho_tol=1e-8):
+        q, lam = _f64(q), _f64(lam)
+        self._call("validate_eigen_pairs", q, q.shape[0], q.shape[1], lam, lam.shape[0], ortho_tol)
+
+    def default_lambda_tilde(self, lam):
+        lam = _f64(lam)
+        out = C.c_double()
+        self._call("default_lambda_tilde", lam, lam.shape[0], C.byref(out))
+        return out.value
+
+
+# ---- numpy restatement of the eigenpair operators (the "port") -----------------
+# Pinned against the reference by tests/golden/eigops.npz (tests/test_oracle_pins.py).
+
+def eig_materialize_port(q, lam, lambda_tilde=None):
+    """eigensolve.cpp:278-292 (sum_c lambda_c q_c q_c^T) and :309-327
+    (minus lambda_tilde q_c q_c^T per column, plus lambda_tilde on the diagonal)."""
+    q, lam = _f64(q), _f64(lam)
+    h = np.zeros((q.shape[0], q.shape[0]))
+    for c in range(q.shape[1]):
+        h += lam[c] * np.outer(q[:, c], q[:, c])
+    if lambda_tilde is not None:
+        for c in range(q.shape[1]):
+            h -= lambda_tilde * np.outer(q[:, c], q[:, c])
+        h[np.diag_indices_from(h)] += lambda_tilde
+    return h
+
+
+def eig_apply_port(q, lam, x, lambda_tilde=None):
+    """(A x, x^T A x): eigensolve.cpp:294-305 (low rank), :329-350 (full rank)."""
+    q, lam, x = _f64(q), _f64(lam), _f64(x)
+    t = q.T @ x  # project(): eigensolve.cpp:263-269
+    y = q @ (lam * t)
+    quad = float(np.sum(lam * t * t))
+    if lambda_tilde is not None:
+        y = y + lambda_tilde * (x - q @ t)
+        quad = quad + lambda_tilde * float(x @ x) - lambda_tilde * float(t @ t)
+    return y, quad

@@ -388,4 +388,44 @@ int ref_hessian_lanczos(const int64_t* w, int L, int act, int mode, const double
     });
 }
 
+// The consumers of eigenpairs on the reference itself (eigensolve.cpp:11-30,
+// 278-358).  full = 0: low_rank_*; 1: full_rank_* with lambda_tilde.  h (p x p),
+// y (xlen) and quad are each skipped when null; x may be null when only h is
+// wanted.  The reference's own ShapeError / ContractError come back as rc 1 / 2.
+int ref_eig_ops(const double* q, const double* lambda, int64_t p, int64_t k, int full, double lambda_tilde,
+                int64_t memory_cap, const double* x, int64_t xlen, double* h, double* y, double* quad) {
+    return guard([&] {
+        EigenPairs e{DenseMatrix(p, k, std::vector<double>(q, q + p * k)),
+                     DenseVector(std::vector<double>(lambda, lambda + k))};
+        if (h) {
+            const DenseMatrix m = full ? full_rank_materialize(e, lambda_tilde, (std::size_t)memory_cap)
+                                       : low_rank_materialize(e, (std::size_t)memory_cap);
+            std::memcpy(h, m.data(), sizeof(double) * p * p);
+        }
+        if (!x) return;
+        const DenseVector xv(std::vector<double>(x, x + xlen));
+        if (quad) *quad = full ? full_rank_quadform(e, lambda_tilde, xv) : low_rank_quadform(e, xv);
+        if (y) {
+            const DenseVector r = full ? full_rank_apply(e, lambda_tilde, xv) : low_rank_apply(e, xv);
+            std::memcpy(y, r.data(), sizeof(double) * r.len());
+        }
+    });
+}
+
+int ref_validate_eigen_pairs(const double* q, int64_t p, int64_t k, const double* lambda, int64_t lambda_len,
+                             double ortho_tol) {
+    return guard([&] {
+        EigenPairs e{DenseMatrix(p, k, std::vector<double>(q, q + p * k)),
+                     DenseVector(std::vector<double>(lambda, lambda + lambda_len))};
+        validate_eigen_pairs(e, ortho_tol);
+    });
+}
+
+int ref_default_lambda_tilde(const double* lambda, int64_t k, double* out) {
+    return guard([&] {
+        EigenPairs e{DenseMatrix(std::max<int64_t>(k, 1), k, 0.0), DenseVector(std::vector<double>(lambda, lambda + k))};
+        *out = default_lambda_tilde(e);
+    });
+}
+
 }  // extern "C"

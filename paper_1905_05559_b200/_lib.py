@@ -81,6 +81,11 @@ SIGNATURES = {
     "curvkit_cost": [_MP, dptr, dptr, dptr, i64, i32, dptr],
     "curvkit_opg_topk_from_jacobian": [dptr, i64, i64, i64, i64, i64, u64, i32, dptr, dptr],
     "curvkit_dev_opg_topk_from_jacobian": [vptr, i64, i64, i64, i64, i64, i64, u64, i32, vptr, vptr, vptr],
+    "curvkit_eig_validate": [i64, i64, dptr, dptr, i64, C.c_double],
+    "curvkit_eig_materialize": [i64, i64, dptr, dptr, i32, C.c_double, i64, i32, dptr],
+    "curvkit_eig_apply": [i64, i64, dptr, dptr, i32, C.c_double, i64, dptr, i64, i32, dptr, dptr],
+    "curvkit_dev_eig_materialize": [i64, i64, vptr, i64, vptr, i32, C.c_double, i32, vptr, i64, vptr],
+    "curvkit_dev_eig_apply": [i64, i64, vptr, i64, vptr, i32, C.c_double, i64, vptr, i64, vptr, i64, dptr, i32, vptr],
     "curvkit_hessian_topk_lanczos": [_MP, dptr, dptr, dptr, i64, i64, i64, i64, C.c_double, u64, i32, dptr, dptr, dptr,
                                      C.POINTER(i64)],
 }

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "curvature.cuh"
 #include "eigen.cuh"
+#include "eigops.cuh"
 #include "lanczos.cuh"
 #include "gemm_tc.cuh"
 #include "incremental.cuh"
@@ -477,6 +478,46 @@ void host_forward_cost(const ModelDesc& md, const double* params, const double* 
 
 }  // namespace
 
+// ---- helpers of the eigenpair operators (eigensolve.cpp:253-275) ---------------
+namespace {
+
+void check_eig_shape(int64_t p, int64_t k, const void* q, const void* lambda, const char* who) {
+    if (p < 1 || k < 0 || k > p) shape(std::string(who) + ": bad eigenpair shape");
+    if (k > 0 && (!q || !lambda)) contract(std::string(who) + ": null eigenpairs");
+}
+
+void check_lambda_tilde(int32_t full_rank, double lambda_tilde) {  // eigensolve.cpp:271-275
+    if (full_rank && !(lambda_tilde > 0.0))
+        contract("full-rank approximation requires lambda_tilde > 0, got " + std::to_string(lambda_tilde));
+}
+
+void check_dense_cap(int64_t p, int64_t cap, const char* who) {  // eigensolve.cpp:255-261
+    if (p > cap)
+        contract(std::string(who) + ": P = " + std::to_string(p) + " exceeds the dense memory cap " +
+                 std::to_string(cap) + "; use the implicit quadform/apply forms instead");
+}
+
+// host doubles (rows x cols, dense) -> device T (rows x ld)
+template <class T>
+DevMem upload_as(const double* h, int64_t rows, int64_t cols, int64_t ld, cudaStream_t s) {
+    DevMem out((size_t)std::max<int64_t>(1, rows * ld) * sizeof(T), s);
+    if (rows * cols == 0) return out;
+    if (std::is_same_v<T, double> && ld == cols) {
+        CK_CUDA(cudaMemcpyAsync(out.p, h, (size_t)rows * cols * sizeof(double), cudaMemcpyHostToDevice, s));
+        return out;
+    }
+    DevMem st((size_t)rows * cols * sizeof(double), s);
+    CK_CUDA(cudaMemcpyAsync(st.p, h, (size_t)rows * cols * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (ld != cols) CK_CUDA(cudaMemsetAsync(out.p, 0, (size_t)rows * ld * sizeof(T), s));
+    convert_rows_kernel<double, T><<<blocks_for(rows * cols), 256, 0, s>>>(dptr<double>(st), cols, dptr<T>(out), ld,
+                                                                           rows, cols);
+    CK_LAUNCH();
+    CK_CUDA(cudaStreamSynchronize(s));  // st is released in stream order, h may be pageable
+    return out;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* curvkit_last_error(void) { return g_err.c_str(); }
@@ -828,6 +869,120 @@ int curvkit_dev_symmetrize_units(const curvkit_model* model, int32_t precision, 
         cudaStream_t s = dev_stream(stream);
         if (is_f64(precision)) symmetrize_units<double>(md, (double*)full, ldf, s);
         else symmetrize_units<float>(md, (float*)full, ldf, s);
+    });
+}
+
+// ---- operators on eigenpairs (eigensolve.cpp:11-30, 253-358) -----------------
+
+int curvkit_eig_validate(int64_t p, int64_t k, const double* q, const double* lambda, int64_t lambda_len,
+                         double ortho_tol) {
+    return guard([&] {
+        if (lambda_len != k) shape("EigenPairs: lambda length does not match column count");
+        if (k > p) shape("EigenPairs: more columns than rows");
+        if (k < 0 || p < 0) shape("EigenPairs: bad shape");
+        if (k == 0) return;
+        if (!q || !lambda) contract("EigenPairs: null eigenpairs");
+        for (int64_t i = 0; i + 1 < k; ++i)
+            if (lambda[i] < lambda[i + 1]) contract("EigenPairs: eigenvalues not sorted descending");
+        cudaStream_t s = lib_stream();
+        DevMem qd = upload_as<double>(q, p, k, k, s);
+        const double err = eigops::ortho_error<double>(s, p, k, dptr<double>(qd), k);
+        if (!(err <= ortho_tol)) contract("EigenPairs: columns are not orthonormal");
+    });
+}
+
+int curvkit_eig_materialize(int64_t p, int64_t k, const double* q, const double* lambda, int32_t full_rank,
+                            double lambda_tilde, int64_t memory_cap, int32_t precision, double* h_out) {
+    return guard([&] {
+        const char* who = full_rank ? "full_rank_materialize" : "low_rank_materialize";
+        check_lambda_tilde(full_rank, lambda_tilde);
+        check_eig_shape(p, k, q, lambda, who);
+        check_dense_cap(p, memory_cap, who);
+        if (!h_out) contract(std::string(who) + ": null output");
+        const bool f64 = is_f64(precision);
+        cudaStream_t s = lib_stream();
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t ldq = round_up(std::max<int64_t>(k, 1), 4), ldh = round_up(p, 4);
+            DevMem qd = upload_as<T>(q, p, k, ldq, s), ld = upload_as<T>(lambda, 1, k, k, s);
+            DevMem H((size_t)p * ldh * sizeof(T), s);
+            if (k == 0) CK_CUDA(cudaMemsetAsync(H.p, 0, (size_t)p * ldh * sizeof(T), s));
+            eigops::materialize<T>(precision, s, p, k, dptr<T>(qd), ldq, dptr<T>(ld), full_rank != 0, lambda_tilde,
+                                   dptr<T>(H), ldh);
+            download<T, double>(dptr<T>(H), ldh, p, p, h_out, s);
+        };
+        if (f64) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_eig_apply(int64_t p, int64_t k, const double* q, const double* lambda, int32_t full_rank,
+                      double lambda_tilde, int64_t nvec, const double* x, int64_t x_len, int32_t precision,
+                      double* y_out, double* quad_out) {
+    return guard([&] {
+        check_lambda_tilde(full_rank, lambda_tilde);
+        check_eig_shape(p, k, q, lambda, "eigen operator");
+        if (x_len != p)  // eigensolve.cpp:263-269
+            shape("eigen operator: vector length " + std::to_string(x_len) + " does not match P = " +
+                  std::to_string(p));
+        if (nvec < 1) return;
+        if (!x) contract("eigen operator: null vector");
+        const bool f64 = is_f64(precision);
+        cudaStream_t s = lib_stream();
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t ldq = round_up(std::max<int64_t>(k, 1), 4);
+            DevMem qd = upload_as<T>(q, p, k, ldq, s), ld = upload_as<T>(lambda, 1, k, k, s);
+            DevMem xd = upload_as<T>(x, nvec, p, p, s);
+            DevMem yd((size_t)(y_out ? nvec * p : 1) * sizeof(T), s), qf((size_t)nvec * sizeof(double), s);
+            eigops::apply<T>(s, p, k, dptr<T>(qd), ldq, dptr<T>(ld), full_rank != 0, lambda_tilde, nvec, dptr<T>(xd),
+                             p, y_out ? dptr<T>(yd) : nullptr, p, quad_out ? dptr<double>(qf) : nullptr);
+            if (y_out) download<T, double>(dptr<T>(yd), p, nvec, p, y_out, s);
+            if (quad_out) {
+                CK_CUDA(cudaMemcpyAsync(quad_out, qf.p, (size_t)nvec * sizeof(double), cudaMemcpyDeviceToHost, s));
+                CK_CUDA(cudaStreamSynchronize(s));
+            }
+        };
+        if (f64) run(double{});
+        else run(float{});
+    });
+}
+
+int curvkit_dev_eig_materialize(int64_t p, int64_t k, const void* q, int64_t ldq, const void* lambda,
+                                int32_t full_rank, double lambda_tilde, int32_t precision, void* h, int64_t ldh,
+                                void* stream) {
+    return guard([&] {
+        const char* who = full_rank ? "full_rank_materialize" : "low_rank_materialize";
+        check_lambda_tilde(full_rank, lambda_tilde);
+        check_eig_shape(p, k, q, lambda, who);
+        if (!h || ldh < p || ldq < k) shape(std::string(who) + ": bad leading dimension or null output");
+        const bool f64 = is_f64(precision);
+        cudaStream_t s = dev_stream(stream);
+        if (k == 0) CK_CUDA(cudaMemsetAsync(h, 0, (size_t)p * ldh * (f64 ? 8 : 4), s));
+        if (f64)
+            eigops::materialize<double>(precision, s, p, k, (const double*)q, ldq, (const double*)lambda, full_rank != 0,
+                                        lambda_tilde, (double*)h, ldh);
+        else
+            eigops::materialize<float>(precision, s, p, k, (const float*)q, ldq, (const float*)lambda, full_rank != 0,
+                                       lambda_tilde, (float*)h, ldh);
+    });
+}
+
+int curvkit_dev_eig_apply(int64_t p, int64_t k, const void* q, int64_t ldq, const void* lambda, int32_t full_rank,
+                          double lambda_tilde, int64_t nvec, const void* x, int64_t ldx, void* y, int64_t ldy,
+                          double* quad, int32_t precision, void* stream) {
+    return guard([&] {
+        check_lambda_tilde(full_rank, lambda_tilde);
+        check_eig_shape(p, k, q, lambda, "eigen operator");
+        if (nvec < 1) return;
+        if (!x || ldx < p || ldq < k || (y && ldy < p)) shape("eigen operator: bad leading dimension or null vector");
+        cudaStream_t s = dev_stream(stream);
+        if (is_f64(precision))
+            eigops::apply<double>(s, p, k, (const double*)q, ldq, (const double*)lambda, full_rank != 0, lambda_tilde,
+                                  nvec, (const double*)x, ldx, (double*)y, ldy, quad);
+        else
+            eigops::apply<float>(s, p, k, (const float*)q, ldq, (const float*)lambda, full_rank != 0, lambda_tilde,
+                                 nvec, (const float*)x, ldx, (float*)y, ldy, quad);
     });
 }
 

@@ -484,54 +484,85 @@ def dev_opg_topk_from_jacobian(J, ldj, n, p, k, oversample, power_iters, seed, q
                                                                _stream(stream)))
 
 
-# ---- low/full-rank operators from eigenpairs (eigensolve.hpp:83-97) ------------
+# ---- low/full-rank operators from eigenpairs (eigensolve.hpp:83-101) -----------
+# All of them run on the device through the C-ABI (curvkit_eig_*): the Gram of
+# validate, the symmetric GEMM of materialize, the two passes over Q of
+# apply / quadform.  Shape and contract errors are raised by the library with the
+# reference's text (eigensolve.cpp:11-30, 255-275).
+
+def _pairs(pairs: EigenPairs):
+    q = np.ascontiguousarray(pairs.q, dtype=np.float64)
+    lam = np.ascontiguousarray(pairs.lam, dtype=np.float64).reshape(-1)
+    if q.ndim != 2:
+        raise ShapeError("EigenPairs: q must be a P x K matrix")
+    return q, lam
+
 
 def validate_eigen_pairs(pairs: EigenPairs, ortho_tol: float = 1e-8) -> None:
     """curv::validate_eigen_pairs (eigensolve.cpp:11-30): lambda length,
     descending order and column orthonormality within ortho_tol."""
-    q = np.asarray(pairs.q, dtype=np.float64)
-    lam = np.asarray(pairs.lam, dtype=np.float64)
+    q, lam = _pairs(pairs)
+    p, k = q.shape
+    _lib.check(_lib.load().curvkit_eig_validate(p, k, _p(q), _p(lam), lam.shape[0], float(ortho_tol)))
+
+
+def _materialize(pairs, full, lambda_tilde, memory_cap, precision):
+    q, lam = _pairs(pairs)
     p, k = q.shape
     if lam.shape[0] != k:
         raise ShapeError("EigenPairs: lambda length does not match column count")
-    if k > p:
-        raise ShapeError("EigenPairs: more columns than rows")
-    if np.any(lam[:-1] < lam[1:]):
-        raise ContractError("EigenPairs: eigenvalues not sorted descending")
-    if k and np.abs(q.T @ q - np.eye(k)).max() > ortho_tol:
-        raise ContractError("EigenPairs: columns are not orthonormal")
+    # the dense-cap refusal comes first in the library; allocate only when it will pass
+    out = np.empty((p, p) if p <= memory_cap and (not full or lambda_tilde > 0.0) else (0, 0), dtype=np.float64)
+    _lib.check(_lib.load().curvkit_eig_materialize(p, k, _p(q), _p(lam), 1 if full else 0, float(lambda_tilde),
+                                                   int(memory_cap), _prec(precision), _p(out)))
+    return out
 
 
-def _check_dense_cap(p: int, memory_cap: int, who: str):  # eigensolve.cpp:255-261
-    if p > memory_cap:
-        raise ContractError(f"{who}: P = {p} exceeds the dense memory cap {memory_cap}; "
-                            "use the implicit quadform/apply forms instead")
+def low_rank_materialize(pairs: EigenPairs, memory_cap: int = 4096, precision: str = "f64") -> np.ndarray:
+    """curv::low_rank_materialize (eigensolve.cpp:278-292): Q diag(lambda) Q^T."""
+    return _materialize(pairs, False, 0.0, memory_cap, precision)
 
 
-def low_rank_materialize(pairs: EigenPairs, memory_cap: int = 4096) -> np.ndarray:
-    """curv::low_rank_materialize (eigensolve.cpp): Q diag(lambda) Q^T."""
-    q = np.asarray(pairs.q, dtype=np.float64)
-    _check_dense_cap(q.shape[0], memory_cap, "low_rank_materialize")
-    return (q * np.asarray(pairs.lam)) @ q.T
+def full_rank_materialize(pairs: EigenPairs, lambda_tilde: float, memory_cap: int = 4096,
+                          precision: str = "f64") -> np.ndarray:
+    """curv::full_rank_materialize (eigensolve.cpp:309-327):
+    Q diag(lambda) Q^T + lambda_tilde (I - Q Q^T)."""
+    return _materialize(pairs, True, lambda_tilde, memory_cap, precision)
 
 
-def full_rank_materialize(pairs: EigenPairs, lambda_tilde: float, memory_cap: int = 4096) -> np.ndarray:
-    """curv::full_rank_materialize: Q diag(lambda) Q^T + lambda_tilde (I - Q Q^T)."""
-    if not lambda_tilde > 0.0:
-        raise ContractError(f"full-rank approximation requires lambda_tilde > 0, got {lambda_tilde}")
-    q = np.asarray(pairs.q, dtype=np.float64)
-    _check_dense_cap(q.shape[0], memory_cap, "full_rank_materialize")
-    return low_rank_materialize(pairs, memory_cap) - lambda_tilde * (q @ q.T) + lambda_tilde * np.eye(q.shape[0])
+def eig_apply(pairs: EigenPairs, x, lambda_tilde: float = None, want_y: bool = True, want_quad: bool = True,
+              precision: str = "f64"):
+    """Batched form of the four implicit operators: x is one vector (P) or a
+    stack (nvec x P); returns (A x, x^T A x) with A the low-rank operator
+    (lambda_tilde None) or its full-rank extension."""
+    q, lam = _pairs(pairs)
+    p, k = q.shape
+    if lam.shape[0] != k:
+        raise ShapeError("EigenPairs: lambda length does not match column count")
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    single = xs.ndim == 1
+    xs = xs.reshape(1, -1) if single else xs
+    nvec, xlen = xs.shape
+    full = lambda_tilde is not None
+    ok = xlen == p and (not full or lambda_tilde > 0.0)
+    y = np.empty((nvec, p), dtype=np.float64) if want_y and ok else None
+    quad = np.empty(nvec, dtype=np.float64) if want_quad and ok else None
+    _lib.check(_lib.load().curvkit_eig_apply(p, k, _p(q), _p(lam), 1 if full else 0,
+                                             float(lambda_tilde) if full else 0.0, nvec, _p(xs), xlen,
+                                             _prec(precision), _p(y), _p(quad)))
+    if single:
+        return (y[0] if y is not None else None), (float(quad[0]) if quad is not None else None)
+    return y, quad
 
 
-def low_rank_quadform(pairs: EigenPairs, x) -> float:
-    t = pairs.q.T @ np.asarray(x, dtype=np.float64)
-    return float(np.sum(pairs.lam * t * t))
+def low_rank_quadform(pairs: EigenPairs, x, precision: str = "f64") -> float:
+    """curv::low_rank_quadform (eigensolve.cpp:294-299)."""
+    return eig_apply(pairs, x, None, want_y=False, precision=precision)[1]
 
 
-def low_rank_apply(pairs: EigenPairs, x) -> np.ndarray:
-    t = pairs.q.T @ np.asarray(x, dtype=np.float64)
-    return pairs.q @ (pairs.lam * t)
+def low_rank_apply(pairs: EigenPairs, x, precision: str = "f64") -> np.ndarray:
+    """curv::low_rank_apply (eigensolve.cpp:301-305)."""
+    return eig_apply(pairs, x, None, want_quad=False, precision=precision)[0]
 
 
 def default_lambda_tilde(pairs: EigenPairs) -> float:  # eigensolve.cpp:350-358
@@ -544,20 +575,14 @@ def default_lambda_tilde(pairs: EigenPairs) -> float:  # eigensolve.cpp:350-358
     return lk
 
 
-def full_rank_quadform(pairs: EigenPairs, lambda_tilde: float, x) -> float:
-    if not lambda_tilde > 0.0:
-        raise ContractError(f"full-rank approximation requires lambda_tilde > 0, got {lambda_tilde}")
-    x = np.asarray(x, dtype=np.float64)
-    t = pairs.q.T @ x
-    return float(np.sum(pairs.lam * t * t) + lambda_tilde * x @ x - lambda_tilde * t @ t)
+def full_rank_quadform(pairs: EigenPairs, lambda_tilde: float, x, precision: str = "f64") -> float:
+    """curv::full_rank_quadform (eigensolve.cpp:329-339)."""
+    return eig_apply(pairs, x, float(lambda_tilde), want_y=False, precision=precision)[1]
 
 
-def full_rank_apply(pairs: EigenPairs, lambda_tilde: float, x) -> np.ndarray:
-    if not lambda_tilde > 0.0:
-        raise ContractError(f"full-rank approximation requires lambda_tilde > 0, got {lambda_tilde}")
-    x = np.asarray(x, dtype=np.float64)
-    t = pairs.q.T @ x
-    return pairs.q @ (pairs.lam * t) + lambda_tilde * (x - pairs.q @ t)
+def full_rank_apply(pairs: EigenPairs, lambda_tilde: float, x, precision: str = "f64") -> np.ndarray:
+    """curv::full_rank_apply (eigensolve.cpp:341-350)."""
+    return eig_apply(pairs, x, float(lambda_tilde), want_quad=False, precision=precision)[0]
 
 
 # ---- device-resident entry points (torch tensors or raw pointers) -------------
@@ -822,3 +847,24 @@ def dev_jacobian_apply(spec, params, x, labels, n, p_begin, p_end, inp, ld_in, l
     _lib.check(_lib.load().curvkit_dev_jacobian_apply(C.byref(spec._c()), _ptr(params), _ptr(x), _ptr(labels), n,
                                                        _prec(precision), p_begin, p_end, 1 if transpose else 0,
                                                        _ptr(inp), ld_in, l, _ptr(out), ld_out, _stream(stream)))
+
+
+def dev_eig_materialize(p, k, q, ldq, lam, out, ldh, lambda_tilde=None, precision="tf32", stream=None):
+    """Q diag(lambda) Q^T (lambda_tilde None) or its full-rank extension into the
+    device matrix out (p x p, ldh); q, lam, out in the precision's storage type."""
+    full = lambda_tilde is not None
+    _lib.check(_lib.load().curvkit_dev_eig_materialize(p, k, _ptr(q), ldq, _ptr(lam), 1 if full else 0,
+                                                       float(lambda_tilde) if full else 0.0, _prec(precision),
+                                                       _ptr(out), ldh, _stream(stream)))
+
+
+def dev_eig_apply(p, k, q, ldq, lam, nvec, x, ldx, y=None, ldy=0, quad=None, lambda_tilde=None, precision="tf32",
+                  stream=None):
+    """y[v] = A x[v] and quad[v] = x[v]^T A x[v] (fp64) for nvec device vectors."""
+    full = lambda_tilde is not None
+    null = C.c_void_p(0)
+    _lib.check(_lib.load().curvkit_dev_eig_apply(p, k, _ptr(q), ldq, _ptr(lam), 1 if full else 0,
+                                                 float(lambda_tilde) if full else 0.0, nvec, _ptr(x), ldx,
+                                                 _ptr(y) if y is not None else null, ldy,
+                                                 C.cast(_ptr(quad), _lib.dptr) if quad is not None else None,
+                                                 _prec(precision), _stream(stream)))

@@ -87,22 +87,3 @@ def test_host_api_contract_errors():
         curv.HvpOperator(spec, p, curv.Batch(x, y), 2)
     with pytest.raises(ContractError, match="unknown precision"):
         curv.assemble_opg(spec, p, curv.Batch(x, y), precision="bf16")
-
-
-def test_low_full_rank_algebra_host():
-    # eigensolve.cpp:295-348 operator algebra on host-side eigenpairs
-    rng = np.random.default_rng(106)
-    a = rng.normal(size=(30, 30)); a = a + a.T
-    w, v = np.linalg.eigh(a)
-    pairs = curv.EigenPairs(v[:, ::-1][:, :4].copy(), np.array([10.0, 8.0, 6.0, 4.0]))
-    low = pairs.q @ np.diag(pairs.lam) @ pairs.q.T
-    full = low + 0.5 * (np.eye(30) - pairs.q @ pairs.q.T)
-    for _ in range(5):
-        x = rng.normal(size=30)
-        assert abs(curv.low_rank_quadform(pairs, x) - x @ low @ x) <= 1e-10 * max(1, abs(x @ low @ x))
-        assert abs(curv.full_rank_quadform(pairs, 0.5, x) - x @ full @ x) <= 1e-10 * max(1, abs(x @ full @ x))
-        assert np.allclose(curv.full_rank_apply(pairs, 0.5, x), full @ x, atol=1e-10)
-        assert np.allclose(curv.low_rank_apply(pairs, x), low @ x, atol=1e-10)
-    assert curv.default_lambda_tilde(pairs) == 4.0
-    with pytest.raises(ContractError):
-        curv.full_rank_quadform(pairs, 0.0, x)

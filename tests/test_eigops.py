@@ -1,0 +1,243 @@
+"""The consumers of eigenpairs (curv::validate_eigen_pairs, low_rank_* and
+full_rank_*, eigensolve.cpp:11-30 and 278-358) against vectors the reference
+itself produced (tests/golden/eigops.npz, tests/golden/make_eigops_golden.py).
+
+CPU: the numpy restatement in oracle/ against the golden vectors, and the
+contract / shape errors of the C-ABI (raised before any device work, with the
+reference's text).  GPU: every operator through the C-ABI in f64 / f32 / tf32 /
+f16s, batched vectors, the device entry points at config-1 and config-4 size.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, rel_fro
+from oracle import oracle as orc
+from paper_1905_05559_b200 import curv
+from paper_1905_05559_b200.errors import ContractError, ShapeError
+
+CASES = ["c0_opg", "ortho300", "k1", "full_k", "thin2000"]
+ROWS = (0, 7, 1023, 1999)  # make_eigops_golden.py keeps these matrix rows when P > 400
+# relative Frobenius tolerance per precision mode (north_star: 1e-5 fp64, 1e-3 fp32 / TF32)
+TOL = {"f64": 1e-12, "f32": 1e-5, "tf32x3": 1e-5, "tf32": 1e-3, "f16s": 1e-3}
+
+
+def case(name):
+    d = np.load(os.path.join(GOLDEN, "eigops.npz"))
+    return {k.split("/", 1)[1]: d[k] for k in d.files if k.startswith(name + "/")}
+
+
+def rows_of(m, p):
+    return m[list(ROWS)] if p > 400 else m
+
+
+# ---- CPU: the oracle restatement against the reference's vectors ----------------
+
+@pytest.mark.parametrize("name", CASES)
+def test_port_matches_reference_vectors(name):
+    c = case(name)
+    q, lam, lt = c["q"], c["lam"], float(c["lt"])
+    p = q.shape[0]
+    assert rel_fro(rows_of(orc.eig_materialize_port(q, lam), p), c["low"]) <= 1e-13
+    assert rel_fro(rows_of(orc.eig_materialize_port(q, lam, lt), p), c["full"]) <= 1e-13
+    for i, x in enumerate(c["x"]):
+        y, qf = orc.eig_apply_port(q, lam, x)
+        assert rel_fro(y, c["low_y"][i]) <= 1e-12 and abs(qf - c["low_quad"][i]) <= 1e-12 * max(1, abs(qf))
+        y, qf = orc.eig_apply_port(q, lam, x, lt)
+        assert rel_fro(y, c["full_y"][i]) <= 1e-12 and abs(qf - c["full_quad"][i]) <= 1e-12 * max(1, abs(qf))
+
+
+def test_golden_default_lambda_tilde_is_smallest_eigenvalue():
+    for name in ("c0_opg", "thin2000"):  # generated with curv::default_lambda_tilde
+        c = case(name)
+        assert float(c["lt"]) == c["lam"][-1] == curv.default_lambda_tilde(curv.EigenPairs(c["q"], c["lam"]))
+    with pytest.raises(ContractError, match="not positive"):
+        curv.default_lambda_tilde(curv.EigenPairs(np.eye(3)[:, :2], np.array([1.0, -0.5])))
+    with pytest.raises(ContractError, match="no eigenvalues"):
+        curv.default_lambda_tilde(curv.EigenPairs(np.zeros((3, 0)), np.zeros(0)))
+
+
+def test_contract_errors_before_device_work():
+    """The refusals of eigensolve.cpp:11-30 and 255-275, with the reference's text;
+    none of them needs a GPU (they are raised before any device call)."""
+    c = case("k1")
+    pairs = curv.EigenPairs(c["q"], c["lam"])
+    p = c["q"].shape[0]
+    with pytest.raises(ContractError, match=r"low_rank_materialize: P = 50 exceeds the dense memory cap 8; use the "
+                                            r"implicit quadform/apply forms instead"):
+        curv.low_rank_materialize(pairs, memory_cap=8)
+    with pytest.raises(ContractError, match="full_rank_materialize: P = 50 exceeds the dense memory cap 49"):
+        curv.full_rank_materialize(pairs, 0.5, memory_cap=49)
+    for bad in (0.0, -1.0, float("nan")):
+        with pytest.raises(ContractError, match="full-rank approximation requires lambda_tilde > 0, got"):
+            curv.full_rank_materialize(pairs, bad)  # checked before the memory cap, as in the reference
+        with pytest.raises(ContractError, match="full-rank approximation requires lambda_tilde > 0"):
+            curv.full_rank_quadform(pairs, bad, np.zeros(p))
+        with pytest.raises(ContractError, match="full-rank approximation requires lambda_tilde > 0"):
+            curv.full_rank_apply(pairs, bad, np.zeros(p))
+    with pytest.raises(ShapeError, match="eigen operator: vector length 49 does not match P = 50"):
+        curv.low_rank_apply(pairs, np.zeros(p - 1))
+    with pytest.raises(ShapeError, match="eigen operator: vector length 51 does not match P = 50"):
+        curv.full_rank_quadform(pairs, 0.5, np.zeros(p + 1))
+    with pytest.raises(ShapeError, match="lambda length does not match column count"):
+        curv.validate_eigen_pairs(curv.EigenPairs(c["q"], np.array([2.0, 1.0])))
+    with pytest.raises(ShapeError, match="more columns than rows"):
+        curv.validate_eigen_pairs(curv.EigenPairs(np.zeros((2, 3)), np.array([3.0, 2.0, 1.0])))
+    q2 = case("c0_opg")["q"]
+    with pytest.raises(ContractError, match="eigenvalues not sorted descending"):
+        curv.validate_eigen_pairs(curv.EigenPairs(q2, np.array([1.0, 3.0, 2.0, 1.0, 0.5, 0.1])))
+    with pytest.raises(ContractError, match="unknown precision"):
+        curv.low_rank_apply(pairs, np.zeros(p), precision="bf16")
+
+
+@pytest.mark.skipif(not orc.Ref.available(), reason="oracle/_ref not built")
+def test_reference_raises_the_same_refusals():
+    ref = orc.Ref()
+    c = case("k1")
+    with pytest.raises(orc.OracleError, match="exceeds the dense memory cap 8; use the implicit"):
+        ref.eig_ops(c["q"], c["lam"], materialize=True, memory_cap=8)
+    with pytest.raises(orc.OracleError, match="requires lambda_tilde > 0"):
+        ref.eig_ops(c["q"], c["lam"], lambda_tilde=0.0, materialize=True, memory_cap=8)
+    with pytest.raises(orc.OracleError, match="vector length 49 does not match P = 50"):
+        ref.eig_ops(c["q"], c["lam"], x=np.zeros(49))
+
+
+# ---- GPU: the operators through the C-ABI ---------------------------------------
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["f64", "f32", "tf32", "tf32x3", "f16s"])
+@pytest.mark.parametrize("name", CASES)
+def test_materialize_matches_reference(name, prec):
+    c = case(name)
+    pairs = curv.EigenPairs(c["q"], c["lam"])
+    p = c["q"].shape[0]
+    low = curv.low_rank_materialize(pairs, precision=prec)
+    full = curv.full_rank_materialize(pairs, float(c["lt"]), precision=prec)
+    assert low.shape == full.shape == (p, p)
+    assert np.array_equal(low, low.T) and np.array_equal(full, full.T)  # mirrored lower tiles: exactly symmetric
+    assert rel_fro(rows_of(low, p), c["low"]) <= TOL[prec]
+    assert rel_fro(rows_of(full, p), c["full"]) <= TOL[prec]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["f64", "f32", "tf32"])
+@pytest.mark.parametrize("name", CASES)
+def test_apply_and_quadform_match_reference(name, prec):
+    c = case(name)
+    pairs = curv.EigenPairs(c["q"], c["lam"])
+    lt = float(c["lt"])
+    tol = 1e-12 if prec == "f64" else 2e-5  # the implicit forms run exact FMAs in every fp32 mode
+    for i, x in enumerate(c["x"]):
+        assert rel_fro(curv.low_rank_apply(pairs, x, precision=prec), c["low_y"][i]) <= tol
+        assert rel_fro(curv.full_rank_apply(pairs, lt, x, precision=prec), c["full_y"][i]) <= tol
+        scale = max(1.0, float(np.sum(c["lam"][0] * x * x)))
+        assert abs(curv.low_rank_quadform(pairs, x, precision=prec) - c["low_quad"][i]) <= tol * scale
+        assert abs(curv.full_rank_quadform(pairs, lt, x, precision=prec) - c["full_quad"][i]) <= tol * scale
+
+
+@pytest.mark.gpu
+def test_batched_vectors_equal_single_calls():
+    c = case("ortho300")
+    pairs = curv.EigenPairs(c["q"], c["lam"])
+    lt = float(c["lt"])
+    xs = np.concatenate([c["x"], c["x"][::-1] * 0.5, c["x"][:1] - c["x"][1:2]])  # 7 vectors: two passes of four
+    for ltv in (None, lt):
+        y, quad = curv.eig_apply(pairs, xs, ltv)
+        for i, x in enumerate(xs):
+            y1, q1 = curv.eig_apply(pairs, x, ltv)
+            assert np.array_equal(y[i], y1) and quad[i] == q1  # fixed-order reductions: bitwise
+    ref_y = np.array([orc.eig_apply_port(c["q"], c["lam"], x, lt)[0] for x in xs])
+    assert rel_fro(y, ref_y) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_validate_eigen_pairs_on_device():
+    for name in CASES:
+        c = case(name)
+        curv.validate_eigen_pairs(curv.EigenPairs(c["q"], c["lam"]))
+    c = case("ortho300")
+    q = c["q"].copy()
+    q[:, 5] += 1e-6 * q[:, 6]  # |q5.q6| = 1e-6 > 1e-8
+    with pytest.raises(ContractError, match="columns are not orthonormal"):
+        curv.validate_eigen_pairs(curv.EigenPairs(q, c["lam"]))
+    curv.validate_eigen_pairs(curv.EigenPairs(q, c["lam"]), ortho_tol=1e-5)
+    q = c["q"].copy()
+    q[:, 36] *= 1.0 + 1e-6  # the last column's norm
+    with pytest.raises(ContractError, match="columns are not orthonormal"):
+        curv.validate_eigen_pairs(curv.EigenPairs(q, c["lam"]))
+
+
+@pytest.mark.gpu
+def test_empty_basis():
+    """k = 0: the low-rank operator is zero, the full-rank one lambda_tilde I."""
+    pairs = curv.EigenPairs(np.zeros((9, 0)), np.zeros(0))
+    x = np.arange(9.0)
+    assert np.array_equal(curv.low_rank_materialize(pairs), np.zeros((9, 9)))
+    assert np.array_equal(curv.full_rank_materialize(pairs, 0.5), 0.5 * np.eye(9))
+    assert np.array_equal(curv.low_rank_apply(pairs, x), np.zeros(9))
+    assert np.allclose(curv.full_rank_apply(pairs, 0.5, x), 0.5 * x, rtol=1e-15)
+    assert curv.full_rank_quadform(pairs, 0.5, x) == pytest.approx(0.5 * x @ x, rel=1e-15)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec,dt", [("tf32", "float32"), ("f16s", "float32"), ("f64", "float64")])
+def test_device_entry_points_config1_size(prec, dt):
+    """P = 25 450 (config 1), k = 100: the materialised matrix against its own
+    implicit forms and against fp64 torch products of the same eigenpairs."""
+    import torch
+    tdt = getattr(torch, dt)
+    dev = torch.device("cuda", 0)
+    p, k, lt = 25450, 100, 0.02
+    g = torch.Generator(device="cpu").manual_seed(11)
+    q64, _ = torch.linalg.qr(torch.randn(p, k, generator=g, dtype=torch.float64))
+    lam64 = (2.0 * 0.93 ** torch.arange(k, dtype=torch.float64))
+    ldq, ldh = 104, (p + 3) // 4 * 4
+    q = torch.zeros((p, ldq), dtype=tdt, device=dev)
+    q[:, :k] = q64.to(dev).to(tdt)
+    lam = lam64.to(dev).to(tdt)
+    h = torch.empty((p, ldh), dtype=tdt, device=dev)
+    xs = torch.randn(5, p, generator=g, dtype=torch.float64).to(dev).to(tdt)
+    y = torch.empty_like(xs)
+    quad = torch.empty(5, dtype=torch.float64, device=dev)
+    qd, ld_ = q[:, :k].double(), lam.double()
+    for ltv in (None, lt):
+        curv.dev_eig_materialize(p, k, q, ldq, lam, h, ldh, lambda_tilde=ltv, precision=prec)
+        curv.dev_eig_apply(p, k, q, ldq, lam, 5, xs, p, y, p, quad, lambda_tilde=ltv, precision=prec)
+        torch.cuda.synchronize()
+        hm = h[:, :p]
+        assert torch.equal(hm, hm.T)
+        shift = 0.0 if ltv is None else ltv
+        xd = xs.double()
+        t = xd @ qd
+        y_ref = (t * (ld_ - shift)) @ qd.T + shift * xd
+        quad_ref = (t * t * (ld_ - shift)).sum(1) + shift * (xd * xd).sum(1)
+        tol = 1e-12 if prec == "f64" else 2e-5
+        assert float(torch.linalg.norm(y.double() - y_ref) / torch.linalg.norm(y_ref)) <= tol
+        assert float(((quad - quad_ref).abs() / quad_ref.abs().clamp_min(1.0)).max()) <= tol
+        # whole matrix: H X against the fp64 products (every entry of H enters)
+        hx = (hm.double() @ xd.T).T
+        assert float(torch.linalg.norm(hx - y_ref) / torch.linalg.norm(y_ref)) <= TOL[prec]
+
+
+@pytest.mark.gpu
+def test_device_apply_config4_size():
+    """P = 1 055 242 (config 4), k = 100, fp32 storage: two passes over the 422 MB basis."""
+    import torch
+    dev = torch.device("cuda", 0)
+    p, k, lt = 1055242, 100, 0.38
+    g = torch.Generator(device=dev).manual_seed(5)
+    q, _ = torch.linalg.qr(torch.randn(p, k, generator=g, dtype=torch.float32, device=dev))
+    q = q.contiguous()
+    lam = torch.linspace(0.5, 0.38, k, device=dev)
+    xs = torch.randn(4, p, generator=g, dtype=torch.float32, device=dev)
+    y = torch.empty_like(xs)
+    quad = torch.empty(4, dtype=torch.float64, device=dev)
+    curv.dev_eig_apply(p, k, q, k, lam, 4, xs, p, y, p, quad, lambda_tilde=lt, precision="f32")
+    torch.cuda.synchronize()
+    qd, xd, ld_ = q.double(), xs.double(), lam.double()
+    t = xd @ qd
+    y_ref = (t * (ld_ - lt)) @ qd.T + lt * xd
+    quad_ref = (t * t * (ld_ - lt)).sum(1) + lt * (xd * xd).sum(1)
+    assert float(torch.linalg.norm(y.double() - y_ref) / torch.linalg.norm(y_ref)) <= 2e-6
+    assert float(((quad - quad_ref).abs() / quad_ref.abs()).max()) <= 2e-6

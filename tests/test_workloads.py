@@ -37,27 +37,3 @@ def test_draw_is_deterministic_and_one_hot():
     widths = W.CONFIGS["c0"].widths
     r = np.sqrt(6.0 / (widths[0] + widths[1]))
     assert np.abs(p[:32]).max() <= r and np.all(p[32:40] == 0.0)  # Glorot W, zero biases
-
-
-def test_eigen_pair_helpers_match_reference_forms():
-    """validate_eigen_pairs and the materialised low/full-rank forms
-    (eigensolve.cpp) against their implicit quadform/apply forms."""
-    import numpy as np
-    import pytest
-    from paper_1905_05559_b200 import curv
-    rng = np.random.default_rng(3)
-    q, _ = np.linalg.qr(rng.standard_normal((12, 4)))
-    pairs = curv.EigenPairs(q, np.array([4.0, 3.0, 2.0, 1.0]))
-    curv.validate_eigen_pairs(pairs)
-    x = rng.standard_normal(12)
-    L = curv.low_rank_materialize(pairs)
-    F = curv.full_rank_materialize(pairs, 0.5)
-    np.testing.assert_allclose(L @ x, curv.low_rank_apply(pairs, x), rtol=1e-12)
-    np.testing.assert_allclose(F @ x, curv.full_rank_apply(pairs, 0.5, x), rtol=1e-12)
-    assert abs(x @ F @ x - curv.full_rank_quadform(pairs, 0.5, x)) < 1e-10
-    with pytest.raises(curv.ContractError):
-        curv.validate_eigen_pairs(curv.EigenPairs(q, np.array([1.0, 3.0, 2.0, 1.0])))
-    with pytest.raises(curv.ContractError):
-        curv.low_rank_materialize(pairs, memory_cap=8)
-    with pytest.raises(curv.ContractError):
-        curv.full_rank_materialize(pairs, 0.0)
