@@ -26,7 +26,6 @@ namespace ck {
 namespace eigops {
 
 constexpr int kVecTile = 4;   // vectors sharing one pass over Q
-constexpr int kColTile = 4;   // 32-column groups held in registers per pass (k <= 128 in one pass)
 
 // qs[i][c] = q[i][c] (lambda[c] - shift), qp[i][c] = q[i][c]; columns [k, ldk) zero
 template <class T>
@@ -72,57 +71,90 @@ void materialize(int prec, cudaStream_t s, int64_t p, int64_t k, const T* q, int
     }
 }
 
-// Partial projections of one row chunk: part[v][c][b] = sum_{i in chunk b} x[v][i] q[i][c]
-// and part[v][k][b] = sum x[v][i]^2.  A warp takes rows i (four per iteration: 16
-// loads in flight per lane), its lanes the columns c = lane + 32 j (coalesced rows
-// of Q); the block's warps are summed through shared memory in warp order.
 template <class T>
+struct alignas(16) Vec16 {
+    static constexpr int W = 16 / sizeof(T);  // elements per 16-byte group
+    T v[W];
+};
+
+// 16-byte read-once load (ld.global.cs: evict-first in L1/L2)
+template <class T>
+__device__ __forceinline__ Vec16<T> ld16_stream(const T* p) {
+    uint4 u;
+    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p));
+    Vec16<T> out;
+    memcpy(&out, &u, 16);
+    return out;
+}
+
+// Partial projections of one row chunk: part[v][c][b] = sum_{i in chunk b} x[v][i] q[i][c]
+// and part[v][k][b] = sum x[v][i]^2.  A warp takes rows i, RU per iteration; lane l
+// holds the 16-byte column group l of the pass (columns c0 + W l ..), so a row of
+// the pass is one 16-byte load per lane (VEC: rows 16-byte aligned) and RU of them
+// are in flight.  The block's warps are summed through shared memory in warp order.
+template <class T, int NV, bool VEC>
 __global__ void __launch_bounds__(256) project_kernel(const T* __restrict__ q, int64_t ldq, int64_t p, int64_t k,
                                                       int64_t c0, const T* __restrict__ x, int64_t ldx, int nv,
                                                       int64_t chunk, double* __restrict__ part) {
-    __shared__ double red[8][kVecTile][32 * kColTile + 1];
+    using V = Vec16<T>;
+    constexpr int W = V::W, PC = 32 * W, RU = 8;  // PC: columns per pass
+    __shared__ double red[8][NV][PC + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t r0 = blockIdx.x * chunk, r1 = min(p, r0 + chunk);
-    constexpr int RU = 4;  // rows per iteration
-    T acc[kVecTile][kColTile] = {};
-    T xx[kVecTile] = {};
-    bool col[kColTile];
-#pragma unroll
-    for (int j = 0; j < kColTile; ++j) col[j] = c0 + lane + 32 * j < k;
-    for (int64_t i = r0 + warp; i < r1; i += 8 * RU) {
-        T qv[RU][kColTile], xv[RU][kVecTile];
+    const int64_t cl = c0 + (int64_t)W * lane;  // this lane's first column
+    // lanes past the last column group read group 0 instead (their sums are dropped below)
+    const int64_t cld = cl < k ? cl : c0;
+    T acc[NV][W] = {};
+    T xx[NV] = {};
+    auto rows_step = [&](int64_t i, auto full) {
+        constexpr bool kFull = decltype(full)::value;  // all RU rows inside the chunk: loads without predicates
+        V qv[RU];
+        T xv[RU][NV];
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
             const int64_t r = i + 8 * u;
+            const bool ok = kFull || r < r1;
+            if constexpr (VEC) {
+                if (ok) {
+                    qv[u] = ld16_stream<T>(q + r * ldq + cld);
+                } else {
 #pragma unroll
-            for (int j = 0; j < kColTile; ++j) qv[u][j] = (r < r1 && col[j]) ? q[r * ldq + c0 + lane + 32 * j] : T(0);
+                    for (int w = 0; w < W; ++w) qv[u].v[w] = T(0);
+                }
+            } else {
 #pragma unroll
-            for (int v = 0; v < kVecTile; ++v) xv[u][v] = (r < r1 && v < nv) ? x[v * ldx + r] : T(0);
+                for (int w = 0; w < W; ++w) qv[u].v[w] = (ok && cl + w < k) ? q[r * ldq + cl + w] : T(0);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) xv[u][v] = (ok && v < nv) ? x[v * ldx + r] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < RU; ++u)
 #pragma unroll
-            for (int v = 0; v < kVecTile; ++v) {
+            for (int v = 0; v < NV; ++v) {
 #pragma unroll
-                for (int j = 0; j < kColTile; ++j) acc[v][j] += xv[u][v] * qv[u][j];
+                for (int w = 0; w < W; ++w) acc[v][w] += xv[u][v] * qv[u].v[w];
                 xx[v] += xv[u][v] * xv[u][v];
             }
-    }
+    };
+    int64_t i = r0 + warp;
+    for (; i + 8 * (RU - 1) < r1; i += 8 * RU) rows_step(i, std::true_type{});
+    if (i < r1) rows_step(i, std::false_type{});
 #pragma unroll
-    for (int v = 0; v < kVecTile; ++v) {
+    for (int v = 0; v < NV; ++v) {
 #pragma unroll
-        for (int j = 0; j < kColTile; ++j) red[warp][v][lane + 32 * j] = (double)acc[v][j];
-        if (lane == 0) red[warp][v][32 * kColTile] = (double)xx[v];
+        for (int w = 0; w < W; ++w) red[warp][v][W * lane + w] = (double)acc[v][w];
+        if (lane == 0) red[warp][v][PC] = (double)xx[v];
     }
     __syncthreads();
     const int64_t nb = gridDim.x;
-    for (int e = threadIdx.x; e < nv * (32 * kColTile + 1); e += 256) {
-        const int v = e / (32 * kColTile + 1), cc = e % (32 * kColTile + 1);
+    for (int e = threadIdx.x; e < nv * (PC + 1); e += 256) {
+        const int v = e / (PC + 1), cc = e % (PC + 1);
         double sum = 0.0;
         for (int w = 0; w < 8; ++w) sum += red[w][v][cc];
-        if (cc == 32 * kColTile) {
+        if (cc == PC) {
             if (c0 == 0) part[(v * (k + 1) + k) * nb + blockIdx.x] = sum;
-        } else if (c0 + cc < k) {
+        } else if (c0 + cc < k) {  // (a VEC group's columns past k were read from the row's pitch: dropped here)
             part[(v * (k + 1) + c0 + cc) * nb + blockIdx.x] = sum;
         }
     }
@@ -138,137 +170,237 @@ __device__ __forceinline__ double chunk_sum(const double* __restrict__ row, int6
     return s;
 }
 
-// t[v][c] = the chunk partials summed in fixed order (fp64); ts = (lambda - shift) t
-// in T for the expansion; quad[v] = sum_c lambda_c t_c^2 + lambda_tilde (x.x - t.t)
-// (eigensolve.cpp:294-299, :329-339).  One block per vector, one warp per column.
+// tsum[v][c] = the chunk partials of column c (c = k: x.x) summed in fixed order
+// (fp64); one warp per column
+__global__ void __launch_bounds__(256) project_sum_kernel(const double* __restrict__ part, int64_t nblocks, int64_t k,
+                                                          double* __restrict__ tsum) {
+    const int v = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c = (int64_t)blockIdx.x * 8 + warp;
+    if (c > k) return;
+    const double t = chunk_sum(part + ((int64_t)v * (k + 1) + c) * nblocks, nblocks, lane);
+    if (lane == 0) tsum[(int64_t)v * (k + 1) + c] = t;
+}
+
+// ts = (lambda - shift) t in T for the expansion (pitch kt, pad zeroed);
+// quad[v] = sum_c lambda_c t_c^2 + lambda_tilde (x.x - t.t) (eigensolve.cpp:294-299,
+// :329-339).  One block per vector; fixed summation order.
 template <class T>
-__global__ void __launch_bounds__(256) project_finish_kernel(const double* __restrict__ part, int64_t nblocks, int nv,
-                                                             int64_t k, const T* __restrict__ lam, int full,
-                                                             double lambda_tilde, T* __restrict__ ts, int64_t kt,
+__global__ void __launch_bounds__(256) project_finish_kernel(const double* __restrict__ tsum, int64_t k,
+                                                             const T* __restrict__ lam, int full, double lambda_tilde,
+                                                             T* __restrict__ ts, int64_t kt,
                                                              double* __restrict__ quad) {
-    __shared__ double s_lt[8], s_tt[8];
-    const int v = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double* pv = part + (int64_t)v * (k + 1) * nblocks;
+    __shared__ double s_lt[256], s_tt[256];
+    const int v = blockIdx.x;
+    const double* tv = tsum + (int64_t)v * (k + 1);
     double lt = 0.0, tt = 0.0;
-    for (int64_t c = warp; c < k; c += 8) {
-        const double t = chunk_sum(pv + c * nblocks, nblocks, lane);
-        const double l = (double)lam[c];
-        if (ts && lane == 0) ts[v * kt + c] = (T)((l - (full ? lambda_tilde : 0.0)) * t);
+    for (int64_t c = threadIdx.x; c < kt; c += 256) {
+        if (c >= k) {
+            if (ts) ts[v * kt + c] = T(0);  // the pad columns of the expansion's 16-byte groups
+            continue;
+        }
+        const double t = tv[c], l = (double)lam[c];
+        if (ts) ts[v * kt + c] = (T)((l - (full ? lambda_tilde : 0.0)) * t);
         lt += l * t * t;
         tt += t * t;
     }
-    if (ts)  // the pad columns of the expansion's 16-byte groups
-        for (int64_t c = k + threadIdx.x; c < kt; c += 256) ts[v * kt + c] = T(0);
-    if (lane == 0) {
-        s_lt[warp] = lt;
-        s_tt[warp] = tt;
-    }
+    s_lt[threadIdx.x] = lt;
+    s_tt[threadIdx.x] = tt;
     __syncthreads();
-    if (warp == 0 && quad) {
-        const double xx = chunk_sum(pv + k * nblocks, nblocks, lane);
-        if (lane == 0) {
-            double a = 0.0, b = 0.0;
-            for (int i = 0; i < 8; ++i) {
-                a += s_lt[i];
-                b += s_tt[i];
-            }
-            quad[v] = full ? a + lambda_tilde * xx - lambda_tilde * b : a;
+    if (threadIdx.x == 0 && quad) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < 256; ++i) {
+            a += s_lt[i];
+            b += s_tt[i];
         }
+        quad[v] = full ? a + lambda_tilde * tv[k] - lambda_tilde * b : a;
     }
 }
 
-// y[v][i] = sum_c ts[v][c] q[i][c] + shift x[v][i].  A block stages kExpRows rows of
-// Q (column chunks of ExpCols) in shared memory with coalesced loads; thread (row r,
-// class g) then sums its row over the 16-byte column groups g, g + 4, ... (one
-// LDS.128 of Q and one 16-byte load of ts per vector for W columns; the row pitch
-// puts a quarter-warp's 16-byte reads on distinct banks), the four classes are
-// added in fixed order, and y is stored coalesced along i.
+// y[v][i] = sum_c ts[v][c] q[i][c] + shift x[v][i].  A block walks tiles of kExpRows
+// rows of Q, in column chunks of at most ExpTile::Cols, through two shared-memory
+// buffers: the 16-byte cp.async copies of the next (tile, chunk) are in flight while
+// the current one is summed (VEC: rows 16-byte aligned; otherwise plain loads, one
+// buffer).  The row pitch puts a quarter-warp's 16-byte reads on distinct banks.
+// Thread (row r, class g) sums its row over the 16-byte column groups g, g + 4, ...
+// (one LDS.128 of Q and one of the staged ts chunk per vector for W columns), the
+// four classes are added in fixed order, and y is stored coalesced along i.
 constexpr int kExpRows = 64;
 template <class T>
 struct ExpTile {
-    static constexpr int W = 16 / sizeof(T);           // elements per 16-byte group
-    static constexpr int Cols = 1024 / sizeof(T);      // 256 (float) / 128 (double) columns per chunk
-    static constexpr int Pitch = Cols + W;             // 260 / 130: 16-byte groups of 8 rows on distinct banks
-    static constexpr size_t bytes = (size_t)(kExpRows * Pitch + 4 * kVecTile * kExpRows) * sizeof(T);
+    static constexpr int W = 16 / sizeof(T);
+    static constexpr int Cols = 1024 / sizeof(T);  // at most 256 (float) / 128 (double) columns per chunk
+    // smallest pitch >= cols (a multiple of W) whose 4-byte word count is 4 mod 32
+    static int pitch(int64_t k) {
+        const int colsw = (int)round_up(std::min<int64_t>(k, Cols), W);
+        const int mod = 32 / (int)(sizeof(T) / 4), want = W;  // elements: float 4 mod 32, double 2 mod 16
+        int pt = colsw;
+        while (pt % mod != want) pt += W;
+        return pt;
+    }
+    // per buffer: the Q tile and the ts chunk [kVecTile][pitch]; then the class sums
+    static size_t bytes(int64_t k, bool two) {
+        return (size_t)((two ? 2 : 1) * (kExpRows + kVecTile) * pitch(k) + 4 * kVecTile * kExpRows) * sizeof(T);
+    }
 };
 
-template <class T>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gmem), "r"(src_bytes) : "memory");
+}
+
+template <class T, int NV, bool VEC>
 __global__ void __launch_bounds__(256) expand_kernel(const T* __restrict__ q, int64_t ldq, int64_t p, int64_t k,
-                                                     const T* __restrict__ ts, int64_t kt, int nv, T shift,
+                                                     const T* __restrict__ ts, int64_t kt, int nv, int pitch, T shift,
                                                      const T* __restrict__ x, int64_t ldx, T* __restrict__ y,
                                                      int64_t ldy) {
     using E = ExpTile<T>;
-    constexpr int W = E::W;
-    struct alignas(16) Vec {
-        T v[W];
-    };
+    using V = Vec16<T>;
+    constexpr int W = E::W, NB = VEC ? 2 : 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* tile = reinterpret_cast<T*>(smem_raw);      // [kExpRows][Pitch]
-    T* red = tile + kExpRows * E::Pitch;           // [4][kVecTile][kExpRows]
+    T* tiles = reinterpret_cast<T*>(smem_raw);               // [NB][kExpRows + kVecTile][pitch]: Q rows, then ts rows
+    const int bufsz = (kExpRows + kVecTile) * pitch;
+    T* red = tiles + NB * bufsz;                             // [4][kVecTile][kExpRows]
     const int t = threadIdx.x, r = t % kExpRows, g = t / kExpRows;
     const int64_t ntiles = ceil_div(p, kExpRows);
-    for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        const int64_t i0 = tl * kExpRows;
-        const int rows = (int)min((int64_t)kExpRows, p - i0);
-        T acc[kVecTile] = {};
-        for (int64_t c0 = 0; c0 < k; c0 += E::Cols) {
-            const int cols = (int)min((int64_t)E::Cols, k - c0);
-            const int colsw = (cols + W - 1) / W * W;
-            __syncthreads();  // the previous chunk's readers are done
-            if (ldq == k && cols == k) {  // the tile is one contiguous run of rows * k elements
-                const T* src = q + i0 * k;
-                const int total = rows * cols, dr = 256 / cols, dc = 256 % cols;
-                int rr = t / cols, c = t % cols;
-#pragma unroll 8
-                for (int e = t; e < total; e += 256) {
-                    tile[rr * E::Pitch + c] = src[e];
-                    rr += dr;
-                    c += dc;
-                    if (c >= cols) {
-                        c -= cols;
-                        ++rr;
-                    }
-                }
+    const int64_t nchunks = ceil_div(k, (int64_t)E::Cols);
+    // this block's work items: (tile blockIdx.x + j gridDim.x, chunk c), j-major
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t nitems = my_tiles * nchunks;
+    auto item_rows = [&](int64_t it, int64_t& i0, int64_t& c0, int& rows, int& cols) {
+        i0 = (blockIdx.x + (it / nchunks) * gridDim.x) * kExpRows;
+        c0 = (it % nchunks) * E::Cols;
+        rows = (int)min((int64_t)kExpRows, p - i0);
+        cols = (int)min((int64_t)E::Cols, k - c0);
+    };
+    // stage item `it` into buffer `b`: cp.async (VEC; the ragged last group zero-filled
+    // past k) or plain loads
+    auto stage = [&](int64_t it, int b) {
+        int64_t i0, c0;
+        int rows, cols;
+        item_rows(it, i0, c0, rows, cols);
+        T* tile = tiles + b * bufsz;
+        const int nvr = (cols + W - 1) / W;
+        // the chunk of ts (kt is a multiple of 4 and its pad is zero: whole 16-byte groups)
+        for (int e = t; e < NV * nvr; e += 256) {
+            const int v = e / nvr, cv = e % nvr;
+            if constexpr (VEC) {
+                cp_async16(tile + (kExpRows + v) * pitch + W * cv, ts + v * kt + c0 + W * cv, 16);
             } else {
-                for (int rr = t / 32; rr < rows; rr += 8) {
-                    const T* src = q + (i0 + rr) * ldq + c0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) tile[(kExpRows + v) * pitch + W * cv + w] = ts[v * kt + c0 + W * cv + w];
+            }
+        }
+        if constexpr (VEC) {
+            const int total = rows * nvr, dr = 256 / nvr, dc = 256 % nvr;
+            int rr = t / nvr, cv = t % nvr;
+            for (int e = t; e < total; e += 256) {
+                const int valid = min(W, cols - W * cv) * (int)sizeof(T);
+                cp_async16(tile + rr * pitch + W * cv, q + (i0 + rr) * ldq + c0 + W * cv, valid);
+                rr += dr;
+                cv += dc;
+                if (cv >= nvr) {
+                    cv -= nvr;
+                    ++rr;
+                }
+            }
+        } else {
+            for (int rr = t / 32; rr < rows; rr += 8) {
+                const T* src = q + (i0 + rr) * ldq + c0;
 #pragma unroll 4
-                    for (int c = t % 32; c < cols; c += 32) tile[rr * E::Pitch + c] = src[c];
-                }
-            }
-            if (colsw != cols)  // zero the ragged end of the last 16-byte group
-                for (int e = t; e < rows * (colsw - cols); e += 256)
-                    tile[(e / (colsw - cols)) * E::Pitch + cols + e % (colsw - cols)] = T(0);
-            __syncthreads();
-            if (r < rows) {
-                const T* row = tile + r * E::Pitch;
-#pragma unroll 2
-                for (int c = g * W; c < colsw; c += 4 * W) {
-                    const Vec qv = *reinterpret_cast<const Vec*>(row + c);
-#pragma unroll
-                    for (int v = 0; v < kVecTile; ++v) {
-                        if (v >= nv) break;
-                        const Vec tv = *reinterpret_cast<const Vec*>(ts + v * kt + c0 + c);
-#pragma unroll
-                        for (int u = 0; u < W; ++u) acc[v] += qv.v[u] * tv.v[u];
-                    }
-                }
+                for (int c = t % 32; c < nvr * W; c += 32) tile[rr * pitch + c] = c < cols ? src[c] : T(0);
             }
         }
-        __syncthreads();  // (k = 0: no chunk loop ran) red's previous readers are done
-#pragma unroll
-        for (int v = 0; v < kVecTile; ++v) red[(g * kVecTile + v) * kExpRows + r] = acc[v];
-        __syncthreads();
-        for (int e = t; e < nv * kExpRows; e += 256) {
-            const int v = e / kExpRows, rr = e % kExpRows;
-            if (rr >= rows) continue;
-            T sum = red[(0 * kVecTile + v) * kExpRows + rr];
-#pragma unroll
-            for (int gg = 1; gg < 4; ++gg) sum += red[(gg * kVecTile + v) * kExpRows + rr];
-            const int64_t i = i0 + rr;
-            y[v * ldy + i] = sum + (shift != T(0) ? shift * x[v * ldx + i] : T(0));
-        }
+    };
+    if constexpr (VEC) {
+        if (nitems > 0) stage(0, 0);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    T acc[NV] = {};
+    for (int64_t it = 0; it < nitems; ++it) {
+        int64_t i0, c0;
+        int rows, cols;
+        item_rows(it, i0, c0, rows, cols);
+        const int b = VEC ? (int)(it & 1) : 0;
+        if constexpr (VEC) {
+            if (it + 1 < nitems) stage(it + 1, b ^ 1);  // (its last readers passed the barrier below)
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            stage(it, 0);
+        }
+        __syncthreads();
+        if (r < rows) {
+            const T* row = tiles + b * bufsz + r * pitch;
+            const T* st = tiles + b * bufsz + kExpRows * pitch;
+            const int colsw = (cols + W - 1) / W * W;
+#pragma unroll 4
+            for (int c = g * W; c < colsw; c += 4 * W) {
+                const V qv = *reinterpret_cast<const V*>(row + c);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const V tv = *reinterpret_cast<const V*>(st + v * pitch + c);
+#pragma unroll
+                    for (int u = 0; u < W; ++u) acc[v] += qv.v[u] * tv.v[u];
+                }
+            }
+        }
+        if (c0 + E::Cols >= k) {  // the tile's last chunk: add the four classes, store y
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                red[(g * kVecTile + v) * kExpRows + r] = acc[v];
+                acc[v] = T(0);
+            }
+            __syncthreads();
+            for (int e = t; e < nv * kExpRows; e += 256) {
+                const int v = e / kExpRows, rr = e % kExpRows;
+                if (rr >= rows) continue;
+                T sum = red[(0 * kVecTile + v) * kExpRows + rr];
+#pragma unroll
+                for (int gg = 1; gg < 4; ++gg) sum += red[(gg * kVecTile + v) * kExpRows + rr];
+                const int64_t i = i0 + rr;
+                y[v * ldy + i] = sum + (shift != T(0) ? shift * x[v * ldx + i] : T(0));
+            }
+        }
+        __syncthreads();  // the buffer and red may be rewritten
+    }
+    if constexpr (VEC) asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// k = 0: y = shift x
+template <class T>
+__global__ void scale_vec_kernel(const T* __restrict__ x, int64_t ldx, T* __restrict__ y, int64_t ldy, int64_t p,
+                                 int nv, T shift) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p * nv) return;
+    const int64_t v = i / p, j = i % p;
+    y[v * ldy + j] = shift * x[v * ldx + j];
+}
+
+template <class T, int NV, bool VEC>
+void launch_project(cudaStream_t s, int64_t nblocks, const T* q, int64_t ldq, int64_t p, int64_t k, int64_t c0,
+                    const T* x, int64_t ldx, int nv, int64_t chunk, double* part) {
+    project_kernel<T, NV, VEC><<<(unsigned)nblocks, 256, 0, s>>>(q, ldq, p, k, c0, x, ldx, nv, chunk, part);
+    CK_LAUNCH();
+}
+
+template <class T, int NV, bool VEC>
+void launch_expand(cudaStream_t s, const T* q, int64_t ldq, int64_t p, int64_t k, const T* ts, int64_t kt, int nv,
+                   T shift, const T* x, int64_t ldx, T* y, int64_t ldy) {
+    if (k == 0) {
+        scale_vec_kernel<T><<<(unsigned)ceil_div(p * nv, 256), 256, 0, s>>>(x, ldx, y, ldy, p, nv, shift);
+        CK_LAUNCH();
+        return;
+    }
+    const size_t smem = ExpTile<T>::bytes(k, VEC), smem_max = ExpTile<T>::bytes(ExpTile<T>::Cols, VEC);
+    func_attr_once((const void*)expand_kernel<T, NV, VEC>, [smem_max] {
+        CK_CUDA(cudaFuncSetAttribute(expand_kernel<T, NV, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_max));
+    });
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(6, (int64_t)(200 * 1024) / (int64_t)smem));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(per_sm * 148, ceil_div(p, kExpRows)));
+    expand_kernel<T, NV, VEC><<<(unsigned)grid, 256, smem, s>>>(q, ldq, p, k, ts, kt, nv, ExpTile<T>::pitch(k), shift,
+                                                                x, ldx, y, ldy);
+    CK_LAUNCH();
 }
 
 // y (nvec x p, ldy) and/or quad (nvec, fp64) for x (nvec x p, ldx); y or quad may be null
@@ -276,33 +408,50 @@ template <class T>
 void apply(cudaStream_t s, int64_t p, int64_t k, const T* q, int64_t ldq, const T* lam, bool full, double lambda_tilde,
            int64_t nvec, const T* x, int64_t ldx, T* y, int64_t ldy, double* quad) {
     if (nvec < 1) return;
+    constexpr int W = Vec16<T>::W;
     const int64_t nblocks = std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(p, 256)));
     const int64_t chunk = ceil_div(p, nblocks);
     DevMem part((size_t)(nblocks * kVecTile * (k + 1)) * sizeof(double), s);
+    DevMem tsum((size_t)(kVecTile * (k + 1)) * sizeof(double), s);
     const int64_t kt = round_up(std::max<int64_t>(k, 1), 4);
     DevMem ts((size_t)(kVecTile * kt) * sizeof(T), s);
     const T shift = full ? (T)lambda_tilde : T(0);
-    const size_t smem = ExpTile<T>::bytes;
-    func_attr_once((const void*)expand_kernel<T>, [smem] {
-        CK_CUDA(cudaFuncSetAttribute(expand_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    });
+    // 16-byte loads of Q when every row starts 16-byte aligned
+    const bool vec = ldq % W == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
     ProfScope ps("eig_apply", s, 4.0 * (double)p * k * nvec, 2.0 * ceil_div(nvec, kVecTile) * sizeof(T) * p * k);
     for (int64_t v0 = 0; v0 < nvec; v0 += kVecTile) {
         const int nv = (int)std::min<int64_t>(kVecTile, nvec - v0);
+        const T* xv = x + v0 * ldx;
         // (k = 0: one pass still sums x.x for the full-rank quadform)
-        for (int64_t c0 = 0; c0 < std::max<int64_t>(k, 1); c0 += 32 * kColTile) {
-            project_kernel<T><<<(unsigned)nblocks, 256, 0, s>>>(q, ldq, p, k, c0, x + v0 * ldx, ldx, nv, chunk,
-                                                               dptr<double>(part));
-            CK_LAUNCH();
+        for (int64_t c0 = 0; c0 < std::max<int64_t>(k, 1); c0 += 32 * W) {
+            double* pd = dptr<double>(part);
+            if (nv == 1) {
+                if (vec) launch_project<T, 1, true>(s, nblocks, q, ldq, p, k, c0, xv, ldx, nv, chunk, pd);
+                else launch_project<T, 1, false>(s, nblocks, q, ldq, p, k, c0, xv, ldx, nv, chunk, pd);
+            } else {
+                if (vec) launch_project<T, kVecTile, true>(s, nblocks, q, ldq, p, k, c0, xv, ldx, nv, chunk, pd);
+                else launch_project<T, kVecTile, false>(s, nblocks, q, ldq, p, k, c0, xv, ldx, nv, chunk, pd);
+            }
         }
-        project_finish_kernel<T><<<nv, 256, 0, s>>>(dptr<double>(part), nblocks, nv, k, lam, full ? 1 : 0, lambda_tilde,
+        project_sum_kernel<<<dim3((unsigned)ceil_div(k + 1, 8), (unsigned)nv), 256, 0, s>>>(dptr<double>(part), nblocks, k,
+                                                                                          dptr<double>(tsum));
+        CK_LAUNCH();
+        project_finish_kernel<T><<<nv, 256, 0, s>>>(dptr<double>(tsum), k, lam, full ? 1 : 0, lambda_tilde,
                                                    y ? dptr<T>(ts) : nullptr, kt, quad ? quad + v0 : nullptr);
         CK_LAUNCH();
         if (!y) continue;
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(3 * 148, ceil_div(p, kExpRows)));
-        expand_kernel<T><<<(unsigned)grid, 256, smem, s>>>(q, ldq, p, k, dptr<T>(ts), kt, nv, shift, x + v0 * ldx, ldx,
-                                                          y + v0 * ldy, ldy);
-        CK_LAUNCH();
+        T* yv = y + v0 * ldy;
+        auto ex = [&](auto nvc) {
+            constexpr int NVC = decltype(nvc)::value;
+            if (vec) launch_expand<T, NVC, true>(s, q, ldq, p, k, dptr<T>(ts), kt, nv, shift, xv, ldx, yv, ldy);
+            else launch_expand<T, NVC, false>(s, q, ldq, p, k, dptr<T>(ts), kt, nv, shift, xv, ldx, yv, ldy);
+        };
+        switch (nv) {
+            case 1: ex(std::integral_constant<int, 1>{}); break;
+            case 2: ex(std::integral_constant<int, 2>{}); break;
+            case 3: ex(std::integral_constant<int, 3>{}); break;
+            default: ex(std::integral_constant<int, 4>{}); break;
+        }
     }
 }
 
