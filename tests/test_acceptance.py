@@ -6,9 +6,11 @@ they lie (this container; the binaries travel to the GPU box):
   _ref/acceptance_ref   the unmodified reference library
   _ref/acceptance_b200  curvature.cpp replaced by integration/curvature_b200.cpp
                         (assemble_hessian / assemble_jacobian / assemble_opg on
-                        the C-ABI, fp64) and curv::hvp routed to
-                        integration/hvp_b200.cpp by a link-time --wrap
-Criteria 3, 4, 5, 6 and 9 then exercise the GPU path through the reference's
+                        the C-ABI, fp64), curv::hvp routed to
+                        integration/hvp_b200.cpp and the eigenpair operators
+                        (validate_eigen_pairs, low_rank_*, full_rank_*) to
+                        integration/eigops_b200.cpp by link-time --wrap
+Criteria 3, 4, 5, 6, 8 and 9 then exercise the GPU path through the reference's
 own API; the suite's tolerances are the reference's."""
 import os
 import subprocess
