@@ -564,6 +564,55 @@ def run_extra(torch, dev, stream, pk, pk_kind):
                                     "(F16S: exactly scaled TF32-class operands); all 100 eigenvalues within 1e-3 "
                                     "(same test, auto_f16s)")
     out["c4_topk"] = c4
+    # what the reference does with the eigenpairs (low_rank_* / full_rank_*, eigensolve.cpp:278-358):
+    # the full-rank operator of the eigenpairs just computed, applied at config-4 size (HBM bound:
+    # Q is read twice per apply, once per quadform), and materialised at config-1 size
+    hbm = float(pk["hbm_gbs"])
+
+    def timed_ms(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    P4 = wl.P
+    lt = float(lam[-1].item())
+    eo = {"workload": f"eigenpair operators on the c4 top-{k} pairs (P={P4}, Q = {4 * P4 * k / 1e6:.0f} MB > L2) and a "
+                      f"k={k} basis at c1 size", "dtype": "f32"}
+    for nvec in (1, 4):
+        xs = torch.randn((nvec, P4), dtype=torch.float32, device=dev)
+        ys = torch.empty_like(xs)
+        quad = torch.empty(nvec, dtype=torch.float64, device=dev)
+        ms_a = timed_ms(lambda: curv.dev_eig_apply(P4, k, q, k, lam, nvec, xs, P4, ys, P4, quad, lambda_tilde=lt,
+                                                   precision="f32", stream=stream), 20)
+        ms_q = timed_ms(lambda: curv.dev_eig_apply(P4, k, q, k, lam, nvec, xs, P4, None, 0, quad, lambda_tilde=lt,
+                                                   precision="f32", stream=stream), 20)
+        eo[f"full_rank_apply_nvec{nvec}"] = {
+            "ms": ms_a, "roofline": {"bound": "hbm", "achieved": 2 * 4.0 * P4 * k / ms_a / 1e6, "peak": hbm,
+                                     "unit": "GB/s", "frac": 2 * 4.0 * P4 * k / ms_a / 1e6 / hbm,
+                                     "algorithmic_bytes": "2 passes over Q (P x k fp32) per four vectors"}}
+        eo[f"full_rank_quadform_nvec{nvec}"] = {
+            "ms": ms_q, "roofline": {"bound": "hbm", "achieved": 4.0 * P4 * k / ms_q / 1e6, "peak": hbm, "unit": "GB/s",
+                                     "frac": 4.0 * P4 * k / ms_q / 1e6 / hbm,
+                                     "algorithmic_bytes": "1 pass over Q per four vectors"}}
+        del xs, ys
+    P1 = CONFIGS["c1"].P
+    ld1 = (P1 + 3) // 4 * 4
+    q1, _ = torch.linalg.qr(torch.randn((P1, k), dtype=torch.float32, device=dev))
+    q1 = q1.contiguous()
+    h1 = torch.empty((P1, ld1), dtype=torch.float32, device=dev)
+    ms_m = timed_ms(lambda: curv.dev_eig_materialize(P1, k, q1, k, lam, h1, ld1, lambda_tilde=lt, precision="tf32",
+                                                     stream=stream), 10)
+    eo["full_rank_materialize_c1"] = {
+        "ms": ms_m, "roofline": {"bound": "hbm", "achieved": 4.0 * P1 * P1 / ms_m / 1e6, "peak": hbm, "unit": "GB/s",
+                                 "frac": 4.0 * P1 * P1 / ms_m / 1e6 / hbm,
+                                 "algorithmic_bytes": "P^2 fp32 entries stored once (K = k = 100: output bound)"}}
+    out["eigen_operators"] = eo
     return out
 
 
