@@ -602,7 +602,7 @@ def run_extra(torch, dev, stream, pk, pk_kind):
                                      "algorithmic_bytes": "1 pass over Q per four vectors"}}
         del xs, ys
     P1 = CONFIGS["c1"].P
-    ld1 = (P1 + 3) // 4 * 4
+    ld1 = (P1 + 31) // 32 * 32  # 128-byte row pitch: whole-line block stores
     q1, _ = torch.linalg.qr(torch.randn((P1, k), dtype=torch.float32, device=dev))
     q1 = q1.contiguous()
     h1 = torch.empty((P1, ld1), dtype=torch.float32, device=dev)

@@ -321,7 +321,7 @@ void host_hessian(const ModelDesc& md, const double* params, const double* x, co
     Resident<T> r;
     upload_and_forward<T>(md, params, x, lab, n, r, s);
     tm.mark("upload+forward");
-    const int64_t ldh = round_up(md.P, 4);
+    const int64_t ldh = round_up(md.P, 32);  // 128-byte row pitch: the block stores write whole lines
     DevMem H((size_t)md.P * ldh * sizeof(T), s);
     const double asym = hessian_into<T>(md, dptr<T>(r.params), r.cache, dptr<T>(H), ldh, prec, verify, s);
     tm.mark("compute");
@@ -362,7 +362,7 @@ void host_opg(const ModelDesc& md, const double* params, const double* x, const 
     Resident<T> r;
     upload_and_forward<T>(md, params, x, lab, n, r, s);
     tm.mark("upload+forward");
-    const int64_t ldg = round_up(md.P, 4);
+    const int64_t ldg = round_up(md.P, 32);  // 128-byte row pitch: the block stores write whole lines
     DevMem G((size_t)md.P * ldg * sizeof(T), s);
     opg_into<T>(md, r.cache, dptr<T>(G), ldg, prec, s);
     tm.mark("compute");
@@ -903,7 +903,7 @@ int curvkit_eig_materialize(int64_t p, int64_t k, const double* q, const double*
         cudaStream_t s = lib_stream();
         auto run = [&](auto tag) {
             using T = decltype(tag);
-            const int64_t ldq = round_up(std::max<int64_t>(k, 1), 4), ldh = round_up(p, 4);
+            const int64_t ldq = round_up(std::max<int64_t>(k, 1), 4), ldh = round_up(p, 32);  // 128-byte row pitch
             DevMem qd = upload_as<T>(q, p, k, ldq, s), ld = upload_as<T>(lambda, 1, k, k, s);
             DevMem H((size_t)p * ldh * sizeof(T), s);
             if (k == 0) CK_CUDA(cudaMemsetAsync(H.p, 0, (size_t)p * ldh * sizeof(T), s));

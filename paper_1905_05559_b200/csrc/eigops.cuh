@@ -64,6 +64,8 @@ void materialize(int prec, cudaStream_t s, int64_t p, int64_t k, const T* q, int
                                                                          dptr<T>(qp), ldk);
     CK_LAUNCH();
     EpiSymLower<T> e{h, ldh, T(1)};
+    static const bool lsu = getenv("CURVKIT_EIG_MAT_LSU") != nullptr;  // dev: blocks stored by the LSU instead of TMA boxes
+    if (lsu) e.tma = 0;
     CurvGemm<T, EpiSymLower<T>>::run(prec, s, p, p, k, kmaj(dptr<T>(qs), ldk), kmaj(dptr<T>(qp), ldk), e);
     if (full) {
         add_diag_kernel<T><<<(unsigned)ceil_div(p, 256), 256, 0, s>>>(h, ldh, p, shift);

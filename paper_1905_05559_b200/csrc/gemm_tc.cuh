@@ -193,6 +193,7 @@ struct TcShape {
     int f16 = 0;
     const float* rsc = nullptr;
     const float* csc = nullptr;
+    int dev = 0;  // dev (CURVKIT_DEV_PAIR): 1 no direct TMA boxes, 2 no mirror TMA boxes, 4 mirror blocks by the LSU
 };
 
 // Epilogues whose interior blocks are stored by TMA boxes (Epi::tma_block)
@@ -450,6 +451,12 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return p;
 }
 
+__device__ __forceinline__ uint64_t evict_normal_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void tma2_2d(void* dst, const CUtensorMap* map, uint32_t bar_leader, int32_t c0,
                                         int32_t c1, uint64_t pol) {
     asm volatile(
@@ -599,15 +606,18 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// all but the newest store group have read their shared-memory source
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <int BN>
 struct PairSmem {
     static constexpr int A_BYTES = 128 * BK * 4;       // own 128 rows
     static constexpr int B_BYTES = (BN / 2) * BK * 4;  // own half of B
-    // per epilogue warp a 1024-aligned 5 KB slot: the 32 x 36 staging block,
-    // or the swizzled 32 x 32 TMA store box
-    static constexpr int EPI_SLOT = 5 * 1024;
+    // per epilogue warp a 1024-aligned 8 KB slot: the 32 x 36 staging block, or two
+    // swizzled 32 x 32 TMA store boxes (a block and its mirror: one store is in
+    // flight while the other box is filled)
+    static constexpr int EPI_SLOT = 8 * 1024;
     static constexpr int EPI_BYTES = EPI_WARPS * EPI_SLOT;
     static constexpr int MAX_SMEM = 227 * 1024;
     __host__ __device__ static constexpr int stage_bytes(int nsplit) { return (A_BYTES + B_BYTES) * (nsplit == 1 ? 1 : 2); }
@@ -776,7 +786,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
         const int chalf = ew / 4;    // column half of the tile
         uint8_t* slot = reinterpret_cast<uint8_t*>(epi_buf) + ew * S::EPI_SLOT;
         float(*buf)[36] = reinterpret_cast<float(*)[36]>(slot);
-        float* box = reinterpret_cast<float*>(slot);  // 32 rows x 128 B, 128-byte swizzle
+        float* box = reinterpret_cast<float*>(slot);          // 32 rows x 128 B, 128-byte swizzle
+        float* box2 = reinterpret_cast<float*>(slot + 4096);  // the mirrored block's box
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -800,11 +811,12 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                 }
                 if (row0 < sh.M) {
                     if constexpr (EpiTma<Epi>::value) {
-                        // the slot is free once the previous box's TMA store has read it
-                        if (lane == 0) bulk_wait_read();
-                        __syncwarp();
                         int64_t gr0, gc0;
                         if (epi.tma_block(row0, col0, sh.M, sh.N, gr0, gc0)) {
+                            // store groups complete in order: with at most one pending, the
+                            // store before the last one -- this box's previous use -- has read it
+                            if (lane == 0) bulk_wait_read1();
+                            __syncwarp();
 #pragma unroll
                             for (int c = 0; c < 32; ++c) v[c] *= epi.alpha;
 #pragma unroll
@@ -814,22 +826,33 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_const
                             fence_proxy_async();
                             __syncwarp();
                             if (lane == 0) {
-                                tma_store_2d(&mapC, box, (int32_t)gc0, (int32_t)gr0);
+                                if (!(sh.dev & 1)) tma_store_2d(&mapC, box, (int32_t)gc0, (int32_t)gr0);
                                 bulk_commit();
-                                bulk_wait_read();
+                                bulk_wait_read1();  // the previous mirror box has been read
                             }
                             __syncwarp();
+                            if (sh.dev & 4) {
+                                // mirrored block from registers: row gc0 + c of C gets this block's
+                                // column c, the 32 lanes writing 128 contiguous bytes (LSU, no box)
+                                float* mcol = epi.c + gc0 * epi.ldc + gr0 + lane;
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) __stcs(mcol + c * epi.ldc, v[c]);
+                                continue;
+                            }
 #pragma unroll
                             for (int c = 0; c < 32; ++c)
-                                box[c * 32 + ((((lane >> 2) ^ (c & 7)) << 2) | (lane & 3))] = v[c];
+                                box2[c * 32 + ((((lane >> 2) ^ (c & 7)) << 2) | (lane & 3))] = v[c];
                             fence_proxy_async();
                             __syncwarp();
                             if (lane == 0) {
-                                tma_store_2d(&mapC, box, (int32_t)gr0, (int32_t)gc0);
+                                if (!(sh.dev & 2)) tma_store_2d(&mapC, box2, (int32_t)gr0, (int32_t)gc0);
                                 bulk_commit();
                             }
                             continue;
                         }
+                        // the staging block below overlaps both boxes: every store has read them
+                        if (lane == 0) bulk_wait_read();
+                        __syncwarp();
                     }
                     stage_block(buf, v, lane);
                     if constexpr (EpiSplitK<Epi>::value)
@@ -1488,6 +1511,8 @@ void gemm_tf32(int prec, cudaStream_t s, int64_t M, int64_t N, int64_t K, Opnd<f
                    (uint32_t)tc::BK * 128u, 512u, 1024u, 1u, a3, b3, ksplit, A.once, B.once};
     static const int group_env = getenv("CURVKIT_GROUP_M") ? atoi(getenv("CURVKIT_GROUP_M")) : 0;  // dev knob
     if (group_env > 0) sh.group_m = group_env;
+    static const int dev_env = getenv("CURVKIT_DEV_PAIR") ? atoi(getenv("CURVKIT_DEV_PAIR")) : 0;  // dev ablations
+    sh.dev = dev_env;
     const int bn = N >= 192 ? 256 : (N > 64 ? 128 : 64);
     DevMem alo, blo, ahi, bhi;
     const float* pa = A.p;

@@ -437,7 +437,8 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
         int il, cl;
         row_ic(rho, il, cl);
         uint8_t* gbase = epi_base + grp * 4 * SLOT;  // [buf][layout][CH][128] floats
-        const uint64_t spol = evict_first_policy();
+        // (dev 1024 / 2048: evict_normal / evict_last instead)
+        const uint64_t spol = (p.dev & 1024) ? evict_normal_policy() : (p.dev & 2048) ? evict_last_policy() : evict_first_policy();
         const uint32_t te_leader = map_to_leader(smem_u32(&tempty[0]));
         const int half = bn / 2;
         int acc = 0;

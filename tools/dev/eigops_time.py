@@ -21,14 +21,15 @@ def timeit(f, reps=20):
 for p, k in ((25450, 100), (55050, 100)):
     q, _ = torch.linalg.qr(torch.randn(p, k, device=dev))
     q = q.contiguous(); lam = torch.linspace(2, 1, k, device=dev)
-    ldh = (p + 3) // 4 * 4
-    h = torch.empty((p, ldh), device=dev)
-    for prec in ("tf32", "f16s", "f32"):
-        for lt in (None, 0.5):
-            ms = timeit(lambda: curv.dev_eig_materialize(p, k, q, k, lam, h, ldh, lambda_tilde=lt, precision=prec), 10)
-            print(f"materialize P={p} k={k} {prec} full={lt is not None}: {ms:.3f} ms, "
-                  f"{4.0 * p * p / ms / 1e6:.0f} GB/s stored, {2.0 * p * p * k / ms / 1e9:.1f} TF/s (full square)")
-    del h
+    for ldh in ((p + 3) // 4 * 4, (p + 31) // 32 * 32):
+        h = torch.empty((p, ldh), device=dev)
+        print("ldh", ldh)
+        for prec in ("tf32", "f32"):
+            for lt in (None, 0.5):
+                ms = timeit(lambda: curv.dev_eig_materialize(p, k, q, k, lam, h, ldh, lambda_tilde=lt, precision=prec), 10)
+                print(f"materialize P={p} k={k} {prec} full={lt is not None}: {ms:.3f} ms, "
+                      f"{4.0 * p * p / ms / 1e6:.0f} GB/s stored, {2.0 * p * p * k / ms / 1e9:.1f} TF/s (full square)")
+        del h
 for p, k in ((1055242, 100), (1055242, 120), (109386, 100)):
     q = torch.randn(p, k, device=dev); lam = torch.linspace(2, 1, k, device=dev)
     for nvec in (1, 4, 16):
