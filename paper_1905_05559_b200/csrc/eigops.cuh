@@ -265,21 +265,23 @@ __global__ void __launch_bounds__(256) expand_kernel(const T* __restrict__ q, in
     const int t = threadIdx.x, r = t % kExpRows, g = t / kExpRows;
     const int64_t ntiles = ceil_div(p, kExpRows);
     const int64_t nchunks = ceil_div(k, (int64_t)E::Cols);
-    // this block's work items: (tile blockIdx.x + j gridDim.x, chunk c), j-major
+    // this block's work items: (tile blockIdx.x + j gridDim.x, chunk ch), j-major, walked
+    // by (j, ch) counters (no 64-bit divisions in the loop)
+    const int nch = (int)nchunks;
     const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t nitems = my_tiles * nchunks;
-    auto item_rows = [&](int64_t it, int64_t& i0, int64_t& c0, int& rows, int& cols) {
-        i0 = (blockIdx.x + (it / nchunks) * gridDim.x) * kExpRows;
-        c0 = (it % nchunks) * E::Cols;
+    auto item_rows = [&](int64_t j, int ch, int64_t& i0, int64_t& c0, int& rows, int& cols) {
+        i0 = (blockIdx.x + j * gridDim.x) * kExpRows;
+        c0 = (int64_t)ch * E::Cols;
         rows = (int)min((int64_t)kExpRows, p - i0);
         cols = (int)min((int64_t)E::Cols, k - c0);
     };
     // stage item `it` into buffer `b`: cp.async (VEC; the ragged last group zero-filled
     // past k) or plain loads
-    auto stage = [&](int64_t it, int b) {
+    auto stage = [&](int64_t j, int ch, int b) {
         int64_t i0, c0;
         int rows, cols;
-        item_rows(it, i0, c0, rows, cols);
+        item_rows(j, ch, i0, c0, rows, cols);
         T* tile = tiles + b * bufsz;
         const int nvr = (cols + W - 1) / W;
         // the chunk of ts (kt is a multiple of 4 and its pad is zero: whole 16-byte groups)
@@ -294,10 +296,12 @@ __global__ void __launch_bounds__(256) expand_kernel(const T* __restrict__ q, in
         }
         if constexpr (VEC) {
             const int total = rows * nvr, dr = 256 / nvr, dc = 256 % nvr;
+            const int tail = (cols - W * (nvr - 1)) * (int)sizeof(T);  // valid bytes of a row's last group
+            const T* gsrc = q + i0 * ldq + c0;
+            const int ldqi = (int)ldq;  // (row offsets inside a tile fit 32 bits: 64 rows)
             int rr = t / nvr, cv = t % nvr;
             for (int e = t; e < total; e += 256) {
-                const int valid = min(W, cols - W * cv) * (int)sizeof(T);
-                cp_async16(tile + rr * pitch + W * cv, q + (i0 + rr) * ldq + c0 + W * cv, valid);
+                cp_async16(tile + rr * pitch + W * cv, gsrc + rr * ldqi + W * cv, cv == nvr - 1 ? tail : 16);
                 rr += dr;
                 cv += dc;
                 if (cv >= nvr) {
@@ -314,21 +318,25 @@ __global__ void __launch_bounds__(256) expand_kernel(const T* __restrict__ q, in
         }
     };
     if constexpr (VEC) {
-        if (nitems > 0) stage(0, 0);
+        if (nitems > 0) stage(0, 0, 0);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     T acc[NV] = {};
+    int64_t j = 0;
+    int ch = 0;
     for (int64_t it = 0; it < nitems; ++it) {
         int64_t i0, c0;
         int rows, cols;
-        item_rows(it, i0, c0, rows, cols);
+        item_rows(j, ch, i0, c0, rows, cols);
         const int b = VEC ? (int)(it & 1) : 0;
+        const int chn = ch + 1 < nch ? ch + 1 : 0;  // the next item
+        const int64_t jn = chn ? j : j + 1;
         if constexpr (VEC) {
-            if (it + 1 < nitems) stage(it + 1, b ^ 1);  // (its last readers passed the barrier below)
+            if (it + 1 < nitems) stage(jn, chn, b ^ 1);  // (its last readers passed the barrier below)
             asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
-            stage(it, 0);
+            stage(j, ch, 0);
         }
         __syncthreads();
         if (r < rows) {
@@ -364,6 +372,8 @@ __global__ void __launch_bounds__(256) expand_kernel(const T* __restrict__ q, in
             }
         }
         __syncthreads();  // the buffer and red may be rewritten
+        j = jn;
+        ch = chn;
     }
     if constexpr (VEC) asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
