@@ -241,3 +241,36 @@ def test_device_apply_config4_size():
     quad_ref = (t * t * (ld_ - lt)).sum(1) + lt * (xd * xd).sum(1)
     assert float(torch.linalg.norm(y.double() - y_ref) / torch.linalg.norm(y_ref)) <= 2e-6
     assert float(((quad - quad_ref).abs() / quad_ref.abs()).max()) <= 2e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec,dt", [("f32", "float32"), ("tf32", "float32"), ("f64", "float64")])
+@pytest.mark.parametrize("name", ["c0_opg", "ortho300", "k1"])
+def test_device_entry_points_unpadded_operands(name, prec, dt):
+    """Dense device operands as a caller may hold them: ldq = k and ldh = P (odd, or not a
+    multiple of 4: rows that are not 16-byte aligned take the scalar-load and
+    scalar-store forms of the kernels)."""
+    import torch
+    tdt = getattr(torch, dt)
+    dev = torch.device("cuda", 0)
+    c = case(name)
+    p, k = c["q"].shape
+    lt = float(c["lt"])
+    q = torch.tensor(c["q"], dtype=tdt, device=dev).contiguous()
+    lam = torch.tensor(c["lam"], dtype=tdt, device=dev)
+    xs = torch.tensor(c["x"], dtype=tdt, device=dev).contiguous()
+    h = torch.empty((p, p), dtype=tdt, device=dev)
+    y = torch.empty_like(xs)
+    quad = torch.empty(xs.shape[0], dtype=torch.float64, device=dev)
+    tol = {"f64": 1e-12, "f32": 1e-5, "tf32": 1e-3}[prec]
+    atol = 1e-12 if prec == "f64" else 2e-5
+    for ltv, hk, yk, qk in ((None, "low", "low_y", "low_quad"), (lt, "full", "full_y", "full_quad")):
+        curv.dev_eig_materialize(p, k, q, k, lam, h, p, lambda_tilde=ltv, precision=prec)
+        curv.dev_eig_apply(p, k, q, k, lam, xs.shape[0], xs, p, y, p, quad, lambda_tilde=ltv, precision=prec)
+        torch.cuda.synchronize()
+        hh = h.double().cpu().numpy()
+        assert np.array_equal(hh, hh.T)
+        assert rel_fro(rows_of(hh, p), c[hk]) <= tol
+        assert rel_fro(y.double().cpu().numpy(), c[yk]) <= atol
+        scale = np.maximum(1.0, np.abs(c[qk]))
+        assert np.max(np.abs(quad.cpu().numpy() - c[qk]) / scale) <= atol
