@@ -243,22 +243,20 @@ LanczosOut lanczos_topk(const ModelDesc& md, const T* params, const Cache<T>& c,
     for (int64_t j = 0; j < max_steps; ++j) {
         T* vj = V + j * P;
         eng.hvp(params, c, vj, 1, P, w, P, alpha_h);
-        // alpha_j and the recurrence, then two full Gram-Schmidt passes
-        lz_dots_kernel<T><<<1, 256, 0, s>>>(vj, P, w, sc);
+        // alpha_j and the recurrence, then two full Gram-Schmidt passes.  alpha_j stays on
+        // the device (sc[1] -> the recurrence coefficients) and comes to the host with
+        // ||w||^2 in the step's one synchronisation
+        lz_dots_kernel<T><<<1, 256, 0, s>>>(vj, P, w, sc + 1);
         CK_LAUNCH();
-        double alpha = 0.0;
-        CK_CUDA(cudaMemcpyAsync(&alpha, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK_CUDA(cudaStreamSynchronize(s));
         if (j > 0) {  // w -= alpha v_j + beta_{j-1} v_{j-1}: V_{j-1}, V_j with coefficients (beta, alpha)
-            const double rec2[2] = {betas[j - 1], alpha};
-            CK_CUDA(cudaMemcpyAsync(cf, rec2, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaMemcpyAsync(cf, &betas[j - 1], sizeof(double), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaMemcpyAsync(cf + 1, sc + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
             lz_sub_kernel<T><<<gb, 256, 0, s>>>(V + (j - 1) * P, P, 2, cf, w);
         } else {
-            CK_CUDA(cudaMemcpyAsync(cf, &alpha, sizeof(double), cudaMemcpyHostToDevice, s));
+            CK_CUDA(cudaMemcpyAsync(cf, sc + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
             lz_sub_kernel<T><<<gb, 256, 0, s>>>(vj, P, 1, cf, w);
         }
         CK_LAUNCH();
-        alphas.push_back(alpha);
         for (int pass = 0; pass < 2; ++pass) {
             lz_dots_kernel<T><<<(unsigned)(j + 1), 256, 0, s>>>(V, P, w, cf);
             CK_LAUNCH();
@@ -267,9 +265,11 @@ LanczosOut lanczos_topk(const ModelDesc& md, const T* params, const Cache<T>& c,
         }
         lz_dots_kernel<T><<<1, 256, 0, s>>>(w, P, w, sc);
         CK_LAUNCH();
-        double b2 = 0.0;
-        CK_CUDA(cudaMemcpyAsync(&b2, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
+        double hs[2] = {0.0, 0.0};  // ||w||^2, alpha_j
+        CK_CUDA(cudaMemcpyAsync(hs, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK_CUDA(cudaStreamSynchronize(s));
+        const double b2 = hs[0], alpha = hs[1];
+        alphas.push_back(alpha);
         const double beta = std::sqrt(b2);
         opnorm = std::max(opnorm, std::fabs(alpha) + beta + (j > 0 ? betas[j - 1] : 0.0));
 
