@@ -524,6 +524,33 @@ __global__ void __launch_bounds__(256) rgen_kernel(RGenArgs<T> g) {
                 if (g.q) d = reinterpret_cast<const V*>(g.dkT + o * g.ldn)[e];
                 last_o = wt ? o : -1;
             }
+            // four consecutive weight tangents of one unit: their eight loads are issued
+            // before the first store (the compiler will not move loads across the stores
+            // to R on its own)
+            if (wt && g.q && jj + 4 <= jj1 && i + 4 <= g.tink) {
+                V sv[4], qv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    sv[u] = reinterpret_cast<const V*>(g.akT + (i + u) * g.ldn)[e];
+                    qv[u] = reinterpret_cast<const V*>(g.q + ((i + u) * g.tm1 + opp) * g.ldn)[e];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    V r = p;  // (the same operation order as the single-row form below)
+                    r.x *= sv[u].x; r.y *= sv[u].y; r.z *= sv[u].z; r.w *= sv[u].w;
+                    r.x += d.x * qv[u].x; r.y += d.y * qv[u].y; r.z += d.z * qv[u].z; r.w += d.w * qv[u].w;
+                    if constexpr (sizeof(T) == 4) {
+                        if (g.round) {
+                            r.x = round_tf32(r.x); r.y = round_tf32(r.y); r.z = round_tf32(r.z); r.w = round_tf32(r.w);
+                        }
+                        __stcs(reinterpret_cast<V*>(g.R + (opp * g.J + jj + u) * g.ldr) + e, r);
+                    } else {
+                        reinterpret_cast<V*>(g.R + (opp * g.J + jj + u) * g.ldr)[e] = r;
+                    }
+                }
+                jj += 3;  // (the loop adds the fourth)
+                continue;
+            }
             V r = p;
             if (wt) {
                 const V s = reinterpret_cast<const V*>(g.akT + i * g.ldn)[e];
