@@ -512,7 +512,7 @@ symkr_kernel(const __grid_constant__ CUtensorMap mapAbar8, const __grid_constant
                             const bool row_o = quad == 0 || quad == 2;
                             const int32_t d2 = bx.y - (row_o ? 0 : (int32_t)p.u0);
                             const int32_t d3 = bx.x - (row_o ? (int32_t)p.u0 : 0);
-                            if (d3 >= 0) {
+                            if (d3 >= 0 && !(p.dev & 4096)) {  // dev 4096: staging and barriers, no boxes
                                 if (ic) tma_store_4d(mp, src, (int32_t)c0, (int32_t)i0, d2, d3, spol);
                                 else tma_store_4d(mp, src, (int32_t)i0, (int32_t)c0, d2, d3, spol);
                             }

@@ -1,4 +1,4 @@
-for d in 0 2 256 512; do echo "DEV_SYMKR=$d"; CURVKIT_DEV_SYMKR=$d timeout 600 python bench.py --config c1 --no-extra --no-e2e --no-cpu-baseline --steps 20 2>&1 | python -c "
+for d in 0 4096 2; do echo "DEV_SYMKR=$d"; CURVKIT_DEV_SYMKR=$d timeout 600 python bench.py --config c1 --no-extra --no-e2e --no-cpu-baseline --steps 20 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
     if l.startswith('{'):
