@@ -360,6 +360,17 @@ int curvkit_dev_eig_apply(int64_t p, int64_t k, const void* q, int64_t ldq, cons
                           double lambda_tilde, int64_t nvec, const void* x, int64_t ldx, void* y, int64_t ldy,
                           double* quad, int32_t precision, void* stream);
 
+/* curvkit_dev_eig_apply on the row shards of the sharded top-k solvers: q
+ * (p_local x k), x and y (nvec x p_local) hold this rank's parameter rows
+ * [p_begin, p_end) of curvkit_topk_shard_rows (any row partition works; a rank
+ * may hold none).  One all-reduce of nvec (k + 1) doubles (the projections
+ * Q^T x and x.x) per four vectors; quad is the quadratic form of the whole
+ * vector, identical on every rank. */
+int curvkit_dev_eig_apply_sharded(int64_t p_local, int64_t k, const void* q, int64_t ldq, const void* lambda,
+                                  int32_t full_rank, double lambda_tilde, int64_t nvec, const void* x, int64_t ldx,
+                                  void* y, int64_t ldy, double* quad, int32_t precision, void* stream,
+                                  curvkit_comm comm);
+
 /* The curvature GEMM engine on its own (fp32 storage): C[m][n] = alpha *
  * sum_k A(m,k) B(n,k) with A(m,k) = a[m*lda+k] if a_kmajor else a[k*lda+m]
  * (likewise B).  TF32/TF32X3 run the tcgen05 kernel, F32 the SIMT one. */

@@ -86,6 +86,8 @@ SIGNATURES = {
     "curvkit_eig_apply": [i64, i64, dptr, dptr, i32, C.c_double, i64, dptr, i64, i32, dptr, dptr],
     "curvkit_dev_eig_materialize": [i64, i64, vptr, i64, vptr, i32, C.c_double, i32, vptr, i64, vptr],
     "curvkit_dev_eig_apply": [i64, i64, vptr, i64, vptr, i32, C.c_double, i64, vptr, i64, vptr, i64, dptr, i32, vptr],
+    "curvkit_dev_eig_apply_sharded": [i64, i64, vptr, i64, vptr, i32, C.c_double, i64, vptr, i64, vptr, i64, dptr, i32,
+                                      vptr, vptr],
     "curvkit_hessian_topk_lanczos": [_MP, dptr, dptr, dptr, i64, i64, i64, i64, C.c_double, u64, i32, dptr, dptr, dptr,
                                      C.POINTER(i64)],
 }

@@ -1363,4 +1363,27 @@ int curvkit_dev_opg_topk_filtered(const curvkit_model* model, const void* params
     });
 }
 
+int curvkit_dev_eig_apply_sharded(int64_t p_local, int64_t k, const void* q, int64_t ldq, const void* lambda,
+                                  int32_t full_rank, double lambda_tilde, int64_t nvec, const void* x, int64_t ldx,
+                                  void* y, int64_t ldy, double* quad, int32_t precision, void* stream,
+                                  curvkit_comm comm) {
+    return guard([&] {
+        check_lambda_tilde(full_rank, lambda_tilde);
+        if (!comm) contract("eigen operator: null communicator");
+        if (p_local < 0 || k < 0) shape("eigen operator: bad eigenpair shape");
+        if (k > 0 && !lambda) contract("eigen operator: null eigenpairs");
+        if (p_local > 0 && ((k > 0 && !q) || !x)) contract("eigen operator: null shard");
+        if (nvec < 1) return;
+        if (ldx < p_local || ldq < k || (y && ldy < p_local)) shape("eigen operator: bad leading dimension");
+        cudaStream_t s = dev_stream(stream);
+        const Comm* cm = &comm->c;
+        if (is_f64(precision))
+            eigops::apply<double>(s, p_local, k, (const double*)q, ldq, (const double*)lambda, full_rank != 0,
+                                  lambda_tilde, nvec, (const double*)x, ldx, (double*)y, ldy, quad, cm);
+        else
+            eigops::apply<float>(s, p_local, k, (const float*)q, ldq, (const float*)lambda, full_rank != 0,
+                                 lambda_tilde, nvec, (const float*)x, ldx, (float*)y, ldy, quad, cm);
+    });
+}
+
 }  // extern "C"

@@ -17,6 +17,7 @@
 //                 projection pass alone (the reference's expression, fp64).
 #pragma once
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "curvature.cuh"
 #include "eigen.cuh"
@@ -398,6 +399,7 @@ void launch_project(cudaStream_t s, int64_t nblocks, const T* q, int64_t ldq, in
 template <class T, int NV, bool VEC>
 void launch_expand(cudaStream_t s, const T* q, int64_t ldq, int64_t p, int64_t k, const T* ts, int64_t kt, int nv,
                    T shift, const T* x, int64_t ldx, T* y, int64_t ldy) {
+    if (p == 0) return;  // a rank without rows (sharded apply)
     if (k == 0) {
         scale_vec_kernel<T><<<(unsigned)ceil_div(p * nv, 256), 256, 0, s>>>(x, ldx, y, ldy, p, nv, shift);
         CK_LAUNCH();
@@ -415,10 +417,14 @@ void launch_expand(cudaStream_t s, const T* q, int64_t ldq, int64_t p, int64_t k
     CK_LAUNCH();
 }
 
-// y (nvec x p, ldy) and/or quad (nvec, fp64) for x (nvec x p, ldx); y or quad may be null
+// y (nvec x p, ldy) and/or quad (nvec, fp64) for x (nvec x p, ldx); y or quad may be null.
+// With a communicator, q, x and y hold this rank's parameter rows (the row shards of
+// the sharded top-k solvers): the projections t = Q^T x and x.x are summed over the
+// ranks -- one all-reduce of nvec (k + 1) doubles -- and every rank expands its own
+// rows; quad is the whole vector's quadratic form, identical on every rank.
 template <class T>
 void apply(cudaStream_t s, int64_t p, int64_t k, const T* q, int64_t ldq, const T* lam, bool full, double lambda_tilde,
-           int64_t nvec, const T* x, int64_t ldx, T* y, int64_t ldy, double* quad) {
+           int64_t nvec, const T* x, int64_t ldx, T* y, int64_t ldy, double* quad, const Comm* comm = nullptr) {
     if (nvec < 1) return;
     constexpr int W = Vec16<T>::W;
     const int64_t nblocks = std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(p, 256)));
@@ -448,6 +454,7 @@ void apply(cudaStream_t s, int64_t p, int64_t k, const T* q, int64_t ldq, const 
         project_sum_kernel<<<dim3((unsigned)ceil_div(k + 1, 8), (unsigned)nv), 256, 0, s>>>(dptr<double>(part), nblocks, k,
                                                                                           dptr<double>(tsum));
         CK_LAUNCH();
+        if (comm) comm->sum(dptr<double>(tsum), (size_t)nv * (size_t)(k + 1), s);
         project_finish_kernel<T><<<nv, 256, 0, s>>>(dptr<double>(tsum), k, lam, full ? 1 : 0, lambda_tilde,
                                                    y ? dptr<T>(ts) : nullptr, kt, quad ? quad + v0 : nullptr);
         CK_LAUNCH();

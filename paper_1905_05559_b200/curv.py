@@ -868,3 +868,17 @@ def dev_eig_apply(p, k, q, ldq, lam, nvec, x, ldx, y=None, ldy=0, quad=None, lam
                                                  _ptr(y) if y is not None else null, ldy,
                                                  C.cast(_ptr(quad), _lib.dptr) if quad is not None else None,
                                                  _prec(precision), _stream(stream)))
+
+
+def dev_eig_apply_sharded(p_local, k, q, ldq, lam, nvec, x, ldx, comm, y=None, ldy=0, quad=None, lambda_tilde=None,
+                          precision="tf32", stream=None):
+    """dev_eig_apply on this rank's parameter rows (the row shards of the sharded
+    top-k solvers): one all-reduce of nvec (k + 1) doubles over comm; quad is the
+    whole vector's quadratic form on every rank."""
+    full = lambda_tilde is not None
+    null = C.c_void_p(0)
+    _lib.check(_lib.load().curvkit_dev_eig_apply_sharded(
+        p_local, k, _ptr(q) if q is not None else null, ldq, _ptr(lam), 1 if full else 0,
+        float(lambda_tilde) if full else 0.0, nvec, _ptr(x) if x is not None else null, ldx,
+        _ptr(y) if y is not None else null, ldy, C.cast(_ptr(quad), _lib.dptr) if quad is not None else None,
+        _prec(precision), _stream(stream), comm.handle))

@@ -274,3 +274,140 @@ def test_device_entry_points_unpadded_operands(name, prec, dt):
         assert rel_fro(y.double().cpu().numpy(), c[yk]) <= atol
         scale = np.maximum(1.0, np.abs(c[qk]))
         assert np.max(np.abs(quad.cpu().numpy() - c[qk]) / scale) <= atol
+
+
+# ---- row-sharded apply (the consumer of the sharded top-k solvers' output) ------
+
+def _shard_apply_worker(rank, world, port, q):
+    """Two processes on cuda:0 over the host transport: each holds its rows of Q, x, y."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    try:
+        torch.cuda.set_device(0)
+        dev = "cuda:0"
+        c = case("ortho300")
+        p, k = c["q"].shape
+        lt = float(c["lt"])
+        cut = [0, 113, p]  # an uneven row partition
+        r0, r1 = cut[rank], cut[rank + 1]
+        comm = curv.Comm.create_host(rank, world)
+        for prec, tdt in (("f64", torch.float64), ("f32", torch.float32)):
+            ql = torch.tensor(c["q"][r0:r1], dtype=tdt, device=dev).contiguous()
+            lam = torch.tensor(c["lam"], dtype=tdt, device=dev)
+            xl = torch.tensor(c["x"][:, r0:r1], dtype=tdt, device=dev).contiguous()
+            yl = torch.empty_like(xl)
+            quad = torch.empty(xl.shape[0], dtype=torch.float64, device=dev)
+            for key, ltv in (("low", None), ("full", lt)):
+                curv.dev_eig_apply_sharded(r1 - r0, k, ql, k, lam, xl.shape[0], xl, r1 - r0, comm, yl, r1 - r0, quad,
+                                           lambda_tilde=ltv, precision=prec)
+                torch.cuda.synchronize()
+                ref_y = c[key + "_y"][:, r0:r1]
+                out[(prec, key)] = (float(np.linalg.norm(yl.double().cpu().numpy() - ref_y) / np.linalg.norm(ref_y)),
+                                    quad.cpu().numpy().tolist())
+        comm.close()
+    except Exception as ex:  # noqa: BLE001
+        out = {"error": repr(ex)}
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_apply_two_processes_host_transport():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    qq = ctx.Queue()
+    port = 29700 + os.getpid() % 1000
+    procs = [ctx.Process(target=_shard_apply_worker, args=(r, 2, port, qq)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    outs = dict(qq.get(timeout=600) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    c = case("ortho300")
+    for rank in (0, 1):
+        assert "error" not in outs[rank], outs[rank]
+    for prec, tol in (("f64", 1e-12), ("f32", 2e-5)):
+        for key in ("low", "full"):
+            e0, q0 = outs[0][(prec, key)]
+            e1, q1 = outs[1][(prec, key)]
+            assert e0 <= tol and e1 <= tol, (prec, key, e0, e1)
+            assert q0 == q1  # the all-reduced projections are the same bytes on every rank
+            ref = c[key + "_quad"]
+            assert np.max(np.abs(np.array(q0) - ref) / np.maximum(1.0, np.abs(ref))) <= tol
+
+
+@pytest.mark.gpu
+def test_sharded_apply_nccl_loopback_equals_unsharded(monkeypatch):
+    """One rank holding every row: the NCCL all-reduce of the projections runs
+    (CURVKIT_COMM_LOOPBACK=1) and the result equals the unsharded call bitwise."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("CURVKIT_COMM_LOOPBACK", "1")
+    dev = "cuda:0"
+    c = case("thin2000")
+    p, k = c["q"].shape
+    q = torch.tensor(c["q"], dtype=torch.float32, device=dev).contiguous()
+    lam = torch.tensor(c["lam"], dtype=torch.float32, device=dev)
+    xs = torch.tensor(c["x"], dtype=torch.float32, device=dev).contiguous()
+    y0, y1 = torch.empty_like(xs), torch.empty_like(xs)
+    q0 = torch.empty(3, dtype=torch.float64, device=dev)
+    q1 = torch.empty(3, dtype=torch.float64, device=dev)
+    curv.dev_eig_apply(p, k, q, k, lam, 3, xs, p, y0, p, q0, lambda_tilde=float(c["lt"]), precision="f32")
+    comm = curv.Comm.create(0, 1, lambda b: b)
+    try:
+        curv.dev_eig_apply_sharded(p, k, q, k, lam, 3, xs, p, comm, y1, p, q1, lambda_tilde=float(c["lt"]),
+                                   precision="f32")
+    finally:
+        comm.close()
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1) and torch.equal(q0, q1)
+
+
+def _gloo_apply_worker(rank, world, port, q):
+    """The exchange of curvkit_dev_eig_apply_sharded restated in numpy over gloo:
+    partial projections of this rank's rows, one all-reduce of k + 1 doubles,
+    local expansion."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = case("ortho300")
+    p, k = c["q"].shape
+    lt = float(c["lt"])
+    cut = [0, 113, p]
+    r0, r1 = cut[rank], cut[rank + 1]
+    ql, lam = c["q"][r0:r1], c["lam"]
+    res = []
+    for v in range(c["x"].shape[0]):
+        xl = c["x"][v, r0:r1]
+        t = torch.tensor(np.concatenate([ql.T @ xl, [xl @ xl]]))  # (Q^T x)_local, (x.x)_local
+        dist.all_reduce(t)
+        t = t.numpy()
+        yl = ql @ ((lam - lt) * t[:k]) + lt * xl
+        quad = float(np.sum(lam * t[:k] ** 2) + lt * t[k] - lt * np.sum(t[:k] ** 2))
+        res.append((yl, quad))
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_sharded_apply():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    qq = ctx.Queue()
+    port = 29800 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gloo_apply_worker, args=(r, 2, port, qq)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    outs = dict(qq.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    c = case("ortho300")
+    for v in range(c["x"].shape[0]):
+        y = np.concatenate([outs[0][v][0], outs[1][v][0]])
+        assert rel_fro(y, c["full_y"][v]) <= 1e-12
+        assert outs[0][v][1] == outs[1][v][1]
+        assert abs(outs[0][v][1] - c["full_quad"][v]) <= 1e-12 * max(1.0, abs(c["full_quad"][v]))
