@@ -411,3 +411,29 @@ def test_gloo_two_ranks_sharded_apply():
         assert rel_fro(y, c["full_y"][v]) <= 1e-12
         assert outs[0][v][1] == outs[1][v][1]
         assert abs(outs[0][v][1] - c["full_quad"][v]) <= 1e-12 * max(1.0, abs(c["full_quad"][v]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,prec,tol", [("float32", "f32", 2e-5), ("float64", "f64", 1e-12)])
+def test_device_apply_wide_basis(dt, prec, tol):
+    """k = 300 > the 256 (fp32) / 128 (fp64) columns of one expansion chunk and the 128 / 64
+    columns of one projection pass: the accumulators persist across the chunks."""
+    import torch
+    tdt = getattr(torch, dt)
+    dev = torch.device("cuda", 0)
+    p, k, lt = 1500, 300, 0.05
+    g = torch.Generator(device="cpu").manual_seed(21)
+    q64, _ = torch.linalg.qr(torch.randn(p, k, generator=g, dtype=torch.float64))
+    lam64 = torch.linspace(3.0, 0.1, k, dtype=torch.float64)
+    x64 = torch.randn(5, p, generator=g, dtype=torch.float64)
+    q, lam, xs = q64.to(dev).to(tdt).contiguous(), lam64.to(dev).to(tdt), x64.to(dev).to(tdt).contiguous()
+    y = torch.empty_like(xs)
+    quad = torch.empty(5, dtype=torch.float64, device=dev)
+    curv.dev_eig_apply(p, k, q, k, lam, 5, xs, p, y, p, quad, lambda_tilde=lt, precision=prec)
+    torch.cuda.synchronize()
+    qd, xd, ld_ = q.double(), xs.double(), lam.double()
+    t = xd @ qd
+    y_ref = (t * (ld_ - lt)) @ qd.T + lt * xd
+    quad_ref = (t * t * (ld_ - lt)).sum(1) + lt * (xd * xd).sum(1)
+    assert float(torch.linalg.norm(y.double() - y_ref) / torch.linalg.norm(y_ref)) <= tol
+    assert float(((quad - quad_ref).abs() / quad_ref.abs().clamp_min(1.0)).max()) <= tol
