@@ -7,7 +7,7 @@ dev = torch.device("cuda", 0)
 p, k = 25450, 100
 q, _ = torch.linalg.qr(torch.randn(p, k, device=dev)); q = q.contiguous()
 lam = torch.linspace(2, 1, k, device=dev)
-ldh = (p + 3) // 4 * 4
+ldh = (p + 31) // 32 * 32
 h = torch.empty((p, ldh), device=dev)
 for _ in range(2):
     curv.dev_eig_materialize(p, k, q, k, lam, h, ldh, lambda_tilde=0.5, precision="tf32")
