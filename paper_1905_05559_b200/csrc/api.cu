@@ -350,6 +350,26 @@ void opg_into(const ModelDesc& md, const Cache<T>& c, T* G, int64_t ldg, int pre
     eng.opg(dptr<T>(J), ldj, c.n, G, ldg, rb, re);
 }
 
+// a second stream per (thread, device) for downloads that overlap compute
+cudaStream_t copy_stream() {
+    static thread_local std::vector<std::pair<int, cudaStream_t>> streams;
+    int dev = 0;
+    CK_CUDA(cudaGetDevice(&dev));
+    for (const auto& ds : streams)
+        if (ds.first == dev) return ds.second;
+    cudaStream_t s = nullptr;
+    CK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    streams.emplace_back(dev, s);
+    return s;
+}
+
+// opg_into restricted to a row range assembles those rows and their mirrors: the
+// J-free route (TF32 class, f32, f64 orbit kernels) does; the J SYRK route too
+template <class T>
+bool opg_rows_supported(const ModelDesc&, int prec) {
+    return tf32_class(prec) && sizeof(T) == 4;
+}
+
 template <class T, class U>
 void host_opg(const ModelDesc& md, const double* params, const double* x, const double* y, int64_t n,
               const curvkit_curvature_config* cfg, int prec, U* g_out) {
@@ -364,6 +384,33 @@ void host_opg(const ModelDesc& md, const double* params, const double* x, const 
     tm.mark("upload+forward");
     const int64_t ldg = round_up(md.P, 32);  // 128-byte row pitch: the block stores write whole lines
     DevMem G((size_t)md.P * ldg * sizeof(T), s);
+    // Two phases when the result is large and goes out unconverted: the rows of the
+    // layers above the first (with their mirrors in the first layer's rows) are
+    // assembled first and travel to the host on a second stream while the first
+    // layer's diagonal block -- most of the work -- is computed.
+    const int64_t split = md.S > 1 ? md.woff[1] : md.P;
+    static const bool serial = getenv("CURVKIT_SERIAL_DOWNLOAD") != nullptr;  // dev: one phase
+    if (std::is_same_v<T, U> && !serial && split < md.P && md.P * md.P * (int64_t)sizeof(T) >= (int64_t(1) << 30) &&
+        opg_rows_supported<T>(md, prec)) {
+        T* Gd = dptr<T>(G);
+        opg_into<T>(md, r.cache, Gd, ldg, prec, s, split, md.P);
+        cudaEvent_t upper_done;
+        CK_CUDA(cudaEventCreateWithFlags(&upper_done, cudaEventDisableTiming));
+        cudaStream_t s2 = copy_stream();
+        CK_CUDA(cudaEventRecord(upper_done, s));
+        CK_CUDA(cudaStreamWaitEvent(s2, upper_done, 0));
+        CK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<T*>(g_out) + split * md.P, md.P * sizeof(T), Gd + split * ldg,
+                                  ldg * sizeof(T), md.P * sizeof(T), md.P - split, cudaMemcpyDeviceToHost, s2));
+        opg_into<T>(md, r.cache, Gd, ldg, prec, s, 0, split);
+        tm.mark("compute");
+        CK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<T*>(g_out), md.P * sizeof(T), Gd, ldg * sizeof(T), md.P * sizeof(T),
+                                  split, cudaMemcpyDeviceToHost, s));
+        CK_CUDA(cudaStreamSynchronize(s));
+        CK_CUDA(cudaStreamSynchronize(s2));  // (G is released in s's order: both copies have read it)
+        cudaEventDestroy(upper_done);
+        tm.mark("download");
+        return;
+    }
     opg_into<T>(md, r.cache, dptr<T>(G), ldg, prec, s);
     tm.mark("compute");
     download<T, U>(dptr<T>(G), ldg, md.P, md.P, g_out, s);

@@ -500,3 +500,42 @@ def test_wide_layer_orbits_against_oracle(prec):
     assert rel_fro(hr.h, H_ref) <= tol, rel_fro(hr.h, H_ref)
     assert rel_fro(G, G_ref) <= tol, rel_fro(G, G_ref)
     assert np.array_equal(hr.h, hr.h.T) and np.array_equal(G, G.T)
+
+
+@pytest.mark.gpu
+def test_host_f32_entry_points_equal_device_results():
+    """curvkit_assemble_opg_f32 / _hessian_f32 (fp32 host output; for G above 1 GiB the
+    two-phase form: the upper layers' rows travel to the host while the first
+    layer's block is computed) against the device entry points on the same inputs:
+    the same kernels, so the same bytes."""
+    import ctypes as C
+
+    import torch
+    from paper_1905_05559_b200 import _lib
+    lib = _lib.load()
+    wl = CONFIGS["c1"]
+    params, x, y, lab = wl.draw()
+    spec = curv.ModelSpec(wl.widths, wl.activation)
+    P, n = wl.P, wl.n
+    dev = "cuda:0"
+    p_d = torch.tensor(params, dtype=torch.float32, device=dev)
+    x_d = torch.tensor(x, dtype=torch.float32, device=dev)
+    l_d = torch.tensor(lab, dtype=torch.int32, device=dev)
+    ld = (P + 31) // 32 * 32
+    cfg = curv.CurvatureConfig(batch_size_h=n, batch_size_g=n, memory_cap=1 << 40)._c()
+    m = spec._c()
+    dp = lambda a: np.ascontiguousarray(a).ctypes.data_as(_lib.dptr)  # noqa: E731
+    pp, xp, yp = (np.ascontiguousarray(a, dtype=np.float64) for a in (params, x, y))
+    for host_fn, dev_fn in ((lib.curvkit_assemble_opg_f32, curv.dev_assemble_opg),
+                            (lib.curvkit_assemble_hessian_f32, curv.dev_assemble_hessian)):
+        h = torch.full((P, P), float("nan"), dtype=torch.float32).pin_memory()
+        _lib.check(host_fn(C.byref(m), dp(pp), dp(xp), dp(yp), n, C.byref(cfg), curv.PRECISION["tf32"],
+                           C.cast(h.data_ptr(), _lib.fptr)))
+        d = torch.empty((P, ld), dtype=torch.float32, device=dev)
+        dev_fn(spec, p_d, x_d, l_d, n, d, ld, precision="tf32")
+        torch.cuda.synchronize()
+        hd = d[:, :P].cpu()
+        assert not torch.isnan(h).any()
+        assert torch.equal(h, hd)
+        assert torch.equal(h, h.T)
+        del h, d, hd
