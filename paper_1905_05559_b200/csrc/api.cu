@@ -57,11 +57,12 @@ int guard(F&& f) {
 }
 
 // bytes of pool memory kept mapped between calls (CURVKIT_POOL_KEEP_GB,
-// default 16): a host that re-runs config-4 sized calls keeps its J mapped
+// default 64): a host that re-runs config-3 sized calls keeps its 48 GB result and J mapped
+// (re-mapping them cost 100-400 ms per call at a 16 GB threshold)
 size_t pool_keep_bytes() {
     static const size_t keep = [] {
         const char* e = getenv("CURVKIT_POOL_KEEP_GB");
-        const double gb = e ? atof(e) : 16.0;
+        const double gb = e ? atof(e) : 64.0;
         return (size_t)((gb > 0 ? gb : 0.0) * double(1ull << 30));
     }();
     return keep;
@@ -143,7 +144,7 @@ void check_memory_cap(int64_t p, int64_t cap, const char* who) {  // curvature.c
 
 // Never release the stream-ordered pool at synchronisation points inside a
 // call: a sync while an 84 GB J is live would otherwise unmap every freed
-// workspace and re-map it on the next allocation.  Keep up to 16 GB mapped
+// workspace and re-map it on the next allocation.  Keep up to 64 GB mapped
 // between calls (curvature workspaces are reused); trim_pool returns the
 // rest once the call's frees have completed.
 void keep_pool_memory() {
