@@ -342,8 +342,10 @@ void jacobian_full(const ModelDesc& md, const Cache<T>& c, DevMem& J, int64_t& l
 // Khatri-Rao route in TF32 mode, else per-example gradients J and the SYRK
 template <class T>
 void opg_into(const ModelDesc& md, const Cache<T>& c, T* G, int64_t ldg, int prec, cudaStream_t s, int64_t rb = 0,
-              int64_t re = -1) {
+              int64_t re = -1, int64_t pair_q0 = 0, int64_t pair_q1 = -1) {
     Engine<T> eng{md, s, prec};
+    eng.pair_q0 = pair_q0;
+    eng.pair_q1 = pair_q1;
     if (eng.opg_kr(c, G, ldg, rb, re < 0 ? INT64_MAX : re)) return;
     DevMem J;
     int64_t ldj;
@@ -394,21 +396,55 @@ void host_opg(const ModelDesc& md, const double* params, const double* x, const 
     if (std::is_same_v<T, U> && !serial && split < md.P && md.P * md.P * (int64_t)sizeof(T) >= (int64_t(1) << 30) &&
         opg_rows_supported<T>(md, prec)) {
         T* Gd = dptr<T>(G);
-        opg_into<T>(md, r.cache, Gd, ldg, prec, s, split, md.P);
-        cudaEvent_t upper_done;
-        CK_CUDA(cudaEventCreateWithFlags(&upper_done, cudaEventDisableTiming));
+        T* hG = reinterpret_cast<T*>(g_out);
         cudaStream_t s2 = copy_stream();
-        CK_CUDA(cudaEventRecord(upper_done, s));
-        CK_CUDA(cudaStreamWaitEvent(s2, upper_done, 0));
-        CK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<T*>(g_out) + split * md.P, md.P * sizeof(T), Gd + split * ldg,
-                                  ldg * sizeof(T), md.P * sizeof(T), md.P - split, cudaMemcpyDeviceToHost, s2));
-        opg_into<T>(md, r.cache, Gd, ldg, prec, s, 0, split);
+        std::vector<cudaEvent_t> evs;
+        // on every exit (errors included) the copy stream has finished reading G before
+        // G's stream-ordered release on s
+        struct Drain {
+            cudaStream_t st;
+            std::vector<cudaEvent_t>& ev;
+            ~Drain() {
+                cudaStreamSynchronize(st);
+                for (cudaEvent_t e : ev) cudaEventDestroy(e);
+            }
+        } drain{s2, evs};
+        // rows [r0, r1) are final on s: they follow on the copy stream
+        auto send_rows = [&](int64_t r0, int64_t r1, bool new_event) {
+            if (r0 >= r1) return;
+            if (new_event) {
+                cudaEvent_t e;
+                CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                evs.push_back(e);
+                CK_CUDA(cudaEventRecord(e, s));
+                CK_CUDA(cudaStreamWaitEvent(s2, e, 0));
+            }
+            CK_CUDA(cudaMemcpy2DAsync(hG + r0 * md.P, md.P * sizeof(T), Gd + r0 * ldg, ldg * sizeof(T),
+                                      md.P * sizeof(T), r1 - r0, cudaMemcpyDeviceToHost, s2));
+        };
+        opg_into<T>(md, r.cache, Gd, ldg, prec, s, split, md.P);
+        send_rows(split, md.P, true);
+        // the first layer's diagonal block in ranges of its units o'', last range first and
+        // of equal pair counts: when a range's launch ends, the rows of its units are final
+        const int64_t U0 = md.w[1], tk0 = md.w[0];
+        const int nchunk = U0 >= 16 ? 4 : 1;
+        std::vector<int64_t> cut(nchunk + 1, 0);
+        cut[nchunk] = U0;
+        const double total = (double)U0 * (U0 + 1) / 2.0;
+        for (int j = 1; j < nchunk; ++j) {
+            int64_t u = 0;
+            while (u < U0 && (double)u * (u + 1) / 2.0 < total * j / nchunk) ++u;
+            cut[j] = std::max(cut[j - 1], std::min(u, U0));
+        }
+        for (int j = nchunk - 1; j >= 0; --j) {
+            if (cut[j] >= cut[j + 1]) continue;
+            opg_into<T>(md, r.cache, Gd, ldg, prec, s, 0, split, cut[j], cut[j + 1]);
+            send_rows(md.woff[0] + cut[j] * tk0, md.woff[0] + cut[j + 1] * tk0, true);  // weight rows of the units
+            send_rows(md.boff[0] + cut[j], md.boff[0] + cut[j + 1], false);             // their bias rows
+        }
         tm.mark("compute");
-        CK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<T*>(g_out), md.P * sizeof(T), Gd, ldg * sizeof(T), md.P * sizeof(T),
-                                  split, cudaMemcpyDeviceToHost, s));
         CK_CUDA(cudaStreamSynchronize(s));
-        CK_CUDA(cudaStreamSynchronize(s2));  // (G is released in s's order: both copies have read it)
-        cudaEventDestroy(upper_done);
+        CK_CUDA(cudaStreamSynchronize(s2));
         tm.mark("download");
         return;
     }

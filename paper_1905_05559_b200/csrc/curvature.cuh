@@ -78,6 +78,11 @@ struct SymKrArgs {
     // >= 0: prof holds only the tangents of units prof_t0, prof_t0 + 1, ... and
     // Pi[o][o''] is read as prof[(o'' - prof_t0) U + o] (the profile is symmetric)
     int64_t prof_t0 = -1;
+    // whole-block assembly in pieces: only the packed columns (o, o'') with o'' in
+    // [pair_q0, pair_q1) (pair_q1 < 0: all), all four images of each stored.  Run
+    // over descending o'' ranges, the rows of a range's units are complete when its
+    // launch ends (the host-buffer OPG downloads them while the next range runs).
+    int64_t pair_q0 = 0, pair_q1 = -1;
 };
 
 // kF16S OPG rectangles (blocks m < k): J^T in fp16 with an exact power-of-two
@@ -236,6 +241,8 @@ struct Engine {
     const ModelDesc& md;
     cudaStream_t s;
     int prec;
+    // opg_kr: restrict the diagonal blocks' packed columns (SymKrArgs::pair_q0 / pair_q1)
+    int64_t pair_q0 = 0, pair_q1 = -1;
 
     // ---------------------------------------------------------------- grad
     void grad(const Cache<T>& c, T* g) {
@@ -440,6 +447,9 @@ struct Engine {
                         sa.u1 = band->u1[k];
                         sa.bwoff = band->bw[k];
                         sa.bboff = band->bb[k];
+                    } else {
+                        sa.pair_q0 = pair_q0;
+                        sa.pair_q1 = pair_q1;
                     }
                     if (!SymKr<T>::run(prec, s, sa)) throw CurvError(kCudaError, "opg_kr: diagonal block kernel unavailable");
                 } else {

@@ -906,9 +906,12 @@ struct SymKr<float> {
         if (u0 < 0 || u1 > U || u0 >= u1) return true;
         const int64_t bwoff = a.bwoff < 0 ? a.woff : a.bwoff, bboff = a.bboff < 0 ? a.boff : a.bboff;
         // packed columns, o-major
+        // (pair_q0 / pair_q1: a sub-range of o'' with the rows left unrestricted)
+        const int64_t q0 = std::max(u0, a.pair_q0), q1 = a.pair_q1 < 0 ? u1 : std::min(u1, a.pair_q1);
+        if (q0 >= q1) return true;
         std::vector<int4> pairs;
-        for (int64_t o = 0; o < u1; ++o)
-            for (int64_t q = std::max(o, u0); q < u1; ++q) pairs.push_back(make_int4((int)o, (int)q, 0, 0));
+        for (int64_t o = 0; o < q1; ++o)
+            for (int64_t q = std::max(o, q0); q < q1; ++q) pairs.push_back(make_int4((int)o, (int)q, 0, 0));
         const int64_t np = (int64_t)pairs.size();
         // TMA box decomposition per 8-column chunk (chunks start at multiples of 8:
         // tile widths are multiples of 16): runs of one o with consecutive o''; a
