@@ -503,7 +503,8 @@ def test_wide_layer_orbits_against_oracle(prec):
 
 
 @pytest.mark.gpu
-def test_host_f32_entry_points_equal_device_results():
+@pytest.mark.parametrize("shape", ["c1", "wide_upper"])
+def test_host_f32_entry_points_equal_device_results(shape):
     """curvkit_assemble_opg_f32 / _hessian_f32 (fp32 host output; for G above 1 GiB the
     two-phase form: the upper layers' rows travel to the host while the first
     layer's block is computed) against the device entry points on the same inputs:
@@ -513,10 +514,20 @@ def test_host_f32_entry_points_equal_device_results():
     import torch
     from paper_1905_05559_b200 import _lib
     lib = _lib.load()
-    wl = CONFIGS["c1"]
-    params, x, y, lab = wl.draw()
-    spec = curv.ModelSpec(wl.widths, wl.activation)
-    P, n = wl.P, wl.n
+    if shape == "c1":  # first layer of 32 units: its block in four unit ranges
+        wl = CONFIGS["c1"]
+        params, x, y, lab = wl.draw()
+        spec = curv.ModelSpec(wl.widths, wl.activation)
+        P, n = wl.P, wl.n
+    else:  # 12 units in the first layer (one range) and 39% of the rows in the layers above it
+        rng = np.random.default_rng(17)
+        widths, n = [1200, 12, 400, 10], 256
+        spec = curv.ModelSpec(widths, "tanh")
+        P = curv.param_count(spec)
+        params = rng.normal(0.0, 0.05, P)
+        x = rng.normal(0.0, 1.0, (n, widths[0]))
+        lab = rng.integers(0, widths[-1], n)
+        y = np.eye(widths[-1])[lab]
     dev = "cuda:0"
     p_d = torch.tensor(params, dtype=torch.float32, device=dev)
     x_d = torch.tensor(x, dtype=torch.float32, device=dev)
