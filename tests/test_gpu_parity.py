@@ -537,13 +537,14 @@ def test_host_f32_entry_points_equal_device_results(shape):
     m = spec._c()
     dp = lambda a: np.ascontiguousarray(a).ctypes.data_as(_lib.dptr)  # noqa: E731
     pp, xp, yp = (np.ascontiguousarray(a, dtype=np.float64) for a in (params, x, y))
-    for host_fn, dev_fn in ((lib.curvkit_assemble_opg_f32, curv.dev_assemble_opg),
-                            (lib.curvkit_assemble_hessian_f32, curv.dev_assemble_hessian)):
+    for host_fn, dev_fn, prec in ((lib.curvkit_assemble_opg_f32, curv.dev_assemble_opg, "tf32"),
+                                  (lib.curvkit_assemble_opg_f32, curv.dev_assemble_opg, "f16s"),
+                                  (lib.curvkit_assemble_hessian_f32, curv.dev_assemble_hessian, "tf32")):
         h = torch.full((P, P), float("nan"), dtype=torch.float32).pin_memory()
-        _lib.check(host_fn(C.byref(m), dp(pp), dp(xp), dp(yp), n, C.byref(cfg), curv.PRECISION["tf32"],
+        _lib.check(host_fn(C.byref(m), dp(pp), dp(xp), dp(yp), n, C.byref(cfg), curv.PRECISION[prec],
                            C.cast(h.data_ptr(), _lib.fptr)))
         d = torch.empty((P, ld), dtype=torch.float32, device=dev)
-        dev_fn(spec, p_d, x_d, l_d, n, d, ld, precision="tf32")
+        dev_fn(spec, p_d, x_d, l_d, n, d, ld, precision=prec)
         torch.cuda.synchronize()
         hd = d[:, :P].cpu()
         assert not torch.isnan(h).any()
