@@ -437,3 +437,51 @@ def test_device_apply_wide_basis(dt, prec, tol):
     quad_ref = (t * t * (ld_ - lt)).sum(1) + lt * (xd * xd).sum(1)
     assert float(torch.linalg.norm(y.double() - y_ref) / torch.linalg.norm(y_ref)) <= tol
     assert float(((quad - quad_ref).abs() / quad_ref.abs().clamp_min(1.0)).max()) <= tol
+
+
+@pytest.mark.gpu
+def test_random_shapes_against_the_port():
+    """Forty seeded shapes (P from 1 to 700, k from 0 to P, 1 to 6 vectors, padded and
+    unpadded leading dimensions, fp64 and fp32) through the device entry points
+    against the numpy port: ragged tiles, single rows, k = P."""
+    import torch
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(2024)
+    for trial in range(40):
+        p = int(rng.choice([1, 2, 3, 7, 31, 32, 33, 64, 65, 129, 255, 300, 511, 700]))
+        k = int(rng.integers(0, min(p, 140) + 1))
+        nvec = int(rng.integers(1, 7))
+        f64 = bool(trial % 2)
+        tdt, prec, tol = (torch.float64, "f64", 1e-11) if f64 else (torch.float32, "f32", 5e-5)
+        qn = np.linalg.qr(rng.standard_normal((p, max(k, 1))))[0][:, :k] if k else np.zeros((p, 0))
+        lam = np.sort(rng.uniform(0.1, 3.0, k))[::-1].copy()
+        lt = float(rng.uniform(0.01, 0.5)) if trial % 3 else None
+        xs = rng.standard_normal((nvec, p))
+        ldq = k + int(rng.integers(0, 6)) if k else 4
+        ldx = p + int(rng.integers(0, 5))
+        ldh = p + int(rng.integers(0, 9))
+        q = torch.zeros((p, ldq), dtype=tdt, device=dev)
+        q[:, :k] = torch.tensor(qn, dtype=tdt, device=dev)
+        lamd = torch.tensor(lam, dtype=tdt, device=dev) if k else torch.zeros(1, dtype=tdt, device=dev)
+        xd = torch.zeros((nvec, ldx), dtype=tdt, device=dev)
+        xd[:, :p] = torch.tensor(xs, dtype=tdt, device=dev)
+        y = torch.full((nvec, ldx), float("nan"), dtype=tdt, device=dev)
+        quad = torch.empty(nvec, dtype=torch.float64, device=dev)
+        h = torch.full((p, ldh), float("nan"), dtype=tdt, device=dev)
+        curv.dev_eig_apply(p, k, q, ldq, lamd, nvec, xd, ldx, y, ldx, quad, lambda_tilde=lt, precision=prec)
+        curv.dev_eig_materialize(p, k, q, ldq, lamd, h, ldh, lambda_tilde=lt, precision=prec)
+        torch.cuda.synchronize()
+        tag = (trial, p, k, nvec, prec, lt, ldq, ldx, ldh)
+        qr_, xr = q[:, :k].double().cpu().numpy(), xd[:, :p].double().cpu().numpy()  # the operands as stored
+        lr = lamd[:k].double().cpu().numpy()
+        href = orc.eig_materialize_port(qr_, lr, lt) if k else (np.eye(p) * lt if lt else np.zeros((p, p)))
+        hh = h[:, :p].double().cpu().numpy()
+        assert np.array_equal(hh, hh.T), tag
+        assert np.abs(hh - href).max() <= tol * max(1.0, np.abs(href).max()), tag
+        for v in range(nvec):
+            yr, qf = (orc.eig_apply_port(qr_, lr, xr[v], lt) if k else
+                      ((lt or 0.0) * xr[v], (lt or 0.0) * float(xr[v] @ xr[v])))
+            assert np.abs(y[v, :p].double().cpu().numpy() - yr).max() <= tol * max(1.0, np.abs(yr).max()), tag
+            assert abs(float(quad[v]) - qf) <= tol * max(1.0, abs(qf)), tag
+        if ldx > p:
+            assert torch.isnan(y[:, p:]).all(), tag  # nothing written past the vectors
